@@ -1,0 +1,135 @@
+/*
+ * tdw.h -- C ABI of libtdw (B200-native MOT hot path of the time-domain BEM,
+ * arXiv 2111.05205).  Plain C: pointers, sizes and POD structs only.
+ *
+ * Every entry point replaces one reference interface (paths relative to
+ * /root/reference/pkg/src/tdwavebem/):
+ *
+ *   tdw_coeff_table     <- elemint.retarded_coeff_table          elemint.py:89-186
+ *   tdw_problem_create  <- marching.ProblemSpec (+mesh_stats,     marching.py:33-69,
+ *                          compute_gamma_star)                    mesh.py:85-107
+ *   tdw_assemble        <- marching.build_retarded_matrices       marching.py:132-181
+ *                          + build_step_matrix                    marching.py:279-289
+ *   tdw_march           <- marching.march (+greville inputs,      marching.py:292-338
+ *                          TimeHistory outputs)                   marching.py:184-276
+ *   tdw_march_resident  <- same time loop, inputs/outputs resident on the device (benchmark form)
+ *   tdw_nccl_unique_id / tdw_comm_init  <- (none in the reference; row-sharded multi-GPU)
+ *
+ * Host buffers are C-contiguous float64 / int64; the library copies in and out
+ * and owns all device memory behind the opaque handles.  A ctx is bound to one
+ * CUDA device and is not re-entrant.
+ */
+#ifndef TDW_H
+#define TDW_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* return codes (mapped to the reference's exceptions by the Python shim) */
+#define TDW_OK 0
+#define TDW_ERR_INVALID_ARG 1       /* ValueError   (elemint.py:109-113, 154-155) */
+#define TDW_ERR_UNSUPPORTED_ORDER 2 /* ValueError   (elemint.py:109-110) */
+#define TDW_ERR_SINGULAR 3          /* RuntimeError (marching.py:284-288) */
+#define TDW_ERR_RESIDUAL 4          /* RuntimeError (marching.py:331-333) */
+#define TDW_ERR_CUDA 5
+#define TDW_ERR_NCCL 6
+#define TDW_ERR_STATE 7             /* call order (e.g. march before assemble) */
+#define TDW_ERR_LIMIT 8             /* a structural limit of the banded store was exceeded */
+
+typedef struct tdw_ctx tdw_ctx;
+typedef struct tdw_problem tdw_problem;
+
+/* kind: 0 = "uw" (U, W), 1 = "bm" (Burton-Miller Ubar, Wbar) */
+#define TDW_KIND_UW 0
+#define TDW_KIND_BM 1
+/* bie: 0 = "obie", 1 = "bmbie" */
+#define TDW_BIE_OBIE 0
+#define TDW_BIE_BMBIE 1
+
+typedef struct {
+  int32_t ns;                /* elements (= collocation points)                 */
+  int32_t nv;                /* vertices                                         */
+  const double* vertices;    /* (nv, 3)                                          */
+  const int64_t* triangles;  /* (ns, 3)                                          */
+  const double* phi;         /* (ns,) 1 = u unknown (q given), 0 = q unknown     */
+  int32_t bie;               /* TDW_BIE_*                                        */
+  int32_t d;                 /* B-spline order, 1..3                             */
+  double c, dt;
+  int32_t nt;                /* time steps; the loop solves nt-1 of them         */
+  int32_t window;            /* 1 = sliding window at gamma* (reference default) */
+  int32_t nranks, rank;      /* row sharding; 1, 0 for a single GPU              */
+} tdw_problem_desc;
+
+typedef struct {
+  int32_t gamma_star;        /* compute_gamma_star (marching.py:67-69)           */
+  int32_t n_lags;            /* min(gamma*, nt-1) (window) or nt-1               */
+  int32_t row_lo, row_hi;    /* rows owned by this rank (internal order)         */
+  int64_t n_band;            /* stored (i,j,gamma) entries of the banded store   */
+  int64_t n_pairs;           /* (i,j) pairs with a non-empty band                */
+  int64_t n_evals;           /* closed-form (i,j,gamma) evaluations in assembly  */
+  int64_t store_bytes;       /* device bytes of the banded store (coef+headers)  */
+  int32_t step_nnz;          /* nnz of the lag-1 step matrix                     */
+  int32_t jacobi_iters;      /* fixed Jacobi sweeps per step                     */
+  double jacobi_bound;       /* max_i sum_{j!=i} |A_ij| / |A_ii|                 */
+  double t_assemble_ms;      /* device time of tdw_assemble                      */
+  double t_fill_ms;          /* device time of the coefficient fill kernel       */
+} tdw_info;
+
+typedef struct {
+  double total_ms;           /* device time of the whole timed loop              */
+  double conv_ms;            /* summed device time of the history-convolution kernel */
+  double solve_ms;           /* summed device time of the solve/update kernel    */
+  double comm_ms;            /* summed device time of the NCCL all-gather        */
+  int32_t conv_launches;
+  int32_t steps;
+} tdw_timing;
+
+int tdw_init(int device, tdw_ctx** out);
+int tdw_finalize(tdw_ctx* ctx);
+const char* tdw_last_error(const tdw_ctx* ctx);
+int tdw_device_count(void);
+
+/* elemint.retarded_coeff_table: n triples, host arrays. nx may be NULL for kind 0. */
+int tdw_coeff_table(tdw_ctx* ctx, int64_t n, const double* P, const double* A, const double* B,
+                    const double* C, const double* ez, const double* s, int d, double c, double dt,
+                    int kind, const double* nx, double* out0, double* out1);
+
+/* Same, DEVICE pointers, on the ctx stream; *ms = kernel time (may be NULL). */
+int tdw_coeff_table_device(tdw_ctx* ctx, int64_t n, const double* P, const double* A,
+                           const double* B, const double* C, const double* ez, const double* s,
+                           int d, double c, double dt, int kind, const double* nx, double* out0,
+                           double* out1, float* ms);
+
+int tdw_problem_create(tdw_ctx* ctx, const tdw_problem_desc* desc, tdw_problem** out);
+int tdw_assemble(tdw_problem* pb);
+int tdw_problem_info(const tdw_problem* pb, tdw_info* out);
+
+/* Full march with host buffers.  u_known/q_known: (nt-1, ns) Greville samples
+ * (marching.py:258-276).  Outputs (nt-1, ns): u, q, tau, sigma; rhs_trace may be NULL.
+ * status: 0 stable, 1 unstable (blow-up detector, marching.py:336-338). */
+int tdw_march(tdw_problem* pb, const double* u_known, const double* q_known, double threshold,
+              double* u, double* q, double* tau, double* sigma, double* rhs_trace,
+              int32_t* n_steps, int32_t* status);
+
+/* Benchmark form: known data already uploaded (tdw_upload_known), the time loop
+ * runs n_repeat times on device-resident data; timings from CUDA events. */
+int tdw_upload_known(tdw_problem* pb, const double* u_known, const double* q_known);
+int tdw_march_resident(tdw_problem* pb, double threshold, int n_repeat, int time_kernels,
+                       tdw_timing* timing);
+int tdw_download(tdw_problem* pb, double* u, double* q, double* tau, double* sigma,
+                 int32_t* n_steps, int32_t* status);
+
+int tdw_problem_destroy(tdw_problem* pb);
+
+/* Multi-GPU (one process per GPU): rank 0 makes the id, the host broadcasts it
+ * (torch.distributed), every rank calls tdw_comm_init before tdw_problem_create. */
+int tdw_nccl_unique_id(char out[128]);
+int tdw_comm_init(tdw_ctx* ctx, const char id[128], int nranks, int rank);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TDW_H */

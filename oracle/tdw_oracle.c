@@ -1,0 +1,572 @@
+/*
+ * tdw_oracle.c -- CPU restatement of the reference MOT hot path.
+ *
+ * TEST INFRASTRUCTURE ONLY.  This library is the parity checker for the CUDA
+ * product path and the CPU baseline timed by bench.py (cpu_baseline, --impl
+ * reference).  It is never linked into or called by paper_2111_05205_b200/.
+ *
+ * It restates, line for line in behaviour (not in code), the reference files:
+ *   retarded_coeff_table      pkg/src/tdwavebem/elemint.py:89-186
+ *     _edge_frames            elemint.py:36-57
+ *     _clip_limits            elemint.py:60-76
+ *     _masked_forms           elemint.py:79-86
+ *     closed-form bundles     _closed_forms.py (re-derived: oracle/closed_forms.h)
+ *   mesh_stats / radii        mesh.py:64-75, 85-107
+ *   compute_gamma_star        marching.py:67-69
+ *   _arrival_sorted_pairs     marching.py:93-129
+ *   build_retarded_matrices   marching.py:132-181  (lag CSR, no upper cutoff)
+ *   TimeHistory sums          marching.py:205-242
+ *   build_step_matrix + march marching.py:279-338  (sigma/tau form)
+ * The sparse LU (scipy SuperLU) of the reference is replaced by Gauss-Seidel
+ * iterated to round-off on the strictly diagonally dominant step matrix
+ * (cond(A) <= 1.51), followed by the reference's residual test.
+ *
+ * Parity is pinned against tests/golden/*.npz produced by running the
+ * reference itself (tests/golden/make_golden.py).
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+#include "closed_forms.h"
+
+#define OR_OK 0
+#define OR_INVALID 1
+#define OR_SINGULAR 2
+#define OR_RESIDUAL 3
+#define OR_NOMEM 4
+
+static const double Y_TOL = 1e-12; /* elemint.py:33 */
+
+typedef void (*bundle_fn)(double, double, double, double, double*);
+
+static bundle_fn uw_fn(int d) {
+  return d == 1 ? tdw_uw_d1 : d == 2 ? tdw_uw_d2 : d == 3 ? tdw_uw_d3 : 0;
+}
+static bundle_fn bm_fn(int d) {
+  return d == 1 ? tdw_bm_d1 : d == 2 ? tdw_bm_d2 : d == 3 ? tdw_bm_d3 : 0;
+}
+
+static inline double ipow(double v, int e) {
+  double r = 1.0;
+  for (int k = 0; k < e; ++k) r *= v;
+  return r;
+}
+
+static inline double clipd(double a, double lo, double hi) {
+  /* np.clip(a, lo, hi) == minimum(maximum(a, lo), hi) */
+  double t = a > lo ? a : lo;
+  return t < hi ? t : hi;
+}
+
+/* One (P, triangle ABC, s) triple -> (U, W) or (Ubar, Wbar).
+ * kind 0 = "uw", 1 = "bm".  Follows elemint.py:116-186. */
+static void coeff_one(const double* P, const double* A, const double* B, const double* C,
+                      const double* ez, double s, int d, double K, int kind,
+                      const double* nx, double* out0, double* out1) {
+  const double* V1[3] = {A, B, C};
+  const double* V2[3] = {B, C, A};
+  double zs = (P[0] - A[0]) * ez[0] + (P[1] - A[1]) * ez[1] + (P[2] - A[2]) * ez[2];
+  double O[3] = {P[0] - zs * ez[0], P[1] - zs * ez[1], P[2] - zs * ez[2]};
+  double x1[3], x2[3], y[3], elen[3], xh[3][3], yh[3][3];
+  for (int e = 0; e < 3; ++e) {
+    double ev[3] = {V2[e][0] - V1[e][0], V2[e][1] - V1[e][1], V2[e][2] - V1[e][2]};
+    elen[e] = sqrt(ev[0] * ev[0] + ev[1] * ev[1] + ev[2] * ev[2]);
+    for (int k = 0; k < 3; ++k) xh[e][k] = ev[k] / elen[e];
+    yh[e][0] = ez[1] * xh[e][2] - ez[2] * xh[e][1];
+    yh[e][1] = ez[2] * xh[e][0] - ez[0] * xh[e][2];
+    yh[e][2] = ez[0] * xh[e][1] - ez[1] * xh[e][0];
+    double rel[3] = {V1[e][0] - O[0], V1[e][1] - O[1], V1[e][2] - O[2]};
+    x1[e] = rel[0] * xh[e][0] + rel[1] * xh[e][1] + rel[2] * xh[e][2];
+    x2[e] = x1[e] + elen[e];
+    y[e] = rel[0] * yh[e][0] + rel[1] * yh[e][1] + rel[2] * yh[e][2];
+  }
+  double za = fabs(zs);
+  double emax = elen[0];
+  if (elen[1] > emax) emax = elen[1];
+  if (elen[2] > emax) emax = elen[2];
+  double zscale = emax + fabs(zs);
+  double sgn = zs > 1e-12 * zscale ? 1.0 : -1.0;
+  double nx3 = 0.0;
+  if (kind == 1) nx3 = nx[0] * ez[0] + nx[1] * ez[1] + nx[2] * ez[2];
+
+  double acc0 = 0.0, acc1 = 0.0;
+  for (int e = 0; e < 3; ++e) {
+    double scale = elen[e] + za;
+    int alive = (fabs(y[e]) > Y_TOL * scale) && (s > za);
+    double xc2 = s * s - y[e] * y[e] - za * za;
+    int has = xc2 > 0.0;
+    double xc = sqrt(has ? xc2 : 0.0);
+    double xlo = clipd(x1[e], -xc, xc), xhi = clipd(x2[e], -xc, xc);
+    int fmask = has && (xhi > xlo) && alive;
+    int m1 = fmask && (x1[e] > -xc) && (x1[e] < xc);
+    int m2 = fmask && (x2[e] > -xc) && (x2[e] < xc);
+    double datan = 0.0, pw = 0.0;
+    if (alive) {
+      datan = atan(x2[e] / y[e]) - atan(x1[e] / y[e]);
+      pw = s - za;
+    }
+    double t0, t1;
+    if (kind == 0) {
+      double lo[2] = {0, 0}, hi[2] = {0, 0};
+      if (fmask) {
+        uw_fn(d)(xlo, y[e], za, s, lo);
+        uw_fn(d)(xhi, y[e], za, s, hi);
+      }
+      double a0 = -ipow(pw, d + 1) / (d + 1) * datan;
+      double az = sgn * ipow(pw, d) * datan;
+      t0 = a0 + hi[0] - lo[0];
+      t1 = az + sgn * (hi[1] - lo[1]);
+    } else {
+      double lo[8] = {0}, hi[8] = {0};
+      if (fmask) {
+        bm_fn(d)(xlo, y[e], za, s, lo);
+        bm_fn(d)(xhi, y[e], za, s, hi);
+      }
+      if (!m1) { lo[0] = 0.0; lo[1] = 0.0; }
+      if (!m2) { hi[0] = 0.0; hi[1] = 0.0; }
+      double n1 = nx[0] * xh[e][0] + nx[1] * xh[e][1] + nx[2] * xh[e][2];
+      double n2 = nx[0] * yh[e][0] + nx[1] * yh[e][1] + nx[2] * yh[e][2];
+      double pwd = ipow(pw, d);
+      double az = sgn * pwd * datan;
+      double as = -pwd * datan;
+      double azz = d > 1 ? -d * ipow(pw, d - 1) * datan : -(pw > 0.0 ? 1.0 : 0.0) * datan;
+      double azs = -sgn * azz;
+      double dPx = lo[0] - hi[0];
+      double dPy = -(hi[2] - lo[2]);
+      double dz = az + sgn * (hi[3] - lo[3]);
+      double ds = as + hi[4] - lo[4];
+      double dzPx = sgn * (lo[1] - hi[1]);
+      double dzPy = -sgn * (hi[5] - lo[5]);
+      double dzz = azz + hi[6] - lo[6];
+      double dzs = azs + sgn * (hi[7] - lo[7]);
+      t0 = n1 * dPx + n2 * dPy + nx3 * dz - ds;
+      t1 = n1 * dzPx + n2 * dzPy + nx3 * dzz - dzs;
+    }
+    acc0 += t0;
+    acc1 += t1;
+  }
+  if (kind == 0) {
+    *out0 = K * acc0;
+    *out1 = -K * acc1;
+  } else {
+    *out0 = K * acc0;
+    *out1 = -K * acc1;
+  }
+}
+
+static double kfac(int d, double c, double dt) {
+  double cd = c * dt, p = 1.0;
+  for (int k = 0; k < d; ++k) p *= cd;
+  return 1.0 / (4.0 * M_PI * p);
+}
+
+/* retarded_coeff_table (elemint.py:89).  Arrays are C-contiguous (n,3) / (n,). */
+int oracle_coeff_table(int64_t n, const double* P, const double* A, const double* B,
+                       const double* C, const double* ez, const double* s, int d, double c,
+                       double dt, int kind, const double* nx, double* out0, double* out1) {
+  if (d < 1 || d > 3) return OR_INVALID;
+  if (kind != 0 && kind != 1) return OR_INVALID;
+  if (kind == 1 && !nx) return OR_INVALID;
+  double K = kfac(d, c, dt);
+#pragma omp parallel for schedule(static)
+  for (int64_t t = 0; t < n; ++t) {
+    coeff_one(P + 3 * t, A + 3 * t, B + 3 * t, C + 3 * t, ez + 3 * t, s[t], d, K, kind,
+              kind == 1 ? nx + 3 * t : 0, out0 + t, out1 + t);
+  }
+  return OR_OK;
+}
+
+/* ------------------------------------------------------------------------ */
+/* mesh-derived quantities (mesh.py:42-75)                                    */
+typedef struct {
+  int ns;
+  const double* verts;
+  const int64_t* tris;
+  double *v0, *v1, *v2, *nrm, *cen, *rad;
+} omesh;
+
+static int mesh_build(omesh* m, int ns, const double* verts, const int64_t* tris) {
+  m->ns = ns;
+  m->verts = verts;
+  m->tris = tris;
+  m->v0 = malloc(sizeof(double) * 3 * ns);
+  m->v1 = malloc(sizeof(double) * 3 * ns);
+  m->v2 = malloc(sizeof(double) * 3 * ns);
+  m->nrm = malloc(sizeof(double) * 3 * ns);
+  m->cen = malloc(sizeof(double) * 3 * ns);
+  m->rad = malloc(sizeof(double) * ns);
+  if (!m->v0 || !m->v1 || !m->v2 || !m->nrm || !m->cen || !m->rad) return OR_NOMEM;
+  for (int e = 0; e < ns; ++e) {
+    const double* a = verts + 3 * tris[3 * e];
+    const double* b = verts + 3 * tris[3 * e + 1];
+    const double* cc = verts + 3 * tris[3 * e + 2];
+    double u[3], w[3], cr[3];
+    for (int k = 0; k < 3; ++k) {
+      m->v0[3 * e + k] = a[k];
+      m->v1[3 * e + k] = b[k];
+      m->v2[3 * e + k] = cc[k];
+      u[k] = b[k] - a[k];
+      w[k] = cc[k] - a[k];
+    }
+    cr[0] = u[1] * w[2] - u[2] * w[1];
+    cr[1] = u[2] * w[0] - u[0] * w[2];
+    cr[2] = u[0] * w[1] - u[1] * w[0];
+    double nn = sqrt(cr[0] * cr[0] + cr[1] * cr[1] + cr[2] * cr[2]);
+    double r = 0.0;
+    for (int k = 0; k < 3; ++k) {
+      m->nrm[3 * e + k] = cr[k] / nn;
+      m->cen[3 * e + k] = (a[k] + b[k] + cc[k]) / 3.0;
+    }
+    const double* vv[3] = {a, b, cc};
+    for (int q = 0; q < 3; ++q) {
+      double dx = vv[q][0] - m->cen[3 * e], dy = vv[q][1] - m->cen[3 * e + 1],
+             dz = vv[q][2] - m->cen[3 * e + 2];
+      double dd = sqrt(dx * dx + dy * dy + dz * dz);
+      if (dd > r) r = dd;
+    }
+    m->rad[e] = r;
+  }
+  return OR_OK;
+}
+
+static void mesh_free(omesh* m) {
+  free(m->v0); free(m->v1); free(m->v2); free(m->nrm); free(m->cen); free(m->rad);
+}
+
+/* max vertex diameter over used vertices (mesh.py:85-107) */
+double oracle_max_diameter(int nv, const double* verts, int ns, const int64_t* tris) {
+  char* used = calloc(nv, 1);
+  for (int64_t k = 0; k < 3 * (int64_t)ns; ++k) used[tris[k]] = 1;
+  double dmax = 0.0;
+#pragma omp parallel for reduction(max : dmax) schedule(dynamic, 16)
+  for (int i = 0; i < nv; ++i) {
+    if (!used[i]) continue;
+    for (int j = 0; j < nv; ++j) {
+      if (!used[j]) continue;
+      double dx = verts[3 * i] - verts[3 * j], dy = verts[3 * i + 1] - verts[3 * j + 1],
+             dz = verts[3 * i + 2] - verts[3 * j + 2];
+      double d2 = dx * dx + dy * dy + dz * dz;
+      if (d2 > dmax) dmax = d2;
+    }
+  }
+  free(used);
+  return sqrt(dmax);
+}
+
+int oracle_gamma_star(int nv, const double* verts, int ns, const int64_t* tris, int d, double c,
+                      double dt) {
+  double diam = oracle_max_diameter(nv, verts, ns, tris);
+  return (int)ceil(diam / (c * dt)) + d + 1;
+}
+
+/* ------------------------------------------------------------------------ */
+/* Lag CSR store: for row i, the arrived columns j (increasing) with their
+ * arrival lag a_ij (marching.py:110) and the per-lag values for g = a..G. */
+typedef struct {
+  int ns, G;
+  int64_t* rowptr;  /* pairs per row */
+  int32_t* col;
+  int32_t* arr;
+  int64_t* vptr;    /* offset of the pair's first value (lag a) */
+  double *U, *W;
+  int64_t nvals;
+} lagstore;
+
+static int arrival_of(const omesh* m, int i, int j, double c, double dt) {
+  double dx = m->cen[3 * i] - m->cen[3 * j], dy = m->cen[3 * i + 1] - m->cen[3 * j + 1],
+         dz = m->cen[3 * i + 2] - m->cen[3 * j + 2];
+  double dist = sqrt(dx * dx + dy * dy + dz * dz);
+  dist = dist - m->rad[j];
+  if (dist < 0.0) dist = 0.0;
+  int a = (int)ceil(dist / (c * dt)) - 1;
+  return a > 1 ? a : 1;
+}
+
+static void lag_free(lagstore* L) {
+  free(L->rowptr); free(L->col); free(L->arr); free(L->vptr); free(L->U); free(L->W);
+}
+
+static int lag_build(lagstore* L, const omesh* m, int row_lo, int row_hi, int G, int bie, int d,
+                     double c, double dt) {
+  int nr = row_hi - row_lo, ns = m->ns;
+  L->ns = ns;
+  L->G = G;
+  L->rowptr = calloc(nr + 1, sizeof(int64_t));
+  int64_t* vcount = calloc(nr + 1, sizeof(int64_t));
+  if (!L->rowptr || !vcount) return OR_NOMEM;
+#pragma omp parallel for schedule(dynamic, 8)
+  for (int r = 0; r < nr; ++r) {
+    int64_t np = 0, nv = 0;
+    for (int j = 0; j < ns; ++j) {
+      int a = arrival_of(m, row_lo + r, j, c, dt);
+      if (a <= G) { np++; nv += G - a + 1; }
+    }
+    L->rowptr[r + 1] = np;
+    vcount[r + 1] = nv;
+  }
+  for (int r = 0; r < nr; ++r) { L->rowptr[r + 1] += L->rowptr[r]; vcount[r + 1] += vcount[r]; }
+  int64_t npairs = L->rowptr[nr];
+  L->nvals = vcount[nr];
+  L->col = malloc(sizeof(int32_t) * (npairs ? npairs : 1));
+  L->arr = malloc(sizeof(int32_t) * (npairs ? npairs : 1));
+  L->vptr = malloc(sizeof(int64_t) * (npairs ? npairs : 1));
+  L->U = malloc(sizeof(double) * (L->nvals ? L->nvals : 1));
+  L->W = malloc(sizeof(double) * (L->nvals ? L->nvals : 1));
+  if (!L->col || !L->arr || !L->vptr || !L->U || !L->W) { free(vcount); return OR_NOMEM; }
+  double K = kfac(d, c, dt);
+  int kind = bie == 1 ? 1 : 0;
+#pragma omp parallel for schedule(dynamic, 4)
+  for (int r = 0; r < nr; ++r) {
+    int i = row_lo + r;
+    int64_t p = L->rowptr[r], v = vcount[r];
+    double nxi[3] = {-m->nrm[3 * i], -m->nrm[3 * i + 1], -m->nrm[3 * i + 2]};
+    for (int j = 0; j < ns; ++j) {
+      int a = arrival_of(m, i, j, c, dt);
+      if (a > G) continue;
+      L->col[p] = j;
+      L->arr[p] = a;
+      L->vptr[p] = v;
+      for (int g = a; g <= G; ++g) {
+        double s = (double)g * c * dt;
+        coeff_one(m->cen + 3 * i, m->v0 + 3 * j, m->v1 + 3 * j, m->v2 + 3 * j, m->nrm + 3 * j, s,
+                  d, K, kind, nxi, L->U + v, L->W + v);
+        ++v;
+      }
+      ++p;
+    }
+  }
+  free(vcount);
+  return OR_OK;
+}
+
+/* b_r += U_g tau - W_g sigma over the stored rows (one lag) -- the reference
+ * accumulates b += (U@tau - W@sig) per lag (marching.py:320-327). */
+static void lag_apply(const lagstore* L, int nr, int g, const double* tau, const double* sig,
+                      double* b, int first) {
+#pragma omp parallel for schedule(static) if (nr >= 2048)
+  for (int r = 0; r < nr; ++r) {
+    double su = 0.0, sw = 0.0;
+    for (int64_t p = L->rowptr[r]; p < L->rowptr[r + 1]; ++p) {
+      int a = L->arr[p];
+      if (a > g) continue;
+      int64_t v = L->vptr[p] + (g - a);
+      int j = L->col[p];
+      su += L->U[v] * tau[j];
+      sw += L->W[v] * sig[j];
+    }
+    b[r] = first ? (su - sw) : b[r] + (su - sw);
+  }
+}
+
+static double weights_d[4][5] = {
+    {0}, {1.0, -2.0, 1.0}, {0.5, -1.5, 1.5, -0.5}, {1.0 / 6, -2.0 / 3, 1.0, -2.0 / 3, 1.0 / 6}};
+
+/* Full march (marching.py:292-338).  All history arrays are (nt-1, ns).
+ * u_known / q_known are the Greville samples (marching.py:258-276).
+ * rhs_trace may be NULL.  Returns status in *status (0 stable, 1 unstable). */
+int oracle_march(int nv, const double* verts, int ns, const int64_t* tris, const double* phi,
+                 int bie, int d, double c, double dt, int nt, int window, double threshold,
+                 const double* u_known, const double* q_known, double* u, double* q, double* tau,
+                 double* sig, double* rhs_trace, int* n_steps, int* status, double* t_asm_out) {
+  if (d < 1 || d > 3 || nt < 2) return OR_INVALID;
+  omesh m;
+  int rc = mesh_build(&m, ns, verts, tris);
+  if (rc) return rc;
+  int gstar = oracle_gamma_star(nv, verts, ns, tris, d, c, dt);
+  int n_lags = window ? (gstar < nt - 1 ? gstar : nt - 1) : nt - 1;
+  lagstore L;
+  memset(&L, 0, sizeof(L));
+#ifdef _OPENMP
+  double t0 = omp_get_wtime();
+#endif
+  rc = lag_build(&L, &m, 0, ns, n_lags, bie, d, c, dt);
+#ifdef _OPENMP
+  if (t_asm_out) *t_asm_out = omp_get_wtime() - t0;
+#endif
+  if (rc) { mesh_free(&m); lag_free(&L); return rc; }
+  const double* w = weights_d[d];
+  double w0 = w[0];
+  /* step matrix A = w0 (W1 phi - U1 (1 - phi)) in row-compressed form */
+  int64_t* arow = calloc(ns + 1, sizeof(int64_t));
+  for (int i = 0; i < ns; ++i) {
+    int64_t cnt = 0;
+    for (int64_t p = L.rowptr[i]; p < L.rowptr[i + 1]; ++p) cnt += (L.arr[p] <= 1);
+    arow[i + 1] = arow[i] + cnt;
+  }
+  int32_t* acol = malloc(sizeof(int32_t) * (arow[ns] + 1));
+  double* aval = malloc(sizeof(double) * (arow[ns] + 1));
+  double* adiag = malloc(sizeof(double) * ns);
+  for (int i = 0; i < ns; ++i) {
+    int64_t k = arow[i];
+    adiag[i] = 0.0;
+    for (int64_t p = L.rowptr[i]; p < L.rowptr[i + 1]; ++p) {
+      if (L.arr[p] > 1) continue;
+      int j = L.col[p];
+      int64_t v = L.vptr[p];
+      double val = w0 * (L.W[v] * phi[j] - L.U[v] * (1.0 - phi[j]));
+      acol[k] = j;
+      aval[k] = val;
+      if (j == i) adiag[i] = val;
+      ++k;
+    }
+    if (adiag[i] == 0.0) { rc = OR_SINGULAR; }
+  }
+  double *b = malloc(sizeof(double) * ns), *x = malloc(sizeof(double) * ns),
+         *tt = malloc(sizeof(double) * ns), *st = malloc(sizeof(double) * ns),
+         *tw = malloc(sizeof(double) * ns), *sw = malloc(sizeof(double) * ns);
+  memset(u, 0, sizeof(double) * (size_t)(nt - 1) * ns);
+  memset(q, 0, sizeof(double) * (size_t)(nt - 1) * ns);
+  memset(tau, 0, sizeof(double) * (size_t)(nt - 1) * ns);
+  memset(sig, 0, sizeof(double) * (size_t)(nt - 1) * ns);
+  *status = 0;
+  *n_steps = 0;
+  for (int alpha = 1; alpha < nt && rc == OR_OK; ++alpha) {
+    int beta0 = alpha - 1;
+    int beta_star = alpha - gstar;
+    const double* uk = u_known + (size_t)beta0 * ns;
+    const double* qk = q_known + (size_t)beta0 * ns;
+    /* tilde sums (marching.py:227-237) */
+    for (int j = 0; j < ns; ++j) {
+      tt[j] = w0 * qk[j] * phi[j];
+      st[j] = w0 * uk[j] * (1.0 - phi[j]);
+    }
+    int kt = d + 1 < beta0 ? d + 1 : beta0;
+    for (int k = 1; k <= kt; ++k)
+      for (int j = 0; j < ns; ++j) {
+        tt[j] += w[k] * q[(size_t)(beta0 - k) * ns + j];
+        st[j] += w[k] * u[(size_t)(beta0 - k) * ns + j];
+      }
+    lag_apply(&L, ns, 1, tt, st, b, 1);
+    int gmax = alpha < n_lags ? alpha : n_lags;
+    for (int g = 2; g <= gmax; ++g) {
+      int beta = alpha - g;
+      const double *tp, *sp;
+      if (window && beta - beta_star <= d) {
+        /* windowed_sums (marching.py:216-225) */
+        int kmax = d + 1;
+        if (beta - beta_star < kmax) kmax = beta - beta_star;
+        if (beta < kmax) kmax = beta;
+        for (int j = 0; j < ns; ++j) { tw[j] = 0.0; sw[j] = 0.0; }
+        for (int k = 0; k <= kmax; ++k)
+          for (int j = 0; j < ns; ++j) {
+            tw[j] += w[k] * q[(size_t)(beta - k) * ns + j];
+            sw[j] += w[k] * u[(size_t)(beta - k) * ns + j];
+          }
+        tp = tw; sp = sw;
+      } else {
+        tp = tau + (size_t)beta * ns;
+        sp = sig + (size_t)beta * ns;
+      }
+      lag_apply(&L, ns, g, tp, sp, b, 0);
+    }
+    if (rhs_trace) memcpy(rhs_trace + (size_t)beta0 * ns, b, sizeof(double) * ns);
+    /* solve A x = b: Gauss-Seidel to round-off, then the reference residual test */
+    double bn = 0.0;
+    for (int i = 0; i < ns; ++i) { x[i] = b[i] / adiag[i]; bn += b[i] * b[i]; }
+    bn = sqrt(bn);
+    for (int it = 0; it < 200; ++it) {
+      double dn = 0.0, xn = 0.0;
+      for (int i = 0; i < ns; ++i) {
+        double acc = b[i];
+        for (int64_t k = arow[i]; k < arow[i + 1]; ++k)
+          if (acol[k] != i) acc -= aval[k] * x[acol[k]];
+        double xi = acc / adiag[i];
+        dn += (xi - x[i]) * (xi - x[i]);
+        xn += xi * xi;
+        x[i] = xi;
+      }
+      if (dn <= 1e-34 * xn || xn == 0.0) break;
+    }
+    double rn = 0.0;
+    for (int i = 0; i < ns; ++i) {
+      double acc = -b[i];
+      for (int64_t k = arow[i]; k < arow[i + 1]; ++k) acc += aval[k] * x[acol[k]];
+      rn += acc * acc;
+    }
+    rn = sqrt(rn);
+    if (rn > 1e-10 * (bn > 1e-300 ? bn : 1e-300)) { rc = OR_RESIDUAL; break; }
+    /* finalize_step (marching.py:239-242) */
+    double xmax = 0.0;
+    for (int j = 0; j < ns; ++j) {
+      size_t o = (size_t)beta0 * ns + j;
+      u[o] = phi[j] == 1.0 ? x[j] : uk[j];
+      q[o] = phi[j] == 1.0 ? qk[j] : x[j];
+      if (fabs(x[j]) > xmax) xmax = fabs(x[j]);
+    }
+    int ks = d + 1 < beta0 ? d + 1 : beta0;
+    for (int j = 0; j < ns; ++j) {
+      double ta = 0.0, sa = 0.0;
+      for (int k = 0; k <= ks; ++k) {
+        ta += w[k] * q[(size_t)(beta0 - k) * ns + j];
+        sa += w[k] * u[(size_t)(beta0 - k) * ns + j];
+      }
+      tau[(size_t)beta0 * ns + j] = ta;
+      sig[(size_t)beta0 * ns + j] = sa;
+    }
+    *n_steps = alpha;
+    if (xmax > threshold) { *status = 1; break; }
+  }
+  free(b); free(x); free(tt); free(st); free(tw); free(sw);
+  free(arow); free(acol); free(aval); free(adiag);
+  lag_free(&L);
+  mesh_free(&m);
+  return rc;
+}
+
+/* Bounded CPU-baseline sample (bench.py cpu_baseline / --impl reference):
+ * assemble the lag CSR for rows [row_lo, row_hi) and run n_steps of the
+ * per-step history SpMVs for those rows over synthetic densities.  Returns the
+ * assembly and loop wall seconds and the number of stored lag-CSR triples. */
+int oracle_sample(int nv, const double* verts, int ns, const int64_t* tris, int bie, int d,
+                  double c, double dt, int nt, int row_lo, int row_hi, int n_steps,
+                  double* t_asm, double* t_loop, int64_t* n_triples) {
+  omesh m;
+  int rc = mesh_build(&m, ns, verts, tris);
+  if (rc) return rc;
+  int gstar = oracle_gamma_star(nv, verts, ns, tris, d, c, dt);
+  int n_lags = gstar < nt - 1 ? gstar : nt - 1;
+  lagstore L;
+  memset(&L, 0, sizeof(L));
+  int nr = row_hi - row_lo;
+#ifdef _OPENMP
+  double t0 = omp_get_wtime();
+#endif
+  rc = lag_build(&L, &m, row_lo, row_hi, n_lags, bie, d, c, dt);
+#ifdef _OPENMP
+  *t_asm = omp_get_wtime() - t0;
+#endif
+  *n_triples = L.nvals;
+  double* hist = malloc(sizeof(double) * 2 * (size_t)ns * (n_lags + 1));
+  for (size_t k = 0; k < 2 * (size_t)ns * (n_lags + 1); ++k) hist[k] = 1e-3 * (double)(k % 97);
+  double* b = malloc(sizeof(double) * (nr > 0 ? nr : 1));
+#ifdef _OPENMP
+  t0 = omp_get_wtime();
+#endif
+  for (int st = 0; st < n_steps && rc == OR_OK; ++st) {
+    for (int g = 1; g <= n_lags; ++g) {
+      const double* tp = hist + (size_t)(2 * g) * ns / 2;
+      const double* sp = hist + (size_t)(2 * g + 1) * ns / 2;
+      lag_apply(&L, nr, g, tp, sp, b, g == 1);
+    }
+  }
+#ifdef _OPENMP
+  *t_loop = omp_get_wtime() - t0;
+#endif
+  free(hist); free(b);
+  lag_free(&L);
+  mesh_free(&m);
+  return rc;
+}
+
+int oracle_num_threads(void) {
+#ifdef _OPENMP
+  return omp_get_max_threads();
+#else
+  return 1;
+#endif
+}

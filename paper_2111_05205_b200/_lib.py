@@ -1,0 +1,146 @@
+"""ctypes binding of libtdw.so (the C ABI declared in include/tdw.h).
+
+The product path has no CPU fallback: if the library is missing or no CUDA
+device is visible, every entry point raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from pathlib import Path
+
+import numpy as np
+
+LIB_PATH = Path(__file__).resolve().parent / "libtdw.so"
+
+TDW_OK = 0
+_ERRORS = {1: ValueError, 2: ValueError, 3: RuntimeError, 4: RuntimeError, 5: RuntimeError,
+           6: RuntimeError, 7: RuntimeError, 8: RuntimeError}
+
+_dp = C.POINTER(C.c_double)
+_i64p = C.POINTER(C.c_int64)
+_i32p = C.POINTER(C.c_int32)
+
+
+class ProblemDesc(C.Structure):
+    _fields_ = [("ns", C.c_int32), ("nv", C.c_int32), ("vertices", _dp), ("triangles", _i64p),
+                ("phi", _dp), ("bie", C.c_int32), ("d", C.c_int32), ("c", C.c_double),
+                ("dt", C.c_double), ("nt", C.c_int32), ("window", C.c_int32),
+                ("nranks", C.c_int32), ("rank", C.c_int32)]
+
+
+class Info(C.Structure):
+    _fields_ = [("gamma_star", C.c_int32), ("n_lags", C.c_int32), ("row_lo", C.c_int32),
+                ("row_hi", C.c_int32), ("n_band", C.c_int64), ("n_pairs", C.c_int64),
+                ("n_evals", C.c_int64), ("store_bytes", C.c_int64), ("step_nnz", C.c_int32),
+                ("jacobi_iters", C.c_int32), ("jacobi_bound", C.c_double),
+                ("t_assemble_ms", C.c_double), ("t_fill_ms", C.c_double)]
+
+    def asdict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+class Timing(C.Structure):
+    _fields_ = [("total_ms", C.c_double), ("conv_ms", C.c_double), ("solve_ms", C.c_double),
+                ("comm_ms", C.c_double), ("conv_launches", C.c_int32), ("steps", C.c_int32)]
+
+    def asdict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+EXPORTS = {
+    "tdw_init": ([C.c_int, C.POINTER(C.c_void_p)], C.c_int),
+    "tdw_finalize": ([C.c_void_p], C.c_int),
+    "tdw_last_error": ([C.c_void_p], C.c_char_p),
+    "tdw_device_count": ([], C.c_int),
+    "tdw_coeff_table": ([C.c_void_p, C.c_int64, _dp, _dp, _dp, _dp, _dp, _dp, C.c_int, C.c_double,
+                         C.c_double, C.c_int, _dp, _dp, _dp], C.c_int),
+    "tdw_coeff_table_device": ([C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p,
+                                C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_double,
+                                C.c_double, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,
+                                C.POINTER(C.c_float)], C.c_int),
+    "tdw_problem_create": ([C.c_void_p, C.POINTER(ProblemDesc), C.POINTER(C.c_void_p)], C.c_int),
+    "tdw_assemble": ([C.c_void_p], C.c_int),
+    "tdw_problem_info": ([C.c_void_p, C.POINTER(Info)], C.c_int),
+    "tdw_march": ([C.c_void_p, _dp, _dp, C.c_double, _dp, _dp, _dp, _dp, _dp, _i32p, _i32p],
+                  C.c_int),
+    "tdw_upload_known": ([C.c_void_p, _dp, _dp], C.c_int),
+    "tdw_march_resident": ([C.c_void_p, C.c_double, C.c_int, C.c_int, C.POINTER(Timing)], C.c_int),
+    "tdw_download": ([C.c_void_p, _dp, _dp, _dp, _dp, _i32p, _i32p], C.c_int),
+    "tdw_problem_destroy": ([C.c_void_p], C.c_int),
+    "tdw_nccl_unique_id": ([C.c_char_p], C.c_int),
+    "tdw_comm_init": ([C.c_void_p, C.c_char_p, C.c_int, C.c_int], C.c_int),
+}
+
+_lib = None
+
+
+def load():
+    """Load libtdw.so (raises if it was not built)."""
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise RuntimeError(f"{LIB_PATH} is missing: run __graft_entry__.build() "
+                               "(the CUDA path has no CPU fallback)")
+        lib = C.CDLL(str(LIB_PATH))
+        for name, (args, res) in EXPORTS.items():
+            fn = getattr(lib, name)
+            fn.argtypes = args
+            fn.restype = res
+        _lib = lib
+    return _lib
+
+
+def dptr(a: np.ndarray):
+    return a.ctypes.data_as(_dp)
+
+
+def check(rc: int, ctx=None, what: str = ""):
+    if rc == TDW_OK:
+        return
+    msg = ""
+    if ctx is not None and ctx.value:
+        raw = load().tdw_last_error(ctx)
+        msg = raw.decode() if raw else ""
+    exc = _ERRORS.get(rc, RuntimeError)
+    raise exc(f"{what}: {msg or f'libtdw error {rc}'}")
+
+
+class Context:
+    """One CUDA device, one stream (tdw_ctx)."""
+
+    def __init__(self, device: int | None = None):
+        lib = load()
+        if device is None:
+            device = int(os.environ.get("LOCAL_RANK", "0"))
+        if lib.tdw_device_count() <= device:
+            raise RuntimeError("no CUDA device visible: the MOT path runs on the GPU only")
+        self.h = C.c_void_p()
+        check(lib.tdw_init(int(device), C.byref(self.h)), None, "tdw_init")
+        self.device = device
+
+    def close(self):
+        if self.h.value:
+            load().tdw_finalize(self.h)
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+_default_ctx: Context | None = None
+
+
+def default_context() -> Context:
+    global _default_ctx
+    if _default_ctx is None:
+        _default_ctx = Context()
+    return _default_ctx
+
+
+def set_default_context(ctx: Context):
+    global _default_ctx
+    _default_ctx = ctx

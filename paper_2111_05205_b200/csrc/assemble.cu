@@ -1,0 +1,510 @@
+// assemble.cu -- banded kappa-combined coefficient store + lag-1 step matrix.
+//
+// Replaces marching.build_retarded_matrices (marching.py:132-181) and
+// build_step_matrix (marching.py:279-289).  Instead of the reference's per-lag
+// CSR of U^(g) over every arrived pair (no upper cutoff, marching.py:76-81),
+// the store holds the kappa-combined coefficients
+//     V^(gamma)_ij = sum_{kappa=0}^{d+1} w^kappa U^(gamma-kappa)_ij
+// (and the same for W) only on each pair's band [glo, ghi], where
+//     glo = max(arrival_ij, floor(r_min/(c dt)) + 1)       (first lag the wavefront touches E_j)
+//     ghi = min(cap, floor(r_max/(c dt)) + 1 + d)          (after that V is identically zero:
+//                                                          U is a degree-d polynomial in gamma
+//                                                          once the wavefront has passed E_j and
+//                                                          the w^kappa annihilate it)
+// arrival_ij is the reference's conservative lag (marching.py:108-110); U^(g)
+// for g < arrival_ij is zero exactly as in the reference's lag CSR.  The history
+// sum b = sum_g (U^(g) tau - W^(g) sigma) (marching.py:320-327) is then the
+// banded convolution sum_gamma (V_U^(gamma) q - V_W^(gamma) u).
+//
+// Layout: rows in Morton order, columns cut in
+// 32-wide J-tiles.  A segment = (row, J-tile) = 32 pairs = one warp; its pairs
+// are sorted by band length (descending) and their coefficients are stored
+// k-major ("jagged"): entry (k, lane) at segoff + sum_{k'<k} n_k' + lane where
+// n_k = #pairs with len > k.  The convolution warp therefore reads 16 B per
+// lane per k fully coalesced with no padding.
+#include <cub/cub.cuh>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <climits>
+#include <cmath>
+
+#include "coeff.cuh"
+#include "tdw_impl.cuh"
+
+namespace tdw {
+
+#define FULLMASK 0xffffffffu
+
+struct Elem {
+  double v0[3], v1[3], v2[3], n[3], c[3], rad;
+};
+
+__device__ __forceinline__ void load_elem(const double* __restrict__ E, int j, Elem& e) {
+  const double* p = E + (size_t)j * TDW_ELEM_STRIDE;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    e.v0[k] = p[k];
+    e.v1[k] = p[3 + k];
+    e.v2[k] = p[6 + k];
+    e.n[k] = p[9 + k];
+    e.c[k] = p[12 + k];
+  }
+  e.rad = p[15];
+}
+
+__device__ __forceinline__ double dot3(const double* a, const double* b) {
+  return a[0] * b[0] + a[1] * b[1] + a[2] * b[2];
+}
+
+// exact point-triangle distance (closest point by Voronoi region)
+__device__ double point_triangle_distance(const double* p, const double* a, const double* b,
+                                          const double* c) {
+  double ab[3], ac[3], ap[3], q[3];
+  for (int k = 0; k < 3; ++k) {
+    ab[k] = b[k] - a[k];
+    ac[k] = c[k] - a[k];
+    ap[k] = p[k] - a[k];
+  }
+  double d1 = dot3(ab, ap), d2 = dot3(ac, ap);
+  if (d1 <= 0.0 && d2 <= 0.0) {
+    for (int k = 0; k < 3; ++k) q[k] = a[k];
+  } else {
+    double bp[3] = {p[0] - b[0], p[1] - b[1], p[2] - b[2]};
+    double d3 = dot3(ab, bp), d4 = dot3(ac, bp);
+    double cp[3] = {p[0] - c[0], p[1] - c[1], p[2] - c[2]};
+    double d5 = dot3(ab, cp), d6 = dot3(ac, cp);
+    double vc = d1 * d4 - d3 * d2, vb = d5 * d2 - d1 * d6, va = d3 * d6 - d5 * d4;
+    if (d3 >= 0.0 && d4 <= d3) {
+      for (int k = 0; k < 3; ++k) q[k] = b[k];
+    } else if (vc <= 0.0 && d1 >= 0.0 && d3 <= 0.0) {
+      double v = d1 / (d1 - d3);
+      for (int k = 0; k < 3; ++k) q[k] = a[k] + v * ab[k];
+    } else if (d6 >= 0.0 && d5 <= d6) {
+      for (int k = 0; k < 3; ++k) q[k] = c[k];
+    } else if (vb <= 0.0 && d2 >= 0.0 && d6 <= 0.0) {
+      double w = d2 / (d2 - d6);
+      for (int k = 0; k < 3; ++k) q[k] = a[k] + w * ac[k];
+    } else if (va <= 0.0 && (d4 - d3) >= 0.0 && (d5 - d6) >= 0.0) {
+      double w = (d4 - d3) / ((d4 - d3) + (d5 - d6));
+      for (int k = 0; k < 3; ++k) q[k] = b[k] + w * (c[k] - b[k]);
+    } else {
+      double den = 1.0 / (va + vb + vc);
+      double v = vb * den, w = vc * den;
+      for (int k = 0; k < 3; ++k) q[k] = a[k] + ab[k] * v + ac[k] * w;
+    }
+  }
+  double dx = p[0] - q[0], dy = p[1] - q[1], dz = p[2] - q[2];
+  return sqrt(dx * dx + dy * dy + dz * dz);
+}
+
+// conservative arrival lag of the reference (marching.py:108-110)
+__device__ __forceinline__ int arrival_lag(const double* ci, const Elem& ej, double cdt) {
+  double dx = ci[0] - ej.c[0], dy = ci[1] - ej.c[1], dz = ci[2] - ej.c[2];
+  double dist = sqrt(dx * dx + dy * dy + dz * dz);
+  dist = fmax(dist - ej.rad, 0.0);
+  int a = (int)ceil(dist / cdt) - 1;
+  return a > 1 ? a : 1;
+}
+
+struct Band {
+  int glo, ghi, arr;
+};
+
+__device__ __forceinline__ Band pair_band(const double* ci, const Elem& ej, double cdt, int d,
+                                          int cap) {
+  Band b;
+  b.arr = arrival_lag(ci, ej, cdt);
+  double rmin = point_triangle_distance(ci, ej.v0, ej.v1, ej.v2);
+  double r0 = sqrt((ci[0] - ej.v0[0]) * (ci[0] - ej.v0[0]) + (ci[1] - ej.v0[1]) * (ci[1] - ej.v0[1]) +
+                   (ci[2] - ej.v0[2]) * (ci[2] - ej.v0[2]));
+  double r1 = sqrt((ci[0] - ej.v1[0]) * (ci[0] - ej.v1[0]) + (ci[1] - ej.v1[1]) * (ci[1] - ej.v1[1]) +
+                   (ci[2] - ej.v1[2]) * (ci[2] - ej.v1[2]));
+  double r2 = sqrt((ci[0] - ej.v2[0]) * (ci[0] - ej.v2[0]) + (ci[1] - ej.v2[1]) * (ci[1] - ej.v2[1]) +
+                   (ci[2] - ej.v2[2]) * (ci[2] - ej.v2[2]));
+  double rmax = fmax(fmax(r0, r1), r2);
+  // first lag with c*g*dt > r_min (with a relative guard: an extra noise-level
+  // entry is harmless, a missing one is not)
+  int g0 = (int)floor(rmin / cdt * (1.0 - 1e-10)) + 1;
+  b.glo = max(max(g0, b.arr), 1);
+  int gfull = (int)floor(rmax / cdt * (1.0 + 1e-10)) + 1;
+  b.ghi = min(cap, gfull + d);
+  return b;
+}
+
+__device__ __forceinline__ void bspline_weights(int d, double* w) {
+  if (d == 1) { w[0] = 1.0; w[1] = -2.0; w[2] = 1.0; }
+  if (d == 2) { w[0] = 0.5; w[1] = -1.5; w[2] = 1.5; w[3] = -0.5; }
+  if (d == 3) { w[0] = 1.0 / 6.0; w[1] = -(2.0 / 3.0); w[2] = 1.0; w[3] = -(2.0 / 3.0); w[4] = 1.0 / 6.0; }
+}
+
+struct AsmArgs {
+  const double* elem;
+  int ns, row_lo, rows_loc, ntiles, d, cap;
+  double c, dt, K;
+  uint32_t* hdr;
+  unsigned long long* segcount;  // count pass output / fill pass: segoff
+  int2* unit;
+  unsigned long long* n_evals;
+  unsigned long long* n_pairs;
+  double2* coef;
+  int* flags;
+};
+
+__global__ void __launch_bounds__(256) count_kernel(AsmArgs a) {
+  const int lane = threadIdx.x & 31;
+  const long long seg = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long nseg = (long long)a.rows_loc * a.ntiles;
+  if (seg >= nseg) return;
+  const int rloc = (int)(seg / a.ntiles), t = (int)(seg % a.ntiles);
+  const int i = a.row_lo + rloc, j = t * TDW_TJ + lane;
+  const double cdt = a.c * a.dt;
+  int len = 0, glo = 0;
+  if (i < a.ns && j < a.ns) {
+    Elem ej;
+    load_elem(a.elem, j, ej);
+    const double* ci = a.elem + (size_t)i * TDW_ELEM_STRIDE + 12;
+    Band b = pair_band(ci, ej, cdt, a.d, a.cap);
+    if (b.ghi >= b.glo) {
+      len = b.ghi - b.glo + 1;
+      glo = b.glo;
+    }
+    if (len > 255) { atomicExch(&a.flags[3], 2); len = 255; }
+  }
+  int rank = 0;
+#pragma unroll
+  for (int m = 0; m < 32; ++m) {
+    int lm = __shfl_sync(FULLMASK, len, m);
+    rank += (lm > len) || (lm == len && m < lane);
+  }
+  a.hdr[seg * TDW_TJ + rank] = hdr_pack(lane, len, glo);
+  int tot = len, gmin = len ? glo : INT_MAX, gmax = len ? glo + len - 1 : -1, np = len ? 1 : 0;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    tot += __shfl_xor_sync(FULLMASK, tot, o);
+    np += __shfl_xor_sync(FULLMASK, np, o);
+    gmin = min(gmin, __shfl_xor_sync(FULLMASK, gmin, o));
+    gmax = max(gmax, __shfl_xor_sync(FULLMASK, gmax, o));
+  }
+  if (lane == 0) {
+    a.segcount[seg] = (unsigned long long)tot;
+    if (np) {
+      atomicAdd(a.n_pairs, (unsigned long long)np);
+      int2* u = &a.unit[(rloc / TDW_TI) * a.ntiles + t];
+      atomicMin(&u->x, gmin);
+      atomicMax(&u->y, gmax);
+    }
+  }
+}
+
+template <int D, bool BM>
+__global__ void __launch_bounds__(128) fill_kernel(AsmArgs a) {
+  const int lane = threadIdx.x & 31;
+  const long long seg = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const long long nseg = (long long)a.rows_loc * a.ntiles;
+  if (seg >= nseg) return;
+  const uint32_t h = a.hdr[seg * TDW_TJ + lane];
+  const int len = hdr_len(h), glo = hdr_glo(h), jl = hdr_jl(h);
+  const int lmax = __shfl_sync(FULLMASK, len, 0);
+  if (lmax == 0) return;
+  const int rloc = (int)(seg / a.ntiles), t = (int)(seg % a.ntiles);
+  const int i = a.row_lo + rloc, j = t * TDW_TJ + jl;
+  const unsigned long long base = a.segcount[seg];  // exclusive offsets after the scan
+  const double cdt = a.c * a.dt;
+  double w[D + 2];
+  bspline_weights(D, w);
+  double ru[D + 2], rw[D + 2];
+#pragma unroll
+  for (int k = 0; k < D + 2; ++k) { ru[k] = 0.0; rw[k] = 0.0; }
+  PairGeom g;
+  long long nev = 0;
+  if (len > 0) {
+    Elem ej;
+    load_elem(a.elem, j, ej);
+    const double* pi = a.elem + (size_t)i * TDW_ELEM_STRIDE;
+    double ci[3] = {pi[12], pi[13], pi[14]};
+    double nx[3] = {-pi[9], -pi[10], -pi[11]};  // BM operator normal (marching.py:168-173)
+    pair_geom<BM>(ci, ej.v0, ej.v1, ej.v2, ej.n, nx, g);
+    const int arr = arrival_lag(ci, ej, cdt);
+    const int gfirst = max(max(arr, 1), glo - (D + 1));
+    for (int gg = gfirst; gg < glo; ++gg) {
+      double u, v;
+      coeff_eval<D, BM>(g, (double)gg * a.c * a.dt, a.K, u, v);
+#pragma unroll
+      for (int k = D + 1; k > 0; --k) { ru[k] = ru[k - 1]; rw[k] = rw[k - 1]; }
+      ru[0] = u;
+      rw[0] = v;
+      ++nev;
+    }
+  }
+  unsigned long long off = base;
+  for (int k = 0; k < lmax; ++k) {
+    const unsigned m = __ballot_sync(FULLMASK, len > k);
+    if (len > k) {
+      const int gg = glo + k;
+      double u, v;
+      coeff_eval<D, BM>(g, (double)gg * a.c * a.dt, a.K, u, v);
+#pragma unroll
+      for (int q = D + 1; q > 0; --q) { ru[q] = ru[q - 1]; rw[q] = rw[q - 1]; }
+      ru[0] = u;
+      rw[0] = v;
+      ++nev;
+      double vu = 0.0, vw = 0.0;
+#pragma unroll
+      for (int q = 0; q < D + 2; ++q) {
+        vu += w[q] * ru[q];
+        vw += w[q] * rw[q];
+      }
+      a.coef[off + lane] = make_double2(vu, vw);
+    }
+    off += __popc(m);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) nev += __shfl_xor_sync(FULLMASK, nev, o);
+  if (lane == 0) atomicAdd(a.n_evals, (unsigned long long)nev);
+}
+
+struct StepArgs {
+  const double* elem;
+  const double* phi;
+  int ns, ntiles, d;
+  double c, dt, K, w0;
+  int* acol;      // [TDW_ELL_MAX][ns]
+  double* aval;   // [TDW_ELL_MAX][ns]
+  double* adiag;  // [ns]
+  int* flags;     // [4]: ell width max at [2], overflow at [3]
+  unsigned long long* bound_bits;
+  unsigned long long* nnz;
+};
+
+// lag-1 step matrix A = w0 (W1 phi - U1 (1 - phi)) over all rows (replicated
+// on every rank): exactly the pairs whose band starts at gamma = 1.
+template <int D, bool BM>
+__global__ void __launch_bounds__(128) stepmat_kernel(StepArgs a) {
+  const int lane = threadIdx.x & 31;
+  const int i = (int)(((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  if (i >= a.ns) return;
+  const double cdt = a.c * a.dt;
+  const double* pi = a.elem + (size_t)i * TDW_ELEM_STRIDE;
+  double ci[3] = {pi[12], pi[13], pi[14]};
+  double nx[3] = {-pi[9], -pi[10], -pi[11]};
+  int cnt = 0;
+  double diag = 0.0, offsum = 0.0;
+  for (int t = 0; t < a.ntiles; ++t) {
+    const int j = t * TDW_TJ + lane;
+    bool take = false;
+    Elem ej;
+    if (j < a.ns) {
+      load_elem(a.elem, j, ej);
+      double dx = ci[0] - ej.c[0], dy = ci[1] - ej.c[1], dz = ci[2] - ej.c[2];
+      double dcc = sqrt(dx * dx + dy * dy + dz * dz);
+      if (dcc - ej.rad <= 2.0 * cdt * (1.0 + 1e-9)) {
+        Band b = pair_band(ci, ej, cdt, a.d, 1 << 30);
+        take = (b.glo == 1);
+      }
+    }
+    const unsigned m = __ballot_sync(FULLMASK, take);
+    const int pos = cnt + __popc(m & ((1u << lane) - 1u));
+    if (take) {
+      PairGeom g;
+      pair_geom<BM>(ci, ej.v0, ej.v1, ej.v2, ej.n, nx, g);
+      double u, w;
+      coeff_eval<D, BM>(g, 1.0 * a.c * a.dt, a.K, u, w);
+      const double pj = a.phi[j];
+      const double val = a.w0 * (w * pj - u * (1.0 - pj));
+      if (pos < TDW_ELL_MAX) {
+        a.acol[(size_t)pos * a.ns + i] = j;
+        a.aval[(size_t)pos * a.ns + i] = val;
+      }
+      if (j == i) diag = val;
+      else offsum += fabs(val);
+    }
+    cnt += __popc(m);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    diag += __shfl_xor_sync(FULLMASK, diag, o);
+    offsum += __shfl_xor_sync(FULLMASK, offsum, o);
+  }
+  for (int p = cnt + lane; p < TDW_ELL_MAX; p += 32) {
+    a.acol[(size_t)p * a.ns + i] = i;
+    a.aval[(size_t)p * a.ns + i] = 0.0;
+  }
+  if (lane == 0) {
+    a.adiag[i] = diag;
+    atomicMax(&a.flags[2], cnt);
+    if (cnt > TDW_ELL_MAX) atomicExch(&a.flags[3], 1);
+    atomicAdd(a.nnz, (unsigned long long)cnt);
+    double bound = diag != 0.0 ? offsum / fabs(diag) : 1e300;
+    atomicMax(a.bound_bits, (unsigned long long)__double_as_longlong(bound));
+  }
+}
+
+template <int D, bool BM>
+static void launch_fill(const AsmArgs& a, long long nseg, cudaStream_t st) {
+  const int threads = 128;
+  long long blocks = (nseg * 32 + threads - 1) / threads;
+  fill_kernel<D, BM><<<(unsigned)blocks, threads, 0, st>>>(a);
+}
+
+template <int D, bool BM>
+static void launch_step(const StepArgs& a, cudaStream_t st) {
+  const int threads = 128;
+  long long blocks = ((long long)a.ns * 32 + threads - 1) / threads;
+  stepmat_kernel<D, BM><<<(unsigned)blocks, threads, 0, st>>>(a);
+}
+
+__global__ void fill_unit_init(int2* u, long long n) {
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n;
+       k += (long long)gridDim.x * blockDim.x)
+    u[k] = make_int2(INT_MAX, -1);
+}
+
+}  // namespace tdw
+
+using namespace tdw;
+
+int tdw_assemble_impl(tdw_problem* pb) {
+  tdw_ctx* ctx = pb->ctx;
+  cudaStream_t st = ctx->stream;
+  cudaEvent_t e0, e1, f0, f1;
+  TDW_CUDA(ctx, cudaEventCreate(&e0));
+  TDW_CUDA(ctx, cudaEventCreate(&e1));
+  TDW_CUDA(ctx, cudaEventCreate(&f0));
+  TDW_CUDA(ctx, cudaEventCreate(&f1));
+  TDW_CUDA(ctx, cudaEventRecord(e0, st));
+
+  const long long nseg = (long long)pb->rows_per_rank * pb->ntiles;
+  const long long nunit = (long long)pb->n_iblk * pb->ntiles;
+  TDW_CUDA(ctx, cudaMalloc(&pb->d_hdr, sizeof(uint32_t) * nseg * TDW_TJ));
+  TDW_CUDA(ctx, cudaMalloc(&pb->d_segoff, sizeof(unsigned long long) * (nseg + 1)));
+  TDW_CUDA(ctx, cudaMalloc(&pb->d_unit, sizeof(int2) * nunit));
+  unsigned long long* d_cnt = nullptr;  // {n_evals, n_pairs, nnz, bound_bits}
+  TDW_CUDA(ctx, cudaMalloc(&d_cnt, sizeof(unsigned long long) * 4));
+  TDW_CUDA(ctx, cudaMemsetAsync(d_cnt, 0, sizeof(unsigned long long) * 4, st));
+  TDW_CUDA(ctx, cudaMemsetAsync(pb->d_flags, 0, sizeof(int) * 4, st));
+  fill_unit_init<<<256, 256, 0, st>>>(pb->d_unit, nunit);
+
+  AsmArgs a{};
+  a.elem = pb->d_elem;
+  a.ns = pb->ns;
+  a.row_lo = pb->row_lo;
+  a.rows_loc = pb->rows_per_rank;
+  a.ntiles = pb->ntiles;
+  a.d = pb->d;
+  a.cap = pb->cap;
+  a.c = pb->c;
+  a.dt = pb->dt;
+  a.K = pb->K;
+  a.hdr = pb->d_hdr;
+  a.segcount = pb->d_segoff;
+  a.unit = pb->d_unit;
+  a.n_evals = d_cnt;
+  a.n_pairs = d_cnt + 1;
+  a.flags = pb->d_flags;
+  {
+    const int threads = 256;
+    long long blocks = (nseg * 32 + threads - 1) / threads;
+    count_kernel<<<(unsigned)blocks, threads, 0, st>>>(a);
+    TDW_CUDA(ctx, cudaGetLastError());
+  }
+  // exclusive scan of the segment entry counts -> segment offsets (in place)
+  {
+    size_t tmp_bytes = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, pb->d_segoff, pb->d_segoff, nseg + 1, st);
+    void* tmp = nullptr;
+    TDW_CUDA(ctx, cudaMalloc(&tmp, tmp_bytes));
+    // the element after the last segment must be zero before the scan
+    TDW_CUDA(ctx, cudaMemsetAsync(pb->d_segoff + nseg, 0, sizeof(unsigned long long), st));
+    cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, pb->d_segoff, pb->d_segoff, nseg + 1, st);
+    TDW_CUDA(ctx, cudaGetLastError());
+    TDW_CUDA(ctx, cudaStreamSynchronize(st));
+    cudaFree(tmp);
+  }
+  int hflags[4];
+  TDW_CUDA(ctx, cudaMemcpy(hflags, pb->d_flags, sizeof(hflags), cudaMemcpyDeviceToHost));
+  if (hflags[3] == 2)
+    return tdw_fail(ctx, TDW_ERR_LIMIT, "a pair band exceeds 255 lags (c*dt far below the element size)");
+  unsigned long long n_band = 0;
+  TDW_CUDA(ctx, cudaMemcpy(&n_band, pb->d_segoff + nseg, sizeof(n_band), cudaMemcpyDeviceToHost));
+  pb->n_band = (int64_t)n_band;
+  {
+    std::vector<int2> hu(nunit);
+    TDW_CUDA(ctx, cudaMemcpy(hu.data(), pb->d_unit, sizeof(int2) * nunit, cudaMemcpyDeviceToHost));
+    int wm = 1;
+    for (const int2& u : hu)
+      if (u.y >= u.x) wm = std::max(wm, u.y - u.x + 1);
+    pb->wmax = wm;
+  }
+  TDW_CUDA(ctx, cudaMalloc(&pb->d_coef, sizeof(double2) * (n_band ? n_band : 1)));
+  a.coef = pb->d_coef;
+  TDW_CUDA(ctx, cudaEventRecord(f0, st));
+  const bool bm = pb->bie == TDW_BIE_BMBIE;
+  if (pb->d == 1) { if (bm) launch_fill<1, true>(a, nseg, st); else launch_fill<1, false>(a, nseg, st); }
+  if (pb->d == 2) { if (bm) launch_fill<2, true>(a, nseg, st); else launch_fill<2, false>(a, nseg, st); }
+  if (pb->d == 3) { if (bm) launch_fill<3, true>(a, nseg, st); else launch_fill<3, false>(a, nseg, st); }
+  TDW_CUDA(ctx, cudaGetLastError());
+  TDW_CUDA(ctx, cudaEventRecord(f1, st));
+
+  // lag-1 step matrix (all rows)
+  TDW_CUDA(ctx, cudaMalloc(&pb->d_acol, sizeof(int) * (size_t)TDW_ELL_MAX * pb->ns));
+  TDW_CUDA(ctx, cudaMalloc(&pb->d_aval, sizeof(double) * (size_t)TDW_ELL_MAX * pb->ns));
+  TDW_CUDA(ctx, cudaMalloc(&pb->d_adiag, sizeof(double) * pb->ns));
+  StepArgs s{};
+  s.elem = pb->d_elem;
+  s.phi = pb->d_phi;
+  s.ns = pb->ns;
+  s.ntiles = pb->ntiles;
+  s.d = pb->d;
+  s.c = pb->c;
+  s.dt = pb->dt;
+  s.K = pb->K;
+  s.w0 = pb->d == 1 ? 1.0 : (pb->d == 2 ? 0.5 : 1.0 / 6.0);
+  s.acol = pb->d_acol;
+  s.aval = pb->d_aval;
+  s.adiag = pb->d_adiag;
+  s.flags = pb->d_flags;
+  s.bound_bits = d_cnt + 3;
+  s.nnz = d_cnt + 2;
+  if (pb->d == 1) { if (bm) launch_step<1, true>(s, st); else launch_step<1, false>(s, st); }
+  if (pb->d == 2) { if (bm) launch_step<2, true>(s, st); else launch_step<2, false>(s, st); }
+  if (pb->d == 3) { if (bm) launch_step<3, true>(s, st); else launch_step<3, false>(s, st); }
+  TDW_CUDA(ctx, cudaGetLastError());
+  TDW_CUDA(ctx, cudaEventRecord(e1, st));
+  TDW_CUDA(ctx, cudaStreamSynchronize(st));
+
+  unsigned long long hc[4];
+  TDW_CUDA(ctx, cudaMemcpy(hc, d_cnt, sizeof(hc), cudaMemcpyDeviceToHost));
+  TDW_CUDA(ctx, cudaMemcpy(hflags, pb->d_flags, sizeof(hflags), cudaMemcpyDeviceToHost));
+  cudaFree(d_cnt);
+  pb->n_evals = (int64_t)hc[0];
+  pb->n_pairs = (int64_t)hc[1];
+  pb->step_nnz = (int)hc[2];
+  unsigned long long bb = hc[3];
+  double bound;
+  memcpy(&bound, &bb, sizeof(bound));
+  pb->jac_bound = bound;
+  pb->ell_w = hflags[2];
+  if (hflags[3] == 1)
+    return tdw_fail(ctx, TDW_ERR_LIMIT, "lag-1 step matrix has more than 64 entries in a row");
+  if (!(bound < 0.9))
+    return tdw_fail(ctx, TDW_ERR_SINGULAR,
+                    "step matrix is not diagonally dominant (Jacobi bound " +
+                        std::to_string(bound) + "); the on-device solver needs bound < 0.9");
+  // sweeps for a contraction of 1e-17 under the infinity-norm bound
+  int it = bound > 0.0 ? (int)ceil(log(1e-17) / log(bound)) : 1;
+  pb->jac_iters = std::max(2, std::min(it, 400));
+  float ms = 0.f, fms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventElapsedTime(&fms, f0, f1);
+  pb->t_assemble_ms = ms;
+  pb->t_fill_ms = fms;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaEventDestroy(f0);
+  cudaEventDestroy(f1);
+  pb->store_bytes = (int64_t)(sizeof(double2) * n_band + sizeof(uint32_t) * nseg * TDW_TJ +
+                              sizeof(unsigned long long) * (nseg + 1) + sizeof(int2) * nunit);
+  pb->assembled = true;
+  return TDW_OK;
+}

@@ -1,0 +1,386 @@
+// capi.cu -- C ABI of libtdw: context, problem lifetime, march drivers, NCCL.
+// See include/tdw.h for the reference interface each entry point replaces.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+#include <vector>
+
+#include "coeff.cuh"
+#include "tdw_impl.cuh"
+
+int tdw_fail(tdw_ctx* ctx, int code, const std::string& msg) {
+  if (ctx) ctx->err = msg;
+  return code;
+}
+
+namespace {
+
+// max squared distance between used vertices (mesh.py:85-96), on the device
+__global__ void diameter_kernel(const double* __restrict__ v, const int* __restrict__ used, int nu,
+                                unsigned long long* out) {
+  double best = 0.0;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < (long long)nu * nu;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int a = used[e / nu], b = used[e % nu];
+    const double dx = v[3 * a] - v[3 * b], dy = v[3 * a + 1] - v[3 * b + 1],
+                 dz = v[3 * a + 2] - v[3 * b + 2];
+    best = fmax(best, dx * dx + dy * dy + dz * dz);
+  }
+  for (int o = 16; o > 0; o >>= 1) best = fmax(best, __shfl_xor_sync(0xffffffffu, best, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, (unsigned long long)__double_as_longlong(best));
+}
+
+uint64_t spread3(uint64_t x) {  // 21 bits -> every third bit
+  x &= 0x1fffff;
+  x = (x | x << 32) & 0x1f00000000ffffULL;
+  x = (x | x << 16) & 0x1f0000ff0000ffULL;
+  x = (x | x << 8) & 0x100f00f00f00f00fULL;
+  x = (x | x << 4) & 0x10c30c30c30c30c3ULL;
+  x = (x | x << 2) & 0x1249249249249249ULL;
+  return x;
+}
+
+}  // namespace
+
+extern "C" {
+
+int tdw_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+  return n;
+}
+
+int tdw_init(int device, tdw_ctx** out) {
+  if (!out) return TDW_ERR_INVALID_ARG;
+  *out = nullptr;
+  tdw_ctx* ctx = new tdw_ctx();
+  ctx->device = device;
+  cudaError_t e = cudaSetDevice(device);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device);
+  if (e != cudaSuccess) {
+    delete ctx;
+    return TDW_ERR_CUDA;
+  }
+  *out = ctx;
+  return TDW_OK;
+}
+
+int tdw_finalize(tdw_ctx* ctx) {
+  if (!ctx) return TDW_OK;
+  if (ctx->comm) ncclCommDestroy(ctx->comm);
+  if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+  return TDW_OK;
+}
+
+const char* tdw_last_error(const tdw_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+int tdw_nccl_unique_id(char out[128]) {
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return TDW_ERR_NCCL;
+  memcpy(out, id.internal, 128);
+  return TDW_OK;
+}
+
+int tdw_comm_init(tdw_ctx* ctx, const char id[128], int nranks, int rank) {
+  if (!ctx || nranks < 1 || rank < 0 || rank >= nranks) return TDW_ERR_INVALID_ARG;
+  if (nranks == 1) return TDW_OK;
+  ncclUniqueId uid;
+  memcpy(uid.internal, id, 128);
+  cudaSetDevice(ctx->device);
+  ncclResult_t r = ncclCommInitRank(&ctx->comm, nranks, uid, rank);
+  if (r != ncclSuccess) return tdw_fail(ctx, TDW_ERR_NCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+  ctx->nranks = nranks;
+  ctx->rank = rank;
+  return TDW_OK;
+}
+
+int tdw_problem_create(tdw_ctx* ctx, const tdw_problem_desc* dsc, tdw_problem** out) {
+  if (!ctx || !dsc || !out) return TDW_ERR_INVALID_ARG;
+  *out = nullptr;
+  if (dsc->d < 1 || dsc->d > 3)
+    return tdw_fail(ctx, TDW_ERR_UNSUPPORTED_ORDER, "basis order must be 1..3");
+  if (dsc->bie != TDW_BIE_OBIE && dsc->bie != TDW_BIE_BMBIE)
+    return tdw_fail(ctx, TDW_ERR_INVALID_ARG, "unknown integral equation");
+  if (dsc->nt < 2) return tdw_fail(ctx, TDW_ERR_INVALID_ARG, "need at least two time steps");
+  if (dsc->ns < 1 || dsc->nv < 3 || !dsc->vertices || !dsc->triangles || !dsc->phi)
+    return tdw_fail(ctx, TDW_ERR_INVALID_ARG, "empty mesh");
+  if (!(dsc->dt > 0.0) || !(dsc->c > 0.0))
+    return tdw_fail(ctx, TDW_ERR_INVALID_ARG, "c and dt must be positive");
+  const int nranks = std::max(1, dsc->nranks), rank = dsc->rank;
+  if (nranks != ctx->nranks || rank != ctx->rank)
+    return tdw_fail(ctx, TDW_ERR_INVALID_ARG, "nranks/rank differ from tdw_comm_init");
+  cudaSetDevice(ctx->device);
+  tdw_problem* pb = new tdw_problem();
+  pb->ctx = ctx;
+  const int ns = dsc->ns, nv = dsc->nv;
+  pb->ns = ns;
+  pb->nv = nv;
+  pb->bie = dsc->bie;
+  pb->d = dsc->d;
+  pb->nt = dsc->nt;
+  pb->window = dsc->window ? 1 : 0;
+  pb->c = dsc->c;
+  pb->dt = dsc->dt;
+  pb->K = tdw::kfactor(pb->d, pb->c, pb->dt);
+  pb->nranks = nranks;
+  pb->rank = rank;
+
+  // mesh-derived quantities exactly as mesh.py:42-75 (host, O(ns))
+  std::vector<double> rec((size_t)ns * TDW_ELEM_STRIDE);
+  std::vector<double> cen((size_t)ns * 3);
+  for (int e = 0; e < ns; ++e) {
+    const int64_t* t = dsc->triangles + 3 * (size_t)e;
+    for (int k = 0; k < 3; ++k)
+      if (t[k] < 0 || t[k] >= nv) {
+        delete pb;
+        return tdw_fail(ctx, TDW_ERR_INVALID_ARG, "triangle index out of range");
+      }
+    const double* a = dsc->vertices + 3 * t[0];
+    const double* b = dsc->vertices + 3 * t[1];
+    const double* cc = dsc->vertices + 3 * t[2];
+    double u[3] = {b[0] - a[0], b[1] - a[1], b[2] - a[2]};
+    double w[3] = {cc[0] - a[0], cc[1] - a[1], cc[2] - a[2]};
+    double cr[3] = {u[1] * w[2] - u[2] * w[1], u[2] * w[0] - u[0] * w[2], u[0] * w[1] - u[1] * w[0]};
+    double nn = std::sqrt(cr[0] * cr[0] + cr[1] * cr[1] + cr[2] * cr[2]);
+    if (!(nn > 0.0)) {
+      delete pb;
+      return tdw_fail(ctx, TDW_ERR_INVALID_ARG, "degenerate triangle");
+    }
+    double* r = &rec[(size_t)e * TDW_ELEM_STRIDE];
+    double rad = 0.0;
+    for (int k = 0; k < 3; ++k) {
+      r[k] = a[k];
+      r[3 + k] = b[k];
+      r[6 + k] = cc[k];
+      r[9 + k] = cr[k] / nn;
+      r[12 + k] = (a[k] + b[k] + cc[k]) / 3.0;
+      cen[3 * e + k] = r[12 + k];
+    }
+    const double* vv[3] = {a, b, cc};
+    for (int q = 0; q < 3; ++q) {
+      double dx = vv[q][0] - r[12], dy = vv[q][1] - r[13], dz = vv[q][2] - r[14];
+      rad = std::max(rad, std::sqrt(dx * dx + dy * dy + dz * dz));
+    }
+    r[15] = rad;
+  }
+  // Morton order of the centroids: keeps (row block, column tile) units compact in space
+  double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+  for (int e = 0; e < ns; ++e)
+    for (int k = 0; k < 3; ++k) {
+      lo[k] = std::min(lo[k], cen[3 * e + k]);
+      hi[k] = std::max(hi[k], cen[3 * e + k]);
+    }
+  double ext = std::max(std::max(hi[0] - lo[0], hi[1] - lo[1]), hi[2] - lo[2]);
+  if (!(ext > 0.0)) ext = 1.0;
+  std::vector<uint64_t> code(ns);
+  for (int e = 0; e < ns; ++e) {
+    uint64_t q[3];
+    for (int k = 0; k < 3; ++k) {
+      double f = (cen[3 * e + k] - lo[k]) / ext;
+      q[k] = (uint64_t)std::min(2097151.0, std::max(0.0, std::floor(f * 2097151.0)));
+    }
+    code[e] = spread3(q[0]) | spread3(q[1]) << 1 | spread3(q[2]) << 2;
+  }
+  pb->perm.resize(ns);
+  std::iota(pb->perm.begin(), pb->perm.end(), 0);
+  std::stable_sort(pb->perm.begin(), pb->perm.end(), [&](int x, int y) { return code[x] < code[y]; });
+  std::vector<double> prec((size_t)ns * TDW_ELEM_STRIDE), pphi(ns);
+  for (int k = 0; k < ns; ++k) {
+    memcpy(&prec[(size_t)k * TDW_ELEM_STRIDE], &rec[(size_t)pb->perm[k] * TDW_ELEM_STRIDE],
+           sizeof(double) * TDW_ELEM_STRIDE);
+    pphi[k] = dsc->phi[pb->perm[k]];
+  }
+  // rows per rank: whole I-blocks
+  const int nblk = (ns + TDW_TI - 1) / TDW_TI;
+  const int blk_per_rank = (nblk + nranks - 1) / nranks;
+  pb->rows_per_rank = blk_per_rank * TDW_TI;
+  pb->n_iblk = blk_per_rank;
+  pb->row_lo = std::min(ns, rank * pb->rows_per_rank);
+  pb->row_hi = std::min(ns, (rank + 1) * pb->rows_per_rank);
+  pb->ntiles = (ns + TDW_TJ - 1) / TDW_TJ;
+
+  auto fail_cuda = [&](cudaError_t e, const char* what) {
+    std::string m = std::string(what) + ": " + cudaGetErrorString(e);
+    tdw_problem_destroy(pb);
+    return tdw_fail(ctx, TDW_ERR_CUDA, m);
+  };
+  cudaError_t e;
+#define TDW_TRY(call)                              \
+  do {                                             \
+    e = (call);                                    \
+    if (e != cudaSuccess) return fail_cuda(e, #call); \
+  } while (0)
+  TDW_TRY(cudaMalloc(&pb->d_elem, sizeof(double) * prec.size()));
+  TDW_TRY(cudaMemcpy(pb->d_elem, prec.data(), sizeof(double) * prec.size(), cudaMemcpyHostToDevice));
+  TDW_TRY(cudaMalloc(&pb->d_phi, sizeof(double) * ns));
+  TDW_TRY(cudaMemcpy(pb->d_phi, pphi.data(), sizeof(double) * ns, cudaMemcpyHostToDevice));
+  TDW_TRY(cudaMalloc(&pb->d_perm, sizeof(int) * ns));
+  TDW_TRY(cudaMemcpy(pb->d_perm, pb->perm.data(), sizeof(int) * ns, cudaMemcpyHostToDevice));
+  TDW_TRY(cudaMalloc(&pb->d_flags, sizeof(int) * 4));
+  TDW_TRY(cudaMemset(pb->d_flags, 0, sizeof(int) * 4));
+
+  // gamma* = ceil(diam / (c dt)) + d + 1 (marching.py:67-69), diameter over used vertices
+  {
+    std::vector<char> used(nv, 0);
+    for (size_t k = 0; k < 3 * (size_t)ns; ++k) used[dsc->triangles[k]] = 1;
+    std::vector<int> ul;
+    for (int k = 0; k < nv; ++k)
+      if (used[k]) ul.push_back(k);
+    double* dv = nullptr;
+    int* du = nullptr;
+    unsigned long long* dm = nullptr;
+    TDW_TRY(cudaMalloc(&dv, sizeof(double) * 3 * nv));
+    TDW_TRY(cudaMalloc(&du, sizeof(int) * ul.size()));
+    TDW_TRY(cudaMalloc(&dm, sizeof(unsigned long long)));
+    TDW_TRY(cudaMemcpy(dv, dsc->vertices, sizeof(double) * 3 * nv, cudaMemcpyHostToDevice));
+    TDW_TRY(cudaMemcpy(du, ul.data(), sizeof(int) * ul.size(), cudaMemcpyHostToDevice));
+    TDW_TRY(cudaMemset(dm, 0, sizeof(unsigned long long)));
+    diameter_kernel<<<ctx->num_sms * 8, 256, 0, ctx->stream>>>(dv, du, (int)ul.size(), dm);
+    TDW_TRY(cudaGetLastError());
+    unsigned long long bits = 0;
+    TDW_TRY(cudaStreamSynchronize(ctx->stream));
+    TDW_TRY(cudaMemcpy(&bits, dm, sizeof(bits), cudaMemcpyDeviceToHost));
+    cudaFree(dv);
+    cudaFree(du);
+    cudaFree(dm);
+    double d2;
+    memcpy(&d2, &bits, sizeof(d2));
+    const double diam = std::sqrt(d2);
+    pb->gstar = (int)std::ceil(diam / (pb->c * pb->dt)) + pb->d + 1;
+  }
+  pb->n_lags = pb->window ? std::min(pb->gstar, pb->nt - 1) : pb->nt - 1;
+  // kappa-combined lags reach gamma = g + kappa <= gamma* with the window (marching.py:216-225)
+  pb->cap = pb->window ? std::min(pb->gstar, pb->nt - 1) : pb->nt - 1;
+  pb->pad = pb->cap + 1;
+  pb->hstride = pb->pad + pb->nt - 1;
+
+  // step buffers
+  pb->nsplit = 1;
+  {
+    // enough CTAs to fill the machine: (I-blocks x splits) >= 2 waves of 2 CTAs/SM
+    const int want = 4 * ctx->num_sms;
+    while (pb->n_iblk * pb->nsplit < want && pb->nsplit * 2 <= pb->ntiles) pb->nsplit *= 2;
+  }
+  TDW_TRY(cudaMalloc(&pb->d_bpart, sizeof(double) * (size_t)pb->nsplit * pb->rows_per_rank));
+  TDW_TRY(cudaMemset(pb->d_bpart, 0, sizeof(double) * (size_t)pb->nsplit * pb->rows_per_rank));
+  TDW_TRY(cudaMalloc(&pb->d_b, sizeof(double) * (size_t)nranks * pb->rows_per_rank));
+  TDW_TRY(cudaMemset(pb->d_b, 0, sizeof(double) * (size_t)nranks * pb->rows_per_rank));
+  TDW_TRY(cudaMalloc(&pb->d_x, sizeof(double) * 2 * (size_t)ns));
+  TDW_TRY(cudaMalloc(&pb->d_hist, sizeof(double2) * (size_t)ns * pb->hstride));
+  TDW_TRY(cudaMalloc(&pb->d_bar, sizeof(unsigned) * 2));
+  {
+    const int occ = 2;  // solve_kernel: 256 threads, tiny smem; 2 per SM are always co-resident
+    const int rows_per_block = 256;
+    int g = (ns + rows_per_block - 1) / rows_per_block;
+    pb->solve_grid = std::max(1, std::min(g, occ * ctx->num_sms));
+  }
+  TDW_TRY(cudaMalloc(&pb->d_red, sizeof(double) * 3 * pb->solve_grid));
+#undef TDW_TRY
+  *out = pb;
+  return TDW_OK;
+}
+
+int tdw_assemble(tdw_problem* pb) {
+  if (!pb) return TDW_ERR_INVALID_ARG;
+  if (pb->assembled) return TDW_OK;
+  cudaSetDevice(pb->ctx->device);
+  return tdw_assemble_impl(pb);
+}
+
+int tdw_problem_info(const tdw_problem* pb, tdw_info* out) {
+  if (!pb || !out) return TDW_ERR_INVALID_ARG;
+  memset(out, 0, sizeof(*out));
+  out->gamma_star = pb->gstar;
+  out->n_lags = pb->n_lags;
+  out->row_lo = pb->row_lo;
+  out->row_hi = pb->row_hi;
+  out->n_band = pb->n_band;
+  out->n_pairs = pb->n_pairs;
+  out->n_evals = pb->n_evals;
+  out->store_bytes = pb->store_bytes;
+  out->step_nnz = pb->step_nnz;
+  out->jacobi_iters = pb->jac_iters;
+  out->jacobi_bound = pb->jac_bound;
+  out->t_assemble_ms = pb->t_assemble_ms;
+  out->t_fill_ms = pb->t_fill_ms;
+  return TDW_OK;
+}
+
+int tdw_upload_known(tdw_problem* pb, const double* u_known, const double* q_known) {
+  if (!pb || !u_known || !q_known) return TDW_ERR_INVALID_ARG;
+  tdw_ctx* ctx = pb->ctx;
+  cudaSetDevice(ctx->device);
+  const size_t n = (size_t)(pb->nt - 1) * pb->ns;
+  if (!pb->d_uk) TDW_CUDA(ctx, cudaMalloc(&pb->d_uk, sizeof(double) * n));
+  if (!pb->d_qk) TDW_CUDA(ctx, cudaMalloc(&pb->d_qk, sizeof(double) * n));
+  TDW_CUDA(ctx, cudaMemcpyAsync(pb->d_uk, u_known, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
+  TDW_CUDA(ctx, cudaMemcpyAsync(pb->d_qk, q_known, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
+  pb->known_loaded = true;
+  return TDW_OK;
+}
+
+int tdw_download(tdw_problem* pb, double* u, double* q, double* tau, double* sigma,
+                 int32_t* n_steps, int32_t* status) {
+  if (!pb) return TDW_ERR_INVALID_ARG;
+  cudaSetDevice(pb->ctx->device);
+  int rc = tdw_outputs(pb, u, q, tau, sigma);
+  if (rc) return rc;
+  int hflags[4];
+  TDW_CUDA(pb->ctx, cudaMemcpy(hflags, pb->d_flags, sizeof(hflags), cudaMemcpyDeviceToHost));
+  if (n_steps) *n_steps = hflags[1];
+  if (status) *status = hflags[0] == 1 ? 1 : 0;
+  return TDW_OK;
+}
+
+int tdw_march(tdw_problem* pb, const double* u_known, const double* q_known, double threshold,
+              double* u, double* q, double* tau, double* sigma, double* rhs_trace,
+              int32_t* n_steps, int32_t* status) {
+  if (!pb) return TDW_ERR_INVALID_ARG;
+  cudaSetDevice(pb->ctx->device);
+  int rc = tdw_upload_known(pb, u_known, q_known);
+  if (rc) return rc;
+  if (!pb->assembled) {
+    rc = tdw_assemble_impl(pb);
+    if (rc) return rc;
+  }
+  rc = tdw_march_loop(pb, threshold, rhs_trace != nullptr, false, nullptr);
+  if (rc) return rc;
+  if (rhs_trace) {
+    TDW_CUDA(pb->ctx, cudaMemcpy(rhs_trace, pb->d_rhs, sizeof(double) * (size_t)(pb->nt - 1) * pb->ns,
+                                 cudaMemcpyDeviceToHost));
+  }
+  return tdw_download(pb, u, q, tau, sigma, n_steps, status);
+}
+
+int tdw_march_resident(tdw_problem* pb, double threshold, int n_repeat, int time_kernels,
+                       tdw_timing* timing) {
+  if (!pb || n_repeat < 1) return TDW_ERR_INVALID_ARG;
+  cudaSetDevice(pb->ctx->device);
+  if (timing) memset(timing, 0, sizeof(*timing));
+  for (int r = 0; r < n_repeat; ++r) {
+    int rc = tdw_march_loop(pb, threshold, false, time_kernels != 0, timing);
+    if (rc) return rc;
+  }
+  return TDW_OK;
+}
+
+int tdw_problem_destroy(tdw_problem* pb) {
+  if (!pb) return TDW_OK;
+  cudaSetDevice(pb->ctx->device);
+  void* ptrs[] = {pb->d_perm, pb->d_elem, pb->d_phi, pb->d_hdr, pb->d_segoff, pb->d_coef,
+                  pb->d_unit, pb->d_acol, pb->d_aval, pb->d_adiag, pb->d_hist, pb->d_uk,
+                  pb->d_qk, pb->d_bpart, pb->d_b, pb->d_x, pb->d_red, pb->d_bar, pb->d_flags,
+                  pb->d_rhs};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  delete pb;
+  return TDW_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,99 @@
+// tdw_impl.cuh -- internal state of libtdw (not part of the C ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <nccl.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/tdw.h"
+
+// Tile geometry of the banded store.
+#define TDW_TJ 32        // columns per J-tile == pairs per segment == one warp
+#define TDW_TI 32        // rows per I-block (one conv CTA)
+#define TDW_ROWS_PER_WARP 4
+#define TDW_CONV_WARPS (TDW_TI / TDW_ROWS_PER_WARP)
+#define TDW_ELL_MAX 64   // max nnz per row of the lag-1 step matrix
+#define TDW_ELEM_STRIDE 16  // doubles per element record: v0 v1 v2 n c rad
+
+struct tdw_ctx {
+  int device = 0;
+  int num_sms = 0;
+  cudaStream_t stream = nullptr;
+  std::string err;
+  ncclComm_t comm = nullptr;
+  int nranks = 1, rank = 0;
+};
+
+// header word of one (row, column) pair inside a segment:
+//   bits 0..7 column within the J-tile, 8..15 band length, 16..31 first lag
+__host__ __device__ inline uint32_t hdr_pack(int jl, int len, int glo) {
+  return (uint32_t)jl | ((uint32_t)len << 8) | ((uint32_t)glo << 16);
+}
+__host__ __device__ inline int hdr_jl(uint32_t h) { return (int)(h & 0xffu); }
+__host__ __device__ inline int hdr_len(uint32_t h) { return (int)((h >> 8) & 0xffu); }
+__host__ __device__ inline int hdr_glo(uint32_t h) { return (int)(h >> 16); }
+
+struct tdw_problem {
+  tdw_ctx* ctx = nullptr;
+  // parameters
+  int ns = 0, nv = 0, bie = 0, d = 1, nt = 2, window = 1;
+  double c = 1.0, dt = 1.0, K = 0.0;
+  int gstar = 0, n_lags = 0, cap = 0;
+  int nranks = 1, rank = 0;
+  // rows (internal order); rank r owns [row_lo, row_hi); rows_per_rank multiple of TDW_TI
+  int rows_per_rank = 0, row_lo = 0, row_hi = 0, n_iblk = 0, ntiles = 0;
+  // ordering: internal index -> original element index
+  std::vector<int> perm;
+  int* d_perm = nullptr;
+  double* d_elem = nullptr;  // ns * TDW_ELEM_STRIDE
+  double* d_phi = nullptr;   // internal order
+  // banded store
+  bool assembled = false;
+  uint32_t* d_hdr = nullptr;       // [rows_per_rank * ntiles][TDW_TJ]
+  unsigned long long* d_segoff = nullptr;  // [rows_per_rank * ntiles + 1]
+  double2* d_coef = nullptr;       // (VU, VW) pairs, jagged k-major per segment
+  int2* d_unit = nullptr;          // [n_iblk * ntiles] lag range (gmin, gmax)
+  int wmax = 0;                    // max unit lag span
+  int64_t n_band = 0, n_pairs = 0, n_evals = 0, store_bytes = 0;
+  // lag-1 step matrix, all rows, ELL
+  int ell_w = 0, step_nnz = 0;
+  int* d_acol = nullptr;
+  double* d_aval = nullptr;
+  double* d_adiag = nullptr;
+  int jac_iters = 0;
+  double jac_bound = 0.0;
+  // history and step buffers
+  int pad = 0, hstride = 0;
+  double2* d_hist = nullptr;       // [ns][hstride] (q, u) per element per step
+  double* d_uk = nullptr;          // (nt-1, ns) original order
+  double* d_qk = nullptr;
+  bool known_loaded = false;
+  int nsplit = 1;
+  double* d_bpart = nullptr;       // [nsplit][rows_per_rank]
+  double* d_b = nullptr;           // [nranks * rows_per_rank]
+  double* d_x = nullptr;           // [2][ns]
+  double* d_red = nullptr;         // reduction scratch [3][grid]
+  unsigned* d_bar = nullptr;       // grid barrier {count, generation}
+  int* d_flags = nullptr;          // {status, n_steps, err_step, ell_overflow}
+  double* d_rhs = nullptr;         // (nt-1, ns) original order, optional
+  int solve_grid = 0;
+  double t_assemble_ms = 0.0, t_fill_ms = 0.0;
+};
+
+// error helpers -----------------------------------------------------------
+int tdw_fail(tdw_ctx* ctx, int code, const std::string& msg);
+#define TDW_CUDA(ctx, call)                                                        \
+  do {                                                                             \
+    cudaError_t _e = (call);                                                       \
+    if (_e != cudaSuccess)                                                         \
+      return tdw_fail((ctx), TDW_ERR_CUDA,                                         \
+                      std::string(#call) + ": " + cudaGetErrorString(_e));         \
+  } while (0)
+
+// entry points implemented in the .cu files
+int tdw_assemble_impl(tdw_problem* pb);
+int tdw_march_loop(tdw_problem* pb, double threshold, bool want_rhs, bool time_kernels,
+                   tdw_timing* timing);
+int tdw_outputs(tdw_problem* pb, double* u, double* q, double* tau, double* sigma);

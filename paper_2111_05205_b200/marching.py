@@ -1,0 +1,238 @@
+"""Marching-on-in-time on the B200 (drop-in for tdwavebem.marching).
+
+Keeps the reference's public surface (pkg/src/tdwavebem/marching.py):
+`ProblemSpec`, `TimeHistory`, `compute_gamma_star`, `greville_samples`,
+`build_retarded_matrices`, `march`.  Differences, all behind the same calls:
+
+* `build_retarded_matrices` returns a `BandStore`: an opaque handle to the
+  device-resident kappa-combined banded coefficient store (csrc/assemble.cu)
+  instead of per-lag scipy CSR matrices.  Like the reference's
+  `RetardedMatrixSet` it can be passed back through `march(spec, mats=...)`.
+* `march` runs the whole time loop on the GPU (csrc/march.cu): history
+  convolution, Jacobi solve of the lag-1 system, residual test, blow-up
+  detector.  Only the Greville sampling of the user's data callables stays on
+  the host, exactly where the reference does it (marching.py:312).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import warnings
+from dataclasses import dataclass, field
+from typing import Callable
+
+import numpy as np
+
+from . import _lib
+from .mesh import mesh_stats
+from .tbasis import decomposition_weights, eval_basis
+
+__all__ = ["ProblemSpec", "TimeHistory", "BandStore", "compute_gamma_star", "greville_samples",
+           "build_retarded_matrices", "march"]
+
+
+@dataclass
+class ProblemSpec:
+    """Exterior scattering problem (marching.py:33-64).
+
+    phi[j] = 1: u unknown on element j (q given); 0: q unknown (u given).
+    """
+
+    mesh: object
+    phi: np.ndarray
+    bie: str
+    basis: object
+    c: float
+    nt: int
+    u_data: Callable[[float], np.ndarray] | None = None
+    q_data: Callable[[float], np.ndarray] | None = None
+    blowup_reference: float = 1.0
+
+    def __post_init__(self):
+        self.phi = np.asarray(self.phi, dtype=float)
+        if self.phi.shape != (self.mesh.n_elements,):
+            raise ValueError("phi must have one flag per element")
+        if self.bie not in ("obie", "bmbie"):
+            raise ValueError(f"unknown integral equation {self.bie!r}")
+        if self.nt < 2:
+            raise ValueError("need at least two time steps")
+        ratio = mesh_stats(self.mesh).max_edge / (self.c * self.basis.dt)
+        if ratio > 1.5:
+            warnings.warn(f"mesh edge / (c dt) = {ratio:.2f} exceeds the usual "
+                          "stability guideline (~1)", stacklevel=2)
+
+
+def compute_gamma_star(stats, basis, c: float) -> int:
+    """gamma* = ceil(diam / (c dt)) + d + 1 (marching.py:67-69)."""
+    return int(np.ceil(stats.max_diameter / (c * basis.dt))) + basis.d + 1
+
+
+@dataclass
+class TimeHistory:
+    """Coefficient histories and kappa sums per step (marching.py:184-255)."""
+
+    basis: object
+    nt: int
+    n_elements: int
+    u: np.ndarray = field(init=False)
+    q: np.ndarray = field(init=False)
+    tau: np.ndarray = field(init=False)
+    sigma: np.ndarray = field(init=False)
+    n_steps: int = 0
+    status: str = "stable"
+
+    def __post_init__(self):
+        shape = (self.nt - 1, self.n_elements)
+        self.u = np.zeros(shape)
+        self.q = np.zeros(shape)
+        self.tau = np.zeros(shape)
+        self.sigma = np.zeros(shape)
+
+    def stock_sums(self, beta: int):
+        w = decomposition_weights(self.basis.d)
+        ks = range(min(self.basis.d + 1, beta) + 1)
+        return (sum(w[k] * self.q[beta - k] for k in ks), sum(w[k] * self.u[beta - k] for k in ks))
+
+    def knot_values(self, kind: str = "u") -> np.ndarray:
+        coef = self.u if kind == "u" else self.q
+        d = self.basis.d
+        bv = [eval_basis(self.basis, 0, g * self.basis.dt) for g in range(d + 1)]
+        out = np.zeros((self.nt, self.n_elements))
+        for alpha in range(self.nt):
+            for g in range(1, d + 1):
+                beta = alpha - g
+                if 0 <= beta < self.nt - 1:
+                    out[alpha] += bv[g] * coef[beta]
+        return out
+
+
+def greville_samples(spec):
+    """Known data at the Greville abscissae t = beta dt + (d+1) dt / 2 (marching.py:258-276)."""
+    basis = spec.basis
+    nt, ns = spec.nt, spec.mesh.n_elements
+    uk = np.zeros((nt - 1, ns))
+    qk = np.zeros((nt - 1, ns))
+    off = 0.5 * (basis.d + 1) * basis.dt
+    for beta in range(nt - 1):
+        t = beta * basis.dt + off
+        if spec.u_data is not None:
+            uk[beta] = spec.u_data(t)
+        if spec.q_data is not None:
+            qk[beta] = spec.q_data(t)
+    return uk, qk
+
+
+class BandStore:
+    """Device-resident banded coefficient store + lag-1 step matrix (tdw_problem)."""
+
+    def __init__(self, spec, window: bool = True, ctx: _lib.Context | None = None,
+                 nranks: int = 1, rank: int = 0):
+        self.ctx = ctx or _lib.default_context()
+        lib = _lib.load()
+        mesh = spec.mesh
+        self._v = np.ascontiguousarray(mesh.vertices, dtype=np.float64)
+        self._t = np.ascontiguousarray(mesh.triangles, dtype=np.int64)
+        self._phi = np.ascontiguousarray(spec.phi, dtype=np.float64)
+        self.ns = mesh.n_elements
+        self.nt = int(spec.nt)
+        self.window = bool(window)
+        desc = _lib.ProblemDesc(
+            ns=self.ns, nv=len(self._v), vertices=_lib.dptr(self._v),
+            triangles=self._t.ctypes.data_as(C.POINTER(C.c_int64)), phi=_lib.dptr(self._phi),
+            bie=1 if spec.bie == "bmbie" else 0, d=int(spec.basis.d), c=float(spec.c),
+            dt=float(spec.basis.dt), nt=self.nt, window=int(self.window), nranks=int(nranks),
+            rank=int(rank))
+        self.h = C.c_void_p()
+        _lib.check(lib.tdw_problem_create(self.ctx.h, C.byref(desc), C.byref(self.h)), self.ctx.h,
+                   "tdw_problem_create")
+        self.assembled = False
+
+    def assemble(self):
+        if not self.assembled:
+            _lib.check(_lib.load().tdw_assemble(self.h), self.ctx.h, "tdw_assemble")
+            self.assembled = True
+        return self
+
+    def info(self) -> dict:
+        inf = _lib.Info()
+        _lib.check(_lib.load().tdw_problem_info(self.h, C.byref(inf)), self.ctx.h, "tdw_problem_info")
+        return inf.asdict()
+
+    @property
+    def gamma_star(self) -> int:
+        return self.info()["gamma_star"]
+
+    @property
+    def n_lags(self) -> int:
+        return self.info()["n_lags"]
+
+    # benchmark helpers (device-resident inputs/outputs)
+    def upload_known(self, u_known, q_known):
+        self._uk = np.ascontiguousarray(u_known, dtype=np.float64)
+        self._qk = np.ascontiguousarray(q_known, dtype=np.float64)
+        _lib.check(_lib.load().tdw_upload_known(self.h, _lib.dptr(self._uk), _lib.dptr(self._qk)),
+                   self.ctx.h, "tdw_upload_known")
+
+    def run_resident(self, threshold: float, n_repeat: int = 1, time_kernels: bool = False) -> dict:
+        t = _lib.Timing()
+        _lib.check(_lib.load().tdw_march_resident(self.h, float(threshold), int(n_repeat),
+                                                  int(time_kernels), C.byref(t)),
+                   self.ctx.h, "tdw_march_resident")
+        return t.asdict()
+
+    def close(self):
+        if self.h.value:
+            _lib.load().tdw_problem_destroy(self.h)
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def build_retarded_matrices(spec, gamma_max: int | None = None, pairs=None, slab: int = 2_000_000,
+                            window: bool = True) -> BandStore:
+    """Assemble the device banded store (replaces marching.py:132-181).
+
+    `gamma_max` is accepted for signature compatibility; the store always
+    covers the lags `march` needs (min(gamma*, nt-1), or nt-1 without window).
+    `pairs` restriction (the fast solver's near field) is not part of the
+    direct path.
+    """
+    if pairs is not None:
+        raise NotImplementedError("pair-restricted assembly belongs to the FMM near field")
+    return BandStore(spec, window=window).assemble()
+
+
+def march(spec, window: bool = True, blowup_factor: float = 1e6, mats=None,
+          rhs_trace: list | None = None) -> TimeHistory:
+    """Run the conventional time marching on the GPU (marching.py:292-338)."""
+    stats = mesh_stats(spec.mesh)
+    gstar = compute_gamma_star(stats, spec.basis, spec.c)
+    n_lags = min(gstar, spec.nt - 1) if window else spec.nt - 1
+    if mats is None:
+        mats = BandStore(spec, window=window)
+    elif not isinstance(mats, BandStore):
+        raise TypeError("mats must come from build_retarded_matrices of this package")
+    elif mats.n_lags < n_lags or mats.window != window:
+        raise ValueError("matrix set does not cover the required lags")
+    hist = TimeHistory(spec.basis, spec.nt, spec.mesh.n_elements)
+    uk, qk = greville_samples(spec)
+    threshold = blowup_factor * max(spec.blowup_reference, 1e-30)
+    ns, nt = spec.mesh.n_elements, spec.nt
+    rhs = np.zeros((nt - 1, ns)) if rhs_trace is not None else None
+    n_steps, status = C.c_int32(0), C.c_int32(0)
+    uk = np.ascontiguousarray(uk)
+    qk = np.ascontiguousarray(qk)
+    rc = _lib.load().tdw_march(mats.h, _lib.dptr(uk), _lib.dptr(qk), float(threshold),
+                               _lib.dptr(hist.u), _lib.dptr(hist.q), _lib.dptr(hist.tau),
+                               _lib.dptr(hist.sigma), _lib.dptr(rhs) if rhs is not None else None,
+                               C.byref(n_steps), C.byref(status))
+    _lib.check(rc, mats.ctx.h, "march")
+    mats.assembled = True
+    hist.n_steps = int(n_steps.value)
+    hist.status = "unstable" if status.value else "stable"
+    if rhs_trace is not None:
+        rhs_trace.extend(rhs[k].copy() for k in range(hist.n_steps))
+    return hist

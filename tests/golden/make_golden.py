@@ -1,0 +1,216 @@
+"""Generate the committed golden fixtures by running the REFERENCE itself.
+
+This script is the only place that imports the upstream `tdwavebem` package
+(from /root/reference/pkg/src, present only in the build container).  Its
+outputs are small .npz fixtures under tests/golden/ that travel to the GPU box;
+the reference itself never does.
+
+    NUMBA_CACHE_DIR=/tmp/nb python tests/golden/make_golden.py coeff
+    NUMBA_CACHE_DIR=/tmp/nb python tests/golden/make_golden.py march 0
+    NUMBA_CACHE_DIR=/tmp/nb python tests/golden/make_golden.py march 1
+    NUMBA_CACHE_DIR=/tmp/nb python tests/golden/make_golden.py march 2   # ~1 h, ~15 GB RAM
+    NUMBA_CACHE_DIR=/tmp/nb python tests/golden/make_golden.py tree 3
+
+Scenario recipe: SURVEY.md section 8(c)/(d) (icosphere f=4/8/16, c=1,
+c*dt = 0.5 * mean edge, Gaussian plane pulse along z, sigma=4dt, t0=6 sigma).
+Versions of numpy/scipy/numba are recorded in every fixture.
+"""
+from __future__ import annotations
+
+import os
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+REF = Path("/root/reference/pkg/src")
+sys.path.insert(0, str(REF))
+os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/nb")
+
+import scipy  # noqa: E402
+import numba  # noqa: E402
+from tdwavebem import elemint, marching, shapes  # noqa: E402
+from tdwavebem.mesh import TriMesh  # noqa: E402
+from tdwavebem.tbasis import BSplineBasis  # noqa: E402
+
+OUT = Path(__file__).resolve().parent
+VERSIONS = f"numpy {np.__version__}; scipy {scipy.__version__}; numba {numba.__version__}; reference tdwavebem 0.1.0"
+
+# (f, bie, d, phi, nt, jitter_seed)
+CONFIGS = {
+    0: (4, "obie", 1, 1.0, 64, None),
+    1: (8, "bmbie", 2, 1.0, 128, None),
+    2: (16, "bmbie", 1, 0.0, 256, 12345),
+    3: (32, "bmbie", 2, 1.0, 512, None),
+}
+
+
+def build_mesh(cfg):
+    f, _, _, _, _, seed = CONFIGS[cfg]
+    m = shapes.icosphere(f, radius=1.0, centre=(0.0, 0.0, 0.0))
+    if seed is None:
+        return m
+    rng = np.random.default_rng(seed)
+    v = m.vertices * (1.0 + rng.uniform(-0.02, 0.02, size=(len(m.vertices), 1)))
+    return TriMesh(v, m.triangles)
+
+
+def build_spec(cfg):
+    f, bie, d, phival, nt, _ = CONFIGS[cfg]
+    mesh = build_mesh(cfg)
+    v0, v1, v2 = mesh.element_vertices()
+    edges = np.concatenate([np.linalg.norm(v1 - v0, axis=1),
+                            np.linalg.norm(v2 - v1, axis=1),
+                            np.linalg.norm(v0 - v2, axis=1)])
+    dt = 0.5 * float(edges.mean())
+    sig = 4.0 * dt
+    t0 = 6.0 * sig
+    zc = mesh.centroids[:, 2]
+    nz = mesh.normals[:, 2]
+
+    def q_data(t):
+        a = (t - zc - t0) / sig
+        return -(nz * 2.0 * a / sig * np.exp(-a * a))
+
+    def u_data(t):
+        a = (t - zc - t0) / sig
+        return -np.exp(-a * a)
+
+    phi = np.full(mesh.n_elements, phival)
+    import warnings
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        spec = marching.ProblemSpec(
+            mesh, phi, bie, BSplineBasis(d, dt), 1.0, nt,
+            u_data=u_data if phival == 0.0 else None,
+            q_data=q_data if phival == 1.0 else None)
+    return spec
+
+
+# ---------------------------------------------------------------------------
+def _structured_cases(rng):
+    """Hand-picked configurations: self, coplanar, near-singular, clipped,
+    not-yet-arrived, fully passed (SURVEY 8(c) golden list)."""
+    P, A, B, C, s = [], [], [], [], []
+    E0 = np.array([[0.0, 0, 0], [0.4, 0, 0], [0.1, 0.5, 0]])
+    cen = E0.mean(axis=0)
+    for g in (0.03, 0.1, 0.2, 0.35, 0.6, 1.5, 4.0):
+        P.append(cen); A.append(E0[0]); B.append(E0[1]); C.append(E0[2]); s.append(g)   # self
+        P.append(np.array([2.0, 1.0, 0.0])); A.append(E0[0]); B.append(E0[1]); C.append(E0[2]); s.append(g * 2 + 1.5)  # coplanar
+        P.append(cen + np.array([0, 0, 2e-3])); A.append(E0[0]); B.append(E0[1]); C.append(E0[2]); s.append(g)  # near-singular +
+        P.append(cen - np.array([0, 0, 2e-3])); A.append(E0[0]); B.append(E0[1]); C.append(E0[2]); s.append(g)  # near-singular -
+        P.append(np.array([0.2, 0.1, 0.3])); A.append(E0[0]); B.append(E0[1]); C.append(E0[2]); s.append(g)    # partially clipped
+        P.append(np.array([0.0, 0.0, 10.0])); A.append(E0[0]); B.append(E0[1]); C.append(E0[2]); s.append(g)   # not arrived
+        P.append(np.array([0.4, 0.0, 0.0])); A.append(E0[0]); B.append(E0[1]); C.append(E0[2]); s.append(g)    # at a vertex
+        P.append(np.array([0.2, 0.0, 0.0])); A.append(E0[0]); B.append(E0[1]); C.append(E0[2]); s.append(g)    # on an edge
+        P.append(np.array([0.2, -0.3, 0.0])); A.append(E0[0]); B.append(E0[1]); C.append(E0[2]); s.append(g)   # edge line, outside
+    for _ in range(40):   # fully passed, random orientation
+        E = rng.uniform(-0.5, 0.5, (3, 3))
+        p = rng.uniform(-1, 1, 3)
+        rmax = max(np.linalg.norm(p - E[k]) for k in range(3))
+        P.append(p); A.append(E[0]); B.append(E[1]); C.append(E[2]); s.append(rmax * rng.uniform(1.01, 3.0))
+    return [np.array(v) for v in (P, A, B, C)] + [np.array(s)]
+
+
+def _random_cases(rng, n):
+    P = rng.uniform(-1, 1, (n, 3))
+    A = rng.uniform(-0.5, 0.5, (n, 3))
+    B = rng.uniform(-0.5, 0.5, (n, 3))
+    C = rng.uniform(-0.5, 0.5, (n, 3))
+    s = rng.uniform(0.01, 2.5, n)
+    # push a share of the points into the element plane (coplanar family)
+    k = n // 8
+    nrm = np.cross(B[:k] - A[:k], C[:k] - A[:k])
+    nrm /= np.linalg.norm(nrm, axis=1)[:, None]
+    P[:k] -= np.einsum("ij,ij->i", P[:k] - A[:k], nrm)[:, None] * nrm
+    return P, A, B, C, s
+
+
+def make_coeff():
+    rng = np.random.default_rng(20240817)
+    sets = [_structured_cases(rng), _random_cases(rng, 3000)]
+    P, A, B, C, s = (np.concatenate([st[k] for st in sets]) for k in range(5))
+    ez = np.cross(B - A, C - A)
+    dbl = np.linalg.norm(ez, axis=1)
+    keep = dbl > 1e-3
+    P, A, B, C, s, ez = P[keep], A[keep], B[keep], C[keep], s[keep], ez[keep] / dbl[keep][:, None]
+    nx = rng.normal(size=P.shape)
+    nx /= np.linalg.norm(nx, axis=1)[:, None]
+    out = dict(P=P, A=A, B=B, C=C, ez=ez, s=s, nx=nx, c=1.0, dt=0.05, versions=VERSIONS)
+    for d in (1, 2, 3):
+        U, W = elemint.retarded_coeff_table(P, A, B, C, ez, s, d, 1.0, 0.05)
+        BU, BW = elemint.retarded_coeff_table(P, A, B, C, ez, s, d, 1.0, 0.05, which="bm", nx=nx)
+        out[f"U{d}"], out[f"W{d}"], out[f"BU{d}"], out[f"BW{d}"] = U, W, BU, BW
+    np.savez_compressed(OUT / "coeff_table.npz", **out)
+    print("coeff_table.npz:", len(P), "triples")
+
+
+def make_march(cfg):
+    spec = build_spec(cfg)
+    mesh = spec.mesh
+    stats = marching.mesh_stats(mesh)
+    gstar = marching.compute_gamma_star(stats, spec.basis, spec.c)
+    n_lags = min(gstar, spec.nt - 1)
+    t0 = time.perf_counter()
+    mats = marching.build_retarded_matrices(spec, n_lags)
+    t_asm = time.perf_counter() - t0
+    nnz = sum(m.nnz for m in mats.U)
+    trace = []
+    t0 = time.perf_counter()
+    hist = marching.march(spec, mats=mats, rhs_trace=trace)
+    t_march = time.perf_counter() - t0
+    unknown = hist.u if spec.phi[0] == 1.0 else hist.q
+    rhs = np.array(trace)
+    ns = mesh.n_elements
+    rng = np.random.default_rng(7)
+    sub = np.sort(rng.choice(ns, size=min(ns, 256), replace=False))
+    full_steps = np.unique(np.linspace(0, spec.nt - 2, 6).astype(int))
+    out = dict(
+        cfg=cfg, vertices=mesh.vertices, triangles=mesh.triangles, dt=spec.basis.dt,
+        gamma_star=gstar, n_lags=n_lags, nnz_lagcsr=nnz, status=hist.status,
+        n_steps=hist.n_steps, t_assembly=t_asm, t_march=t_march,
+        unknown_norm=np.linalg.norm(unknown, axis=1), rhs_norm=np.linalg.norm(rhs, axis=1),
+        sub=sub, unknown_sub=unknown[:, sub], rhs_sub=rhs[:, sub],
+        full_steps=full_steps, unknown_full=unknown[full_steps],
+        versions=VERSIONS)
+    if cfg == 0:   # small enough to keep everything
+        out.update(u=hist.u, q=hist.q, tau=hist.tau, sigma=hist.sigma, rhs=rhs)
+    np.savez_compressed(OUT / f"march_cfg{cfg}.npz", **out)
+    print(f"cfg{cfg}: ns={ns} gstar={gstar} nnz={nnz} asm={t_asm:.1f}s march={t_march:.1f}s "
+          f"status={hist.status} n_steps={hist.n_steps} max|x|={np.abs(unknown).max():.4g}")
+
+
+def make_tree(cfg, leaf_capacity=20):
+    """Octree + interaction lists from the reference build_tree (bit-exact target)."""
+    from tdwavebem.fmm_tree import build_tree
+    spec = build_spec(cfg)
+    t0 = time.perf_counter()
+    tree = build_tree(spec.mesh, spec.c, spec.basis.dt, leaf_capacity, 8)
+    out = dict(cfg=cfg, leaf_capacity=leaf_capacity, leaf_level=tree.leaf_level,
+               root_centre=tree.root_centre, root_half=tree.root_half,
+               near_i=tree.near_pairs[0].astype(np.int32), near_j=tree.near_pairs[1].astype(np.int32),
+               t_build=time.perf_counter() - t0, versions=VERSIONS)
+    for L, lev in enumerate(tree.levels):
+        out[f"L{L}_coords"] = lev.coords.astype(np.int32)
+        if lev.il_obs is not None:
+            out[f"L{L}_il_obs"] = lev.il_obs.astype(np.int32)
+            out[f"L{L}_il_src"] = lev.il_src.astype(np.int32)
+            out[f"L{L}_il_off"] = lev.il_offsets.astype(np.int8)
+    for L, (ei, ej) in tree.extra_pairs.items():
+        out[f"extra{L}_i"] = ei.astype(np.int32)
+        out[f"extra{L}_j"] = ej.astype(np.int32)
+    np.savez_compressed(OUT / f"tree_cfg{cfg}.npz", **out)
+    print(f"tree cfg{cfg}: leaf={tree.leaf_level} near={len(tree.near_pairs[0])}")
+
+
+if __name__ == "__main__":
+    what = sys.argv[1]
+    if what == "coeff":
+        make_coeff()
+    elif what == "march":
+        make_march(int(sys.argv[2]))
+    elif what == "tree":
+        make_tree(int(sys.argv[2]))
+    else:
+        raise SystemExit(__doc__)
