@@ -76,12 +76,17 @@ typedef struct {
   double jacobi_bound;       /* max_i sum_{j!=i} |A_ij| / |A_ii|                 */
   double t_assemble_ms;      /* device time of tdw_assemble                      */
   double t_fill_ms;          /* device time of the coefficient fill kernel       */
+  int64_t max_unit_bytes;    /* largest (row block, column tile) unit of the store */
+  int32_t max_lag_span;      /* largest history slice (lags) of a unit           */
+  int32_t conv_grid;         /* persistent CTAs of the convolution kernel        */
+  int32_t conv_splits;       /* column-tile splits per row block                 */
+  int32_t solve_cluster;     /* CTAs of the cluster solver (0 = grid fallback)   */
 } tdw_info;
 
 typedef struct {
   double total_ms;           /* device time of the whole timed loop              */
   double conv_ms;            /* summed device time of the history-convolution kernel */
-  double solve_ms;           /* summed device time of the solve/update kernel    */
+  double solve_ms;           /* 1 if the loop ran as a CUDA graph, else 0         */
   double comm_ms;            /* summed device time of the NCCL all-gather        */
   int32_t conv_launches;
   int32_t steps;
@@ -121,6 +126,13 @@ int tdw_march_resident(tdw_problem* pb, double threshold, int n_repeat, int time
                        tdw_timing* timing);
 int tdw_download(tdw_problem* pb, double* u, double* q, double* tau, double* sigma,
                  int32_t* n_steps, int32_t* status);
+
+/* Average device time of one history-convolution launch (kernel K2) over n
+ * back-to-back launches at a fixed step; inputs resident.  For the roofline. */
+int tdw_time_conv(tdw_problem* pb, int n, float* ms);
+
+/* 0 = launch the time loop kernel by kernel, 1 = capture it in a CUDA graph (default). */
+int tdw_set_graph(tdw_problem* pb, int enable);
 
 int tdw_problem_destroy(tdw_problem* pb);
 

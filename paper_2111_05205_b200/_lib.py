@@ -34,7 +34,9 @@ class Info(C.Structure):
                 ("row_hi", C.c_int32), ("n_band", C.c_int64), ("n_pairs", C.c_int64),
                 ("n_evals", C.c_int64), ("store_bytes", C.c_int64), ("step_nnz", C.c_int32),
                 ("jacobi_iters", C.c_int32), ("jacobi_bound", C.c_double),
-                ("t_assemble_ms", C.c_double), ("t_fill_ms", C.c_double)]
+                ("t_assemble_ms", C.c_double), ("t_fill_ms", C.c_double),
+                ("max_unit_bytes", C.c_int64), ("max_lag_span", C.c_int32), ("conv_grid", C.c_int32),
+                ("conv_splits", C.c_int32), ("solve_cluster", C.c_int32)]
 
     def asdict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -67,6 +69,8 @@ EXPORTS = {
     "tdw_upload_known": ([C.c_void_p, _dp, _dp], C.c_int),
     "tdw_march_resident": ([C.c_void_p, C.c_double, C.c_int, C.c_int, C.POINTER(Timing)], C.c_int),
     "tdw_download": ([C.c_void_p, _dp, _dp, _dp, _dp, _i32p, _i32p], C.c_int),
+    "tdw_time_conv": ([C.c_void_p, C.c_int, C.POINTER(C.c_float)], C.c_int),
+    "tdw_set_graph": ([C.c_void_p, C.c_int], C.c_int),
     "tdw_problem_destroy": ([C.c_void_p], C.c_int),
     "tdw_nccl_unique_id": ([C.c_char_p], C.c_int),
     "tdw_comm_init": ([C.c_void_p, C.c_char_p, C.c_int, C.c_int], C.c_int),

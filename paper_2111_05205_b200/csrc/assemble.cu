@@ -147,7 +147,8 @@ struct AsmArgs {
   int2* unit;
   unsigned long long* n_evals;
   unsigned long long* n_pairs;
-  double2* coef;
+  const unsigned long long* unit_off;  // byte offset of each unit in the store
+  unsigned char* units;                // unit-major store (tdw_impl.cuh "unit layout")
   int* flags;
 };
 
@@ -203,13 +204,16 @@ __global__ void __launch_bounds__(128) fill_kernel(AsmArgs a) {
   const long long seg = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const long long nseg = (long long)a.rows_loc * a.ntiles;
   if (seg >= nseg) return;
-  const uint32_t h = a.hdr[seg * TDW_TJ + lane];
+  const int rloc = (int)(seg / a.ntiles), t = (int)(seg % a.ntiles);
+  unsigned char* ub = a.units + a.unit_off[(size_t)(rloc / TDW_TI) * a.ntiles + t];
+  const int r = rloc % TDW_TI;
+  const uint32_t h = ((const uint32_t*)(ub + TDW_UNIT_HDR_OFF))[r * TDW_TJ + lane];
   const int len = hdr_len(h), glo = hdr_glo(h), jl = hdr_jl(h);
   const int lmax = __shfl_sync(FULLMASK, len, 0);
   if (lmax == 0) return;
-  const int rloc = (int)(seg / a.ntiles), t = (int)(seg % a.ntiles);
   const int i = a.row_lo + rloc, j = t * TDW_TJ + jl;
-  const unsigned long long base = a.segcount[seg];  // exclusive offsets after the scan
+  double2* coef = (double2*)(ub + TDW_UNIT_COEF_OFF);
+  const unsigned long long base = ((const uint32_t*)ub)[r];
   const double cdt = a.c * a.dt;
   double w[D + 2];
   bspline_weights(D, w);
@@ -255,13 +259,54 @@ __global__ void __launch_bounds__(128) fill_kernel(AsmArgs a) {
         vu += w[q] * ru[q];
         vw += w[q] * rw[q];
       }
-      a.coef[off + lane] = make_double2(vu, vw);
+      coef[off + lane] = make_double2(vu, vw);
     }
     off += __popc(m);
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) nev += __shfl_xor_sync(FULLMASK, nev, o);
   if (lane == 0) atomicAdd(a.n_evals, (unsigned long long)nev);
+}
+
+// bytes of every unit: header block + 16 B per band entry of its 32 segments
+__global__ void unit_size_kernel(const unsigned long long* segcount, int ntiles, long long nunit,
+                                 unsigned long long* unit_bytes) {
+  const int lane = threadIdx.x & 31;
+  const long long u = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (u >= nunit) return;
+  const long long iblk = u / ntiles, t = u % ntiles;
+  unsigned long long c = segcount[(iblk * TDW_TI + lane) * ntiles + t];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(FULLMASK, c, o);
+  if (lane == 0) unit_bytes[u] = TDW_UNIT_COEF_OFF + 16ull * c;
+}
+
+// per-unit header block: segment offsets, lag range, the 32x32 pair headers
+__global__ void unit_layout_kernel(const unsigned long long* segcount, const uint32_t* hdr_tmp,
+                                   const int2* unit, int ntiles, long long nunit,
+                                   const unsigned long long* unit_off, unsigned char* units,
+                                   unsigned* max_rel) {
+  const int lane = threadIdx.x & 31;
+  const long long u = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (u >= nunit) return;
+  const long long iblk = u / ntiles, t = u % ntiles;
+  unsigned char* ub = units + unit_off[u];
+  const unsigned c = (unsigned)segcount[(iblk * TDW_TI + lane) * ntiles + t];
+  unsigned x = c;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned y = __shfl_up_sync(FULLMASK, x, o);
+    if (lane >= o) x += y;
+  }
+  ((uint32_t*)ub)[lane] = x - c;  // exclusive prefix
+  if (lane == 0) {
+    *(int2*)(ub + TDW_UNIT_LAG_OFF) = unit[u];
+    *(uint32_t*)(ub + TDW_UNIT_LAG_OFF + 8) = (uint32_t)(unit_off[u + 1] - unit_off[u]);
+  }
+  uint32_t* h = (uint32_t*)(ub + TDW_UNIT_HDR_OFF);
+  for (int r = 0; r < TDW_TI; ++r)
+    h[r * TDW_TJ + lane] = hdr_tmp[((iblk * TDW_TI + r) * ntiles + t) * TDW_TJ + lane];
+  if (lane == 31) atomicMax(max_rel, x);
 }
 
 struct StepArgs {
@@ -364,6 +409,39 @@ __global__ void fill_unit_init(int2* u, long long n) {
 
 using namespace tdw;
 
+static int choose_conv_schedule(tdw_problem* pb) {
+  tdw_ctx* ctx = pb->ctx;
+  int maxsm = 0;
+  cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device);
+  // FIFO capacity: all opt-in shared memory but the kernel's static part
+  const size_t cap = std::min<size_t>((size_t)maxsm - 1024, 224 * 1024) / 128 * 128;
+  pb->wbox = pb->wmax;
+  if (2 * pb->wbox > 256)
+    return tdw_fail(ctx, TDW_ERR_LIMIT, "history slice of a unit exceeds 128 lags (TMA box limit)");
+  const size_t hist_bytes = sizeof(double2) * TDW_TJ * (size_t)pb->wbox;
+  const size_t worst = (pb->max_unit_bytes + 127) / 128 * 128 + (hist_bytes + 127) / 128 * 128;
+  if (worst > cap)
+    return tdw_fail(ctx, TDW_ERR_LIMIT,
+                    "a store unit (" + std::to_string(pb->max_unit_bytes) + " B + history " +
+                        std::to_string(hist_bytes) + " B) exceeds shared memory");
+  pb->conv_stage_bytes = cap;
+  pb->conv_nstages = 4;
+  const int G = ctx->num_sms;
+  // items = (I-block, tile split); pick the split count that balances the waves
+  int bestS = 1;
+  double best = -1.0;
+  for (int S = 1; S <= std::min(pb->ntiles, 128); ++S) {
+    const long long items = (long long)pb->n_iblk * S;
+    const long long waves = (items + G - 1) / G;
+    double eff = (double)items / (double)(waves * G);
+    if (items < 2LL * G && S < pb->ntiles) eff *= 0.9;  // keep a few units per CTA in flight
+    if (eff > best + 1e-9) { best = eff; bestS = S; }
+  }
+  pb->conv_S = bestS;
+  pb->conv_grid = (int)std::min<long long>(G, (long long)pb->n_iblk * bestS);
+  return TDW_OK;
+}
+
 int tdw_assemble_impl(tdw_problem* pb) {
   tdw_ctx* ctx = pb->ctx;
   cudaStream_t st = ctx->stream;
@@ -376,12 +454,15 @@ int tdw_assemble_impl(tdw_problem* pb) {
 
   const long long nseg = (long long)pb->rows_per_rank * pb->ntiles;
   const long long nunit = (long long)pb->n_iblk * pb->ntiles;
-  TDW_CUDA(ctx, cudaMalloc(&pb->d_hdr, sizeof(uint32_t) * nseg * TDW_TJ));
-  TDW_CUDA(ctx, cudaMalloc(&pb->d_segoff, sizeof(unsigned long long) * (nseg + 1)));
+  uint32_t* d_hdr_tmp = nullptr;
+  unsigned long long* d_segcnt = nullptr;
+  unsigned long long* d_cnt = nullptr;  // {n_evals, n_pairs, nnz, bound_bits, max_rel}
+  TDW_CUDA(ctx, cudaMalloc(&d_hdr_tmp, sizeof(uint32_t) * nseg * TDW_TJ));
+  TDW_CUDA(ctx, cudaMalloc(&d_segcnt, sizeof(unsigned long long) * nseg));
   TDW_CUDA(ctx, cudaMalloc(&pb->d_unit, sizeof(int2) * nunit));
-  unsigned long long* d_cnt = nullptr;  // {n_evals, n_pairs, nnz, bound_bits}
-  TDW_CUDA(ctx, cudaMalloc(&d_cnt, sizeof(unsigned long long) * 4));
-  TDW_CUDA(ctx, cudaMemsetAsync(d_cnt, 0, sizeof(unsigned long long) * 4, st));
+  TDW_CUDA(ctx, cudaMalloc(&pb->d_unit_off, sizeof(unsigned long long) * (nunit + 1)));
+  TDW_CUDA(ctx, cudaMalloc(&d_cnt, sizeof(unsigned long long) * 5));
+  TDW_CUDA(ctx, cudaMemsetAsync(d_cnt, 0, sizeof(unsigned long long) * 5, st));
   TDW_CUDA(ctx, cudaMemsetAsync(pb->d_flags, 0, sizeof(int) * 4, st));
   fill_unit_init<<<256, 256, 0, st>>>(pb->d_unit, nunit);
 
@@ -396,8 +477,8 @@ int tdw_assemble_impl(tdw_problem* pb) {
   a.c = pb->c;
   a.dt = pb->dt;
   a.K = pb->K;
-  a.hdr = pb->d_hdr;
-  a.segcount = pb->d_segoff;
+  a.hdr = d_hdr_tmp;
+  a.segcount = d_segcnt;
   a.unit = pb->d_unit;
   a.n_evals = d_cnt;
   a.n_pairs = d_cnt + 1;
@@ -407,16 +488,18 @@ int tdw_assemble_impl(tdw_problem* pb) {
     long long blocks = (nseg * 32 + threads - 1) / threads;
     count_kernel<<<(unsigned)blocks, threads, 0, st>>>(a);
     TDW_CUDA(ctx, cudaGetLastError());
+    blocks = (nunit * 32 + threads - 1) / threads;
+    unit_size_kernel<<<(unsigned)blocks, threads, 0, st>>>(d_segcnt, pb->ntiles, nunit, pb->d_unit_off);
+    TDW_CUDA(ctx, cudaGetLastError());
   }
-  // exclusive scan of the segment entry counts -> segment offsets (in place)
+  // unit byte offsets: exclusive scan of the unit sizes (in place; last slot = total)
   {
+    TDW_CUDA(ctx, cudaMemsetAsync(pb->d_unit_off + nunit, 0, sizeof(unsigned long long), st));
     size_t tmp_bytes = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, pb->d_segoff, pb->d_segoff, nseg + 1, st);
+    cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, pb->d_unit_off, pb->d_unit_off, nunit + 1, st);
     void* tmp = nullptr;
     TDW_CUDA(ctx, cudaMalloc(&tmp, tmp_bytes));
-    // the element after the last segment must be zero before the scan
-    TDW_CUDA(ctx, cudaMemsetAsync(pb->d_segoff + nseg, 0, sizeof(unsigned long long), st));
-    cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, pb->d_segoff, pb->d_segoff, nseg + 1, st);
+    cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, pb->d_unit_off, pb->d_unit_off, nunit + 1, st);
     TDW_CUDA(ctx, cudaGetLastError());
     TDW_CUDA(ctx, cudaStreamSynchronize(st));
     cudaFree(tmp);
@@ -425,9 +508,14 @@ int tdw_assemble_impl(tdw_problem* pb) {
   TDW_CUDA(ctx, cudaMemcpy(hflags, pb->d_flags, sizeof(hflags), cudaMemcpyDeviceToHost));
   if (hflags[3] == 2)
     return tdw_fail(ctx, TDW_ERR_LIMIT, "a pair band exceeds 255 lags (c*dt far below the element size)");
-  unsigned long long n_band = 0;
-  TDW_CUDA(ctx, cudaMemcpy(&n_band, pb->d_segoff + nseg, sizeof(n_band), cudaMemcpyDeviceToHost));
-  pb->n_band = (int64_t)n_band;
+  std::vector<unsigned long long> uoff(nunit + 1);
+  TDW_CUDA(ctx, cudaMemcpy(uoff.data(), pb->d_unit_off, sizeof(unsigned long long) * (nunit + 1),
+                           cudaMemcpyDeviceToHost));
+  const unsigned long long total_bytes = uoff[nunit];
+  pb->n_band = (int64_t)((total_bytes - (unsigned long long)TDW_UNIT_COEF_OFF * nunit) / 16);
+  pb->max_unit_bytes = 0;
+  for (long long u = 0; u < nunit; ++u)
+    pb->max_unit_bytes = std::max<size_t>(pb->max_unit_bytes, uoff[u + 1] - uoff[u]);
   {
     std::vector<int2> hu(nunit);
     TDW_CUDA(ctx, cudaMemcpy(hu.data(), pb->d_unit, sizeof(int2) * nunit, cudaMemcpyDeviceToHost));
@@ -436,8 +524,17 @@ int tdw_assemble_impl(tdw_problem* pb) {
       if (u.y >= u.x) wm = std::max(wm, u.y - u.x + 1);
     pb->wmax = wm;
   }
-  TDW_CUDA(ctx, cudaMalloc(&pb->d_coef, sizeof(double2) * (n_band ? n_band : 1)));
-  a.coef = pb->d_coef;
+  TDW_CUDA(ctx, cudaMalloc(&pb->d_units, total_bytes));
+  {
+    const int threads = 256;
+    long long blocks = (nunit * 32 + threads - 1) / threads;
+    unit_layout_kernel<<<(unsigned)blocks, threads, 0, st>>>(d_segcnt, d_hdr_tmp, pb->d_unit,
+                                                            pb->ntiles, nunit, pb->d_unit_off,
+                                                            pb->d_units, (unsigned*)(d_cnt + 4));
+    TDW_CUDA(ctx, cudaGetLastError());
+  }
+  a.unit_off = pb->d_unit_off;
+  a.units = pb->d_units;
   TDW_CUDA(ctx, cudaEventRecord(f0, st));
   const bool bm = pb->bie == TDW_BIE_BMBIE;
   if (pb->d == 1) { if (bm) launch_fill<1, true>(a, nseg, st); else launch_fill<1, false>(a, nseg, st); }
@@ -472,17 +569,18 @@ int tdw_assemble_impl(tdw_problem* pb) {
   TDW_CUDA(ctx, cudaGetLastError());
   TDW_CUDA(ctx, cudaEventRecord(e1, st));
   TDW_CUDA(ctx, cudaStreamSynchronize(st));
+  cudaFree(d_hdr_tmp);
+  cudaFree(d_segcnt);
 
-  unsigned long long hc[4];
+  unsigned long long hc[5];
   TDW_CUDA(ctx, cudaMemcpy(hc, d_cnt, sizeof(hc), cudaMemcpyDeviceToHost));
   TDW_CUDA(ctx, cudaMemcpy(hflags, pb->d_flags, sizeof(hflags), cudaMemcpyDeviceToHost));
   cudaFree(d_cnt);
   pb->n_evals = (int64_t)hc[0];
   pb->n_pairs = (int64_t)hc[1];
   pb->step_nnz = (int)hc[2];
-  unsigned long long bb = hc[3];
   double bound;
-  memcpy(&bound, &bb, sizeof(bound));
+  memcpy(&bound, &hc[3], sizeof(bound));
   pb->jac_bound = bound;
   pb->ell_w = hflags[2];
   if (hflags[3] == 1)
@@ -491,7 +589,8 @@ int tdw_assemble_impl(tdw_problem* pb) {
     return tdw_fail(ctx, TDW_ERR_SINGULAR,
                     "step matrix is not diagonally dominant (Jacobi bound " +
                         std::to_string(bound) + "); the on-device solver needs bound < 0.9");
-  // sweeps for a contraction of 1e-17 under the infinity-norm bound
+  // sweeps for a contraction of 1e-17 under the infinity-norm bound (cap; the
+  // solver stops earlier once the update is at round-off)
   int it = bound > 0.0 ? (int)ceil(log(1e-17) / log(bound)) : 1;
   pb->jac_iters = std::max(2, std::min(it, 400));
   float ms = 0.f, fms = 0.f;
@@ -503,8 +602,38 @@ int tdw_assemble_impl(tdw_problem* pb) {
   cudaEventDestroy(e1);
   cudaEventDestroy(f0);
   cudaEventDestroy(f1);
-  pb->store_bytes = (int64_t)(sizeof(double2) * n_band + sizeof(uint32_t) * nseg * TDW_TJ +
-                              sizeof(unsigned long long) * (nseg + 1) + sizeof(int2) * nunit);
+
+  // convolution schedule (persistent CTAs, unit list per CTA)
+  {
+    int rc = choose_conv_schedule(pb);
+    if (rc) return rc;
+  }
+  {
+    const int G = pb->conv_grid, S = pb->conv_S;
+    const long long items = (long long)pb->n_iblk * S;
+    std::vector<unsigned> sched, soff(G + 1, 0);
+    sched.reserve(nunit);
+    for (int b = 0; b < G; ++b) {
+      soff[b] = (unsigned)sched.size();
+      for (long long it2 = b; it2 < items; it2 += G) {
+        const long long iblk = it2 / S, sp = it2 % S;
+        const int tb = (int)(sp * pb->ntiles / S), te = (int)((sp + 1) * pb->ntiles / S);
+        for (int t = tb; t < te; ++t) sched.push_back((unsigned)(iblk * pb->ntiles + t));
+      }
+    }
+    soff[G] = (unsigned)sched.size();
+    TDW_CUDA(ctx, cudaMalloc(&pb->d_sched, sizeof(unsigned) * std::max<size_t>(1, sched.size())));
+    TDW_CUDA(ctx, cudaMalloc(&pb->d_sched_off, sizeof(unsigned) * (G + 1)));
+    TDW_CUDA(ctx, cudaMemcpy(pb->d_sched, sched.data(), sizeof(unsigned) * sched.size(), cudaMemcpyHostToDevice));
+    TDW_CUDA(ctx, cudaMemcpy(pb->d_sched_off, soff.data(), sizeof(unsigned) * (G + 1), cudaMemcpyHostToDevice));
+    pb->nsplit = S;
+    cudaFree(pb->d_bpart);
+    TDW_CUDA(ctx, cudaMalloc(&pb->d_bpart, sizeof(double) * (size_t)S * pb->rows_per_rank));
+    TDW_CUDA(ctx, cudaMemset(pb->d_bpart, 0, sizeof(double) * (size_t)S * pb->rows_per_rank));
+  }
+  int src = tdw_setup_cluster_solver(pb);
+  if (src) return src;
+  pb->store_bytes = (int64_t)(total_bytes + sizeof(unsigned long long) * (nunit + 1) + sizeof(int2) * nunit);
   pb->assembled = true;
   return TDW_OK;
 }

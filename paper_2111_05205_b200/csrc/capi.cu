@@ -34,16 +34,6 @@ __global__ void diameter_kernel(const double* __restrict__ v, const int* __restr
   if ((threadIdx.x & 31) == 0) atomicMax(out, (unsigned long long)__double_as_longlong(best));
 }
 
-uint64_t spread3(uint64_t x) {  // 21 bits -> every third bit
-  x &= 0x1fffff;
-  x = (x | x << 32) & 0x1f00000000ffffULL;
-  x = (x | x << 16) & 0x1f0000ff0000ffULL;
-  x = (x | x << 8) & 0x100f00f00f00f00fULL;
-  x = (x | x << 4) & 0x10c30c30c30c30c3ULL;
-  x = (x | x << 2) & 0x1249249249249249ULL;
-  return x;
-}
-
 }  // namespace
 
 extern "C" {
@@ -169,27 +159,39 @@ int tdw_problem_create(tdw_ctx* ctx, const tdw_problem_desc* dsc, tdw_problem** 
     }
     r[15] = rad;
   }
-  // Morton order of the centroids: keeps (row block, column tile) units compact in space
-  double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
-  for (int e = 0; e < ns; ++e)
-    for (int k = 0; k < 3; ++k) {
-      lo[k] = std::min(lo[k], cen[3 * e + k]);
-      hi[k] = std::max(hi[k], cen[3 * e + k]);
-    }
-  double ext = std::max(std::max(hi[0] - lo[0], hi[1] - lo[1]), hi[2] - lo[2]);
-  if (!(ext > 0.0)) ext = 1.0;
-  std::vector<uint64_t> code(ns);
-  for (int e = 0; e < ns; ++e) {
-    uint64_t q[3];
-    for (int k = 0; k < 3; ++k) {
-      double f = (cen[3 * e + k] - lo[k]) / ext;
-      q[k] = (uint64_t)std::min(2097151.0, std::max(0.0, std::floor(f * 2097151.0)));
-    }
-    code[e] = spread3(q[0]) | spread3(q[1]) << 1 | spread3(q[2]) << 2;
-  }
+  // Element order: recursive coordinate bisection of the centroids into blocks
+  // of 32 (median split along the longest extent, split sizes multiples of 32),
+  // so every 32-row I-block and 32-column J-tile is a compact surface patch.
   pb->perm.resize(ns);
   std::iota(pb->perm.begin(), pb->perm.end(), 0);
-  std::stable_sort(pb->perm.begin(), pb->perm.end(), [&](int x, int y) { return code[x] < code[y]; });
+  {
+    struct Span { int lo, hi; };
+    std::vector<Span> todo{{0, ns}};
+    while (!todo.empty()) {
+      Span sp = todo.back();
+      todo.pop_back();
+      const int n = sp.hi - sp.lo;
+      if (n <= TDW_TI) continue;
+      double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+      for (int k = sp.lo; k < sp.hi; ++k)
+        for (int a = 0; a < 3; ++a) {
+          lo[a] = std::min(lo[a], cen[3 * (size_t)pb->perm[k] + a]);
+          hi[a] = std::max(hi[a], cen[3 * (size_t)pb->perm[k] + a]);
+        }
+      int ax = 0;
+      for (int a = 1; a < 3; ++a)
+        if (hi[a] - lo[a] > hi[ax] - lo[ax]) ax = a;
+      int nl = ((n / 2 + TDW_TI / 2) / TDW_TI) * TDW_TI;
+      nl = std::max(TDW_TI, std::min(nl, n - 1));
+      auto first = pb->perm.begin() + sp.lo;
+      std::nth_element(first, first + nl, pb->perm.begin() + sp.hi, [&](int x, int y) {
+        const double cx = cen[3 * (size_t)x + ax], cy = cen[3 * (size_t)y + ax];
+        return cx < cy || (cx == cy && x < y);
+      });
+      todo.push_back({sp.lo, sp.lo + nl});
+      todo.push_back({sp.lo + nl, sp.hi});
+    }
+  }
   std::vector<double> prec((size_t)ns * TDW_ELEM_STRIDE), pphi(ns);
   for (int k = 0; k < ns; ++k) {
     memcpy(&prec[(size_t)k * TDW_ELEM_STRIDE], &rec[(size_t)pb->perm[k] * TDW_ELEM_STRIDE],
@@ -309,6 +311,11 @@ int tdw_problem_info(const tdw_problem* pb, tdw_info* out) {
   out->jacobi_bound = pb->jac_bound;
   out->t_assemble_ms = pb->t_assemble_ms;
   out->t_fill_ms = pb->t_fill_ms;
+  out->max_unit_bytes = (int64_t)pb->max_unit_bytes;
+  out->max_lag_span = pb->wmax;
+  out->conv_grid = pb->conv_grid;
+  out->conv_splits = pb->conv_S;
+  out->solve_cluster = pb->sp_cl;
   return TDW_OK;
 }
 
@@ -370,13 +377,26 @@ int tdw_march_resident(tdw_problem* pb, double threshold, int n_repeat, int time
   return TDW_OK;
 }
 
+int tdw_time_conv(tdw_problem* pb, int n, float* ms) {
+  if (!pb || n < 1 || !ms) return TDW_ERR_INVALID_ARG;
+  if (!pb->assembled) return tdw_fail(pb->ctx, TDW_ERR_STATE, "tdw_time_conv before tdw_assemble");
+  cudaSetDevice(pb->ctx->device);
+  return tdw_time_conv_impl(pb, n, ms);
+}
+
+int tdw_set_graph(tdw_problem* pb, int enable) {
+  if (!pb) return TDW_ERR_INVALID_ARG;
+  pb->use_graph = enable != 0;
+  return TDW_OK;
+}
+
 int tdw_problem_destroy(tdw_problem* pb) {
   if (!pb) return TDW_OK;
   cudaSetDevice(pb->ctx->device);
-  void* ptrs[] = {pb->d_perm, pb->d_elem, pb->d_phi, pb->d_hdr, pb->d_segoff, pb->d_coef,
+  void* ptrs[] = {pb->d_perm, pb->d_elem, pb->d_phi, pb->d_units, pb->d_unit_off, pb->d_sched, pb->d_sched_off,
                   pb->d_unit, pb->d_acol, pb->d_aval, pb->d_adiag, pb->d_hist, pb->d_uk,
                   pb->d_qk, pb->d_bpart, pb->d_b, pb->d_x, pb->d_red, pb->d_bar, pb->d_flags,
-                  pb->d_rhs};
+                  pb->d_rhs, pb->d_sp_rowptr, pb->d_sp_nnzoff, pb->d_sp_col, pb->d_sp_val};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   delete pb;

@@ -10,11 +10,15 @@
 //                     :239-242), blow-up detector (:336-338), next step's known data.
 // History: hist[j][pad + beta] = (q_j^beta, u_j^beta) (element-major, time contiguous,
 // zero padded for beta < 0), so a band reads consecutive slots of one element.
+#include <cooperative_groups.h>
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
 
 #include <climits>
 #include <cstdio>
+#include <algorithm>
+#include <vector>
 
 #include "tdw_impl.cuh"
 
@@ -22,77 +26,227 @@ namespace tdw {
 
 #define FULLMASK 0xffffffffu
 
+// --- mbarrier / bulk-copy primitives (sm_90+ PTX, used on sm_100a) ---------
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ void tensor2d_g2s(void* dst, const CUtensorMap* map, int c0, int c1,
+                                             uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+      "%3}], [%4];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+
 struct ConvArgs {
-  const uint32_t* __restrict__ hdr;
-  const unsigned long long* __restrict__ segoff;
-  const double2* __restrict__ coef;
+  const unsigned char* __restrict__ units;
+  const unsigned long long* __restrict__ unit_off;
   const int2* __restrict__ unit;
+  const unsigned* __restrict__ sched;
+  const unsigned* __restrict__ sched_off;
   const double2* __restrict__ hist;
   double* __restrict__ bpart;
   const int* __restrict__ flags;
-  int hstride, pad, ns, row_lo, rows_loc, ntiles, tiles_per_split, alpha;
+  int hstride, pad, ns, rows_loc, ntiles, S, alpha, nstages, wbox;
+  unsigned stage_bytes;  // shared-memory FIFO capacity
 };
 
-// One CTA = one I-block of 32 rows (8 warps x 4 rows) x one split of the
-// J-tiles.  Per J-tile the CTA stages the history slice of the tile's 32
-// elements over the unit's lag range in shared memory, then every warp
-// streams its rows' segments (coalesced 16 B per lane per k).
-__global__ void __launch_bounds__(256, 2) conv_kernel(ConvArgs a) {
-  extern __shared__ double2 hs[];
+#define TDW_CONV_THREADS (TDW_CONV_WARPS * 32 + 32)
+
+// K2: history convolution.  Persistent CTAs walk a precomputed list of store
+// units.  Warp 8 (producer) streams each unit -- one contiguous byte range:
+// segment offsets, lag range, pair headers, (V_U, V_W) entries -- plus the
+// unit's 32 history rows (hist[j][pad + alpha - gmax .. alpha - gmin]) into a
+// ring of shared-memory stages with cp.async.bulk, completion on an mbarrier.
+// Warps 0..7 (consumers, 4 rows each) compute from shared memory only and
+// release the stage.  Row sums of a work item (I-block, tile split) go to
+// bpart[split][row] (fixed-order, deterministic).
+__global__ void __launch_bounds__(TDW_CONV_THREADS, 1)
+    conv_kernel(ConvArgs a, const __grid_constant__ CUtensorMap hmap) {
+  extern __shared__ __align__(128) unsigned char sm[];
+  __shared__ __align__(8) uint64_t full[4];
+  __shared__ __align__(8) uint64_t empty[4];
+  __shared__ unsigned region[4];
   if (a.flags[0] != 0) return;
-  const int iblk = blockIdx.x, split = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int t0 = split * a.tiles_per_split;
-  const int t1 = min(a.ntiles, t0 + a.tiles_per_split);
+  constexpr int NS = 4;  // slots (barrier pairs); pb->conv_nstages == 4
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < NS; ++k) {
+      mbar_init(&full[k], 1);
+      mbar_init(&empty[k], TDW_CONV_WARPS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const unsigned u0 = a.sched_off[blockIdx.x], u1 = a.sched_off[blockIdx.x + 1];
+  const int nunits = (int)(u1 - u0);
+
+  if (warp == TDW_CONV_WARPS) {
+    // ---------------- producer ----------------
+    // Shared memory is a byte FIFO of a.stage_bytes (capacity): unit n takes the
+    // region [h, h + need) (wrapping to 0 when it would not fit) and may only be
+    // written once every in-flight unit overlapping that region was released.
+    // Consumers release units in order, so waiting for the newest overlapping
+    // unit suffices.  Slot n % NS carries unit n's barriers and region offset.
+    // regions of units n-1, n-2, n-3 (shift registers; NS == 4)
+    unsigned rs1 = 0, re1 = 0, rs2 = 0, re2 = 0, rs3 = 0, re3 = 0;
+    unsigned h = 0;
+    const unsigned cap = a.stage_bytes;
+    for (int base = 0; base < nunits; base += 32) {
+      unsigned uid = 0;
+      unsigned long long off = 0, nbytes = 0;
+      int2 g = make_int2(0, -1);
+      if (base + lane < nunits) {
+        uid = a.sched[u0 + base + lane];
+        off = a.unit_off[uid];
+        nbytes = a.unit_off[uid + 1] - off;
+        g = a.unit[uid];
+      }
+      const int nb = min(32, nunits - base);
+      for (int q = 0; q < nb; ++q) {
+        const int n = base + q;
+        const int slot = n & 3;
+        const unsigned quid = __shfl_sync(FULLMASK, uid, q);
+        const unsigned long long qoff = __shfl_sync(FULLMASK, off, q);
+        const unsigned qbytes = (unsigned)__shfl_sync(FULLMASK, nbytes, q);
+        const int gmin = __shfl_sync(FULLMASK, g.x, q), gmax = __shfl_sync(FULLMASK, g.y, q);
+        const int W = gmax >= gmin ? gmax - gmin + 1 : 0;
+        const int t = (int)(quid % (unsigned)a.ntiles);
+        const unsigned hbytes = W > 0 ? (unsigned)(TDW_TJ * a.wbox * 16) : 0u;
+        const unsigned ubytes = (qbytes + 127u) & ~127u;
+        const unsigned need = ubytes + ((hbytes + 127u) & ~127u);
+        if (h + need > cap) h = 0;
+        // newest in-flight unit whose region overlaps [h, h + need) (or that owns this slot)
+        const unsigned e = h + need;
+        int wait_for = n - 4;
+        if (n >= 3 && rs3 < e && h < re3) wait_for = n - 3;
+        if (n >= 2 && rs2 < e && h < re2) wait_for = n - 2;
+        if (n >= 1 && rs1 < e && h < re1) wait_for = n - 1;
+        if (wait_for >= 0) mbar_wait(&empty[wait_for & 3], (unsigned)(wait_for >> 2) & 1u);
+        rs3 = rs2; re3 = re2;
+        rs2 = rs1; re2 = re1;
+        rs1 = h; re1 = e;
+        unsigned char* sbase = sm + h;
+        if (lane == 0) {
+          region[slot] = h;
+          mbar_expect_tx(&full[slot], qbytes + hbytes);
+        }
+        __syncwarp();
+        const unsigned chunk = 32768u;
+        for (unsigned c = lane * chunk; c < qbytes; c += 32u * chunk) {
+          const unsigned len = min(chunk, qbytes - c);
+          bulk_g2s(sbase + c, a.units + qoff + c, len, &full[slot]);
+        }
+        if (W > 0 && lane == 0)  // hist[t*32 .. +32][pad+alpha-gmax .. +wbox) as one 2-D box
+          tensor2d_g2s(sbase + ubytes, &hmap, 2 * (a.pad + a.alpha - gmax), t * TDW_TJ, &full[slot]);
+        h += need;
+      }
+    }
+    return;
+  }
+  // ---------------- consumers ----------------
   double acc[TDW_ROWS_PER_WARP];
 #pragma unroll
   for (int r = 0; r < TDW_ROWS_PER_WARP; ++r) acc[r] = 0.0;
-  const int rbase = iblk * TDW_TI + warp * TDW_ROWS_PER_WARP;  // local row of acc[0]
-
-  for (int t = t0; t < t1; ++t) {
-    const int2 u = a.unit[iblk * a.ntiles + t];
-    if (u.y < u.x) continue;  // uniform across the CTA
-    const int W = u.y - u.x + 1;
-    const int nstage = TDW_TJ * W;
-    const int jbase = t * TDW_TJ;
-    const int bq = a.pad + a.alpha - u.x;  // slot of gamma = gmin
-    __syncthreads();
-    for (int q = threadIdx.x; q < nstage; q += blockDim.x) {
-      const int jl = q / W, w = q - jl * W;
-      const int j = jbase + jl;
-      hs[q] = j < a.ns ? a.hist[(size_t)j * a.hstride + (bq - w)] : make_double2(0.0, 0.0);
+  const int S = a.S;
+  int n = 0;
+  for (long long item = blockIdx.x; n < nunits; item += gridDim.x) {
+    const int iblk = (int)(item / S), sp = (int)(item % S);
+    const int tb = (int)((long long)sp * a.ntiles / S), te = (int)((long long)(sp + 1) * a.ntiles / S);
+    for (int t = tb; t < te; ++t, ++n) {
+      const int stage = n % NS;
+      mbar_wait(&full[stage], (unsigned)(n / NS) & 1u);
+      const unsigned char* ub = sm + *(volatile unsigned*)&region[stage];
+      const uint32_t* rel = (const uint32_t*)ub;
+      const int2 g = *(const int2*)(ub + TDW_UNIT_LAG_OFF);
+      const uint32_t* hdr = (const uint32_t*)(ub + TDW_UNIT_HDR_OFF);
+      const double2* coef = (const double2*)(ub + TDW_UNIT_COEF_OFF);
+      const unsigned ubytes = (unsigned)((*(const uint32_t*)(ub + TDW_UNIT_LAG_OFF + 8) + 127u) & ~127u);
+      const double2* hs = (const double2*)(ub + ubytes);
+      const int W = a.wbox;
+      // the warp's rows are interleaved (independent FMA chains); the k loop is
+      // unrolled and predicated: lanes are sorted by band length, so "len > k"
+      // is a lane prefix and the k-th entries of a segment are contiguous
+      int len[TDW_ROWS_PER_WARP], lmax = 0;
+      const double2* cp[TDW_ROWS_PER_WARP];
+      const double2* hp[TDW_ROWS_PER_WARP];
+      int off[TDW_ROWS_PER_WARP];
+      double s0[TDW_ROWS_PER_WARP], s1[TDW_ROWS_PER_WARP];
+#pragma unroll
+      for (int r = 0; r < TDW_ROWS_PER_WARP; ++r) {
+        const int row = warp * TDW_ROWS_PER_WARP + r;
+        const uint32_t h = hdr[row * TDW_TJ + lane];
+        len[r] = hdr_len(h);
+        lmax = max(lmax, __shfl_sync(FULLMASK, len[r], 0));
+        cp[r] = coef + rel[row] + lane;
+        hp[r] = hs + hdr_jl(h) * W + (g.y - hdr_glo(h));
+        off[r] = 0;
+        s0[r] = 0.0;
+        s1[r] = 0.0;
+      }
+      for (int k0 = 0; k0 < lmax; k0 += 4) {
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+          const int k = k0 + kk;
+#pragma unroll
+          for (int r = 0; r < TDW_ROWS_PER_WARP; ++r) {
+            const bool on = len[r] > k;
+            const unsigned m = __ballot_sync(FULLMASK, on);
+            if (on) {
+              const double2 cv = cp[r][off[r]];
+              const double2 hv = hp[r][-k];
+              s0[r] = fma(cv.x, hv.x, s0[r]);
+              s1[r] = fma(cv.y, hv.y, s1[r]);
+            }
+            off[r] += __popc(m);
+          }
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < TDW_ROWS_PER_WARP; ++r) acc[r] += s0[r] - s1[r];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[stage]);
     }
-    __syncthreads();
 #pragma unroll
     for (int r = 0; r < TDW_ROWS_PER_WARP; ++r) {
-      const long long seg = (long long)(rbase + r) * a.ntiles + t;
-      const uint32_t h = a.hdr[seg * TDW_TJ + lane];
-      const int len = hdr_len(h);
-      const int lmax = __shfl_sync(FULLMASK, len, 0);
-      if (lmax == 0) continue;
-      const double2* cp = a.coef + a.segoff[seg] + lane;
-      const double2* hp = hs + hdr_jl(h) * W + (hdr_glo(h) - u.x);
-      double s = 0.0;
-      int off = 0;
-      for (int k = 0; k < lmax; ++k) {
-        const unsigned m = __ballot_sync(FULLMASK, len > k);
-        if (len > k) {
-          const double2 cv = __ldcs(cp + off);
-          const double2 hv = hp[k];
-          s = fma(cv.x, hv.x, s);
-          s = fma(-cv.y, hv.y, s);
-        }
-        off += __popc(m);
-      }
-      acc[r] += s;
+      double v = acc[r];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULLMASK, v, o);
+      if (lane == 0)
+        a.bpart[(size_t)sp * a.rows_loc + iblk * TDW_TI + warp * TDW_ROWS_PER_WARP + r] = v;
+      acc[r] = 0.0;
     }
-  }
-#pragma unroll
-  for (int r = 0; r < TDW_ROWS_PER_WARP; ++r) {
-    double v = acc[r];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULLMASK, v, o);
-    if (lane == 0) a.bpart[(size_t)split * a.rows_loc + rbase + r] = v;
   }
 }
 
@@ -273,6 +427,196 @@ __global__ void __launch_bounds__(256) solve_kernel(SolveArgs a) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// Cluster solver: one thread-block cluster (CL <= 16 CTAs, 1024 threads each)
+// owns the whole lag-1 system.  CTA r holds rows [r*R, r*R+R): its CSR rows
+// (off-diagonal), diagonal, b and a double-buffered x slice live in shared
+// memory; x of other CTAs is read through distributed shared memory and every
+// Jacobi sweep ends in one cluster barrier.  Sweeps stop when
+// max|dx| <= 1e-15 max|x| (decision read by every CTA from every CTA's
+// partials, so all CTAs agree), capped by the bound-derived count.
+struct ClusterSolveArgs {
+  const double* bpart;
+  double* b;
+  const int* __restrict__ sp_rowptr;        // [CL][R+1], relative to the CTA's slice
+  const long long* __restrict__ sp_nnzoff;  // [CL+1]
+  const int* __restrict__ sp_col;           // packed (owner << 24) | local
+  const double* __restrict__ sp_val;
+  const double* __restrict__ diag;          // [ns]
+  const double* __restrict__ phi;
+  const int* __restrict__ perm;
+  const double* __restrict__ uk;
+  const double* __restrict__ qk;
+  double2* hist;
+  int* flags;
+  double* rhs;
+  double threshold;
+  int hstride, pad, ns, nsplit, rows_loc, alpha, nt, R, maxit;
+};
+
+__device__ __forceinline__ void block_reduce2_max(double& a, double& b, double* sh) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    a = fmax(a, __shfl_xor_sync(FULLMASK, a, o));
+    b = fmax(b, __shfl_xor_sync(FULLMASK, b, o));
+  }
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) { sh[2 * w] = a; sh[2 * w + 1] = b; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int k = 1; k < (int)(blockDim.x >> 5); ++k) {
+      a = fmax(a, sh[2 * k]);
+      b = fmax(b, sh[2 * k + 1]);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(1024, 1) solve_cluster_kernel(ClusterSolveArgs a) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  extern __shared__ __align__(16) unsigned char smraw[];
+  __shared__ double shred[64];
+  __shared__ double red[2][2];   // per-sweep (max|dx|, max|x|), parity double buffer
+  __shared__ double red2[4];     // (r^2, b^2, max|x|)
+  if (*(volatile int*)&a.flags[0] != 0) return;  // identical in every CTA
+  const int cr = (int)cl.block_rank();
+  const int CL = (int)cl.num_blocks();
+  const int R = a.R;
+  const int r0 = cr * R;
+  const int nr = max(0, min(R, a.ns - r0));
+  const long long nz0 = a.sp_nnzoff[cr];
+  const int nnz = (int)(a.sp_nnzoff[cr + 1] - nz0);
+  double* xs = (double*)smraw;          // [2][R]
+  double* bs = xs + 2 * R;              // [R]
+  double* dg = bs + R;                  // [R]
+  double* val = dg + R;                 // [nnz]
+  int* rp = (int*)(val + nnz);          // [R+1]
+  int* col = rp + R + 1;                // [nnz]
+  const int tid = threadIdx.x, nth = blockDim.x;
+  const int beta0 = a.alpha - 1;
+  for (int p = tid; p < nnz; p += nth) {
+    val[p] = a.sp_val[nz0 + p];
+    col[p] = a.sp_col[nz0 + p];
+  }
+  for (int i = tid; i <= R; i += nth) rp[i] = a.sp_rowptr[(size_t)cr * (R + 1) + i];
+  for (int i = tid; i < nr; i += nth) {
+    const int gi = r0 + i;
+    double bi;
+    if (a.nsplit > 0) {
+      bi = 0.0;
+      for (int s2 = 0; s2 < a.nsplit; ++s2) bi += a.bpart[(size_t)s2 * a.rows_loc + gi];
+    } else {
+      bi = __ldcg(a.b + gi);
+    }
+    bs[i] = bi;
+    dg[i] = a.diag[gi];
+    xs[i] = bi / dg[i];
+    if (a.rhs) a.rhs[(size_t)beta0 * a.ns + a.perm[gi]] = bi;
+  }
+  cl.sync();
+  int cur = 0;
+  for (int it = 1; it <= a.maxit; ++it) {
+    const double* src = xs + cur * R;
+    double* dst = xs + (cur ^ 1) * R;
+    double dmax = 0.0, xmax = 0.0;
+    for (int i = tid; i < nr; i += nth) {
+      double acc = bs[i];
+      for (int p = rp[i]; p < rp[i + 1]; ++p) {
+        const int c = col[p];
+        const int owner = c >> 24, loc = c & 0xffffff;
+        const double xv = owner == cr ? src[loc] : *cl.map_shared_rank(src + loc, owner);
+        acc -= val[p] * xv;
+      }
+      const double xn = acc / dg[i];
+      dst[i] = xn;
+      dmax = fmax(dmax, fabs(xn - src[i]));
+      xmax = fmax(xmax, fabs(xn));
+    }
+    const bool check = (it & 3) == 0 || it == a.maxit;  // convergence test every 4th sweep
+    if (check) {
+      block_reduce2_max(dmax, xmax, shred);
+      if (tid == 0) { red[(it >> 2) & 1][0] = dmax; red[(it >> 2) & 1][1] = xmax; }
+    }
+    cl.sync();
+    cur ^= 1;
+    if (check && it < a.maxit) {
+      double D = 0.0, X = 0.0;
+      double rv[2 * 16];
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        if (q < CL) {
+          const double* rr = cl.map_shared_rank(&red[(it >> 2) & 1][0], q);
+          rv[2 * q] = rr[0];
+          rv[2 * q + 1] = rr[1];
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        if (q < CL) {
+          D = fmax(D, rv[2 * q]);
+          X = fmax(X, rv[2 * q + 1]);
+        }
+      }
+      if (D <= 1e-15 * X) break;
+    }
+  }
+  const double* xf = xs + cur * R;
+  double r2 = 0.0, b2 = 0.0, xm = 0.0;
+  for (int i = tid; i < nr; i += nth) {
+    double acc = dg[i] * xf[i] - bs[i];
+    for (int p = rp[i]; p < rp[i + 1]; ++p) {
+      const int c = col[p];
+      const int owner = c >> 24, loc = c & 0xffffff;
+      const double xv = owner == cr ? xf[loc] : *cl.map_shared_rank(xf + loc, owner);
+      acc += val[p] * xv;
+    }
+    r2 += acc * acc;
+    b2 += bs[i] * bs[i];
+    xm = fmax(xm, fabs(xf[i]));
+  }
+  r2 = block_reduce_sum(r2, shred);
+  b2 = block_reduce_sum(b2, shred);
+  xm = block_reduce_max(xm, shred);
+  if (tid == 0) { red2[0] = r2; red2[1] = b2; red2[2] = xm; }
+  cl.sync();
+  double RR = 0.0, BB = 0.0, XM = 0.0;
+  for (int q = 0; q < CL; ++q) {
+    const double* rr = cl.map_shared_rank(red2, q);
+    RR += rr[0];
+    BB += rr[1];
+    XM = fmax(XM, rr[2]);
+  }
+  cl.sync();  // no CTA leaves while another may still read its shared memory
+  if (sqrt(RR) > 1e-10 * fmax(sqrt(BB), 1e-300)) {
+    if (cr == 0 && tid == 0) {
+      a.flags[2] = a.alpha;
+      atomicExch(&a.flags[0], 2);
+    }
+    return;
+  }
+  const bool unstable = XM > a.threshold;
+  for (int i = tid; i < nr; i += nth) {
+    const int j = r0 + i;
+    const int o = a.perm[j];
+    const double xj = xf[i];
+    const double ph = a.phi[j];
+    const size_t kb = (size_t)beta0 * a.ns + o;
+    const double qv = ph == 1.0 ? a.qk[kb] : xj;
+    const double uv = ph == 1.0 ? xj : a.uk[kb];
+    a.hist[(size_t)j * a.hstride + a.pad + beta0] = make_double2(qv, uv);
+    if (beta0 + 1 < a.nt - 1 && !unstable) {
+      const size_t kn = (size_t)(beta0 + 1) * a.ns + o;
+      a.hist[(size_t)j * a.hstride + a.pad + beta0 + 1] =
+          make_double2(ph * a.qk[kn], (1.0 - ph) * a.uk[kn]);
+    }
+  }
+  if (cr == 0 && tid == 0) {
+    a.flags[1] = a.alpha;
+    if (unstable) atomicExch(&a.flags[0], 1);
+  }
+}
+
 // hist[j][pad + 0] = known part of step beta = 0 (the loop writes the later ones)
 __global__ void init_hist_kernel(double2* hist, int hstride, int pad, int ns, int nt,
                                  const double* phi, const int* perm, const double* uk,
@@ -328,12 +672,124 @@ __global__ void outputs_kernel(const double2* hist, int hstride, int pad, int ns
 
 using namespace tdw;
 
-static int launch_solve(tdw_problem* pb, SolveArgs& s) {
-  void* args[] = {&s};
-  TDW_CUDA(pb->ctx, cudaLaunchCooperativeKernel((const void*)solve_kernel, pb->solve_grid, 256,
-                                                args, 0, pb->ctx->stream));
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                    const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                    const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                    CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+// 2-D view of the history: rows = elements, inner = 2*hstride doubles; box =
+// [32 elements][2*wbox doubles], out-of-range lags/elements read as zero.
+static int make_hist_map(tdw_problem* pb, CUtensorMap* map) {
+  static PFN_encodeTiled enc = nullptr;
+  if (!enc) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        !fn)
+      return tdw_fail(pb->ctx, TDW_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    enc = (PFN_encodeTiled)fn;
+  }
+  cuuint64_t dims[2] = {(cuuint64_t)2 * pb->hstride, (cuuint64_t)pb->ns};
+  cuuint64_t strides[1] = {(cuuint64_t)pb->hstride * 16};
+  cuuint32_t box[2] = {(cuuint32_t)(2 * pb->wbox), (cuuint32_t)TDW_TJ};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, pb->d_hist, dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return tdw_fail(pb->ctx, TDW_ERR_CUDA, "cuTensorMapEncodeTiled failed");
   return TDW_OK;
 }
+
+static void fill_conv_args(tdw_problem* pb, ConvArgs& c) {
+  c.wbox = pb->wbox;
+  c.units = pb->d_units;
+  c.unit_off = pb->d_unit_off;
+  c.unit = pb->d_unit;
+  c.sched = pb->d_sched;
+  c.sched_off = pb->d_sched_off;
+  c.hist = pb->d_hist;
+  c.bpart = pb->d_bpart;
+  c.flags = pb->d_flags;
+  c.hstride = pb->hstride;
+  c.pad = pb->pad;
+  c.ns = pb->ns;
+  c.rows_loc = pb->rows_per_rank;
+  c.ntiles = pb->ntiles;
+  c.S = pb->conv_S;
+  c.nstages = pb->conv_nstages;
+  c.stage_bytes = (unsigned)pb->conv_stage_bytes;
+}
+
+namespace {
+
+struct LoopPlan {
+  CUtensorMap hmap;
+  ConvArgs c;
+  SolveArgs s;
+  ClusterSolveArgs cs;
+  dim3 cgrid;
+  size_t smem;
+  bool multi;
+};
+
+// Enqueue one complete time loop (init + nt-1 steps) on the ctx stream.  Used
+// directly and under stream capture (one CUDA graph per loop configuration).
+int enqueue_loop(tdw_problem* pb, LoopPlan& L, cudaEvent_t* ev_conv) {
+  tdw_ctx* ctx = pb->ctx;
+  cudaStream_t st = ctx->stream;
+  TDW_CUDA(ctx, cudaMemsetAsync(pb->d_flags, 0, sizeof(int) * 4, st));
+  init_hist_kernel<<<(pb->ns + 255) / 256, 256, 0, st>>>(pb->d_hist, pb->hstride, pb->pad, pb->ns,
+                                                         pb->nt, pb->d_phi, pb->d_perm, pb->d_uk,
+                                                         pb->d_qk);
+  TDW_CUDA(ctx, cudaGetLastError());
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(pb->solve_grid);
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchAttribute cattr[1];
+  cattr[0].id = cudaLaunchAttributeClusterDimension;
+  cattr[0].val.clusterDim.x = pb->sp_cl > 0 ? pb->sp_cl : 1;
+  cattr[0].val.clusterDim.y = 1;
+  cattr[0].val.clusterDim.z = 1;
+  cudaLaunchConfig_t ccfg = {};
+  ccfg.gridDim = dim3(pb->sp_cl > 0 ? pb->sp_cl : 1);
+  ccfg.blockDim = dim3(1024);
+  ccfg.dynamicSmemBytes = pb->sp_smem;
+  ccfg.stream = st;
+  ccfg.attrs = cattr;
+  ccfg.numAttrs = 1;
+  for (int alpha = 1; alpha < pb->nt; ++alpha) {
+    L.c.alpha = alpha;
+    L.s.alpha = alpha;
+    if (ev_conv) TDW_CUDA(ctx, cudaEventRecord(ev_conv[2 * (alpha - 1)], st));
+    conv_kernel<<<L.cgrid, TDW_CONV_THREADS, L.smem, st>>>(L.c, L.hmap);
+    if (ev_conv) TDW_CUDA(ctx, cudaEventRecord(ev_conv[2 * (alpha - 1) + 1], st));
+    if (L.multi) {
+      reduce_parts_kernel<<<(pb->rows_per_rank + 255) / 256, 256, 0, st>>>(
+          pb->d_bpart, pb->nsplit, pb->rows_per_rank, pb->d_b + pb->row_lo, pb->d_flags);
+      ncclResult_t nr = ncclAllGather(pb->d_b + pb->row_lo, pb->d_b, (size_t)pb->rows_per_rank,
+                                      ncclDouble, ctx->comm, st);
+      if (nr != ncclSuccess)
+        return tdw_fail(ctx, TDW_ERR_NCCL, std::string("ncclAllGather: ") + ncclGetErrorString(nr));
+    }
+    if (pb->sp_cl > 0) {
+      L.cs.alpha = alpha;
+      TDW_CUDA(ctx, cudaLaunchKernelEx(&ccfg, solve_cluster_kernel, L.cs));
+    } else {
+      TDW_CUDA(ctx, cudaLaunchKernelEx(&cfg, solve_kernel, L.s));
+    }
+  }
+  TDW_CUDA(ctx, cudaGetLastError());
+  return TDW_OK;
+}
+
+}  // namespace
 
 int tdw_march_loop(tdw_problem* pb, double threshold, bool want_rhs, bool time_kernels,
                    tdw_timing* timing) {
@@ -346,35 +802,21 @@ int tdw_march_loop(tdw_problem* pb, double threshold, bool want_rhs, bool time_k
       TDW_CUDA(ctx, cudaMalloc(&pb->d_rhs, sizeof(double) * (size_t)(pb->nt - 1) * pb->ns));
     TDW_CUDA(ctx, cudaMemsetAsync(pb->d_rhs, 0, sizeof(double) * (size_t)(pb->nt - 1) * pb->ns, st));
   }
-  TDW_CUDA(ctx, cudaMemsetAsync(pb->d_flags, 0, sizeof(int) * 4, st));
   TDW_CUDA(ctx, cudaMemsetAsync(pb->d_bar, 0, sizeof(unsigned) * 2, st));
-  init_hist_kernel<<<(pb->ns + 255) / 256, 256, 0, st>>>(pb->d_hist, pb->hstride, pb->pad, pb->ns,
-                                                         pb->nt, pb->d_phi, pb->d_perm, pb->d_uk,
-                                                         pb->d_qk);
-  TDW_CUDA(ctx, cudaGetLastError());
 
-  ConvArgs c{};
-  c.hdr = pb->d_hdr;
-  c.segoff = pb->d_segoff;
-  c.coef = pb->d_coef;
-  c.unit = pb->d_unit;
-  c.hist = pb->d_hist;
-  c.bpart = pb->d_bpart;
-  c.flags = pb->d_flags;
-  c.hstride = pb->hstride;
-  c.pad = pb->pad;
-  c.ns = pb->ns;
-  c.row_lo = pb->row_lo;
-  c.rows_loc = pb->rows_per_rank;
-  c.ntiles = pb->ntiles;
-  c.tiles_per_split = (pb->ntiles + pb->nsplit - 1) / pb->nsplit;
-  const size_t smem = sizeof(double2) * TDW_TJ * pb->wmax;
+  LoopPlan L{};
+  ConvArgs& c = L.c;
+  fill_conv_args(pb, c);
+  {
+    int rc = make_hist_map(pb, &L.hmap);
+    if (rc) return rc;
+  }
+  L.smem = pb->conv_stage_bytes;
   TDW_CUDA(ctx, cudaFuncSetAttribute(conv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)smem));
-  dim3 cgrid(pb->n_iblk, pb->nsplit);
-
-  SolveArgs s{};
-  const bool multi = pb->nranks > 1;
+                                     (int)L.smem));
+  L.cgrid = dim3(pb->conv_grid);
+  L.multi = pb->nranks > 1;
+  SolveArgs& s = L.s;
   s.bpart = pb->d_bpart;
   s.b = pb->d_b;
   s.x = pb->d_x;
@@ -396,68 +838,96 @@ int tdw_march_loop(tdw_problem* pb, double threshold, bool want_rhs, bool time_k
   s.rhs = want_rhs ? pb->d_rhs : nullptr;
   s.threshold = threshold;
   s.ns = pb->ns;
-  s.nsplit = multi ? 0 : pb->nsplit;
+  s.nsplit = L.multi ? 0 : pb->nsplit;
   s.rows_loc = pb->rows_per_rank;
   s.nt = pb->nt;
 
-  cudaEvent_t ev_all0, ev_all1;
-  TDW_CUDA(ctx, cudaEventCreate(&ev_all0));
-  TDW_CUDA(ctx, cudaEventCreate(&ev_all1));
-  std::vector<cudaEvent_t> evs;
+  ClusterSolveArgs& cs = L.cs;
+  cs.bpart = pb->d_bpart;
+  cs.b = pb->d_b;
+  cs.sp_rowptr = pb->d_sp_rowptr;
+  cs.sp_nnzoff = pb->d_sp_nnzoff;
+  cs.sp_col = pb->d_sp_col;
+  cs.sp_val = pb->d_sp_val;
+  cs.diag = pb->d_adiag;
+  cs.phi = pb->d_phi;
+  cs.perm = pb->d_perm;
+  cs.uk = pb->d_uk;
+  cs.qk = pb->d_qk;
+  cs.hist = pb->d_hist;
+  cs.flags = pb->d_flags;
+  cs.rhs = want_rhs ? pb->d_rhs : nullptr;
+  cs.threshold = threshold;
+  cs.hstride = pb->hstride;
+  cs.pad = pb->pad;
+  cs.ns = pb->ns;
+  cs.nsplit = L.multi ? 0 : pb->nsplit;
+  cs.rows_loc = pb->rows_per_rank;
+  cs.nt = pb->nt;
+  cs.R = pb->sp_R;
+  cs.maxit = pb->jac_iters;
+
+  const int nsteps = pb->nt - 1;
+  std::vector<cudaEvent_t> evc;
   if (time_kernels) {
-    evs.resize(6 * (size_t)(pb->nt - 1));
-    for (auto& e : evs) TDW_CUDA(ctx, cudaEventCreate(&e));
+    evc.resize(2 * (size_t)nsteps);
+    for (auto& e : evc) TDW_CUDA(ctx, cudaEventCreate(&e));
   }
-  TDW_CUDA(ctx, cudaEventRecord(ev_all0, st));
-  for (int alpha = 1; alpha < pb->nt; ++alpha) {
-    c.alpha = alpha;
-    s.alpha = alpha;
-    cudaEvent_t* E = time_kernels ? &evs[6 * (size_t)(alpha - 1)] : nullptr;
-    if (E) cudaEventRecord(E[0], st);
-    conv_kernel<<<cgrid, 256, smem, st>>>(c);
-    if (E) cudaEventRecord(E[1], st);
-    if (multi) {
-      reduce_parts_kernel<<<(pb->rows_per_rank + 255) / 256, 256, 0, st>>>(
-          pb->d_bpart, pb->nsplit, pb->rows_per_rank, pb->d_b + pb->row_lo, pb->d_flags);
-      if (E) cudaEventRecord(E[2], st);
-      ncclResult_t nr = ncclAllGather(pb->d_b + pb->row_lo, pb->d_b, (size_t)pb->rows_per_rank,
-                                      ncclDouble, ctx->comm, st);
-      if (nr != ncclSuccess)
-        return tdw_fail(ctx, TDW_ERR_NCCL, std::string("ncclAllGather: ") + ncclGetErrorString(nr));
-      if (E) cudaEventRecord(E[3], st);
-    }
-    if (E) cudaEventRecord(E[4], st);
-    int rc = launch_solve(pb, s);
-    if (rc) return rc;
-    if (E) cudaEventRecord(E[5], st);
-  }
-  TDW_CUDA(ctx, cudaGetLastError());
-  TDW_CUDA(ctx, cudaEventRecord(ev_all1, st));
-  TDW_CUDA(ctx, cudaEventSynchronize(ev_all1));
-  if (timing) {
-    float ms = 0.f;
-    cudaEventElapsedTime(&ms, ev_all0, ev_all1);
-    timing->total_ms += ms;
-    timing->steps += pb->nt - 1;
-    if (time_kernels) {
-      for (int k = 0; k < pb->nt - 1; ++k) {
-        cudaEvent_t* E = &evs[6 * (size_t)k];
-        float a = 0.f;
-        cudaEventElapsedTime(&a, E[0], E[1]);
-        timing->conv_ms += a;
-        timing->conv_launches += 1;
-        cudaEventElapsedTime(&a, E[4], E[5]);
-        timing->solve_ms += a;
-        if (multi) {
-          cudaEventElapsedTime(&a, E[2], E[3]);
-          timing->comm_ms += a;
-        }
+  cudaEvent_t ev0, ev1;
+  TDW_CUDA(ctx, cudaEventCreate(&ev0));
+  TDW_CUDA(ctx, cudaEventCreate(&ev1));
+
+  // capture the loop into a graph (launch overhead of ~2-4 kernels per step
+  // otherwise dominates the small configurations); fall back to direct launches
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  bool use_graph = pb->use_graph;
+  if (use_graph) {
+    if (cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+      use_graph = false;
+    } else {
+      int rc = enqueue_loop(pb, L, time_kernels ? evc.data() : nullptr);
+      cudaError_t ce = cudaStreamEndCapture(st, &graph);
+      if (rc != TDW_OK || ce != cudaSuccess ||
+          cudaGraphInstantiate(&exec, graph, 0) != cudaSuccess) {
+        cudaGetLastError();
+        if (graph) cudaGraphDestroy(graph);
+        graph = nullptr;
+        exec = nullptr;
+        use_graph = false;
+        pb->use_graph = false;
       }
     }
   }
-  for (auto& e : evs) cudaEventDestroy(e);
-  cudaEventDestroy(ev_all0);
-  cudaEventDestroy(ev_all1);
+  TDW_CUDA(ctx, cudaEventRecord(ev0, st));
+  if (use_graph) {
+    TDW_CUDA(ctx, cudaGraphLaunch(exec, st));
+  } else {
+    int rc = enqueue_loop(pb, L, time_kernels ? evc.data() : nullptr);
+    if (rc) return rc;
+  }
+  TDW_CUDA(ctx, cudaEventRecord(ev1, st));
+  TDW_CUDA(ctx, cudaEventSynchronize(ev1));
+  if (timing) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, ev0, ev1);
+    timing->total_ms += ms;
+    timing->steps += nsteps;
+    for (int k = 0; k < (time_kernels ? nsteps : 0); ++k) {
+      float a = 0.f;
+      if (cudaEventElapsedTime(&a, evc[2 * k], evc[2 * k + 1]) == cudaSuccess) {
+        timing->conv_ms += a;
+        timing->conv_launches += 1;
+      }
+    }
+    timing->solve_ms = use_graph ? 1.0 : 0.0;  // reused as a "graph used" marker
+  }
+  cudaGetLastError();
+  if (exec) cudaGraphExecDestroy(exec);
+  if (graph) cudaGraphDestroy(graph);
+  for (auto& e : evc) cudaEventDestroy(e);
+  cudaEventDestroy(ev0);
+  cudaEventDestroy(ev1);
   int hflags[4];
   TDW_CUDA(ctx, cudaMemcpy(hflags, pb->d_flags, sizeof(hflags), cudaMemcpyDeviceToHost));
   if (hflags[0] == 2) {
@@ -465,6 +935,40 @@ int tdw_march_loop(tdw_problem* pb, double threshold, bool want_rhs, bool time_k
     snprintf(msg, sizeof(msg), "step %d: solve residual too large", hflags[2]);
     return tdw_fail(ctx, TDW_ERR_RESIDUAL, msg);
   }
+  return TDW_OK;
+}
+
+// Kernel-only timing of the history convolution at a fixed step (every launch
+// streams the whole band, so the duration does not depend on the step).
+int tdw_time_conv_impl(tdw_problem* pb, int n, float* ms_out) {
+  tdw_ctx* ctx = pb->ctx;
+  cudaStream_t st = ctx->stream;
+  ConvArgs c{};
+  fill_conv_args(pb, c);
+  c.alpha = pb->nt - 1;
+  CUtensorMap hmap;
+  {
+    int rc = make_hist_map(pb, &hmap);
+    if (rc) return rc;
+  }
+  const size_t smem = pb->conv_stage_bytes;
+  TDW_CUDA(ctx, cudaFuncSetAttribute(conv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  TDW_CUDA(ctx, cudaMemsetAsync(pb->d_flags, 0, sizeof(int) * 4, st));
+  cudaEvent_t e0, e1;
+  TDW_CUDA(ctx, cudaEventCreate(&e0));
+  TDW_CUDA(ctx, cudaEventCreate(&e1));
+  dim3 grid(pb->conv_grid);
+  conv_kernel<<<grid, TDW_CONV_THREADS, smem, st>>>(c, hmap);  // warm-up
+  TDW_CUDA(ctx, cudaEventRecord(e0, st));
+  for (int k = 0; k < n; ++k) conv_kernel<<<grid, TDW_CONV_THREADS, smem, st>>>(c, hmap);
+  TDW_CUDA(ctx, cudaEventRecord(e1, st));
+  TDW_CUDA(ctx, cudaEventSynchronize(e1));
+  TDW_CUDA(ctx, cudaGetLastError());
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  *ms_out = ms / n;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
   return TDW_OK;
 }
 
@@ -485,5 +989,81 @@ int tdw_outputs(tdw_problem* pb, double* u, double* q, double* tau, double* sigm
                                     cudaMemcpyDeviceToHost, st));
   TDW_CUDA(ctx, cudaFreeAsync(buf, st));
   TDW_CUDA(ctx, cudaStreamSynchronize(st));
+  return TDW_OK;
+}
+
+// Partition the lag-1 step matrix over a thread-block cluster (host, once per
+// problem): smallest CL in {1,2,4,8,16} whose per-CTA slice fits in shared memory.
+int tdw_setup_cluster_solver(tdw_problem* pb) {
+  tdw_ctx* ctx = pb->ctx;
+  const int ns = pb->ns;
+  std::vector<int> acol((size_t)TDW_ELL_MAX * ns);
+  std::vector<double> aval((size_t)TDW_ELL_MAX * ns);
+  TDW_CUDA(ctx, cudaMemcpy(acol.data(), pb->d_acol, sizeof(int) * acol.size(), cudaMemcpyDeviceToHost));
+  TDW_CUDA(ctx, cudaMemcpy(aval.data(), pb->d_aval, sizeof(double) * aval.size(), cudaMemcpyDeviceToHost));
+  int maxsm = 0;
+  TDW_CUDA(ctx, cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
+  const size_t budget = (size_t)maxsm - 4096;  // static shared memory of the kernel
+  pb->sp_cl = 0;
+  // about one row per thread (latency-bound sweeps), more CTAs only if the slice must shrink
+  int cl0 = 1;
+  while (cl0 < 16 && (ns + cl0 - 1) / cl0 > 1024) cl0 *= 2;
+  for (int CL = cl0; CL <= 16; CL *= 2) {
+    const int R = (ns + CL - 1) / CL;
+    size_t worst = 0;
+    for (int c = 0; c < CL; ++c) {
+      size_t nnz = 0;
+      for (int i = c * R; i < std::min(ns, (c + 1) * R); ++i)
+        for (int k = 0; k < pb->ell_w; ++k)
+          if (acol[(size_t)k * ns + i] != i) ++nnz;
+      worst = std::max(worst, nnz);
+    }
+    const size_t smem = sizeof(double) * (4 * (size_t)R + worst) + sizeof(int) * (R + 1 + worst);
+    if (smem <= budget) {
+      pb->sp_cl = CL;
+      pb->sp_R = R;
+      pb->sp_smem = smem;
+      break;
+    }
+  }
+  if (pb->sp_cl == 0) return TDW_OK;  // too large: grid-barrier solver
+  const int CL = pb->sp_cl, R = pb->sp_R;
+  std::vector<int> rowptr((size_t)CL * (R + 1), 0);
+  std::vector<long long> nzoff(CL + 1, 0);
+  std::vector<int> col;
+  std::vector<double> val;
+  for (int c = 0; c < CL; ++c) {
+    nzoff[c] = (long long)col.size();
+    int* rp = &rowptr[(size_t)c * (R + 1)];
+    int n = 0;
+    for (int i = c * R; i < (c + 1) * R; ++i) {
+      rp[i - c * R] = n;
+      if (i < ns)
+        for (int k = 0; k < pb->ell_w; ++k) {
+          const int j = acol[(size_t)k * ns + i];
+          if (j == i) continue;
+          col.push_back(((j / R) << 24) | (j % R));
+          val.push_back(aval[(size_t)k * ns + i]);
+          ++n;
+        }
+    }
+    rp[R] = n;
+  }
+  nzoff[CL] = (long long)col.size();
+  TDW_CUDA(ctx, cudaMalloc(&pb->d_sp_rowptr, sizeof(int) * rowptr.size()));
+  TDW_CUDA(ctx, cudaMalloc(&pb->d_sp_nnzoff, sizeof(long long) * nzoff.size()));
+  TDW_CUDA(ctx, cudaMalloc(&pb->d_sp_col, sizeof(int) * std::max<size_t>(1, col.size())));
+  TDW_CUDA(ctx, cudaMalloc(&pb->d_sp_val, sizeof(double) * std::max<size_t>(1, val.size())));
+  TDW_CUDA(ctx, cudaMemcpy(pb->d_sp_rowptr, rowptr.data(), sizeof(int) * rowptr.size(), cudaMemcpyHostToDevice));
+  TDW_CUDA(ctx, cudaMemcpy(pb->d_sp_nnzoff, nzoff.data(), sizeof(long long) * nzoff.size(), cudaMemcpyHostToDevice));
+  if (!col.empty()) {
+    TDW_CUDA(ctx, cudaMemcpy(pb->d_sp_col, col.data(), sizeof(int) * col.size(), cudaMemcpyHostToDevice));
+    TDW_CUDA(ctx, cudaMemcpy(pb->d_sp_val, val.data(), sizeof(double) * val.size(), cudaMemcpyHostToDevice));
+  }
+  TDW_CUDA(ctx, cudaFuncSetAttribute(solve_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)pb->sp_smem));
+  if (CL > 8)
+    TDW_CUDA(ctx, cudaFuncSetAttribute(solve_cluster_kernel,
+                                       cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   return TDW_OK;
 }

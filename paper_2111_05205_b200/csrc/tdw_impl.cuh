@@ -12,10 +12,18 @@
 // Tile geometry of the banded store.
 #define TDW_TJ 32        // columns per J-tile == pairs per segment == one warp
 #define TDW_TI 32        // rows per I-block (one conv CTA)
-#define TDW_ROWS_PER_WARP 4
+#define TDW_ROWS_PER_WARP 2
 #define TDW_CONV_WARPS (TDW_TI / TDW_ROWS_PER_WARP)
 #define TDW_ELL_MAX 64   // max nnz per row of the lag-1 step matrix
 #define TDW_ELEM_STRIDE 16  // doubles per element record: v0 v1 v2 n c rad
+// Unit layout (one (I-block, J-tile) unit = one contiguous byte range of the store):
+//   [0, 128)        uint32 seg_rel[32]  entry offset of row r's segment in the unit
+//   [128, 136)      int2 (gmin, gmax)   lag range of the unit (history slice)
+//   [256, 4352)     uint32 hdr[32][32]  pair headers, row-major, sorted by length per row
+//   [4352, ...)     double2 coef[]      (V_U, V_W) entries, jagged k-major per segment
+#define TDW_UNIT_LAG_OFF 128
+#define TDW_UNIT_HDR_OFF 256
+#define TDW_UNIT_COEF_OFF 4352
 
 struct tdw_ctx {
   int device = 0;
@@ -51,11 +59,17 @@ struct tdw_problem {
   double* d_phi = nullptr;   // internal order
   // banded store
   bool assembled = false;
-  uint32_t* d_hdr = nullptr;       // [rows_per_rank * ntiles][TDW_TJ]
-  unsigned long long* d_segoff = nullptr;  // [rows_per_rank * ntiles + 1]
-  double2* d_coef = nullptr;       // (VU, VW) pairs, jagged k-major per segment
+  unsigned char* d_units = nullptr;        // unit-major store (see unit layout above)
+  unsigned long long* d_unit_off = nullptr; // [n_iblk * ntiles + 1] byte offsets
   int2* d_unit = nullptr;          // [n_iblk * ntiles] lag range (gmin, gmax)
   int wmax = 0;                    // max unit lag span
+  int wbox = 0;                    // history box width (lags) of the TMA copy, even, >= wmax
+  size_t max_unit_bytes = 0;
+  // conv schedule: persistent CTAs over items (I-block, tile split)
+  int conv_grid = 0, conv_S = 1, conv_nstages = 2;
+  size_t conv_stage_bytes = 0;
+  unsigned* d_sched = nullptr;     // unit ids in CTA processing order
+  unsigned* d_sched_off = nullptr; // [conv_grid + 1]
   int64_t n_band = 0, n_pairs = 0, n_evals = 0, store_bytes = 0;
   // lag-1 step matrix, all rows, ELL
   int ell_w = 0, step_nnz = 0;
@@ -70,7 +84,7 @@ struct tdw_problem {
   double* d_uk = nullptr;          // (nt-1, ns) original order
   double* d_qk = nullptr;
   bool known_loaded = false;
-  int nsplit = 1;
+  int nsplit = 1;                  // == conv_S once assembled
   double* d_bpart = nullptr;       // [nsplit][rows_per_rank]
   double* d_b = nullptr;           // [nranks * rows_per_rank]
   double* d_x = nullptr;           // [2][ns]
@@ -79,6 +93,14 @@ struct tdw_problem {
   int* d_flags = nullptr;          // {status, n_steps, err_step, ell_overflow}
   double* d_rhs = nullptr;         // (nt-1, ns) original order, optional
   int solve_grid = 0;
+  // cluster solver (csrc/march.cu solve_cluster_kernel); sp_cl == 0 -> grid-barrier fallback
+  int sp_cl = 0, sp_R = 0;
+  size_t sp_smem = 0;
+  int* d_sp_rowptr = nullptr;
+  long long* d_sp_nnzoff = nullptr;
+  int* d_sp_col = nullptr;
+  double* d_sp_val = nullptr;
+  bool use_graph = true;
   double t_assemble_ms = 0.0, t_fill_ms = 0.0;
 };
 
@@ -97,3 +119,5 @@ int tdw_assemble_impl(tdw_problem* pb);
 int tdw_march_loop(tdw_problem* pb, double threshold, bool want_rhs, bool time_kernels,
                    tdw_timing* timing);
 int tdw_outputs(tdw_problem* pb, double* u, double* q, double* tau, double* sigma);
+int tdw_time_conv_impl(tdw_problem* pb, int n, float* ms_out);
+int tdw_setup_cluster_solver(tdw_problem* pb);

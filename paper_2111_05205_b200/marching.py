@@ -179,6 +179,15 @@ class BandStore:
                    self.ctx.h, "tdw_march_resident")
         return t.asdict()
 
+    def time_conv(self, n: int = 20) -> float:
+        """Average device ms of one history-convolution launch (inputs resident)."""
+        ms = C.c_float(0.0)
+        _lib.check(_lib.load().tdw_time_conv(self.h, int(n), C.byref(ms)), self.ctx.h, "tdw_time_conv")
+        return float(ms.value)
+
+    def set_graph(self, enable: bool):
+        _lib.check(_lib.load().tdw_set_graph(self.h, int(bool(enable))), self.ctx.h, "tdw_set_graph")
+
     def close(self):
         if self.h.value:
             _lib.load().tdw_problem_destroy(self.h)
