@@ -1,0 +1,292 @@
+"""Benchmark of the MOT hot path (driver contract: one JSON line on rank 0).
+
+Workload (default --config 2 = BASELINE.json configs[2], the configuration the
+metric is quoted on at 1/2/4/8 B200): 5120-element jittered unit icosphere,
+Burton-Miller d=1, Dirichlet, Nt=256, direct (banded) history convolution,
+rows sharded over the GPUs.  A bench *step* is one complete time loop: the
+Nt-1 = 255 MOT time steps of the configuration.
+
+  value   MOT time-steps/s of the time loop, banded coefficient store resident
+          in HBM (1.5 GB, i.e. larger than the 126 MB L2: no flush needed),
+          device time (CUDA events on the library stream) max over ranks.
+  e2e     the same metric through the public API march(spec, mats=store):
+          Greville sampling of the user's data callables, H2D of the known
+          data, the loop, D2H of u, q, tau, sigma -- every step.
+  roofline  K2 (history convolution): 16 B x N_band per launch / average
+          launch time measured with CUDA events around every K2 launch of the
+          timed region, against the measured HBM copy bandwidth.
+  cpu_baseline / --impl reference: the C oracle port (oracle/) of the
+          reference's march (sigma/tau lag-CSR form) on the host cores, timed
+          on a bounded row sample and extrapolated (see `sample`).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "MOT time-steps/s"
+HBM_FALLBACK = 6650.0  # GB/s, B200_PROFILING.md fallback
+
+
+def peaks():
+    try:
+        return json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+    except Exception:
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([v.strip() for v in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = sorted(float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit())
+        mx = max((float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()), default=None)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for s in self.samples for k in range(4)
+                          if len(s) > 2 + k and s[2 + k].lower() == "active"})
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def cpu_sample(spec, rows: int, steps: int):
+    """Oracle port of the reference march on `rows` collocation rows (all columns):
+    assembly of their lag-CSR and `steps` time steps of the lag SpMVs.  Returns
+    extrapolated full-problem MOT steps/s (loop only) and the sample record."""
+    from oracle import oracle
+    ns = spec.mesh.n_elements
+    lo = (ns - rows) // 2
+    t_asm, t_loop, ntrip = oracle.sample(spec.mesh.vertices, spec.mesh.triangles, spec.bie,
+                                         spec.basis.d, spec.c, spec.basis.dt, spec.nt, lo, lo + rows, steps)
+    per_step_full = t_loop / steps * ns / rows
+    return 1.0 / per_step_full, {"t_asm_s": t_asm, "t_loop_s": t_loop, "rows": rows, "steps": steps,
+                                 "lagcsr_triples": ntrip, "asm_triples_per_s": ntrip / max(t_asm, 1e-12)}
+
+
+def run_reference(args, world, rank):
+    """--impl reference: the reference algorithm on the host cores (oracle port)."""
+    import numpy as np  # noqa: F401
+    from oracle import oracle
+    from paper_2111_05205_b200 import scenarios
+    if rank != 0:
+        return
+    spec = scenarios.build_spec(args.config)
+    oracle.build()
+    rows = args.ref_rows
+    for _ in range(args.warmup):
+        cpu_sample(spec, rows, 4)
+    vals = []
+    recs = []
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        v, rec = cpu_sample(spec, rows, spec.nt - 1)
+        vals.append(v)
+        recs.append(rec)
+    wall = time.perf_counter() - t0
+    value = sum(vals) / len(vals)
+    cores = oracle.num_threads()
+    sample = (f"{rows} of {spec.mesh.n_elements} collocation rows x all columns, {spec.nt - 1} MOT steps "
+              f"of the reference's sigma/tau lag-CSR SpMVs, extrapolated by rows; "
+              f"oracle port (C, OpenMP) of marching.march")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * (spec.nt - 1) / value,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded scenario)",
+        "config": {"workload": scenarios.DESCRIPTION[args.config], "ns": spec.mesh.n_elements,
+                   "nt": spec.nt, "parallelism": "host threads"},
+        "cpu_baseline": {"value": value, "unit": "steps/s", "cores": cores, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "sample_records": recs[-1], "wall_s": wall,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, world, rank, local):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2111_05205_b200 import _lib, distributed, marching, scenarios
+
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    ctx = _lib.Context(local)
+    _lib.set_default_context(ctx)
+    if world > 1:
+        distributed.init_comm(ctx, dist)
+
+    def barrier():
+        torch.cuda.synchronize(local)
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    spec = scenarios.build_spec(args.config)
+    ns, nt = spec.mesh.n_elements, spec.nt
+    thr = 1e6 * max(spec.blowup_reference, 1e-30)
+
+    # assembly (K1 fused with the kappa combination): timed separately
+    store = marching.BandStore(spec, nranks=world, rank=rank).assemble()
+    info = store.info()
+    uk, qk = marching.greville_samples(spec)
+    store.upload_known(uk, qk)
+
+    for _ in range(args.warmup):
+        store.run_resident(thr, 1)
+    barrier()
+    with ClockSampler(local) as clk:
+        tm = store.run_resident(thr, args.steps, time_kernels=True)
+        barrier()
+    dev_ms = max_over_ranks(tm["total_ms"])
+    conv_ms = max_over_ranks(tm["conv_ms"] / max(tm["conv_launches"], 1))
+    steps_total = args.steps * (nt - 1)
+    value = steps_total / (dev_ms * 1e-3)
+
+    # e2e: public API with host buffers, every step
+    for _ in range(max(1, args.warmup // 2)):
+        marching.march(spec, mats=store)
+    barrier()
+    t0 = time.perf_counter()
+    e2e_steps = max(2, args.steps // 2)
+    for _ in range(e2e_steps):
+        h = marching.march(spec, mats=store)
+    barrier()
+    e2e_s = max_over_ranks(time.perf_counter() - t0)
+    e2e = e2e_steps * (nt - 1) / e2e_s
+    h2d = 2 * (nt - 1) * ns * 8
+    d2h = 4 * (nt - 1) * ns * 8
+
+    # roofline of K2 (history convolution), algorithmic bytes = 16 B per band entry
+    pk = peaks()
+    peak = pk.get("hbm_gbs")
+    peak_src = "measured" if peak else "fallback"
+    peak = peak or HBM_FALLBACK
+    n_band = max_over_ranks(float(info["n_band"]))
+    achieved = 16.0 * n_band / (conv_ms * 1e-3) / 1e9
+    traffic = None
+    prof = ROOT / "profiles" / "traffic.json"
+    if prof.exists():
+        try:
+            traffic = json.loads(prof.read_text()).get(f"config{args.config}")
+        except Exception:
+            traffic = None
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            v, rec = cpu_sample(spec, args.cpu_rows, nt - 1)
+            from oracle import oracle
+            cpu = {"value": v, "unit": "steps/s", "cores": oracle.num_threads(), "kind": "port",
+                   "sample": (f"{args.cpu_rows} of {ns} rows x all columns, {nt - 1} steps of the "
+                              f"reference's sigma/tau lag-CSR SpMVs (oracle port, C/OpenMP), "
+                              f"extrapolated by rows; assembly {rec['asm_triples_per_s']:.3e} triples/s")}
+        except Exception as exc:  # the CPU leg must not sink the GPU line
+            cpu = {"value": None, "unit": "steps/s", "cores": os.cpu_count(), "kind": "port",
+                   "sample": f"failed: {exc}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": dev_ms / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded BASELINE scenario, generated meshes and incident pulse)",
+            "config": {"workload": scenarios.DESCRIPTION[args.config], "ns": ns, "nt": nt,
+                       "mot_steps_per_bench_step": nt - 1, "parallelism": f"rows x{world}",
+                       "l2": "banded store 1.5 GB > 126 MB L2 (no flush needed)"
+                       if args.config >= 2 else "store fits in L2",
+                       "gamma_star": info["gamma_star"], "n_band": int(n_band)},
+            "e2e": {"value": e2e, "unit": "steps/s", "h2d_bytes_per_step": h2d * (nt - 1) // (nt - 1),
+                    "d2h_bytes_per_step": d2h, "api": "marching.march(spec, mats=store)"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "kernel": "conv_kernel (K2)",
+                         "peak_source": peak_src, "avg_launch_ms": conv_ms},
+            "cpu_baseline": cpu,
+            "clocks": clk.summary(),
+            "gpu_launches": int(tm["steps"] * (2 if world == 1 else 3) + args.steps),
+            "assembly": {"ms": info["t_assemble_ms"], "evals": info["n_evals"],
+                         "evals_per_s": info["n_evals"] / (info["t_fill_ms"] * 1e-3),
+                         "metric": "(i,j,gamma) layer-potential evals/s (fill kernel, fp64)"},
+            "graph": bool(tm.get("solve_ms", 0) > 0),
+        }
+        print(json.dumps(line), flush=True)
+    store.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--cpu-rows", type=int, default=64)
+    ap.add_argument("--ref-rows", type=int, default=64)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    world, rank, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+    else:
+        run_ours(args, world, rank, local)
+
+
+if __name__ == "__main__":
+    main()

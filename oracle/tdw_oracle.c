@@ -265,15 +265,15 @@ int oracle_gamma_star(int nv, const double* verts, int ns, const int64_t* tris, 
 }
 
 /* ------------------------------------------------------------------------ */
-/* Lag CSR store: for row i, the arrived columns j (increasing) with their
- * arrival lag a_ij (marching.py:110) and the per-lag values for g = a..G. */
+/* Lag CSR store, the reference's RetardedMatrixSet (marching.py:72-90, 132-181):
+ * for each lag g = 1..G a CSR matrix over the stored rows holding U^(g), W^(g)
+ * of every pair already arrived by g (arrival a_ij <= g, marching.py:108-110),
+ * columns increasing within a row, no upper cutoff. */
 typedef struct {
-  int ns, G;
-  int64_t* rowptr;  /* pairs per row */
-  int32_t* col;
-  int32_t* arr;
-  int64_t* vptr;    /* offset of the pair's first value (lag a) */
-  double *U, *W;
+  int nr, G;
+  int64_t** rowptr; /* [G][nr+1] */
+  int32_t** col;    /* [G][nnz_g] */
+  double **U, **W;  /* [G][nnz_g] */
   int64_t nvals;
 } lagstore;
 
@@ -288,76 +288,88 @@ static int arrival_of(const omesh* m, int i, int j, double c, double dt) {
 }
 
 static void lag_free(lagstore* L) {
-  free(L->rowptr); free(L->col); free(L->arr); free(L->vptr); free(L->U); free(L->W);
+  for (int g = 0; g < L->G; ++g) {
+    if (L->rowptr) free(L->rowptr[g]);
+    if (L->col) free(L->col[g]);
+    if (L->U) free(L->U[g]);
+    if (L->W) free(L->W[g]);
+  }
+  free(L->rowptr); free(L->col); free(L->U); free(L->W);
 }
 
 static int lag_build(lagstore* L, const omesh* m, int row_lo, int row_hi, int G, int bie, int d,
                      double c, double dt) {
   int nr = row_hi - row_lo, ns = m->ns;
-  L->ns = ns;
+  L->nr = nr;
   L->G = G;
-  L->rowptr = calloc(nr + 1, sizeof(int64_t));
-  int64_t* vcount = calloc(nr + 1, sizeof(int64_t));
-  if (!L->rowptr || !vcount) return OR_NOMEM;
+  L->nvals = 0;
+  L->rowptr = calloc(G, sizeof(int64_t*));
+  L->col = calloc(G, sizeof(int32_t*));
+  L->U = calloc(G, sizeof(double*));
+  L->W = calloc(G, sizeof(double*));
+  if (!L->rowptr || !L->col || !L->U || !L->W) return OR_NOMEM;
+  /* per row: arrivals of all columns (int8 would do; int keeps it simple) */
+  int* arr = malloc(sizeof(int) * (size_t)nr * ns);
+  if (!arr) return OR_NOMEM;
 #pragma omp parallel for schedule(dynamic, 8)
-  for (int r = 0; r < nr; ++r) {
-    int64_t np = 0, nv = 0;
-    for (int j = 0; j < ns; ++j) {
-      int a = arrival_of(m, row_lo + r, j, c, dt);
-      if (a <= G) { np++; nv += G - a + 1; }
+  for (int r = 0; r < nr; ++r)
+    for (int j = 0; j < ns; ++j) arr[(size_t)r * ns + j] = arrival_of(m, row_lo + r, j, c, dt);
+  for (int g = 1; g <= G; ++g) {
+    int64_t* rp = calloc(nr + 1, sizeof(int64_t));
+    if (!rp) { free(arr); return OR_NOMEM; }
+#pragma omp parallel for schedule(static)
+    for (int r = 0; r < nr; ++r) {
+      int64_t k = 0;
+      for (int j = 0; j < ns; ++j) k += arr[(size_t)r * ns + j] <= g;
+      rp[r + 1] = k;
     }
-    L->rowptr[r + 1] = np;
-    vcount[r + 1] = nv;
+    for (int r = 0; r < nr; ++r) rp[r + 1] += rp[r];
+    L->rowptr[g - 1] = rp;
+    L->col[g - 1] = malloc(sizeof(int32_t) * (rp[nr] ? rp[nr] : 1));
+    L->U[g - 1] = malloc(sizeof(double) * (rp[nr] ? rp[nr] : 1));
+    L->W[g - 1] = malloc(sizeof(double) * (rp[nr] ? rp[nr] : 1));
+    if (!L->col[g - 1] || !L->U[g - 1] || !L->W[g - 1]) { free(arr); return OR_NOMEM; }
+    L->nvals += rp[nr];
   }
-  for (int r = 0; r < nr; ++r) { L->rowptr[r + 1] += L->rowptr[r]; vcount[r + 1] += vcount[r]; }
-  int64_t npairs = L->rowptr[nr];
-  L->nvals = vcount[nr];
-  L->col = malloc(sizeof(int32_t) * (npairs ? npairs : 1));
-  L->arr = malloc(sizeof(int32_t) * (npairs ? npairs : 1));
-  L->vptr = malloc(sizeof(int64_t) * (npairs ? npairs : 1));
-  L->U = malloc(sizeof(double) * (L->nvals ? L->nvals : 1));
-  L->W = malloc(sizeof(double) * (L->nvals ? L->nvals : 1));
-  if (!L->col || !L->arr || !L->vptr || !L->U || !L->W) { free(vcount); return OR_NOMEM; }
   double K = kfac(d, c, dt);
   int kind = bie == 1 ? 1 : 0;
 #pragma omp parallel for schedule(dynamic, 4)
   for (int r = 0; r < nr; ++r) {
     int i = row_lo + r;
-    int64_t p = L->rowptr[r], v = vcount[r];
     double nxi[3] = {-m->nrm[3 * i], -m->nrm[3 * i + 1], -m->nrm[3 * i + 2]};
+    int64_t* pos = malloc(sizeof(int64_t) * G);
+    for (int g = 0; g < G; ++g) pos[g] = L->rowptr[g][r];
     for (int j = 0; j < ns; ++j) {
-      int a = arrival_of(m, i, j, c, dt);
-      if (a > G) continue;
-      L->col[p] = j;
-      L->arr[p] = a;
-      L->vptr[p] = v;
+      int a = arr[(size_t)r * ns + j];
       for (int g = a; g <= G; ++g) {
         double s = (double)g * c * dt;
+        int64_t q = pos[g - 1]++;
+        L->col[g - 1][q] = j;
         coeff_one(m->cen + 3 * i, m->v0 + 3 * j, m->v1 + 3 * j, m->v2 + 3 * j, m->nrm + 3 * j, s,
-                  d, K, kind, nxi, L->U + v, L->W + v);
-        ++v;
+                  d, K, kind, nxi, L->U[g - 1] + q, L->W[g - 1] + q);
       }
-      ++p;
     }
+    free(pos);
   }
-  free(vcount);
+  free(arr);
   return OR_OK;
 }
 
-/* b_r += U_g tau - W_g sigma over the stored rows (one lag) -- the reference
- * accumulates b += (U@tau - W@sig) per lag (marching.py:320-327). */
-static void lag_apply(const lagstore* L, int nr, int g, const double* tau, const double* sig,
-                      double* b, int first) {
-#pragma omp parallel for schedule(static) if (nr >= 2048)
+/* b_r (+)= U_g tau - W_g sigma over the stored rows (one lag): the reference's
+ * b += U[g-1] @ tau - W[g-1] @ sig (marching.py:320-327). */
+static void lag_apply(const lagstore* L, int g, const double* tau, const double* sig, double* b,
+                      int first) {
+  const int nr = L->nr;
+  const int64_t* rp = L->rowptr[g - 1];
+  const int32_t* col = L->col[g - 1];
+  const double* U = L->U[g - 1];
+  const double* W = L->W[g - 1];
+#pragma omp parallel for schedule(static) if (rp[nr] >= 32768)
   for (int r = 0; r < nr; ++r) {
     double su = 0.0, sw = 0.0;
-    for (int64_t p = L->rowptr[r]; p < L->rowptr[r + 1]; ++p) {
-      int a = L->arr[p];
-      if (a > g) continue;
-      int64_t v = L->vptr[p] + (g - a);
-      int j = L->col[p];
-      su += L->U[v] * tau[j];
-      sw += L->W[v] * sig[j];
+    for (int64_t p = rp[r]; p < rp[r + 1]; ++p) {
+      su += U[p] * tau[col[p]];
+      sw += W[p] * sig[col[p]];
     }
     b[r] = first ? (su - sw) : b[r] + (su - sw);
   }
@@ -391,30 +403,19 @@ int oracle_march(int nv, const double* verts, int ns, const int64_t* tris, const
   if (rc) { mesh_free(&m); lag_free(&L); return rc; }
   const double* w = weights_d[d];
   double w0 = w[0];
-  /* step matrix A = w0 (W1 phi - U1 (1 - phi)) in row-compressed form */
-  int64_t* arow = calloc(ns + 1, sizeof(int64_t));
-  for (int i = 0; i < ns; ++i) {
-    int64_t cnt = 0;
-    for (int64_t p = L.rowptr[i]; p < L.rowptr[i + 1]; ++p) cnt += (L.arr[p] <= 1);
-    arow[i + 1] = arow[i] + cnt;
-  }
-  int32_t* acol = malloc(sizeof(int32_t) * (arow[ns] + 1));
+  /* step matrix A = w0 (W1 phi - U1 (1 - phi)) (marching.py:279-289), lag-1 CSR pattern */
+  const int64_t* arow = L.rowptr[0];
+  const int32_t* acol = L.col[0];
   double* aval = malloc(sizeof(double) * (arow[ns] + 1));
   double* adiag = malloc(sizeof(double) * ns);
   for (int i = 0; i < ns; ++i) {
-    int64_t k = arow[i];
     adiag[i] = 0.0;
-    for (int64_t p = L.rowptr[i]; p < L.rowptr[i + 1]; ++p) {
-      if (L.arr[p] > 1) continue;
-      int j = L.col[p];
-      int64_t v = L.vptr[p];
-      double val = w0 * (L.W[v] * phi[j] - L.U[v] * (1.0 - phi[j]));
-      acol[k] = j;
-      aval[k] = val;
-      if (j == i) adiag[i] = val;
-      ++k;
+    for (int64_t k = arow[i]; k < arow[i + 1]; ++k) {
+      int j = acol[k];
+      aval[k] = w0 * (L.W[0][k] * phi[j] - L.U[0][k] * (1.0 - phi[j]));
+      if (j == i) adiag[i] = aval[k];
     }
-    if (adiag[i] == 0.0) { rc = OR_SINGULAR; }
+    if (adiag[i] == 0.0) rc = OR_SINGULAR;
   }
   double *b = malloc(sizeof(double) * ns), *x = malloc(sizeof(double) * ns),
          *tt = malloc(sizeof(double) * ns), *st = malloc(sizeof(double) * ns),
@@ -441,7 +442,7 @@ int oracle_march(int nv, const double* verts, int ns, const int64_t* tris, const
         tt[j] += w[k] * q[(size_t)(beta0 - k) * ns + j];
         st[j] += w[k] * u[(size_t)(beta0 - k) * ns + j];
       }
-    lag_apply(&L, ns, 1, tt, st, b, 1);
+    lag_apply(&L, 1, tt, st, b, 1);
     int gmax = alpha < n_lags ? alpha : n_lags;
     for (int g = 2; g <= gmax; ++g) {
       int beta = alpha - g;
@@ -462,7 +463,7 @@ int oracle_march(int nv, const double* verts, int ns, const int64_t* tris, const
         tp = tau + (size_t)beta * ns;
         sp = sig + (size_t)beta * ns;
       }
-      lag_apply(&L, ns, g, tp, sp, b, 0);
+      lag_apply(&L, g, tp, sp, b, 0);
     }
     if (rhs_trace) memcpy(rhs_trace + (size_t)beta0 * ns, b, sizeof(double) * ns);
     /* solve A x = b: Gauss-Seidel to round-off, then the reference residual test */
@@ -512,7 +513,7 @@ int oracle_march(int nv, const double* verts, int ns, const int64_t* tris, const
     if (xmax > threshold) { *status = 1; break; }
   }
   free(b); free(x); free(tt); free(st); free(tw); free(sw);
-  free(arow); free(acol); free(aval); free(adiag);
+  free(aval); free(adiag);
   lag_free(&L);
   mesh_free(&m);
   return rc;
@@ -551,7 +552,7 @@ int oracle_sample(int nv, const double* verts, int ns, const int64_t* tris, int 
     for (int g = 1; g <= n_lags; ++g) {
       const double* tp = hist + (size_t)(2 * g) * ns / 2;
       const double* sp = hist + (size_t)(2 * g + 1) * ns / 2;
-      lag_apply(&L, nr, g, tp, sp, b, g == 1);
+      lag_apply(&L, g, tp, sp, b, g == 1);
     }
   }
 #ifdef _OPENMP

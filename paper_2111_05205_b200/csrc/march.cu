@@ -767,9 +767,9 @@ int enqueue_loop(tdw_problem* pb, LoopPlan& L, cudaEvent_t* ev_conv) {
   for (int alpha = 1; alpha < pb->nt; ++alpha) {
     L.c.alpha = alpha;
     L.s.alpha = alpha;
-    if (ev_conv) TDW_CUDA(ctx, cudaEventRecord(ev_conv[2 * (alpha - 1)], st));
+    if (ev_conv) TDW_CUDA(ctx, cudaEventRecordWithFlags(ev_conv[2 * (alpha - 1)], st, cudaEventRecordExternal));
     conv_kernel<<<L.cgrid, TDW_CONV_THREADS, L.smem, st>>>(L.c, L.hmap);
-    if (ev_conv) TDW_CUDA(ctx, cudaEventRecord(ev_conv[2 * (alpha - 1) + 1], st));
+    if (ev_conv) TDW_CUDA(ctx, cudaEventRecordWithFlags(ev_conv[2 * (alpha - 1) + 1], st, cudaEventRecordExternal));
     if (L.multi) {
       reduce_parts_kernel<<<(pb->rows_per_rank + 255) / 256, 256, 0, st>>>(
           pb->d_bpart, pb->nsplit, pb->rows_per_rank, pb->d_b + pb->row_lo, pb->d_flags);
