@@ -147,6 +147,7 @@ struct AsmArgs {
   int2* unit;
   unsigned long long* n_evals;
   unsigned long long* n_pairs;
+  const double* phi;                   // internal order
   const unsigned long long* unit_off;  // byte offset of each unit in the store
   unsigned char* units;                // unit-major store (tdw_impl.cuh "unit layout")
   int* flags;
@@ -161,12 +162,14 @@ __global__ void __launch_bounds__(256) count_kernel(AsmArgs a) {
   const int i = a.row_lo + rloc, j = t * TDW_TJ + lane;
   const double cdt = a.c * a.dt;
   int len = 0, glo = 0;
+  bool any = false;
   if (i < a.ns && j < a.ns) {
     Elem ej;
     load_elem(a.elem, j, ej);
     const double* ci = a.elem + (size_t)i * TDW_ELEM_STRIDE + 12;
     Band b = pair_band(ci, ej, cdt, a.d, a.cap);
-    if (b.ghi >= b.glo) {
+    any = b.ghi >= b.glo;
+    if (any) {
       len = b.ghi - b.glo + 1;
       glo = b.glo;
     }
@@ -179,7 +182,7 @@ __global__ void __launch_bounds__(256) count_kernel(AsmArgs a) {
     rank += (lm > len) || (lm == len && m < lane);
   }
   a.hdr[seg * TDW_TJ + rank] = hdr_pack(lane, len, glo);
-  int tot = len, gmin = len ? glo : INT_MAX, gmax = len ? glo + len - 1 : -1, np = len ? 1 : 0;
+  int tot = len, gmin = len ? glo : INT_MAX, gmax = len ? glo + len - 1 : -1, np = any ? 1 : 0;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     tot += __shfl_xor_sync(FULLMASK, tot, o);
@@ -189,8 +192,8 @@ __global__ void __launch_bounds__(256) count_kernel(AsmArgs a) {
   }
   if (lane == 0) {
     a.segcount[seg] = (unsigned long long)tot;
-    if (np) {
-      atomicAdd(a.n_pairs, (unsigned long long)np);
+    if (np) atomicAdd(a.n_pairs, (unsigned long long)np);
+    if (tot) {
       int2* u = &a.unit[(rloc / TDW_TI) * a.ntiles + t];
       atomicMin(&u->x, gmin);
       atomicMax(&u->y, gmax);
@@ -259,6 +262,15 @@ __global__ void __launch_bounds__(128) fill_kernel(AsmArgs a) {
         vu += w[q] * ru[q];
         vw += w[q] * rw[q];
       }
+      if (gg == TDW_NEAR_LAGS) {
+        // lag 2: keep only the coefficient of the KNOWN density of element j
+        // (q if phi_j = 1, u if phi_j = 0); the unknown one is applied by the
+        // solve of the previous step (near structure), so the convolution of
+        // step alpha+1 never waits for the solve of step alpha.
+        const double pj = a.phi[j];
+        vu = pj == 1.0 ? vu : 0.0;
+        vw = pj == 1.0 ? 0.0 : vw;
+      }
       coef[off + lane] = make_double2(vu, vw);
     }
     off += __popc(m);
@@ -309,77 +321,115 @@ __global__ void unit_layout_kernel(const unsigned long long* segcount, const uin
   if (lane == 31) atomicMax(max_rel, x);
 }
 
-struct StepArgs {
+struct NearArgs {
   const double* elem;
   const double* phi;
-  int ns, ntiles, d;
-  double c, dt, K, w0;
-  int* acol;      // [TDW_ELL_MAX][ns]
+  int ns, ntiles, d, cap;
+  double c, dt, K;
+  int* ncol;      // [TDW_NEAR_MAX][ns]
+  double* nval;   // [TDW_NEAR_MAX][ns]: coefficient of the unknown density at lag 2
+  int* acol;      // [TDW_ELL_MAX][ns]  lag-1 step matrix (pairs with V^(1))
   double* aval;   // [TDW_ELL_MAX][ns]
   double* adiag;  // [ns]
-  int* flags;     // [4]: ell width max at [2], overflow at [3]
+  int* flags;     // [4]: [2] max near width, [3] overflow
+  int* ell_w;
   unsigned long long* bound_bits;
   unsigned long long* nnz;
+  unsigned long long* n_near;
+  unsigned long long* n_evals;
 };
 
-// lag-1 step matrix A = w0 (W1 phi - U1 (1 - phi)) over all rows (replicated
-// on every rank): exactly the pairs whose band starts at gamma = 1.
+// Rows of the lag-1 step matrix and of the lag-2 "unknown" coupling, all rows
+// (replicated on every rank).  With V^(1) = w0 U^(1), V^(2) = w0 U^(2) + w1 U^(1)
+// (U^(g) = 0 for g < arrival; zero outside the pair's band, as in the store):
+//   A_ij   = V_W^(1) phi_j - V_U^(1) (1 - phi_j)      (build_step_matrix, marching.py:279-289)
+//   N_ij   = -V_W^(2) if phi_j = 1 else V_U^(2)       (b_i += N_ij x_j^(alpha-2))
 template <int D, bool BM>
-__global__ void __launch_bounds__(128) stepmat_kernel(StepArgs a) {
+__global__ void __launch_bounds__(128) near_kernel(NearArgs a) {
   const int lane = threadIdx.x & 31;
   const int i = (int)(((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
   if (i >= a.ns) return;
   const double cdt = a.c * a.dt;
+  double w[D + 2];
+  bspline_weights(D, w);
   const double* pi = a.elem + (size_t)i * TDW_ELEM_STRIDE;
   double ci[3] = {pi[12], pi[13], pi[14]};
   double nx[3] = {-pi[9], -pi[10], -pi[11]};
-  int cnt = 0;
+  int cnt = 0, acnt = 0;
   double diag = 0.0, offsum = 0.0;
+  long long nev = 0;
   for (int t = 0; t < a.ntiles; ++t) {
     const int j = t * TDW_TJ + lane;
-    bool take = false;
     Elem ej;
+    Band b{0, -1, 1};
+    bool cand = false;
     if (j < a.ns) {
       load_elem(a.elem, j, ej);
       double dx = ci[0] - ej.c[0], dy = ci[1] - ej.c[1], dz = ci[2] - ej.c[2];
       double dcc = sqrt(dx * dx + dy * dy + dz * dz);
-      if (dcc - ej.rad <= 2.0 * cdt * (1.0 + 1e-9)) {
-        Band b = pair_band(ci, ej, cdt, a.d, 1 << 30);
-        take = (b.glo == 1);
+      if (dcc - ej.rad <= (TDW_NEAR_LAGS + 1) * cdt * (1.0 + 1e-9)) {
+        b = pair_band(ci, ej, cdt, a.d, a.cap);
+        cand = true;
       }
     }
-    const unsigned m = __ballot_sync(FULLMASK, take);
-    const int pos = cnt + __popc(m & ((1u << lane) - 1u));
-    if (take) {
+    const bool has1 = cand && b.glo <= 1 && b.ghi >= 1;
+    const bool has2 = cand && b.glo <= 2 && b.ghi >= 2;
+    const unsigned m1 = __ballot_sync(FULLMASK, has1);
+    const unsigned m2 = __ballot_sync(FULLMASK, has2);
+    const int apos = acnt + __popc(m1 & ((1u << lane) - 1u));
+    const int pos = cnt + __popc(m2 & ((1u << lane) - 1u));
+    if (has1 || has2) {
       PairGeom g;
       pair_geom<BM>(ci, ej.v0, ej.v1, ej.v2, ej.n, nx, g);
-      double u, w;
-      coeff_eval<D, BM>(g, 1.0 * a.c * a.dt, a.K, u, w);
+      double u1 = 0.0, w1 = 0.0, u2 = 0.0, w2 = 0.0;
+      if (b.arr <= 1) { coeff_eval<D, BM>(g, 1.0 * a.c * a.dt, a.K, u1, w1); ++nev; }
+      if (b.arr <= 2) { coeff_eval<D, BM>(g, 2.0 * a.c * a.dt, a.K, u2, w2); ++nev; }
       const double pj = a.phi[j];
-      const double val = a.w0 * (w * pj - u * (1.0 - pj));
-      if (pos < TDW_ELL_MAX) {
-        a.acol[(size_t)pos * a.ns + i] = j;
-        a.aval[(size_t)pos * a.ns + i] = val;
+      if (has1) {
+        const double v1u = w[0] * u1, v1w = w[0] * w1;
+        const double val = v1w * pj - v1u * (1.0 - pj);
+        if (apos < TDW_ELL_MAX) {
+          a.acol[(size_t)apos * a.ns + i] = j;
+          a.aval[(size_t)apos * a.ns + i] = val;
+        }
+        if (j == i) diag = val;
+        else offsum += fabs(val);
       }
-      if (j == i) diag = val;
-      else offsum += fabs(val);
+      if (has2) {
+        double v2u = 0.0, v2w = 0.0;
+        v2u = w[0] * u2 + w[1] * u1;
+        v2w = w[0] * w2 + w[1] * w1;
+        if (pos < TDW_NEAR_MAX) {
+          a.ncol[(size_t)pos * a.ns + i] = j;
+          a.nval[(size_t)pos * a.ns + i] = pj == 1.0 ? -v2w : v2u;
+        }
+      }
     }
-    cnt += __popc(m);
+    cnt += __popc(m2);
+    acnt += __popc(m1);
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     diag += __shfl_xor_sync(FULLMASK, diag, o);
     offsum += __shfl_xor_sync(FULLMASK, offsum, o);
+    nev += __shfl_xor_sync(FULLMASK, nev, o);
   }
-  for (int p = cnt + lane; p < TDW_ELL_MAX; p += 32) {
+  for (int p = cnt + lane; p < TDW_NEAR_MAX; p += 32) {
+    a.ncol[(size_t)p * a.ns + i] = i;
+    a.nval[(size_t)p * a.ns + i] = 0.0;
+  }
+  for (int p = acnt + lane; p < TDW_ELL_MAX; p += 32) {
     a.acol[(size_t)p * a.ns + i] = i;
     a.aval[(size_t)p * a.ns + i] = 0.0;
   }
   if (lane == 0) {
     a.adiag[i] = diag;
     atomicMax(&a.flags[2], cnt);
-    if (cnt > TDW_ELL_MAX) atomicExch(&a.flags[3], 1);
-    atomicAdd(a.nnz, (unsigned long long)cnt);
+    atomicMax(a.ell_w, acnt);
+    if (cnt > TDW_NEAR_MAX || acnt > TDW_ELL_MAX) atomicExch(&a.flags[3], 1);
+    atomicAdd(a.nnz, (unsigned long long)acnt);
+    atomicAdd(a.n_near, (unsigned long long)cnt);
+    atomicAdd(a.n_evals, (unsigned long long)nev);
     double bound = diag != 0.0 ? offsum / fabs(diag) : 1e300;
     atomicMax(a.bound_bits, (unsigned long long)__double_as_longlong(bound));
   }
@@ -393,10 +443,10 @@ static void launch_fill(const AsmArgs& a, long long nseg, cudaStream_t st) {
 }
 
 template <int D, bool BM>
-static void launch_step(const StepArgs& a, cudaStream_t st) {
+static void launch_near(const NearArgs& a, cudaStream_t st) {
   const int threads = 128;
   long long blocks = ((long long)a.ns * 32 + threads - 1) / threads;
-  stepmat_kernel<D, BM><<<(unsigned)blocks, threads, 0, st>>>(a);
+  near_kernel<D, BM><<<(unsigned)blocks, threads, 0, st>>>(a);
 }
 
 __global__ void fill_unit_init(int2* u, long long n) {
@@ -426,7 +476,11 @@ static int choose_conv_schedule(tdw_problem* pb) {
                         std::to_string(hist_bytes) + " B) exceeds shared memory");
   pb->conv_stage_bytes = cap;
   pb->conv_nstages = 4;
-  const int G = ctx->num_sms;
+  // keep the solver's SMs free (overlap) unless the bandwidth they would add to
+  // the convolution is worth more than the solve time (~100 us per step)
+  const double conv_est = (double)(pb->n_band * 16) / 6.0e12;
+  const bool reserve = conv_est * pb->sp_cl / ctx->num_sms < 100e-6;
+  const int G = std::max(1, ctx->num_sms - (reserve ? pb->sp_cl : 0));
   // items = (I-block, tile split); pick the split count that balances the waves
   int bestS = 1;
   double best = -1.0;
@@ -456,13 +510,13 @@ int tdw_assemble_impl(tdw_problem* pb) {
   const long long nunit = (long long)pb->n_iblk * pb->ntiles;
   uint32_t* d_hdr_tmp = nullptr;
   unsigned long long* d_segcnt = nullptr;
-  unsigned long long* d_cnt = nullptr;  // {n_evals, n_pairs, nnz, bound_bits, max_rel}
+  unsigned long long* d_cnt = nullptr;  // {n_evals, n_pairs, nnz, bound_bits, max_rel, n_near, near_evals}
   TDW_CUDA(ctx, cudaMalloc(&d_hdr_tmp, sizeof(uint32_t) * nseg * TDW_TJ));
   TDW_CUDA(ctx, cudaMalloc(&d_segcnt, sizeof(unsigned long long) * nseg));
   TDW_CUDA(ctx, cudaMalloc(&pb->d_unit, sizeof(int2) * nunit));
   TDW_CUDA(ctx, cudaMalloc(&pb->d_unit_off, sizeof(unsigned long long) * (nunit + 1)));
-  TDW_CUDA(ctx, cudaMalloc(&d_cnt, sizeof(unsigned long long) * 5));
-  TDW_CUDA(ctx, cudaMemsetAsync(d_cnt, 0, sizeof(unsigned long long) * 5, st));
+  TDW_CUDA(ctx, cudaMalloc(&d_cnt, sizeof(unsigned long long) * 8));
+  TDW_CUDA(ctx, cudaMemsetAsync(d_cnt, 0, sizeof(unsigned long long) * 8, st));
   TDW_CUDA(ctx, cudaMemsetAsync(pb->d_flags, 0, sizeof(int) * 4, st));
   fill_unit_init<<<256, 256, 0, st>>>(pb->d_unit, nunit);
 
@@ -535,6 +589,7 @@ int tdw_assemble_impl(tdw_problem* pb) {
   }
   a.unit_off = pb->d_unit_off;
   a.units = pb->d_units;
+  a.phi = pb->d_phi;
   TDW_CUDA(ctx, cudaEventRecord(f0, st));
   const bool bm = pb->bie == TDW_BIE_BMBIE;
   if (pb->d == 1) { if (bm) launch_fill<1, true>(a, nseg, st); else launch_fill<1, false>(a, nseg, st); }
@@ -543,48 +598,64 @@ int tdw_assemble_impl(tdw_problem* pb) {
   TDW_CUDA(ctx, cudaGetLastError());
   TDW_CUDA(ctx, cudaEventRecord(f1, st));
 
-  // lag-1 step matrix (all rows)
+  // near part (lags 1, 2) and lag-1 step matrix, all rows
   TDW_CUDA(ctx, cudaMalloc(&pb->d_acol, sizeof(int) * (size_t)TDW_ELL_MAX * pb->ns));
   TDW_CUDA(ctx, cudaMalloc(&pb->d_aval, sizeof(double) * (size_t)TDW_ELL_MAX * pb->ns));
   TDW_CUDA(ctx, cudaMalloc(&pb->d_adiag, sizeof(double) * pb->ns));
-  StepArgs s{};
+  TDW_CUDA(ctx, cudaMalloc(&pb->d_ncol, sizeof(int) * (size_t)TDW_NEAR_MAX * pb->ns));
+  TDW_CUDA(ctx, cudaMalloc(&pb->d_nval, sizeof(double) * (size_t)TDW_NEAR_MAX * pb->ns));
+  int* d_ellw = nullptr;
+  TDW_CUDA(ctx, cudaMalloc(&d_ellw, sizeof(int)));
+  TDW_CUDA(ctx, cudaMemsetAsync(d_ellw, 0, sizeof(int), st));
+  NearArgs s{};
   s.elem = pb->d_elem;
   s.phi = pb->d_phi;
   s.ns = pb->ns;
   s.ntiles = pb->ntiles;
   s.d = pb->d;
+  s.cap = pb->cap;
   s.c = pb->c;
   s.dt = pb->dt;
   s.K = pb->K;
-  s.w0 = pb->d == 1 ? 1.0 : (pb->d == 2 ? 0.5 : 1.0 / 6.0);
+  s.ncol = pb->d_ncol;
+  s.nval = pb->d_nval;
   s.acol = pb->d_acol;
   s.aval = pb->d_aval;
   s.adiag = pb->d_adiag;
   s.flags = pb->d_flags;
+  s.ell_w = d_ellw;
   s.bound_bits = d_cnt + 3;
   s.nnz = d_cnt + 2;
-  if (pb->d == 1) { if (bm) launch_step<1, true>(s, st); else launch_step<1, false>(s, st); }
-  if (pb->d == 2) { if (bm) launch_step<2, true>(s, st); else launch_step<2, false>(s, st); }
-  if (pb->d == 3) { if (bm) launch_step<3, true>(s, st); else launch_step<3, false>(s, st); }
+  s.n_near = d_cnt + 5;
+  s.n_evals = d_cnt + 6;
+  if (pb->d == 1) { if (bm) launch_near<1, true>(s, st); else launch_near<1, false>(s, st); }
+  if (pb->d == 2) { if (bm) launch_near<2, true>(s, st); else launch_near<2, false>(s, st); }
+  if (pb->d == 3) { if (bm) launch_near<3, true>(s, st); else launch_near<3, false>(s, st); }
   TDW_CUDA(ctx, cudaGetLastError());
   TDW_CUDA(ctx, cudaEventRecord(e1, st));
   TDW_CUDA(ctx, cudaStreamSynchronize(st));
   cudaFree(d_hdr_tmp);
   cudaFree(d_segcnt);
 
-  unsigned long long hc[5];
+  unsigned long long hc[8];
   TDW_CUDA(ctx, cudaMemcpy(hc, d_cnt, sizeof(hc), cudaMemcpyDeviceToHost));
   TDW_CUDA(ctx, cudaMemcpy(hflags, pb->d_flags, sizeof(hflags), cudaMemcpyDeviceToHost));
+  int hellw = 0;
+  TDW_CUDA(ctx, cudaMemcpy(&hellw, d_ellw, sizeof(int), cudaMemcpyDeviceToHost));
   cudaFree(d_cnt);
+  cudaFree(d_ellw);
   pb->n_evals = (int64_t)hc[0];
+  pb->n_near = (int64_t)hc[5];
+  pb->n_near_evals = (int64_t)hc[6];
+  pb->near_w = hflags[2];
   pb->n_pairs = (int64_t)hc[1];
   pb->step_nnz = (int)hc[2];
   double bound;
   memcpy(&bound, &hc[3], sizeof(bound));
   pb->jac_bound = bound;
-  pb->ell_w = hflags[2];
+  pb->ell_w = hellw;
   if (hflags[3] == 1)
-    return tdw_fail(ctx, TDW_ERR_LIMIT, "lag-1 step matrix has more than 64 entries in a row");
+    return tdw_fail(ctx, TDW_ERR_LIMIT, "near structure: more than the supported pairs within 2 c dt of a row");
   if (!(bound < 0.9))
     return tdw_fail(ctx, TDW_ERR_SINGULAR,
                     "step matrix is not diagonally dominant (Jacobi bound " +
@@ -603,6 +674,12 @@ int tdw_assemble_impl(tdw_problem* pb) {
   cudaEventDestroy(f0);
   cudaEventDestroy(f1);
 
+  // cluster solver first: its CTAs' SMs are kept free of convolution CTAs so
+  // the far convolution of the next step overlaps the solve
+  {
+    int src = tdw_setup_cluster_solver(pb);
+    if (src) return src;
+  }
   // convolution schedule (persistent CTAs, unit list per CTA)
   {
     int rc = choose_conv_schedule(pb);
@@ -628,11 +705,10 @@ int tdw_assemble_impl(tdw_problem* pb) {
     TDW_CUDA(ctx, cudaMemcpy(pb->d_sched_off, soff.data(), sizeof(unsigned) * (G + 1), cudaMemcpyHostToDevice));
     pb->nsplit = S;
     cudaFree(pb->d_bpart);
-    TDW_CUDA(ctx, cudaMalloc(&pb->d_bpart, sizeof(double) * (size_t)S * pb->rows_per_rank));
-    TDW_CUDA(ctx, cudaMemset(pb->d_bpart, 0, sizeof(double) * (size_t)S * pb->rows_per_rank));
+    TDW_CUDA(ctx, cudaMalloc(&pb->d_bpart, 2 * sizeof(double) * (size_t)S * pb->rows_per_rank));
+    TDW_CUDA(ctx, cudaMemset(pb->d_bpart, 0, 2 * sizeof(double) * (size_t)S * pb->rows_per_rank));
+    TDW_CUDA(ctx, cudaMalloc(&pb->d_bnear, 2 * sizeof(double) * (size_t)pb->ns));
   }
-  int src = tdw_setup_cluster_solver(pb);
-  if (src) return src;
   pb->store_bytes = (int64_t)(total_bytes + sizeof(unsigned long long) * (nunit + 1) + sizeof(int2) * nunit);
   pb->assembled = true;
   return TDW_OK;

@@ -261,47 +261,6 @@ __global__ void reduce_parts_kernel(const double* __restrict__ bpart, int nsplit
   }
 }
 
-struct SolveArgs {
-  const double* bpart;  // nsplit > 0: sum partials here (single GPU); else read b
-  double* b;
-  double* x;            // [2][ns]
-  const int* __restrict__ acol;
-  const double* __restrict__ aval;
-  const double* __restrict__ adiag;
-  int ell_w, iters;
-  const double* __restrict__ phi;
-  const int* __restrict__ perm;
-  const double* __restrict__ uk;
-  const double* __restrict__ qk;
-  double2* hist;
-  int hstride, pad;
-  double* red;          // [3][gridDim]
-  unsigned* bar;        // {count, generation}
-  int* flags;           // {status, n_steps, err_step, -}
-  double* rhs;          // optional (nt-1, ns) original order
-  double threshold;
-  int ns, nsplit, rows_loc, alpha, nt;
-};
-
-__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned nblocks) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    volatile unsigned* gen = bar + 1;
-    const unsigned g = *gen;
-    __threadfence();
-    const unsigned arrived = atomicAdd(bar, 1u);
-    if (arrived == nblocks - 1) {
-      atomicExch(bar, 0u);
-      __threadfence();
-      atomicAdd(bar + 1, 1u);
-    } else {
-      while (*gen == g) __nanosleep(20);
-    }
-    __threadfence();
-  }
-  __syncthreads();
-}
-
 __device__ __forceinline__ double block_reduce_sum(double v, double* sh) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULLMASK, v, o);
@@ -328,105 +287,6 @@ __device__ __forceinline__ double block_reduce_max(double v, double* sh) {
   return t;
 }
 
-// Cooperative (all CTAs co-resident) per-step solve + history update.
-__global__ void __launch_bounds__(256) solve_kernel(SolveArgs a) {
-  __shared__ double sh[32];
-  if (*(volatile int*)&a.flags[0] != 0) return;  // every CTA sees the same flag
-  const int nth = gridDim.x * blockDim.x;
-  const int tid = blockIdx.x * blockDim.x + threadIdx.x;
-  const int beta0 = a.alpha - 1;
-  double* x0 = a.x;
-  double* x1 = a.x + a.ns;
-  // right-hand side (+ first Jacobi iterate)
-  for (int i = tid; i < a.ns; i += nth) {
-    double bi;
-    if (a.nsplit > 0) {
-      bi = 0.0;
-      for (int s = 0; s < a.nsplit; ++s) bi += a.bpart[(size_t)s * a.rows_loc + i];
-      a.b[i] = bi;
-    } else {
-      bi = __ldcg(a.b + i);
-    }
-    x0[i] = bi / a.adiag[i];
-    if (a.rhs) a.rhs[(size_t)beta0 * a.ns + a.perm[i]] = bi;
-  }
-  grid_barrier(a.bar, gridDim.x);
-  // Jacobi sweeps (strictly diagonally dominant A, bound < 0.9 checked at assembly)
-  for (int it = 0; it < a.iters; ++it) {
-    const double* xin = (it & 1) ? x1 : x0;
-    double* xout = (it & 1) ? x0 : x1;
-    for (int i = tid; i < a.ns; i += nth) {
-      double acc = __ldcg(a.b + i);
-      for (int k = 0; k < a.ell_w; ++k) {
-        const int j = a.acol[(size_t)k * a.ns + i];
-        if (j != i) acc -= a.aval[(size_t)k * a.ns + i] * __ldcg(xin + j);
-      }
-      xout[i] = acc / a.adiag[i];
-    }
-    grid_barrier(a.bar, gridDim.x);
-  }
-  const double* xf = (a.iters & 1) ? x1 : x0;
-  // residual and blow-up reductions
-  double r2 = 0.0, b2 = 0.0, xm = 0.0;
-  for (int i = tid; i < a.ns; i += nth) {
-    const double bi = __ldcg(a.b + i);
-    double acc = -bi;
-    for (int k = 0; k < a.ell_w; ++k)
-      acc += a.aval[(size_t)k * a.ns + i] * __ldcg(xf + a.acol[(size_t)k * a.ns + i]);
-    r2 += acc * acc;
-    b2 += bi * bi;
-    xm = fmax(xm, fabs(__ldcg(xf + i)));
-  }
-  r2 = block_reduce_sum(r2, sh);
-  b2 = block_reduce_sum(b2, sh);
-  xm = block_reduce_max(xm, sh);
-  if (threadIdx.x == 0) {
-    a.red[blockIdx.x] = r2;
-    a.red[gridDim.x + blockIdx.x] = b2;
-    a.red[2 * gridDim.x + blockIdx.x] = xm;
-  }
-  grid_barrier(a.bar, gridDim.x);
-  __shared__ int s_bad;
-  __shared__ double s_xmax;
-  if (threadIdx.x == 0) {
-    double R = 0.0, B = 0.0, X = 0.0;
-    for (int k = 0; k < (int)gridDim.x; ++k) {
-      R += __ldcg(a.red + k);
-      B += __ldcg(a.red + gridDim.x + k);
-      X = fmax(X, __ldcg(a.red + 2 * gridDim.x + k));
-    }
-    s_bad = sqrt(R) > 1e-10 * fmax(sqrt(B), 1e-300);
-    s_xmax = X;
-  }
-  __syncthreads();
-  if (s_bad) {
-    if (tid == 0) {
-      a.flags[2] = a.alpha;
-      atomicExch(&a.flags[0], 2);  // residual failure: the reference raises here
-    }
-    return;
-  }
-  // finalize_step: promote x into u/q by phi, then the next step's known part
-  for (int j = tid; j < a.ns; j += nth) {
-    const int o = a.perm[j];
-    const double xj = __ldcg(xf + j);
-    const double ph = a.phi[j];
-    const size_t kb = (size_t)beta0 * a.ns + o;
-    const double qv = ph == 1.0 ? a.qk[kb] : xj;
-    const double uv = ph == 1.0 ? xj : a.uk[kb];
-    a.hist[(size_t)j * a.hstride + a.pad + beta0] = make_double2(qv, uv);
-    if (beta0 + 1 < a.nt - 1 && !(s_xmax > a.threshold)) {
-      const size_t kn = (size_t)(beta0 + 1) * a.ns + o;
-      a.hist[(size_t)j * a.hstride + a.pad + beta0 + 1] =
-          make_double2(ph * a.qk[kn], (1.0 - ph) * a.uk[kn]);
-    }
-  }
-  if (tid == 0) {
-    a.flags[1] = a.alpha;
-    if (s_xmax > a.threshold) atomicExch(&a.flags[0], 1);  // "unstable"
-  }
-}
-
 // ---------------------------------------------------------------------------
 // Cluster solver: one thread-block cluster (CL <= 16 CTAs, 1024 threads each)
 // owns the whole lag-1 system.  CTA r holds rows [r*R, r*R+R): its CSR rows
@@ -435,25 +295,6 @@ __global__ void __launch_bounds__(256) solve_kernel(SolveArgs a) {
 // Jacobi sweep ends in one cluster barrier.  Sweeps stop when
 // max|dx| <= 1e-15 max|x| (decision read by every CTA from every CTA's
 // partials, so all CTAs agree), capped by the bound-derived count.
-struct ClusterSolveArgs {
-  const double* bpart;
-  double* b;
-  const int* __restrict__ sp_rowptr;        // [CL][R+1], relative to the CTA's slice
-  const long long* __restrict__ sp_nnzoff;  // [CL+1]
-  const int* __restrict__ sp_col;           // packed (owner << 24) | local
-  const double* __restrict__ sp_val;
-  const double* __restrict__ diag;          // [ns]
-  const double* __restrict__ phi;
-  const int* __restrict__ perm;
-  const double* __restrict__ uk;
-  const double* __restrict__ qk;
-  double2* hist;
-  int* flags;
-  double* rhs;
-  double threshold;
-  int hstride, pad, ns, nsplit, rows_loc, alpha, nt, R, maxit;
-};
-
 __device__ __forceinline__ void block_reduce2_max(double& a, double& b, double* sh) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -472,13 +313,47 @@ __device__ __forceinline__ void block_reduce2_max(double& a, double& b, double* 
   }
 }
 
+struct ClusterSolveArgs {
+  const double* bpart;                      // far partials of this step (nsplit > 0)
+  double* b;                                // all-gathered far rhs (nsplit == 0)
+  const double* bnear_in;                   // lag-2 unknown term of this step (from the previous solve)
+  double* bnear_out;                        // same for the next step
+  const int* __restrict__ sp_rowptr;        // [CL][R+1], relative to the CTA's slice
+  const long long* __restrict__ sp_nnzoff;  // [CL+1]
+  const int* __restrict__ sp_col;           // packed (owner << 24) | local
+  const double* __restrict__ sp_val;
+  const double* __restrict__ diag;          // [ns]
+  const int* __restrict__ ncol;             // [near_w][ns] packed (owner << 24) | local
+  const double* __restrict__ nval;          // [near_w][ns]
+  const double* __restrict__ phi;
+  const int* __restrict__ perm;
+  const double* __restrict__ uk;
+  const double* __restrict__ qk;
+  double2* hist;
+  int* flags;
+  double* rhs;
+  double threshold;
+  int hstride, pad, ns, nsplit, rows_loc, alpha, nt, R, maxit, near_w;
+};
+
+// K3/K4: one thread-block cluster (CL <= 16 CTAs, 1024 threads) owns the whole
+// lag-1 system.  CTA r holds rows [r*R, r*R+R): its off-diagonal CSR rows,
+// diagonal, b and a double-buffered x slice live in shared memory; x of the
+// other CTAs is read through distributed shared memory; every Jacobi sweep
+// ends in one cluster barrier.  Sweeps stop once max|dx| <= 1e-15 max|x| (tested
+// every 4th sweep; every CTA reads every CTA's partials, so all agree), capped
+// by the bound-derived count.  Then: residual test (marching.py:331-333),
+// finalize_step (:239-242), blow-up detector (:336-338), and the lag-2 term of
+// the unknown density for the next step, b'_i = sum_j N_ij x_j, while x is
+// still in shared memory.
 __global__ void __launch_bounds__(1024, 1) solve_cluster_kernel(ClusterSolveArgs a) {
   namespace cg = cooperative_groups;
   cg::cluster_group cl = cg::this_cluster();
   extern __shared__ __align__(16) unsigned char smraw[];
   __shared__ double shred[64];
-  __shared__ double red[2][2];   // per-sweep (max|dx|, max|x|), parity double buffer
+  __shared__ double red[2][2];   // per-check (max|dx|, max|x|), parity double buffer
   __shared__ double red2[4];     // (r^2, b^2, max|x|)
+  __shared__ int s_stop;
   if (*(volatile int*)&a.flags[0] != 0) return;  // identical in every CTA
   const int cr = (int)cl.block_rank();
   const int CL = (int)cl.num_blocks();
@@ -509,11 +384,13 @@ __global__ void __launch_bounds__(1024, 1) solve_cluster_kernel(ClusterSolveArgs
     } else {
       bi = __ldcg(a.b + gi);
     }
+    bi += a.bnear_in[gi];
     bs[i] = bi;
     dg[i] = a.diag[gi];
     xs[i] = bi / dg[i];
     if (a.rhs) a.rhs[(size_t)beta0 * a.ns + a.perm[gi]] = bi;
   }
+  if (tid == 0) s_stop = 0;
   cl.sync();
   int cur = 0;
   for (int it = 1; it <= a.maxit; ++it) {
@@ -533,32 +410,25 @@ __global__ void __launch_bounds__(1024, 1) solve_cluster_kernel(ClusterSolveArgs
       dmax = fmax(dmax, fabs(xn - src[i]));
       xmax = fmax(xmax, fabs(xn));
     }
-    const bool check = (it & 3) == 0 || it == a.maxit;  // convergence test every 4th sweep
+    const bool check = (it & 3) == 0 && it < a.maxit;
     if (check) {
       block_reduce2_max(dmax, xmax, shred);
       if (tid == 0) { red[(it >> 2) & 1][0] = dmax; red[(it >> 2) & 1][1] = xmax; }
     }
     cl.sync();
     cur ^= 1;
-    if (check && it < a.maxit) {
-      double D = 0.0, X = 0.0;
-      double rv[2 * 16];
-#pragma unroll
-      for (int q = 0; q < 16; ++q) {
-        if (q < CL) {
+    if (check) {
+      if (tid == 0) {
+        double D = 0.0, X = 0.0;
+        for (int q = 0; q < CL; ++q) {
           const double* rr = cl.map_shared_rank(&red[(it >> 2) & 1][0], q);
-          rv[2 * q] = rr[0];
-          rv[2 * q + 1] = rr[1];
+          D = fmax(D, rr[0]);
+          X = fmax(X, rr[1]);
         }
+        s_stop = D <= 1e-15 * X;
       }
-#pragma unroll
-      for (int q = 0; q < 16; ++q) {
-        if (q < CL) {
-          D = fmax(D, rv[2 * q]);
-          X = fmax(X, rv[2 * q + 1]);
-        }
-      }
-      if (D <= 1e-15 * X) break;
+      __syncthreads();
+      if (s_stop) break;
     }
   }
   const double* xf = xs + cur * R;
@@ -580,6 +450,18 @@ __global__ void __launch_bounds__(1024, 1) solve_cluster_kernel(ClusterSolveArgs
   xm = block_reduce_max(xm, shred);
   if (tid == 0) { red2[0] = r2; red2[1] = b2; red2[2] = xm; }
   cl.sync();
+  // lag-2 term of the unknown density for the next step (x still in shared memory)
+  for (int i = tid; i < nr; i += nth) {
+    const int gi = r0 + i;
+    double acc = 0.0;
+    for (int k = 0; k < a.near_w; ++k) {
+      const int c = a.ncol[(size_t)k * a.ns + gi];
+      const int owner = c >> 24, loc = c & 0xffffff;
+      const double xv = owner == cr ? xf[loc] : *cl.map_shared_rank(xf + loc, owner);
+      acc += a.nval[(size_t)k * a.ns + gi] * xv;
+    }
+    a.bnear_out[gi] = acc;
+  }
   double RR = 0.0, BB = 0.0, XM = 0.0;
   for (int q = 0; q < CL; ++q) {
     const double* rr = cl.map_shared_rank(red2, q);
@@ -605,11 +487,6 @@ __global__ void __launch_bounds__(1024, 1) solve_cluster_kernel(ClusterSolveArgs
     const double qv = ph == 1.0 ? a.qk[kb] : xj;
     const double uv = ph == 1.0 ? xj : a.uk[kb];
     a.hist[(size_t)j * a.hstride + a.pad + beta0] = make_double2(qv, uv);
-    if (beta0 + 1 < a.nt - 1 && !unstable) {
-      const size_t kn = (size_t)(beta0 + 1) * a.ns + o;
-      a.hist[(size_t)j * a.hstride + a.pad + beta0 + 1] =
-          make_double2(ph * a.qk[kn], (1.0 - ph) * a.uk[kn]);
-    }
   }
   if (cr == 0 && tid == 0) {
     a.flags[1] = a.alpha;
@@ -617,16 +494,24 @@ __global__ void __launch_bounds__(1024, 1) solve_cluster_kernel(ClusterSolveArgs
   }
 }
 
-// hist[j][pad + 0] = known part of step beta = 0 (the loop writes the later ones)
+// hist[j][pad + beta] = known part (phi q_known, (1-phi) u_known) of every
+// step; the solve of step beta+1 overwrites it with the full (q, u).  Zero pad
+// for beta < 0.
 __global__ void init_hist_kernel(double2* hist, int hstride, int pad, int ns, int nt,
                                  const double* phi, const int* perm, const double* uk,
                                  const double* qk) {
-  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < ns; j += gridDim.x * blockDim.x) {
-    double2* h = hist + (size_t)j * hstride;
-    for (int s = 0; s < hstride; ++s) h[s] = make_double2(0.0, 0.0);
-    const int o = perm[j];
-    const double ph = phi[j];
-    h[pad] = make_double2(ph * qk[o], (1.0 - ph) * uk[o]);
+  const long long n = (long long)ns * hstride;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int j = (int)(e / hstride), sl = (int)(e % hstride);
+    const int beta = sl - pad;
+    double2 v = make_double2(0.0, 0.0);
+    if (beta >= 0 && beta < nt - 1) {
+      const double ph = phi[j];
+      const size_t o = (size_t)beta * ns + perm[j];
+      v = make_double2(ph * qk[o], (1.0 - ph) * uk[o]);
+    }
+    hist[e] = v;
   }
 }
 
@@ -725,66 +610,74 @@ namespace {
 struct LoopPlan {
   CUtensorMap hmap;
   ConvArgs c;
-  SolveArgs s;
   ClusterSolveArgs cs;
   dim3 cgrid;
   size_t smem;
   bool multi;
 };
 
-// Enqueue one complete time loop (init + nt-1 steps) on the ctx stream.  Used
-// directly and under stream capture (one CUDA graph per loop configuration).
+// Enqueue one complete time loop.  Two streams: the far convolution F(alpha)
+// runs on the side stream as soon as the solve of step alpha-2 has finalized
+// the history it reads (lags >= 3; lag 1 = known data written up front; lag 2
+// = known component only), so F(alpha+1) overlaps the solve of step alpha.
+//   F(alpha)      waits solve(alpha-2)            writes bpart[alpha & 1]
+//   solve(alpha)  waits F(alpha), solve(alpha-1)  reads bpart[alpha & 1], bnear[alpha & 1]
+// Also used under stream capture (one CUDA graph per loop configuration).
 int enqueue_loop(tdw_problem* pb, LoopPlan& L, cudaEvent_t* ev_conv) {
   tdw_ctx* ctx = pb->ctx;
-  cudaStream_t st = ctx->stream;
+  cudaStream_t st = ctx->stream, sc = pb->side;
+  const int nt = pb->nt;
   TDW_CUDA(ctx, cudaMemsetAsync(pb->d_flags, 0, sizeof(int) * 4, st));
-  init_hist_kernel<<<(pb->ns + 255) / 256, 256, 0, st>>>(pb->d_hist, pb->hstride, pb->pad, pb->ns,
-                                                         pb->nt, pb->d_phi, pb->d_perm, pb->d_uk,
-                                                         pb->d_qk);
+  TDW_CUDA(ctx, cudaMemsetAsync(pb->d_bnear, 0, sizeof(double) * 2 * (size_t)pb->ns, st));
+  init_hist_kernel<<<2 * ctx->num_sms, 256, 0, st>>>(pb->d_hist, pb->hstride, pb->pad, pb->ns, nt,
+                                                    pb->d_phi, pb->d_perm, pb->d_uk, pb->d_qk);
   TDW_CUDA(ctx, cudaGetLastError());
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeCooperative;
-  attr[0].val.cooperative = 1;
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(pb->solve_grid);
-  cfg.blockDim = dim3(256);
-  cfg.dynamicSmemBytes = 0;
-  cfg.stream = st;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
   cudaLaunchAttribute cattr[1];
   cattr[0].id = cudaLaunchAttributeClusterDimension;
-  cattr[0].val.clusterDim.x = pb->sp_cl > 0 ? pb->sp_cl : 1;
+  cattr[0].val.clusterDim.x = pb->sp_cl;
   cattr[0].val.clusterDim.y = 1;
   cattr[0].val.clusterDim.z = 1;
   cudaLaunchConfig_t ccfg = {};
-  ccfg.gridDim = dim3(pb->sp_cl > 0 ? pb->sp_cl : 1);
+  ccfg.gridDim = dim3(pb->sp_cl);
   ccfg.blockDim = dim3(1024);
   ccfg.dynamicSmemBytes = pb->sp_smem;
   ccfg.stream = st;
   ccfg.attrs = cattr;
   ccfg.numAttrs = 1;
-  for (int alpha = 1; alpha < pb->nt; ++alpha) {
+  cudaEvent_t* evS = pb->ev_solve.data();  // solve(alpha) done
+  cudaEvent_t* evF = pb->ev_conv.data();   // F(alpha) done
+  TDW_CUDA(ctx, cudaEventRecord(pb->ev_fork, st));
+  TDW_CUDA(ctx, cudaStreamWaitEvent(sc, pb->ev_fork, 0));
+  const size_t nb = (size_t)pb->nsplit * pb->rows_per_rank;
+  for (int alpha = 1; alpha < nt; ++alpha) {
+    // far convolution of step alpha on the side stream
+    if (alpha >= 3) TDW_CUDA(ctx, cudaStreamWaitEvent(sc, evS[alpha - 2], 0));
     L.c.alpha = alpha;
-    L.s.alpha = alpha;
-    if (ev_conv) TDW_CUDA(ctx, cudaEventRecordWithFlags(ev_conv[2 * (alpha - 1)], st, cudaEventRecordExternal));
-    conv_kernel<<<L.cgrid, TDW_CONV_THREADS, L.smem, st>>>(L.c, L.hmap);
-    if (ev_conv) TDW_CUDA(ctx, cudaEventRecordWithFlags(ev_conv[2 * (alpha - 1) + 1], st, cudaEventRecordExternal));
+    L.c.bpart = pb->d_bpart + (alpha & 1) * nb;
+    if (ev_conv) TDW_CUDA(ctx, cudaEventRecordWithFlags(ev_conv[2 * (alpha - 1)], sc, cudaEventRecordExternal));
+    conv_kernel<<<L.cgrid, TDW_CONV_THREADS, L.smem, sc>>>(L.c, L.hmap);
+    if (ev_conv) TDW_CUDA(ctx, cudaEventRecordWithFlags(ev_conv[2 * (alpha - 1) + 1], sc, cudaEventRecordExternal));
+    TDW_CUDA(ctx, cudaEventRecord(evF[alpha], sc));
+    // solve of step alpha on the main stream
+    TDW_CUDA(ctx, cudaStreamWaitEvent(st, evF[alpha], 0));
     if (L.multi) {
       reduce_parts_kernel<<<(pb->rows_per_rank + 255) / 256, 256, 0, st>>>(
-          pb->d_bpart, pb->nsplit, pb->rows_per_rank, pb->d_b + pb->row_lo, pb->d_flags);
+          pb->d_bpart + (alpha & 1) * nb, pb->nsplit, pb->rows_per_rank, pb->d_b + pb->row_lo,
+          pb->d_flags);
       ncclResult_t nr = ncclAllGather(pb->d_b + pb->row_lo, pb->d_b, (size_t)pb->rows_per_rank,
                                       ncclDouble, ctx->comm, st);
       if (nr != ncclSuccess)
         return tdw_fail(ctx, TDW_ERR_NCCL, std::string("ncclAllGather: ") + ncclGetErrorString(nr));
     }
-    if (pb->sp_cl > 0) {
-      L.cs.alpha = alpha;
-      TDW_CUDA(ctx, cudaLaunchKernelEx(&ccfg, solve_cluster_kernel, L.cs));
-    } else {
-      TDW_CUDA(ctx, cudaLaunchKernelEx(&cfg, solve_kernel, L.s));
-    }
+    L.cs.alpha = alpha;
+    L.cs.bpart = pb->d_bpart + (alpha & 1) * nb;
+    L.cs.bnear_in = pb->d_bnear + (alpha & 1) * (size_t)pb->ns;
+    L.cs.bnear_out = pb->d_bnear + ((alpha + 1) & 1) * (size_t)pb->ns;
+    TDW_CUDA(ctx, cudaLaunchKernelEx(&ccfg, solve_cluster_kernel, L.cs));
+    TDW_CUDA(ctx, cudaEventRecord(evS[alpha], st));
   }
+  // join the side stream
+  TDW_CUDA(ctx, cudaStreamWaitEvent(st, evF[nt - 1], 0));
   TDW_CUDA(ctx, cudaGetLastError());
   return TDW_OK;
 }
@@ -802,11 +695,19 @@ int tdw_march_loop(tdw_problem* pb, double threshold, bool want_rhs, bool time_k
       TDW_CUDA(ctx, cudaMalloc(&pb->d_rhs, sizeof(double) * (size_t)(pb->nt - 1) * pb->ns));
     TDW_CUDA(ctx, cudaMemsetAsync(pb->d_rhs, 0, sizeof(double) * (size_t)(pb->nt - 1) * pb->ns, st));
   }
-  TDW_CUDA(ctx, cudaMemsetAsync(pb->d_bar, 0, sizeof(unsigned) * 2, st));
+  if (!pb->side) {
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    TDW_CUDA(ctx, cudaStreamCreateWithPriority(&pb->side, cudaStreamNonBlocking, lo));
+    pb->ev_solve.resize(pb->nt);
+    pb->ev_conv.resize(pb->nt);
+    for (auto& e : pb->ev_solve) TDW_CUDA(ctx, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    for (auto& e : pb->ev_conv) TDW_CUDA(ctx, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    TDW_CUDA(ctx, cudaEventCreateWithFlags(&pb->ev_fork, cudaEventDisableTiming));
+  }
 
   LoopPlan L{};
-  ConvArgs& c = L.c;
-  fill_conv_args(pb, c);
+  fill_conv_args(pb, L.c);
   {
     int rc = make_hist_map(pb, &L.hmap);
     if (rc) return rc;
@@ -816,40 +717,16 @@ int tdw_march_loop(tdw_problem* pb, double threshold, bool want_rhs, bool time_k
                                      (int)L.smem));
   L.cgrid = dim3(pb->conv_grid);
   L.multi = pb->nranks > 1;
-  SolveArgs& s = L.s;
-  s.bpart = pb->d_bpart;
-  s.b = pb->d_b;
-  s.x = pb->d_x;
-  s.acol = pb->d_acol;
-  s.aval = pb->d_aval;
-  s.adiag = pb->d_adiag;
-  s.ell_w = pb->ell_w;
-  s.iters = pb->jac_iters;
-  s.phi = pb->d_phi;
-  s.perm = pb->d_perm;
-  s.uk = pb->d_uk;
-  s.qk = pb->d_qk;
-  s.hist = pb->d_hist;
-  s.hstride = pb->hstride;
-  s.pad = pb->pad;
-  s.red = pb->d_red;
-  s.bar = pb->d_bar;
-  s.flags = pb->d_flags;
-  s.rhs = want_rhs ? pb->d_rhs : nullptr;
-  s.threshold = threshold;
-  s.ns = pb->ns;
-  s.nsplit = L.multi ? 0 : pb->nsplit;
-  s.rows_loc = pb->rows_per_rank;
-  s.nt = pb->nt;
-
   ClusterSolveArgs& cs = L.cs;
-  cs.bpart = pb->d_bpart;
   cs.b = pb->d_b;
   cs.sp_rowptr = pb->d_sp_rowptr;
   cs.sp_nnzoff = pb->d_sp_nnzoff;
   cs.sp_col = pb->d_sp_col;
   cs.sp_val = pb->d_sp_val;
   cs.diag = pb->d_adiag;
+  cs.ncol = pb->d_ncol_packed;
+  cs.nval = pb->d_nval;
+  cs.near_w = pb->near_w;
   cs.phi = pb->d_phi;
   cs.perm = pb->d_perm;
   cs.uk = pb->d_uk;
@@ -877,7 +754,7 @@ int tdw_march_loop(tdw_problem* pb, double threshold, bool want_rhs, bool time_k
   TDW_CUDA(ctx, cudaEventCreate(&ev0));
   TDW_CUDA(ctx, cudaEventCreate(&ev1));
 
-  // capture the loop into a graph (launch overhead of ~2-4 kernels per step
+  // capture the loop into a graph (launch overhead of ~2 kernels per step
   // otherwise dominates the small configurations); fall back to direct launches
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
@@ -1026,7 +903,8 @@ int tdw_setup_cluster_solver(tdw_problem* pb) {
       break;
     }
   }
-  if (pb->sp_cl == 0) return TDW_OK;  // too large: grid-barrier solver
+  if (pb->sp_cl == 0)
+    return tdw_fail(ctx, TDW_ERR_LIMIT, "lag-1 system too large for a 16-CTA cluster's shared memory");
   const int CL = pb->sp_cl, R = pb->sp_R;
   std::vector<int> rowptr((size_t)CL * (R + 1), 0);
   std::vector<long long> nzoff(CL + 1, 0);
@@ -1059,6 +937,14 @@ int tdw_setup_cluster_solver(tdw_problem* pb) {
   if (!col.empty()) {
     TDW_CUDA(ctx, cudaMemcpy(pb->d_sp_col, col.data(), sizeof(int) * col.size(), cudaMemcpyHostToDevice));
     TDW_CUDA(ctx, cudaMemcpy(pb->d_sp_val, val.data(), sizeof(double) * val.size(), cudaMemcpyHostToDevice));
+  }
+  {
+    // near columns in the cluster's (owner, local) packing
+    std::vector<int> ncol((size_t)TDW_NEAR_MAX * ns);
+    TDW_CUDA(ctx, cudaMemcpy(ncol.data(), pb->d_ncol, sizeof(int) * ncol.size(), cudaMemcpyDeviceToHost));
+    for (int& j : ncol) j = ((j / R) << 24) | (j % R);
+    TDW_CUDA(ctx, cudaMalloc(&pb->d_ncol_packed, sizeof(int) * ncol.size()));
+    TDW_CUDA(ctx, cudaMemcpy(pb->d_ncol_packed, ncol.data(), sizeof(int) * ncol.size(), cudaMemcpyHostToDevice));
   }
   TDW_CUDA(ctx, cudaFuncSetAttribute(solve_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)pb->sp_smem));

@@ -15,6 +15,8 @@
 #define TDW_ROWS_PER_WARP 2
 #define TDW_CONV_WARPS (TDW_TI / TDW_ROWS_PER_WARP)
 #define TDW_ELL_MAX 64   // max nnz per row of the lag-1 step matrix
+#define TDW_NEAR_LAGS 2  // the unknown density enters the store's lag-2 entries via the solve
+#define TDW_NEAR_MAX 128 // max pairs per row with a band starting at lag <= 2
 #define TDW_ELEM_STRIDE 16  // doubles per element record: v0 v1 v2 n c rad
 // Unit layout (one (I-block, J-tile) unit = one contiguous byte range of the store):
 //   [0, 128)        uint32 seg_rel[32]  entry offset of row r's segment in the unit
@@ -77,6 +79,17 @@ struct tdw_problem {
   double* d_aval = nullptr;
   double* d_adiag = nullptr;
   int jac_iters = 0;
+  // near part (lags 1..TDW_NEAR_LAGS), all rows, ELL [TDW_NEAR_MAX][ns]
+  int near_w = 0;
+  int64_t n_near = 0, n_near_evals = 0;
+  int* d_ncol = nullptr;
+  double* d_nval = nullptr;
+  int* d_ncol_packed = nullptr;    // ncol in the cluster solver's (owner << 24 | local) form
+  double* d_bnear = nullptr;       // [2][ns] lag-2 unknown term, produced by the previous solve
+  // pipelined loop: side stream for the far convolution, per-step events
+  cudaStream_t side = nullptr;
+  std::vector<cudaEvent_t> ev_solve, ev_conv;
+  cudaEvent_t ev_fork = nullptr;
   double jac_bound = 0.0;
   // history and step buffers
   int pad = 0, hstride = 0;
@@ -85,7 +98,7 @@ struct tdw_problem {
   double* d_qk = nullptr;
   bool known_loaded = false;
   int nsplit = 1;                  // == conv_S once assembled
-  double* d_bpart = nullptr;       // [nsplit][rows_per_rank]
+  double* d_bpart = nullptr;       // [2][nsplit][rows_per_rank] (step parity)
   double* d_b = nullptr;           // [nranks * rows_per_rank]
   double* d_x = nullptr;           // [2][ns]
   double* d_red = nullptr;         // reduction scratch [3][grid]
