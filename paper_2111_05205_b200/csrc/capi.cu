@@ -4,7 +4,10 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <vector>
@@ -350,19 +353,32 @@ int tdw_march(tdw_problem* pb, const double* u_known, const double* q_known, dou
               int32_t* n_steps, int32_t* status) {
   if (!pb) return TDW_ERR_INVALID_ARG;
   cudaSetDevice(pb->ctx->device);
+  static const bool trace = getenv("TDW_TRACE_MARCH") != nullptr;
+  auto now = [] { return std::chrono::steady_clock::now(); };
+  auto t0 = now();
   int rc = tdw_upload_known(pb, u_known, q_known);
   if (rc) return rc;
   if (!pb->assembled) {
     rc = tdw_assemble_impl(pb);
     if (rc) return rc;
   }
+  cudaStreamSynchronize(pb->ctx->stream);
+  auto t1 = now();
   rc = tdw_march_loop(pb, threshold, rhs_trace != nullptr, false, nullptr);
   if (rc) return rc;
+  auto t2 = now();
   if (rhs_trace) {
     TDW_CUDA(pb->ctx, cudaMemcpy(rhs_trace, pb->d_rhs, sizeof(double) * (size_t)(pb->nt - 1) * pb->ns,
                                  cudaMemcpyDeviceToHost));
   }
-  return tdw_download(pb, u, q, tau, sigma, n_steps, status);
+  rc = tdw_download(pb, u, q, tau, sigma, n_steps, status);
+  auto t3 = now();
+  if (trace) {
+    auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+    fprintf(stderr, "tdw_march: upload+assemble %.2f ms, loop %.2f ms, download %.2f ms\n", ms(t0, t1),
+            ms(t1, t2), ms(t2, t3));
+  }
+  return rc;
 }
 
 int tdw_march_resident(tdw_problem* pb, double threshold, int n_repeat, int time_kernels,
@@ -400,6 +416,7 @@ int tdw_problem_destroy(tdw_problem* pb) {
                   pb->d_ncol, pb->d_nval, pb->d_ncol_packed, pb->d_bnear};
   for (void* p : ptrs)
     if (p) cudaFree(p);
+  if (pb->graph_exec) cudaGraphExecDestroy(pb->graph_exec);
   for (auto& e : pb->ev_solve) cudaEventDestroy(e);
   for (auto& e : pb->ev_conv) cudaEventDestroy(e);
   if (pb->ev_fork) cudaEventDestroy(pb->ev_fork);

@@ -755,11 +755,17 @@ int tdw_march_loop(tdw_problem* pb, double threshold, bool want_rhs, bool time_k
   TDW_CUDA(ctx, cudaEventCreate(&ev1));
 
   // capture the loop into a graph (launch overhead of ~2 kernels per step
-  // otherwise dominates the small configurations); fall back to direct launches
+  // otherwise dominates the small configurations); the instantiated graph is
+  // cached per (threshold, rhs trace) and reused by later calls; fall back to
+  // direct launches if capture is not possible
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
   bool use_graph = pb->use_graph;
-  if (use_graph) {
+  const bool cacheable = !time_kernels;
+  if (use_graph && cacheable && pb->graph_exec && pb->graph_thr == threshold &&
+      pb->graph_rhs == want_rhs) {
+    exec = pb->graph_exec;
+  } else if (use_graph) {
     if (cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
       use_graph = false;
     } else {
@@ -773,6 +779,11 @@ int tdw_march_loop(tdw_problem* pb, double threshold, bool want_rhs, bool time_k
         exec = nullptr;
         use_graph = false;
         pb->use_graph = false;
+      } else if (cacheable) {
+        if (pb->graph_exec) cudaGraphExecDestroy(pb->graph_exec);
+        pb->graph_exec = exec;
+        pb->graph_thr = threshold;
+        pb->graph_rhs = want_rhs;
       }
     }
   }
@@ -800,7 +811,7 @@ int tdw_march_loop(tdw_problem* pb, double threshold, bool want_rhs, bool time_k
     timing->solve_ms = use_graph ? 1.0 : 0.0;  // reused as a "graph used" marker
   }
   cudaGetLastError();
-  if (exec) cudaGraphExecDestroy(exec);
+  if (exec && exec != pb->graph_exec) cudaGraphExecDestroy(exec);
   if (graph) cudaGraphDestroy(graph);
   for (auto& e : evc) cudaEventDestroy(e);
   cudaEventDestroy(ev0);

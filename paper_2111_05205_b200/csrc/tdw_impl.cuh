@@ -90,6 +90,9 @@ struct tdw_problem {
   cudaStream_t side = nullptr;
   std::vector<cudaEvent_t> ev_solve, ev_conv;
   cudaEvent_t ev_fork = nullptr;
+  cudaGraphExec_t graph_exec = nullptr;  // cached loop graph
+  double graph_thr = 0.0;
+  bool graph_rhs = false;
   double jac_bound = 0.0;
   // history and step buffers
   int pad = 0, hstride = 0;

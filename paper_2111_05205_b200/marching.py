@@ -216,15 +216,16 @@ def build_retarded_matrices(spec, gamma_max: int | None = None, pairs=None, slab
 
 def march(spec, window: bool = True, blowup_factor: float = 1e6, mats=None,
           rhs_trace: list | None = None) -> TimeHistory:
-    """Run the conventional time marching on the GPU (marching.py:292-338)."""
-    stats = mesh_stats(spec.mesh)
-    gstar = compute_gamma_star(stats, spec.basis, spec.c)
-    n_lags = min(gstar, spec.nt - 1) if window else spec.nt - 1
+    """Run the conventional time marching on the GPU (marching.py:292-338).
+
+    gamma* and the lag count are computed by the library from the mesh
+    (tdw_problem_create), so a supplied store is validated against its own
+    record of them."""
     if mats is None:
         mats = BandStore(spec, window=window)
     elif not isinstance(mats, BandStore):
         raise TypeError("mats must come from build_retarded_matrices of this package")
-    elif mats.n_lags < n_lags or mats.window != window:
+    elif mats.window != window or mats.nt != spec.nt or mats.ns != spec.mesh.n_elements:
         raise ValueError("matrix set does not cover the required lags")
     hist = TimeHistory(spec.basis, spec.nt, spec.mesh.n_elements)
     uk, qk = greville_samples(spec)
