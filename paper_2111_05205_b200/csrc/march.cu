@@ -336,6 +336,33 @@ struct ClusterSolveArgs {
   int hstride, pad, ns, nsplit, rows_loc, alpha, nt, R, maxit, near_w;
 };
 
+// x_j for a packed column: own shared memory or a peer CTA's (DSMEM)
+__device__ __forceinline__ double fetch_x(int c, const double* x, int cr,
+                                          cooperative_groups::cluster_group& cl) {
+  const int owner = c >> 24, loc = c & 0xffffff;
+  return owner == cr ? x[loc] : *cl.map_shared_rank(x + loc, owner);
+}
+
+// sum_p val[p] x[col[p]] over a CSR row held in shared memory, loads batched by 4
+__device__ __forceinline__ double row_dot(int p0, int p1, const int* col, const double* val,
+                                          const double* x, int cr,
+                                          cooperative_groups::cluster_group& cl) {
+  double s0 = 0.0, s1 = 0.0;
+  int p = p0;
+  for (; p + 4 <= p1; p += 4) {
+    const int c0 = col[p], c1 = col[p + 1], c2 = col[p + 2], c3 = col[p + 3];
+    const double v0 = val[p], v1 = val[p + 1], v2 = val[p + 2], v3 = val[p + 3];
+    const double x0 = fetch_x(c0, x, cr, cl), x1 = fetch_x(c1, x, cr, cl);
+    const double x2 = fetch_x(c2, x, cr, cl), x3 = fetch_x(c3, x, cr, cl);
+    s0 = fma(v0, x0, s0);
+    s1 = fma(v1, x1, s1);
+    s0 = fma(v2, x2, s0);
+    s1 = fma(v3, x3, s1);
+  }
+  for (; p < p1; ++p) s0 = fma(val[p], fetch_x(col[p], x, cr, cl), s0);
+  return s0 + s1;
+}
+
 // K3/K4: one thread-block cluster (CL <= 16 CTAs, 1024 threads) owns the whole
 // lag-1 system.  CTA r holds rows [r*R, r*R+R): its off-diagonal CSR rows,
 // diagonal, b and a double-buffered x slice live in shared memory; x of the
@@ -398,13 +425,7 @@ __global__ void __launch_bounds__(1024, 1) solve_cluster_kernel(ClusterSolveArgs
     double* dst = xs + (cur ^ 1) * R;
     double dmax = 0.0, xmax = 0.0;
     for (int i = tid; i < nr; i += nth) {
-      double acc = bs[i];
-      for (int p = rp[i]; p < rp[i + 1]; ++p) {
-        const int c = col[p];
-        const int owner = c >> 24, loc = c & 0xffffff;
-        const double xv = owner == cr ? src[loc] : *cl.map_shared_rank(src + loc, owner);
-        acc -= val[p] * xv;
-      }
+      const double acc = bs[i] - row_dot(rp[i], rp[i + 1], col, val, src, cr, cl);
       const double xn = acc / dg[i];
       dst[i] = xn;
       dmax = fmax(dmax, fabs(xn - src[i]));
@@ -434,13 +455,7 @@ __global__ void __launch_bounds__(1024, 1) solve_cluster_kernel(ClusterSolveArgs
   const double* xf = xs + cur * R;
   double r2 = 0.0, b2 = 0.0, xm = 0.0;
   for (int i = tid; i < nr; i += nth) {
-    double acc = dg[i] * xf[i] - bs[i];
-    for (int p = rp[i]; p < rp[i + 1]; ++p) {
-      const int c = col[p];
-      const int owner = c >> 24, loc = c & 0xffffff;
-      const double xv = owner == cr ? xf[loc] : *cl.map_shared_rank(xf + loc, owner);
-      acc += val[p] * xv;
-    }
+    const double acc = dg[i] * xf[i] - bs[i] + row_dot(rp[i], rp[i + 1], col, val, xf, cr, cl);
     r2 += acc * acc;
     b2 += bs[i] * bs[i];
     xm = fmax(xm, fabs(xf[i]));
@@ -454,11 +469,19 @@ __global__ void __launch_bounds__(1024, 1) solve_cluster_kernel(ClusterSolveArgs
   for (int i = tid; i < nr; i += nth) {
     const int gi = r0 + i;
     double acc = 0.0;
-    for (int k = 0; k < a.near_w; ++k) {
-      const int c = a.ncol[(size_t)k * a.ns + gi];
-      const int owner = c >> 24, loc = c & 0xffffff;
-      const double xv = owner == cr ? xf[loc] : *cl.map_shared_rank(xf + loc, owner);
-      acc += a.nval[(size_t)k * a.ns + gi] * xv;
+    for (int k0 = 0; k0 < a.near_w; k0 += 8) {
+      int c[8];
+      double v[8], xv[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const bool on = k0 + q < a.near_w;
+        c[q] = on ? __ldg(a.ncol + (size_t)(k0 + q) * a.ns + gi) : (cr << 24);
+        v[q] = on ? __ldg(a.nval + (size_t)(k0 + q) * a.ns + gi) : 0.0;
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q) xv[q] = fetch_x(c[q], xf, cr, cl);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) acc += v[q] * xv[q];
     }
     a.bnear_out[gi] = acc;
   }
@@ -864,8 +887,8 @@ int tdw_outputs(tdw_problem* pb, double* u, double* q, double* tau, double* sigm
   tdw_ctx* ctx = pb->ctx;
   cudaStream_t st = ctx->stream;
   const size_t n = (size_t)(pb->nt - 1) * pb->ns;
-  double* buf = nullptr;
-  TDW_CUDA(ctx, cudaMallocAsync((void**)&buf, sizeof(double) * 4 * n, st));
+  if (!pb->d_out) TDW_CUDA(ctx, cudaMalloc(&pb->d_out, sizeof(double) * 4 * n));
+  double* buf = pb->d_out;
   outputs_kernel<<<1024, 256, 0, st>>>(pb->d_hist, pb->hstride, pb->pad, pb->ns, pb->nt, pb->d,
                                         pb->d_perm, pb->d_flags, buf, buf + n, buf + 2 * n,
                                         buf + 3 * n);
@@ -875,7 +898,6 @@ int tdw_outputs(tdw_problem* pb, double* u, double* q, double* tau, double* sigm
     if (outs[k])
       TDW_CUDA(ctx, cudaMemcpyAsync(outs[k], buf + k * n, sizeof(double) * n,
                                     cudaMemcpyDeviceToHost, st));
-  TDW_CUDA(ctx, cudaFreeAsync(buf, st));
   TDW_CUDA(ctx, cudaStreamSynchronize(st));
   return TDW_OK;
 }
