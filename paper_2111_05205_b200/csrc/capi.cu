@@ -385,10 +385,36 @@ int tdw_march_resident(tdw_problem* pb, double threshold, int n_repeat, int time
                        tdw_timing* timing) {
   if (!pb || n_repeat < 1) return TDW_ERR_INVALID_ARG;
   cudaSetDevice(pb->ctx->device);
+  static const bool trace = getenv("TDW_TRACE_SOLVE") != nullptr;
+  if (trace && !pb->d_trace) {
+    TDW_CUDA(pb->ctx, cudaMalloc(&pb->d_trace, sizeof(unsigned long long) * 16 * pb->nt));
+    TDW_CUDA(pb->ctx, cudaMemset(pb->d_trace, 0, sizeof(unsigned long long) * 16 * pb->nt));
+    if (pb->graph_exec) { cudaGraphExecDestroy(pb->graph_exec); pb->graph_exec = nullptr; }
+  }
   if (timing) memset(timing, 0, sizeof(*timing));
   for (int r = 0; r < n_repeat; ++r) {
     int rc = tdw_march_loop(pb, threshold, false, time_kernels != 0, timing);
     if (rc) return rc;
+  }
+  if (trace) {
+    std::vector<unsigned long long> h((size_t)16 * pb->nt);
+    TDW_CUDA(pb->ctx, cudaMemcpy(h.data(), pb->d_trace, sizeof(unsigned long long) * h.size(),
+                                 cudaMemcpyDeviceToHost));
+    double acc[9] = {0};
+    int n = 0;
+    double sw = 0;
+    for (int a = 2; a < pb->nt; ++a) {
+      const unsigned long long* t = &h[(size_t)16 * a];
+      if (!t[0] || !t[8]) continue;
+      for (int k = 1; k <= 8; ++k) acc[k] += (double)(t[k] - t[k - 1]);
+      sw += (double)t[15];
+      ++n;
+    }
+    if (n)
+      fprintf(stderr, "solve phases (us, mean of %d steps): load %.2f sync %.2f sweeps(%.1f) %.2f resid %.2f "
+              "sync %.2f near %.2f sync %.2f final %.2f\n", n, acc[1] / n / 1e3, acc[2] / n / 1e3, sw / n,
+              acc[3] / n / 1e3, acc[4] / n / 1e3, acc[5] / n / 1e3, acc[6] / n / 1e3, acc[7] / n / 1e3,
+              acc[8] / n / 1e3);
   }
   return TDW_OK;
 }
@@ -413,7 +439,7 @@ int tdw_problem_destroy(tdw_problem* pb) {
                   pb->d_unit, pb->d_acol, pb->d_aval, pb->d_adiag, pb->d_hist, pb->d_uk,
                   pb->d_qk, pb->d_bpart, pb->d_b, pb->d_x, pb->d_red, pb->d_bar, pb->d_flags,
                   pb->d_rhs, pb->d_sp_rowptr, pb->d_sp_nnzoff, pb->d_sp_col, pb->d_sp_val,
-                  pb->d_ncol, pb->d_nval, pb->d_ncol_packed, pb->d_bnear, pb->d_out};
+                  pb->d_ncol, pb->d_nval, pb->d_ncol_packed, pb->d_bnear, pb->d_out, pb->d_trace};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (pb->graph_exec) cudaGraphExecDestroy(pb->graph_exec);

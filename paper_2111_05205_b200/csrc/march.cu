@@ -17,6 +17,7 @@
 
 #include <climits>
 #include <cstdio>
+#include <cstdlib>
 #include <algorithm>
 #include <vector>
 
@@ -243,22 +244,32 @@ __global__ void __launch_bounds__(TDW_CONV_THREADS, 1)
       double v = acc[r];
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULLMASK, v, o);
-      if (lane == 0)
-        a.bpart[(size_t)sp * a.rows_loc + iblk * TDW_TI + warp * TDW_ROWS_PER_WARP + r] = v;
+      if (lane == 0)  // row-major partials: a row's S partials are contiguous
+        a.bpart[(size_t)(iblk * TDW_TI + warp * TDW_ROWS_PER_WARP + r) * S + sp] = v;
       acc[r] = 0.0;
     }
   }
+}
+
+// fixed-order sum of a row's split partials, loads issued 8 at a time
+__device__ __forceinline__ double sum_parts(const double* __restrict__ p, int n) {
+  double acc = 0.0;
+  for (int k0 = 0; k0 < n; k0 += 8) {
+    double v[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) v[q] = k0 + q < n ? __ldcg(p + k0 + q) : 0.0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc += v[q];
+  }
+  return acc;
 }
 
 // sum of the split partials of the own rows into b (multi-GPU path, before the all-gather)
 __global__ void reduce_parts_kernel(const double* __restrict__ bpart, int nsplit, int rows_loc,
                                     double* __restrict__ bown, const int* flags) {
   if (flags[0] != 0) return;
-  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < rows_loc; r += gridDim.x * blockDim.x) {
-    double v = 0.0;
-    for (int s = 0; s < nsplit; ++s) v += bpart[(size_t)s * rows_loc + r];
-    bown[r] = v;
-  }
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < rows_loc; r += gridDim.x * blockDim.x)
+    bown[r] = sum_parts(bpart + (size_t)r * nsplit, nsplit);
 }
 
 __device__ __forceinline__ double block_reduce_sum(double v, double* sh) {
@@ -333,8 +344,17 @@ struct ClusterSolveArgs {
   int* flags;
   double* rhs;
   double threshold;
+  unsigned long long* trace;                // optional phase timestamps (globaltimer, ns)
   int hstride, pad, ns, nsplit, rows_loc, alpha, nt, R, maxit, near_w;
 };
+
+__device__ __forceinline__ void trace_mark(unsigned long long* t, int k) {
+  if (t && threadIdx.x == 0 && blockIdx.x == 0) {
+    unsigned long long v;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
+    t[k] = v;
+  }
+}
 
 // x_j for a packed column: own shared memory or a peer CTA's (DSMEM)
 __device__ __forceinline__ double fetch_x(int c, const double* x, int cr,
@@ -397,6 +417,8 @@ __global__ void __launch_bounds__(1024, 1) solve_cluster_kernel(ClusterSolveArgs
   int* col = rp + R + 1;                // [nnz]
   const int tid = threadIdx.x, nth = blockDim.x;
   const int beta0 = a.alpha - 1;
+  unsigned long long* tr = a.trace ? a.trace + (size_t)a.alpha * 16 : nullptr;
+  trace_mark(tr, 0);
   for (int p = tid; p < nnz; p += nth) {
     val[p] = a.sp_val[nz0 + p];
     col[p] = a.sp_col[nz0 + p];
@@ -406,8 +428,7 @@ __global__ void __launch_bounds__(1024, 1) solve_cluster_kernel(ClusterSolveArgs
     const int gi = r0 + i;
     double bi;
     if (a.nsplit > 0) {
-      bi = 0.0;
-      for (int s2 = 0; s2 < a.nsplit; ++s2) bi += a.bpart[(size_t)s2 * a.rows_loc + gi];
+      bi = sum_parts(a.bpart + (size_t)gi * a.nsplit, a.nsplit);
     } else {
       bi = __ldcg(a.b + gi);
     }
@@ -418,8 +439,11 @@ __global__ void __launch_bounds__(1024, 1) solve_cluster_kernel(ClusterSolveArgs
     if (a.rhs) a.rhs[(size_t)beta0 * a.ns + a.perm[gi]] = bi;
   }
   if (tid == 0) s_stop = 0;
+  trace_mark(tr, 1);
   cl.sync();
+  trace_mark(tr, 2);
   int cur = 0;
+  int sweeps = 0;
   for (int it = 1; it <= a.maxit; ++it) {
     const double* src = xs + cur * R;
     double* dst = xs + (cur ^ 1) * R;
@@ -438,20 +462,28 @@ __global__ void __launch_bounds__(1024, 1) solve_cluster_kernel(ClusterSolveArgs
     }
     cl.sync();
     cur ^= 1;
+    sweeps = it;
     if (check) {
-      if (tid == 0) {
+      if (tid < 32) {  // lane q reads CTA q's partials (DSMEM), then a warp max
         double D = 0.0, X = 0.0;
-        for (int q = 0; q < CL; ++q) {
-          const double* rr = cl.map_shared_rank(&red[(it >> 2) & 1][0], q);
-          D = fmax(D, rr[0]);
-          X = fmax(X, rr[1]);
+        if (tid < CL) {
+          const double* rr = cl.map_shared_rank(&red[(it >> 2) & 1][0], tid);
+          D = rr[0];
+          X = rr[1];
         }
-        s_stop = D <= 1e-15 * X;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          D = fmax(D, __shfl_xor_sync(FULLMASK, D, o));
+          X = fmax(X, __shfl_xor_sync(FULLMASK, X, o));
+        }
+        if (tid == 0) s_stop = D <= 1e-15 * X;
       }
       __syncthreads();
       if (s_stop) break;
     }
   }
+  trace_mark(tr, 3);
+  if (tr && tid == 0 && cr == 0) tr[15] = sweeps;
   const double* xf = xs + cur * R;
   double r2 = 0.0, b2 = 0.0, xm = 0.0;
   for (int i = tid; i < nr; i += nth) {
@@ -464,7 +496,9 @@ __global__ void __launch_bounds__(1024, 1) solve_cluster_kernel(ClusterSolveArgs
   b2 = block_reduce_sum(b2, shred);
   xm = block_reduce_max(xm, shred);
   if (tid == 0) { red2[0] = r2; red2[1] = b2; red2[2] = xm; }
+  trace_mark(tr, 4);
   cl.sync();
+  trace_mark(tr, 5);
   // lag-2 term of the unknown density for the next step (x still in shared memory)
   for (int i = tid; i < nr; i += nth) {
     const int gi = r0 + i;
@@ -486,13 +520,27 @@ __global__ void __launch_bounds__(1024, 1) solve_cluster_kernel(ClusterSolveArgs
     a.bnear_out[gi] = acc;
   }
   double RR = 0.0, BB = 0.0, XM = 0.0;
-  for (int q = 0; q < CL; ++q) {
-    const double* rr = cl.map_shared_rank(red2, q);
-    RR += rr[0];
-    BB += rr[1];
-    XM = fmax(XM, rr[2]);
+  if (tid < 32) {
+    if (tid < CL) {
+      const double* rr = cl.map_shared_rank(red2, tid);
+      RR = rr[0];
+      BB = rr[1];
+      XM = rr[2];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      RR += __shfl_xor_sync(FULLMASK, RR, o);
+      BB += __shfl_xor_sync(FULLMASK, BB, o);
+      XM = fmax(XM, __shfl_xor_sync(FULLMASK, XM, o));
+    }
+    if (tid == 0) { red2[3] = RR; red[0][0] = BB; red[0][1] = XM; }
   }
+  trace_mark(tr, 6);
   cl.sync();  // no CTA leaves while another may still read its shared memory
+  trace_mark(tr, 7);
+  RR = red2[3];
+  BB = red[0][0];
+  XM = red[0][1];
   if (sqrt(RR) > 1e-10 * fmax(sqrt(BB), 1e-300)) {
     if (cr == 0 && tid == 0) {
       a.flags[2] = a.alpha;
@@ -515,6 +563,7 @@ __global__ void __launch_bounds__(1024, 1) solve_cluster_kernel(ClusterSolveArgs
     a.flags[1] = a.alpha;
     if (unstable) atomicExch(&a.flags[0], 1);
   }
+  trace_mark(tr, 8);
 }
 
 // hist[j][pad + beta] = known part (phi q_known, (1-phi) u_known) of every
@@ -766,6 +815,7 @@ int tdw_march_loop(tdw_problem* pb, double threshold, bool want_rhs, bool time_k
   cs.nt = pb->nt;
   cs.R = pb->sp_R;
   cs.maxit = pb->jac_iters;
+  cs.trace = pb->d_trace;
 
   const int nsteps = pb->nt - 1;
   std::vector<cudaEvent_t> evc;
@@ -918,6 +968,7 @@ int tdw_setup_cluster_solver(tdw_problem* pb) {
   // about one row per thread (latency-bound sweeps), more CTAs only if the slice must shrink
   int cl0 = 1;
   while (cl0 < 16 && (ns + cl0 - 1) / cl0 > 1024) cl0 *= 2;
+  if (const char* e = getenv("TDW_SOLVE_CL")) cl0 = std::max(1, std::min(16, atoi(e)));
   for (int CL = cl0; CL <= 16; CL *= 2) {
     const int R = (ns + CL - 1) / CL;
     size_t worst = 0;

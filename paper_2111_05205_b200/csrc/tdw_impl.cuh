@@ -108,7 +108,8 @@ struct tdw_problem {
   unsigned* d_bar = nullptr;       // grid barrier {count, generation}
   int* d_flags = nullptr;          // {status, n_steps, err_step, ell_overflow}
   double* d_rhs = nullptr;         // (nt-1, ns) original order, optional
-  double* d_out = nullptr;         // [4][(nt-1) ns] u, q, tau, sigma staging for the download
+  double* d_out = nullptr;
+  unsigned long long* d_trace = nullptr;  // [nt][16] solve phase timestamps (TDW_TRACE_SOLVE)         // [4][(nt-1) ns] u, q, tau, sigma staging for the download
   int solve_grid = 0;
   // cluster solver (csrc/march.cu solve_cluster_kernel); sp_cl == 0 -> grid-barrier fallback
   int sp_cl = 0, sp_R = 0;
