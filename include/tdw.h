@@ -136,6 +136,13 @@ int tdw_set_graph(tdw_problem* pb, int enable);
 
 int tdw_problem_destroy(tdw_problem* pb);
 
+/* Test harness of the row-sharded path on ONE device: create the shard of rank
+ * desc->rank of desc->nranks without a communicator, then run all shards in one
+ * process with the per-step all-gather emulated by device copies.  Every shard
+ * must be assembled and have its known data uploaded; outputs via tdw_download. */
+int tdw_problem_create_shard(tdw_ctx* ctx, const tdw_problem_desc* desc, tdw_problem** out);
+int tdw_march_emulated(tdw_problem** shards, int n, double threshold);
+
 /* Multi-GPU (one process per GPU): rank 0 makes the id, the host broadcasts it
  * (torch.distributed), every rank calls tdw_comm_init before tdw_problem_create. */
 int tdw_nccl_unique_id(char out[128]);

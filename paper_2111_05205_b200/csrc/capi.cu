@@ -94,6 +94,26 @@ int tdw_comm_init(tdw_ctx* ctx, const char id[128], int nranks, int rank) {
 }
 
 int tdw_problem_create(tdw_ctx* ctx, const tdw_problem_desc* dsc, tdw_problem** out) {
+  return tdw_problem_create_impl(ctx, dsc, out, false);
+}
+
+int tdw_problem_create_shard(tdw_ctx* ctx, const tdw_problem_desc* dsc, tdw_problem** out) {
+  return tdw_problem_create_impl(ctx, dsc, out, true);
+}
+
+int tdw_march_emulated(tdw_problem** pbs, int n, double threshold) {
+  if (!pbs || n < 1) return TDW_ERR_INVALID_ARG;
+  for (int r = 0; r < n; ++r)
+    if (!pbs[r] || pbs[r]->nranks != n || pbs[r]->rank != r || pbs[r]->ctx != pbs[0]->ctx)
+      return TDW_ERR_INVALID_ARG;
+  cudaSetDevice(pbs[0]->ctx->device);
+  return tdw_march_emulated_impl(pbs, n, threshold);
+}
+
+}  // extern "C"
+
+int tdw_problem_create_impl(tdw_ctx* ctx, const tdw_problem_desc* dsc, tdw_problem** out,
+                            bool shard_only) {
   if (!ctx || !dsc || !out) return TDW_ERR_INVALID_ARG;
   *out = nullptr;
   if (dsc->d < 1 || dsc->d > 3)
@@ -106,7 +126,8 @@ int tdw_problem_create(tdw_ctx* ctx, const tdw_problem_desc* dsc, tdw_problem** 
   if (!(dsc->dt > 0.0) || !(dsc->c > 0.0))
     return tdw_fail(ctx, TDW_ERR_INVALID_ARG, "c and dt must be positive");
   const int nranks = std::max(1, dsc->nranks), rank = dsc->rank;
-  if (nranks != ctx->nranks || rank != ctx->rank)
+  if (rank < 0 || rank >= nranks) return tdw_fail(ctx, TDW_ERR_INVALID_ARG, "rank out of range");
+  if (!shard_only && (nranks != ctx->nranks || rank != ctx->rank))
     return tdw_fail(ctx, TDW_ERR_INVALID_ARG, "nranks/rank differ from tdw_comm_init");
   cudaSetDevice(ctx->device);
   tdw_problem* pb = new tdw_problem();
@@ -206,8 +227,9 @@ int tdw_problem_create(tdw_ctx* ctx, const tdw_problem_desc* dsc, tdw_problem** 
   const int blk_per_rank = (nblk + nranks - 1) / nranks;
   pb->rows_per_rank = blk_per_rank * TDW_TI;
   pb->n_iblk = blk_per_rank;
-  pb->row_lo = std::min(ns, rank * pb->rows_per_rank);
+  pb->row_lo = rank * pb->rows_per_rank;  // may exceed ns on a rank without rows
   pb->row_hi = std::min(ns, (rank + 1) * pb->rows_per_rank);
+  pb->b_off = rank * pb->rows_per_rank;
   pb->ntiles = (ns + TDW_TJ - 1) / TDW_TJ;
 
   auto fail_cuda = [&](cudaError_t e, const char* what) {
@@ -290,6 +312,8 @@ int tdw_problem_create(tdw_ctx* ctx, const tdw_problem_desc* dsc, tdw_problem** 
   *out = pb;
   return TDW_OK;
 }
+
+extern "C" {
 
 int tdw_assemble(tdw_problem* pb) {
   if (!pb) return TDW_ERR_INVALID_ARG;

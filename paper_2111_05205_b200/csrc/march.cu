@@ -688,97 +688,8 @@ struct LoopPlan {
   bool multi;
 };
 
-// Enqueue one complete time loop.  Two streams: the far convolution F(alpha)
-// runs on the side stream as soon as the solve of step alpha-2 has finalized
-// the history it reads (lags >= 3; lag 1 = known data written up front; lag 2
-// = known component only), so F(alpha+1) overlaps the solve of step alpha.
-//   F(alpha)      waits solve(alpha-2)            writes bpart[alpha & 1]
-//   solve(alpha)  waits F(alpha), solve(alpha-1)  reads bpart[alpha & 1], bnear[alpha & 1]
-// Also used under stream capture (one CUDA graph per loop configuration).
-int enqueue_loop(tdw_problem* pb, LoopPlan& L, cudaEvent_t* ev_conv) {
+int make_plan(tdw_problem* pb, LoopPlan& L, double threshold, bool want_rhs) {
   tdw_ctx* ctx = pb->ctx;
-  cudaStream_t st = ctx->stream, sc = pb->side;
-  const int nt = pb->nt;
-  TDW_CUDA(ctx, cudaMemsetAsync(pb->d_flags, 0, sizeof(int) * 4, st));
-  TDW_CUDA(ctx, cudaMemsetAsync(pb->d_bnear, 0, sizeof(double) * 2 * (size_t)pb->ns, st));
-  init_hist_kernel<<<2 * ctx->num_sms, 256, 0, st>>>(pb->d_hist, pb->hstride, pb->pad, pb->ns, nt,
-                                                    pb->d_phi, pb->d_perm, pb->d_uk, pb->d_qk);
-  TDW_CUDA(ctx, cudaGetLastError());
-  cudaLaunchAttribute cattr[1];
-  cattr[0].id = cudaLaunchAttributeClusterDimension;
-  cattr[0].val.clusterDim.x = pb->sp_cl;
-  cattr[0].val.clusterDim.y = 1;
-  cattr[0].val.clusterDim.z = 1;
-  cudaLaunchConfig_t ccfg = {};
-  ccfg.gridDim = dim3(pb->sp_cl);
-  ccfg.blockDim = dim3(1024);
-  ccfg.dynamicSmemBytes = pb->sp_smem;
-  ccfg.stream = st;
-  ccfg.attrs = cattr;
-  ccfg.numAttrs = 1;
-  cudaEvent_t* evS = pb->ev_solve.data();  // solve(alpha) done
-  cudaEvent_t* evF = pb->ev_conv.data();   // F(alpha) done
-  TDW_CUDA(ctx, cudaEventRecord(pb->ev_fork, st));
-  TDW_CUDA(ctx, cudaStreamWaitEvent(sc, pb->ev_fork, 0));
-  const size_t nb = (size_t)pb->nsplit * pb->rows_per_rank;
-  for (int alpha = 1; alpha < nt; ++alpha) {
-    // far convolution of step alpha on the side stream
-    if (alpha >= 3) TDW_CUDA(ctx, cudaStreamWaitEvent(sc, evS[alpha - 2], 0));
-    L.c.alpha = alpha;
-    L.c.bpart = pb->d_bpart + (alpha & 1) * nb;
-    if (ev_conv) TDW_CUDA(ctx, cudaEventRecordWithFlags(ev_conv[2 * (alpha - 1)], sc, cudaEventRecordExternal));
-    conv_kernel<<<L.cgrid, TDW_CONV_THREADS, L.smem, sc>>>(L.c, L.hmap);
-    if (ev_conv) TDW_CUDA(ctx, cudaEventRecordWithFlags(ev_conv[2 * (alpha - 1) + 1], sc, cudaEventRecordExternal));
-    TDW_CUDA(ctx, cudaEventRecord(evF[alpha], sc));
-    // solve of step alpha on the main stream
-    TDW_CUDA(ctx, cudaStreamWaitEvent(st, evF[alpha], 0));
-    if (L.multi) {
-      reduce_parts_kernel<<<(pb->rows_per_rank + 255) / 256, 256, 0, st>>>(
-          pb->d_bpart + (alpha & 1) * nb, pb->nsplit, pb->rows_per_rank, pb->d_b + pb->row_lo,
-          pb->d_flags);
-      ncclResult_t nr = ncclAllGather(pb->d_b + pb->row_lo, pb->d_b, (size_t)pb->rows_per_rank,
-                                      ncclDouble, ctx->comm, st);
-      if (nr != ncclSuccess)
-        return tdw_fail(ctx, TDW_ERR_NCCL, std::string("ncclAllGather: ") + ncclGetErrorString(nr));
-    }
-    L.cs.alpha = alpha;
-    L.cs.bpart = pb->d_bpart + (alpha & 1) * nb;
-    L.cs.bnear_in = pb->d_bnear + (alpha & 1) * (size_t)pb->ns;
-    L.cs.bnear_out = pb->d_bnear + ((alpha + 1) & 1) * (size_t)pb->ns;
-    TDW_CUDA(ctx, cudaLaunchKernelEx(&ccfg, solve_cluster_kernel, L.cs));
-    TDW_CUDA(ctx, cudaEventRecord(evS[alpha], st));
-  }
-  // join the side stream
-  TDW_CUDA(ctx, cudaStreamWaitEvent(st, evF[nt - 1], 0));
-  TDW_CUDA(ctx, cudaGetLastError());
-  return TDW_OK;
-}
-
-}  // namespace
-
-int tdw_march_loop(tdw_problem* pb, double threshold, bool want_rhs, bool time_kernels,
-                   tdw_timing* timing) {
-  tdw_ctx* ctx = pb->ctx;
-  cudaStream_t st = ctx->stream;
-  if (!pb->assembled) return tdw_fail(ctx, TDW_ERR_STATE, "tdw_march before tdw_assemble");
-  if (!pb->known_loaded) return tdw_fail(ctx, TDW_ERR_STATE, "known boundary data not uploaded");
-  if (want_rhs) {
-    if (!pb->d_rhs)
-      TDW_CUDA(ctx, cudaMalloc(&pb->d_rhs, sizeof(double) * (size_t)(pb->nt - 1) * pb->ns));
-    TDW_CUDA(ctx, cudaMemsetAsync(pb->d_rhs, 0, sizeof(double) * (size_t)(pb->nt - 1) * pb->ns, st));
-  }
-  if (!pb->side) {
-    int lo = 0, hi = 0;
-    cudaDeviceGetStreamPriorityRange(&lo, &hi);
-    TDW_CUDA(ctx, cudaStreamCreateWithPriority(&pb->side, cudaStreamNonBlocking, lo));
-    pb->ev_solve.resize(pb->nt);
-    pb->ev_conv.resize(pb->nt);
-    for (auto& e : pb->ev_solve) TDW_CUDA(ctx, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    for (auto& e : pb->ev_conv) TDW_CUDA(ctx, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    TDW_CUDA(ctx, cudaEventCreateWithFlags(&pb->ev_fork, cudaEventDisableTiming));
-  }
-
-  LoopPlan L{};
   fill_conv_args(pb, L.c);
   {
     int rc = make_hist_map(pb, &L.hmap);
@@ -817,6 +728,132 @@ int tdw_march_loop(tdw_problem* pb, double threshold, bool want_rhs, bool time_k
   cs.maxit = pb->jac_iters;
   cs.trace = pb->d_trace;
 
+  return TDW_OK;
+}
+
+// zero flags and lag-2 buffers, write the known data of every step into the history
+int begin_loop(tdw_problem* pb, cudaStream_t st) {
+  tdw_ctx* ctx = pb->ctx;
+  TDW_CUDA(ctx, cudaMemsetAsync(pb->d_flags, 0, sizeof(int) * 4, st));
+  TDW_CUDA(ctx, cudaMemsetAsync(pb->d_bnear, 0, sizeof(double) * 2 * (size_t)pb->ns, st));
+  init_hist_kernel<<<2 * ctx->num_sms, 256, 0, st>>>(pb->d_hist, pb->hstride, pb->pad, pb->ns,
+                                                    pb->nt, pb->d_phi, pb->d_perm, pb->d_uk, pb->d_qk);
+  TDW_CUDA(ctx, cudaGetLastError());
+  return TDW_OK;
+}
+
+int launch_conv(tdw_problem* pb, LoopPlan& L, int alpha, cudaStream_t s) {
+  const size_t nb = (size_t)pb->nsplit * pb->rows_per_rank;
+  L.c.alpha = alpha;
+  L.c.bpart = pb->d_bpart + (alpha & 1) * nb;
+  conv_kernel<<<L.cgrid, TDW_CONV_THREADS, L.smem, s>>>(L.c, L.hmap);
+  TDW_CUDA(pb->ctx, cudaGetLastError());
+  return TDW_OK;
+}
+
+// own rows of b from the split partials (row-sharded runs, before the exchange)
+int launch_reduce(tdw_problem* pb, int alpha, cudaStream_t s) {
+  const size_t nb = (size_t)pb->nsplit * pb->rows_per_rank;
+  reduce_parts_kernel<<<(pb->rows_per_rank + 255) / 256, 256, 0, s>>>(
+      pb->d_bpart + (alpha & 1) * nb, pb->nsplit, pb->rows_per_rank, pb->d_b + pb->b_off,
+      pb->d_flags);
+  TDW_CUDA(pb->ctx, cudaGetLastError());
+  return TDW_OK;
+}
+
+int launch_solve(tdw_problem* pb, LoopPlan& L, int alpha, cudaStream_t s) {
+  const size_t nb = (size_t)pb->nsplit * pb->rows_per_rank;
+  cudaLaunchAttribute cattr[1];
+  cattr[0].id = cudaLaunchAttributeClusterDimension;
+  cattr[0].val.clusterDim.x = pb->sp_cl;
+  cattr[0].val.clusterDim.y = 1;
+  cattr[0].val.clusterDim.z = 1;
+  cudaLaunchConfig_t ccfg = {};
+  ccfg.gridDim = dim3(pb->sp_cl);
+  ccfg.blockDim = dim3(1024);
+  ccfg.dynamicSmemBytes = pb->sp_smem;
+  ccfg.stream = s;
+  ccfg.attrs = cattr;
+  ccfg.numAttrs = 1;
+  L.cs.alpha = alpha;
+  L.cs.bpart = pb->d_bpart + (alpha & 1) * nb;
+  L.cs.bnear_in = pb->d_bnear + (alpha & 1) * (size_t)pb->ns;
+  L.cs.bnear_out = pb->d_bnear + ((alpha + 1) & 1) * (size_t)pb->ns;
+  TDW_CUDA(pb->ctx, cudaLaunchKernelEx(&ccfg, solve_cluster_kernel, L.cs));
+  return TDW_OK;
+}
+
+// Enqueue one complete time loop.  Two streams: the far convolution F(alpha)
+// runs on the side stream as soon as the solve of step alpha-2 has finalized
+// the history it reads (lags >= 3; lag 1 = known data written up front; lag 2
+// = known component only), so F(alpha+1) overlaps the solve of step alpha.
+//   F(alpha)      waits solve(alpha-2)            writes bpart[alpha & 1]
+//   solve(alpha)  waits F(alpha), solve(alpha-1)  reads bpart[alpha & 1], bnear[alpha & 1]
+// Also used under stream capture (one CUDA graph per loop configuration).
+int enqueue_loop(tdw_problem* pb, LoopPlan& L, cudaEvent_t* ev_conv) {
+  tdw_ctx* ctx = pb->ctx;
+  cudaStream_t st = ctx->stream, sc = pb->side;
+  const int nt = pb->nt;
+  int rc = begin_loop(pb, st);
+  if (rc) return rc;
+  cudaEvent_t* evS = pb->ev_solve.data();  // solve(alpha) done
+  cudaEvent_t* evF = pb->ev_conv.data();   // F(alpha) done
+  TDW_CUDA(ctx, cudaEventRecord(pb->ev_fork, st));
+  TDW_CUDA(ctx, cudaStreamWaitEvent(sc, pb->ev_fork, 0));
+  for (int alpha = 1; alpha < nt; ++alpha) {
+    // far convolution of step alpha on the side stream
+    if (alpha >= 3) TDW_CUDA(ctx, cudaStreamWaitEvent(sc, evS[alpha - 2], 0));
+    if (ev_conv) TDW_CUDA(ctx, cudaEventRecordWithFlags(ev_conv[2 * (alpha - 1)], sc, cudaEventRecordExternal));
+    if ((rc = launch_conv(pb, L, alpha, sc))) return rc;
+    if (ev_conv) TDW_CUDA(ctx, cudaEventRecordWithFlags(ev_conv[2 * (alpha - 1) + 1], sc, cudaEventRecordExternal));
+    TDW_CUDA(ctx, cudaEventRecord(evF[alpha], sc));
+    // solve of step alpha on the main stream
+    TDW_CUDA(ctx, cudaStreamWaitEvent(st, evF[alpha], 0));
+    if (L.multi) {
+      if ((rc = launch_reduce(pb, alpha, st))) return rc;
+      ncclResult_t nr = ncclAllGather(pb->d_b + pb->b_off, pb->d_b, (size_t)pb->rows_per_rank,
+                                      ncclDouble, ctx->comm, st);
+      if (nr != ncclSuccess)
+        return tdw_fail(ctx, TDW_ERR_NCCL, std::string("ncclAllGather: ") + ncclGetErrorString(nr));
+    }
+    if ((rc = launch_solve(pb, L, alpha, st))) return rc;
+    TDW_CUDA(ctx, cudaEventRecord(evS[alpha], st));
+  }
+  // join the side stream
+  TDW_CUDA(ctx, cudaStreamWaitEvent(st, evF[nt - 1], 0));
+  TDW_CUDA(ctx, cudaGetLastError());
+  return TDW_OK;
+}
+
+}  // namespace
+
+int tdw_march_loop(tdw_problem* pb, double threshold, bool want_rhs, bool time_kernels,
+                   tdw_timing* timing) {
+  tdw_ctx* ctx = pb->ctx;
+  cudaStream_t st = ctx->stream;
+  if (!pb->assembled) return tdw_fail(ctx, TDW_ERR_STATE, "tdw_march before tdw_assemble");
+  if (!pb->known_loaded) return tdw_fail(ctx, TDW_ERR_STATE, "known boundary data not uploaded");
+  if (want_rhs) {
+    if (!pb->d_rhs)
+      TDW_CUDA(ctx, cudaMalloc(&pb->d_rhs, sizeof(double) * (size_t)(pb->nt - 1) * pb->ns));
+    TDW_CUDA(ctx, cudaMemsetAsync(pb->d_rhs, 0, sizeof(double) * (size_t)(pb->nt - 1) * pb->ns, st));
+  }
+  if (!pb->side) {
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    TDW_CUDA(ctx, cudaStreamCreateWithPriority(&pb->side, cudaStreamNonBlocking, lo));
+    pb->ev_solve.resize(pb->nt);
+    pb->ev_conv.resize(pb->nt);
+    for (auto& e : pb->ev_solve) TDW_CUDA(ctx, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    for (auto& e : pb->ev_conv) TDW_CUDA(ctx, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    TDW_CUDA(ctx, cudaEventCreateWithFlags(&pb->ev_fork, cudaEventDisableTiming));
+  }
+
+  LoopPlan L{};
+  {
+    int rc = make_plan(pb, L, threshold, want_rhs);
+    if (rc) return rc;
+  }
   const int nsteps = pb->nt - 1;
   std::vector<cudaEvent_t> evc;
   if (time_kernels) {
@@ -895,6 +932,48 @@ int tdw_march_loop(tdw_problem* pb, double threshold, bool want_rhs, bool time_k
     char msg[128];
     snprintf(msg, sizeof(msg), "step %d: solve residual too large", hflags[2]);
     return tdw_fail(ctx, TDW_ERR_RESIDUAL, msg);
+  }
+  return TDW_OK;
+}
+
+// Row-sharded loop of n problems (ranks) on ONE device and stream, the per-step
+// exchange emulated by device copies of each rank's own rows of b into every
+// rank's b (the in-place all-gather).  Test harness for the sharded code path
+// on a single GPU: no kernel waits on another, launches are sequential.
+int tdw_march_emulated_impl(tdw_problem** pbs, int n, double threshold) {
+  tdw_ctx* ctx = pbs[0]->ctx;
+  cudaStream_t st = ctx->stream;
+  std::vector<LoopPlan> L(n);
+  for (int r = 0; r < n; ++r) {
+    if (!pbs[r]->assembled || !pbs[r]->known_loaded)
+      return tdw_fail(ctx, TDW_ERR_STATE, "emulated march: shard not assembled or data missing");
+    int rc = make_plan(pbs[r], L[r], threshold, false);
+    if (!rc) rc = begin_loop(pbs[r], st);
+    if (rc) return rc;
+  }
+  const int nt = pbs[0]->nt;
+  const size_t rpr = (size_t)pbs[0]->rows_per_rank;
+  for (int alpha = 1; alpha < nt; ++alpha) {
+    for (int r = 0; r < n; ++r) {
+      int rc = launch_conv(pbs[r], L[r], alpha, st);
+      if (!rc) rc = launch_reduce(pbs[r], alpha, st);
+      if (rc) return rc;
+    }
+    for (int r = 0; r < n; ++r)
+      for (int q = 0; q < n; ++q)
+        if (q != r)
+          TDW_CUDA(ctx, cudaMemcpyAsync(pbs[q]->d_b + pbs[r]->b_off, pbs[r]->d_b + pbs[r]->b_off,
+                                        sizeof(double) * rpr, cudaMemcpyDeviceToDevice, st));
+    for (int r = 0; r < n; ++r) {
+      int rc = launch_solve(pbs[r], L[r], alpha, st);
+      if (rc) return rc;
+    }
+  }
+  TDW_CUDA(ctx, cudaStreamSynchronize(st));
+  for (int r = 0; r < n; ++r) {
+    int hflags[4];
+    TDW_CUDA(ctx, cudaMemcpy(hflags, pbs[r]->d_flags, sizeof(hflags), cudaMemcpyDeviceToHost));
+    if (hflags[0] == 2) return tdw_fail(ctx, TDW_ERR_RESIDUAL, "emulated march: residual too large");
   }
   return TDW_OK;
 }

@@ -54,6 +54,7 @@ struct tdw_problem {
   int nranks = 1, rank = 0;
   // rows (internal order); rank r owns [row_lo, row_hi); rows_per_rank multiple of TDW_TI
   int rows_per_rank = 0, row_lo = 0, row_hi = 0, n_iblk = 0, ntiles = 0;
+  int b_off = 0;                   // rank * rows_per_rank: this rank's block of the gathered b
   // ordering: internal index -> original element index
   std::vector<int> perm;
   int* d_perm = nullptr;
@@ -139,3 +140,5 @@ int tdw_march_loop(tdw_problem* pb, double threshold, bool want_rhs, bool time_k
 int tdw_outputs(tdw_problem* pb, double* u, double* q, double* tau, double* sigma);
 int tdw_time_conv_impl(tdw_problem* pb, int n, float* ms_out);
 int tdw_setup_cluster_solver(tdw_problem* pb);
+int tdw_march_emulated_impl(tdw_problem** pbs, int n, double threshold);
+int tdw_problem_create_impl(tdw_ctx* ctx, const tdw_problem_desc* dsc, tdw_problem** out, bool shard_only);

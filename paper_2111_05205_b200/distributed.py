@@ -72,3 +72,27 @@ def gather_rows(dist, own: np.ndarray, ns: int) -> np.ndarray:
     out = [torch.zeros(rpr, dtype=torch.float64) for _ in range(world)]
     dist.all_gather(out, t)
     return torch.cat(out).numpy()[:ns]
+
+
+def march_emulated(spec, nranks: int, window: bool = True, blowup_factor: float = 1e6):
+    """Run the row-sharded march of `nranks` shards on ONE GPU (tdw_march_emulated):
+    every shard assembles only its rows; the per-step all-gather is emulated by
+    device copies.  Returns the TimeHistory of every shard (they solve the same
+    system redundantly, so all of them hold the full history)."""
+    import ctypes as C
+
+    from . import marching
+    shards = [marching.BandStore(spec, window=window, nranks=nranks, rank=r, shard_only=True).assemble()
+              for r in range(nranks)]
+    uk, qk = marching.greville_samples(spec)
+    for sh in shards:
+        sh.upload_known(uk, qk)
+    arr = (C.c_void_p * nranks)(*[sh.h.value for sh in shards])
+    thr = blowup_factor * max(spec.blowup_reference, 1e-30)
+    _lib.check(_lib.load().tdw_march_emulated(arr, nranks, float(thr)), shards[0].ctx.h,
+               "tdw_march_emulated")
+    out = [sh.download() for sh in shards]
+    infos = [sh.info() for sh in shards]
+    for sh in shards:
+        sh.close()
+    return out, infos

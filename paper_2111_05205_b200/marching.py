@@ -125,7 +125,7 @@ class BandStore:
     """Device-resident banded coefficient store + lag-1 step matrix (tdw_problem)."""
 
     def __init__(self, spec, window: bool = True, ctx: _lib.Context | None = None,
-                 nranks: int = 1, rank: int = 0):
+                 nranks: int = 1, rank: int = 0, shard_only: bool = False):
         self.ctx = ctx or _lib.default_context()
         lib = _lib.load()
         mesh = spec.mesh
@@ -134,6 +134,7 @@ class BandStore:
         self._phi = np.ascontiguousarray(spec.phi, dtype=np.float64)
         self.ns = mesh.n_elements
         self.nt = int(spec.nt)
+        self._spec_basis = spec.basis
         self.window = bool(window)
         desc = _lib.ProblemDesc(
             ns=self.ns, nv=len(self._v), vertices=_lib.dptr(self._v),
@@ -142,8 +143,10 @@ class BandStore:
             dt=float(spec.basis.dt), nt=self.nt, window=int(self.window), nranks=int(nranks),
             rank=int(rank))
         self.h = C.c_void_p()
-        _lib.check(lib.tdw_problem_create(self.ctx.h, C.byref(desc), C.byref(self.h)), self.ctx.h,
+        create = lib.tdw_problem_create_shard if shard_only else lib.tdw_problem_create
+        _lib.check(create(self.ctx.h, C.byref(desc), C.byref(self.h)), self.ctx.h,
                    "tdw_problem_create")
+        self.nranks, self.rank = int(nranks), int(rank)
         self.assembled = False
 
     def assemble(self):
@@ -178,6 +181,18 @@ class BandStore:
                                                   int(time_kernels), C.byref(t)),
                    self.ctx.h, "tdw_march_resident")
         return t.asdict()
+
+    def download(self) -> "TimeHistory":
+        """Device history -> TimeHistory (after run_resident / an emulated march)."""
+        hist = TimeHistory(self._spec_basis, self.nt, self.ns)
+        n_steps, status = C.c_int32(0), C.c_int32(0)
+        _lib.check(_lib.load().tdw_download(self.h, _lib.dptr(hist.u), _lib.dptr(hist.q),
+                                            _lib.dptr(hist.tau), _lib.dptr(hist.sigma),
+                                            C.byref(n_steps), C.byref(status)), self.ctx.h,
+                   "tdw_download")
+        hist.n_steps = int(n_steps.value)
+        hist.status = "unstable" if status.value else "stable"
+        return hist
 
     def time_conv(self, n: int = 20) -> float:
         """Average device ms of one history-convolution launch (inputs resident)."""

@@ -1,0 +1,45 @@
+"""The row-sharded (multi-GPU) code path, emulated on one B200.
+
+tdw_march_emulated runs R shards (ranks) in one process on one device: each
+shard assembles only its rows of the banded store and convolves them, reduces
+its split partials into its block of b, the in-place all-gather is replaced by
+device copies, and every shard runs the redundant cluster solve.  Only the NCCL
+call itself is not exercised (it is a plain in-place ncclAllGather).  Results
+must equal the single-rank march (the per-row partial sums are grouped
+differently, so agreement is to round-off, not bitwise) and all shards must
+hold identical histories.
+"""
+import numpy as np
+import pytest
+
+from conftest import per_step_rel
+from paper_2111_05205_b200 import distributed, marching, scenarios
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("cfg,nranks", [(0, 2), (0, 3), (1, 2), (2, 2), (2, 4), (2, 8)])
+def test_sharded_equals_single_rank(cfg, nranks):
+    spec = scenarios.build_spec(cfg)
+    ref = marching.march(spec)
+    hs, infos = distributed.march_emulated(spec, nranks)
+    rows = [(i["row_lo"], i["row_hi"]) for i in infos]
+    assert rows[0][0] == 0 and max(hi for _, hi in rows) == spec.mesh.n_elements
+    assert sum(i["n_pairs"] for i in infos) > 0
+    x_ref = ref.u if spec.phi[0] == 1.0 else ref.q
+    for h in hs:
+        assert h.status == ref.status and h.n_steps == ref.n_steps
+        x = h.u if spec.phi[0] == 1.0 else h.q
+        assert per_step_rel(x, x_ref).max() < 1e-11
+        np.testing.assert_array_equal(h.u, hs[0].u)
+        np.testing.assert_array_equal(h.q, hs[0].q)
+
+
+def test_shards_partition_the_band():
+    """The shards' stores partition the single-rank store (same band entries)."""
+    spec = scenarios.build_spec(0)
+    full = marching.BandStore(spec).assemble().info()
+    shards = [marching.BandStore(spec, nranks=3, rank=r, shard_only=True).assemble().info()
+              for r in range(3)]
+    assert sum(s["n_band"] for s in shards) == full["n_band"]
+    assert sum(s["n_pairs"] for s in shards) == full["n_pairs"]
