@@ -296,8 +296,9 @@ int tdw_problem_create_impl(tdw_ctx* ctx, const tdw_problem_desc* dsc, tdw_probl
   }
   TDW_TRY(cudaMalloc(&pb->d_bpart, sizeof(double) * (size_t)pb->nsplit * pb->rows_per_rank));
   TDW_TRY(cudaMemset(pb->d_bpart, 0, sizeof(double) * (size_t)pb->nsplit * pb->rows_per_rank));
-  TDW_TRY(cudaMalloc(&pb->d_b, sizeof(double) * (size_t)nranks * pb->rows_per_rank));
-  TDW_TRY(cudaMemset(pb->d_b, 0, sizeof(double) * (size_t)nranks * pb->rows_per_rank));
+  pb->bstride = (size_t)nranks * pb->rows_per_rank;
+  TDW_TRY(cudaMalloc(&pb->d_b, sizeof(double) * 2 * pb->bstride));
+  TDW_TRY(cudaMemset(pb->d_b, 0, sizeof(double) * 2 * pb->bstride));
   TDW_TRY(cudaMalloc(&pb->d_x, sizeof(double) * 2 * (size_t)ns));
   TDW_TRY(cudaMalloc(&pb->d_hist, sizeof(double2) * (size_t)ns * pb->hstride));
   TDW_TRY(cudaMalloc(&pb->d_bar, sizeof(unsigned) * 2));

@@ -18,6 +18,7 @@
 #include <climits>
 #include <cstdio>
 #include <cstdlib>
+#include <string>
 #include <algorithm>
 #include <vector>
 
@@ -566,6 +567,205 @@ __global__ void __launch_bounds__(1024, 1) solve_cluster_kernel(ClusterSolveArgs
   trace_mark(tr, 8);
 }
 
+// Register-resident variant of the cluster solve, for slices of <= 1024 rows
+// with <= MAXNZ off-diagonal entries per row: thread t of CTA r owns row
+// r*R + t for the whole solve, keeps its (packed column, value) pairs, 1/A_ii
+// and b_i in registers, and per sweep issues all neighbour loads (own shared
+// memory or a peer's via DSMEM) before one fused multiply-add chain.  The
+// convergence test (every 4th sweep) folds warp maxima into a 3-deep ring of
+// shared-memory slots with atomicMax on the (non-negative) double bits: peers
+// read slot c%3 after the sweep barrier, slot (c+1)%3 is cleared meanwhile.
+template <int MAXNZ>
+constexpr int reg_threads() { return MAXNZ <= 8 ? 1024 : (MAXNZ <= 16 ? 512 : 256); }
+
+template <int MAXNZ>
+__global__ void __launch_bounds__(reg_threads<MAXNZ>(), 1) solve_reg_kernel(ClusterSolveArgs a) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  __shared__ double xs[2][1024];
+  __shared__ unsigned long long chk[3][2];
+  __shared__ double shred[64];
+  __shared__ double red2[4];
+  if (*(volatile int*)&a.flags[0] != 0) return;
+  const int cr = (int)cl.block_rank();
+  const int CL = (int)cl.num_blocks();
+  const int R = a.R;
+  const int r0 = cr * R;
+  const int nr = max(0, min(R, a.ns - r0));
+  const int tid = threadIdx.x;
+  const bool own = tid < nr;
+  const int gi = r0 + tid;
+  const int beta0 = a.alpha - 1;
+  unsigned long long* tr = a.trace ? a.trace + (size_t)a.alpha * 16 : nullptr;
+  trace_mark(tr, 0);
+  int c[MAXNZ];
+  double v[MAXNZ];
+  int nz = 0;
+  double bi = 0.0, invd = 0.0, di = 1.0;
+  if (own) {
+    const long long nz0 = a.sp_nnzoff[cr];
+    const int p0 = a.sp_rowptr[(size_t)cr * (R + 1) + tid];
+    nz = a.sp_rowptr[(size_t)cr * (R + 1) + tid + 1] - p0;
+#pragma unroll
+    for (int k = 0; k < MAXNZ; ++k) {
+      c[k] = k < nz ? __ldg(a.sp_col + nz0 + p0 + k) : (cr << 24);
+      v[k] = k < nz ? __ldg(a.sp_val + nz0 + p0 + k) : 0.0;
+    }
+    if (a.nsplit > 0) bi = sum_parts(a.bpart + (size_t)gi * a.nsplit, a.nsplit);
+    else bi = __ldcg(a.b + gi);
+    bi += a.bnear_in[gi];
+    di = a.diag[gi];
+    invd = 1.0 / di;
+    xs[0][tid] = bi * invd;
+    if (a.rhs) a.rhs[(size_t)beta0 * a.ns + a.perm[gi]] = bi;
+  }
+  if (tid < 6) chk[tid >> 1][tid & 1] = 0ull;
+  trace_mark(tr, 1);
+  cl.sync();
+  trace_mark(tr, 2);
+  int cur = 0, sweeps = 0, ncheck = 0;
+  __shared__ int s_stop;
+  for (int it = 1; it <= a.maxit; ++it) {
+    const double* src = xs[cur];
+    const bool check = (it & 3) == 0 && it < a.maxit;
+    if (check && tid < 2) chk[(ncheck + 1) % 3][tid] = 0ull;
+    double xn = 0.0;
+    if (own) {
+      double xv[MAXNZ];
+#pragma unroll
+      for (int k = 0; k < MAXNZ; ++k) xv[k] = k < nz ? fetch_x(c[k], src, cr, cl) : 0.0;
+      double s0 = bi, s1 = 0.0;
+#pragma unroll
+      for (int k = 0; k < MAXNZ; k += 2) {
+        s0 = fma(-v[k], xv[k], s0);
+        if (k + 1 < MAXNZ) s1 = fma(-v[k + 1], xv[k + 1], s1);
+      }
+      xn = (s0 + s1) * invd;
+      xs[cur ^ 1][tid] = xn;
+    }
+    if (check) {
+      double dmax = own ? fabs(xn - src[tid]) : 0.0, xmax = fabs(xn);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        dmax = fmax(dmax, __shfl_xor_sync(FULLMASK, dmax, o));
+        xmax = fmax(xmax, __shfl_xor_sync(FULLMASK, xmax, o));
+      }
+      if ((tid & 31) == 0) {
+        atomicMax(&chk[ncheck % 3][0], (unsigned long long)__double_as_longlong(dmax));
+        atomicMax(&chk[ncheck % 3][1], (unsigned long long)__double_as_longlong(xmax));
+      }
+    }
+    cl.sync();
+    cur ^= 1;
+    sweeps = it;
+    if (check) {
+      if (tid < 32) {
+        unsigned long long D = 0, X = 0;
+        if (tid < CL) {
+          const unsigned long long* rr = cl.map_shared_rank(&chk[ncheck % 3][0], tid);
+          D = rr[0];
+          X = rr[1];
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          D = max(D, __shfl_xor_sync(FULLMASK, D, o));
+          X = max(X, __shfl_xor_sync(FULLMASK, X, o));
+        }
+        if (tid == 0)
+          s_stop = __longlong_as_double((long long)D) <= 1e-15 * __longlong_as_double((long long)X);
+      }
+      __syncthreads();
+      ++ncheck;
+      if (s_stop) break;
+    }
+  }
+  trace_mark(tr, 3);
+  if (tr && tid == 0 && cr == 0) tr[15] = sweeps;
+  const double* xf = xs[cur];
+  double r2 = 0.0, b2 = 0.0, xm = 0.0, xi = 0.0;
+  if (own) {
+    xi = xf[tid];
+    double xv[MAXNZ];
+#pragma unroll
+    for (int k = 0; k < MAXNZ; ++k) xv[k] = k < nz ? fetch_x(c[k], xf, cr, cl) : 0.0;
+    double acc = di * xi - bi;
+#pragma unroll
+    for (int k = 0; k < MAXNZ; ++k) acc = fma(v[k], xv[k], acc);
+    r2 = acc * acc;
+    b2 = bi * bi;
+    xm = fabs(xi);
+  }
+  r2 = block_reduce_sum(r2, shred);
+  b2 = block_reduce_sum(b2, shred);
+  xm = block_reduce_max(xm, shred);
+  if (tid == 0) { red2[0] = r2; red2[1] = b2; red2[2] = xm; }
+  trace_mark(tr, 4);
+  cl.sync();
+  trace_mark(tr, 5);
+  // lag-2 term of the unknown density for the next step (x still in shared memory)
+  if (own) {
+    double acc = 0.0;
+    for (int k0 = 0; k0 < a.near_w; k0 += 16) {
+      int cc[16];
+      double vv[16], xv[16];
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        const bool on = k0 + q < a.near_w;
+        cc[q] = on ? __ldg(a.ncol + (size_t)(k0 + q) * a.ns + gi) : (cr << 24);
+        vv[q] = on ? __ldg(a.nval + (size_t)(k0 + q) * a.ns + gi) : 0.0;
+      }
+#pragma unroll
+      for (int q = 0; q < 16; ++q) xv[q] = fetch_x(cc[q], xf, cr, cl);
+#pragma unroll
+      for (int q = 0; q < 16; ++q) acc = fma(vv[q], xv[q], acc);
+    }
+    a.bnear_out[gi] = acc;
+  }
+  double RR = 0.0, BB = 0.0, XM = 0.0;
+  if (tid < 32) {
+    if (tid < CL) {
+      const double* rr = cl.map_shared_rank(red2, tid);
+      RR = rr[0];
+      BB = rr[1];
+      XM = rr[2];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      RR += __shfl_xor_sync(FULLMASK, RR, o);
+      BB += __shfl_xor_sync(FULLMASK, BB, o);
+      XM = fmax(XM, __shfl_xor_sync(FULLMASK, XM, o));
+    }
+    if (tid == 0) { shred[0] = RR; shred[1] = BB; shred[2] = XM; }
+  }
+  trace_mark(tr, 6);
+  cl.sync();  // no CTA leaves while another may still read its shared memory
+  trace_mark(tr, 7);
+  RR = shred[0];
+  BB = shred[1];
+  XM = shred[2];
+  if (sqrt(RR) > 1e-10 * fmax(sqrt(BB), 1e-300)) {
+    if (cr == 0 && tid == 0) {
+      a.flags[2] = a.alpha;
+      atomicExch(&a.flags[0], 2);
+    }
+    return;
+  }
+  const bool unstable = XM > a.threshold;
+  if (own) {
+    const int o = a.perm[gi];
+    const double ph = a.phi[gi];
+    const size_t kb = (size_t)beta0 * a.ns + o;
+    const double qv = ph == 1.0 ? a.qk[kb] : xi;
+    const double uv = ph == 1.0 ? xi : a.uk[kb];
+    a.hist[(size_t)gi * a.hstride + a.pad + beta0] = make_double2(qv, uv);
+  }
+  if (cr == 0 && tid == 0) {
+    a.flags[1] = a.alpha;
+    if (unstable) atomicExch(&a.flags[0], 1);
+  }
+  trace_mark(tr, 8);
+}
+
 // hist[j][pad + beta] = known part (phi q_known, (1-phi) u_known) of every
 // step; the solve of step beta+1 overwrites it with the full (q, u).  Zero pad
 // for beta < 0.
@@ -721,7 +921,7 @@ int make_plan(tdw_problem* pb, LoopPlan& L, double threshold, bool want_rhs) {
   cs.hstride = pb->hstride;
   cs.pad = pb->pad;
   cs.ns = pb->ns;
-  cs.nsplit = L.multi ? 0 : pb->nsplit;
+  cs.nsplit = 0;  // the convolution's last arriver already summed the splits into b
   cs.rows_loc = pb->rows_per_rank;
   cs.nt = pb->nt;
   cs.R = pb->sp_R;
@@ -747,15 +947,10 @@ int launch_conv(tdw_problem* pb, LoopPlan& L, int alpha, cudaStream_t s) {
   L.c.alpha = alpha;
   L.c.bpart = pb->d_bpart + (alpha & 1) * nb;
   conv_kernel<<<L.cgrid, TDW_CONV_THREADS, L.smem, s>>>(L.c, L.hmap);
-  TDW_CUDA(pb->ctx, cudaGetLastError());
-  return TDW_OK;
-}
-
-// own rows of b from the split partials (row-sharded runs, before the exchange)
-int launch_reduce(tdw_problem* pb, int alpha, cudaStream_t s) {
-  const size_t nb = (size_t)pb->nsplit * pb->rows_per_rank;
-  reduce_parts_kernel<<<(pb->rows_per_rank + 255) / 256, 256, 0, s>>>(
-      pb->d_bpart + (alpha & 1) * nb, pb->nsplit, pb->rows_per_rank, pb->d_b + pb->b_off,
+  // fixed-order sum of the split partials into this step's b (own rows), on the
+  // convolution's stream: off the solve's critical path
+  reduce_parts_kernel<<<(pb->rows_per_rank + 127) / 128, 128, 0, s>>>(
+      L.c.bpart, pb->nsplit, pb->rows_per_rank, pb->d_b + (alpha & 1) * pb->bstride + pb->b_off,
       pb->d_flags);
   TDW_CUDA(pb->ctx, cudaGetLastError());
   return TDW_OK;
@@ -770,16 +965,24 @@ int launch_solve(tdw_problem* pb, LoopPlan& L, int alpha, cudaStream_t s) {
   cattr[0].val.clusterDim.z = 1;
   cudaLaunchConfig_t ccfg = {};
   ccfg.gridDim = dim3(pb->sp_cl);
-  ccfg.blockDim = dim3(1024);
+  ccfg.blockDim = dim3(pb->sp_reg == 0 ? 1024 : (pb->sp_reg == 8 ? 1024 : (pb->sp_reg == 16 ? 512 : 256)));
   ccfg.dynamicSmemBytes = pb->sp_smem;
   ccfg.stream = s;
   ccfg.attrs = cattr;
   ccfg.numAttrs = 1;
   L.cs.alpha = alpha;
   L.cs.bpart = pb->d_bpart + (alpha & 1) * nb;
+  L.cs.b = pb->d_b + (alpha & 1) * pb->bstride;
   L.cs.bnear_in = pb->d_bnear + (alpha & 1) * (size_t)pb->ns;
   L.cs.bnear_out = pb->d_bnear + ((alpha + 1) & 1) * (size_t)pb->ns;
-  TDW_CUDA(pb->ctx, cudaLaunchKernelEx(&ccfg, solve_cluster_kernel, L.cs));
+  if (pb->sp_reg > 0) {
+    ccfg.dynamicSmemBytes = 0;
+    if (pb->sp_reg == 8) TDW_CUDA(pb->ctx, cudaLaunchKernelEx(&ccfg, solve_reg_kernel<8>, L.cs));
+    else if (pb->sp_reg == 16) TDW_CUDA(pb->ctx, cudaLaunchKernelEx(&ccfg, solve_reg_kernel<16>, L.cs));
+    else TDW_CUDA(pb->ctx, cudaLaunchKernelEx(&ccfg, solve_reg_kernel<24>, L.cs));
+  } else {
+    TDW_CUDA(pb->ctx, cudaLaunchKernelEx(&ccfg, solve_cluster_kernel, L.cs));
+  }
   return TDW_OK;
 }
 
@@ -810,9 +1013,9 @@ int enqueue_loop(tdw_problem* pb, LoopPlan& L, cudaEvent_t* ev_conv) {
     // solve of step alpha on the main stream
     TDW_CUDA(ctx, cudaStreamWaitEvent(st, evF[alpha], 0));
     if (L.multi) {
-      if ((rc = launch_reduce(pb, alpha, st))) return rc;
-      ncclResult_t nr = ncclAllGather(pb->d_b + pb->b_off, pb->d_b, (size_t)pb->rows_per_rank,
-                                      ncclDouble, ctx->comm, st);
+      double* bb = pb->d_b + (alpha & 1) * pb->bstride;
+      ncclResult_t nr = ncclAllGather(bb + pb->b_off, bb, (size_t)pb->rows_per_rank, ncclDouble,
+                                      ctx->comm, st);
       if (nr != ncclSuccess)
         return tdw_fail(ctx, TDW_ERR_NCCL, std::string("ncclAllGather: ") + ncclGetErrorString(nr));
     }
@@ -956,13 +1159,14 @@ int tdw_march_emulated_impl(tdw_problem** pbs, int n, double threshold) {
   for (int alpha = 1; alpha < nt; ++alpha) {
     for (int r = 0; r < n; ++r) {
       int rc = launch_conv(pbs[r], L[r], alpha, st);
-      if (!rc) rc = launch_reduce(pbs[r], alpha, st);
       if (rc) return rc;
     }
+    const size_t par = (size_t)(alpha & 1);
     for (int r = 0; r < n; ++r)
       for (int q = 0; q < n; ++q)
         if (q != r)
-          TDW_CUDA(ctx, cudaMemcpyAsync(pbs[q]->d_b + pbs[r]->b_off, pbs[r]->d_b + pbs[r]->b_off,
+          TDW_CUDA(ctx, cudaMemcpyAsync(pbs[q]->d_b + par * pbs[q]->bstride + pbs[r]->b_off,
+                                        pbs[r]->d_b + par * pbs[r]->bstride + pbs[r]->b_off,
                                         sizeof(double) * rpr, cudaMemcpyDeviceToDevice, st));
     for (int r = 0; r < n; ++r) {
       int rc = launch_solve(pbs[r], L[r], alpha, st);
@@ -1044,11 +1248,35 @@ int tdw_setup_cluster_solver(tdw_problem* pb) {
   TDW_CUDA(ctx, cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
   const size_t budget = (size_t)maxsm - 4096;  // static shared memory of the kernel
   pb->sp_cl = 0;
-  // about one row per thread (latency-bound sweeps), more CTAs only if the slice must shrink
+  pb->sp_reg = 0;
+  int maxoff = 0;
+  for (int i = 0; i < ns; ++i) {
+    int k2 = 0;
+    for (int k = 0; k < pb->ell_w; ++k) k2 += acol[(size_t)k * ns + i] != i;
+    maxoff = std::max(maxoff, k2);
+  }
+  const char* solver_env = getenv("TDW_SOLVER");
+  const bool smem_only = solver_env && std::string(solver_env) == "smem";
+  const char* cl_env = getenv("TDW_SOLVE_CL");
+  if (!smem_only && maxoff <= 24) {
+    // register-resident solver: one row per thread, thread count by register budget
+    const int mz = maxoff <= 8 ? 8 : (maxoff <= 16 ? 16 : 24);
+    const int T = mz == 8 ? 1024 : (mz == 16 ? 512 : 256);
+    int CL = 1;
+    while (CL < 16 && (ns + CL - 1) / CL > T) CL *= 2;
+    if (cl_env) CL = std::max(CL, std::min(16, atoi(cl_env)));
+    if ((ns + CL - 1) / CL <= T) {
+      pb->sp_reg = mz;
+      pb->sp_cl = CL;
+      pb->sp_R = (ns + CL - 1) / CL;
+      pb->sp_smem = 0;
+    }
+  }
+  // shared-memory solver: about one row per thread, more CTAs only if the slice must shrink
   int cl0 = 1;
   while (cl0 < 16 && (ns + cl0 - 1) / cl0 > 1024) cl0 *= 2;
-  if (const char* e = getenv("TDW_SOLVE_CL")) cl0 = std::max(1, std::min(16, atoi(e)));
-  for (int CL = cl0; CL <= 16; CL *= 2) {
+  if (cl_env) cl0 = std::max(1, std::min(16, atoi(cl_env)));
+  for (int CL = cl0; CL <= 16 && pb->sp_cl == 0; CL *= 2) {
     const int R = (ns + CL - 1) / CL;
     size_t worst = 0;
     for (int c = 0; c < CL; ++c) {
@@ -1063,7 +1291,6 @@ int tdw_setup_cluster_solver(tdw_problem* pb) {
       pb->sp_cl = CL;
       pb->sp_R = R;
       pb->sp_smem = smem;
-      break;
     }
   }
   if (pb->sp_cl == 0)
@@ -1111,8 +1338,12 @@ int tdw_setup_cluster_solver(tdw_problem* pb) {
   }
   TDW_CUDA(ctx, cudaFuncSetAttribute(solve_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)pb->sp_smem));
-  if (CL > 8)
+  if (CL > 8) {
     TDW_CUDA(ctx, cudaFuncSetAttribute(solve_cluster_kernel,
                                        cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    TDW_CUDA(ctx, cudaFuncSetAttribute(solve_reg_kernel<8>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    TDW_CUDA(ctx, cudaFuncSetAttribute(solve_reg_kernel<16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    TDW_CUDA(ctx, cudaFuncSetAttribute(solve_reg_kernel<24>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  }
   return TDW_OK;
 }

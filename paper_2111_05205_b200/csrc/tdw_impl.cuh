@@ -103,7 +103,8 @@ struct tdw_problem {
   bool known_loaded = false;
   int nsplit = 1;                  // == conv_S once assembled
   double* d_bpart = nullptr;       // [2][nsplit][rows_per_rank] (step parity)
-  double* d_b = nullptr;           // [nranks * rows_per_rank]
+  double* d_b = nullptr;           // [2][bstride] (step parity), bstride = nranks * rows_per_rank
+  size_t bstride = 0;
   double* d_x = nullptr;           // [2][ns]
   double* d_red = nullptr;         // reduction scratch [3][grid]
   unsigned* d_bar = nullptr;       // grid barrier {count, generation}
@@ -114,6 +115,7 @@ struct tdw_problem {
   int solve_grid = 0;
   // cluster solver (csrc/march.cu solve_cluster_kernel); sp_cl == 0 -> grid-barrier fallback
   int sp_cl = 0, sp_R = 0;
+  int sp_reg = 0;                  // >0: register-resident solver with that many off-diagonal slots
   size_t sp_smem = 0;
   int* d_sp_rowptr = nullptr;
   long long* d_sp_nnzoff = nullptr;
