@@ -204,6 +204,58 @@ def make_tree(cfg, leaf_capacity=20):
     print(f"tree cfg{cfg}: leaf={tree.leaf_level} near={len(tree.near_pairs[0])}")
 
 
+def make_fmm_setup():
+    """Setup math of the FMM from the reference: interpolation rows, transfer
+    matrices, the triangle rule, cmp_coeff, Toeplitz kernel tensors and the
+    materialised M2L matrix (fmm_interp.py, fmm.py:44-162).  The node-offset sign
+    of _KernelCache._positions is corrected by
+    substituting a positions function written here; everything else is the
+    reference's own code path."""
+    from tdwavebem import fmm, fmm_interp
+    from tdwavebem.fmm_tree import build_tree
+
+    def positions_fixed(self, level, offset):
+        h = self.tree.levels[level].half_width
+        off = np.asarray(offset, float) * 2.0 * h
+        g = -h * self._node_diff
+        d = [off[k] + g for k in range(3)]
+        return np.sqrt(d[0][:, None, None] ** 2 + d[1][None, :, None] ** 2 + d[2][None, None, :] ** 2)
+
+    fmm._KernelCache._positions = positions_fixed
+    rng = np.random.default_rng(11)
+    out = dict(versions=VERSIONS)
+    for p in (4, 5, 6):
+        sch = fmm_interp.InterpScheme(p)
+        xi = rng.uniform(-1.0, 1.0, 200)
+        xe = rng.uniform(-1.9, 1.9, 200)
+        out[f"interp{p}_xi"], out[f"interp{p}_xe"] = xi, xe
+        out[f"interp{p}_w"], out[f"interp{p}_dw"] = sch.weights(xi), sch.dweights(xi)
+        out[f"interp{p}_we"], out[f"interp{p}_dwe"] = sch.weights(xe, 1.0), sch.dweights(xe, 1.0)
+        out[f"interp{p}_t0"], out[f"interp{p}_t1"] = sch.transfer(0), sch.transfer(1)
+    E = rng.uniform(-1, 1, (3, 3))
+    out["tri_E"] = E
+    out["tri_pts"], out["tri_w"] = fmm_interp.triangle_gauss_rule(E)
+    out["cmp"] = np.array([[p, m, k, fmm.cmp_coeff(p, m, k)] for p in (2, 3) for m in range(p - 1)
+                           for k in range(0, 9)], dtype=float)
+    spec = build_spec(1)
+    tree = build_tree(spec.mesh, spec.c, spec.basis.dt, 20, 8)
+    for d in (1, 2):
+        cache = fmm._KernelCache(tree, d, 4, 4)
+        lev = tree.leaf_level
+        offs = tree.levels[lev].il_offsets[[0, len(tree.levels[lev].il_offsets) // 2, -1]]
+        out[f"kc{d}_level"] = lev
+        out[f"kc{d}_offsets"] = offs
+        for k, off in enumerate(offs):
+            for pp in range(0, d + 1):
+                out[f"kc{d}_{k}_{pp}"] = cache.get(lev, off, pp)
+            out[f"kc{d}_{k}_dark"] = np.array([cache.lag_is_dark(lev, off, l) for l in range(1, 10)])
+        out[f"m2l{d}"] = fmm.dense_m2l_matrix(tree, d, 4, 4, lev, offs[1], 3, 0)
+        if d == 2:
+            out["m2l2_p1"] = fmm.dense_m2l_matrix(tree, d, 4, 4, lev, offs[1], tree.mu + 1, 1)
+    np.savez_compressed(OUT / "fmm_setup.npz", **out)
+    print("fmm_setup.npz")
+
+
 if __name__ == "__main__":
     what = sys.argv[1]
     if what == "coeff":
@@ -212,5 +264,7 @@ if __name__ == "__main__":
         make_march(int(sys.argv[2]))
     elif what == "tree":
         make_tree(int(sys.argv[2]))
+    elif what == "fmm_setup":
+        make_fmm_setup()
     else:
         raise SystemExit(__doc__)
