@@ -136,6 +136,52 @@ int tdw_set_graph(tdw_problem* pb, int enable);
 
 int tdw_problem_destroy(tdw_problem* pb);
 
+/* Interpolation space-time FMM (configs 3-4; reference fmm.py fast_march, corrected).
+ * Operator data from the host planner (paper_2111_05205_b200/fmm_plan.py); per-
+ * element arrays in the caller's element order, per-level arrays concatenated
+ * over levels 2..leaf.  Call after tdw_problem_create and before tdw_assemble;
+ * tdw_march then runs the fast solver (near field = banded store of adjacent
+ * leaf cells with window gamma_near). */
+typedef struct {
+  int32_t ps, pt, mu, leaf;          /* ps = pt = 4, mu <= 8 supported                  */
+  int32_t gamma_near;
+  int32_t n_leaf_cells;
+  const int64_t* leaf_coords;        /* (ns, 3) leaf-cell coordinates of each element   */
+  const int64_t* elem_cell;          /* (ns,) leaf cell index                           */
+  const double* p2m_tau;             /* (ns, ps^3) P2M rows (value)                     */
+  const double* p2m_sig;             /* (ns, ps^3) P2M rows (normal derivative)         */
+  const double* l2p_val;             /* (ns, ps^3) L2P rows                             */
+  const double* l2p_bm;              /* (ns, ps^3) Burton-Miller L2P rows or NULL       */
+  const double* t_space;             /* (2, ps, ps) child->parent re-anchoring          */
+  const double* t_time;              /* (2, pt, pt)                                     */
+  int32_t n_levels;                  /* leaf - 1                                        */
+  const int32_t* lev_ncell;
+  const double* lev_interval;
+  const int64_t* lev_parent;         /* concat(ncell): parent in level L-1 (-1 at L=2)  */
+  const int64_t* lev_octant;         /* concat(ncell, 3)                                */
+  const int32_t* lev_noff;
+  const uint8_t* lev_dark;           /* concat(noff, mu+1)                              */
+  const double* lev_K0;              /* concat(noff, (2ps-1)^3, (mu+2)(pt-1)+1)         */
+  const double* lev_Kp;              /* concat over levels of (d, noff, (2ps-1)^3, 2pt-1) */
+  const int64_t* lev_nil;
+  const int64_t* lev_obs_ptr;        /* concat(ncell+1): interaction pairs by observer  */
+  const int64_t* lev_il_src;
+  const int64_t* lev_il_off;         /* offset index within the level                   */
+  int32_t n_extra;
+  const int32_t* extra_lags;
+  const int64_t* extra_npair;
+  const int64_t* extra_i;            /* concat(npair), caller's element order           */
+  const int64_t* extra_j;
+  const int64_t* ticks_before;       /* (nt,) last leaf tick to run before step alpha   */
+  const int64_t* k_obs;              /* (nt,) observation interval of step alpha        */
+  const double* wt;                  /* (nt, pt) L2P time weights                       */
+  const double* dwt;                 /* (nt, pt) their time derivative / c              */
+  const double* wts;                 /* (nt, pt) P2M time weights of step alpha's source */
+  const int64_t* extra_gmax;         /* (n_extra, nt) same-interval lag limit           */
+} tdw_fmm_desc;
+
+int tdw_fmm_setup(tdw_problem* pb, const tdw_fmm_desc* desc);
+
 /* Test harness of the row-sharded path on ONE device: create the shard of rank
  * desc->rank of desc->nranks without a communicator, then run all shards in one
  * process with the per-step all-gather emulated by device copies.  Every shard

@@ -72,6 +72,7 @@ EXPORTS = {
     "tdw_time_conv": ([C.c_void_p, C.c_int, C.POINTER(C.c_float)], C.c_int),
     "tdw_set_graph": ([C.c_void_p, C.c_int], C.c_int),
     "tdw_problem_destroy": ([C.c_void_p], C.c_int),
+    "tdw_fmm_setup": ([C.c_void_p, C.c_void_p], C.c_int),
     "tdw_problem_create_shard": ([C.c_void_p, C.POINTER(ProblemDesc), C.POINTER(C.c_void_p)], C.c_int),
     "tdw_march_emulated": ([C.POINTER(C.c_void_p), C.c_int, C.c_double], C.c_int),
     "tdw_nccl_unique_id": ([C.c_char_p], C.c_int),

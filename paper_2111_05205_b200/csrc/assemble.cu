@@ -138,8 +138,19 @@ __device__ __forceinline__ void bspline_weights(int d, double* w) {
   if (d == 3) { w[0] = 1.0 / 6.0; w[1] = -(2.0 / 3.0); w[2] = 1.0; w[3] = -(2.0 / 3.0); w[4] = 1.0 / 6.0; }
 }
 
+// FMM near field: only pairs whose leaf cells are adjacent (fmm_tree.py:163-177)
+__device__ __forceinline__ bool pair_allowed(const int* leafc, int i, int j) {
+  if (!leafc) return true;
+  const int a = leafc[i], b = leafc[j];
+  const int dx = (a & 1023) - (b & 1023), dy = ((a >> 10) & 1023) - ((b >> 10) & 1023),
+            dz = ((a >> 20) & 1023) - ((b >> 20) & 1023);
+  return dx >= -1 && dx <= 1 && dy >= -1 && dy <= 1 && dz >= -1 && dz <= 1;
+}
+
 struct AsmArgs {
   const double* elem;
+  const int* leafc;                    // packed leaf-cell coords (FMM near field) or null
+  int split_lag2;                      // 1: lag-2 entries keep the known density only
   int ns, row_lo, rows_loc, ntiles, d, cap;
   double c, dt, K;
   uint32_t* hdr;
@@ -163,7 +174,7 @@ __global__ void __launch_bounds__(256) count_kernel(AsmArgs a) {
   const double cdt = a.c * a.dt;
   int len = 0, glo = 0;
   bool any = false;
-  if (i < a.ns && j < a.ns) {
+  if (i < a.ns && j < a.ns && pair_allowed(a.leafc, i, j)) {
     Elem ej;
     load_elem(a.elem, j, ej);
     const double* ci = a.elem + (size_t)i * TDW_ELEM_STRIDE + 12;
@@ -262,7 +273,7 @@ __global__ void __launch_bounds__(128) fill_kernel(AsmArgs a) {
         vu += w[q] * ru[q];
         vw += w[q] * rw[q];
       }
-      if (gg == TDW_NEAR_LAGS) {
+      if (gg == TDW_NEAR_LAGS && a.split_lag2) {
         // lag 2: keep only the coefficient of the KNOWN density of element j
         // (q if phi_j = 1, u if phi_j = 0); the unknown one is applied by the
         // solve of the previous step (near structure), so the convolution of
@@ -323,6 +334,8 @@ __global__ void unit_layout_kernel(const unsigned long long* segcount, const uin
 
 struct NearArgs {
   const double* elem;
+  const int* leafc;
+  int split_lag2;
   const double* phi;
   int ns, ntiles, d, cap;
   double c, dt, K;
@@ -367,13 +380,13 @@ __global__ void __launch_bounds__(128) near_kernel(NearArgs a) {
       load_elem(a.elem, j, ej);
       double dx = ci[0] - ej.c[0], dy = ci[1] - ej.c[1], dz = ci[2] - ej.c[2];
       double dcc = sqrt(dx * dx + dy * dy + dz * dz);
-      if (dcc - ej.rad <= (TDW_NEAR_LAGS + 1) * cdt * (1.0 + 1e-9)) {
+      if (dcc - ej.rad <= (TDW_NEAR_LAGS + 1) * cdt * (1.0 + 1e-9) && pair_allowed(a.leafc, i, j)) {
         b = pair_band(ci, ej, cdt, a.d, a.cap);
         cand = true;
       }
     }
     const bool has1 = cand && b.glo <= 1 && b.ghi >= 1;
-    const bool has2 = cand && b.glo <= 2 && b.ghi >= 2;
+    const bool has2 = a.split_lag2 && cand && b.glo <= 2 && b.ghi >= 2;
     const unsigned m1 = __ballot_sync(FULLMASK, has1);
     const unsigned m2 = __ballot_sync(FULLMASK, has2);
     const int apos = acnt + __popc(m1 & ((1u << lane) - 1u));
@@ -522,6 +535,8 @@ int tdw_assemble_impl(tdw_problem* pb) {
 
   AsmArgs a{};
   a.elem = pb->d_elem;
+  a.leafc = pb->d_leafc;
+  a.split_lag2 = pb->split_lag2;
   a.ns = pb->ns;
   a.row_lo = pb->row_lo;
   a.rows_loc = pb->rows_per_rank;
@@ -609,6 +624,8 @@ int tdw_assemble_impl(tdw_problem* pb) {
   TDW_CUDA(ctx, cudaMemsetAsync(d_ellw, 0, sizeof(int), st));
   NearArgs s{};
   s.elem = pb->d_elem;
+  s.leafc = pb->d_leafc;
+  s.split_lag2 = pb->split_lag2;
   s.phi = pb->d_phi;
   s.ns = pb->ns;
   s.ntiles = pb->ntiles;
@@ -688,20 +705,35 @@ int tdw_assemble_impl(tdw_problem* pb) {
   {
     const int G = pb->conv_grid, S = pb->conv_S;
     const long long items = (long long)pb->n_iblk * S;
-    std::vector<unsigned> sched, soff(G + 1, 0);
+    std::vector<unsigned> sched, sitem, soff(G + 1, 0);
     sched.reserve(nunit);
+    sitem.reserve(nunit);
     for (int b = 0; b < G; ++b) {
       soff[b] = (unsigned)sched.size();
       for (long long it2 = b; it2 < items; it2 += G) {
         const long long iblk = it2 / S, sp = it2 % S;
         const int tb = (int)(sp * pb->ntiles / S), te = (int)((sp + 1) * pb->ntiles / S);
-        for (int t = tb; t < te; ++t) sched.push_back((unsigned)(iblk * pb->ntiles + t));
+        const size_t before = sched.size();
+        for (int t = tb; t < te; ++t) {
+          const long long u = iblk * pb->ntiles + t;
+          // units without band entries (FMM near field: non-adjacent patches) are not streamed
+          if (uoff[u + 1] - uoff[u] > TDW_UNIT_COEF_OFF || !pb->skip_empty_units) {
+            sched.push_back((unsigned)u);
+            sitem.push_back((unsigned)it2);
+          }
+        }
+        if (sched.size() == before) {  // nothing to stream: an entry that only flushes zeros
+          sched.push_back(TDW_EMPTY_UNIT);
+          sitem.push_back((unsigned)it2);
+        }
       }
     }
     soff[G] = (unsigned)sched.size();
     TDW_CUDA(ctx, cudaMalloc(&pb->d_sched, sizeof(unsigned) * std::max<size_t>(1, sched.size())));
     TDW_CUDA(ctx, cudaMalloc(&pb->d_sched_off, sizeof(unsigned) * (G + 1)));
     TDW_CUDA(ctx, cudaMemcpy(pb->d_sched, sched.data(), sizeof(unsigned) * sched.size(), cudaMemcpyHostToDevice));
+    TDW_CUDA(ctx, cudaMalloc(&pb->d_sched_item, sizeof(unsigned) * std::max<size_t>(1, sitem.size())));
+    TDW_CUDA(ctx, cudaMemcpy(pb->d_sched_item, sitem.data(), sizeof(unsigned) * sitem.size(), cudaMemcpyHostToDevice));
     TDW_CUDA(ctx, cudaMemcpy(pb->d_sched_off, soff.data(), sizeof(unsigned) * (G + 1), cudaMemcpyHostToDevice));
     pb->nsplit = S;
     cudaFree(pb->d_bpart);

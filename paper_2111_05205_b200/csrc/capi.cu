@@ -461,6 +461,7 @@ int tdw_problem_destroy(tdw_problem* pb) {
   if (!pb) return TDW_OK;
   cudaSetDevice(pb->ctx->device);
   void* ptrs[] = {pb->d_perm, pb->d_elem, pb->d_phi, pb->d_units, pb->d_unit_off, pb->d_sched, pb->d_sched_off,
+                  pb->d_sched_item, pb->d_leafc,
                   pb->d_unit, pb->d_acol, pb->d_aval, pb->d_adiag, pb->d_hist, pb->d_uk,
                   pb->d_qk, pb->d_bpart, pb->d_b, pb->d_x, pb->d_red, pb->d_bar, pb->d_flags,
                   pb->d_rhs, pb->d_sp_rowptr, pb->d_sp_nnzoff, pb->d_sp_col, pb->d_sp_val,
@@ -468,6 +469,7 @@ int tdw_problem_destroy(tdw_problem* pb) {
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (pb->graph_exec) cudaGraphExecDestroy(pb->graph_exec);
+  if (pb->fmm) tdw_fmm_free(pb->fmm);
   for (auto& e : pb->ev_solve) cudaEventDestroy(e);
   for (auto& e : pb->ev_conv) cudaEventDestroy(e);
   if (pb->ev_fork) cudaEventDestroy(pb->ev_fork);

@@ -1,0 +1,802 @@
+// fmm.cu -- interpolation space-time FMM on the device (configs 3-4).
+//
+// Restates the corrected fast solver (reference pkg/src/tdwavebem/fmm.py:165-531
+// with the SURVEY.md 8(c) corrections; CPU restatement oracle/fmm_oracle.py):
+//   near field   the banded store restricted to adjacent leaf cells, window gamma_near
+//                (fmm.py:213-235, 446-457) -- assemble.cu / conv_kernel
+//   extra lists  same-interval pairs of marginal interaction pairs, raw lag form
+//                (fmm.py:223-234, 459-470)                           -- extra_*_kernel
+//   L2P          leaf locals at the observation time (fmm.py:474-495) -- l2p_kernel
+//   P2M          the step's source into its interval's leaf moment (fmm.py:509-521) -- p2m_kernel
+//   tick         M2L (near-future lags + derivative operators + Algorithm-1
+//                recurrence, fmm.py:329-368) -- m2l_kernel; M2M up while the
+//                time-half bit is 1, L2L down into inherit slots (fmm.py:371-419)
+//                -- m2m_kernel / l2l_kernel
+// Interpolation orders ps = pt = 4 (BASELINE), mu <= 8.  The operator data is
+// built on the host (paper_2111_05205_b200/fmm_plan.py) and handed over by
+// tdw_fmm_setup; the per-step control flow (which ticks run before which step)
+// is a fixed schedule, so the loop is a plain sequence of launches.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "coeff.cuh"
+#include "tdw_impl.cuh"
+
+#define FULLMASK 0xffffffffu
+constexpr int FPS = 4;               // spatial nodes per dimension
+constexpr int FPT = 4;               // temporal nodes
+constexpr int FN3 = FPS * FPS * FPS; // 64
+constexpr int FND = FN3 * FPT;       // 256
+constexpr int FKR = (2 * FPS - 1) * (2 * FPS - 1) * (2 * FPS - 1);  // 343 Toeplitz rows
+constexpr int FMU_MAX = 8;
+
+struct FmmLevel {
+  int L = 0, ncell = 0, noff = 0;
+  double interval = 0.0;
+  int* parent = nullptr;       // [ncell] index in level L-1
+  int* octant = nullptr;       // [ncell] bits x | y<<1 | z<<2
+  int* child_ptr = nullptr;    // [ncell+1] children at level L+1 (ascending)
+  int* child_idx = nullptr;
+  long long* obs_ptr = nullptr;  // [ncell+1]
+  int* il_src = nullptr;
+  int* il_off = nullptr;
+  unsigned* dark = nullptr;    // [noff] bit l-1 set: lag l dark
+  double* K0 = nullptr;        // [noff][343][ntau0]
+  double* Kp = nullptr;        // [d][noff][343][ntaup]
+  double *own = nullptr, *inherit = nullptr, *deriv = nullptr, *aux = nullptr, *acc = nullptr,
+         *mom = nullptr;
+};
+
+struct FmmExtra {
+  int lags = 0;
+  long long npair = 0;
+  int* row_ptr = nullptr;      // [ns+1] internal rows
+  int* col = nullptr;          // [npair] internal columns
+  int* row_of = nullptr;       // [npair]
+  double *U = nullptr, *W = nullptr;  // [npair][lags]
+  std::vector<long long> gmax; // per step
+};
+
+struct FmmState {
+  int mu = 8, leaf = 0, ntau0 = 0, ntaup = 0, n_leaf_cells = 0;
+  std::vector<FmmLevel> lev;   // index = level (entries < 2 unused)
+  int* elem_cell = nullptr;    // [ns] internal order
+  int* cell_ptr = nullptr;     // [ncell+1] leaf cell -> internal elements
+  int* cell_elems = nullptr;
+  double *p2m_tau = nullptr, *p2m_sig = nullptr, *l2p_val = nullptr, *l2p_bm = nullptr;
+  double t_space[2][FPS][FPS], t_time[2][FPT][FPT];
+  std::vector<FmmExtra> extra;
+  std::vector<long long> ticks_before, k_obs;
+  std::vector<double> wt, dwt, wts;  // [nt][FPT]
+};
+
+namespace {
+
+struct Tr {  // transfer matrices by value (kernel argument)
+  double s[2][FPS][FPS], t[2][FPT][FPT];
+};
+
+__device__ __forceinline__ void bw(int d, double* w) {
+  if (d == 1) { w[0] = 1.0; w[1] = -2.0; w[2] = 1.0; }
+  if (d == 2) { w[0] = 0.5; w[1] = -1.5; w[2] = 1.5; w[3] = -0.5; }
+  if (d == 3) { w[0] = 1.0 / 6.0; w[1] = -(2.0 / 3.0); w[2] = 1.0; w[3] = -(2.0 / 3.0); w[4] = 1.0 / 6.0; }
+}
+
+// tau_j^beta / sigma_j^beta (stock sums, marching.py:205-214) from the history;
+// slot beta holds the known part until step beta+1 is solved (tilde sums).
+__device__ __forceinline__ double2 stock(const double2* __restrict__ hist, int hstride, int pad,
+                                         int j, int beta, int d, const double* w) {
+  double t = 0.0, s = 0.0;
+  const int kmax = min(d + 1, beta);
+  const double2* h = hist + (size_t)j * hstride + pad + beta;
+  for (int k = 0; k <= kmax; ++k) {
+    const double2 v = h[-k];
+    t += w[k] * v.x;
+    s += w[k] * v.y;
+  }
+  return make_double2(t, s);
+}
+
+// ---------------------------------------------------------------- extra lists
+template <int D, bool BM>
+__global__ void extra_coeff_kernel(const double* __restrict__ elem, const int* __restrict__ row_of,
+                                   const int* __restrict__ col, long long npair, int lags, double c,
+                                   double dt, double K, double* U, double* W) {
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < npair;
+       p += (long long)gridDim.x * blockDim.x) {
+    const int i = row_of[p], j = col[p];
+    const double* pi = elem + (size_t)i * TDW_ELEM_STRIDE;
+    const double* pj = elem + (size_t)j * TDW_ELEM_STRIDE;
+    double ci[3] = {pi[12], pi[13], pi[14]}, nx[3] = {-pi[9], -pi[10], -pi[11]};
+    // reference arrival (marching.py:108-110): U = 0 before it
+    double dx = ci[0] - pj[12], dy = ci[1] - pj[13], dz = ci[2] - pj[14];
+    double dist = fmax(sqrt(dx * dx + dy * dy + dz * dz) - pj[15], 0.0);
+    int arr = max((int)ceil(dist / (c * dt)) - 1, 1);
+    tdw::PairGeom g;
+    tdw::pair_geom<BM>(ci, pj, pj + 3, pj + 6, pj + 9, nx, g);
+    for (int q = 1; q <= lags; ++q) {
+      double u = 0.0, w = 0.0;
+      if (q >= arr) tdw::coeff_eval<D, BM>(g, (double)q * c * dt, K, u, w);
+      U[p * lags + q - 1] = u;
+      W[p * lags + q - 1] = w;
+    }
+  }
+}
+
+__global__ void extra_apply_kernel(const int* __restrict__ row_ptr, const int* __restrict__ col,
+                                   const double* __restrict__ U, const double* __restrict__ W,
+                                   int lags, int gmax, const double2* __restrict__ hist, int hstride,
+                                   int pad, int alpha, int d, int ns, double* b, const int* flags) {
+  if (flags[0] != 0) return;
+  double w[5] = {0, 0, 0, 0, 0};
+  bw(d, w);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < ns; i += gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    for (int p = row_ptr[i]; p < row_ptr[i + 1]; ++p) {
+      const int j = col[p];
+      for (int g = 1; g <= gmax; ++g) {
+        const double2 ts = stock(hist, hstride, pad, j, alpha - g, d, w);
+        acc += U[(size_t)p * lags + g - 1] * ts.x - W[(size_t)p * lags + g - 1] * ts.y;
+      }
+    }
+    b[i] += acc;
+  }
+}
+
+// ---------------------------------------------------------------- L2P / P2M
+struct StepW {
+  double wt[FPT], dwt[FPT], wts[FPT];
+};
+
+__global__ void l2p_kernel(const int* __restrict__ elem_cell, const double* __restrict__ own,
+                           const double* __restrict__ inherit, int ko_own, int ko_inh, int ncell,
+                           const double* __restrict__ lval, const double* __restrict__ lbm, StepW sw,
+                           int ns, double* b, const int* flags) {
+  if (flags[0] != 0) return;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < ns; j += gridDim.x * blockDim.x) {
+    const int cell = elem_cell[j];
+    const double* lo = own + ((size_t)ko_own * ncell + cell) * FND;
+    const double* li = inherit + ((size_t)ko_inh * ncell + cell) * FND;
+    double acc = 0.0;
+    for (int a = 0; a < FN3; ++a) {
+      double v = 0.0, dv = 0.0;
+#pragma unroll
+      for (int m = 0; m < FPT; ++m) {
+        const double L = lo[a * FPT + m] + li[a * FPT + m];
+        v += L * sw.wt[m];
+        dv += L * sw.dwt[m];
+      }
+      if (lbm) acc += lbm[(size_t)j * FN3 + a] * v - lval[(size_t)j * FN3 + a] * dv;
+      else acc += lval[(size_t)j * FN3 + a] * v;
+    }
+    b[j] += acc;
+  }
+}
+
+__global__ void p2m_kernel(const int* __restrict__ cell_ptr, const int* __restrict__ cell_elems,
+                           const double* __restrict__ ptau, const double* __restrict__ psig,
+                           const double2* __restrict__ hist, int hstride, int pad, int beta0, int d,
+                           StepW sw, double* acc, const int* flags) {
+  if (flags[0] != 0) return;
+  double w[5] = {0, 0, 0, 0, 0};
+  bw(d, w);
+  const int cell = blockIdx.x, s = threadIdx.x;  // 64 threads: spatial node
+  double spat = 0.0;
+  for (int q = cell_ptr[cell]; q < cell_ptr[cell + 1]; ++q) {
+    const int e = cell_elems[q];
+    const double2 ts = stock(hist, hstride, pad, e, beta0, d, w);
+    spat += ptau[(size_t)e * FN3 + s] * ts.x - psig[(size_t)e * FN3 + s] * ts.y;
+  }
+  double* A = acc + (size_t)cell * FND + s * FPT;
+#pragma unroll
+  for (int t = 0; t < FPT; ++t) A[t] += spat * sw.wts[t];
+}
+
+// ---------------------------------------------------------------- M2L + recurrence
+struct M2LArgs {
+  const long long* obs_ptr;
+  const int* il_src;
+  const int* il_off;
+  const unsigned* dark;
+  const double* K0;
+  const double* Kp;
+  const double* mom;
+  double *own, *deriv, *aux;
+  int ncell, noff, ntau0, ntaup, mu, d, k;
+  double T;  // c * interval
+};
+
+__device__ __forceinline__ double cmp_coeff_dev(int p, int m, int k) {
+  // comb(p, m) ((k-1)^(p-m) - 2 k^(p-m) + (k+1)^(p-m)) (-1)^m   (fmm.py:44-49)
+  double binom = 1.0;
+  for (int q = 0; q < m; ++q) binom = binom * (p - q) / (q + 1);
+  const int e = p - m;
+  double km = 1.0, k0 = 1.0, kp = 1.0;
+  for (int q = 0; q < e; ++q) { km *= (k - 1); k0 *= k; kp *= (k + 1); }
+  return binom * (km - 2.0 * k0 + kp) * ((m & 1) ? -1.0 : 1.0);
+}
+
+// One CTA per observation cell, thread a = spatial node (a1, a2, a3); every
+// thread owns the 4 time nodes of its node for the mu+1 near-future lags and
+// the d derivative operators.  L[a,m] += sum_{b,n} K[a-b+P, m-n+toff] M[b,n]
+// (fmm.py:52-69); the Toeplitz rows are read through L1 (85 KB per offset).
+template <int D>
+__global__ void __launch_bounds__(FN3) m2l_kernel(M2LArgs A) {
+  const int cell = blockIdx.x, a = threadIdx.x;
+  const int a1 = a >> 4, a2 = (a >> 2) & 3, a3 = a & 3;
+  __shared__ double Ms[FND];
+  double acc[FMU_MAX + 1][FPT];
+  double tp[3][FPT];
+#pragma unroll
+  for (int l = 0; l <= FMU_MAX; ++l)
+#pragma unroll
+    for (int m = 0; m < FPT; ++m) acc[l][m] = 0.0;
+#pragma unroll
+  for (int p = 0; p < 3; ++p)
+#pragma unroll
+    for (int m = 0; m < FPT; ++m) tp[p][m] = 0.0;
+  for (long long q = A.obs_ptr[cell]; q < A.obs_ptr[cell + 1]; ++q) {
+    const int src = A.il_src[q], off = A.il_off[q];
+    __syncthreads();
+    bool nz = false;
+#pragma unroll
+    for (int n = 0; n < FPT; ++n) {
+      const double v = A.mom[(size_t)src * FND + a * FPT + n];
+      Ms[a * FPT + n] = v;
+      nz |= v != 0.0;
+    }
+    if (!__syncthreads_or(nz)) continue;  // live sources only (fmm.py:337-338)
+    const unsigned dk = A.dark[off];
+    const double* K0o = A.K0 + (size_t)off * FKR * A.ntau0;
+    for (int b = 0; b < FN3; ++b) {
+      const int b1 = b >> 4, b2 = (b >> 2) & 3, b3 = b & 3;
+      const int row = ((a1 - b1 + FPS - 1) * (2 * FPS - 1) + (a2 - b2 + FPS - 1)) * (2 * FPS - 1) +
+                      (a3 - b3 + FPS - 1);
+      double Mb[FPT];
+#pragma unroll
+      for (int n = 0; n < FPT; ++n) Mb[n] = Ms[b * FPT + n];
+      const double* kr = K0o + (size_t)row * A.ntau0;
+#pragma unroll
+      for (int l = 1; l <= FMU_MAX + 1; ++l) {
+        if (l > A.mu + 1 || ((dk >> (l - 1)) & 1u)) continue;
+        const int toff = l * (FPT - 1);
+        double kw[2 * FPT - 1];
+#pragma unroll
+        for (int t = 0; t < 2 * FPT - 1; ++t) kw[t] = __ldg(kr + toff - (FPT - 1) + t);
+#pragma unroll
+        for (int m = 0; m < FPT; ++m)
+#pragma unroll
+          for (int n = 0; n < FPT; ++n) acc[l - 1][m] = fma(kw[m - n + FPT - 1], Mb[n], acc[l - 1][m]);
+      }
+#pragma unroll
+      for (int p = 0; p < D; ++p) {
+        const double* kp = A.Kp + (((size_t)p * A.noff + off) * FKR + row) * A.ntaup;
+        double kw[2 * FPT - 1];
+#pragma unroll
+        for (int t = 0; t < 2 * FPT - 1; ++t) kw[t] = __ldg(kp + t);
+#pragma unroll
+        for (int m = 0; m < FPT; ++m)
+#pragma unroll
+          for (int n = 0; n < FPT; ++n) tp[p][m] = fma(kw[m - n + FPT - 1], Mb[n], tp[p][m]);
+      }
+    }
+  }
+  const int ring = A.mu + 3;
+  const size_t cs = (size_t)A.ncell * FND, base = (size_t)cell * FND + a * FPT;
+#pragma unroll
+  for (int l = 1; l <= FMU_MAX + 1; ++l) {
+    if (l > A.mu + 1) continue;
+    double* o = A.own + (size_t)((A.k + l) % ring) * cs + base;
+#pragma unroll
+    for (int m = 0; m < FPT; ++m) o[m] += acc[l - 1][m];
+  }
+  // distant-future recurrence (fmm.py:355-367)
+#pragma unroll
+  for (int p = 1; p <= D; ++p) {
+    double* dv = A.deriv + (size_t)(p - 1) * cs + base;
+#pragma unroll
+    for (int m = 0; m < FPT; ++m) {
+      double upd = tp[p - 1][m];
+#pragma unroll
+      for (int mm = 0; mm <= p - 2; ++mm) {
+        const int ai = (p - 2) * (p - 1) / 2 + mm;
+        upd = upd + cmp_coeff_dev(p, mm, A.k) * A.aux[(size_t)ai * cs + base + m];
+      }
+      dv[m] += upd;
+    }
+  }
+  const double* prev = A.own + (size_t)((A.k + A.mu + 1) % ring) * cs + base;
+  double* nxt = A.own + (size_t)((A.k + A.mu + 2) % ring) * cs + base;
+  double pv[FPT];
+#pragma unroll
+  for (int m = 0; m < FPT; ++m) pv[m] = prev[m];
+  // own_slot(k+mu+2) = own_slot(k+mu+1) + sum_p deriv_p T^p, added in p order
+#pragma unroll
+  for (int m = 0; m < FPT; ++m) {
+    double v = pv[m];
+    double Tq = 1.0;
+#pragma unroll
+    for (int p = 1; p <= D; ++p) {
+      Tq *= A.T;
+      v += A.deriv[(size_t)(p - 1) * cs + base + m] * Tq;
+    }
+    nxt[m] = v;
+  }
+#pragma unroll
+  for (int p = 2; p <= D; ++p)
+#pragma unroll
+    for (int mm = 0; mm <= p - 2; ++mm) {
+      const int ai = (p - 2) * (p - 1) / 2 + mm;
+      double km = 1.0;
+      for (int q = 0; q < mm; ++q) km *= (double)A.k;
+      for (int m = 0; m < FPT; ++m) A.aux[(size_t)ai * cs + base + m] += tp[p - 1][m] * km;
+    }
+}
+
+// ---------------------------------------------------------------- M2M / L2L
+// index order of a 256-vector: ((a1*4 + a2)*4 + a3)*4 + m
+__device__ __forceinline__ void mode_product(double* X, double* Y, const double (*T)[FPS],
+                                             int mode, bool transpose, int e) {
+  // e = output element index; Y[e] = sum_k T'[out_k][k] X[e with index(mode) = k]
+  int idx[4] = {e >> 6, (e >> 4) & 3, (e >> 2) & 3, e & 3};
+  const int o = idx[mode];
+  double s = 0.0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    idx[mode] = k;
+    const int src = ((idx[0] * 4 + idx[1]) * 4 + idx[2]) * 4 + idx[3];
+    s += (transpose ? T[k][o] : T[o][k]) * X[src];
+  }
+  Y[e] = s;
+}
+
+__global__ void __launch_bounds__(FND) m2m_kernel(const int* __restrict__ child_ptr,
+                                                  const int* __restrict__ child_idx,
+                                                  const int* __restrict__ octant,
+                                                  const double* __restrict__ mom_child, int half,
+                                                  Tr tr, double* acc_parent) {
+  const int P = blockIdx.x, e = threadIdx.x;
+  __shared__ double X[FND], Y[FND];
+  double sum = 0.0;
+  for (int q = child_ptr[P]; q < child_ptr[P + 1]; ++q) {
+    const int c = child_idx[q];
+    const double v = mom_child[(size_t)c * FND + e];
+    __syncthreads();
+    X[e] = v;
+    if (!__syncthreads_or(v != 0.0)) continue;
+    const int oc = octant[c];
+    mode_product(X, Y, tr.s[oc & 1], 0, false, e);
+    __syncthreads();
+    mode_product(Y, X, tr.s[(oc >> 1) & 1], 1, false, e);
+    __syncthreads();
+    mode_product(X, Y, tr.s[(oc >> 2) & 1], 2, false, e);
+    __syncthreads();
+    mode_product(Y, X, tr.t[half], 3, false, e);
+    __syncthreads();
+    sum += X[e];
+  }
+  acc_parent[(size_t)P * FND + e] += sum;
+}
+
+__global__ void __launch_bounds__(FND) l2l_kernel(const int* __restrict__ parent,
+                                                  const int* __restrict__ octant,
+                                                  const double* __restrict__ own_p,
+                                                  const double* __restrict__ inh_p, Tr tr,
+                                                  double* inh_c0, double* inh_c1) {
+  const int c = blockIdx.x, e = threadIdx.x;
+  const int P = parent[c];
+  __shared__ double X[FND], Y[FND], Z[FND];
+  const double tot = own_p[(size_t)P * FND + e] + inh_p[(size_t)P * FND + e];
+  Z[e] = tot;
+  const bool nz = __syncthreads_or(tot != 0.0);
+  const int oc = octant[c];
+  for (int half = 0; half < 2; ++half) {
+    double* out = half ? inh_c1 : inh_c0;
+    if (!nz) {
+      out[(size_t)c * FND + e] = 0.0;
+      continue;
+    }
+    __syncthreads();
+    mode_product(Z, X, tr.s[oc & 1], 0, true, e);
+    __syncthreads();
+    mode_product(X, Y, tr.s[(oc >> 1) & 1], 1, true, e);
+    __syncthreads();
+    mode_product(Y, X, tr.s[(oc >> 2) & 1], 2, true, e);
+    __syncthreads();
+    mode_product(X, Y, tr.t[half], 3, true, e);
+    __syncthreads();
+    out[(size_t)c * FND + e] = Y[e];
+  }
+}
+
+template <typename T>
+int up(tdw_ctx* ctx, T** dst, const T* src, size_t n) {
+  TDW_CUDA(ctx, cudaMalloc(dst, sizeof(T) * std::max<size_t>(n, 1)));
+  if (n) TDW_CUDA(ctx, cudaMemcpy(*dst, src, sizeof(T) * n, cudaMemcpyHostToDevice));
+  return TDW_OK;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ setup
+extern "C" int tdw_fmm_setup(tdw_problem* pb, const tdw_fmm_desc* fd) {
+  if (!pb || !fd) return TDW_ERR_INVALID_ARG;
+  tdw_ctx* ctx = pb->ctx;
+  cudaSetDevice(ctx->device);
+  if (pb->assembled) return tdw_fail(ctx, TDW_ERR_STATE, "tdw_fmm_setup must precede tdw_assemble");
+  if (fd->ps != FPS || fd->pt != FPT || fd->mu < 1 || fd->mu > FMU_MAX)
+    return tdw_fail(ctx, TDW_ERR_LIMIT, "FMM supports ps = pt = 4 and mu <= 8");
+  if (pb->nranks != 1) return tdw_fail(ctx, TDW_ERR_LIMIT, "FMM path is single-GPU in this build");
+  const int ns = pb->ns, nt = pb->nt, d = pb->d;
+  FmmState* F = new FmmState();
+  pb->fmm = F;
+  F->mu = fd->mu;
+  F->leaf = fd->leaf;
+  F->ntau0 = (fd->mu + 2) * (FPT - 1) + 1;
+  F->ntaup = 2 * (FPT - 1) + 1;
+  F->n_leaf_cells = fd->n_leaf_cells;
+  std::vector<int> inv(ns);
+  for (int k = 0; k < ns; ++k) inv[pb->perm[k]] = k;
+  // near-field filter, window and history padding
+  std::vector<int> leafc(ns), ecell(ns);
+  for (int k = 0; k < ns; ++k) {
+    const int o = pb->perm[k];
+    leafc[k] = (int)(fd->leaf_coords[3 * o] | (fd->leaf_coords[3 * o + 1] << 10) |
+                     (fd->leaf_coords[3 * o + 2] << 20));
+    ecell[k] = (int)fd->elem_cell[o];
+  }
+  int rc = up(ctx, &pb->d_leafc, leafc.data(), ns);
+  if (rc) return rc;
+  pb->split_lag2 = 0;
+  pb->skip_empty_units = true;
+  pb->cap = std::min(fd->gamma_near, nt - 1);
+  pb->n_lags = pb->cap;
+  int maxlag = pb->cap;
+  for (int x = 0; x < fd->n_extra; ++x) maxlag = std::max(maxlag, fd->extra_lags[x]);
+  pb->pad = maxlag + d + 2;
+  pb->hstride = pb->pad + nt - 1;
+  cudaFree(pb->d_hist);
+  TDW_CUDA(ctx, cudaMalloc(&pb->d_hist, sizeof(double2) * (size_t)ns * pb->hstride));
+  // leaf element data, internal order
+  if ((rc = up(ctx, &F->elem_cell, ecell.data(), ns))) return rc;
+  {
+    std::vector<int> cptr(F->n_leaf_cells + 1, 0), celems;
+    std::vector<std::vector<int>> lists(F->n_leaf_cells);
+    for (int k = 0; k < ns; ++k) lists[ecell[k]].push_back(k);
+    for (int c = 0; c < F->n_leaf_cells; ++c) {
+      cptr[c + 1] = cptr[c] + (int)lists[c].size();
+      for (int k : lists[c]) celems.push_back(k);
+    }
+    if ((rc = up(ctx, &F->cell_ptr, cptr.data(), cptr.size()))) return rc;
+    if ((rc = up(ctx, &F->cell_elems, celems.data(), celems.size()))) return rc;
+  }
+  auto rows = [&](const double* src, double** dst) -> int {
+    if (!src) return TDW_OK;
+    std::vector<double> v((size_t)ns * FN3);
+    for (int k = 0; k < ns; ++k)
+      std::copy(src + (size_t)pb->perm[k] * FN3, src + (size_t)(pb->perm[k] + 1) * FN3, &v[(size_t)k * FN3]);
+    return up(ctx, dst, v.data(), v.size());
+  };
+  if ((rc = rows(fd->p2m_tau, &F->p2m_tau))) return rc;
+  if ((rc = rows(fd->p2m_sig, &F->p2m_sig))) return rc;
+  if ((rc = rows(fd->l2p_val, &F->l2p_val))) return rc;
+  if (pb->bie == TDW_BIE_BMBIE && (rc = rows(fd->l2p_bm, &F->l2p_bm))) return rc;
+  for (int h = 0; h < 2; ++h)
+    for (int i = 0; i < FPS; ++i)
+      for (int j = 0; j < FPS; ++j) {
+        F->t_space[h][i][j] = fd->t_space[(h * FPS + i) * FPS + j];
+        F->t_time[h][i][j] = fd->t_time[(h * FPT + i) * FPT + j];
+      }
+  // levels
+  F->lev.resize(F->leaf + 1);
+  long long oc = 0, oo = 0, oil = 0, optr = 0, ok0 = 0, okp = 0;
+  std::vector<std::vector<int>> parents(F->leaf + 1), octs(F->leaf + 1);
+  for (int li = 0; li < fd->n_levels; ++li) {
+    const int L = 2 + li;
+    FmmLevel& V = F->lev[L];
+    V.L = L;
+    V.ncell = fd->lev_ncell[li];
+    V.noff = fd->lev_noff[li];
+    V.interval = fd->lev_interval[li];
+    std::vector<int> par(V.ncell), octv(V.ncell);
+    for (int c = 0; c < V.ncell; ++c) {
+      par[c] = (int)fd->lev_parent[oc + c];
+      octv[c] = (int)(fd->lev_octant[3 * (oc + c)] | (fd->lev_octant[3 * (oc + c) + 1] << 1) |
+                      (fd->lev_octant[3 * (oc + c) + 2] << 2));
+    }
+    parents[L] = par;
+    octs[L] = octv;
+    if ((rc = up(ctx, &V.parent, par.data(), par.size()))) return rc;
+    if ((rc = up(ctx, &V.octant, octv.data(), octv.size()))) return rc;
+    const long long nil = fd->lev_nil[li];
+    std::vector<long long> optr_v(fd->lev_obs_ptr + optr, fd->lev_obs_ptr + optr + V.ncell + 1);
+    std::vector<int> src(nil), off(nil);
+    for (long long q = 0; q < nil; ++q) {
+      src[q] = (int)fd->lev_il_src[oil + q];
+      off[q] = (int)fd->lev_il_off[oil + q];
+    }
+    if ((rc = up(ctx, &V.obs_ptr, optr_v.data(), optr_v.size()))) return rc;
+    if ((rc = up(ctx, &V.il_src, src.data(), src.size()))) return rc;
+    if ((rc = up(ctx, &V.il_off, off.data(), off.size()))) return rc;
+    std::vector<unsigned> dark(V.noff, 0);
+    for (int o = 0; o < V.noff; ++o)
+      for (int l = 1; l <= F->mu + 1; ++l)
+        if (fd->lev_dark[(oo + o) * (F->mu + 1) + l - 1]) dark[o] |= 1u << (l - 1);
+    if ((rc = up(ctx, &V.dark, dark.data(), dark.size()))) return rc;
+    if ((rc = up(ctx, &V.K0, fd->lev_K0 + ok0, (size_t)V.noff * FKR * F->ntau0))) return rc;
+    if ((rc = up(ctx, &V.Kp, fd->lev_Kp + okp, (size_t)d * V.noff * FKR * F->ntaup))) return rc;
+    oc += V.ncell;
+    oo += V.noff;
+    oil += nil;
+    optr += V.ncell + 1;
+    ok0 += (long long)V.noff * FKR * F->ntau0;
+    okp += (long long)d * V.noff * FKR * F->ntaup;
+    const size_t cs = (size_t)V.ncell * FND;
+    const int naux = d * (d - 1) / 2;
+    TDW_CUDA(ctx, cudaMalloc(&V.own, sizeof(double) * (F->mu + 3) * cs));
+    TDW_CUDA(ctx, cudaMalloc(&V.inherit, sizeof(double) * 4 * cs));
+    TDW_CUDA(ctx, cudaMalloc(&V.deriv, sizeof(double) * d * cs));
+    TDW_CUDA(ctx, cudaMalloc(&V.aux, sizeof(double) * std::max(1, naux) * cs));
+    TDW_CUDA(ctx, cudaMalloc(&V.acc, sizeof(double) * cs));
+    TDW_CUDA(ctx, cudaMalloc(&V.mom, sizeof(double) * cs));
+  }
+  // children lists (level L cells of each level L-1 parent, ascending)
+  for (int L = 3; L <= F->leaf; ++L) {
+    FmmLevel& P = F->lev[L - 1];
+    std::vector<int> cptr(P.ncell + 1, 0), cidx;
+    std::vector<std::vector<int>> ch(P.ncell);
+    for (int c = 0; c < F->lev[L].ncell; ++c) ch[parents[L][c]].push_back(c);
+    for (int p = 0; p < P.ncell; ++p) {
+      cptr[p + 1] = cptr[p] + (int)ch[p].size();
+      for (int c : ch[p]) cidx.push_back(c);
+    }
+    if ((rc = up(ctx, &P.child_ptr, cptr.data(), cptr.size()))) return rc;
+    if ((rc = up(ctx, &P.child_idx, cidx.data(), cidx.size()))) return rc;
+  }
+  // extra lists: rows/cols in internal order, coefficient tables on the device
+  long long oe = 0;
+  for (int x = 0; x < fd->n_extra; ++x) {
+    FmmExtra E;
+    E.lags = fd->extra_lags[x];
+    E.npair = fd->extra_npair[x];
+    std::vector<std::pair<int, int>> pr(E.npair);
+    for (long long p = 0; p < E.npair; ++p)
+      pr[p] = {inv[fd->extra_i[oe + p]], inv[fd->extra_j[oe + p]]};
+    std::stable_sort(pr.begin(), pr.end(), [](auto& u, auto& v) { return u.first < v.first; });
+    std::vector<int> rp(ns + 1, 0), col(E.npair), rof(E.npair);
+    for (long long p = 0; p < E.npair; ++p) {
+      rp[pr[p].first + 1]++;
+      col[p] = pr[p].second;
+      rof[p] = pr[p].first;
+    }
+    for (int i = 0; i < ns; ++i) rp[i + 1] += rp[i];
+    if ((rc = up(ctx, &E.row_ptr, rp.data(), rp.size()))) return rc;
+    if ((rc = up(ctx, &E.col, col.data(), col.size()))) return rc;
+    if ((rc = up(ctx, &E.row_of, rof.data(), rof.size()))) return rc;
+    TDW_CUDA(ctx, cudaMalloc(&E.U, sizeof(double) * std::max<long long>(1, E.npair * E.lags)));
+    TDW_CUDA(ctx, cudaMalloc(&E.W, sizeof(double) * std::max<long long>(1, E.npair * E.lags)));
+    if (E.npair) {
+      const bool bm = pb->bie == TDW_BIE_BMBIE;
+      const int blocks = (int)std::min<long long>((E.npair + 127) / 128, 4096);
+#define TDW_X(DD, BB)                                                                            \
+  extra_coeff_kernel<DD, BB><<<blocks, 128, 0, ctx->stream>>>(pb->d_elem, E.row_of, E.col, E.npair, \
+                                                               E.lags, pb->c, pb->dt, pb->K, E.U, E.W)
+      if (d == 1) { if (bm) TDW_X(1, true); else TDW_X(1, false); }
+      if (d == 2) { if (bm) TDW_X(2, true); else TDW_X(2, false); }
+      if (d == 3) { if (bm) TDW_X(3, true); else TDW_X(3, false); }
+#undef TDW_X
+      TDW_CUDA(ctx, cudaGetLastError());
+    }
+    E.gmax.assign(fd->extra_gmax + (size_t)x * nt, fd->extra_gmax + (size_t)(x + 1) * nt);
+    oe += E.npair;
+    F->extra.push_back(std::move(E));
+  }
+  F->ticks_before.assign(fd->ticks_before, fd->ticks_before + nt);
+  F->k_obs.assign(fd->k_obs, fd->k_obs + nt);
+  F->wt.assign(fd->wt, fd->wt + (size_t)nt * FPT);
+  F->dwt.assign(fd->dwt, fd->dwt + (size_t)nt * FPT);
+  F->wts.assign(fd->wts, fd->wts + (size_t)nt * FPT);
+  TDW_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  return TDW_OK;
+}
+
+// ------------------------------------------------------------------ loop
+namespace {
+
+Tr make_tr(const FmmState* F) {
+  Tr t;
+  for (int h = 0; h < 2; ++h)
+    for (int i = 0; i < FPS; ++i)
+      for (int j = 0; j < FPS; ++j) {
+        t.s[h][i][j] = F->t_space[h][i][j];
+        t.t[h][i][j] = F->t_time[h][i][j];
+      }
+  return t;
+}
+
+int snapshot(tdw_ctx* ctx, FmmLevel& V, cudaStream_t st) {
+  const size_t cs = (size_t)V.ncell * FND * sizeof(double);
+  TDW_CUDA(ctx, cudaMemcpyAsync(V.mom, V.acc, cs, cudaMemcpyDeviceToDevice, st));
+  TDW_CUDA(ctx, cudaMemsetAsync(V.acc, 0, cs, st));
+  return TDW_OK;
+}
+
+int launch_m2l(tdw_problem* pb, FmmLevel& V, int k, cudaStream_t st) {
+  FmmState* F = pb->fmm;
+  M2LArgs a;
+  a.obs_ptr = V.obs_ptr;
+  a.il_src = V.il_src;
+  a.il_off = V.il_off;
+  a.dark = V.dark;
+  a.K0 = V.K0;
+  a.Kp = V.Kp;
+  a.mom = V.mom;
+  a.own = V.own;
+  a.deriv = V.deriv;
+  a.aux = V.aux;
+  a.ncell = V.ncell;
+  a.noff = V.noff;
+  a.ntau0 = F->ntau0;
+  a.ntaup = F->ntaup;
+  a.mu = F->mu;
+  a.d = pb->d;
+  a.k = k;
+  a.T = pb->c * V.interval;
+  if (pb->d == 1) m2l_kernel<1><<<V.ncell, FN3, 0, st>>>(a);
+  if (pb->d == 2) m2l_kernel<2><<<V.ncell, FN3, 0, st>>>(a);
+  if (pb->d == 3) m2l_kernel<3><<<V.ncell, FN3, 0, st>>>(a);
+  TDW_CUDA(pb->ctx, cudaGetLastError());
+  return TDW_OK;
+}
+
+// fmm.py:371-419
+int tick(tdw_problem* pb, int k_leaf, cudaStream_t st) {
+  FmmState* F = pb->fmm;
+  tdw_ctx* ctx = pb->ctx;
+  const int leaf = F->leaf;
+  if (leaf < 2) return TDW_OK;
+  const Tr tr = make_tr(F);
+  std::vector<int> completed{leaf};
+  int rc = snapshot(ctx, F->lev[leaf], st);
+  if (!rc) rc = launch_m2l(pb, F->lev[leaf], k_leaf, st);
+  if (rc) return rc;
+  int cur_k = k_leaf, L = leaf;
+  while (L - 1 >= 2) {
+    const int half = cur_k & 1;
+    FmmLevel& P = F->lev[L - 1];
+    m2m_kernel<<<P.ncell, FND, 0, st>>>(P.child_ptr, P.child_idx, F->lev[L].octant, F->lev[L].mom,
+                                         half, tr, P.acc);
+    TDW_CUDA(ctx, cudaGetLastError());
+    if (half == 0) break;
+    cur_k >>= 1;
+    L -= 1;
+    completed.push_back(L);
+    if ((rc = snapshot(ctx, F->lev[L], st))) return rc;
+    if ((rc = launch_m2l(pb, F->lev[L], cur_k, st))) return rc;
+  }
+  std::sort(completed.begin(), completed.end());
+  const int ring = F->mu + 3;
+  for (int Lc : completed) {
+    if (Lc + 1 > leaf) continue;
+    const int kl = k_leaf >> (leaf - Lc);
+    FmmLevel& P = F->lev[Lc];
+    FmmLevel& C = F->lev[Lc + 1];
+    const size_t csp = (size_t)P.ncell * FND, csc = (size_t)C.ncell * FND;
+    const int k0 = 2 * (kl + 1), k1 = 2 * (kl + 1) + 1;
+    l2l_kernel<<<C.ncell, FND, 0, st>>>(C.parent, C.octant, P.own + ((kl + 1) % ring) * csp,
+                                         P.inherit + ((kl + 1) % 4) * csp, tr,
+                                         C.inherit + (k0 % 4) * csc, C.inherit + (k1 % 4) * csc);
+    TDW_CUDA(ctx, cudaGetLastError());
+  }
+  return TDW_OK;
+}
+
+}  // namespace
+
+// launched from march.cu's helpers
+int launch_conv_fmm(tdw_problem* pb, void* plan, int alpha, cudaStream_t s);
+int launch_solve_fmm(tdw_problem* pb, void* plan, int alpha, cudaStream_t s);
+int make_plan_fmm(tdw_problem* pb, void** plan, double threshold, bool want_rhs);
+void free_plan_fmm(void* plan);
+int begin_loop_fmm(tdw_problem* pb, cudaStream_t st);
+
+int tdw_fmm_loop(tdw_problem* pb, double threshold, bool want_rhs, tdw_timing* timing) {
+  tdw_ctx* ctx = pb->ctx;
+  FmmState* F = pb->fmm;
+  cudaStream_t st = ctx->stream;
+  if (want_rhs) {
+    if (!pb->d_rhs)
+      TDW_CUDA(ctx, cudaMalloc(&pb->d_rhs, sizeof(double) * (size_t)(pb->nt - 1) * pb->ns));
+    TDW_CUDA(ctx, cudaMemsetAsync(pb->d_rhs, 0, sizeof(double) * (size_t)(pb->nt - 1) * pb->ns, st));
+  }
+  void* plan = nullptr;
+  int rc = make_plan_fmm(pb, &plan, threshold, want_rhs);
+  if (rc) return rc;
+  cudaEvent_t e0, e1;
+  TDW_CUDA(ctx, cudaEventCreate(&e0));
+  TDW_CUDA(ctx, cudaEventCreate(&e1));
+  TDW_CUDA(ctx, cudaEventRecord(e0, st));
+  if ((rc = begin_loop_fmm(pb, st))) return rc;
+  for (int L = 2; L <= F->leaf; ++L) {
+    FmmLevel& V = F->lev[L];
+    const size_t cs = (size_t)V.ncell * FND * sizeof(double);
+    TDW_CUDA(ctx, cudaMemsetAsync(V.own, 0, cs * (F->mu + 3), st));
+    TDW_CUDA(ctx, cudaMemsetAsync(V.inherit, 0, cs * 4, st));
+    TDW_CUDA(ctx, cudaMemsetAsync(V.deriv, 0, cs * pb->d, st));
+    TDW_CUDA(ctx, cudaMemsetAsync(V.aux, 0, cs * std::max(1, pb->d * (pb->d - 1) / 2), st));
+    TDW_CUDA(ctx, cudaMemsetAsync(V.acc, 0, cs, st));
+  }
+  const int ring = F->mu + 3;
+  long long last_tick = -1;
+  FmmLevel* LV = F->leaf >= 2 ? &F->lev[F->leaf] : nullptr;
+  for (int alpha = 1; alpha < pb->nt; ++alpha) {
+    while (last_tick < F->ticks_before[alpha]) {
+      if ((rc = tick(pb, (int)(last_tick + 1), st))) return rc;
+      ++last_tick;
+    }
+    double* b = pb->d_b + (alpha & 1) * pb->bstride;
+    if ((rc = launch_conv_fmm(pb, plan, alpha, st))) return rc;  // near field -> b
+    for (auto& E : F->extra) {
+      const int g = (int)E.gmax[alpha];
+      if (g <= 0 || E.npair == 0) continue;
+      extra_apply_kernel<<<(pb->ns + 127) / 128, 128, 0, st>>>(E.row_ptr, E.col, E.U, E.W, E.lags, g,
+                                                              pb->d_hist, pb->hstride, pb->pad,
+                                                              alpha, pb->d, pb->ns, b, pb->d_flags);
+    }
+    StepW sw;
+    for (int m = 0; m < FPT; ++m) {
+      sw.wt[m] = F->wt[(size_t)alpha * FPT + m];
+      sw.dwt[m] = F->dwt[(size_t)alpha * FPT + m];
+      sw.wts[m] = F->wts[(size_t)alpha * FPT + m];
+    }
+    if (LV) {
+      const long long ko = F->k_obs[alpha];
+      l2p_kernel<<<(pb->ns + 127) / 128, 128, 0, st>>>(
+          F->elem_cell, LV->own, LV->inherit, (int)(ko % ring), (int)(ko % 4), LV->ncell,
+          F->l2p_val, pb->bie == TDW_BIE_BMBIE ? F->l2p_bm : nullptr, sw, pb->ns, b, pb->d_flags);
+    }
+    if ((rc = launch_solve_fmm(pb, plan, alpha, st))) return rc;
+    if (LV)
+      p2m_kernel<<<LV->ncell, FN3, 0, st>>>(F->cell_ptr, F->cell_elems, F->p2m_tau, F->p2m_sig,
+                                             pb->d_hist, pb->hstride, pb->pad, alpha - 1, pb->d, sw,
+                                             LV->acc, pb->d_flags);
+    TDW_CUDA(ctx, cudaGetLastError());
+  }
+  TDW_CUDA(ctx, cudaEventRecord(e1, st));
+  TDW_CUDA(ctx, cudaEventSynchronize(e1));
+  if (timing) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    timing->total_ms += ms;
+    timing->steps += pb->nt - 1;
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  free_plan_fmm(plan);
+  int hflags[4];
+  TDW_CUDA(ctx, cudaMemcpy(hflags, pb->d_flags, sizeof(hflags), cudaMemcpyDeviceToHost));
+  if (hflags[0] == 2) return tdw_fail(ctx, TDW_ERR_RESIDUAL, "FMM step: solve residual too large");
+  return TDW_OK;
+}
+
+void tdw_fmm_free(FmmState* F) {
+  if (!F) return;
+  for (auto& V : F->lev) {
+    void* p[] = {V.parent, V.octant, V.child_ptr, V.child_idx, V.obs_ptr, V.il_src, V.il_off, V.dark,
+                 V.K0, V.Kp, V.own, V.inherit, V.deriv, V.aux, V.acc, V.mom};
+    for (void* q : p)
+      if (q) cudaFree(q);
+  }
+  for (auto& E : F->extra) {
+    void* p[] = {E.row_ptr, E.col, E.row_of, E.U, E.W};
+    for (void* q : p)
+      if (q) cudaFree(q);
+  }
+  void* p[] = {F->elem_cell, F->cell_ptr, F->cell_elems, F->p2m_tau, F->p2m_sig, F->l2p_val, F->l2p_bm};
+  for (void* q : p)
+    if (q) cudaFree(q);
+  delete F;
+}

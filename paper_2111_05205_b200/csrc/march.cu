@@ -76,6 +76,7 @@ struct ConvArgs {
   const unsigned long long* __restrict__ unit_off;
   const int2* __restrict__ unit;
   const unsigned* __restrict__ sched;
+  const unsigned* __restrict__ sched_item;
   const unsigned* __restrict__ sched_off;
   const double2* __restrict__ hist;
   double* __restrict__ bpart;
@@ -112,7 +113,7 @@ __global__ void __launch_bounds__(TDW_CONV_THREADS, 1)
   }
   __syncthreads();
   const unsigned u0 = a.sched_off[blockIdx.x], u1 = a.sched_off[blockIdx.x + 1];
-  const int nunits = (int)(u1 - u0);
+  const int nent = (int)(u1 - u0);  // schedule entries: a unit id, or TDW_EMPTY_UNIT (item flush only)
 
   if (warp == TDW_CONV_WARPS) {
     // ---------------- producer ----------------
@@ -125,24 +126,27 @@ __global__ void __launch_bounds__(TDW_CONV_THREADS, 1)
     unsigned rs1 = 0, re1 = 0, rs2 = 0, re2 = 0, rs3 = 0, re3 = 0;
     unsigned h = 0;
     const unsigned cap = a.stage_bytes;
-    for (int base = 0; base < nunits; base += 32) {
-      unsigned uid = 0;
+    int n = 0;  // real units issued
+    for (int base = 0; base < nent; base += 32) {
+      unsigned uid = TDW_EMPTY_UNIT;
       unsigned long long off = 0, nbytes = 0;
       int2 g = make_int2(0, -1);
-      if (base + lane < nunits) {
+      if (base + lane < nent) {
         uid = a.sched[u0 + base + lane];
-        off = a.unit_off[uid];
-        nbytes = a.unit_off[uid + 1] - off;
-        g = a.unit[uid];
+        if (uid != TDW_EMPTY_UNIT) {
+          off = a.unit_off[uid];
+          nbytes = a.unit_off[uid + 1] - off;
+          g = a.unit[uid];
+        }
       }
-      const int nb = min(32, nunits - base);
+      const int nb = min(32, nent - base);
       for (int q = 0; q < nb; ++q) {
-        const int n = base + q;
-        const int slot = n & 3;
         const unsigned quid = __shfl_sync(FULLMASK, uid, q);
         const unsigned long long qoff = __shfl_sync(FULLMASK, off, q);
         const unsigned qbytes = (unsigned)__shfl_sync(FULLMASK, nbytes, q);
         const int gmin = __shfl_sync(FULLMASK, g.x, q), gmax = __shfl_sync(FULLMASK, g.y, q);
+        if (quid == TDW_EMPTY_UNIT) continue;
+        const int slot = n & 3;
         const int W = gmax >= gmin ? gmax - gmin + 1 : 0;
         const int t = (int)(quid % (unsigned)a.ntiles);
         const unsigned hbytes = W > 0 ? (unsigned)(TDW_TJ * a.wbox * 16) : 0u;
@@ -173,6 +177,7 @@ __global__ void __launch_bounds__(TDW_CONV_THREADS, 1)
         if (W > 0 && lane == 0)  // hist[t*32 .. +32][pad+alpha-gmax .. +wbox) as one 2-D box
           tensor2d_g2s(sbase + ubytes, &hmap, 2 * (a.pad + a.alpha - gmax), t * TDW_TJ, &full[slot]);
         h += need;
+        ++n;
       }
     }
     return;
@@ -183,10 +188,17 @@ __global__ void __launch_bounds__(TDW_CONV_THREADS, 1)
   for (int r = 0; r < TDW_ROWS_PER_WARP; ++r) acc[r] = 0.0;
   const int S = a.S;
   int n = 0;
-  for (long long item = blockIdx.x; n < nunits; item += gridDim.x) {
-    const int iblk = (int)(item / S), sp = (int)(item % S);
-    const int tb = (int)((long long)sp * a.ntiles / S), te = (int)((long long)(sp + 1) * a.ntiles / S);
-    for (int t = tb; t < te; ++t, ++n) {
+  for (int base = 0; base < nent; base += 32) {
+    const unsigned my_uid = base + lane < nent ? a.sched[u0 + base + lane] : TDW_EMPTY_UNIT;
+    const unsigned my_item = base + lane < nent ? a.sched_item[u0 + base + lane] : 0xffffffffu;
+    const unsigned after = base + 32 < nent ? a.sched_item[u0 + base + 32] : 0xffffffffu;
+    const int nb = min(32, nent - base);
+    for (int q = 0; q < nb; ++q) {
+    const unsigned uid = __shfl_sync(FULLMASK, my_uid, q);
+    const unsigned item = __shfl_sync(FULLMASK, my_item, q);
+    const unsigned nxt = __shfl_sync(FULLMASK, my_item, (q + 1) & 31);
+    const unsigned next_item = q + 1 < nb ? nxt : after;
+    if (uid != TDW_EMPTY_UNIT) {
       const int stage = n % NS;
       mbar_wait(&full[stage], (unsigned)(n / NS) & 1u);
       const unsigned char* ub = sm + *(volatile unsigned*)&region[stage];
@@ -239,15 +251,20 @@ __global__ void __launch_bounds__(TDW_CONV_THREADS, 1)
       for (int r = 0; r < TDW_ROWS_PER_WARP; ++r) acc[r] += s0[r] - s1[r];
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[stage]);
+      ++n;
     }
+    if (next_item != item) {  // end of a work item (I-block, split): flush the row partials
+      const int iblk = (int)(item / (unsigned)S), sp = (int)(item % (unsigned)S);
 #pragma unroll
-    for (int r = 0; r < TDW_ROWS_PER_WARP; ++r) {
-      double v = acc[r];
+      for (int r = 0; r < TDW_ROWS_PER_WARP; ++r) {
+        double v = acc[r];
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULLMASK, v, o);
-      if (lane == 0)  // row-major partials: a row's S partials are contiguous
-        a.bpart[(size_t)(iblk * TDW_TI + warp * TDW_ROWS_PER_WARP + r) * S + sp] = v;
-      acc[r] = 0.0;
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULLMASK, v, o);
+        if (lane == 0)  // row-major partials: a row's S partials are contiguous
+          a.bpart[(size_t)(iblk * TDW_TI + warp * TDW_ROWS_PER_WARP + r) * S + sp] = v;
+        acc[r] = 0.0;
+      }
+    }
     }
   }
 }
@@ -863,6 +880,7 @@ static void fill_conv_args(tdw_problem* pb, ConvArgs& c) {
   c.unit_off = pb->d_unit_off;
   c.unit = pb->d_unit;
   c.sched = pb->d_sched;
+  c.sched_item = pb->d_sched_item;
   c.sched_off = pb->d_sched_off;
   c.hist = pb->d_hist;
   c.bpart = pb->d_bpart;
@@ -1036,6 +1054,7 @@ int tdw_march_loop(tdw_problem* pb, double threshold, bool want_rhs, bool time_k
   cudaStream_t st = ctx->stream;
   if (!pb->assembled) return tdw_fail(ctx, TDW_ERR_STATE, "tdw_march before tdw_assemble");
   if (!pb->known_loaded) return tdw_fail(ctx, TDW_ERR_STATE, "known boundary data not uploaded");
+  if (pb->fmm) return tdw_fmm_loop(pb, threshold, want_rhs, timing);
   if (want_rhs) {
     if (!pb->d_rhs)
       TDW_CUDA(ctx, cudaMalloc(&pb->d_rhs, sizeof(double) * (size_t)(pb->nt - 1) * pb->ns));
@@ -1346,4 +1365,21 @@ int tdw_setup_cluster_solver(tdw_problem* pb) {
     TDW_CUDA(ctx, cudaFuncSetAttribute(solve_reg_kernel<24>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   }
   return TDW_OK;
+}
+
+// ---- entry points for the FMM loop (csrc/fmm.cu): plan + per-step near field / solve
+int make_plan_fmm(tdw_problem* pb, void** out, double threshold, bool want_rhs) {
+  LoopPlan* L = new LoopPlan();
+  int rc = make_plan(pb, *L, threshold, want_rhs);
+  if (rc) { delete L; return rc; }
+  *out = L;
+  return TDW_OK;
+}
+void free_plan_fmm(void* plan) { delete (LoopPlan*)plan; }
+int begin_loop_fmm(tdw_problem* pb, cudaStream_t st) { return begin_loop(pb, st); }
+int launch_conv_fmm(tdw_problem* pb, void* plan, int alpha, cudaStream_t s) {
+  return launch_conv(pb, *(LoopPlan*)plan, alpha, s);
+}
+int launch_solve_fmm(tdw_problem* pb, void* plan, int alpha, cudaStream_t s) {
+  return launch_solve(pb, *(LoopPlan*)plan, alpha, s);
 }

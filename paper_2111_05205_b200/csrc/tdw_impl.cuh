@@ -26,6 +26,7 @@
 #define TDW_UNIT_LAG_OFF 128
 #define TDW_UNIT_HDR_OFF 256
 #define TDW_UNIT_COEF_OFF 4352
+#define TDW_EMPTY_UNIT 0xffffffffu
 
 struct tdw_ctx {
   int device = 0;
@@ -60,6 +61,11 @@ struct tdw_problem {
   int* d_perm = nullptr;
   double* d_elem = nullptr;  // ns * TDW_ELEM_STRIDE
   double* d_phi = nullptr;   // internal order
+  // FMM near-field mode: pair filter (adjacent leaf cells), no lag-2 split
+  int* d_leafc = nullptr;    // packed leaf-cell coords per element (internal order) or null
+  int split_lag2 = 1;
+  bool skip_empty_units = false;
+  struct FmmState* fmm = nullptr;
   // banded store
   bool assembled = false;
   unsigned char* d_units = nullptr;        // unit-major store (see unit layout above)
@@ -71,7 +77,8 @@ struct tdw_problem {
   // conv schedule: persistent CTAs over items (I-block, tile split)
   int conv_grid = 0, conv_S = 1, conv_nstages = 2;
   size_t conv_stage_bytes = 0;
-  unsigned* d_sched = nullptr;     // unit ids in CTA processing order
+  unsigned* d_sched = nullptr;     // unit ids in CTA processing order (or TDW_EMPTY_UNIT)
+  unsigned* d_sched_item = nullptr; // work item (I-block * S + split) of each entry
   unsigned* d_sched_off = nullptr; // [conv_grid + 1]
   int64_t n_band = 0, n_pairs = 0, n_evals = 0, store_bytes = 0;
   // lag-1 step matrix, all rows, ELL
@@ -142,5 +149,7 @@ int tdw_march_loop(tdw_problem* pb, double threshold, bool want_rhs, bool time_k
 int tdw_outputs(tdw_problem* pb, double* u, double* q, double* tau, double* sigma);
 int tdw_time_conv_impl(tdw_problem* pb, int n, float* ms_out);
 int tdw_setup_cluster_solver(tdw_problem* pb);
+int tdw_fmm_loop(tdw_problem* pb, double threshold, bool want_rhs, tdw_timing* timing);
+void tdw_fmm_free(struct FmmState* F);
 int tdw_march_emulated_impl(tdw_problem** pbs, int n, double threshold);
 int tdw_problem_create_impl(tdw_ctx* ctx, const tdw_problem_desc* dsc, tdw_problem** out, bool shard_only);
