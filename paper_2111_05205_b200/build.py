@@ -44,7 +44,7 @@ def build(verbose: bool = False, extra=()) -> Path:
         cmd = common + (["-Xptxas", "-v"] if verbose else []) + ["-c", str(CSRC / src), "-o", str(obj)]
         subprocess.run(cmd, check=True)
     cmd = [nvcc(), "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", str(OUT),
-           *map(str, objs), f"-L{lib}", "-l:libnccl.so.2", f"-Xlinker=-rpath={lib}"]
+           *map(str, objs), f"-L{lib}", "-l:libnccl.so.2", f"-Xlinker=-rpath={lib}", "-lcublas"]
     subprocess.run(cmd, check=True)
     return OUT
 

@@ -16,6 +16,7 @@
 // built on the host (paper_2111_05205_b200/fmm_plan.py) and handed over by
 // tdw_fmm_setup; the per-step control flow (which ticks run before which step)
 // is a fixed schedule, so the loop is a plain sequence of launches.
+#include <cublas_v2.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -48,6 +49,14 @@ struct FmmLevel {
   double* Kp = nullptr;        // [d][noff][343][ntaup]
   double *own = nullptr, *inherit = nullptr, *deriv = nullptr, *aux = nullptr, *acc = nullptr,
          *mom = nullptr;
+  // GEMM form of M2L: pairs grouped by offset, stacked dense operators per offset
+  std::vector<long long> grp;  // [noff+1] pair range of each offset group
+  int* g_obs = nullptr;        // [nil] observer of each grouped pair
+  int* g_src = nullptr;        // [nil] source
+  double* Kop = nullptr;       // [noff][K = 256][M = nops*256] column-major operator stacks
+  double* X = nullptr;         // [nil][256] gathered source moments
+  double* tmp = nullptr;       // [d][ncell][256]
+  long long nil = 0, max_grp = 0;
 };
 
 struct FmmExtra {
@@ -61,7 +70,9 @@ struct FmmExtra {
 };
 
 struct FmmState {
-  int mu = 8, leaf = 0, ntau0 = 0, ntaup = 0, n_leaf_cells = 0;
+  int mu = 8, leaf = 0, ntau0 = 0, ntaup = 0, n_leaf_cells = 0, nops = 0;
+  cublasHandle_t blas = nullptr;
+  double* Y = nullptr;         // [max group][nops*256] GEMM output
   std::vector<FmmLevel> lev;   // index = level (entries < 2 unused)
   int* elem_cell = nullptr;    // [ns] internal order
   int* cell_ptr = nullptr;     // [ncell+1] leaf cell -> internal elements
@@ -195,20 +206,7 @@ __global__ void p2m_kernel(const int* __restrict__ cell_ptr, const int* __restri
   for (int t = 0; t < FPT; ++t) A[t] += spat * sw.wts[t];
 }
 
-// ---------------------------------------------------------------- M2L + recurrence
-struct M2LArgs {
-  const long long* obs_ptr;
-  const int* il_src;
-  const int* il_off;
-  const unsigned* dark;
-  const double* K0;
-  const double* Kp;
-  const double* mom;
-  double *own, *deriv, *aux;
-  int ncell, noff, ntau0, ntaup, mu, d, k;
-  double T;  // c * interval
-};
-
+// ---------------------------------------------------------------- recurrence coefficients
 __device__ __forceinline__ double cmp_coeff_dev(int p, int m, int k) {
   // comb(p, m) ((k-1)^(p-m) - 2 k^(p-m) + (k+1)^(p-m)) (-1)^m   (fmm.py:44-49)
   double binom = 1.0;
@@ -219,121 +217,96 @@ __device__ __forceinline__ double cmp_coeff_dev(int p, int m, int k) {
   return binom * (km - 2.0 * k0 + kp) * ((m & 1) ? -1.0 : 1.0);
 }
 
-// One CTA per observation cell, thread a = spatial node (a1, a2, a3); every
-// thread owns the 4 time nodes of its node for the mu+1 near-future lags and
-// the d derivative operators.  L[a,m] += sum_{b,n} K[a-b+P, m-n+toff] M[b,n]
-// (fmm.py:52-69); the Toeplitz rows are read through L1 (85 KB per offset).
+// ---------------------------------------------------------------- M2L as GEMM
+// Stacked dense operators of one offset: rows op*256 + ((a1*4+a2)*4+a3)*4+m,
+// columns ((b1*4+b2)*4+b3)*4+n (the reference's dense_m2l_matrix layout,
+// fmm.py:134-162); ops 0..mu = lags 1..mu+1 (toff = l (pt-1)), mu+1.. = p = 1..d.
+__global__ void build_kop_kernel(const double* __restrict__ K0, const double* __restrict__ Kp,
+                                 int noff, int ntau0, int ntaup, int mu, int d, double* Kop) {
+  const int nops = mu + 1 + d, M = nops * FND;
+  const long long total = (long long)noff * FND * M;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int off = (int)(e / ((long long)FND * M));
+    const long long rem = e % ((long long)FND * M);
+    const int col = (int)(rem / M), rowf = (int)(rem % M);
+    const int op = rowf / FND, row = rowf % FND;
+    const int a1 = row >> 6, a2 = (row >> 4) & 3, a3 = (row >> 2) & 3, m = row & 3;
+    const int b1 = col >> 6, b2 = (col >> 4) & 3, b3 = (col >> 2) & 3, n = col & 3;
+    const int kr = ((a1 - b1 + FPS - 1) * (2 * FPS - 1) + (a2 - b2 + FPS - 1)) * (2 * FPS - 1) +
+                   (a3 - b3 + FPS - 1);
+    double v;
+    if (op <= mu) {
+      const int l = op + 1;
+      v = K0[((size_t)off * FKR + kr) * ntau0 + (m - n + l * (FPT - 1))];
+    } else {
+      const int p = op - mu - 1;
+      v = Kp[(((size_t)p * noff + off) * FKR + kr) * ntaup + (m - n + FPT - 1)];
+    }
+    Kop[e] = v;
+  }
+}
+
+__global__ void gather_kernel(const int* __restrict__ g_src, long long nil,
+                              const double* __restrict__ mom, double* X) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < nil * FND;
+       e += (long long)gridDim.x * blockDim.x)
+    X[e] = mom[(size_t)g_src[e / FND] * FND + (e % FND)];
+}
+
+// one offset group: targets are distinct cells, so plain adds are race free;
+// groups run one after another on the stream (deterministic order)
+__global__ void scatter_kernel(const int* __restrict__ g_obs, long long p0, long long np,
+                               const double* __restrict__ Y, int nops, int mu, int d, int k,
+                               int ncell, double* own, double* tmp) {
+  const int ring = mu + 3;
+  const long long M = (long long)nops * FND;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < np * M;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long p = e / M;
+    const int r = (int)(e % M);
+    const int op = r / FND, idx = r % FND;
+    const int cell = g_obs[p0 + p];
+    const double v = Y[e];
+    if (op <= mu)
+      own[((size_t)((k + op + 1) % ring) * ncell + cell) * FND + idx] += v;
+    else
+      tmp[((size_t)(op - mu - 1) * ncell + cell) * FND + idx] += v;
+  }
+}
+
+// distant-future recurrence, elementwise (fmm.py:355-367)
 template <int D>
-__global__ void __launch_bounds__(FN3) m2l_kernel(M2LArgs A) {
-  const int cell = blockIdx.x, a = threadIdx.x;
-  const int a1 = a >> 4, a2 = (a >> 2) & 3, a3 = a & 3;
-  __shared__ double Ms[FND];
-  double acc[FMU_MAX + 1][FPT];
-  double tp[3][FPT];
+__global__ void recurrence_kernel(double* own, double* deriv, double* aux, const double* tmp,
+                                  int ncell, int mu, int k, double T) {
+  const int ring = mu + 3;
+  const size_t cs = (size_t)ncell * FND;
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < cs; e += (size_t)gridDim.x * blockDim.x) {
 #pragma unroll
-  for (int l = 0; l <= FMU_MAX; ++l)
+    for (int p = 1; p <= D; ++p) {
+      double upd = tmp[(size_t)(p - 1) * cs + e];
 #pragma unroll
-    for (int m = 0; m < FPT; ++m) acc[l][m] = 0.0;
-#pragma unroll
-  for (int p = 0; p < 3; ++p)
-#pragma unroll
-    for (int m = 0; m < FPT; ++m) tp[p][m] = 0.0;
-  for (long long q = A.obs_ptr[cell]; q < A.obs_ptr[cell + 1]; ++q) {
-    const int src = A.il_src[q], off = A.il_off[q];
-    __syncthreads();
-    bool nz = false;
-#pragma unroll
-    for (int n = 0; n < FPT; ++n) {
-      const double v = A.mom[(size_t)src * FND + a * FPT + n];
-      Ms[a * FPT + n] = v;
-      nz |= v != 0.0;
+      for (int mm = 0; mm <= p - 2; ++mm)
+        upd = upd + cmp_coeff_dev(p, mm, k) * aux[(size_t)((p - 2) * (p - 1) / 2 + mm) * cs + e];
+      deriv[(size_t)(p - 1) * cs + e] += upd;
     }
-    if (!__syncthreads_or(nz)) continue;  // live sources only (fmm.py:337-338)
-    const unsigned dk = A.dark[off];
-    const double* K0o = A.K0 + (size_t)off * FKR * A.ntau0;
-    for (int b = 0; b < FN3; ++b) {
-      const int b1 = b >> 4, b2 = (b >> 2) & 3, b3 = b & 3;
-      const int row = ((a1 - b1 + FPS - 1) * (2 * FPS - 1) + (a2 - b2 + FPS - 1)) * (2 * FPS - 1) +
-                      (a3 - b3 + FPS - 1);
-      double Mb[FPT];
-#pragma unroll
-      for (int n = 0; n < FPT; ++n) Mb[n] = Ms[b * FPT + n];
-      const double* kr = K0o + (size_t)row * A.ntau0;
-#pragma unroll
-      for (int l = 1; l <= FMU_MAX + 1; ++l) {
-        if (l > A.mu + 1 || ((dk >> (l - 1)) & 1u)) continue;
-        const int toff = l * (FPT - 1);
-        double kw[2 * FPT - 1];
-#pragma unroll
-        for (int t = 0; t < 2 * FPT - 1; ++t) kw[t] = __ldg(kr + toff - (FPT - 1) + t);
-#pragma unroll
-        for (int m = 0; m < FPT; ++m)
-#pragma unroll
-          for (int n = 0; n < FPT; ++n) acc[l - 1][m] = fma(kw[m - n + FPT - 1], Mb[n], acc[l - 1][m]);
-      }
-#pragma unroll
-      for (int p = 0; p < D; ++p) {
-        const double* kp = A.Kp + (((size_t)p * A.noff + off) * FKR + row) * A.ntaup;
-        double kw[2 * FPT - 1];
-#pragma unroll
-        for (int t = 0; t < 2 * FPT - 1; ++t) kw[t] = __ldg(kp + t);
-#pragma unroll
-        for (int m = 0; m < FPT; ++m)
-#pragma unroll
-          for (int n = 0; n < FPT; ++n) tp[p][m] = fma(kw[m - n + FPT - 1], Mb[n], tp[p][m]);
-      }
-    }
-  }
-  const int ring = A.mu + 3;
-  const size_t cs = (size_t)A.ncell * FND, base = (size_t)cell * FND + a * FPT;
-#pragma unroll
-  for (int l = 1; l <= FMU_MAX + 1; ++l) {
-    if (l > A.mu + 1) continue;
-    double* o = A.own + (size_t)((A.k + l) % ring) * cs + base;
-#pragma unroll
-    for (int m = 0; m < FPT; ++m) o[m] += acc[l - 1][m];
-  }
-  // distant-future recurrence (fmm.py:355-367)
-#pragma unroll
-  for (int p = 1; p <= D; ++p) {
-    double* dv = A.deriv + (size_t)(p - 1) * cs + base;
-#pragma unroll
-    for (int m = 0; m < FPT; ++m) {
-      double upd = tp[p - 1][m];
-#pragma unroll
-      for (int mm = 0; mm <= p - 2; ++mm) {
-        const int ai = (p - 2) * (p - 1) / 2 + mm;
-        upd = upd + cmp_coeff_dev(p, mm, A.k) * A.aux[(size_t)ai * cs + base + m];
-      }
-      dv[m] += upd;
-    }
-  }
-  const double* prev = A.own + (size_t)((A.k + A.mu + 1) % ring) * cs + base;
-  double* nxt = A.own + (size_t)((A.k + A.mu + 2) % ring) * cs + base;
-  double pv[FPT];
-#pragma unroll
-  for (int m = 0; m < FPT; ++m) pv[m] = prev[m];
-  // own_slot(k+mu+2) = own_slot(k+mu+1) + sum_p deriv_p T^p, added in p order
-#pragma unroll
-  for (int m = 0; m < FPT; ++m) {
-    double v = pv[m];
+    double v = own[(size_t)((k + mu + 1) % ring) * cs + e];
     double Tq = 1.0;
 #pragma unroll
     for (int p = 1; p <= D; ++p) {
-      Tq *= A.T;
-      v += A.deriv[(size_t)(p - 1) * cs + base + m] * Tq;
+      Tq *= T;
+      v += deriv[(size_t)(p - 1) * cs + e] * Tq;
     }
-    nxt[m] = v;
+    own[(size_t)((k + mu + 2) % ring) * cs + e] = v;
+#pragma unroll
+    for (int p = 2; p <= D; ++p)
+#pragma unroll
+      for (int mm = 0; mm <= p - 2; ++mm) {
+        double km = 1.0;
+        for (int q = 0; q < mm; ++q) km *= (double)k;
+        aux[(size_t)((p - 2) * (p - 1) / 2 + mm) * cs + e] += tmp[(size_t)(p - 1) * cs + e] * km;
+      }
   }
-#pragma unroll
-  for (int p = 2; p <= D; ++p)
-#pragma unroll
-    for (int mm = 0; mm <= p - 2; ++mm) {
-      const int ai = (p - 2) * (p - 1) / 2 + mm;
-      double km = 1.0;
-      for (int q = 0; q < mm; ++q) km *= (double)A.k;
-      for (int m = 0; m < FPT; ++m) A.aux[(size_t)ai * cs + base + m] += tp[p - 1][m] * km;
-    }
 }
 
 // ---------------------------------------------------------------- M2M / L2L
@@ -528,6 +501,37 @@ extern "C" int tdw_fmm_setup(tdw_problem* pb, const tdw_fmm_desc* fd) {
     if ((rc = up(ctx, &V.dark, dark.data(), dark.size()))) return rc;
     if ((rc = up(ctx, &V.K0, fd->lev_K0 + ok0, (size_t)V.noff * FKR * F->ntau0))) return rc;
     if ((rc = up(ctx, &V.Kp, fd->lev_Kp + okp, (size_t)d * V.noff * FKR * F->ntaup))) return rc;
+    {
+      // interaction pairs grouped by offset (stable: by observer within a group)
+      std::vector<long long> grp(V.noff + 1, 0);
+      std::vector<int> gobs(nil), gsrc(nil);
+      std::vector<int> obs_of(nil);
+      for (int c = 0; c < V.ncell; ++c)
+        for (long long q = optr_v[c]; q < optr_v[c + 1]; ++q) obs_of[q] = c;
+      for (long long q = 0; q < nil; ++q) grp[off[q] + 1]++;
+      for (int o = 0; o < V.noff; ++o) grp[o + 1] += grp[o];
+      std::vector<long long> fillp(grp.begin(), grp.end() - 1);
+      for (long long q = 0; q < nil; ++q) {
+        const long long t = fillp[off[q]]++;
+        gobs[t] = obs_of[q];
+        gsrc[t] = src[q];
+      }
+      V.grp = grp;
+      V.nil = nil;
+      for (int o = 0; o < V.noff; ++o) V.max_grp = std::max(V.max_grp, grp[o + 1] - grp[o]);
+      if ((rc = up(ctx, &V.g_obs, gobs.data(), gobs.size()))) return rc;
+      if ((rc = up(ctx, &V.g_src, gsrc.data(), gsrc.size()))) return rc;
+      const int nops = F->mu + 1 + d;
+      F->nops = nops;
+      const size_t kop = (size_t)V.noff * FND * nops * FND;
+      TDW_CUDA(ctx, cudaMalloc(&V.Kop, sizeof(double) * std::max<size_t>(1, kop)));
+      if (V.noff)
+        build_kop_kernel<<<4096, 256, 0, ctx->stream>>>(V.K0, V.Kp, V.noff, F->ntau0, F->ntaup, F->mu,
+                                                         d, V.Kop);
+      TDW_CUDA(ctx, cudaGetLastError());
+      TDW_CUDA(ctx, cudaMalloc(&V.X, sizeof(double) * std::max<long long>(1, nil) * FND));
+      TDW_CUDA(ctx, cudaMalloc(&V.tmp, sizeof(double) * d * (size_t)V.ncell * FND));
+    }
     oc += V.ncell;
     oo += V.noff;
     oil += nil;
@@ -594,6 +598,14 @@ extern "C" int tdw_fmm_setup(tdw_problem* pb, const tdw_fmm_desc* fd) {
     oe += E.npair;
     F->extra.push_back(std::move(E));
   }
+  {
+    long long mg = 1;
+    for (int L = 2; L <= F->leaf; ++L) mg = std::max(mg, F->lev[L].max_grp);
+    TDW_CUDA(ctx, cudaMalloc(&F->Y, sizeof(double) * (size_t)mg * std::max(1, F->nops) * FND));
+    if (cublasCreate(&F->blas) != CUBLAS_STATUS_SUCCESS)
+      return tdw_fail(ctx, TDW_ERR_CUDA, "cublasCreate failed");
+    cublasSetMathMode(F->blas, CUBLAS_DEFAULT_MATH);
+  }
   F->ticks_before.assign(fd->ticks_before, fd->ticks_before + nt);
   F->k_obs.assign(fd->k_obs, fd->k_obs + nt);
   F->wt.assign(fd->wt, fd->wt + (size_t)nt * FPT);
@@ -626,29 +638,36 @@ int snapshot(tdw_ctx* ctx, FmmLevel& V, cudaStream_t st) {
 
 int launch_m2l(tdw_problem* pb, FmmLevel& V, int k, cudaStream_t st) {
   FmmState* F = pb->fmm;
-  M2LArgs a;
-  a.obs_ptr = V.obs_ptr;
-  a.il_src = V.il_src;
-  a.il_off = V.il_off;
-  a.dark = V.dark;
-  a.K0 = V.K0;
-  a.Kp = V.Kp;
-  a.mom = V.mom;
-  a.own = V.own;
-  a.deriv = V.deriv;
-  a.aux = V.aux;
-  a.ncell = V.ncell;
-  a.noff = V.noff;
-  a.ntau0 = F->ntau0;
-  a.ntaup = F->ntaup;
-  a.mu = F->mu;
-  a.d = pb->d;
-  a.k = k;
-  a.T = pb->c * V.interval;
-  if (pb->d == 1) m2l_kernel<1><<<V.ncell, FN3, 0, st>>>(a);
-  if (pb->d == 2) m2l_kernel<2><<<V.ncell, FN3, 0, st>>>(a);
-  if (pb->d == 3) m2l_kernel<3><<<V.ncell, FN3, 0, st>>>(a);
-  TDW_CUDA(pb->ctx, cudaGetLastError());
+  tdw_ctx* ctx = pb->ctx;
+  const int d = pb->d, nops = F->nops, M = nops * FND;
+  TDW_CUDA(ctx, cudaMemsetAsync(V.tmp, 0, sizeof(double) * d * (size_t)V.ncell * FND, st));
+  if (V.nil > 0) {
+    gather_kernel<<<(int)std::min<long long>(4096, (V.nil * FND + 255) / 256), 256, 0, st>>>(
+        V.g_src, V.nil, V.mom, V.X);
+    TDW_CUDA(ctx, cudaGetLastError());
+    if (cublasSetStream(F->blas, st) != CUBLAS_STATUS_SUCCESS)
+      return tdw_fail(ctx, TDW_ERR_CUDA, "cublasSetStream failed");
+    const double one = 1.0, zero = 0.0;
+    for (int o = 0; o < V.noff; ++o) {
+      const long long p0 = V.grp[o], np = V.grp[o + 1] - V.grp[o];
+      if (np == 0) continue;
+      // Y (M x np) = Kop_o (M x 256) * X (256 x np), column-major
+      cublasStatus_t bs = cublasDgemm(F->blas, CUBLAS_OP_N, CUBLAS_OP_N, M, (int)np, FND, &one,
+                                      V.Kop + (size_t)o * FND * M, M, V.X + (size_t)p0 * FND, FND,
+                                      &zero, F->Y, M);
+      if (bs != CUBLAS_STATUS_SUCCESS) return tdw_fail(ctx, TDW_ERR_CUDA, "cublasDgemm failed");
+      scatter_kernel<<<(int)std::min<long long>(2048, (np * M + 255) / 256), 256, 0, st>>>(
+          V.g_obs, p0, np, F->Y, nops, F->mu, d, k, V.ncell, V.own, V.tmp);
+    }
+    TDW_CUDA(ctx, cudaGetLastError());
+  }
+  const size_t cs = (size_t)V.ncell * FND;
+  const int blocks = (int)std::min<size_t>(4096, (cs + 255) / 256);
+  const double T = pb->c * V.interval;
+  if (d == 1) recurrence_kernel<1><<<blocks, 256, 0, st>>>(V.own, V.deriv, V.aux, V.tmp, V.ncell, F->mu, k, T);
+  if (d == 2) recurrence_kernel<2><<<blocks, 256, 0, st>>>(V.own, V.deriv, V.aux, V.tmp, V.ncell, F->mu, k, T);
+  if (d == 3) recurrence_kernel<3><<<blocks, 256, 0, st>>>(V.own, V.deriv, V.aux, V.tmp, V.ncell, F->mu, k, T);
+  TDW_CUDA(ctx, cudaGetLastError());
   return TDW_OK;
 }
 
@@ -786,7 +805,8 @@ void tdw_fmm_free(FmmState* F) {
   if (!F) return;
   for (auto& V : F->lev) {
     void* p[] = {V.parent, V.octant, V.child_ptr, V.child_idx, V.obs_ptr, V.il_src, V.il_off, V.dark,
-                 V.K0, V.Kp, V.own, V.inherit, V.deriv, V.aux, V.acc, V.mom};
+                 V.K0, V.Kp, V.own, V.inherit, V.deriv, V.aux, V.acc, V.mom, V.g_obs, V.g_src,
+                 V.Kop, V.X, V.tmp};
     for (void* q : p)
       if (q) cudaFree(q);
   }
@@ -795,7 +815,9 @@ void tdw_fmm_free(FmmState* F) {
     for (void* q : p)
       if (q) cudaFree(q);
   }
-  void* p[] = {F->elem_cell, F->cell_ptr, F->cell_elems, F->p2m_tau, F->p2m_sig, F->l2p_val, F->l2p_bm};
+  if (F->blas) cublasDestroy(F->blas);
+  void* p[] = {F->elem_cell, F->cell_ptr, F->cell_elems, F->p2m_tau, F->p2m_sig, F->l2p_val, F->l2p_bm,
+               F->Y};
   for (void* q : p)
     if (q) cudaFree(q);
   delete F;
