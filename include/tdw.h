@@ -81,6 +81,8 @@ typedef struct {
   int32_t conv_grid;         /* persistent CTAs of the convolution kernel        */
   int32_t conv_splits;       /* column-tile splits per row block                 */
   int32_t solve_cluster;     /* CTAs of the cluster solver (0 = grid fallback)   */
+  int64_t n_units;           /* (row block, column tile) units with band entries */
+  int64_t units_hdr32;       /* of those, units stored with 32-bit pair headers  */
 } tdw_info;
 
 typedef struct {

@@ -36,7 +36,8 @@ class Info(C.Structure):
                 ("jacobi_iters", C.c_int32), ("jacobi_bound", C.c_double),
                 ("t_assemble_ms", C.c_double), ("t_fill_ms", C.c_double),
                 ("max_unit_bytes", C.c_int64), ("max_lag_span", C.c_int32), ("conv_grid", C.c_int32),
-                ("conv_splits", C.c_int32), ("solve_cluster", C.c_int32)]
+                ("conv_splits", C.c_int32), ("solve_cluster", C.c_int32),
+                ("n_units", C.c_int64), ("units_hdr32", C.c_int64)]
 
     def asdict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

@@ -221,12 +221,15 @@ __global__ void __launch_bounds__(128) fill_kernel(AsmArgs a) {
   const int rloc = (int)(seg / a.ntiles), t = (int)(seg % a.ntiles);
   unsigned char* ub = a.units + a.unit_off[(size_t)(rloc / TDW_TI) * a.ntiles + t];
   const int r = rloc % TDW_TI;
-  const uint32_t h = ((const uint32_t*)(ub + TDW_UNIT_HDR_OFF))[r * TDW_TJ + lane];
-  const int len = hdr_len(h), glo = hdr_glo(h), jl = hdr_jl(h);
+  const unsigned coef_off = *(const uint32_t*)(ub + TDW_UNIT_LAG_OFF + 12);
+  const int gmax = ((const int2*)(ub + TDW_UNIT_LAG_OFF))->y;
+  int jl, len, rel;
+  unit_hdr(ub, coef_off, gmax, r * TDW_TJ + lane, jl, len, rel);
+  const int glo = gmax - rel;
   const int lmax = __shfl_sync(FULLMASK, len, 0);
   if (lmax == 0) return;
   const int i = a.row_lo + rloc, j = t * TDW_TJ + jl;
-  double2* coef = (double2*)(ub + TDW_UNIT_COEF_OFF);
+  double2* coef = (double2*)(ub + coef_off);
   const unsigned long long base = ((const uint32_t*)ub)[r];
   const double cdt = a.c * a.dt;
   double w[D + 2];
@@ -291,24 +294,39 @@ __global__ void __launch_bounds__(128) fill_kernel(AsmArgs a) {
   if (lane == 0) atomicAdd(a.n_evals, (unsigned long long)nev);
 }
 
-// bytes of every unit: header block + 16 B per band entry of its 32 segments
-__global__ void unit_size_kernel(const unsigned long long* segcount, int ntiles, long long nunit,
-                                 unsigned long long* unit_bytes) {
+// bytes of every unit: header block + 16 B per band entry of its 32 segments;
+// the header width (16 or 32 bit) follows from the unit's longest band and lag span
+__global__ void unit_size_kernel(const unsigned long long* segcount, const uint32_t* hdr_tmp,
+                                 const int2* unit, int ntiles, long long nunit, int force32,
+                                 unsigned long long* unit_bytes, unsigned* unit_coef,
+                                 unsigned long long* n_band) {
   const int lane = threadIdx.x & 31;
   const long long u = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (u >= nunit) return;
   const long long iblk = u / ntiles, t = u % ntiles;
-  unsigned long long c = segcount[(iblk * TDW_TI + lane) * ntiles + t];
+  const long long sidx = (iblk * TDW_TI + lane) * ntiles + t;
+  unsigned long long c = segcount[sidx];
+  int lmax = hdr_len(hdr_tmp[sidx * TDW_TJ]);  // headers are sorted: rank 0 is the longest
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(FULLMASK, c, o);
-  if (lane == 0) unit_bytes[u] = TDW_UNIT_COEF_OFF + 16ull * c;
+  for (int o = 16; o > 0; o >>= 1) {
+    c += __shfl_xor_sync(FULLMASK, c, o);
+    lmax = max(lmax, __shfl_xor_sync(FULLMASK, lmax, o));
+  }
+  if (lane == 0) {
+    const int2 g = unit[u];
+    const int span = g.y >= g.x ? g.y - g.x : 0;
+    const unsigned coef = (!force32 && lmax <= 31 && span <= 63) ? TDW_UNIT_COEF_OFF16 : TDW_UNIT_COEF_OFF;
+    unit_coef[u] = coef;
+    unit_bytes[u] = coef + 16ull * c;
+    if (c) atomicAdd(n_band, c);
+  }
 }
 
 // per-unit header block: segment offsets, lag range, the 32x32 pair headers
 __global__ void unit_layout_kernel(const unsigned long long* segcount, const uint32_t* hdr_tmp,
-                                   const int2* unit, int ntiles, long long nunit,
-                                   const unsigned long long* unit_off, unsigned char* units,
-                                   unsigned* max_rel) {
+                                   const int2* unit, const unsigned* unit_coef, int ntiles,
+                                   long long nunit, const unsigned long long* unit_off,
+                                   unsigned char* units, unsigned* max_rel) {
   const int lane = threadIdx.x & 31;
   const long long u = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (u >= nunit) return;
@@ -322,13 +340,25 @@ __global__ void unit_layout_kernel(const unsigned long long* segcount, const uin
     if (lane >= o) x += y;
   }
   ((uint32_t*)ub)[lane] = x - c;  // exclusive prefix
+  const int2 g = unit[u];
+  const unsigned coef = unit_coef[u];
   if (lane == 0) {
-    *(int2*)(ub + TDW_UNIT_LAG_OFF) = unit[u];
+    *(int2*)(ub + TDW_UNIT_LAG_OFF) = g;
     *(uint32_t*)(ub + TDW_UNIT_LAG_OFF + 8) = (uint32_t)(unit_off[u + 1] - unit_off[u]);
+    *(uint32_t*)(ub + TDW_UNIT_LAG_OFF + 12) = coef;
   }
-  uint32_t* h = (uint32_t*)(ub + TDW_UNIT_HDR_OFF);
-  for (int r = 0; r < TDW_TI; ++r)
-    h[r * TDW_TJ + lane] = hdr_tmp[((iblk * TDW_TI + r) * ntiles + t) * TDW_TJ + lane];
+  const uint32_t* src = hdr_tmp + (iblk * TDW_TI * ntiles + t) * TDW_TJ + lane;
+  if (coef == TDW_UNIT_COEF_OFF16) {
+    uint16_t* h = (uint16_t*)(ub + TDW_UNIT_HDR_OFF);
+    for (int r = 0; r < TDW_TI; ++r) {
+      const uint32_t w = src[(size_t)r * ntiles * TDW_TJ];
+      const int len = hdr_len(w);
+      h[r * TDW_TJ + lane] = hdr16_pack(hdr_jl(w), len, len ? g.y - hdr_glo(w) : 0);
+    }
+  } else {
+    uint32_t* h = (uint32_t*)(ub + TDW_UNIT_HDR_OFF);
+    for (int r = 0; r < TDW_TI; ++r) h[r * TDW_TJ + lane] = src[(size_t)r * ntiles * TDW_TJ];
+  }
   if (lane == 31) atomicMax(max_rel, x);
 }
 
@@ -529,6 +559,8 @@ int tdw_assemble_impl(tdw_problem* pb) {
   TDW_CUDA(ctx, cudaMalloc(&pb->d_unit, sizeof(int2) * nunit));
   TDW_CUDA(ctx, cudaMalloc(&pb->d_unit_off, sizeof(unsigned long long) * (nunit + 1)));
   TDW_CUDA(ctx, cudaMalloc(&d_cnt, sizeof(unsigned long long) * 8));
+  unsigned* d_ucoef = nullptr;
+  TDW_CUDA(ctx, cudaMalloc(&d_ucoef, sizeof(unsigned) * nunit));
   TDW_CUDA(ctx, cudaMemsetAsync(d_cnt, 0, sizeof(unsigned long long) * 8, st));
   TDW_CUDA(ctx, cudaMemsetAsync(pb->d_flags, 0, sizeof(int) * 4, st));
   fill_unit_init<<<256, 256, 0, st>>>(pb->d_unit, nunit);
@@ -558,7 +590,10 @@ int tdw_assemble_impl(tdw_problem* pb) {
     count_kernel<<<(unsigned)blocks, threads, 0, st>>>(a);
     TDW_CUDA(ctx, cudaGetLastError());
     blocks = (nunit * 32 + threads - 1) / threads;
-    unit_size_kernel<<<(unsigned)blocks, threads, 0, st>>>(d_segcnt, pb->ntiles, nunit, pb->d_unit_off);
+    const char* f32 = getenv("TDW_HDR32");
+    unit_size_kernel<<<(unsigned)blocks, threads, 0, st>>>(d_segcnt, d_hdr_tmp, pb->d_unit, pb->ntiles, nunit,
+                                                          f32 && f32[0] == '1', pb->d_unit_off, d_ucoef,
+                                                          d_cnt + 7);
     TDW_CUDA(ctx, cudaGetLastError());
   }
   // unit byte offsets: exclusive scan of the unit sizes (in place; last slot = total)
@@ -581,23 +616,34 @@ int tdw_assemble_impl(tdw_problem* pb) {
   TDW_CUDA(ctx, cudaMemcpy(uoff.data(), pb->d_unit_off, sizeof(unsigned long long) * (nunit + 1),
                            cudaMemcpyDeviceToHost));
   const unsigned long long total_bytes = uoff[nunit];
-  pb->n_band = (int64_t)((total_bytes - (unsigned long long)TDW_UNIT_COEF_OFF * nunit) / 16);
+  {
+    unsigned long long nb = 0;
+    TDW_CUDA(ctx, cudaMemcpy(&nb, d_cnt + 7, sizeof(nb), cudaMemcpyDeviceToHost));
+    pb->n_band = (int64_t)nb;
+  }
   pb->max_unit_bytes = 0;
   for (long long u = 0; u < nunit; ++u)
     pb->max_unit_bytes = std::max<size_t>(pb->max_unit_bytes, uoff[u + 1] - uoff[u]);
+  std::vector<int2> hu(nunit);
   {
-    std::vector<int2> hu(nunit);
     TDW_CUDA(ctx, cudaMemcpy(hu.data(), pb->d_unit, sizeof(int2) * nunit, cudaMemcpyDeviceToHost));
+    std::vector<unsigned> hc(nunit);
+    TDW_CUDA(ctx, cudaMemcpy(hc.data(), d_ucoef, sizeof(unsigned) * nunit, cudaMemcpyDeviceToHost));
     int wm = 1;
-    for (const int2& u : hu)
-      if (u.y >= u.x) wm = std::max(wm, u.y - u.x + 1);
+    pb->n_units = pb->units_hdr32 = 0;
+    for (long long u = 0; u < nunit; ++u)
+      if (hu[u].y >= hu[u].x) {
+        wm = std::max(wm, hu[u].y - hu[u].x + 1);
+        ++pb->n_units;
+        pb->units_hdr32 += hc[u] == TDW_UNIT_COEF_OFF;
+      }
     pb->wmax = wm;
   }
   TDW_CUDA(ctx, cudaMalloc(&pb->d_units, total_bytes));
   {
     const int threads = 256;
     long long blocks = (nunit * 32 + threads - 1) / threads;
-    unit_layout_kernel<<<(unsigned)blocks, threads, 0, st>>>(d_segcnt, d_hdr_tmp, pb->d_unit,
+    unit_layout_kernel<<<(unsigned)blocks, threads, 0, st>>>(d_segcnt, d_hdr_tmp, pb->d_unit, d_ucoef,
                                                             pb->ntiles, nunit, pb->d_unit_off,
                                                             pb->d_units, (unsigned*)(d_cnt + 4));
     TDW_CUDA(ctx, cudaGetLastError());
@@ -653,6 +699,7 @@ int tdw_assemble_impl(tdw_problem* pb) {
   TDW_CUDA(ctx, cudaStreamSynchronize(st));
   cudaFree(d_hdr_tmp);
   cudaFree(d_segcnt);
+  cudaFree(d_ucoef);
 
   unsigned long long hc[8];
   TDW_CUDA(ctx, cudaMemcpy(hc, d_cnt, sizeof(hc), cudaMemcpyDeviceToHost));
@@ -717,7 +764,7 @@ int tdw_assemble_impl(tdw_problem* pb) {
         for (int t = tb; t < te; ++t) {
           const long long u = iblk * pb->ntiles + t;
           // units without band entries (FMM near field: non-adjacent patches) are not streamed
-          if (uoff[u + 1] - uoff[u] > TDW_UNIT_COEF_OFF || !pb->skip_empty_units) {
+          if (hu[u].y >= hu[u].x || !pb->skip_empty_units) {
             sched.push_back((unsigned)u);
             sitem.push_back((unsigned)it2);
           }

@@ -344,6 +344,8 @@ int tdw_problem_info(const tdw_problem* pb, tdw_info* out) {
   out->conv_grid = pb->conv_grid;
   out->conv_splits = pb->conv_S;
   out->solve_cluster = pb->sp_cl;
+  out->n_units = pb->n_units;
+  out->units_hdr32 = pb->units_hdr32;
   return TDW_OK;
 }
 

@@ -204,8 +204,8 @@ __global__ void __launch_bounds__(TDW_CONV_THREADS, 1)
       const unsigned char* ub = sm + *(volatile unsigned*)&region[stage];
       const uint32_t* rel = (const uint32_t*)ub;
       const int2 g = *(const int2*)(ub + TDW_UNIT_LAG_OFF);
-      const uint32_t* hdr = (const uint32_t*)(ub + TDW_UNIT_HDR_OFF);
-      const double2* coef = (const double2*)(ub + TDW_UNIT_COEF_OFF);
+      const unsigned coef_off = *(const uint32_t*)(ub + TDW_UNIT_LAG_OFF + 12);
+      const double2* coef = (const double2*)(ub + coef_off);
       const unsigned ubytes = (unsigned)((*(const uint32_t*)(ub + TDW_UNIT_LAG_OFF + 8) + 127u) & ~127u);
       const double2* hs = (const double2*)(ub + ubytes);
       const int W = a.wbox;
@@ -220,11 +220,11 @@ __global__ void __launch_bounds__(TDW_CONV_THREADS, 1)
 #pragma unroll
       for (int r = 0; r < TDW_ROWS_PER_WARP; ++r) {
         const int row = warp * TDW_ROWS_PER_WARP + r;
-        const uint32_t h = hdr[row * TDW_TJ + lane];
-        len[r] = hdr_len(h);
+        int jl, hrel;
+        unit_hdr(ub, coef_off, g.y, row * TDW_TJ + lane, jl, len[r], hrel);
         lmax = max(lmax, __shfl_sync(FULLMASK, len[r], 0));
         cp[r] = coef + rel[row] + lane;
-        hp[r] = hs + hdr_jl(h) * W + (g.y - hdr_glo(h));
+        hp[r] = hs + jl * W + hrel;
         off[r] = 0;
         s0[r] = 0.0;
         s1[r] = 0.0;

@@ -21,10 +21,16 @@
 // Unit layout (one (I-block, J-tile) unit = one contiguous byte range of the store):
 //   [0, 128)        uint32 seg_rel[32]  entry offset of row r's segment in the unit
 //   [128, 136)      int2 (gmin, gmax)   lag range of the unit (history slice)
-//   [256, 4352)     uint32 hdr[32][32]  pair headers, row-major, sorted by length per row
-//   [4352, ...)     double2 coef[]      (V_U, V_W) entries, jagged k-major per segment
+//   [136, 140)      uint32              unit bytes
+//   [140, 144)      uint32              coef offset: 2304 (16-bit headers) or 4352 (32-bit)
+//   [256, coef)     hdr[32][32]         pair headers, row-major, sorted by length per row
+//   [coef, ...)     double2 coef[]      (V_U, V_W) entries, jagged k-major per segment
+// A unit whose bands are all <= 31 lags long and whose lag range spans <= 64
+// lags (every unit of the benchmark configurations) carries 16-bit headers;
+// any other unit falls back to 32-bit headers.
 #define TDW_UNIT_LAG_OFF 128
 #define TDW_UNIT_HDR_OFF 256
+#define TDW_UNIT_COEF_OFF16 2304
 #define TDW_UNIT_COEF_OFF 4352
 #define TDW_EMPTY_UNIT 0xffffffffu
 
@@ -45,6 +51,25 @@ __host__ __device__ inline uint32_t hdr_pack(int jl, int len, int glo) {
 __host__ __device__ inline int hdr_jl(uint32_t h) { return (int)(h & 0xffu); }
 __host__ __device__ inline int hdr_len(uint32_t h) { return (int)((h >> 8) & 0xffu); }
 __host__ __device__ inline int hdr_glo(uint32_t h) { return (int)(h >> 16); }
+// 16-bit header: bits 0..4 column, 5..9 band length, 10..15 rel = unit gmax - first lag
+__host__ __device__ inline uint16_t hdr16_pack(int jl, int len, int rel) {
+  return (uint16_t)(jl | (len << 5) | (rel << 10));
+}
+// (column, length, rel) of pair (row, lane) of a unit, either header width
+__device__ __forceinline__ void unit_hdr(const unsigned char* ub, unsigned coef_off, int gmax,
+                                         int idx, int& jl, int& len, int& rel) {
+  if (coef_off == TDW_UNIT_COEF_OFF16) {
+    const unsigned h = ((const uint16_t*)(ub + TDW_UNIT_HDR_OFF))[idx];
+    jl = (int)(h & 31u);
+    len = (int)((h >> 5) & 31u);
+    rel = (int)(h >> 10);
+  } else {
+    const uint32_t h = ((const uint32_t*)(ub + TDW_UNIT_HDR_OFF))[idx];
+    jl = hdr_jl(h);
+    len = hdr_len(h);
+    rel = gmax - hdr_glo(h);
+  }
+}
 
 struct tdw_problem {
   tdw_ctx* ctx = nullptr;
@@ -81,6 +106,7 @@ struct tdw_problem {
   unsigned* d_sched_item = nullptr; // work item (I-block * S + split) of each entry
   unsigned* d_sched_off = nullptr; // [conv_grid + 1]
   int64_t n_band = 0, n_pairs = 0, n_evals = 0, store_bytes = 0;
+  int64_t n_units = 0, units_hdr32 = 0;  // non-empty units; those with 32-bit headers
   // lag-1 step matrix, all rows, ELL
   int ell_w = 0, step_nnz = 0;
   int* d_acol = nullptr;

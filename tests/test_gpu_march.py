@@ -83,9 +83,9 @@ def test_cfg2_full_size_matches_reference():
     np.testing.assert_allclose(np.linalg.norm(h.q, axis=1), g["unknown_norm"], rtol=TOL[1], atol=0)
 
 
-def _mini_spec(d, bie, phi_mode, nt=40, f=4):
+def _mini_spec(d, bie, phi_mode, nt=40, f=4, dt_scale=1.0):
     mesh = scenarios.build_mesh(0, frequency=f)
-    dt = scenarios.time_step(mesh)
+    dt = scenarios.time_step(mesh) * dt_scale
     sig, t0 = 4 * dt, 24 * dt
     zc, nz = mesh.centroids[:, 2].copy(), mesh.normals[:, 2].copy()
     phi = {"neumann": np.ones(mesh.n_elements), "dirichlet": np.zeros(mesh.n_elements),
@@ -117,6 +117,26 @@ def test_parameter_grid_matches_oracle(d, bie, phi_mode):
         ref = r[key]
         mask = np.linalg.norm(ref, axis=1) > 0
         assert per_step_rel(getattr(h, key)[mask], ref[mask]).max() < tol, key
+
+
+def test_header_widths_agree(monkeypatch):
+    """Units carry 16-bit pair headers when their bands are <= 31 lags and their
+    lag range <= 64 lags, 32-bit headers otherwise.  A small time step makes
+    both kinds occur in one store; forcing 32-bit headers everywhere
+    (TDW_HDR32=1) must give the same densities bit for bit."""
+    spec = _mini_spec(1, "obie", "neumann", nt=120, dt_scale=0.2)
+    mixed = marching.BandStore(spec).assemble()
+    inf = mixed.info()
+    assert 0 < inf["units_hdr32"] < inf["n_units"], inf
+    a = marching.march(spec, mats=mixed)
+    monkeypatch.setenv("TDW_HDR32", "1")
+    wide = marching.BandStore(spec).assemble()
+    assert wide.info()["units_hdr32"] == wide.info()["n_units"]
+    b = marching.march(spec, mats=wide)
+    np.testing.assert_array_equal(a.u, b.u)
+    r = _oracle(spec)
+    assert a.status == r["status"] and a.n_steps == r["n_steps"]
+    assert per_step_rel(a.u, r["u"]).max() < 1e-9
 
 
 def test_window_off_is_equivalent():
