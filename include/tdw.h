@@ -192,7 +192,9 @@ int tdw_problem_create_shard(tdw_ctx* ctx, const tdw_problem_desc* desc, tdw_pro
 int tdw_march_emulated(tdw_problem** shards, int n, double threshold);
 
 /* Multi-GPU (one process per GPU): rank 0 makes the id, the host broadcasts it
- * (torch.distributed), every rank calls tdw_comm_init before tdw_problem_create. */
+ * (torch.distributed), every rank calls tdw_comm_init before tdw_problem_create.
+ * nranks == 1 also creates a one-rank communicator, so the exchange path
+ * (all-gather inside the captured loop) can be exercised on a single GPU. */
 int tdw_nccl_unique_id(char out[128]);
 int tdw_comm_init(tdw_ctx* ctx, const char id[128], int nranks, int rank);
 

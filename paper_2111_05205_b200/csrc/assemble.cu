@@ -27,6 +27,7 @@
 
 #include <algorithm>
 #include <climits>
+#include <cstring>
 #include <cmath>
 
 #include "coeff.cuh"
@@ -523,6 +524,7 @@ static int choose_conv_schedule(tdw_problem* pb) {
   // the convolution is worth more than the solve time (~100 us per step)
   const double conv_est = (double)(pb->n_band * 16) / 6.0e12;
   const bool reserve = conv_est * pb->sp_cl / ctx->num_sms < 100e-6;
+  pb->conv_reserve = reserve;
   const int G = std::max(1, ctx->num_sms - (reserve ? pb->sp_cl : 0));
   // items = (I-block, tile split); pick the split count that balances the waves
   int bestS = 1;
@@ -625,17 +627,18 @@ int tdw_assemble_impl(tdw_problem* pb) {
   for (long long u = 0; u < nunit; ++u)
     pb->max_unit_bytes = std::max<size_t>(pb->max_unit_bytes, uoff[u + 1] - uoff[u]);
   std::vector<int2> hu(nunit);
+  std::vector<unsigned> ucoef;  // coefficient offset of every unit (= its header block size)
   {
     TDW_CUDA(ctx, cudaMemcpy(hu.data(), pb->d_unit, sizeof(int2) * nunit, cudaMemcpyDeviceToHost));
-    std::vector<unsigned> hc(nunit);
-    TDW_CUDA(ctx, cudaMemcpy(hc.data(), d_ucoef, sizeof(unsigned) * nunit, cudaMemcpyDeviceToHost));
+    ucoef.resize(nunit);
+    TDW_CUDA(ctx, cudaMemcpy(ucoef.data(), d_ucoef, sizeof(unsigned) * nunit, cudaMemcpyDeviceToHost));
     int wm = 1;
     pb->n_units = pb->units_hdr32 = 0;
     for (long long u = 0; u < nunit; ++u)
       if (hu[u].y >= hu[u].x) {
         wm = std::max(wm, hu[u].y - hu[u].x + 1);
         ++pb->n_units;
-        pb->units_hdr32 += hc[u] == TDW_UNIT_COEF_OFF;
+        pb->units_hdr32 += ucoef[u] == TDW_UNIT_COEF_OFF;
       }
     pb->wmax = wm;
   }
@@ -750,11 +753,62 @@ int tdw_assemble_impl(tdw_problem* pb) {
     if (rc) return rc;
   }
   {
-    const int G = pb->conv_grid, S = pb->conv_S;
-    const long long items = (long long)pb->n_iblk * S;
+    int G = pb->conv_grid, S = pb->conv_S;
     std::vector<unsigned> sched, sitem, soff(G + 1, 0);
     sched.reserve(nunit);
     sitem.reserve(nunit);
+    auto streamed = [&](long long u) { return hu[u].y >= hu[u].x || !pb->skip_empty_units; };
+    const char* sm = getenv("TDW_SCHED");
+    if (!(sm && strcmp(sm, "rr") == 0)) {
+      // byte-balanced contiguous chunks: the units in (I-block, tile) order are cut
+      // into G runs of equal streamed bytes (+ a fixed per-unit cost), so every
+      // persistent CTA ends together.  An I-block cut by chunk boundaries gets one
+      // partial per chunk touching it; S = the most chunks touching one I-block.
+      // weight: coefficient bytes + a fixed per-unit cost (header, history box);
+      // independent of the header width, so both widths give the same schedule
+      const double per_unit = 4096.0;
+      auto weight = [&](long long u) { return (double)(uoff[u + 1] - uoff[u] - ucoef[u]) + per_unit; };
+      double total = 0.0;
+      long long nstream = 0;
+      for (long long u = 0; u < nunit; ++u)
+        if (streamed(u)) {
+          total += weight(u);
+          ++nstream;
+        }
+      G = (int)std::max(1LL, std::min<long long>(ctx->num_sms - (pb->conv_reserve ? pb->sp_cl : 0), nstream));
+      soff.assign(G + 1, 0);
+      std::vector<int> chunk_of(nunit, -1);
+      double acc = 0.0;
+      for (long long u = 0; u < nunit; ++u) {
+        if (!streamed(u)) continue;
+        const double w = weight(u);
+        chunk_of[u] = std::min(G - 1, (int)((acc + 0.5 * w) / total * G));
+        acc += w;
+      }
+      std::vector<int> clo(pb->n_iblk, INT_MAX);
+      S = 1;
+      for (int ib = 0; ib < pb->n_iblk; ++ib) {
+        int lo = INT_MAX, hi = -1;
+        for (int t = 0; t < pb->ntiles; ++t) {
+          const int c = chunk_of[(long long)ib * pb->ntiles + t];
+          if (c >= 0) { lo = std::min(lo, c); hi = std::max(hi, c); }
+        }
+        clo[ib] = lo;
+        if (hi >= 0) S = std::max(S, hi - lo + 1);
+      }
+      int k = 0;
+      for (long long u = 0; u < nunit; ++u) {
+        if (chunk_of[u] < 0) continue;
+        while (k <= chunk_of[u]) soff[k++] = (unsigned)sched.size();
+        const long long ib = u / pb->ntiles;
+        sched.push_back((unsigned)u);
+        sitem.push_back((unsigned)(ib * S + (chunk_of[u] - clo[ib])));
+      }
+      while (k < G) soff[k++] = (unsigned)sched.size();
+      pb->conv_grid = G;
+      pb->conv_S = S;
+    } else {
+    const long long items = (long long)pb->n_iblk * S;
     for (int b = 0; b < G; ++b) {
       soff[b] = (unsigned)sched.size();
       for (long long it2 = b; it2 < items; it2 += G) {
@@ -764,7 +818,7 @@ int tdw_assemble_impl(tdw_problem* pb) {
         for (int t = tb; t < te; ++t) {
           const long long u = iblk * pb->ntiles + t;
           // units without band entries (FMM near field: non-adjacent patches) are not streamed
-          if (hu[u].y >= hu[u].x || !pb->skip_empty_units) {
+          if (streamed(u)) {
             sched.push_back((unsigned)u);
             sitem.push_back((unsigned)it2);
           }
@@ -774,6 +828,7 @@ int tdw_assemble_impl(tdw_problem* pb) {
           sitem.push_back((unsigned)it2);
         }
       }
+    }
     }
     soff[G] = (unsigned)sched.size();
     TDW_CUDA(ctx, cudaMalloc(&pb->d_sched, sizeof(unsigned) * std::max<size_t>(1, sched.size())));

@@ -82,7 +82,9 @@ int tdw_nccl_unique_id(char out[128]) {
 
 int tdw_comm_init(tdw_ctx* ctx, const char id[128], int nranks, int rank) {
   if (!ctx || nranks < 1 || rank < 0 || rank >= nranks) return TDW_ERR_INVALID_ARG;
-  if (nranks == 1) return TDW_OK;
+  if (ctx->comm) return tdw_fail(ctx, TDW_ERR_STATE, "tdw_comm_init: communicator already set");
+  // nranks == 1 also creates a (one-rank) communicator: the march then takes the
+  // exchange path, all-gather included, which lets a single GPU exercise it
   ncclUniqueId uid;
   memcpy(uid.internal, id, 128);
   cudaSetDevice(ctx->device);

@@ -917,7 +917,7 @@ int make_plan(tdw_problem* pb, LoopPlan& L, double threshold, bool want_rhs) {
   TDW_CUDA(ctx, cudaFuncSetAttribute(conv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)L.smem));
   L.cgrid = dim3(pb->conv_grid);
-  L.multi = pb->nranks > 1;
+  L.multi = ctx->comm != nullptr;
   ClusterSolveArgs& cs = L.cs;
   cs.b = pb->d_b;
   cs.sp_rowptr = pb->d_sp_rowptr;
@@ -1054,6 +1054,8 @@ int tdw_march_loop(tdw_problem* pb, double threshold, bool want_rhs, bool time_k
   cudaStream_t st = ctx->stream;
   if (!pb->assembled) return tdw_fail(ctx, TDW_ERR_STATE, "tdw_march before tdw_assemble");
   if (!pb->known_loaded) return tdw_fail(ctx, TDW_ERR_STATE, "known boundary data not uploaded");
+  if (pb->nranks > 1 && !ctx->comm)
+    return tdw_fail(ctx, TDW_ERR_STATE, "row-sharded problem without a communicator (tdw_comm_init)");
   if (pb->fmm) return tdw_fmm_loop(pb, threshold, want_rhs, timing);
   if (want_rhs) {
     if (!pb->d_rhs)

@@ -3,17 +3,20 @@
 tdw_march_emulated runs R shards (ranks) in one process on one device: each
 shard assembles only its rows of the banded store and convolves them, reduces
 its split partials into its block of b, the in-place all-gather is replaced by
-device copies, and every shard runs the redundant cluster solve.  Only the NCCL
-call itself is not exercised (it is a plain in-place ncclAllGather).  Results
+device copies, and every shard runs the redundant cluster solve.  The NCCL
+exchange itself runs through a one-rank communicator (tdw_comm_init with
+nranks = 1): the same captured loop with the in-place ncclAllGather.  Results
 must equal the single-rank march (the per-row partial sums are grouped
 differently, so agreement is to round-off, not bitwise) and all shards must
 hold identical histories.
 """
+import ctypes as C
+
 import numpy as np
 import pytest
 
 from conftest import per_step_rel
-from paper_2111_05205_b200 import distributed, marching, scenarios
+from paper_2111_05205_b200 import _lib, distributed, marching, scenarios
 
 pytestmark = pytest.mark.gpu
 
@@ -43,3 +46,27 @@ def test_shards_partition_the_band():
               for r in range(3)]
     assert sum(s["n_band"] for s in shards) == full["n_band"]
     assert sum(s["n_pairs"] for s in shards) == full["n_pairs"]
+
+
+@pytest.mark.parametrize("cfg", [0, 2])
+def test_one_rank_nccl_exchange_path(cfg):
+    """The NCCL all-gather path (captured into the loop's CUDA graph) on a
+    one-rank communicator gives the single-rank march bit for bit."""
+    spec = scenarios.build_spec(cfg)
+    ref = marching.march(spec)
+    lib = _lib.load()
+    ctx = _lib.Context(0)
+    buf = C.create_string_buffer(128)
+    _lib.check(lib.tdw_nccl_unique_id(buf), ctx.h, "tdw_nccl_unique_id")
+    _lib.check(lib.tdw_comm_init(ctx.h, buf.raw, 1, 0), ctx.h, "tdw_comm_init")
+    with pytest.raises(RuntimeError):
+        _lib.check(lib.tdw_comm_init(ctx.h, buf.raw, 1, 0), ctx.h, "tdw_comm_init")
+    store = marching.BandStore(spec, ctx=ctx).assemble()
+    h1 = marching.march(spec, mats=store)
+    h2 = marching.march(spec, mats=store)
+    for h in (h1, h2):
+        assert h.status == ref.status and h.n_steps == ref.n_steps
+        np.testing.assert_array_equal(h.u, ref.u)
+        np.testing.assert_array_equal(h.q, ref.q)
+    store.close()
+    ctx.close()
