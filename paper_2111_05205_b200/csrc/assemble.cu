@@ -187,13 +187,10 @@ __global__ void __launch_bounds__(256) count_kernel(AsmArgs a) {
     }
     if (len > 255) { atomicExch(&a.flags[3], 2); len = 255; }
   }
-  int rank = 0;
-#pragma unroll
-  for (int m = 0; m < 32; ++m) {
-    int lm = __shfl_sync(FULLMASK, len, m);
-    rank += (lm > len) || (lm == len && m < lane);
-  }
-  a.hdr[seg * TDW_TJ + rank] = hdr_pack(lane, len, glo);
+  // lane = column: the convolution's lanes then read one 512-byte row of the
+  // [lag][column] history box (no shared-memory bank conflicts)
+  a.hdr[seg * TDW_TJ + lane] = hdr_pack(lane, len, glo);
+  const int lmax = __reduce_max_sync(FULLMASK, len);
   int tot = len, gmin = len ? glo : INT_MAX, gmax = len ? glo + len - 1 : -1, np = any ? 1 : 0;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -203,7 +200,7 @@ __global__ void __launch_bounds__(256) count_kernel(AsmArgs a) {
     gmax = max(gmax, __shfl_xor_sync(FULLMASK, gmax, o));
   }
   if (lane == 0) {
-    a.segcount[seg] = (unsigned long long)tot;
+    a.segcount[seg] = (unsigned long long)tot | ((unsigned long long)lmax << TDW_SEG_LMAX_SHIFT);
     if (np) atomicAdd(a.n_pairs, (unsigned long long)np);
     if (tot) {
       int2* u = &a.unit[(rloc / TDW_TI) * a.ntiles + t];
@@ -227,7 +224,7 @@ __global__ void __launch_bounds__(128) fill_kernel(AsmArgs a) {
   int jl, len, rel;
   unit_hdr(ub, coef_off, gmax, r * TDW_TJ + lane, jl, len, rel);
   const int glo = gmax - rel;
-  const int lmax = __shfl_sync(FULLMASK, len, 0);
+  const int lmax = __reduce_max_sync(FULLMASK, len);
   if (lmax == 0) return;
   const int i = a.row_lo + rloc, j = t * TDW_TJ + jl;
   double2* coef = (double2*)(ub + coef_off);
@@ -286,7 +283,7 @@ __global__ void __launch_bounds__(128) fill_kernel(AsmArgs a) {
         vu = pj == 1.0 ? vu : 0.0;
         vw = pj == 1.0 ? 0.0 : vw;
       }
-      coef[off + lane] = make_double2(vu, vw);
+      coef[off + __popc(m & ((1u << lane) - 1u))] = make_double2(vu, vw);
     }
     off += __popc(m);
   }
@@ -306,8 +303,8 @@ __global__ void unit_size_kernel(const unsigned long long* segcount, const uint3
   if (u >= nunit) return;
   const long long iblk = u / ntiles, t = u % ntiles;
   const long long sidx = (iblk * TDW_TI + lane) * ntiles + t;
-  unsigned long long c = segcount[sidx];
-  int lmax = hdr_len(hdr_tmp[sidx * TDW_TJ]);  // headers are sorted: rank 0 is the longest
+  unsigned long long c = segcount[sidx] & TDW_SEG_COUNT_MASK;
+  int lmax = (int)(segcount[sidx] >> TDW_SEG_LMAX_SHIFT);  // longest band of the segment
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     c += __shfl_xor_sync(FULLMASK, c, o);
@@ -333,7 +330,7 @@ __global__ void unit_layout_kernel(const unsigned long long* segcount, const uin
   if (u >= nunit) return;
   const long long iblk = u / ntiles, t = u % ntiles;
   unsigned char* ub = units + unit_off[u];
-  const unsigned c = (unsigned)segcount[(iblk * TDW_TI + lane) * ntiles + t];
+  const unsigned c = (unsigned)(segcount[(iblk * TDW_TI + lane) * ntiles + t] & TDW_SEG_COUNT_MASK);
   unsigned x = c;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -510,8 +507,8 @@ static int choose_conv_schedule(tdw_problem* pb) {
   // FIFO capacity: all opt-in shared memory but the kernel's static part
   const size_t cap = std::min<size_t>((size_t)maxsm - 1024, 224 * 1024) / 128 * 128;
   pb->wbox = pb->wmax;
-  if (2 * pb->wbox > 256)
-    return tdw_fail(ctx, TDW_ERR_LIMIT, "history slice of a unit exceeds 128 lags (TMA box limit)");
+  if (pb->wbox > 256)
+    return tdw_fail(ctx, TDW_ERR_LIMIT, "history slice of a unit exceeds 256 lags (TMA box limit)");
   const size_t hist_bytes = sizeof(double2) * TDW_TJ * (size_t)pb->wbox;
   const size_t worst = (pb->max_unit_bytes + 127) / 128 * 128 + (hist_bytes + 127) / 128 * 128;
   if (worst > cap)

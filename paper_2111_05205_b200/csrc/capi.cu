@@ -288,6 +288,7 @@ int tdw_problem_create_impl(tdw_ctx* ctx, const tdw_problem_desc* dsc, tdw_probl
   pb->cap = pb->window ? std::min(pb->gstar, pb->nt - 1) : pb->nt - 1;
   pb->pad = pb->cap + 1;
   pb->hstride = pb->pad + pb->nt - 1;
+  pb->hcols = pb->ntiles * TDW_TJ;
 
   // step buffers
   pb->nsplit = 1;
@@ -302,7 +303,7 @@ int tdw_problem_create_impl(tdw_ctx* ctx, const tdw_problem_desc* dsc, tdw_probl
   TDW_TRY(cudaMalloc(&pb->d_b, sizeof(double) * 2 * pb->bstride));
   TDW_TRY(cudaMemset(pb->d_b, 0, sizeof(double) * 2 * pb->bstride));
   TDW_TRY(cudaMalloc(&pb->d_x, sizeof(double) * 2 * (size_t)ns));
-  TDW_TRY(cudaMalloc(&pb->d_hist, sizeof(double2) * (size_t)ns * pb->hstride));
+  TDW_TRY(cudaMalloc(&pb->d_hist, sizeof(double2) * (size_t)pb->hcols * pb->hstride));
   TDW_TRY(cudaMalloc(&pb->d_bar, sizeof(unsigned) * 2));
   {
     const int occ = 2;  // solve_kernel: 256 threads, tiny smem; 2 per SM are always co-resident

@@ -98,13 +98,13 @@ __device__ __forceinline__ void bw(int d, double* w) {
 
 // tau_j^beta / sigma_j^beta (stock sums, marching.py:205-214) from the history;
 // slot beta holds the known part until step beta+1 is solved (tilde sums).
-__device__ __forceinline__ double2 stock(const double2* __restrict__ hist, int hstride, int pad,
+__device__ __forceinline__ double2 stock(const double2* __restrict__ hist, int hcols, int pad,
                                          int j, int beta, int d, const double* w) {
   double t = 0.0, s = 0.0;
   const int kmax = min(d + 1, beta);
-  const double2* h = hist + (size_t)j * hstride + pad + beta;
+  const double2* h = hist + (size_t)(pad + beta) * hcols + j;
   for (int k = 0; k <= kmax; ++k) {
-    const double2 v = h[-k];
+    const double2 v = h[-(ptrdiff_t)k * hcols];
     t += w[k] * v.x;
     s += w[k] * v.y;
   }
@@ -139,7 +139,7 @@ __global__ void extra_coeff_kernel(const double* __restrict__ elem, const int* _
 
 __global__ void extra_apply_kernel(const int* __restrict__ row_ptr, const int* __restrict__ col,
                                    const double* __restrict__ U, const double* __restrict__ W,
-                                   int lags, int gmax, const double2* __restrict__ hist, int hstride,
+                                   int lags, int gmax, const double2* __restrict__ hist, int hcols,
                                    int pad, int alpha, int d, int ns, double* b, const int* flags) {
   if (flags[0] != 0) return;
   double w[5] = {0, 0, 0, 0, 0};
@@ -149,7 +149,7 @@ __global__ void extra_apply_kernel(const int* __restrict__ row_ptr, const int* _
     for (int p = row_ptr[i]; p < row_ptr[i + 1]; ++p) {
       const int j = col[p];
       for (int g = 1; g <= gmax; ++g) {
-        const double2 ts = stock(hist, hstride, pad, j, alpha - g, d, w);
+        const double2 ts = stock(hist, hcols, pad, j, alpha - g, d, w);
         acc += U[(size_t)p * lags + g - 1] * ts.x - W[(size_t)p * lags + g - 1] * ts.y;
       }
     }
@@ -189,7 +189,7 @@ __global__ void l2p_kernel(const int* __restrict__ elem_cell, const double* __re
 
 __global__ void p2m_kernel(const int* __restrict__ cell_ptr, const int* __restrict__ cell_elems,
                            const double* __restrict__ ptau, const double* __restrict__ psig,
-                           const double2* __restrict__ hist, int hstride, int pad, int beta0, int d,
+                           const double2* __restrict__ hist, int hcols, int pad, int beta0, int d,
                            StepW sw, double* acc, const int* flags) {
   if (flags[0] != 0) return;
   double w[5] = {0, 0, 0, 0, 0};
@@ -198,7 +198,7 @@ __global__ void p2m_kernel(const int* __restrict__ cell_ptr, const int* __restri
   double spat = 0.0;
   for (int q = cell_ptr[cell]; q < cell_ptr[cell + 1]; ++q) {
     const int e = cell_elems[q];
-    const double2 ts = stock(hist, hstride, pad, e, beta0, d, w);
+    const double2 ts = stock(hist, hcols, pad, e, beta0, d, w);
     spat += ptau[(size_t)e * FN3 + s] * ts.x - psig[(size_t)e * FN3 + s] * ts.y;
   }
   double* A = acc + (size_t)cell * FND + s * FPT;
@@ -431,8 +431,9 @@ extern "C" int tdw_fmm_setup(tdw_problem* pb, const tdw_fmm_desc* fd) {
   for (int x = 0; x < fd->n_extra; ++x) maxlag = std::max(maxlag, fd->extra_lags[x]);
   pb->pad = maxlag + d + 2;
   pb->hstride = pb->pad + nt - 1;
+  pb->hcols = pb->ntiles * TDW_TJ;
   cudaFree(pb->d_hist);
-  TDW_CUDA(ctx, cudaMalloc(&pb->d_hist, sizeof(double2) * (size_t)ns * pb->hstride));
+  TDW_CUDA(ctx, cudaMalloc(&pb->d_hist, sizeof(double2) * (size_t)pb->hcols * pb->hstride));
   // leaf element data, internal order
   if ((rc = up(ctx, &F->elem_cell, ecell.data(), ns))) return rc;
   {
@@ -762,7 +763,7 @@ int tdw_fmm_loop(tdw_problem* pb, double threshold, bool want_rhs, tdw_timing* t
       const int g = (int)E.gmax[alpha];
       if (g <= 0 || E.npair == 0) continue;
       extra_apply_kernel<<<(pb->ns + 127) / 128, 128, 0, st>>>(E.row_ptr, E.col, E.U, E.W, E.lags, g,
-                                                              pb->d_hist, pb->hstride, pb->pad,
+                                                              pb->d_hist, pb->hcols, pb->pad,
                                                               alpha, pb->d, pb->ns, b, pb->d_flags);
     }
     StepW sw;
@@ -780,7 +781,7 @@ int tdw_fmm_loop(tdw_problem* pb, double threshold, bool want_rhs, tdw_timing* t
     if ((rc = launch_solve_fmm(pb, plan, alpha, st))) return rc;
     if (LV)
       p2m_kernel<<<LV->ncell, FN3, 0, st>>>(F->cell_ptr, F->cell_elems, F->p2m_tau, F->p2m_sig,
-                                             pb->d_hist, pb->hstride, pb->pad, alpha - 1, pb->d, sw,
+                                             pb->d_hist, pb->hcols, pb->pad, alpha - 1, pb->d, sw,
                                              LV->acc, pb->d_flags);
     TDW_CUDA(ctx, cudaGetLastError());
   }

@@ -8,8 +8,10 @@
 //   K3/K4 solve_kernel  b = sum of partials, Jacobi sweeps on A x = b (lu.solve, :330),
 //                     residual test (:331-333), promotion of x into u/q (finalize_step,
 //                     :239-242), blow-up detector (:336-338), next step's known data.
-// History: hist[j][pad + beta] = (q_j^beta, u_j^beta) (element-major, time contiguous,
-// zero padded for beta < 0), so a band reads consecutive slots of one element.
+// History: hist[pad + beta][j] = (q_j^beta, u_j^beta) (time-major, one row of hcols
+// elements per step, zero padded for beta < 0 and j >= ns).  The convolution
+// stages a [lags][32 columns] box of it, so the 32 lanes of a warp (one column
+// each) read one 512-byte row: shared-memory reads without bank conflicts.
 #include <cooperative_groups.h>
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -81,7 +83,7 @@ struct ConvArgs {
   const double2* __restrict__ hist;
   double* __restrict__ bpart;
   const int* __restrict__ flags;
-  int hstride, pad, ns, rows_loc, ntiles, S, alpha, nstages, wbox;
+  int hcols, pad, ns, rows_loc, ntiles, S, alpha, nstages, wbox;
   unsigned stage_bytes;  // shared-memory FIFO capacity
 };
 
@@ -90,7 +92,7 @@ struct ConvArgs {
 // K2: history convolution.  Persistent CTAs walk a precomputed list of store
 // units.  Warp 8 (producer) streams each unit -- one contiguous byte range:
 // segment offsets, lag range, pair headers, (V_U, V_W) entries -- plus the
-// unit's 32 history rows (hist[j][pad + alpha - gmax .. alpha - gmin]) into a
+// unit's history box (hist[pad + alpha - gmax .. alpha - gmin][32 columns]) into a
 // ring of shared-memory stages with cp.async.bulk, completion on an mbarrier.
 // Warps 0..7 (consumers, 4 rows each) compute from shared memory only and
 // release the stage.  Row sums of a work item (I-block, tile split) go to
@@ -174,8 +176,8 @@ __global__ void __launch_bounds__(TDW_CONV_THREADS, 1)
           const unsigned len = min(chunk, qbytes - c);
           bulk_g2s(sbase + c, a.units + qoff + c, len, &full[slot]);
         }
-        if (W > 0 && lane == 0)  // hist[t*32 .. +32][pad+alpha-gmax .. +wbox) as one 2-D box
-          tensor2d_g2s(sbase + ubytes, &hmap, 2 * (a.pad + a.alpha - gmax), t * TDW_TJ, &full[slot]);
+        if (W > 0 && lane == 0)  // hist[pad+alpha-gmax .. +wbox)[t*32 .. +32] as one 2-D box
+          tensor2d_g2s(sbase + ubytes, &hmap, 2 * t * TDW_TJ, a.pad + a.alpha - gmax, &full[slot]);
         h += need;
         ++n;
       }
@@ -208,10 +210,11 @@ __global__ void __launch_bounds__(TDW_CONV_THREADS, 1)
       const double2* coef = (const double2*)(ub + coef_off);
       const unsigned ubytes = (unsigned)((*(const uint32_t*)(ub + TDW_UNIT_LAG_OFF + 8) + 127u) & ~127u);
       const double2* hs = (const double2*)(ub + ubytes);
-      const int W = a.wbox;
       // the warp's rows are interleaved (independent FMA chains); the k loop is
-      // unrolled and predicated: lanes are sorted by band length, so "len > k"
-      // is a lane prefix and the k-th entries of a segment are contiguous
+      // unrolled and predicated.  Lane = column: the k-th entries of a segment
+      // are those of the lanes with band > k, packed in lane order; the history
+      // box is [lag][32 columns], so a warp reads one 512-byte row per k.
+      const unsigned lt = (1u << lane) - 1u;
       int len[TDW_ROWS_PER_WARP], lmax = 0;
       const double2* cp[TDW_ROWS_PER_WARP];
       const double2* hp[TDW_ROWS_PER_WARP];
@@ -222,13 +225,14 @@ __global__ void __launch_bounds__(TDW_CONV_THREADS, 1)
         const int row = warp * TDW_ROWS_PER_WARP + r;
         int jl, hrel;
         unit_hdr(ub, coef_off, g.y, row * TDW_TJ + lane, jl, len[r], hrel);
-        lmax = max(lmax, __shfl_sync(FULLMASK, len[r], 0));
-        cp[r] = coef + rel[row] + lane;
-        hp[r] = hs + jl * W + hrel;
+        lmax = max(lmax, len[r]);
+        cp[r] = coef + rel[row];
+        hp[r] = hs + hrel * TDW_TJ + jl;
         off[r] = 0;
         s0[r] = 0.0;
         s1[r] = 0.0;
       }
+      lmax = __reduce_max_sync(FULLMASK, lmax);
       for (int k0 = 0; k0 < lmax; k0 += 4) {
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk) {
@@ -238,8 +242,8 @@ __global__ void __launch_bounds__(TDW_CONV_THREADS, 1)
             const bool on = len[r] > k;
             const unsigned m = __ballot_sync(FULLMASK, on);
             if (on) {
-              const double2 cv = cp[r][off[r]];
-              const double2 hv = hp[r][-k];
+              const double2 cv = cp[r][off[r] + __popc(m & lt)];
+              const double2 hv = hp[r][-k * TDW_TJ];
               s0[r] = fma(cv.x, hv.x, s0[r]);
               s1[r] = fma(cv.y, hv.y, s1[r]);
             }
@@ -363,7 +367,7 @@ struct ClusterSolveArgs {
   double* rhs;
   double threshold;
   unsigned long long* trace;                // optional phase timestamps (globaltimer, ns)
-  int hstride, pad, ns, nsplit, rows_loc, alpha, nt, R, maxit, near_w;
+  int hcols, pad, ns, nsplit, rows_loc, alpha, nt, R, maxit, near_w;
 };
 
 __device__ __forceinline__ void trace_mark(unsigned long long* t, int k) {
@@ -575,7 +579,7 @@ __global__ void __launch_bounds__(1024, 1) solve_cluster_kernel(ClusterSolveArgs
     const size_t kb = (size_t)beta0 * a.ns + o;
     const double qv = ph == 1.0 ? a.qk[kb] : xj;
     const double uv = ph == 1.0 ? xj : a.uk[kb];
-    a.hist[(size_t)j * a.hstride + a.pad + beta0] = make_double2(qv, uv);
+    a.hist[(size_t)(a.pad + beta0) * a.hcols + j] = make_double2(qv, uv);
   }
   if (cr == 0 && tid == 0) {
     a.flags[1] = a.alpha;
@@ -774,7 +778,7 @@ __global__ void __launch_bounds__(reg_threads<MAXNZ>(), 1) solve_reg_kernel(Clus
     const size_t kb = (size_t)beta0 * a.ns + o;
     const double qv = ph == 1.0 ? a.qk[kb] : xi;
     const double uv = ph == 1.0 ? xi : a.uk[kb];
-    a.hist[(size_t)gi * a.hstride + a.pad + beta0] = make_double2(qv, uv);
+    a.hist[(size_t)(a.pad + beta0) * a.hcols + gi] = make_double2(qv, uv);
   }
   if (cr == 0 && tid == 0) {
     a.flags[1] = a.alpha;
@@ -783,19 +787,19 @@ __global__ void __launch_bounds__(reg_threads<MAXNZ>(), 1) solve_reg_kernel(Clus
   trace_mark(tr, 8);
 }
 
-// hist[j][pad + beta] = known part (phi q_known, (1-phi) u_known) of every
+// hist[pad + beta][j] = known part (phi q_known, (1-phi) u_known) of every
 // step; the solve of step beta+1 overwrites it with the full (q, u).  Zero pad
-// for beta < 0.
-__global__ void init_hist_kernel(double2* hist, int hstride, int pad, int ns, int nt,
+// for beta < 0 and for the columns j >= ns.
+__global__ void init_hist_kernel(double2* hist, int hstride, int hcols, int pad, int ns, int nt,
                                  const double* phi, const int* perm, const double* uk,
                                  const double* qk) {
-  const long long n = (long long)ns * hstride;
+  const long long n = (long long)hcols * hstride;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n;
        e += (long long)gridDim.x * blockDim.x) {
-    const int j = (int)(e / hstride), sl = (int)(e % hstride);
+    const int sl = (int)(e / hcols), j = (int)(e % hcols);
     const int beta = sl - pad;
     double2 v = make_double2(0.0, 0.0);
-    if (beta >= 0 && beta < nt - 1) {
+    if (beta >= 0 && beta < nt - 1 && j < ns) {
       const double ph = phi[j];
       const size_t o = (size_t)beta * ns + perm[j];
       v = make_double2(ph * qk[o], (1.0 - ph) * uk[o]);
@@ -806,7 +810,7 @@ __global__ void init_hist_kernel(double2* hist, int hstride, int pad, int ns, in
 
 // (nt-1, ns) outputs in the original element order; kappa sums as stock_sums
 // (marching.py:205-214); rows at and after n_steps stay zero.
-__global__ void outputs_kernel(const double2* hist, int hstride, int pad, int ns, int nt, int d,
+__global__ void outputs_kernel(const double2* hist, int hcols, int pad, int ns, int nt, int d,
                                const int* perm, const int* flags, double* u, double* q,
                                double* tau, double* sig) {
   const int nsteps = flags[1];
@@ -826,15 +830,17 @@ __global__ void outputs_kernel(const double2* hist, int hstride, int pad, int ns
       if (sig) sig[o] = 0.0;
       continue;
     }
-    const double2* h = hist + (size_t)j * hstride + pad;
-    if (q) q[o] = h[beta].x;
-    if (u) u[o] = h[beta].y;
+    const double2* h = hist + (size_t)pad * hcols + j;
+    const double2 hb = h[(size_t)beta * hcols];
+    if (q) q[o] = hb.x;
+    if (u) u[o] = hb.y;
     if (tau || sig) {
       double ta = 0.0, sa = 0.0;
       const int kmax = min(d + 1, beta);
       for (int k = 0; k <= kmax; ++k) {
-        ta += w[k] * h[beta - k].x;
-        sa += w[k] * h[beta - k].y;
+        const double2 v = h[(size_t)(beta - k) * hcols];
+        ta += w[k] * v.x;
+        sa += w[k] * v.y;
       }
       if (tau) tau[o] = ta;
       if (sig) sig[o] = sa;
@@ -851,8 +857,8 @@ typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_
                                     const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
                                     CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
-// 2-D view of the history: rows = elements, inner = 2*hstride doubles; box =
-// [32 elements][2*wbox doubles], out-of-range lags/elements read as zero.
+// 2-D view of the history: rows = steps, inner = 2*hcols doubles; box =
+// [wbox steps][64 doubles = 32 elements x (q, u)].
 static int make_hist_map(tdw_problem* pb, CUtensorMap* map) {
   static PFN_encodeTiled enc = nullptr;
   if (!enc) {
@@ -863,9 +869,9 @@ static int make_hist_map(tdw_problem* pb, CUtensorMap* map) {
       return tdw_fail(pb->ctx, TDW_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
     enc = (PFN_encodeTiled)fn;
   }
-  cuuint64_t dims[2] = {(cuuint64_t)2 * pb->hstride, (cuuint64_t)pb->ns};
-  cuuint64_t strides[1] = {(cuuint64_t)pb->hstride * 16};
-  cuuint32_t box[2] = {(cuuint32_t)(2 * pb->wbox), (cuuint32_t)TDW_TJ};
+  cuuint64_t dims[2] = {(cuuint64_t)2 * pb->hcols, (cuuint64_t)pb->hstride};
+  cuuint64_t strides[1] = {(cuuint64_t)pb->hcols * 16};
+  cuuint32_t box[2] = {(cuuint32_t)(2 * TDW_TJ), (cuuint32_t)pb->wbox};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, pb->d_hist, dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -885,7 +891,7 @@ static void fill_conv_args(tdw_problem* pb, ConvArgs& c) {
   c.hist = pb->d_hist;
   c.bpart = pb->d_bpart;
   c.flags = pb->d_flags;
-  c.hstride = pb->hstride;
+  c.hcols = pb->hcols;
   c.pad = pb->pad;
   c.ns = pb->ns;
   c.rows_loc = pb->rows_per_rank;
@@ -936,7 +942,7 @@ int make_plan(tdw_problem* pb, LoopPlan& L, double threshold, bool want_rhs) {
   cs.flags = pb->d_flags;
   cs.rhs = want_rhs ? pb->d_rhs : nullptr;
   cs.threshold = threshold;
-  cs.hstride = pb->hstride;
+  cs.hcols = pb->hcols;
   cs.pad = pb->pad;
   cs.ns = pb->ns;
   cs.nsplit = 0;  // the convolution's last arriver already summed the splits into b
@@ -954,7 +960,7 @@ int begin_loop(tdw_problem* pb, cudaStream_t st) {
   tdw_ctx* ctx = pb->ctx;
   TDW_CUDA(ctx, cudaMemsetAsync(pb->d_flags, 0, sizeof(int) * 4, st));
   TDW_CUDA(ctx, cudaMemsetAsync(pb->d_bnear, 0, sizeof(double) * 2 * (size_t)pb->ns, st));
-  init_hist_kernel<<<2 * ctx->num_sms, 256, 0, st>>>(pb->d_hist, pb->hstride, pb->pad, pb->ns,
+  init_hist_kernel<<<2 * ctx->num_sms, 256, 0, st>>>(pb->d_hist, pb->hstride, pb->hcols, pb->pad, pb->ns,
                                                     pb->nt, pb->d_phi, pb->d_perm, pb->d_uk, pb->d_qk);
   TDW_CUDA(ctx, cudaGetLastError());
   return TDW_OK;
@@ -1243,7 +1249,7 @@ int tdw_outputs(tdw_problem* pb, double* u, double* q, double* tau, double* sigm
   const size_t n = (size_t)(pb->nt - 1) * pb->ns;
   if (!pb->d_out) TDW_CUDA(ctx, cudaMalloc(&pb->d_out, sizeof(double) * 4 * n));
   double* buf = pb->d_out;
-  outputs_kernel<<<1024, 256, 0, st>>>(pb->d_hist, pb->hstride, pb->pad, pb->ns, pb->nt, pb->d,
+  outputs_kernel<<<1024, 256, 0, st>>>(pb->d_hist, pb->hcols, pb->pad, pb->ns, pb->nt, pb->d,
                                         pb->d_perm, pb->d_flags, buf, buf + n, buf + 2 * n,
                                         buf + 3 * n);
   TDW_CUDA(ctx, cudaGetLastError());

@@ -23,8 +23,10 @@
 //   [128, 136)      int2 (gmin, gmax)   lag range of the unit (history slice)
 //   [136, 140)      uint32              unit bytes
 //   [140, 144)      uint32              coef offset: 2304 (16-bit headers) or 4352 (32-bit)
-//   [256, coef)     hdr[32][32]         pair headers, row-major, sorted by length per row
-//   [coef, ...)     double2 coef[]      (V_U, V_W) entries, jagged k-major per segment
+//   [256, coef)     hdr[32][32]         pair headers, row-major, lane = column
+//   [coef, ...)     double2 coef[]      (V_U, V_W) entries, jagged k-major per segment:
+//                                       the k-th entries of the lanes with band > k,
+//                                       in lane order
 // A unit whose bands are all <= 31 lags long and whose lag range spans <= 64
 // lags (every unit of the benchmark configurations) carries 16-bit headers;
 // any other unit falls back to 32-bit headers.
@@ -33,6 +35,9 @@
 #define TDW_UNIT_COEF_OFF16 2304
 #define TDW_UNIT_COEF_OFF 4352
 #define TDW_EMPTY_UNIT 0xffffffffu
+// assembly scratch: per segment, entry count | longest band << 48
+#define TDW_SEG_LMAX_SHIFT 48
+#define TDW_SEG_COUNT_MASK ((1ull << 48) - 1)
 
 struct tdw_ctx {
   int device = 0;
@@ -131,7 +136,8 @@ struct tdw_problem {
   double jac_bound = 0.0;
   // history and step buffers
   int pad = 0, hstride = 0;
-  double2* d_hist = nullptr;       // [ns][hstride] (q, u) per element per step
+  int hcols = 0;                   // history row length: ntiles * 32 elements (zero padded)
+  double2* d_hist = nullptr;       // [hstride][hcols] (q, u) per step per element, time-major
   double* d_uk = nullptr;          // (nt-1, ns) original order
   double* d_qk = nullptr;
   bool known_loaded = false;
