@@ -520,7 +520,8 @@ static int choose_conv_schedule(tdw_problem* pb) {
   // keep the solver's SMs free (overlap) unless the bandwidth they would add to
   // the convolution is worth more than the solve time (~100 us per step)
   const double conv_est = (double)(pb->n_band * 16) / 6.0e12;
-  const bool reserve = conv_est * pb->sp_cl / ctx->num_sms < 100e-6;
+  const bool reserve = pb->conv_reserve_model >= 0 ? pb->conv_reserve_model == 1
+                                                   : conv_est * pb->sp_cl / ctx->num_sms < 100e-6;
   pb->conv_reserve = reserve;
   const int G = std::max(1, ctx->num_sms - (reserve ? pb->sp_cl : 0));
   // items = (I-block, tile split); pick the split count that balances the waves

@@ -1283,27 +1283,11 @@ int tdw_setup_cluster_solver(tdw_problem* pb) {
     maxoff = std::max(maxoff, k2);
   }
   const char* solver_env = getenv("TDW_SOLVER");
-  const bool smem_only = solver_env && std::string(solver_env) == "smem";
+  const std::string senv = solver_env ? solver_env : "";
   const char* cl_env = getenv("TDW_SOLVE_CL");
-  if (!smem_only && maxoff <= 24) {
-    // register-resident solver: one row per thread, thread count by register budget
-    const int mz = maxoff <= 8 ? 8 : (maxoff <= 16 ? 16 : 24);
-    const int T = mz == 8 ? 1024 : (mz == 16 ? 512 : 256);
-    int CL = 1;
-    while (CL < 16 && (ns + CL - 1) / CL > T) CL *= 2;
-    if (cl_env) CL = std::max(CL, std::min(16, atoi(cl_env)));
-    if ((ns + CL - 1) / CL <= T) {
-      pb->sp_reg = mz;
-      pb->sp_cl = CL;
-      pb->sp_R = (ns + CL - 1) / CL;
-      pb->sp_smem = 0;
-    }
-  }
-  // shared-memory solver: about one row per thread, more CTAs only if the slice must shrink
-  int cl0 = 1;
-  while (cl0 < 16 && (ns + cl0 - 1) / cl0 > 1024) cl0 *= 2;
-  if (cl_env) cl0 = std::max(1, std::min(16, atoi(cl_env)));
-  for (int CL = cl0; CL <= 16 && pb->sp_cl == 0; CL *= 2) {
+  const int cl_force = cl_env ? std::max(1, std::min(16, atoi(cl_env))) : 0;
+  // shared-memory solver footprint at cluster size CL (0: does not fit)
+  auto smem_need = [&](int CL) -> size_t {
     const int R = (ns + CL - 1) / CL;
     size_t worst = 0;
     for (int c = 0; c < CL; ++c) {
@@ -1314,12 +1298,58 @@ int tdw_setup_cluster_solver(tdw_problem* pb) {
       worst = std::max(worst, nnz);
     }
     const size_t smem = sizeof(double) * (4 * (size_t)R + worst) + sizeof(int) * (R + 1 + worst);
-    if (smem <= budget) {
-      pb->sp_cl = CL;
-      pb->sp_R = R;
-      pb->sp_smem = smem;
+    return smem <= budget ? smem : 0;
+  };
+  // candidates: the register-resident solver (one row per thread, thread count
+  // by register budget) at its smallest cluster, the shared-memory solver at
+  // every cluster size that fits
+  struct Cand { int reg, cl, R; size_t smem; double solve_us; };
+  std::vector<Cand> cands;
+  if (senv != "smem" && maxoff <= 24) {
+    const int mz = maxoff <= 8 ? 8 : (maxoff <= 16 ? 16 : 24);
+    const int T = mz == 8 ? 1024 : (mz == 16 ? 512 : 256);
+    int CL = 1;
+    while (CL < 16 && (ns + CL - 1) / CL > T) CL *= 2;
+    if (cl_force) CL = std::max(CL, cl_force);
+    const int R = (ns + CL - 1) / CL;
+    if (R <= T) cands.push_back({mz, CL, R, 0, 30.0 + 0.1 * R});
+  }
+  if (senv != "reg" || cands.empty())
+    for (int CL = 1; CL <= 16; CL *= 2) {
+      if (cl_force && CL != cl_force) continue;
+      const size_t sm = smem_need(CL);
+      const int R = (ns + CL - 1) / CL;
+      if (sm) cands.push_back({0, CL, R, sm, 45.0 + 0.07 * R});
+    }
+  if (cands.empty())
+    return tdw_fail(ctx, TDW_ERR_LIMIT, "lag-1 system too large for a 16-CTA cluster's shared memory");
+  // default: the register solver, else the smallest shared-memory cluster
+  int pick = 0;
+  // Convolution-dominated problems: the convolution streams at ~45 GB/s per SM
+  // (B200, measured), so SMs kept for the solver cost bandwidth.  Step-time
+  // model, per candidate: reserved SMs -> max(conv(N - CL), solve) (the solve
+  // of step alpha overlaps the convolution of alpha+1); otherwise
+  // conv(N) + solve.  Solve-time models fitted on config 2 (5120 rows).
+  const double conv_full = 16.0 * (double)pb->n_band / (45e3 * ctx->num_sms);  // us
+  pb->conv_reserve_model = -1;
+  if (!cl_force && conv_full > 2.0 * cands[0].solve_us) {
+    double best = 1e300;
+    for (size_t c = 0; c < cands.size(); ++c) {
+      const double conv_r = 16.0 * (double)pb->n_band / (45e3 * (ctx->num_sms - cands[c].cl));
+      const double t_res = std::max(conv_r, cands[c].solve_us / 0.7);  // 30% margin on the overlap
+      const double t_ser = conv_full + cands[c].solve_us;
+      const double t = std::min(t_res, t_ser);
+      if (t < best - 1e-9) {
+        best = t;
+        pick = (int)c;
+        pb->conv_reserve_model = t_res <= t_ser ? 1 : 0;
+      }
     }
   }
+  pb->sp_reg = cands[pick].reg;
+  pb->sp_cl = cands[pick].cl;
+  pb->sp_R = cands[pick].R;
+  pb->sp_smem = cands[pick].smem;
   if (pb->sp_cl == 0)
     return tdw_fail(ctx, TDW_ERR_LIMIT, "lag-1 system too large for a 16-CTA cluster's shared memory");
   const int CL = pb->sp_cl, R = pb->sp_R;

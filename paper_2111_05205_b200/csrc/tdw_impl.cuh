@@ -107,6 +107,7 @@ struct tdw_problem {
   // conv schedule: persistent CTAs over items (I-block, tile split)
   int conv_grid = 0, conv_S = 1, conv_nstages = 2;
   bool conv_reserve = false;  // convolution CTAs leave the cluster solver's SMs free
+  int conv_reserve_model = -1;  // the solver setup's step-time model decision (-1: none)
   size_t conv_stage_bytes = 0;
   unsigned* d_sched = nullptr;     // unit ids in CTA processing order (or TDW_EMPTY_UNIT)
   unsigned* d_sched_item = nullptr; // work item (I-block * S + split) of each entry

@@ -139,6 +139,26 @@ def test_header_widths_agree(monkeypatch):
     assert per_step_rel(a.u, r["u"]).max() < 1e-9
 
 
+@pytest.mark.parametrize("env", ["TDW_SOLVER=smem+TDW_SOLVE_CL=2", "TDW_SOLVER=smem+TDW_SOLVE_CL=4",
+                                 "TDW_SOLVER=smem+TDW_SOLVE_CL=16", "TDW_SOLVER=reg"])
+def test_solver_variants_agree(monkeypatch, env):
+    """Every cluster solver the step-time model can pick (register-resident, or
+    shared-memory at 2..16 CTAs; at 2 and 4 CTAs a thread owns several of the
+    2560 / 1280 rows) converges to the same densities on config 2."""
+    spec = scenarios.build_spec(2)
+    ref = marching.march(spec)
+    for kv in env.split("+"):
+        k, v = kv.split("=")
+        monkeypatch.setenv(k, v)
+    store = marching.BandStore(spec).assemble()
+    inf = store.info()
+    if "TDW_SOLVE_CL" in env:
+        assert inf["solve_cluster"] == int(env.split("TDW_SOLVE_CL=")[1])
+    h = marching.march(spec, mats=store)
+    assert h.status == ref.status and h.n_steps == ref.n_steps
+    assert per_step_rel(h.q, ref.q).max() < 1e-11
+
+
 def test_window_off_is_equivalent():
     """window=False keeps the whole history (marching.py:296-300): same result."""
     spec = _mini_spec(1, "bmbie", "neumann", nt=60)
