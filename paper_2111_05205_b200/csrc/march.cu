@@ -64,6 +64,35 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
       : "memory");
 }
 
+// L2 policies: the store streams through once per step (evict first); the
+// history window is re-read by every unit of its column tile (evict last)
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, unsigned bytes, uint64_t* bar,
+                                              uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], "
+      "%4;" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void tensor2d_g2s_hint(void* dst, const CUtensorMap* map, int c0, int c1,
+                                                  uint64_t* bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, "
+      "{%2, %3}], [%4], %5;" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+
 __device__ __forceinline__ void tensor2d_g2s(void* dst, const CUtensorMap* map, int c0, int c1,
                                              uint64_t* bar) {
   asm volatile(
@@ -84,6 +113,7 @@ struct ConvArgs {
   double* __restrict__ bpart;
   const int* __restrict__ flags;
   int hcols, pad, ns, rows_loc, ntiles, S, alpha, nstages, wbox;
+  int l2hint;            // L2 eviction-priority hints on the unit stream / history box
   unsigned stage_bytes;  // shared-memory FIFO capacity
 };
 
@@ -128,6 +158,7 @@ __global__ void __launch_bounds__(TDW_CONV_THREADS, 1)
     unsigned rs1 = 0, re1 = 0, rs2 = 0, re2 = 0, rs3 = 0, re3 = 0;
     unsigned h = 0;
     const unsigned cap = a.stage_bytes;
+    const uint64_t pol_stream = policy_evict_first(), pol_keep = policy_evict_last();
     int n = 0;  // real units issued
     for (int base = 0; base < nent; base += 32) {
       unsigned uid = TDW_EMPTY_UNIT;
@@ -174,10 +205,16 @@ __global__ void __launch_bounds__(TDW_CONV_THREADS, 1)
         const unsigned chunk = 32768u;
         for (unsigned c = lane * chunk; c < qbytes; c += 32u * chunk) {
           const unsigned len = min(chunk, qbytes - c);
-          bulk_g2s(sbase + c, a.units + qoff + c, len, &full[slot]);
+          if (a.l2hint) bulk_g2s_hint(sbase + c, a.units + qoff + c, len, &full[slot], pol_stream);
+          else bulk_g2s(sbase + c, a.units + qoff + c, len, &full[slot]);
         }
-        if (W > 0 && lane == 0)  // hist[pad+alpha-gmax .. +wbox)[t*32 .. +32] as one 2-D box
-          tensor2d_g2s(sbase + ubytes, &hmap, 2 * t * TDW_TJ, a.pad + a.alpha - gmax, &full[slot]);
+        if (W > 0 && lane == 0) {  // hist[pad+alpha-gmax .. +wbox)[t*32 .. +32] as one 2-D box
+          if (a.l2hint)
+            tensor2d_g2s_hint(sbase + ubytes, &hmap, 2 * t * TDW_TJ, a.pad + a.alpha - gmax, &full[slot],
+                              pol_keep);
+          else
+            tensor2d_g2s(sbase + ubytes, &hmap, 2 * t * TDW_TJ, a.pad + a.alpha - gmax, &full[slot]);
+        }
         h += need;
         ++n;
       }
@@ -882,6 +919,10 @@ static int make_hist_map(tdw_problem* pb, CUtensorMap* map) {
 
 static void fill_conv_args(tdw_problem* pb, ConvArgs& c) {
   c.wbox = pb->wbox;
+  {
+    const char* h = getenv("TDW_L2HINT");
+    c.l2hint = h ? atoi(h) : 1;
+  }
   c.units = pb->d_units;
   c.unit_off = pb->d_unit_off;
   c.unit = pb->d_unit;
