@@ -151,7 +151,8 @@ __device__ __forceinline__ bool pair_allowed(const int* leafc, int i, int j) {
 struct AsmArgs {
   const double* elem;
   const int* leafc;                    // packed leaf-cell coords (FMM near field) or null
-  int split_lag2;                      // 1: lag-2 entries keep the known density only
+  int split_lag2;                      // 1: lag 2..kb+1 entries keep the known density only
+  int kb;                              // time steps per convolution pass
   int ns, row_lo, rows_loc, ntiles, d, cap;
   double c, dt, K;
   uint32_t* hdr;
@@ -274,11 +275,11 @@ __global__ void __launch_bounds__(128) fill_kernel(AsmArgs a) {
         vu += w[q] * ru[q];
         vw += w[q] * rw[q];
       }
-      if (gg == TDW_NEAR_LAGS && a.split_lag2) {
-        // lag 2: keep only the coefficient of the KNOWN density of element j
-        // (q if phi_j = 1, u if phi_j = 0); the unknown one is applied by the
-        // solve of the previous step (near structure), so the convolution of
-        // step alpha+1 never waits for the solve of step alpha.
+      if (a.split_lag2 && gg >= 2 && gg <= a.kb + 1) {
+        // lags 2..kb+1: keep only the coefficient of the KNOWN density of
+        // element j (q if phi_j = 1, u if phi_j = 0); the unknown one is applied
+        // by the solves through the near structure, so the convolution pass of
+        // steps alpha..alpha+kb-1 waits only for the solve of step alpha-2.
         const double pj = a.phi[j];
         vu = pj == 1.0 ? vu : 0.0;
         vw = pj == 1.0 ? 0.0 : vw;
@@ -363,12 +364,12 @@ __global__ void unit_layout_kernel(const unsigned long long* segcount, const uin
 struct NearArgs {
   const double* elem;
   const int* leafc;
-  int split_lag2;
+  int split_lag2, kb;
   const double* phi;
   int ns, ntiles, d, cap;
   double c, dt, K;
   int* ncol;      // [TDW_NEAR_MAX][ns]
-  double* nval;   // [TDW_NEAR_MAX][ns]: coefficient of the unknown density at lag 2
+  double* nval;   // [kb][TDW_NEAR_MAX][ns]: coefficient of the unknown density at lag 2 + index
   int* acol;      // [TDW_ELL_MAX][ns]  lag-1 step matrix (pairs with V^(1))
   double* aval;   // [TDW_ELL_MAX][ns]
   double* adiag;  // [ns]
@@ -380,11 +381,12 @@ struct NearArgs {
   unsigned long long* n_evals;
 };
 
-// Rows of the lag-1 step matrix and of the lag-2 "unknown" coupling, all rows
-// (replicated on every rank).  With V^(1) = w0 U^(1), V^(2) = w0 U^(2) + w1 U^(1)
-// (U^(g) = 0 for g < arrival; zero outside the pair's band, as in the store):
-//   A_ij   = V_W^(1) phi_j - V_U^(1) (1 - phi_j)      (build_step_matrix, marching.py:279-289)
-//   N_ij   = -V_W^(2) if phi_j = 1 else V_U^(2)       (b_i += N_ij x_j^(alpha-2))
+// Rows of the lag-1 step matrix and of the "unknown" coupling at the split lags
+// g = 2..kb+1, all rows (replicated on every rank).  With
+// V^(g) = sum_kappa w^kappa U^(g-kappa) (U^(m) = 0 for m < max(1, arrival); zero
+// outside the pair's band, as in the store):
+//   A_ij     = V_W^(1) phi_j - V_U^(1) (1 - phi_j)      (build_step_matrix, marching.py:279-289)
+//   N^g_ij   = -V_W^(g) if phi_j = 1 else V_U^(g)       (b_i^alpha += N^g_ij x_j^(alpha-g))
 template <int D, bool BM>
 __global__ void __launch_bounds__(128) near_kernel(NearArgs a) {
   const int lane = threadIdx.x & 31;
@@ -396,6 +398,8 @@ __global__ void __launch_bounds__(128) near_kernel(NearArgs a) {
   const double* pi = a.elem + (size_t)i * TDW_ELEM_STRIDE;
   double ci[3] = {pi[12], pi[13], pi[14]};
   double nx[3] = {-pi[9], -pi[10], -pi[11]};
+  const int gtop = a.split_lag2 ? a.kb + 1 : 1;  // highest split lag
+  const size_t gstride = (size_t)TDW_NEAR_MAX * a.ns;
   int cnt = 0, acnt = 0;
   double diag = 0.0, offsum = 0.0;
   long long nev = 0;
@@ -408,13 +412,13 @@ __global__ void __launch_bounds__(128) near_kernel(NearArgs a) {
       load_elem(a.elem, j, ej);
       double dx = ci[0] - ej.c[0], dy = ci[1] - ej.c[1], dz = ci[2] - ej.c[2];
       double dcc = sqrt(dx * dx + dy * dy + dz * dz);
-      if (dcc - ej.rad <= (TDW_NEAR_LAGS + 1) * cdt * (1.0 + 1e-9) && pair_allowed(a.leafc, i, j)) {
+      if (dcc - ej.rad <= (gtop + 1) * cdt * (1.0 + 1e-9) && pair_allowed(a.leafc, i, j)) {
         b = pair_band(ci, ej, cdt, a.d, a.cap);
         cand = true;
       }
     }
     const bool has1 = cand && b.glo <= 1 && b.ghi >= 1;
-    const bool has2 = a.split_lag2 && cand && b.glo <= 2 && b.ghi >= 2;
+    const bool has2 = a.split_lag2 && cand && b.glo <= gtop && b.ghi >= 2;
     const unsigned m1 = __ballot_sync(FULLMASK, has1);
     const unsigned m2 = __ballot_sync(FULLMASK, has2);
     const int apos = acnt + __popc(m1 & ((1u << lane) - 1u));
@@ -422,12 +426,15 @@ __global__ void __launch_bounds__(128) near_kernel(NearArgs a) {
     if (has1 || has2) {
       PairGeom g;
       pair_geom<BM>(ci, ej.v0, ej.v1, ej.v2, ej.n, nx, g);
-      double u1 = 0.0, w1 = 0.0, u2 = 0.0, w2 = 0.0;
-      if (b.arr <= 1) { coeff_eval<D, BM>(g, 1.0 * a.c * a.dt, a.K, u1, w1); ++nev; }
-      if (b.arr <= 2) { coeff_eval<D, BM>(g, 2.0 * a.c * a.dt, a.K, u2, w2); ++nev; }
+      // U^(m), m = 1..gtop (zero before arrival)
+      double uu[TDW_KB_MAX + 2], ww[TDW_KB_MAX + 2];
+#pragma unroll
+      for (int m = 0; m < TDW_KB_MAX + 2; ++m) { uu[m] = 0.0; ww[m] = 0.0; }
+      for (int m = 1; m <= gtop; ++m)
+        if (b.arr <= m) { coeff_eval<D, BM>(g, (double)m * a.c * a.dt, a.K, uu[m], ww[m]); ++nev; }
       const double pj = a.phi[j];
       if (has1) {
-        const double v1u = w[0] * u1, v1w = w[0] * w1;
+        const double v1u = w[0] * uu[1], v1w = w[0] * ww[1];
         const double val = v1w * pj - v1u * (1.0 - pj);
         if (apos < TDW_ELL_MAX) {
           a.acol[(size_t)apos * a.ns + i] = j;
@@ -436,13 +443,16 @@ __global__ void __launch_bounds__(128) near_kernel(NearArgs a) {
         if (j == i) diag = val;
         else offsum += fabs(val);
       }
-      if (has2) {
-        double v2u = 0.0, v2w = 0.0;
-        v2u = w[0] * u2 + w[1] * u1;
-        v2w = w[0] * w2 + w[1] * w1;
-        if (pos < TDW_NEAR_MAX) {
-          a.ncol[(size_t)pos * a.ns + i] = j;
-          a.nval[(size_t)pos * a.ns + i] = pj == 1.0 ? -v2w : v2u;
+      if (has2 && pos < TDW_NEAR_MAX) {
+        a.ncol[(size_t)pos * a.ns + i] = j;
+        for (int gg = 2; gg <= gtop; ++gg) {
+          double vu = 0.0, vw = 0.0;
+          for (int k = 0; k <= D + 1 && k < gg; ++k) {
+            vu += w[k] * uu[gg - k];
+            vw += w[k] * ww[gg - k];
+          }
+          const bool in_band = gg >= b.glo && gg <= b.ghi;
+          a.nval[(gg - 2) * gstride + (size_t)pos * a.ns + i] = in_band ? (pj == 1.0 ? -vw : vu) : 0.0;
         }
       }
     }
@@ -457,7 +467,7 @@ __global__ void __launch_bounds__(128) near_kernel(NearArgs a) {
   }
   for (int p = cnt + lane; p < TDW_NEAR_MAX; p += 32) {
     a.ncol[(size_t)p * a.ns + i] = i;
-    a.nval[(size_t)p * a.ns + i] = 0.0;
+    for (int gg = 2; gg <= gtop; ++gg) a.nval[(gg - 2) * gstride + (size_t)p * a.ns + i] = 0.0;
   }
   for (int p = acnt + lane; p < TDW_ELL_MAX; p += 32) {
     a.acol[(size_t)p * a.ns + i] = i;
@@ -507,9 +517,9 @@ static int choose_conv_schedule(tdw_problem* pb) {
   // FIFO capacity: all opt-in shared memory but the kernel's static part
   const size_t cap = std::min<size_t>((size_t)maxsm - 1024, 224 * 1024) / 128 * 128;
   pb->wbox = pb->wmax;
-  if (pb->wbox > 256)
+  if (pb->wbox + pb->kb - 1 > 256)
     return tdw_fail(ctx, TDW_ERR_LIMIT, "history slice of a unit exceeds 256 lags (TMA box limit)");
-  const size_t hist_bytes = sizeof(double2) * TDW_TJ * (size_t)pb->wbox;
+  const size_t hist_bytes = sizeof(double2) * TDW_TJ * (size_t)(pb->wbox + pb->kb - 1);
   const size_t worst = (pb->max_unit_bytes + 127) / 128 * 128 + (hist_bytes + 127) / 128 * 128;
   if (worst > cap)
     return tdw_fail(ctx, TDW_ERR_LIMIT,
@@ -569,6 +579,7 @@ int tdw_assemble_impl(tdw_problem* pb) {
   a.elem = pb->d_elem;
   a.leafc = pb->d_leafc;
   a.split_lag2 = pb->split_lag2;
+  a.kb = pb->kb;
   a.ns = pb->ns;
   a.row_lo = pb->row_lo;
   a.rows_loc = pb->rows_per_rank;
@@ -665,7 +676,7 @@ int tdw_assemble_impl(tdw_problem* pb) {
   TDW_CUDA(ctx, cudaMalloc(&pb->d_aval, sizeof(double) * (size_t)TDW_ELL_MAX * pb->ns));
   TDW_CUDA(ctx, cudaMalloc(&pb->d_adiag, sizeof(double) * pb->ns));
   TDW_CUDA(ctx, cudaMalloc(&pb->d_ncol, sizeof(int) * (size_t)TDW_NEAR_MAX * pb->ns));
-  TDW_CUDA(ctx, cudaMalloc(&pb->d_nval, sizeof(double) * (size_t)TDW_NEAR_MAX * pb->ns));
+  TDW_CUDA(ctx, cudaMalloc(&pb->d_nval, sizeof(double) * (size_t)pb->kb * TDW_NEAR_MAX * pb->ns));
   int* d_ellw = nullptr;
   TDW_CUDA(ctx, cudaMalloc(&d_ellw, sizeof(int)));
   TDW_CUDA(ctx, cudaMemsetAsync(d_ellw, 0, sizeof(int), st));
@@ -673,6 +684,7 @@ int tdw_assemble_impl(tdw_problem* pb) {
   s.elem = pb->d_elem;
   s.leafc = pb->d_leafc;
   s.split_lag2 = pb->split_lag2;
+  s.kb = pb->kb;
   s.phi = pb->d_phi;
   s.ns = pb->ns;
   s.ntiles = pb->ntiles;
@@ -720,7 +732,7 @@ int tdw_assemble_impl(tdw_problem* pb) {
   pb->jac_bound = bound;
   pb->ell_w = hellw;
   if (hflags[3] == 1)
-    return tdw_fail(ctx, TDW_ERR_LIMIT, "near structure: more than the supported pairs within 2 c dt of a row");
+    return tdw_fail(ctx, TDW_ERR_LIMIT, "near structure: more than the supported pairs within (kb + 1) c dt of a row (lower TDW_KB)");
   if (!(bound < 0.9))
     return tdw_fail(ctx, TDW_ERR_SINGULAR,
                     "step matrix is not diagonally dominant (Jacobi bound " +
@@ -837,9 +849,10 @@ int tdw_assemble_impl(tdw_problem* pb) {
     TDW_CUDA(ctx, cudaMemcpy(pb->d_sched_off, soff.data(), sizeof(unsigned) * (G + 1), cudaMemcpyHostToDevice));
     pb->nsplit = S;
     cudaFree(pb->d_bpart);
-    TDW_CUDA(ctx, cudaMalloc(&pb->d_bpart, 2 * sizeof(double) * (size_t)S * pb->rows_per_rank));
-    TDW_CUDA(ctx, cudaMemset(pb->d_bpart, 0, 2 * sizeof(double) * (size_t)S * pb->rows_per_rank));
-    TDW_CUDA(ctx, cudaMalloc(&pb->d_bnear, 2 * sizeof(double) * (size_t)pb->ns));
+    // [kb][rows][S]: one pass's partials (reduced on the pass's stream before the next pass)
+    TDW_CUDA(ctx, cudaMalloc(&pb->d_bpart, pb->kb * sizeof(double) * (size_t)S * pb->rows_per_rank));
+    TDW_CUDA(ctx, cudaMemset(pb->d_bpart, 0, pb->kb * sizeof(double) * (size_t)S * pb->rows_per_rank));
+    TDW_CUDA(ctx, cudaMalloc(&pb->d_bnear, sizeof(double) * (size_t)pb->kb * (pb->kb + 1) * pb->ns));
   }
   pb->store_bytes = (int64_t)(total_bytes + sizeof(unsigned long long) * (nunit + 1) + sizeof(int2) * nunit);
   pb->assembled = true;

@@ -141,6 +141,11 @@ int tdw_problem_create_impl(tdw_ctx* ctx, const tdw_problem_desc* dsc, tdw_probl
   pb->d = dsc->d;
   pb->nt = dsc->nt;
   pb->window = dsc->window ? 1 : 0;
+  {
+    // temporal blocking: one convolution pass computes kb consecutive steps
+    const char* e = getenv("TDW_KB");
+    pb->kb = std::max(1, std::min(TDW_KB_MAX, e ? atoi(e) : 2));
+  }
   pb->c = dsc->c;
   pb->dt = dsc->dt;
   pb->K = tdw::kfactor(pb->d, pb->c, pb->dt);
@@ -300,8 +305,10 @@ int tdw_problem_create_impl(tdw_ctx* ctx, const tdw_problem_desc* dsc, tdw_probl
   TDW_TRY(cudaMalloc(&pb->d_bpart, sizeof(double) * (size_t)pb->nsplit * pb->rows_per_rank));
   TDW_TRY(cudaMemset(pb->d_bpart, 0, sizeof(double) * (size_t)pb->nsplit * pb->rows_per_rank));
   pb->bstride = (size_t)nranks * pb->rows_per_rank;
-  TDW_TRY(cudaMalloc(&pb->d_b, sizeof(double) * 2 * pb->bstride));
-  TDW_TRY(cudaMemset(pb->d_b, 0, sizeof(double) * 2 * pb->bstride));
+  // b ring: step s in slot s % (2 kb) (a pass writes kb slots while the
+  // previous pass's last step is being solved)
+  TDW_TRY(cudaMalloc(&pb->d_b, sizeof(double) * 2 * TDW_KB_MAX * pb->bstride));
+  TDW_TRY(cudaMemset(pb->d_b, 0, sizeof(double) * 2 * TDW_KB_MAX * pb->bstride));
   TDW_TRY(cudaMalloc(&pb->d_x, sizeof(double) * 2 * (size_t)ns));
   TDW_TRY(cudaMalloc(&pb->d_hist, sizeof(double2) * (size_t)pb->hcols * pb->hstride));
   TDW_TRY(cudaMalloc(&pb->d_bar, sizeof(unsigned) * 2));

@@ -126,7 +126,12 @@ struct ConvArgs {
 // ring of shared-memory stages with cp.async.bulk, completion on an mbarrier.
 // Warps 0..7 (consumers, 4 rows each) compute from shared memory only and
 // release the stage.  Row sums of a work item (I-block, tile split) go to
-// bpart[split][row] (fixed-order, deterministic).
+// bpart[step][row][split] (fixed-order, deterministic).
+// Temporal blocking: one pass computes the KB steps alpha..alpha+KB-1 from one
+// read of the store.  Step alpha+i at lag g reads time alpha+i-g, i.e. row
+// (gmax - g + i) of the unit's history box of wbox+KB-1 rows starting at time
+// alpha-gmax.  Every coefficient is read from shared memory once and used KB times.
+template <int KB>
 __global__ void __launch_bounds__(TDW_CONV_THREADS, 1)
     conv_kernel(ConvArgs a, const __grid_constant__ CUtensorMap hmap) {
   extern __shared__ __align__(128) unsigned char sm[];
@@ -182,7 +187,7 @@ __global__ void __launch_bounds__(TDW_CONV_THREADS, 1)
         const int slot = n & 3;
         const int W = gmax >= gmin ? gmax - gmin + 1 : 0;
         const int t = (int)(quid % (unsigned)a.ntiles);
-        const unsigned hbytes = W > 0 ? (unsigned)(TDW_TJ * a.wbox * 16) : 0u;
+        const unsigned hbytes = W > 0 ? (unsigned)(TDW_TJ * (a.wbox + KB - 1) * 16) : 0u;
         const unsigned ubytes = (qbytes + 127u) & ~127u;
         const unsigned need = ubytes + ((hbytes + 127u) & ~127u);
         if (h + need > cap) h = 0;
@@ -222,10 +227,13 @@ __global__ void __launch_bounds__(TDW_CONV_THREADS, 1)
     return;
   }
   // ---------------- consumers ----------------
-  double acc[TDW_ROWS_PER_WARP];
+  double acc[TDW_ROWS_PER_WARP][KB];
 #pragma unroll
-  for (int r = 0; r < TDW_ROWS_PER_WARP; ++r) acc[r] = 0.0;
+  for (int r = 0; r < TDW_ROWS_PER_WARP; ++r)
+#pragma unroll
+    for (int i = 0; i < KB; ++i) acc[r][i] = 0.0;
   const int S = a.S;
+  const size_t step_stride = (size_t)a.rows_loc * S;
   int n = 0;
   for (int base = 0; base < nent; base += 32) {
     const unsigned my_uid = base + lane < nent ? a.sched[u0 + base + lane] : TDW_EMPTY_UNIT;
@@ -250,13 +258,13 @@ __global__ void __launch_bounds__(TDW_CONV_THREADS, 1)
       // the warp's rows are interleaved (independent FMA chains); the k loop is
       // unrolled and predicated.  Lane = column: the k-th entries of a segment
       // are those of the lanes with band > k, packed in lane order; the history
-      // box is [lag][32 columns], so a warp reads one 512-byte row per k.
+      // box is [time][32 columns], so a warp reads one 512-byte row per (k, step).
       const unsigned lt = (1u << lane) - 1u;
       int len[TDW_ROWS_PER_WARP], lmax = 0;
       const double2* cp[TDW_ROWS_PER_WARP];
       const double2* hp[TDW_ROWS_PER_WARP];
       int off[TDW_ROWS_PER_WARP];
-      double s0[TDW_ROWS_PER_WARP], s1[TDW_ROWS_PER_WARP];
+      double s0[TDW_ROWS_PER_WARP][KB], s1[TDW_ROWS_PER_WARP][KB];
 #pragma unroll
       for (int r = 0; r < TDW_ROWS_PER_WARP; ++r) {
         const int row = warp * TDW_ROWS_PER_WARP + r;
@@ -266,8 +274,8 @@ __global__ void __launch_bounds__(TDW_CONV_THREADS, 1)
         cp[r] = coef + rel[row];
         hp[r] = hs + hrel * TDW_TJ + jl;
         off[r] = 0;
-        s0[r] = 0.0;
-        s1[r] = 0.0;
+#pragma unroll
+        for (int i = 0; i < KB; ++i) { s0[r][i] = 0.0; s1[r][i] = 0.0; }
       }
       lmax = __reduce_max_sync(FULLMASK, lmax);
       for (int k0 = 0; k0 < lmax; k0 += 4) {
@@ -280,16 +288,21 @@ __global__ void __launch_bounds__(TDW_CONV_THREADS, 1)
             const unsigned m = __ballot_sync(FULLMASK, on);
             if (on) {
               const double2 cv = cp[r][off[r] + __popc(m & lt)];
-              const double2 hv = hp[r][-k * TDW_TJ];
-              s0[r] = fma(cv.x, hv.x, s0[r]);
-              s1[r] = fma(cv.y, hv.y, s1[r]);
+#pragma unroll
+              for (int i = 0; i < KB; ++i) {
+                const double2 hv = hp[r][(i - k) * TDW_TJ];
+                s0[r][i] = fma(cv.x, hv.x, s0[r][i]);
+                s1[r][i] = fma(cv.y, hv.y, s1[r][i]);
+              }
             }
             off[r] += __popc(m);
           }
         }
       }
 #pragma unroll
-      for (int r = 0; r < TDW_ROWS_PER_WARP; ++r) acc[r] += s0[r] - s1[r];
+      for (int r = 0; r < TDW_ROWS_PER_WARP; ++r)
+#pragma unroll
+        for (int i = 0; i < KB; ++i) acc[r][i] += s0[r][i] - s1[r][i];
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[stage]);
       ++n;
@@ -298,12 +311,15 @@ __global__ void __launch_bounds__(TDW_CONV_THREADS, 1)
       const int iblk = (int)(item / (unsigned)S), sp = (int)(item % (unsigned)S);
 #pragma unroll
       for (int r = 0; r < TDW_ROWS_PER_WARP; ++r) {
-        double v = acc[r];
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULLMASK, v, o);
-        if (lane == 0)  // row-major partials: a row's S partials are contiguous
-          a.bpart[(size_t)(iblk * TDW_TI + warp * TDW_ROWS_PER_WARP + r) * S + sp] = v;
-        acc[r] = 0.0;
+        for (int i = 0; i < KB; ++i) {
+          double v = acc[r][i];
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULLMASK, v, o);
+          if (lane == 0)  // row-major partials: a row's S partials are contiguous
+            a.bpart[i * step_stride + (size_t)(iblk * TDW_TI + warp * TDW_ROWS_PER_WARP + r) * S + sp] = v;
+          acc[r][i] = 0.0;
+        }
       }
     }
     }
@@ -324,11 +340,16 @@ __device__ __forceinline__ double sum_parts(const double* __restrict__ p, int n)
 }
 
 // sum of the split partials of the own rows into b (multi-GPU path, before the all-gather)
+// (blockIdx.y = step alpha + y of the pass; b ring slot (alpha + y) % ring)
 __global__ void reduce_parts_kernel(const double* __restrict__ bpart, int nsplit, int rows_loc,
-                                    double* __restrict__ bown, const int* flags) {
+                                    double* __restrict__ b, size_t bstride, int b_off, int ring,
+                                    int alpha, const int* flags) {
   if (flags[0] != 0) return;
+  const int i = blockIdx.y;
+  double* bown = b + (size_t)((alpha + i) % ring) * bstride + b_off;
+  const double* bp = bpart + (size_t)i * rows_loc * nsplit;
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < rows_loc; r += gridDim.x * blockDim.x)
-    bown[r] = sum_parts(bpart + (size_t)r * nsplit, nsplit);
+    bown[r] = sum_parts(bp + (size_t)r * nsplit, nsplit);
 }
 
 __device__ __forceinline__ double block_reduce_sum(double v, double* sh) {
@@ -386,15 +407,15 @@ __device__ __forceinline__ void block_reduce2_max(double& a, double& b, double* 
 struct ClusterSolveArgs {
   const double* bpart;                      // far partials of this step (nsplit > 0)
   double* b;                                // all-gathered far rhs (nsplit == 0)
-  const double* bnear_in;                   // lag-2 unknown term of this step (from the previous solve)
-  double* bnear_out;                        // same for the next step
+  double* bnear;                            // [kb][kb+1][ns] near terms (see tdw_problem::d_bnear)
+  int kb;                                   // split lags 2..kb+1
   const int* __restrict__ sp_rowptr;        // [CL][R+1], relative to the CTA's slice
   const long long* __restrict__ sp_nnzoff;  // [CL+1]
   const int* __restrict__ sp_col;           // packed (owner << 24) | local
   const double* __restrict__ sp_val;
   const double* __restrict__ diag;          // [ns]
   const int* __restrict__ ncol;             // [near_w][ns] packed (owner << 24) | local
-  const double* __restrict__ nval;          // [near_w][ns]
+  const double* __restrict__ nval;          // [kb][TDW_NEAR_MAX][ns] (lag 2 + index)
   const double* __restrict__ phi;
   const int* __restrict__ perm;
   const double* __restrict__ uk;
@@ -421,6 +442,51 @@ __device__ __forceinline__ double fetch_x(int c, const double* x, int cr,
   const int owner = c >> 24, loc = c & 0xffffff;
   return owner == cr ? x[loc] : *cl.map_shared_rank(x + loc, owner);
 }
+
+// near terms of step alpha: sum over the split lags g = 2..kb+1 (fixed order) of
+// N^g x^(alpha-g), each produced by solve(alpha-g+1) into ring slot alpha % (kb+1)
+__device__ __forceinline__ double near_in(const ClusterSolveArgs& a, int gi) {
+  const int ring = a.kb + 1;
+  double s = 0.0;
+  for (int g = 0; g < a.kb; ++g) s += a.bnear[((size_t)g * ring + a.alpha % ring) * a.ns + gi];
+  return s;
+}
+
+// N^g x^(alpha-1) for the steps alpha-1+g, g = 2..kb+1 (x of this solve)
+template <int CH>
+__device__ __forceinline__ void near_out(const ClusterSolveArgs& a, int gi, const double* xf, int cr,
+                                         cooperative_groups::cluster_group& cl) {
+  double acc[TDW_KB_MAX];
+#pragma unroll
+  for (int g = 0; g < TDW_KB_MAX; ++g) acc[g] = 0.0;
+  const size_t gstride = (size_t)TDW_NEAR_MAX * a.ns;
+  for (int k0 = 0; k0 < a.near_w; k0 += CH) {
+    int cc[CH];
+    double xv[CH];
+#pragma unroll
+    for (int q = 0; q < CH; ++q) {
+      const bool on = k0 + q < a.near_w;
+      cc[q] = on ? __ldg(a.ncol + (size_t)(k0 + q) * a.ns + gi) : (cr << 24);
+    }
+#pragma unroll
+    for (int q = 0; q < CH; ++q) xv[q] = fetch_x(cc[q], xf, cr, cl);
+#pragma unroll
+    for (int g = 0; g < TDW_KB_MAX; ++g) {
+      if (g >= a.kb) break;
+#pragma unroll
+      for (int q = 0; q < CH; ++q) {
+        const bool on = k0 + q < a.near_w;
+        const double v = on ? __ldg(a.nval + g * gstride + (size_t)(k0 + q) * a.ns + gi) : 0.0;
+        acc[g] = fma(v, xv[q], acc[g]);
+      }
+    }
+  }
+  const int ring = a.kb + 1;
+#pragma unroll
+  for (int g = 0; g < TDW_KB_MAX; ++g)
+    if (g < a.kb) a.bnear[((size_t)g * ring + (a.alpha + 1 + g) % ring) * a.ns + gi] = acc[g];
+}
+
 
 // sum_p val[p] x[col[p]] over a CSR row held in shared memory, loads batched by 4
 __device__ __forceinline__ double row_dot(int p0, int p1, const int* col, const double* val,
@@ -491,7 +557,7 @@ __global__ void __launch_bounds__(1024, 1) solve_cluster_kernel(ClusterSolveArgs
     } else {
       bi = __ldcg(a.b + gi);
     }
-    bi += a.bnear_in[gi];
+    bi += near_in(a, gi);
     bs[i] = bi;
     dg[i] = a.diag[gi];
     xs[i] = bi / dg[i];
@@ -558,26 +624,8 @@ __global__ void __launch_bounds__(1024, 1) solve_cluster_kernel(ClusterSolveArgs
   trace_mark(tr, 4);
   cl.sync();
   trace_mark(tr, 5);
-  // lag-2 term of the unknown density for the next step (x still in shared memory)
-  for (int i = tid; i < nr; i += nth) {
-    const int gi = r0 + i;
-    double acc = 0.0;
-    for (int k0 = 0; k0 < a.near_w; k0 += 8) {
-      int c[8];
-      double v[8], xv[8];
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const bool on = k0 + q < a.near_w;
-        c[q] = on ? __ldg(a.ncol + (size_t)(k0 + q) * a.ns + gi) : (cr << 24);
-        v[q] = on ? __ldg(a.nval + (size_t)(k0 + q) * a.ns + gi) : 0.0;
-      }
-#pragma unroll
-      for (int q = 0; q < 8; ++q) xv[q] = fetch_x(c[q], xf, cr, cl);
-#pragma unroll
-      for (int q = 0; q < 8; ++q) acc += v[q] * xv[q];
-    }
-    a.bnear_out[gi] = acc;
-  }
+  // split-lag terms of the unknown density for the next steps (x still in shared memory)
+  for (int i = tid; i < nr; i += nth) near_out<8>(a, r0 + i, xf, cr, cl);
   double RR = 0.0, BB = 0.0, XM = 0.0;
   if (tid < 32) {
     if (tid < CL) {
@@ -671,7 +719,7 @@ __global__ void __launch_bounds__(reg_threads<MAXNZ>(), 1) solve_reg_kernel(Clus
     }
     if (a.nsplit > 0) bi = sum_parts(a.bpart + (size_t)gi * a.nsplit, a.nsplit);
     else bi = __ldcg(a.b + gi);
-    bi += a.bnear_in[gi];
+    bi += near_in(a, gi);
     di = a.diag[gi];
     invd = 1.0 / di;
     xs[0][tid] = bi * invd;
@@ -760,25 +808,8 @@ __global__ void __launch_bounds__(reg_threads<MAXNZ>(), 1) solve_reg_kernel(Clus
   trace_mark(tr, 4);
   cl.sync();
   trace_mark(tr, 5);
-  // lag-2 term of the unknown density for the next step (x still in shared memory)
-  if (own) {
-    double acc = 0.0;
-    for (int k0 = 0; k0 < a.near_w; k0 += 16) {
-      int cc[16];
-      double vv[16], xv[16];
-#pragma unroll
-      for (int q = 0; q < 16; ++q) {
-        const bool on = k0 + q < a.near_w;
-        cc[q] = on ? __ldg(a.ncol + (size_t)(k0 + q) * a.ns + gi) : (cr << 24);
-        vv[q] = on ? __ldg(a.nval + (size_t)(k0 + q) * a.ns + gi) : 0.0;
-      }
-#pragma unroll
-      for (int q = 0; q < 16; ++q) xv[q] = fetch_x(cc[q], xf, cr, cl);
-#pragma unroll
-      for (int q = 0; q < 16; ++q) acc = fma(vv[q], xv[q], acc);
-    }
-    a.bnear_out[gi] = acc;
-  }
+  // split-lag terms of the unknown density for the next steps (x still in shared memory)
+  if (own) near_out<16>(a, gi, xf, cr, cl);
   double RR = 0.0, BB = 0.0, XM = 0.0;
   if (tid < 32) {
     if (tid < CL) {
@@ -895,7 +926,7 @@ typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_
                                     CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
 // 2-D view of the history: rows = steps, inner = 2*hcols doubles; box =
-// [wbox steps][64 doubles = 32 elements x (q, u)].
+// [wbox + kb - 1 steps][64 doubles = 32 elements x (q, u)].
 static int make_hist_map(tdw_problem* pb, CUtensorMap* map) {
   static PFN_encodeTiled enc = nullptr;
   if (!enc) {
@@ -908,13 +939,32 @@ static int make_hist_map(tdw_problem* pb, CUtensorMap* map) {
   }
   cuuint64_t dims[2] = {(cuuint64_t)2 * pb->hcols, (cuuint64_t)pb->hstride};
   cuuint64_t strides[1] = {(cuuint64_t)pb->hcols * 16};
-  cuuint32_t box[2] = {(cuuint32_t)(2 * TDW_TJ), (cuuint32_t)pb->wbox};
+  cuuint32_t box[2] = {(cuuint32_t)(2 * TDW_TJ), (cuuint32_t)(pb->wbox + pb->kb - 1)};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, pb->d_hist, dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return tdw_fail(pb->ctx, TDW_ERR_CUDA, "cuTensorMapEncodeTiled failed");
   return TDW_OK;
+}
+
+// conv_kernel<KB> dispatch on the problem's block size
+static cudaError_t conv_set_smem(int kb, int smem) {
+  switch (kb) {
+    case 1: return cudaFuncSetAttribute(conv_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    case 2: return cudaFuncSetAttribute(conv_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    case 3: return cudaFuncSetAttribute(conv_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    default: return cudaFuncSetAttribute(conv_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  }
+}
+static void conv_launch(int kb, dim3 grid, size_t smem, cudaStream_t s, const ConvArgs& c,
+                        const CUtensorMap& hmap) {
+  switch (kb) {
+    case 1: conv_kernel<1><<<grid, TDW_CONV_THREADS, smem, s>>>(c, hmap); break;
+    case 2: conv_kernel<2><<<grid, TDW_CONV_THREADS, smem, s>>>(c, hmap); break;
+    case 3: conv_kernel<3><<<grid, TDW_CONV_THREADS, smem, s>>>(c, hmap); break;
+    default: conv_kernel<4><<<grid, TDW_CONV_THREADS, smem, s>>>(c, hmap); break;
+  }
 }
 
 static void fill_conv_args(tdw_problem* pb, ConvArgs& c) {
@@ -961,8 +1011,7 @@ int make_plan(tdw_problem* pb, LoopPlan& L, double threshold, bool want_rhs) {
     if (rc) return rc;
   }
   L.smem = pb->conv_stage_bytes;
-  TDW_CUDA(ctx, cudaFuncSetAttribute(conv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)L.smem));
+  TDW_CUDA(ctx, conv_set_smem(pb->kb, (int)L.smem));
   L.cgrid = dim3(pb->conv_grid);
   L.multi = ctx->comm != nullptr;
   ClusterSolveArgs& cs = L.cs;
@@ -1000,29 +1049,28 @@ int make_plan(tdw_problem* pb, LoopPlan& L, double threshold, bool want_rhs) {
 int begin_loop(tdw_problem* pb, cudaStream_t st) {
   tdw_ctx* ctx = pb->ctx;
   TDW_CUDA(ctx, cudaMemsetAsync(pb->d_flags, 0, sizeof(int) * 4, st));
-  TDW_CUDA(ctx, cudaMemsetAsync(pb->d_bnear, 0, sizeof(double) * 2 * (size_t)pb->ns, st));
+  TDW_CUDA(ctx, cudaMemsetAsync(pb->d_bnear, 0, sizeof(double) * pb->kb * (pb->kb + 1) * (size_t)pb->ns, st));
   init_hist_kernel<<<2 * ctx->num_sms, 256, 0, st>>>(pb->d_hist, pb->hstride, pb->hcols, pb->pad, pb->ns,
                                                     pb->nt, pb->d_phi, pb->d_perm, pb->d_uk, pb->d_qk);
   TDW_CUDA(ctx, cudaGetLastError());
   return TDW_OK;
 }
 
-int launch_conv(tdw_problem* pb, LoopPlan& L, int alpha, cudaStream_t s) {
-  const size_t nb = (size_t)pb->nsplit * pb->rows_per_rank;
+// one convolution pass: steps alpha .. alpha + nsteps - 1 (nsteps <= kb)
+int launch_conv(tdw_problem* pb, LoopPlan& L, int alpha, int nsteps, cudaStream_t s) {
   L.c.alpha = alpha;
-  L.c.bpart = pb->d_bpart + (alpha & 1) * nb;
-  conv_kernel<<<L.cgrid, TDW_CONV_THREADS, L.smem, s>>>(L.c, L.hmap);
-  // fixed-order sum of the split partials into this step's b (own rows), on the
+  L.c.bpart = pb->d_bpart;
+  conv_launch(pb->kb, L.cgrid, L.smem, s, L.c, L.hmap);
+  // fixed-order sum of the split partials into the steps' b (own rows), on the
   // convolution's stream: off the solve's critical path
-  reduce_parts_kernel<<<(pb->rows_per_rank + 127) / 128, 128, 0, s>>>(
-      L.c.bpart, pb->nsplit, pb->rows_per_rank, pb->d_b + (alpha & 1) * pb->bstride + pb->b_off,
+  reduce_parts_kernel<<<dim3((pb->rows_per_rank + 127) / 128, nsteps), 128, 0, s>>>(
+      L.c.bpart, pb->nsplit, pb->rows_per_rank, pb->d_b, pb->bstride, pb->b_off, 2 * pb->kb, alpha,
       pb->d_flags);
   TDW_CUDA(pb->ctx, cudaGetLastError());
   return TDW_OK;
 }
 
 int launch_solve(tdw_problem* pb, LoopPlan& L, int alpha, cudaStream_t s) {
-  const size_t nb = (size_t)pb->nsplit * pb->rows_per_rank;
   cudaLaunchAttribute cattr[1];
   cattr[0].id = cudaLaunchAttributeClusterDimension;
   cattr[0].val.clusterDim.x = pb->sp_cl;
@@ -1036,10 +1084,10 @@ int launch_solve(tdw_problem* pb, LoopPlan& L, int alpha, cudaStream_t s) {
   ccfg.attrs = cattr;
   ccfg.numAttrs = 1;
   L.cs.alpha = alpha;
-  L.cs.bpart = pb->d_bpart + (alpha & 1) * nb;
-  L.cs.b = pb->d_b + (alpha & 1) * pb->bstride;
-  L.cs.bnear_in = pb->d_bnear + (alpha & 1) * (size_t)pb->ns;
-  L.cs.bnear_out = pb->d_bnear + ((alpha + 1) & 1) * (size_t)pb->ns;
+  L.cs.bpart = pb->d_bpart;
+  L.cs.b = pb->d_b + (size_t)(alpha % (2 * pb->kb)) * pb->bstride;
+  L.cs.bnear = pb->d_bnear;
+  L.cs.kb = pb->kb;
   if (pb->sp_reg > 0) {
     ccfg.dynamicSmemBytes = 0;
     if (pb->sp_reg == 8) TDW_CUDA(pb->ctx, cudaLaunchKernelEx(&ccfg, solve_reg_kernel<8>, L.cs));
@@ -1051,12 +1099,15 @@ int launch_solve(tdw_problem* pb, LoopPlan& L, int alpha, cudaStream_t s) {
   return TDW_OK;
 }
 
-// Enqueue one complete time loop.  Two streams: the far convolution F(alpha)
-// runs on the side stream as soon as the solve of step alpha-2 has finalized
-// the history it reads (lags >= 3; lag 1 = known data written up front; lag 2
-// = known component only), so F(alpha+1) overlaps the solve of step alpha.
-//   F(alpha)      waits solve(alpha-2)            writes bpart[alpha & 1]
-//   solve(alpha)  waits F(alpha), solve(alpha-1)  reads bpart[alpha & 1], bnear[alpha & 1]
+// Enqueue one complete time loop.  Two streams: the convolution pass P(alpha)
+// of steps alpha..alpha+kb-1 runs on the side stream as soon as the solve of
+// step alpha-2 has finalized the history it reads (times <= alpha-3: full
+// coefficients at lags >= kb+2, known-only ones at lags 2..kb+1 whose unknown
+// part the solves add through the near structure; lag 1 = known data written
+// up front), so P(alpha) overlaps solve(alpha-1) and the solves alpha..alpha+kb-1
+// follow it; per pass the critical path is P + (kb-1) solves.
+//   P(alpha)      waits solve(alpha-2)              writes b[(alpha+i) % 2kb]
+//   solve(s)      waits P(pass of s), solve(s-1)    reads b[s % 2kb], bnear[.][s % (kb+1)]
 // Also used under stream capture (one CUDA graph per loop configuration).
 int enqueue_loop(tdw_problem* pb, LoopPlan& L, cudaEvent_t* ev_conv) {
   tdw_ctx* ctx = pb->ctx;
@@ -1068,27 +1119,34 @@ int enqueue_loop(tdw_problem* pb, LoopPlan& L, cudaEvent_t* ev_conv) {
   cudaEvent_t* evF = pb->ev_conv.data();   // F(alpha) done
   TDW_CUDA(ctx, cudaEventRecord(pb->ev_fork, st));
   TDW_CUDA(ctx, cudaStreamWaitEvent(sc, pb->ev_fork, 0));
-  for (int alpha = 1; alpha < nt; ++alpha) {
-    // far convolution of step alpha on the side stream
+  const int KB = pb->kb;
+  int last_alpha = 1;
+  for (int alpha = 1; alpha < nt; alpha += KB) {
+    const int nb = std::min(KB, nt - alpha);
+    // convolution pass of steps alpha..alpha+nb-1 on the side stream
     if (alpha >= 3) TDW_CUDA(ctx, cudaStreamWaitEvent(sc, evS[alpha - 2], 0));
-    if (ev_conv) TDW_CUDA(ctx, cudaEventRecordWithFlags(ev_conv[2 * (alpha - 1)], sc, cudaEventRecordExternal));
-    if ((rc = launch_conv(pb, L, alpha, sc))) return rc;
-    if (ev_conv) TDW_CUDA(ctx, cudaEventRecordWithFlags(ev_conv[2 * (alpha - 1) + 1], sc, cudaEventRecordExternal));
+    const int pass = (alpha - 1) / KB;
+    if (ev_conv) TDW_CUDA(ctx, cudaEventRecordWithFlags(ev_conv[2 * pass], sc, cudaEventRecordExternal));
+    if ((rc = launch_conv(pb, L, alpha, nb, sc))) return rc;
+    if (ev_conv) TDW_CUDA(ctx, cudaEventRecordWithFlags(ev_conv[2 * pass + 1], sc, cudaEventRecordExternal));
     TDW_CUDA(ctx, cudaEventRecord(evF[alpha], sc));
-    // solve of step alpha on the main stream
+    last_alpha = alpha;
+    // solves of the pass's steps on the main stream
     TDW_CUDA(ctx, cudaStreamWaitEvent(st, evF[alpha], 0));
-    if (L.multi) {
-      double* bb = pb->d_b + (alpha & 1) * pb->bstride;
-      ncclResult_t nr = ncclAllGather(bb + pb->b_off, bb, (size_t)pb->rows_per_rank, ncclDouble,
-                                      ctx->comm, st);
-      if (nr != ncclSuccess)
-        return tdw_fail(ctx, TDW_ERR_NCCL, std::string("ncclAllGather: ") + ncclGetErrorString(nr));
+    for (int s = alpha; s < alpha + nb; ++s) {
+      if (L.multi) {
+        double* bb = pb->d_b + (size_t)(s % (2 * KB)) * pb->bstride;
+        ncclResult_t nr = ncclAllGather(bb + pb->b_off, bb, (size_t)pb->rows_per_rank, ncclDouble,
+                                        ctx->comm, st);
+        if (nr != ncclSuccess)
+          return tdw_fail(ctx, TDW_ERR_NCCL, std::string("ncclAllGather: ") + ncclGetErrorString(nr));
+      }
+      if ((rc = launch_solve(pb, L, s, st))) return rc;
+      TDW_CUDA(ctx, cudaEventRecord(evS[s], st));
     }
-    if ((rc = launch_solve(pb, L, alpha, st))) return rc;
-    TDW_CUDA(ctx, cudaEventRecord(evS[alpha], st));
   }
   // join the side stream
-  TDW_CUDA(ctx, cudaStreamWaitEvent(st, evF[nt - 1], 0));
+  TDW_CUDA(ctx, cudaStreamWaitEvent(st, evF[last_alpha], 0));
   TDW_CUDA(ctx, cudaGetLastError());
   return TDW_OK;
 }
@@ -1182,7 +1240,8 @@ int tdw_march_loop(tdw_problem* pb, double threshold, bool want_rhs, bool time_k
     cudaEventElapsedTime(&ms, ev0, ev1);
     timing->total_ms += ms;
     timing->steps += nsteps;
-    for (int k = 0; k < (time_kernels ? nsteps : 0); ++k) {
+    const int npass = (nsteps + pb->kb - 1) / pb->kb;
+    for (int k = 0; k < (time_kernels ? npass : 0); ++k) {
       float a = 0.f;
       if (cudaEventElapsedTime(&a, evc[2 * k], evc[2 * k + 1]) == cudaSuccess) {
         timing->conv_ms += a;
@@ -1223,22 +1282,26 @@ int tdw_march_emulated_impl(tdw_problem** pbs, int n, double threshold) {
     if (rc) return rc;
   }
   const int nt = pbs[0]->nt;
+  const int KB = pbs[0]->kb;
   const size_t rpr = (size_t)pbs[0]->rows_per_rank;
-  for (int alpha = 1; alpha < nt; ++alpha) {
+  for (int alpha = 1; alpha < nt; alpha += KB) {
+    const int nb = std::min(KB, nt - alpha);
     for (int r = 0; r < n; ++r) {
-      int rc = launch_conv(pbs[r], L[r], alpha, st);
+      int rc = launch_conv(pbs[r], L[r], alpha, nb, st);
       if (rc) return rc;
     }
-    const size_t par = (size_t)(alpha & 1);
-    for (int r = 0; r < n; ++r)
-      for (int q = 0; q < n; ++q)
-        if (q != r)
-          TDW_CUDA(ctx, cudaMemcpyAsync(pbs[q]->d_b + par * pbs[q]->bstride + pbs[r]->b_off,
-                                        pbs[r]->d_b + par * pbs[r]->bstride + pbs[r]->b_off,
-                                        sizeof(double) * rpr, cudaMemcpyDeviceToDevice, st));
-    for (int r = 0; r < n; ++r) {
-      int rc = launch_solve(pbs[r], L[r], alpha, st);
-      if (rc) return rc;
+    for (int s = alpha; s < alpha + nb; ++s) {
+      const size_t slot = (size_t)(s % (2 * KB));
+      for (int r = 0; r < n; ++r)
+        for (int q = 0; q < n; ++q)
+          if (q != r)
+            TDW_CUDA(ctx, cudaMemcpyAsync(pbs[q]->d_b + slot * pbs[q]->bstride + pbs[r]->b_off,
+                                          pbs[r]->d_b + slot * pbs[r]->bstride + pbs[r]->b_off,
+                                          sizeof(double) * rpr, cudaMemcpyDeviceToDevice, st));
+      for (int r = 0; r < n; ++r) {
+        int rc = launch_solve(pbs[r], L[r], s, st);
+        if (rc) return rc;
+      }
     }
   }
   TDW_CUDA(ctx, cudaStreamSynchronize(st));
@@ -1257,22 +1320,22 @@ int tdw_time_conv_impl(tdw_problem* pb, int n, float* ms_out) {
   cudaStream_t st = ctx->stream;
   ConvArgs c{};
   fill_conv_args(pb, c);
-  c.alpha = pb->nt - 1;
+  c.alpha = std::max(1, pb->nt - pb->kb);
   CUtensorMap hmap;
   {
     int rc = make_hist_map(pb, &hmap);
     if (rc) return rc;
   }
   const size_t smem = pb->conv_stage_bytes;
-  TDW_CUDA(ctx, cudaFuncSetAttribute(conv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  TDW_CUDA(ctx, conv_set_smem(pb->kb, (int)smem));
   TDW_CUDA(ctx, cudaMemsetAsync(pb->d_flags, 0, sizeof(int) * 4, st));
   cudaEvent_t e0, e1;
   TDW_CUDA(ctx, cudaEventCreate(&e0));
   TDW_CUDA(ctx, cudaEventCreate(&e1));
   dim3 grid(pb->conv_grid);
-  conv_kernel<<<grid, TDW_CONV_THREADS, smem, st>>>(c, hmap);  // warm-up
+  conv_launch(pb->kb, grid, smem, st, c, hmap);  // warm-up
   TDW_CUDA(ctx, cudaEventRecord(e0, st));
-  for (int k = 0; k < n; ++k) conv_kernel<<<grid, TDW_CONV_THREADS, smem, st>>>(c, hmap);
+  for (int k = 0; k < n; ++k) conv_launch(pb->kb, grid, smem, st, c, hmap);
   TDW_CUDA(ctx, cudaEventRecord(e1, st));
   TDW_CUDA(ctx, cudaEventSynchronize(e1));
   TDW_CUDA(ctx, cudaGetLastError());
@@ -1367,18 +1430,19 @@ int tdw_setup_cluster_solver(tdw_problem* pb) {
   // default: the register solver, else the smallest shared-memory cluster
   int pick = 0;
   // Convolution-dominated problems: the convolution streams at ~45 GB/s per SM
-  // (B200, measured), so SMs kept for the solver cost bandwidth.  Step-time
-  // model, per candidate: reserved SMs -> max(conv(N - CL), solve) (the solve
-  // of step alpha overlaps the convolution of alpha+1); otherwise
-  // conv(N) + solve.  Solve-time models fitted on config 2 (5120 rows).
+  // (B200, measured), so SMs kept for the solver cost bandwidth.  Pass-time
+  // model (kb steps), per candidate: reserved SMs -> max(conv(N - CL), solve)
+  // + (kb - 1) solve (the pass overlaps one solve, the other kb - 1 follow it);
+  // otherwise conv(N) + kb solve.  Solve-time models fitted on config 2.
   const double conv_full = 16.0 * (double)pb->n_band / (45e3 * ctx->num_sms);  // us
   pb->conv_reserve_model = -1;
   if (!cl_force && conv_full > 2.0 * cands[0].solve_us) {
     double best = 1e300;
     for (size_t c = 0; c < cands.size(); ++c) {
       const double conv_r = 16.0 * (double)pb->n_band / (45e3 * (ctx->num_sms - cands[c].cl));
-      const double t_res = std::max(conv_r, cands[c].solve_us / 0.7);  // 30% margin on the overlap
-      const double t_ser = conv_full + cands[c].solve_us;
+      const double sv = cands[c].solve_us;
+      const double t_res = std::max(conv_r, sv / 0.7) + (pb->kb - 1) * sv;  // 30% margin on the overlap
+      const double t_ser = conv_full + pb->kb * sv;
       const double t = std::min(t_res, t_ser);
       if (t < best - 1e-9) {
         best = t;
@@ -1457,7 +1521,7 @@ int make_plan_fmm(tdw_problem* pb, void** out, double threshold, bool want_rhs) 
 void free_plan_fmm(void* plan) { delete (LoopPlan*)plan; }
 int begin_loop_fmm(tdw_problem* pb, cudaStream_t st) { return begin_loop(pb, st); }
 int launch_conv_fmm(tdw_problem* pb, void* plan, int alpha, cudaStream_t s) {
-  return launch_conv(pb, *(LoopPlan*)plan, alpha, s);
+  return launch_conv(pb, *(LoopPlan*)plan, alpha, 1, s);
 }
 int launch_solve_fmm(tdw_problem* pb, void* plan, int alpha, cudaStream_t s) {
   return launch_solve(pb, *(LoopPlan*)plan, alpha, s);

@@ -15,8 +15,8 @@
 #define TDW_ROWS_PER_WARP 2
 #define TDW_CONV_WARPS (TDW_TI / TDW_ROWS_PER_WARP)
 #define TDW_ELL_MAX 64   // max nnz per row of the lag-1 step matrix
-#define TDW_NEAR_LAGS 2  // the unknown density enters the store's lag-2 entries via the solve
-#define TDW_NEAR_MAX 128 // max pairs per row with a band starting at lag <= 2
+#define TDW_KB_MAX 4     // time steps per convolution pass (temporal blocking)
+#define TDW_NEAR_MAX 192 // max pairs per row in the near structure (bands reaching lags 2..kb+1)
 #define TDW_ELEM_STRIDE 16  // doubles per element record: v0 v1 v2 n c rad
 // Unit layout (one (I-block, J-tile) unit = one contiguous byte range of the store):
 //   [0, 128)        uint32 seg_rel[32]  entry offset of row r's segment in the unit
@@ -93,7 +93,8 @@ struct tdw_problem {
   double* d_phi = nullptr;   // internal order
   // FMM near-field mode: pair filter (adjacent leaf cells), no lag-2 split
   int* d_leafc = nullptr;    // packed leaf-cell coords per element (internal order) or null
-  int split_lag2 = 1;
+  int split_lag2 = 1;        // lags 2..kb+1 of the store keep the known density only
+  int kb = 1;                // time steps per convolution pass (1..TDW_KB_MAX)
   bool skip_empty_units = false;
   struct FmmState* fmm = nullptr;
   // banded store
@@ -120,13 +121,14 @@ struct tdw_problem {
   double* d_aval = nullptr;
   double* d_adiag = nullptr;
   int jac_iters = 0;
-  // near part (lags 1..TDW_NEAR_LAGS), all rows, ELL [TDW_NEAR_MAX][ns]
+  // near structure: pairs whose band reaches a split lag g in 2..kb+1, all rows,
+  // ELL columns [TDW_NEAR_MAX][ns], values [kb][TDW_NEAR_MAX][ns] (lag g = 2 + index)
   int near_w = 0;
   int64_t n_near = 0, n_near_evals = 0;
   int* d_ncol = nullptr;
   double* d_nval = nullptr;
   int* d_ncol_packed = nullptr;    // ncol in the cluster solver's (owner << 24 | local) form
-  double* d_bnear = nullptr;       // [2][ns] lag-2 unknown term, produced by the previous solve
+  double* d_bnear = nullptr;       // [kb][kb+1][ns]: N_g x^(beta-1) from solve(beta), for step beta-1+g
   // pipelined loop: side stream for the far convolution, per-step events
   cudaStream_t side = nullptr;
   std::vector<cudaEvent_t> ev_solve, ev_conv;
