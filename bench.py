@@ -262,7 +262,9 @@ def run_ours(args, world, rank, local):
                        "mot_steps_per_bench_step": nt - 1, "parallelism": f"rows x{world}",
                        "l2": "banded store 1.5 GB > 126 MB L2 (no flush needed)"
                        if args.config >= 2 else "store fits in L2",
-                       "gamma_star": info["gamma_star"], "n_band": int(n_band)},
+                       "gamma_star": info["gamma_star"], "n_band": int(n_band),
+                       "steps_per_conv_pass": info["steps_per_pass"],
+                       "solve_cluster": info["solve_cluster"], "conv_grid": info["conv_grid"]},
             "e2e": {"value": e2e, "unit": "steps/s", "h2d_bytes_per_step": h2d * (nt - 1) // (nt - 1),
                     "d2h_bytes_per_step": d2h, "api": "marching.march(spec, mats=store)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -272,7 +274,8 @@ def run_ours(args, world, rank, local):
                          "bytes_per_launch": 16.0 * n_band},
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
-            "gpu_launches": int(tm["steps"] * (2 if world == 1 else 3) + args.steps),
+            # per loop: init_hist + (conv_kernel + reduce_parts) per pass + one solve per step
+            "gpu_launches": int(args.steps * (1 + 2 * (-(-(nt - 1) // info["steps_per_pass"])) + (nt - 1))),
             "assembly": {"ms": info["t_assemble_ms"], "evals": info["n_evals"],
                          "evals_per_s": info["n_evals"] / (info["t_fill_ms"] * 1e-3),
                          "metric": "(i,j,gamma) layer-potential evals/s (fill kernel, fp64)"},

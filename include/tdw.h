@@ -83,6 +83,8 @@ typedef struct {
   int32_t solve_cluster;     /* CTAs of the cluster solver (0 = grid fallback)   */
   int64_t n_units;           /* (row block, column tile) units with band entries */
   int64_t units_hdr32;       /* of those, units stored with 32-bit pair headers  */
+  int32_t steps_per_pass;    /* time steps computed per convolution pass (kb)    */
+  int32_t near_width;        /* widest row of the near structure                 */
 } tdw_info;
 
 typedef struct {

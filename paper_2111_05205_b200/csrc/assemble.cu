@@ -575,6 +575,57 @@ int tdw_assemble_impl(tdw_problem* pb) {
   TDW_CUDA(ctx, cudaMemsetAsync(pb->d_flags, 0, sizeof(int) * 4, st));
   fill_unit_init<<<256, 256, 0, st>>>(pb->d_unit, nunit);
 
+  const bool bm = pb->bie == TDW_BIE_BMBIE;
+  // near structure (split lags 2..kb+1) and lag-1 step matrix, all rows.  Built
+  // first: the temporal block kb shrinks until the near structure fits.
+  TDW_CUDA(ctx, cudaMalloc(&pb->d_acol, sizeof(int) * (size_t)TDW_ELL_MAX * pb->ns));
+  TDW_CUDA(ctx, cudaMalloc(&pb->d_aval, sizeof(double) * (size_t)TDW_ELL_MAX * pb->ns));
+  TDW_CUDA(ctx, cudaMalloc(&pb->d_adiag, sizeof(double) * pb->ns));
+  TDW_CUDA(ctx, cudaMalloc(&pb->d_ncol, sizeof(int) * (size_t)TDW_NEAR_MAX * pb->ns));
+  TDW_CUDA(ctx, cudaMalloc(&pb->d_nval, sizeof(double) * (size_t)pb->kb * TDW_NEAR_MAX * pb->ns));
+  int* d_ellw = nullptr;
+  TDW_CUDA(ctx, cudaMalloc(&d_ellw, sizeof(int)));
+  for (;;) {
+  TDW_CUDA(ctx, cudaMemsetAsync(d_ellw, 0, sizeof(int), st));
+  TDW_CUDA(ctx, cudaMemsetAsync(d_cnt, 0, sizeof(unsigned long long) * 8, st));
+  TDW_CUDA(ctx, cudaMemsetAsync(pb->d_flags, 0, sizeof(int) * 4, st));
+  NearArgs s{};
+  s.elem = pb->d_elem;
+  s.leafc = pb->d_leafc;
+  s.split_lag2 = pb->split_lag2;
+  s.kb = pb->kb;
+  s.phi = pb->d_phi;
+  s.ns = pb->ns;
+  s.ntiles = pb->ntiles;
+  s.d = pb->d;
+  s.cap = pb->cap;
+  s.c = pb->c;
+  s.dt = pb->dt;
+  s.K = pb->K;
+  s.ncol = pb->d_ncol;
+  s.nval = pb->d_nval;
+  s.acol = pb->d_acol;
+  s.aval = pb->d_aval;
+  s.adiag = pb->d_adiag;
+  s.flags = pb->d_flags;
+  s.ell_w = d_ellw;
+  s.bound_bits = d_cnt + 3;
+  s.nnz = d_cnt + 2;
+  s.n_near = d_cnt + 5;
+  s.n_evals = d_cnt + 6;
+  if (pb->d == 1) { if (bm) launch_near<1, true>(s, st); else launch_near<1, false>(s, st); }
+  if (pb->d == 2) { if (bm) launch_near<2, true>(s, st); else launch_near<2, false>(s, st); }
+  if (pb->d == 3) { if (bm) launch_near<3, true>(s, st); else launch_near<3, false>(s, st); }
+  TDW_CUDA(ctx, cudaGetLastError());
+  int nf[4];
+  TDW_CUDA(ctx, cudaMemcpy(nf, pb->d_flags, sizeof(nf), cudaMemcpyDeviceToHost));
+  if (nf[3] == 1 && pb->kb > 1) {
+    --pb->kb;
+    continue;
+  }
+  break;
+  }
+
   AsmArgs a{};
   a.elem = pb->d_elem;
   a.leafc = pb->d_leafc;
@@ -664,50 +715,12 @@ int tdw_assemble_impl(tdw_problem* pb) {
   a.units = pb->d_units;
   a.phi = pb->d_phi;
   TDW_CUDA(ctx, cudaEventRecord(f0, st));
-  const bool bm = pb->bie == TDW_BIE_BMBIE;
   if (pb->d == 1) { if (bm) launch_fill<1, true>(a, nseg, st); else launch_fill<1, false>(a, nseg, st); }
   if (pb->d == 2) { if (bm) launch_fill<2, true>(a, nseg, st); else launch_fill<2, false>(a, nseg, st); }
   if (pb->d == 3) { if (bm) launch_fill<3, true>(a, nseg, st); else launch_fill<3, false>(a, nseg, st); }
   TDW_CUDA(ctx, cudaGetLastError());
   TDW_CUDA(ctx, cudaEventRecord(f1, st));
 
-  // near part (lags 1, 2) and lag-1 step matrix, all rows
-  TDW_CUDA(ctx, cudaMalloc(&pb->d_acol, sizeof(int) * (size_t)TDW_ELL_MAX * pb->ns));
-  TDW_CUDA(ctx, cudaMalloc(&pb->d_aval, sizeof(double) * (size_t)TDW_ELL_MAX * pb->ns));
-  TDW_CUDA(ctx, cudaMalloc(&pb->d_adiag, sizeof(double) * pb->ns));
-  TDW_CUDA(ctx, cudaMalloc(&pb->d_ncol, sizeof(int) * (size_t)TDW_NEAR_MAX * pb->ns));
-  TDW_CUDA(ctx, cudaMalloc(&pb->d_nval, sizeof(double) * (size_t)pb->kb * TDW_NEAR_MAX * pb->ns));
-  int* d_ellw = nullptr;
-  TDW_CUDA(ctx, cudaMalloc(&d_ellw, sizeof(int)));
-  TDW_CUDA(ctx, cudaMemsetAsync(d_ellw, 0, sizeof(int), st));
-  NearArgs s{};
-  s.elem = pb->d_elem;
-  s.leafc = pb->d_leafc;
-  s.split_lag2 = pb->split_lag2;
-  s.kb = pb->kb;
-  s.phi = pb->d_phi;
-  s.ns = pb->ns;
-  s.ntiles = pb->ntiles;
-  s.d = pb->d;
-  s.cap = pb->cap;
-  s.c = pb->c;
-  s.dt = pb->dt;
-  s.K = pb->K;
-  s.ncol = pb->d_ncol;
-  s.nval = pb->d_nval;
-  s.acol = pb->d_acol;
-  s.aval = pb->d_aval;
-  s.adiag = pb->d_adiag;
-  s.flags = pb->d_flags;
-  s.ell_w = d_ellw;
-  s.bound_bits = d_cnt + 3;
-  s.nnz = d_cnt + 2;
-  s.n_near = d_cnt + 5;
-  s.n_evals = d_cnt + 6;
-  if (pb->d == 1) { if (bm) launch_near<1, true>(s, st); else launch_near<1, false>(s, st); }
-  if (pb->d == 2) { if (bm) launch_near<2, true>(s, st); else launch_near<2, false>(s, st); }
-  if (pb->d == 3) { if (bm) launch_near<3, true>(s, st); else launch_near<3, false>(s, st); }
-  TDW_CUDA(ctx, cudaGetLastError());
   TDW_CUDA(ctx, cudaEventRecord(e1, st));
   TDW_CUDA(ctx, cudaStreamSynchronize(st));
   cudaFree(d_hdr_tmp);

@@ -144,7 +144,7 @@ int tdw_problem_create_impl(tdw_ctx* ctx, const tdw_problem_desc* dsc, tdw_probl
   {
     // temporal blocking: one convolution pass computes kb consecutive steps
     const char* e = getenv("TDW_KB");
-    pb->kb = std::max(1, std::min(TDW_KB_MAX, e ? atoi(e) : 2));
+    pb->kb = std::max(1, std::min(TDW_KB_MAX, e ? atoi(e) : 3));
   }
   pb->c = dsc->c;
   pb->dt = dsc->dt;
@@ -356,6 +356,8 @@ int tdw_problem_info(const tdw_problem* pb, tdw_info* out) {
   out->solve_cluster = pb->sp_cl;
   out->n_units = pb->n_units;
   out->units_hdr32 = pb->units_hdr32;
+  out->steps_per_pass = pb->kb;
+  out->near_width = pb->near_w;
   return TDW_OK;
 }
 

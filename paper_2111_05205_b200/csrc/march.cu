@@ -265,6 +265,10 @@ __global__ void __launch_bounds__(TDW_CONV_THREADS, 1)
       const double2* hp[TDW_ROWS_PER_WARP];
       int off[TDW_ROWS_PER_WARP];
       double s0[TDW_ROWS_PER_WARP][KB], s1[TDW_ROWS_PER_WARP][KB];
+      // sliding window of history rows: hw[r][i] = row (hrel - k + i), the value
+      // step i multiplies with entry k; entry k+1 of step i+1 uses the same row,
+      // so each k loads one new row (one history read per coefficient for any KB)
+      double2 hw[TDW_ROWS_PER_WARP][KB];
 #pragma unroll
       for (int r = 0; r < TDW_ROWS_PER_WARP; ++r) {
         const int row = warp * TDW_ROWS_PER_WARP + r;
@@ -275,7 +279,11 @@ __global__ void __launch_bounds__(TDW_CONV_THREADS, 1)
         hp[r] = hs + hrel * TDW_TJ + jl;
         off[r] = 0;
 #pragma unroll
-        for (int i = 0; i < KB; ++i) { s0[r][i] = 0.0; s1[r][i] = 0.0; }
+        for (int i = 0; i < KB; ++i) {
+          s0[r][i] = 0.0;
+          s1[r][i] = 0.0;
+          hw[r][i] = len[r] > 0 ? hp[r][i * TDW_TJ] : make_double2(0.0, 0.0);
+        }
       }
       lmax = __reduce_max_sync(FULLMASK, lmax);
       for (int k0 = 0; k0 < lmax; k0 += 4) {
@@ -290,10 +298,12 @@ __global__ void __launch_bounds__(TDW_CONV_THREADS, 1)
               const double2 cv = cp[r][off[r] + __popc(m & lt)];
 #pragma unroll
               for (int i = 0; i < KB; ++i) {
-                const double2 hv = hp[r][(i - k) * TDW_TJ];
-                s0[r][i] = fma(cv.x, hv.x, s0[r][i]);
-                s1[r][i] = fma(cv.y, hv.y, s1[r][i]);
+                s0[r][i] = fma(cv.x, hw[r][i].x, s0[r][i]);
+                s1[r][i] = fma(cv.y, hw[r][i].y, s1[r][i]);
               }
+#pragma unroll
+              for (int i = KB - 1; i > 0; --i) hw[r][i] = hw[r][i - 1];
+              if (len[r] > k + 1) hw[r][0] = hp[r][(-k - 1) * TDW_TJ];
             }
             off[r] += __popc(m);
           }

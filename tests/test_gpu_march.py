@@ -159,6 +159,27 @@ def test_solver_variants_agree(monkeypatch, env):
     assert per_step_rel(h.q, ref.q).max() < 1e-11
 
 
+@pytest.mark.parametrize("kb", [1, 2, 4])
+def test_temporal_block_sizes_match_reference(monkeypatch, kb):
+    """One convolution pass per kb steps (split lags 2..kb+1 corrected by the
+    solves' near terms) reproduces the reference golden march of config 2 for
+    every block size; the default (3) is covered by the golden tests above."""
+    g = golden("march_cfg2.npz")
+    spec = scenarios.build_spec(2)
+    monkeypatch.setenv("TDW_KB", str(kb))
+    store = marching.BandStore(spec).assemble()
+    assert store.info()["steps_per_pass"] == kb
+    h = marching.march(spec, mats=store)
+    assert h.status == str(g["status"]) and h.n_steps == int(g["n_steps"])
+    assert per_step_rel(h.q[:, g["sub"]], g["unknown_sub"]).max() < TOL[1]
+    r = _oracle(_mini_spec(3, "bmbie", "mixed"))
+    spec_m = _mini_spec(3, "bmbie", "mixed")
+    hm = marching.march(spec_m)
+    for key in ("u", "q"):
+        mask = np.linalg.norm(r[key], axis=1) > 0
+        assert per_step_rel(getattr(hm, key)[mask], r[key][mask]).max() < TOL[3], key
+
+
 def test_window_off_is_equivalent():
     """window=False keeps the whole history (marching.py:296-300): same result."""
     spec = _mini_spec(1, "bmbie", "neumann", nt=60)
