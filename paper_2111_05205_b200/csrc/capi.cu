@@ -144,7 +144,7 @@ int tdw_problem_create_impl(tdw_ctx* ctx, const tdw_problem_desc* dsc, tdw_probl
   {
     // temporal blocking: one convolution pass computes kb consecutive steps
     const char* e = getenv("TDW_KB");
-    pb->kb = std::max(1, std::min(TDW_KB_MAX, e ? atoi(e) : 3));
+    pb->kb = std::max(1, std::min(TDW_KB_MAX, e ? atoi(e) : 4));
   }
   pb->c = dsc->c;
   pb->dt = dsc->dt;

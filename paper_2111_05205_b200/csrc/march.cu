@@ -102,6 +102,14 @@ __device__ __forceinline__ void tensor2d_g2s(void* dst, const CUtensorMap* map, 
       : "memory");
 }
 
+// 16-byte shared-memory load by 32-bit shared address (keeps the consumer's
+// pointers in one register each)
+__device__ __forceinline__ double2 lds_f64x2(unsigned addr) {
+  double2 v;
+  asm("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(addr));
+  return v;
+}
+
 struct ConvArgs {
   const unsigned char* __restrict__ units;
   const unsigned long long* __restrict__ unit_off;
@@ -261,10 +269,14 @@ __global__ void __launch_bounds__(TDW_CONV_THREADS, 1)
       // box is [time][32 columns], so a warp reads one 512-byte row per (k, step).
       const unsigned lt = (1u << lane) - 1u;
       int len[TDW_ROWS_PER_WARP], lmax = 0;
-      const double2* cp[TDW_ROWS_PER_WARP];
-      const double2* hp[TDW_ROWS_PER_WARP];
+      unsigned cp[TDW_ROWS_PER_WARP];  // shared addresses: row's coefficients
+      unsigned hp[TDW_ROWS_PER_WARP];  // and its lane's history column at row hrel
       int off[TDW_ROWS_PER_WARP];
-      double s0[TDW_ROWS_PER_WARP][KB], s1[TDW_ROWS_PER_WARP][KB];
+      // KB == 1: separate per-unit V_U q and V_W u chains (ILP); KB > 1: the
+      // running row sums take the multiply-adds directly -- KB independent
+      // chains already, and registers are short
+      constexpr int NS1 = KB == 1 ? 1 : 0;
+      double s0[TDW_ROWS_PER_WARP][NS1 ? KB : 1], s1[TDW_ROWS_PER_WARP][NS1 ? KB : 1];
       // sliding window of history rows: hw[r][i] = row (hrel - k + i), the value
       // step i multiplies with entry k; entry k+1 of step i+1 uses the same row,
       // so each k loads one new row (one history read per coefficient for any KB)
@@ -275,35 +287,49 @@ __global__ void __launch_bounds__(TDW_CONV_THREADS, 1)
         int jl, hrel;
         unit_hdr(ub, coef_off, g.y, row * TDW_TJ + lane, jl, len[r], hrel);
         lmax = max(lmax, len[r]);
-        cp[r] = coef + rel[row];
-        hp[r] = hs + hrel * TDW_TJ + jl;
+        cp[r] = smem_u32(coef + rel[row]);
+        hp[r] = smem_u32(hs + hrel * TDW_TJ + jl);
         off[r] = 0;
 #pragma unroll
         for (int i = 0; i < KB; ++i) {
-          s0[r][i] = 0.0;
-          s1[r][i] = 0.0;
-          hw[r][i] = len[r] > 0 ? hp[r][i * TDW_TJ] : make_double2(0.0, 0.0);
+          if (NS1) {
+            s0[r][0] = 0.0;
+            s1[r][0] = 0.0;
+          }
+          hw[r][i] = len[r] > 0 ? lds_f64x2(hp[r] + i * TDW_TJ * 16) : make_double2(0.0, 0.0);
         }
       }
       lmax = __reduce_max_sync(FULLMASK, lmax);
-      for (int k0 = 0; k0 < lmax; k0 += 4) {
+      // unrolled by a multiple of KB: the window rotation then maps onto
+      // register renaming (no moves); the shift and the multiply-adds run
+      // unconditionally (a finished lane multiplies zero coefficients with its
+      // stale, finite window), only the two shared-memory loads are predicated
+      constexpr int UK = KB == 1 ? 4 : (KB == 2 ? 4 : KB);
+      for (int k0 = 0; k0 < lmax; k0 += UK) {
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk) {
+        for (int kk = 0; kk < UK; ++kk) {
           const int k = k0 + kk;
 #pragma unroll
           for (int r = 0; r < TDW_ROWS_PER_WARP; ++r) {
             const bool on = len[r] > k;
             const unsigned m = __ballot_sync(FULLMASK, on);
-            if (on) {
-              const double2 cv = cp[r][off[r] + __popc(m & lt)];
+            double2 cv = make_double2(0.0, 0.0);
+            if (on) cv = lds_f64x2(cp[r] + (off[r] + __popc(m & lt)) * 16);
 #pragma unroll
-              for (int i = 0; i < KB; ++i) {
-                s0[r][i] = fma(cv.x, hw[r][i].x, s0[r][i]);
-                s1[r][i] = fma(cv.y, hw[r][i].y, s1[r][i]);
+            for (int i = 0; i < KB; ++i) {
+              if (NS1) {
+                s0[r][0] = fma(cv.x, hw[r][i].x, s0[r][0]);
+                s1[r][0] = fma(cv.y, hw[r][i].y, s1[r][0]);
+              } else {
+                acc[r][i] = fma(-cv.y, hw[r][i].y, fma(cv.x, hw[r][i].x, acc[r][i]));
               }
+            }
+            if (KB > 1) {
 #pragma unroll
               for (int i = KB - 1; i > 0; --i) hw[r][i] = hw[r][i - 1];
-              if (len[r] > k + 1) hw[r][0] = hp[r][(-k - 1) * TDW_TJ];
+              if (len[r] > k + 1) hw[r][0] = lds_f64x2(hp[r] - (k + 1) * TDW_TJ * 16);
+            } else if (len[r] > k + 1) {
+              hw[r][0] = lds_f64x2(hp[r] - (k + 1) * TDW_TJ * 16);
             }
             off[r] += __popc(m);
           }
@@ -311,8 +337,7 @@ __global__ void __launch_bounds__(TDW_CONV_THREADS, 1)
       }
 #pragma unroll
       for (int r = 0; r < TDW_ROWS_PER_WARP; ++r)
-#pragma unroll
-        for (int i = 0; i < KB; ++i) acc[r][i] += s0[r][i] - s1[r][i];
+        if (NS1) acc[r][0] += s0[r][0] - s1[r][0];
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[stage]);
       ++n;
@@ -964,7 +989,9 @@ static cudaError_t conv_set_smem(int kb, int smem) {
     case 1: return cudaFuncSetAttribute(conv_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     case 2: return cudaFuncSetAttribute(conv_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     case 3: return cudaFuncSetAttribute(conv_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    default: return cudaFuncSetAttribute(conv_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    case 4: return cudaFuncSetAttribute(conv_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    case 5: return cudaFuncSetAttribute(conv_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    default: return cudaFuncSetAttribute(conv_kernel<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   }
 }
 static void conv_launch(int kb, dim3 grid, size_t smem, cudaStream_t s, const ConvArgs& c,
@@ -973,7 +1000,9 @@ static void conv_launch(int kb, dim3 grid, size_t smem, cudaStream_t s, const Co
     case 1: conv_kernel<1><<<grid, TDW_CONV_THREADS, smem, s>>>(c, hmap); break;
     case 2: conv_kernel<2><<<grid, TDW_CONV_THREADS, smem, s>>>(c, hmap); break;
     case 3: conv_kernel<3><<<grid, TDW_CONV_THREADS, smem, s>>>(c, hmap); break;
-    default: conv_kernel<4><<<grid, TDW_CONV_THREADS, smem, s>>>(c, hmap); break;
+    case 4: conv_kernel<4><<<grid, TDW_CONV_THREADS, smem, s>>>(c, hmap); break;
+    case 5: conv_kernel<5><<<grid, TDW_CONV_THREADS, smem, s>>>(c, hmap); break;
+    default: conv_kernel<6><<<grid, TDW_CONV_THREADS, smem, s>>>(c, hmap); break;
   }
 }
 

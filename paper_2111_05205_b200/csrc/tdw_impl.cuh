@@ -15,7 +15,7 @@
 #define TDW_ROWS_PER_WARP 2
 #define TDW_CONV_WARPS (TDW_TI / TDW_ROWS_PER_WARP)
 #define TDW_ELL_MAX 64   // max nnz per row of the lag-1 step matrix
-#define TDW_KB_MAX 4     // time steps per convolution pass (temporal blocking)
+#define TDW_KB_MAX 6     // time steps per convolution pass (temporal blocking)
 #define TDW_NEAR_MAX 192 // max pairs per row in the near structure (bands reaching lags 2..kb+1)
 #define TDW_ELEM_STRIDE 16  // doubles per element record: v0 v1 v2 n c rad
 // Unit layout (one (I-block, J-tile) unit = one contiguous byte range of the store):

@@ -159,11 +159,11 @@ def test_solver_variants_agree(monkeypatch, env):
     assert per_step_rel(h.q, ref.q).max() < 1e-11
 
 
-@pytest.mark.parametrize("kb", [1, 2, 4])
+@pytest.mark.parametrize("kb", [1, 2, 3, 6])
 def test_temporal_block_sizes_match_reference(monkeypatch, kb):
     """One convolution pass per kb steps (split lags 2..kb+1 corrected by the
     solves' near terms) reproduces the reference golden march of config 2 for
-    every block size; the default (3) is covered by the golden tests above."""
+    every block size; the default (4) is covered by the golden tests above."""
     g = golden("march_cfg2.npz")
     spec = scenarios.build_spec(2)
     monkeypatch.setenv("TDW_KB", str(kb))
