@@ -479,49 +479,14 @@ __device__ __forceinline__ double fetch_x(int c, const double* x, int cr,
 }
 
 // near terms of step alpha: sum over the split lags g = 2..kb+1 (fixed order) of
-// N^g x^(alpha-g), each produced by solve(alpha-g+1) into ring slot alpha % (kb+1)
+// N^g x^(alpha-g), each produced by near_step_kernel after solve(alpha-g+1) into
+// ring slot alpha % (kb+1)
 __device__ __forceinline__ double near_in(const ClusterSolveArgs& a, int gi) {
   const int ring = a.kb + 1;
   double s = 0.0;
   for (int g = 0; g < a.kb; ++g) s += a.bnear[((size_t)g * ring + a.alpha % ring) * a.ns + gi];
   return s;
 }
-
-// N^g x^(alpha-1) for the steps alpha-1+g, g = 2..kb+1 (x of this solve)
-template <int CH>
-__device__ __forceinline__ void near_out(const ClusterSolveArgs& a, int gi, const double* xf, int cr,
-                                         cooperative_groups::cluster_group& cl) {
-  double acc[TDW_KB_MAX];
-#pragma unroll
-  for (int g = 0; g < TDW_KB_MAX; ++g) acc[g] = 0.0;
-  const size_t gstride = (size_t)TDW_NEAR_MAX * a.ns;
-  for (int k0 = 0; k0 < a.near_w; k0 += CH) {
-    int cc[CH];
-    double xv[CH];
-#pragma unroll
-    for (int q = 0; q < CH; ++q) {
-      const bool on = k0 + q < a.near_w;
-      cc[q] = on ? __ldg(a.ncol + (size_t)(k0 + q) * a.ns + gi) : (cr << 24);
-    }
-#pragma unroll
-    for (int q = 0; q < CH; ++q) xv[q] = fetch_x(cc[q], xf, cr, cl);
-#pragma unroll
-    for (int g = 0; g < TDW_KB_MAX; ++g) {
-      if (g >= a.kb) break;
-#pragma unroll
-      for (int q = 0; q < CH; ++q) {
-        const bool on = k0 + q < a.near_w;
-        const double v = on ? __ldg(a.nval + g * gstride + (size_t)(k0 + q) * a.ns + gi) : 0.0;
-        acc[g] = fma(v, xv[q], acc[g]);
-      }
-    }
-  }
-  const int ring = a.kb + 1;
-#pragma unroll
-  for (int g = 0; g < TDW_KB_MAX; ++g)
-    if (g < a.kb) a.bnear[((size_t)g * ring + (a.alpha + 1 + g) % ring) * a.ns + gi] = acc[g];
-}
-
 
 // sum_p val[p] x[col[p]] over a CSR row held in shared memory, loads batched by 4
 __device__ __forceinline__ double row_dot(int p0, int p1, const int* col, const double* val,
@@ -659,8 +624,6 @@ __global__ void __launch_bounds__(1024, 1) solve_cluster_kernel(ClusterSolveArgs
   trace_mark(tr, 4);
   cl.sync();
   trace_mark(tr, 5);
-  // split-lag terms of the unknown density for the next steps (x still in shared memory)
-  for (int i = tid; i < nr; i += nth) near_out<8>(a, r0 + i, xf, cr, cl);
   double RR = 0.0, BB = 0.0, XM = 0.0;
   if (tid < 32) {
     if (tid < CL) {
@@ -843,8 +806,6 @@ __global__ void __launch_bounds__(reg_threads<MAXNZ>(), 1) solve_reg_kernel(Clus
   trace_mark(tr, 4);
   cl.sync();
   trace_mark(tr, 5);
-  // split-lag terms of the unknown density for the next steps (x still in shared memory)
-  if (own) near_out<16>(a, gi, xf, cr, cl);
   double RR = 0.0, BB = 0.0, XM = 0.0;
   if (tid < 32) {
     if (tid < CL) {
@@ -888,6 +849,60 @@ __global__ void __launch_bounds__(reg_threads<MAXNZ>(), 1) solve_reg_kernel(Clus
     if (unstable) atomicExch(&a.flags[0], 1);
   }
   trace_mark(tr, 8);
+}
+
+// Near terms of the density x^(alpha-1) just solved, for the steps alpha-1+g,
+// g = 2..kb+1: bnear[g-2][(alpha+g-1) % (kb+1)][i] = sum_k N^g_ik x_col(k).
+// One warp per row over the row-major near structure; x from the history
+// (the unknown component of slot alpha-1).  Runs on the whole GPU between two
+// solves (the convolution pass waits for solves, so the SMs are free).
+__global__ void __launch_bounds__(256) near_step_kernel(const int* __restrict__ ncol_rm,
+                                                        const double* __restrict__ nval_rm, int nstride,
+                                                        int near_w, int ns, int kb,
+                                                        const double2* __restrict__ hist, int hcols,
+                                                        int pad, const double* __restrict__ phi,
+                                                        double* __restrict__ bnear, int alpha,
+                                                        const int* flags) {
+  if (*(volatile const int*)flags != 0) return;
+  const int lane = threadIdx.x & 31;
+  const int i = (int)(((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  if (i >= ns) return;
+  const double2* hrow = hist + (size_t)(pad + alpha - 1) * hcols;
+  double acc[TDW_KB_MAX];
+#pragma unroll
+  for (int g = 0; g < TDW_KB_MAX; ++g) acc[g] = 0.0;
+  for (int k = lane; k < near_w; k += 32) {
+    const int j = __ldg(ncol_rm + (size_t)i * nstride + k);
+    const double2 h = __ldcg(hrow + j);
+    const double x = __ldg(phi + j) == 1.0 ? h.y : h.x;
+#pragma unroll
+    for (int g = 0; g < TDW_KB_MAX; ++g)
+      if (g < kb) acc[g] = fma(__ldg(nval_rm + ((size_t)i * kb + g) * nstride + k), x, acc[g]);
+  }
+  const int ring = kb + 1;
+#pragma unroll
+  for (int g = 0; g < TDW_KB_MAX; ++g) {
+    if (g >= kb) break;
+    double v = acc[g];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULLMASK, v, o);
+    if (lane == 0) bnear[((size_t)g * ring + (alpha + 1 + g) % ring) * ns + i] = v;
+  }
+}
+
+// row-major copy of the near structure for near_step_kernel
+__global__ void near_rowmajor_kernel(const int* ncol, const double* nval, int ns, int kb, int nstride,
+                                     int near_w, int* ncol_rm, double* nval_rm) {
+  const long long n = (long long)ns * nstride;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(e / nstride), k = (int)(e % nstride);
+    const bool on = k < near_w;
+    ncol_rm[e] = on ? ncol[(size_t)k * ns + i] : i;
+    for (int g = 0; g < kb; ++g)
+      nval_rm[((size_t)i * kb + g) * nstride + k] =
+          on ? nval[(size_t)g * TDW_NEAR_MAX * ns + (size_t)k * ns + i] : 0.0;
+  }
 }
 
 // hist[pad + beta][j] = known part (phi q_known, (1-phi) u_known) of every
@@ -1134,6 +1149,13 @@ int launch_solve(tdw_problem* pb, LoopPlan& L, int alpha, cudaStream_t s) {
     else TDW_CUDA(pb->ctx, cudaLaunchKernelEx(&ccfg, solve_reg_kernel<24>, L.cs));
   } else {
     TDW_CUDA(pb->ctx, cudaLaunchKernelEx(&ccfg, solve_cluster_kernel, L.cs));
+  }
+  if (pb->near_w > 0 && pb->split_lag2) {
+    const long long threads = (long long)pb->ns * 32;
+    near_step_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(
+        pb->d_ncol_rm, pb->d_nval_rm, pb->near_stride, pb->near_w, pb->ns, pb->kb, pb->d_hist, pb->hcols,
+        pb->pad, pb->d_phi, pb->d_bnear, alpha, pb->d_flags);
+    TDW_CUDA(pb->ctx, cudaGetLastError());
   }
   return TDW_OK;
 }
@@ -1536,6 +1558,14 @@ int tdw_setup_cluster_solver(tdw_problem* pb) {
     for (int& j : ncol) j = ((j / R) << 24) | (j % R);
     TDW_CUDA(ctx, cudaMalloc(&pb->d_ncol_packed, sizeof(int) * ncol.size()));
     TDW_CUDA(ctx, cudaMemcpy(pb->d_ncol_packed, ncol.data(), sizeof(int) * ncol.size(), cudaMemcpyHostToDevice));
+    // row-major near structure for near_step_kernel
+    pb->near_stride = std::max(32, (pb->near_w + 31) / 32 * 32);
+    TDW_CUDA(ctx, cudaMalloc(&pb->d_ncol_rm, sizeof(int) * (size_t)ns * pb->near_stride));
+    TDW_CUDA(ctx, cudaMalloc(&pb->d_nval_rm, sizeof(double) * (size_t)ns * pb->kb * pb->near_stride));
+    near_rowmajor_kernel<<<2 * ctx->num_sms, 256, 0, ctx->stream>>>(pb->d_ncol, pb->d_nval, ns, pb->kb,
+                                                                   pb->near_stride, pb->near_w,
+                                                                   pb->d_ncol_rm, pb->d_nval_rm);
+    TDW_CUDA(ctx, cudaGetLastError());
   }
   TDW_CUDA(ctx, cudaFuncSetAttribute(solve_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)pb->sp_smem));

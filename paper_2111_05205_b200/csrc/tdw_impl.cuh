@@ -128,6 +128,9 @@ struct tdw_problem {
   int* d_ncol = nullptr;
   double* d_nval = nullptr;
   int* d_ncol_packed = nullptr;    // ncol in the cluster solver's (owner << 24 | local) form
+  int near_stride = 0;             // row-major copy for near_step_kernel: [ns][stride], [ns][kb][stride]
+  int* d_ncol_rm = nullptr;
+  double* d_nval_rm = nullptr;
   double* d_bnear = nullptr;       // [kb][kb+1][ns]: N_g x^(beta-1) from solve(beta), for step beta-1+g
   // pipelined loop: side stream for the far convolution, per-step events
   cudaStream_t side = nullptr;
