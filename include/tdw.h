@@ -85,6 +85,7 @@ typedef struct {
   int64_t units_hdr32;       /* of those, units stored with 32-bit pair headers  */
   int32_t steps_per_pass;    /* time steps computed per convolution pass (kb)    */
   int32_t near_width;        /* widest row of the near structure                 */
+  int32_t pass_overlap;      /* solves a convolution pass runs beside            */
 } tdw_info;
 
 typedef struct {

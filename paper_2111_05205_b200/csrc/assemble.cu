@@ -151,8 +151,8 @@ __device__ __forceinline__ bool pair_allowed(const int* leafc, int i, int j) {
 struct AsmArgs {
   const double* elem;
   const int* leafc;                    // packed leaf-cell coords (FMM near field) or null
-  int split_lag2;                      // 1: lag 2..kb+1 entries keep the known density only
-  int kb;                              // time steps per convolution pass
+  int split_lag2;                      // 1: lag 2..nsl+1 entries keep the known density only
+  int nsl;                             // split lags
   int ns, row_lo, rows_loc, ntiles, d, cap;
   double c, dt, K;
   uint32_t* hdr;
@@ -275,11 +275,12 @@ __global__ void __launch_bounds__(128) fill_kernel(AsmArgs a) {
         vu += w[q] * ru[q];
         vw += w[q] * rw[q];
       }
-      if (a.split_lag2 && gg >= 2 && gg <= a.kb + 1) {
-        // lags 2..kb+1: keep only the coefficient of the KNOWN density of
+      if (a.split_lag2 && gg >= 2 && gg <= a.nsl + 1) {
+        // lags 2..nsl+1: keep only the coefficient of the KNOWN density of
         // element j (q if phi_j = 1, u if phi_j = 0); the unknown one is applied
-        // by the solves through the near structure, so the convolution pass of
-        // steps alpha..alpha+kb-1 waits only for the solve of step alpha-2.
+        // through the near structure after each solve, so the convolution pass
+        // of steps alpha..alpha+kb-1 waits only for the solve of step
+        // alpha-1-overlap (nsl = kb + overlap - 1).
         const double pj = a.phi[j];
         vu = pj == 1.0 ? vu : 0.0;
         vw = pj == 1.0 ? 0.0 : vw;
@@ -364,7 +365,7 @@ __global__ void unit_layout_kernel(const unsigned long long* segcount, const uin
 struct NearArgs {
   const double* elem;
   const int* leafc;
-  int split_lag2, kb;
+  int split_lag2, nsl;
   const double* phi;
   int ns, ntiles, d, cap;
   double c, dt, K;
@@ -382,7 +383,7 @@ struct NearArgs {
 };
 
 // Rows of the lag-1 step matrix and of the "unknown" coupling at the split lags
-// g = 2..kb+1, all rows (replicated on every rank).  With
+// g = 2..nsl+1, all rows (replicated on every rank).  With
 // V^(g) = sum_kappa w^kappa U^(g-kappa) (U^(m) = 0 for m < max(1, arrival); zero
 // outside the pair's band, as in the store):
 //   A_ij     = V_W^(1) phi_j - V_U^(1) (1 - phi_j)      (build_step_matrix, marching.py:279-289)
@@ -398,7 +399,7 @@ __global__ void __launch_bounds__(128) near_kernel(NearArgs a) {
   const double* pi = a.elem + (size_t)i * TDW_ELEM_STRIDE;
   double ci[3] = {pi[12], pi[13], pi[14]};
   double nx[3] = {-pi[9], -pi[10], -pi[11]};
-  const int gtop = a.split_lag2 ? a.kb + 1 : 1;  // highest split lag
+  const int gtop = a.split_lag2 ? a.nsl + 1 : 1;  // highest split lag
   const size_t gstride = (size_t)TDW_NEAR_MAX * a.ns;
   int cnt = 0, acnt = 0;
   double diag = 0.0, offsum = 0.0;
@@ -427,9 +428,9 @@ __global__ void __launch_bounds__(128) near_kernel(NearArgs a) {
       PairGeom g;
       pair_geom<BM>(ci, ej.v0, ej.v1, ej.v2, ej.n, nx, g);
       // U^(m), m = 1..gtop (zero before arrival)
-      double uu[TDW_KB_MAX + 2], ww[TDW_KB_MAX + 2];
+      double uu[TDW_NSL_MAX + 2], ww[TDW_NSL_MAX + 2];
 #pragma unroll
-      for (int m = 0; m < TDW_KB_MAX + 2; ++m) { uu[m] = 0.0; ww[m] = 0.0; }
+      for (int m = 0; m < TDW_NSL_MAX + 2; ++m) { uu[m] = 0.0; ww[m] = 0.0; }
       for (int m = 1; m <= gtop; ++m)
         if (b.arr <= m) { coeff_eval<D, BM>(g, (double)m * a.c * a.dt, a.K, uu[m], ww[m]); ++nev; }
       const double pj = a.phi[j];
@@ -576,13 +577,14 @@ int tdw_assemble_impl(tdw_problem* pb) {
   fill_unit_init<<<256, 256, 0, st>>>(pb->d_unit, nunit);
 
   const bool bm = pb->bie == TDW_BIE_BMBIE;
-  // near structure (split lags 2..kb+1) and lag-1 step matrix, all rows.  Built
-  // first: the temporal block kb shrinks until the near structure fits.
+  // near structure (split lags 2..nsl+1) and lag-1 step matrix, all rows.  Built
+  // first: the pass overlap, then the temporal block kb, shrink until the near
+  // structure fits.
   TDW_CUDA(ctx, cudaMalloc(&pb->d_acol, sizeof(int) * (size_t)TDW_ELL_MAX * pb->ns));
   TDW_CUDA(ctx, cudaMalloc(&pb->d_aval, sizeof(double) * (size_t)TDW_ELL_MAX * pb->ns));
   TDW_CUDA(ctx, cudaMalloc(&pb->d_adiag, sizeof(double) * pb->ns));
   TDW_CUDA(ctx, cudaMalloc(&pb->d_ncol, sizeof(int) * (size_t)TDW_NEAR_MAX * pb->ns));
-  TDW_CUDA(ctx, cudaMalloc(&pb->d_nval, sizeof(double) * (size_t)pb->kb * TDW_NEAR_MAX * pb->ns));
+  TDW_CUDA(ctx, cudaMalloc(&pb->d_nval, sizeof(double) * (size_t)pb->nsl * TDW_NEAR_MAX * pb->ns));
   int* d_ellw = nullptr;
   TDW_CUDA(ctx, cudaMalloc(&d_ellw, sizeof(int)));
   for (;;) {
@@ -593,7 +595,7 @@ int tdw_assemble_impl(tdw_problem* pb) {
   s.elem = pb->d_elem;
   s.leafc = pb->d_leafc;
   s.split_lag2 = pb->split_lag2;
-  s.kb = pb->kb;
+  s.nsl = pb->nsl;
   s.phi = pb->d_phi;
   s.ns = pb->ns;
   s.ntiles = pb->ntiles;
@@ -618,9 +620,14 @@ int tdw_assemble_impl(tdw_problem* pb) {
   if (pb->d == 3) { if (bm) launch_near<3, true>(s, st); else launch_near<3, false>(s, st); }
   TDW_CUDA(ctx, cudaGetLastError());
   int nf[4];
-  TDW_CUDA(ctx, cudaMemcpy(nf, pb->d_flags, sizeof(nf), cudaMemcpyDeviceToHost));
-  if (nf[3] == 1 && pb->kb > 1) {
-    --pb->kb;
+  TDW_CUDA(ctx, cudaMemcpyAsync(nf, pb->d_flags, sizeof(nf), cudaMemcpyDeviceToHost, st));
+  TDW_CUDA(ctx, cudaStreamSynchronize(st));
+  if (nf[3] == 1 && pb->nsl > 1) {
+    if (pb->overlap > 1) --pb->overlap;
+    else --pb->kb;
+    pb->overlap = std::min(pb->overlap, pb->kb);
+    pb->nsl = pb->kb + pb->overlap - 1;
+    pb->bring = pb->kb + pb->overlap;
     continue;
   }
   break;
@@ -630,7 +637,7 @@ int tdw_assemble_impl(tdw_problem* pb) {
   a.elem = pb->d_elem;
   a.leafc = pb->d_leafc;
   a.split_lag2 = pb->split_lag2;
-  a.kb = pb->kb;
+  a.nsl = pb->nsl;
   a.ns = pb->ns;
   a.row_lo = pb->row_lo;
   a.rows_loc = pb->rows_per_rank;
@@ -745,7 +752,7 @@ int tdw_assemble_impl(tdw_problem* pb) {
   pb->jac_bound = bound;
   pb->ell_w = hellw;
   if (hflags[3] == 1)
-    return tdw_fail(ctx, TDW_ERR_LIMIT, "near structure: more than the supported pairs within (kb + 1) c dt of a row (lower TDW_KB)");
+    return tdw_fail(ctx, TDW_ERR_LIMIT, "near structure: more than the supported pairs near a row");
   if (!(bound < 0.9))
     return tdw_fail(ctx, TDW_ERR_SINGULAR,
                     "step matrix is not diagonally dominant (Jacobi bound " +
@@ -865,7 +872,7 @@ int tdw_assemble_impl(tdw_problem* pb) {
     // [kb][rows][S]: one pass's partials (reduced on the pass's stream before the next pass)
     TDW_CUDA(ctx, cudaMalloc(&pb->d_bpart, pb->kb * sizeof(double) * (size_t)S * pb->rows_per_rank));
     TDW_CUDA(ctx, cudaMemset(pb->d_bpart, 0, pb->kb * sizeof(double) * (size_t)S * pb->rows_per_rank));
-    TDW_CUDA(ctx, cudaMalloc(&pb->d_bnear, sizeof(double) * (size_t)pb->kb * (pb->kb + 1) * pb->ns));
+    TDW_CUDA(ctx, cudaMalloc(&pb->d_bnear, sizeof(double) * (size_t)pb->nsl * (pb->nsl + 1) * pb->ns));
   }
   pb->store_bytes = (int64_t)(total_bytes + sizeof(unsigned long long) * (nunit + 1) + sizeof(int2) * nunit);
   pb->assembled = true;

@@ -145,6 +145,12 @@ int tdw_problem_create_impl(tdw_ctx* ctx, const tdw_problem_desc* dsc, tdw_probl
     // temporal blocking: one convolution pass computes kb consecutive steps
     const char* e = getenv("TDW_KB");
     pb->kb = std::max(1, std::min(TDW_KB_MAX, e ? atoi(e) : 4));
+    // a pass waits for the solve overlap+1 steps back and runs beside the last
+    // `overlap` solves; the split lags reach kb + overlap
+    const char* o = getenv("TDW_OVERLAP");
+    pb->overlap = std::max(1, std::min(pb->kb, o ? atoi(o) : 2));
+    pb->nsl = pb->kb + pb->overlap - 1;
+    pb->bring = pb->kb + pb->overlap;
   }
   pb->c = dsc->c;
   pb->dt = dsc->dt;
@@ -357,6 +363,7 @@ int tdw_problem_info(const tdw_problem* pb, tdw_info* out) {
   out->n_units = pb->n_units;
   out->units_hdr32 = pb->units_hdr32;
   out->steps_per_pass = pb->kb;
+  out->pass_overlap = pb->overlap;
   out->near_width = pb->near_w;
   return TDW_OK;
 }

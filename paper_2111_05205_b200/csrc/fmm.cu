@@ -425,6 +425,9 @@ extern "C" int tdw_fmm_setup(tdw_problem* pb, const tdw_fmm_desc* fd) {
   if (rc) return rc;
   pb->split_lag2 = 0;
   pb->kb = 1;  // the FMM loop is sequential: one step per convolution pass
+  pb->overlap = 1;
+  pb->nsl = 1;
+  pb->bring = 2;
   pb->skip_empty_units = true;
   pb->cap = std::min(fd->gamma_near, nt - 1);
   pb->n_lags = pb->cap;

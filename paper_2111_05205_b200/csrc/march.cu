@@ -442,8 +442,8 @@ __device__ __forceinline__ void block_reduce2_max(double& a, double& b, double* 
 struct ClusterSolveArgs {
   const double* bpart;                      // far partials of this step (nsplit > 0)
   double* b;                                // all-gathered far rhs (nsplit == 0)
-  double* bnear;                            // [kb][kb+1][ns] near terms (see tdw_problem::d_bnear)
-  int kb;                                   // split lags 2..kb+1
+  double* bnear;                            // [nsl][nsl+1][ns] near terms (see tdw_problem::d_bnear)
+  int nsl;                                  // split lags 2..nsl+1
   const int* __restrict__ sp_rowptr;        // [CL][R+1], relative to the CTA's slice
   const long long* __restrict__ sp_nnzoff;  // [CL+1]
   const int* __restrict__ sp_col;           // packed (owner << 24) | local
@@ -478,13 +478,13 @@ __device__ __forceinline__ double fetch_x(int c, const double* x, int cr,
   return owner == cr ? x[loc] : *cl.map_shared_rank(x + loc, owner);
 }
 
-// near terms of step alpha: sum over the split lags g = 2..kb+1 (fixed order) of
+// near terms of step alpha: sum over the split lags g = 2..nsl+1 (fixed order) of
 // N^g x^(alpha-g), each produced by near_step_kernel after solve(alpha-g+1) into
-// ring slot alpha % (kb+1)
+// ring slot alpha % (nsl+1)
 __device__ __forceinline__ double near_in(const ClusterSolveArgs& a, int gi) {
-  const int ring = a.kb + 1;
+  const int ring = a.nsl + 1;
   double s = 0.0;
-  for (int g = 0; g < a.kb; ++g) s += a.bnear[((size_t)g * ring + a.alpha % ring) * a.ns + gi];
+  for (int g = 0; g < a.nsl; ++g) s += a.bnear[((size_t)g * ring + a.alpha % ring) * a.ns + gi];
   return s;
 }
 
@@ -852,13 +852,13 @@ __global__ void __launch_bounds__(reg_threads<MAXNZ>(), 1) solve_reg_kernel(Clus
 }
 
 // Near terms of the density x^(alpha-1) just solved, for the steps alpha-1+g,
-// g = 2..kb+1: bnear[g-2][(alpha+g-1) % (kb+1)][i] = sum_k N^g_ik x_col(k).
+// g = 2..nsl+1: bnear[g-2][(alpha+g-1) % (nsl+1)][i] = sum_k N^g_ik x_col(k).
 // One warp per row over the row-major near structure; x from the history
 // (the unknown component of slot alpha-1).  Runs on the whole GPU between two
 // solves (the convolution pass waits for solves, so the SMs are free).
 __global__ void __launch_bounds__(256) near_step_kernel(const int* __restrict__ ncol_rm,
                                                         const double* __restrict__ nval_rm, int nstride,
-                                                        int near_w, int ns, int kb,
+                                                        int near_w, int ns, int nsl,
                                                         const double2* __restrict__ hist, int hcols,
                                                         int pad, const double* __restrict__ phi,
                                                         double* __restrict__ bnear, int alpha,
@@ -868,21 +868,21 @@ __global__ void __launch_bounds__(256) near_step_kernel(const int* __restrict__ 
   const int i = (int)(((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
   if (i >= ns) return;
   const double2* hrow = hist + (size_t)(pad + alpha - 1) * hcols;
-  double acc[TDW_KB_MAX];
+  double acc[TDW_NSL_MAX];
 #pragma unroll
-  for (int g = 0; g < TDW_KB_MAX; ++g) acc[g] = 0.0;
+  for (int g = 0; g < TDW_NSL_MAX; ++g) acc[g] = 0.0;
   for (int k = lane; k < near_w; k += 32) {
     const int j = __ldg(ncol_rm + (size_t)i * nstride + k);
     const double2 h = __ldcg(hrow + j);
     const double x = __ldg(phi + j) == 1.0 ? h.y : h.x;
 #pragma unroll
-    for (int g = 0; g < TDW_KB_MAX; ++g)
-      if (g < kb) acc[g] = fma(__ldg(nval_rm + ((size_t)i * kb + g) * nstride + k), x, acc[g]);
+    for (int g = 0; g < TDW_NSL_MAX; ++g)
+      if (g < nsl) acc[g] = fma(__ldg(nval_rm + ((size_t)i * nsl + g) * nstride + k), x, acc[g]);
   }
-  const int ring = kb + 1;
+  const int ring = nsl + 1;
 #pragma unroll
-  for (int g = 0; g < TDW_KB_MAX; ++g) {
-    if (g >= kb) break;
+  for (int g = 0; g < TDW_NSL_MAX; ++g) {
+    if (g >= nsl) break;
     double v = acc[g];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULLMASK, v, o);
@@ -891,7 +891,7 @@ __global__ void __launch_bounds__(256) near_step_kernel(const int* __restrict__ 
 }
 
 // row-major copy of the near structure for near_step_kernel
-__global__ void near_rowmajor_kernel(const int* ncol, const double* nval, int ns, int kb, int nstride,
+__global__ void near_rowmajor_kernel(const int* ncol, const double* nval, int ns, int nsl, int nstride,
                                      int near_w, int* ncol_rm, double* nval_rm) {
   const long long n = (long long)ns * nstride;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n;
@@ -899,8 +899,8 @@ __global__ void near_rowmajor_kernel(const int* ncol, const double* nval, int ns
     const int i = (int)(e / nstride), k = (int)(e % nstride);
     const bool on = k < near_w;
     ncol_rm[e] = on ? ncol[(size_t)k * ns + i] : i;
-    for (int g = 0; g < kb; ++g)
-      nval_rm[((size_t)i * kb + g) * nstride + k] =
+    for (int g = 0; g < nsl; ++g)
+      nval_rm[((size_t)i * nsl + g) * nstride + k] =
           on ? nval[(size_t)g * TDW_NEAR_MAX * ns + (size_t)k * ns + i] : 0.0;
   }
 }
@@ -1103,7 +1103,7 @@ int make_plan(tdw_problem* pb, LoopPlan& L, double threshold, bool want_rhs) {
 int begin_loop(tdw_problem* pb, cudaStream_t st) {
   tdw_ctx* ctx = pb->ctx;
   TDW_CUDA(ctx, cudaMemsetAsync(pb->d_flags, 0, sizeof(int) * 4, st));
-  TDW_CUDA(ctx, cudaMemsetAsync(pb->d_bnear, 0, sizeof(double) * pb->kb * (pb->kb + 1) * (size_t)pb->ns, st));
+  TDW_CUDA(ctx, cudaMemsetAsync(pb->d_bnear, 0, sizeof(double) * pb->nsl * (pb->nsl + 1) * (size_t)pb->ns, st));
   init_hist_kernel<<<2 * ctx->num_sms, 256, 0, st>>>(pb->d_hist, pb->hstride, pb->hcols, pb->pad, pb->ns,
                                                     pb->nt, pb->d_phi, pb->d_perm, pb->d_uk, pb->d_qk);
   TDW_CUDA(ctx, cudaGetLastError());
@@ -1118,7 +1118,7 @@ int launch_conv(tdw_problem* pb, LoopPlan& L, int alpha, int nsteps, cudaStream_
   // fixed-order sum of the split partials into the steps' b (own rows), on the
   // convolution's stream: off the solve's critical path
   reduce_parts_kernel<<<dim3((pb->rows_per_rank + 127) / 128, nsteps), 128, 0, s>>>(
-      L.c.bpart, pb->nsplit, pb->rows_per_rank, pb->d_b, pb->bstride, pb->b_off, 2 * pb->kb, alpha,
+      L.c.bpart, pb->nsplit, pb->rows_per_rank, pb->d_b, pb->bstride, pb->b_off, pb->bring, alpha,
       pb->d_flags);
   TDW_CUDA(pb->ctx, cudaGetLastError());
   return TDW_OK;
@@ -1139,9 +1139,9 @@ int launch_solve(tdw_problem* pb, LoopPlan& L, int alpha, cudaStream_t s) {
   ccfg.numAttrs = 1;
   L.cs.alpha = alpha;
   L.cs.bpart = pb->d_bpart;
-  L.cs.b = pb->d_b + (size_t)(alpha % (2 * pb->kb)) * pb->bstride;
+  L.cs.b = pb->d_b + (size_t)(alpha % pb->bring) * pb->bstride;
   L.cs.bnear = pb->d_bnear;
-  L.cs.kb = pb->kb;
+  L.cs.nsl = pb->nsl;
   if (pb->sp_reg > 0) {
     ccfg.dynamicSmemBytes = 0;
     if (pb->sp_reg == 8) TDW_CUDA(pb->ctx, cudaLaunchKernelEx(&ccfg, solve_reg_kernel<8>, L.cs));
@@ -1153,7 +1153,7 @@ int launch_solve(tdw_problem* pb, LoopPlan& L, int alpha, cudaStream_t s) {
   if (pb->near_w > 0 && pb->split_lag2) {
     const long long threads = (long long)pb->ns * 32;
     near_step_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(
-        pb->d_ncol_rm, pb->d_nval_rm, pb->near_stride, pb->near_w, pb->ns, pb->kb, pb->d_hist, pb->hcols,
+        pb->d_ncol_rm, pb->d_nval_rm, pb->near_stride, pb->near_w, pb->ns, pb->nsl, pb->d_hist, pb->hcols,
         pb->pad, pb->d_phi, pb->d_bnear, alpha, pb->d_flags);
     TDW_CUDA(pb->ctx, cudaGetLastError());
   }
@@ -1162,13 +1162,14 @@ int launch_solve(tdw_problem* pb, LoopPlan& L, int alpha, cudaStream_t s) {
 
 // Enqueue one complete time loop.  Two streams: the convolution pass P(alpha)
 // of steps alpha..alpha+kb-1 runs on the side stream as soon as the solve of
-// step alpha-2 has finalized the history it reads (times <= alpha-3: full
-// coefficients at lags >= kb+2, known-only ones at lags 2..kb+1 whose unknown
-// part the solves add through the near structure; lag 1 = known data written
-// up front), so P(alpha) overlaps solve(alpha-1) and the solves alpha..alpha+kb-1
-// follow it; per pass the critical path is P + (kb-1) solves.
-//   P(alpha)      waits solve(alpha-2)              writes b[(alpha+i) % 2kb]
-//   solve(s)      waits P(pass of s), solve(s-1)    reads b[s % 2kb], bnear[.][s % (kb+1)]
+// step alpha-1-m (m = overlap) has finalized the history it reads with full
+// coefficients (lags >= nsl+2, nsl = kb+m-1); lags 2..nsl+1 hold known-only
+// coefficients whose unknown part near_step_kernel adds after each solve; lag 1
+// = known data written up front.  P(alpha) thus runs beside the solves
+// alpha-m..alpha-1 and the solves alpha..alpha+kb-1 follow it: per pass the
+// critical path is max(P, m solves) + (kb-m) solves.
+//   P(alpha)      waits solve(alpha-1-m)            writes b[(alpha+i) % (kb+m)]
+//   solve(s)      waits P(pass of s), solve(s-1)    reads b[s % (kb+m)], bnear[.][s % (nsl+1)]
 // Also used under stream capture (one CUDA graph per loop configuration).
 int enqueue_loop(tdw_problem* pb, LoopPlan& L, cudaEvent_t* ev_conv) {
   tdw_ctx* ctx = pb->ctx;
@@ -1185,7 +1186,8 @@ int enqueue_loop(tdw_problem* pb, LoopPlan& L, cudaEvent_t* ev_conv) {
   for (int alpha = 1; alpha < nt; alpha += KB) {
     const int nb = std::min(KB, nt - alpha);
     // convolution pass of steps alpha..alpha+nb-1 on the side stream
-    if (alpha >= 3) TDW_CUDA(ctx, cudaStreamWaitEvent(sc, evS[alpha - 2], 0));
+    const int dep = alpha - 1 - pb->overlap;  // the last solve this pass reads
+    if (dep >= 1) TDW_CUDA(ctx, cudaStreamWaitEvent(sc, evS[dep], 0));
     const int pass = (alpha - 1) / KB;
     if (ev_conv) TDW_CUDA(ctx, cudaEventRecordWithFlags(ev_conv[2 * pass], sc, cudaEventRecordExternal));
     if ((rc = launch_conv(pb, L, alpha, nb, sc))) return rc;
@@ -1196,7 +1198,7 @@ int enqueue_loop(tdw_problem* pb, LoopPlan& L, cudaEvent_t* ev_conv) {
     TDW_CUDA(ctx, cudaStreamWaitEvent(st, evF[alpha], 0));
     for (int s = alpha; s < alpha + nb; ++s) {
       if (L.multi) {
-        double* bb = pb->d_b + (size_t)(s % (2 * KB)) * pb->bstride;
+        double* bb = pb->d_b + (size_t)(s % pb->bring) * pb->bstride;
         ncclResult_t nr = ncclAllGather(bb + pb->b_off, bb, (size_t)pb->rows_per_rank, ncclDouble,
                                         ctx->comm, st);
         if (nr != ncclSuccess)
@@ -1352,7 +1354,7 @@ int tdw_march_emulated_impl(tdw_problem** pbs, int n, double threshold) {
       if (rc) return rc;
     }
     for (int s = alpha; s < alpha + nb; ++s) {
-      const size_t slot = (size_t)(s % (2 * KB));
+      const size_t slot = (size_t)(s % pbs[0]->bring);
       for (int r = 0; r < n; ++r)
         for (int q = 0; q < n; ++q)
           if (q != r)
@@ -1502,7 +1504,8 @@ int tdw_setup_cluster_solver(tdw_problem* pb) {
     for (size_t c = 0; c < cands.size(); ++c) {
       const double conv_r = 16.0 * (double)pb->n_band / (45e3 * (ctx->num_sms - cands[c].cl));
       const double sv = cands[c].solve_us;
-      const double t_res = std::max(conv_r, sv / 0.7) + (pb->kb - 1) * sv;  // 30% margin on the overlap
+      const int m = pb->overlap;
+      const double t_res = std::max(conv_r, m * sv / 0.7) + (pb->kb - m) * sv;  // 30% margin on the overlap
       const double t_ser = conv_full + pb->kb * sv;
       const double t = std::min(t_res, t_ser);
       if (t < best - 1e-9) {
@@ -1561,8 +1564,8 @@ int tdw_setup_cluster_solver(tdw_problem* pb) {
     // row-major near structure for near_step_kernel
     pb->near_stride = std::max(32, (pb->near_w + 31) / 32 * 32);
     TDW_CUDA(ctx, cudaMalloc(&pb->d_ncol_rm, sizeof(int) * (size_t)ns * pb->near_stride));
-    TDW_CUDA(ctx, cudaMalloc(&pb->d_nval_rm, sizeof(double) * (size_t)ns * pb->kb * pb->near_stride));
-    near_rowmajor_kernel<<<2 * ctx->num_sms, 256, 0, ctx->stream>>>(pb->d_ncol, pb->d_nval, ns, pb->kb,
+    TDW_CUDA(ctx, cudaMalloc(&pb->d_nval_rm, sizeof(double) * (size_t)ns * pb->nsl * pb->near_stride));
+    near_rowmajor_kernel<<<2 * ctx->num_sms, 256, 0, ctx->stream>>>(pb->d_ncol, pb->d_nval, ns, pb->nsl,
                                                                    pb->near_stride, pb->near_w,
                                                                    pb->d_ncol_rm, pb->d_nval_rm);
     TDW_CUDA(ctx, cudaGetLastError());

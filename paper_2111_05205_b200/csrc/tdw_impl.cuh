@@ -16,7 +16,8 @@
 #define TDW_CONV_WARPS (TDW_TI / TDW_ROWS_PER_WARP)
 #define TDW_ELL_MAX 64   // max nnz per row of the lag-1 step matrix
 #define TDW_KB_MAX 6     // time steps per convolution pass (temporal blocking)
-#define TDW_NEAR_MAX 192 // max pairs per row in the near structure (bands reaching lags 2..kb+1)
+#define TDW_NEAR_MAX 256 // max pairs per row in the near structure (bands reaching a split lag)
+#define TDW_NSL_MAX (2 * TDW_KB_MAX - 1)  // max split lags
 #define TDW_ELEM_STRIDE 16  // doubles per element record: v0 v1 v2 n c rad
 // Unit layout (one (I-block, J-tile) unit = one contiguous byte range of the store):
 //   [0, 128)        uint32 seg_rel[32]  entry offset of row r's segment in the unit
@@ -93,8 +94,11 @@ struct tdw_problem {
   double* d_phi = nullptr;   // internal order
   // FMM near-field mode: pair filter (adjacent leaf cells), no lag-2 split
   int* d_leafc = nullptr;    // packed leaf-cell coords per element (internal order) or null
-  int split_lag2 = 1;        // lags 2..kb+1 of the store keep the known density only
+  int split_lag2 = 1;        // lags 2..nsl+1 of the store keep the known density only
   int kb = 1;                // time steps per convolution pass (1..TDW_KB_MAX)
+  int overlap = 1;           // solves a convolution pass overlaps (1..kb)
+  int nsl = 1;               // split lags: kb + overlap - 1
+  int bring = 2;             // b ring slots: kb + overlap
   bool skip_empty_units = false;
   struct FmmState* fmm = nullptr;
   // banded store
@@ -121,8 +125,8 @@ struct tdw_problem {
   double* d_aval = nullptr;
   double* d_adiag = nullptr;
   int jac_iters = 0;
-  // near structure: pairs whose band reaches a split lag g in 2..kb+1, all rows,
-  // ELL columns [TDW_NEAR_MAX][ns], values [kb][TDW_NEAR_MAX][ns] (lag g = 2 + index)
+  // near structure: pairs whose band reaches a split lag g in 2..nsl+1, all rows,
+  // ELL columns [TDW_NEAR_MAX][ns], values [nsl][TDW_NEAR_MAX][ns] (lag g = 2 + index)
   int near_w = 0;
   int64_t n_near = 0, n_near_evals = 0;
   int* d_ncol = nullptr;
@@ -131,7 +135,7 @@ struct tdw_problem {
   int near_stride = 0;             // row-major copy for near_step_kernel: [ns][stride], [ns][kb][stride]
   int* d_ncol_rm = nullptr;
   double* d_nval_rm = nullptr;
-  double* d_bnear = nullptr;       // [kb][kb+1][ns]: N_g x^(beta-1) from solve(beta), for step beta-1+g
+  double* d_bnear = nullptr;       // [nsl][nsl+1][ns]: N_g x^(beta-1) after solve(beta), for step beta-1+g
   // pipelined loop: side stream for the far convolution, per-step events
   cudaStream_t side = nullptr;
   std::vector<cudaEvent_t> ev_solve, ev_conv;

@@ -159,16 +159,19 @@ def test_solver_variants_agree(monkeypatch, env):
     assert per_step_rel(h.q, ref.q).max() < 1e-11
 
 
-@pytest.mark.parametrize("kb", [1, 2, 3, 6])
-def test_temporal_block_sizes_match_reference(monkeypatch, kb):
-    """One convolution pass per kb steps (split lags 2..kb+1 corrected by the
-    solves' near terms) reproduces the reference golden march of config 2 for
-    every block size; the default (4) is covered by the golden tests above."""
+@pytest.mark.parametrize("kb,overlap", [(1, 1), (2, 1), (2, 2), (3, 2), (4, 1), (6, 3)])
+def test_temporal_block_sizes_match_reference(monkeypatch, kb, overlap):
+    """One convolution pass per kb steps, running beside `overlap` solves
+    (split lags 2..kb+overlap, their unknown part added by the near terms after
+    each solve), reproduces the reference golden march of config 2 for every
+    block size and overlap; the default (4, 4) is covered by the tests above."""
     g = golden("march_cfg2.npz")
     spec = scenarios.build_spec(2)
     monkeypatch.setenv("TDW_KB", str(kb))
+    monkeypatch.setenv("TDW_OVERLAP", str(overlap))
     store = marching.BandStore(spec).assemble()
-    assert store.info()["steps_per_pass"] == kb
+    inf = store.info()
+    assert inf["steps_per_pass"] == kb and inf["pass_overlap"] == overlap, inf
     h = marching.march(spec, mats=store)
     assert h.status == str(g["status"]) and h.n_steps == int(g["n_steps"])
     assert per_step_rel(h.q[:, g["sub"]], g["unknown_sub"]).max() < TOL[1]
