@@ -274,8 +274,9 @@ def run_ours(args, world, rank, local):
                          "bytes_per_launch": 16.0 * n_band},
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
-            # per loop: init_hist + (conv_kernel + reduce_parts) per pass + one solve per step
-            "gpu_launches": int(args.steps * (1 + 2 * (-(-(nt - 1) // info["steps_per_pass"])) + (nt - 1))),
+            # per loop: init_hist + (conv_kernel + reduce_parts) per pass + (solve +
+            # near_step) per step
+            "gpu_launches": int(args.steps * (1 + 2 * (-(-(nt - 1) // info["steps_per_pass"])) + 2 * (nt - 1))),
             "assembly": {"ms": info["t_assemble_ms"], "evals": info["n_evals"],
                          "evals_per_s": info["n_evals"] / (info["t_fill_ms"] * 1e-3),
                          "metric": "(i,j,gamma) layer-potential evals/s (fill kernel, fp64)"},
