@@ -873,30 +873,36 @@ __global__ void __launch_bounds__(256) near_step_kernel(const int* __restrict__ 
                                                         const double* __restrict__ nval_rm, int nstride,
                                                         int near_w, int ns, int nsl,
                                                         const double2* __restrict__ hist, int hcols,
-                                                        int pad, const double* __restrict__ phi,
-                                                        double* __restrict__ bnear, int alpha,
+                                                        int pad, double* __restrict__ bnear, int alpha,
                                                         const int* flags) {
   if (*(volatile const int*)flags != 0) return;
   const int lane = threadIdx.x & 31;
   const int i = (int)(((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
   if (i >= ns) return;
   const double2* hrow = hist + (size_t)(pad + alpha - 1) * hcols;
-  double acc[TDW_NSL_MAX];
+  constexpr int NCH = TDW_NEAR_MAX / 32;
+  // every load of the row issued up front (latency-bound otherwise): columns,
+  // then the history gathers; padding entries (col = i, value 0) are harmless
+  int jj[NCH];
+  double xv[NCH];
 #pragma unroll
-  for (int g = 0; g < TDW_NSL_MAX; ++g) acc[g] = 0.0;
-  for (int k = lane; k < near_w; k += 32) {
-    const int j = __ldg(ncol_rm + (size_t)i * nstride + k);
-    const double2 h = __ldcg(hrow + j);
-    const double x = __ldg(phi + j) == 1.0 ? h.y : h.x;
+  for (int m = 0; m < NCH; ++m)
+    jj[m] = 32 * m < near_w ? __ldg(ncol_rm + (size_t)i * nstride + 32 * m + lane) : 0;
 #pragma unroll
-    for (int g = 0; g < TDW_NSL_MAX; ++g)
-      if (g < nsl) acc[g] = fma(__ldg(nval_rm + ((size_t)i * nsl + g) * nstride + k), x, acc[g]);
+  for (int m = 0; m < NCH; ++m) {
+    xv[m] = 0.0;
+    if (32 * m < near_w) {
+      const double2 h = __ldcg(hrow + (jj[m] & 0x7fffffff));
+      xv[m] = jj[m] < 0 ? h.y : h.x;  // sign bit: phi_j = 1, the unknown is u
+    }
   }
   const int ring = nsl + 1;
+  for (int g = 0; g < nsl; ++g) {
+    const double* vrow = nval_rm + ((size_t)i * nsl + g) * nstride + lane;
+    double v = 0.0;
 #pragma unroll
-  for (int g = 0; g < TDW_NSL_MAX; ++g) {
-    if (g >= nsl) break;
-    double v = acc[g];
+    for (int m = 0; m < NCH; ++m)
+      if (32 * m < near_w) v = fma(__ldg(vrow + 32 * m), xv[m], v);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULLMASK, v, o);
     if (lane == 0) bnear[((size_t)g * ring + (alpha + 1 + g) % ring) * ns + i] = v;
@@ -904,14 +910,15 @@ __global__ void __launch_bounds__(256) near_step_kernel(const int* __restrict__ 
 }
 
 // row-major copy of the near structure for near_step_kernel
-__global__ void near_rowmajor_kernel(const int* ncol, const double* nval, int ns, int nsl, int nstride,
-                                     int near_w, int* ncol_rm, double* nval_rm) {
+__global__ void near_rowmajor_kernel(const int* ncol, const double* nval, const double* phi, int ns,
+                                     int nsl, int nstride, int near_w, int* ncol_rm, double* nval_rm) {
   const long long n = (long long)ns * nstride;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n;
        e += (long long)gridDim.x * blockDim.x) {
     const int i = (int)(e / nstride), k = (int)(e % nstride);
     const bool on = k < near_w;
-    ncol_rm[e] = on ? ncol[(size_t)k * ns + i] : i;
+    const int j = on ? ncol[(size_t)k * ns + i] : i;
+    ncol_rm[e] = j | (phi[j] == 1.0 ? (int)0x80000000 : 0);
     for (int g = 0; g < nsl; ++g)
       nval_rm[((size_t)i * nsl + g) * nstride + k] =
           on ? nval[(size_t)g * TDW_NEAR_MAX * ns + (size_t)k * ns + i] : 0.0;
@@ -1173,7 +1180,7 @@ int launch_solve(tdw_problem* pb, LoopPlan& L, int alpha, cudaStream_t s) {
     const long long threads = (long long)pb->ns * 32;
     near_step_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(
         pb->d_ncol_rm, pb->d_nval_rm, pb->near_stride, pb->near_w, pb->ns, pb->nsl, pb->d_hist, pb->hcols,
-        pb->pad, pb->d_phi, pb->d_bnear, alpha, pb->d_flags);
+        pb->pad, pb->d_bnear, alpha, pb->d_flags);
     TDW_CUDA(pb->ctx, cudaGetLastError());
   }
   return TDW_OK;
@@ -1584,7 +1591,8 @@ int tdw_setup_cluster_solver(tdw_problem* pb) {
     pb->near_stride = std::max(32, (pb->near_w + 31) / 32 * 32);
     TDW_CUDA(ctx, cudaMalloc(&pb->d_ncol_rm, sizeof(int) * (size_t)ns * pb->near_stride));
     TDW_CUDA(ctx, cudaMalloc(&pb->d_nval_rm, sizeof(double) * (size_t)ns * pb->nsl * pb->near_stride));
-    near_rowmajor_kernel<<<2 * ctx->num_sms, 256, 0, ctx->stream>>>(pb->d_ncol, pb->d_nval, ns, pb->nsl,
+    near_rowmajor_kernel<<<2 * ctx->num_sms, 256, 0, ctx->stream>>>(pb->d_ncol, pb->d_nval, pb->d_phi, ns,
+                                                                   pb->nsl,
                                                                    pb->near_stride, pb->near_w,
                                                                    pb->d_ncol_rm, pb->d_nval_rm);
     TDW_CUDA(ctx, cudaGetLastError());

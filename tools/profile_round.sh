@@ -1,0 +1,11 @@
+# ncu evidence for profiles/: launch list of the bench, full captures of the hot kernels (config 2)
+set -e
+python bench.py --steps 2 --warmup 3 --no-cpu > gpurun_out/bench_plain.log 2>&1
+ncu --metrics gpu__time_duration.sum --clock-control none -c 4000 --csv --log-file gpurun_out/launches.csv \
+    python bench.py --steps 2 --warmup 3 --no-cpu > gpurun_out/ncu_launch.log 2>&1
+python tools/prof_step.py 2 64 > gpurun_out/prof_plain.log 2>&1
+for k in conv_kernel solve_reg_kernel near_step_kernel; do
+  ncu --set full --clock-control none --import-source on -k regex:$k -s 8 -c 1 -o gpurun_out/full_$k \
+      python tools/prof_step.py 2 64 > gpurun_out/ncu_$k.log 2>&1
+done
+ls -la gpurun_out
