@@ -376,6 +376,7 @@ struct NearArgs {
   double* adiag;  // [ns]
   int* flags;     // [4]: [2] max near width, [3] overflow
   int* ell_w;
+  int* ncnt;      // [ns] near entries per row
   unsigned long long* bound_bits;
   unsigned long long* nnz;
   unsigned long long* n_near;
@@ -476,6 +477,7 @@ __global__ void __launch_bounds__(128) near_kernel(NearArgs a) {
   }
   if (lane == 0) {
     a.adiag[i] = diag;
+    a.ncnt[i] = min(cnt, TDW_NEAR_MAX);
     atomicMax(&a.flags[2], cnt);
     atomicMax(a.ell_w, acnt);
     if (cnt > TDW_NEAR_MAX || acnt > TDW_ELL_MAX) atomicExch(&a.flags[3], 1);
@@ -585,6 +587,7 @@ int tdw_assemble_impl(tdw_problem* pb) {
   TDW_CUDA(ctx, cudaMalloc(&pb->d_adiag, sizeof(double) * pb->ns));
   TDW_CUDA(ctx, cudaMalloc(&pb->d_ncol, sizeof(int) * (size_t)TDW_NEAR_MAX * pb->ns));
   TDW_CUDA(ctx, cudaMalloc(&pb->d_nval, sizeof(double) * (size_t)pb->nsl * TDW_NEAR_MAX * pb->ns));
+  TDW_CUDA(ctx, cudaMalloc(&pb->d_ncnt, sizeof(int) * (size_t)pb->ns));
   int* d_ellw = nullptr;
   TDW_CUDA(ctx, cudaMalloc(&d_ellw, sizeof(int)));
   for (;;) {
@@ -611,6 +614,7 @@ int tdw_assemble_impl(tdw_problem* pb) {
   s.adiag = pb->d_adiag;
   s.flags = pb->d_flags;
   s.ell_w = d_ellw;
+  s.ncnt = pb->d_ncnt;
   s.bound_bits = d_cnt + 3;
   s.nnz = d_cnt + 2;
   s.n_near = d_cnt + 5;

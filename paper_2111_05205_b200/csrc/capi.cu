@@ -148,7 +148,7 @@ int tdw_problem_create_impl(tdw_ctx* ctx, const tdw_problem_desc* dsc, tdw_probl
     // a pass waits for the solve overlap+1 steps back and runs beside the last
     // `overlap` solves; the split lags reach kb + overlap
     const char* o = getenv("TDW_OVERLAP");
-    pb->overlap = std::max(1, std::min(pb->kb, o ? atoi(o) : 2));
+    pb->overlap = std::max(1, std::min(pb->kb, o ? atoi(o) : 3));
     pb->nsl = pb->kb + pb->overlap - 1;
     pb->bring = pb->kb + pb->overlap;
   }
@@ -486,7 +486,7 @@ int tdw_problem_destroy(tdw_problem* pb) {
                   pb->d_unit, pb->d_acol, pb->d_aval, pb->d_adiag, pb->d_hist, pb->d_uk,
                   pb->d_qk, pb->d_bpart, pb->d_b, pb->d_x, pb->d_red, pb->d_bar, pb->d_flags,
                   pb->d_rhs, pb->d_sp_rowptr, pb->d_sp_nnzoff, pb->d_sp_col, pb->d_sp_val,
-                  pb->d_ncol, pb->d_nval, pb->d_ncol_packed, pb->d_ncol_rm, pb->d_nval_rm, pb->d_bnear, pb->d_out, pb->d_trace};
+                  pb->d_ncol, pb->d_nval, pb->d_ncol_packed, pb->d_ncnt, pb->d_nptr, pb->d_ncol_rm, pb->d_nval_rm, pb->d_bnear, pb->d_out, pb->d_trace};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (pb->graph_exec) cudaGraphExecDestroy(pb->graph_exec);

@@ -869,59 +869,76 @@ __global__ void __launch_bounds__(reg_threads<MAXNZ>(), 1) solve_reg_kernel(Clus
 // One warp per row over the row-major near structure; x from the history
 // (the unknown component of slot alpha-1).  Runs on the whole GPU between two
 // solves (the convolution pass waits for solves, so the SMs are free).
-__global__ void __launch_bounds__(256) near_step_kernel(const int* __restrict__ ncol_rm,
-                                                        const double* __restrict__ nval_rm, int nstride,
-                                                        int near_w, int ns, int nsl,
-                                                        const double2* __restrict__ hist, int hcols,
-                                                        int pad, double* __restrict__ bnear, int alpha,
-                                                        const int* flags) {
+__device__ __forceinline__ uint64_t policy_keep_l2() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ int ldg_keep(const int* p, uint64_t pol) {
+  int v;
+  asm("ld.global.nc.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ double ldg_keep(const double* p, uint64_t pol) {
+  double v;
+  asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+  return v;
+}
+
+__global__ void __launch_bounds__(256) near_step_kernel(const int* __restrict__ nptr,
+                                                        const int* __restrict__ ncnt,
+                                                        const int* __restrict__ ncol_c,
+                                                        const double* __restrict__ nval_c, long long nnz,
+                                                        int ns, int nsl, const double2* __restrict__ hist,
+                                                        int hcols, int pad, double* __restrict__ bnear,
+                                                        int alpha, const int* flags) {
   if (*(volatile const int*)flags != 0) return;
   const int lane = threadIdx.x & 31;
   const int i = (int)(((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
   if (i >= ns) return;
+  const uint64_t keep = policy_keep_l2();  // the near structure is re-read every step
   const double2* hrow = hist + (size_t)(pad + alpha - 1) * hcols;
+  const int p0 = __ldg(nptr + i), cnt = __ldg(ncnt + i);
   constexpr int NCH = TDW_NEAR_MAX / 32;
   // every load of the row issued up front (latency-bound otherwise): columns,
-  // then the history gathers; padding entries (col = i, value 0) are harmless
+  // then the history gathers
   int jj[NCH];
   double xv[NCH];
 #pragma unroll
-  for (int m = 0; m < NCH; ++m)
-    jj[m] = 32 * m < near_w ? __ldg(ncol_rm + (size_t)i * nstride + 32 * m + lane) : 0;
+  for (int m = 0; m < NCH; ++m) jj[m] = 32 * m + lane < cnt ? ldg_keep(ncol_c + p0 + 32 * m + lane, keep) : 0;
 #pragma unroll
   for (int m = 0; m < NCH; ++m) {
     xv[m] = 0.0;
-    if (32 * m < near_w) {
+    if (32 * m + lane < cnt) {
       const double2 h = __ldcg(hrow + (jj[m] & 0x7fffffff));
       xv[m] = jj[m] < 0 ? h.y : h.x;  // sign bit: phi_j = 1, the unknown is u
     }
   }
   const int ring = nsl + 1;
   for (int g = 0; g < nsl; ++g) {
-    const double* vrow = nval_rm + ((size_t)i * nsl + g) * nstride + lane;
+    const double* vrow = nval_c + (size_t)g * nnz + p0 + lane;
     double v = 0.0;
 #pragma unroll
     for (int m = 0; m < NCH; ++m)
-      if (32 * m < near_w) v = fma(__ldg(vrow + 32 * m), xv[m], v);
+      if (32 * m + lane < cnt) v = fma(ldg_keep(vrow + 32 * m, keep), xv[m], v);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULLMASK, v, o);
     if (lane == 0) bnear[((size_t)g * ring + (alpha + 1 + g) % ring) * ns + i] = v;
   }
 }
 
-// row-major copy of the near structure for near_step_kernel
-__global__ void near_rowmajor_kernel(const int* ncol, const double* nval, const double* phi, int ns,
-                                     int nsl, int nstride, int near_w, int* ncol_rm, double* nval_rm) {
-  const long long n = (long long)ns * nstride;
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n;
+// compact row-major copy of the near structure for near_step_kernel
+__global__ void near_compact_kernel(const int* ncol, const double* nval, const double* phi, int ns, int nsl,
+                                    const int* nptr, const int* ncnt, long long nnz, int* ncol_c,
+                                    double* nval_c) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < (long long)ns * TDW_NEAR_MAX;
        e += (long long)gridDim.x * blockDim.x) {
-    const int i = (int)(e / nstride), k = (int)(e % nstride);
-    const bool on = k < near_w;
-    const int j = on ? ncol[(size_t)k * ns + i] : i;
-    ncol_rm[e] = j | (phi[j] == 1.0 ? (int)0x80000000 : 0);
+    const int i = (int)(e / TDW_NEAR_MAX), k = (int)(e % TDW_NEAR_MAX);
+    if (k >= ncnt[i]) continue;
+    const int j = ncol[(size_t)k * ns + i];
+    ncol_c[nptr[i] + k] = j | (phi[j] == 1.0 ? (int)0x80000000 : 0);
     for (int g = 0; g < nsl; ++g)
-      nval_rm[((size_t)i * nsl + g) * nstride + k] =
-          on ? nval[(size_t)g * TDW_NEAR_MAX * ns + (size_t)k * ns + i] : 0.0;
+      nval_c[(size_t)g * nnz + nptr[i] + k] = nval[(size_t)g * TDW_NEAR_MAX * ns + (size_t)k * ns + i];
   }
 }
 
@@ -1179,8 +1196,8 @@ int launch_solve(tdw_problem* pb, LoopPlan& L, int alpha, cudaStream_t s) {
   if (pb->near_w > 0 && pb->split_lag2) {
     const long long threads = (long long)pb->ns * 32;
     near_step_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(
-        pb->d_ncol_rm, pb->d_nval_rm, pb->near_stride, pb->near_w, pb->ns, pb->nsl, pb->d_hist, pb->hcols,
-        pb->pad, pb->d_bnear, alpha, pb->d_flags);
+        pb->d_nptr, pb->d_ncnt, pb->d_ncol_rm, pb->d_nval_rm, (long long)pb->n_near, pb->ns, pb->nsl,
+        pb->d_hist, pb->hcols, pb->pad, pb->d_bnear, alpha, pb->d_flags);
     TDW_CUDA(pb->ctx, cudaGetLastError());
   }
   return TDW_OK;
@@ -1587,14 +1604,22 @@ int tdw_setup_cluster_solver(tdw_problem* pb) {
     for (int& j : ncol) j = ((j / R) << 24) | (j % R);
     TDW_CUDA(ctx, cudaMalloc(&pb->d_ncol_packed, sizeof(int) * ncol.size()));
     TDW_CUDA(ctx, cudaMemcpy(pb->d_ncol_packed, ncol.data(), sizeof(int) * ncol.size(), cudaMemcpyHostToDevice));
-    // row-major near structure for near_step_kernel
-    pb->near_stride = std::max(32, (pb->near_w + 31) / 32 * 32);
-    TDW_CUDA(ctx, cudaMalloc(&pb->d_ncol_rm, sizeof(int) * (size_t)ns * pb->near_stride));
-    TDW_CUDA(ctx, cudaMalloc(&pb->d_nval_rm, sizeof(double) * (size_t)ns * pb->nsl * pb->near_stride));
-    near_rowmajor_kernel<<<2 * ctx->num_sms, 256, 0, ctx->stream>>>(pb->d_ncol, pb->d_nval, pb->d_phi, ns,
-                                                                   pb->nsl,
-                                                                   pb->near_stride, pb->near_w,
-                                                                   pb->d_ncol_rm, pb->d_nval_rm);
+    // compact row-major near structure for near_step_kernel
+    std::vector<int> cnt(ns), ptr(ns);
+    TDW_CUDA(ctx, cudaMemcpy(cnt.data(), pb->d_ncnt, sizeof(int) * ns, cudaMemcpyDeviceToHost));
+    long long nnz = 0;
+    for (int i = 0; i < ns; ++i) {
+      ptr[i] = (int)nnz;
+      nnz += cnt[i];
+    }
+    pb->n_near = nnz;
+    TDW_CUDA(ctx, cudaMalloc(&pb->d_nptr, sizeof(int) * ns));
+    TDW_CUDA(ctx, cudaMemcpy(pb->d_nptr, ptr.data(), sizeof(int) * ns, cudaMemcpyHostToDevice));
+    TDW_CUDA(ctx, cudaMalloc(&pb->d_ncol_rm, sizeof(int) * std::max(1LL, nnz)));
+    TDW_CUDA(ctx, cudaMalloc(&pb->d_nval_rm, sizeof(double) * std::max(1LL, nnz * pb->nsl)));
+    near_compact_kernel<<<2 * ctx->num_sms, 256, 0, ctx->stream>>>(pb->d_ncol, pb->d_nval, pb->d_phi, ns,
+                                                                  pb->nsl, pb->d_nptr, pb->d_ncnt, nnz,
+                                                                  pb->d_ncol_rm, pb->d_nval_rm);
     TDW_CUDA(ctx, cudaGetLastError());
   }
   TDW_CUDA(ctx, cudaFuncSetAttribute(solve_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -132,7 +132,10 @@ struct tdw_problem {
   int* d_ncol = nullptr;
   double* d_nval = nullptr;
   int* d_ncol_packed = nullptr;    // ncol in the cluster solver's (owner << 24 | local) form
-  int near_stride = 0;             // row-major copy for near_step_kernel: [ns][stride], [ns][kb][stride]
+  // compact row-major copy for near_step_kernel: row i holds ncnt[i] entries at
+  // nptr[i]: columns (sign bit = phi_j) and values [nsl][n_near]
+  int* d_ncnt = nullptr;
+  int* d_nptr = nullptr;
   int* d_ncol_rm = nullptr;
   double* d_nval_rm = nullptr;
   double* d_bnear = nullptr;       // [nsl][nsl+1][ns]: N_g x^(beta-1) after solve(beta), for step beta-1+g
