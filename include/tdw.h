@@ -86,6 +86,7 @@ typedef struct {
   int32_t steps_per_pass;    /* time steps computed per convolution pass (kb)    */
   int32_t near_width;        /* widest row of the near structure                 */
   int32_t pass_overlap;      /* solves a convolution pass runs beside            */
+  int32_t solve_halo;        /* halo depth of the communication-avoiding solver (0: none) */
 } tdw_info;
 
 typedef struct {

@@ -364,6 +364,7 @@ int tdw_problem_info(const tdw_problem* pb, tdw_info* out) {
   out->units_hdr32 = pb->units_hdr32;
   out->steps_per_pass = pb->kb;
   out->pass_overlap = pb->overlap;
+  out->solve_halo = pb->sp_halo;
   out->near_width = pb->near_w;
   return TDW_OK;
 }
@@ -486,7 +487,8 @@ int tdw_problem_destroy(tdw_problem* pb) {
                   pb->d_unit, pb->d_acol, pb->d_aval, pb->d_adiag, pb->d_hist, pb->d_uk,
                   pb->d_qk, pb->d_bpart, pb->d_b, pb->d_x, pb->d_red, pb->d_bar, pb->d_flags,
                   pb->d_rhs, pb->d_sp_rowptr, pb->d_sp_nnzoff, pb->d_sp_col, pb->d_sp_val,
-                  pb->d_ncol, pb->d_nval, pb->d_ncol_packed, pb->d_ncnt, pb->d_nptr, pb->d_ncol_rm, pb->d_nval_rm, pb->d_bnear, pb->d_out, pb->d_trace};
+                  pb->d_ncol, pb->d_nval, pb->d_ncol_packed, pb->d_h_ncomp, pb->d_h_gi, pb->d_h_layer, pb->d_h_nz, pb->d_h_col,
+                  pb->d_h_ngat, pb->d_h_gdst, pb->d_h_gsrc, pb->d_h_val, pb->d_ncnt, pb->d_nptr, pb->d_ncol_rm, pb->d_nval_rm, pb->d_bnear, pb->d_out, pb->d_trace};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (pb->graph_exec) cudaGraphExecDestroy(pb->graph_exec);

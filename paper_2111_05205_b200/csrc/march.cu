@@ -22,6 +22,7 @@
 #include <cstdlib>
 #include <string>
 #include <algorithm>
+#include <unordered_map>
 #include <vector>
 
 #include "tdw_impl.cuh"
@@ -446,6 +447,19 @@ struct ClusterSolveArgs {
   int nsl;                                  // split lags 2..nsl+1
   int guess;                                // 1: start Jacobi from 2 x^(beta-1) - x^(beta-2)
   int check_mask;                           // register solver: convergence test when (it & mask) == 0
+  // halo solver (communication-avoiding sweeps): per CTA, the computed rows (own
+  // rows first, then halo layers 1..h-1) and the gathered rows (layers 1..h)
+  int halo;                                 // h (0: plain register solver)
+  int hT, hE, hG;                           // row slots per CTA, extended-set capacity, gather capacity
+  const int* __restrict__ h_ncomp;          // [CL] computed rows
+  const int* __restrict__ h_gi;             // [CL][hT] global row
+  const int* __restrict__ h_layer;          // [CL][hT]
+  const int* __restrict__ h_nz;             // [CL][hT]
+  const int* __restrict__ h_col;            // [CL][hT][MAXNZ] extended-set local index
+  const double* __restrict__ h_val;         // [CL][hT][MAXNZ]
+  const int* __restrict__ h_ngat;           // [CL] gathered rows
+  const int* __restrict__ h_gdst;           // [CL][hG] local index
+  const int* __restrict__ h_gsrc;           // [CL][hG] (owner CTA << 24) | owner-local row
   const int* __restrict__ sp_rowptr;        // [CL][R+1], relative to the CTA's slice
   const long long* __restrict__ sp_nnzoff;  // [CL+1]
   const int* __restrict__ sp_col;           // packed (owner << 24) | local
@@ -864,6 +878,211 @@ __global__ void __launch_bounds__(reg_threads<MAXNZ>(), 1) solve_reg_kernel(Clus
   trace_mark(tr, 8);
 }
 
+// Communication-avoiding variant of the register solver.  CTA r keeps, besides
+// its own rows (layer 0), the halo rows of layers 1..h of the lag-1 coupling
+// graph.  A round gathers x of layers 1..h from the owners (DSMEM, one cluster
+// barrier) and then runs h Jacobi sweeps locally: sweep s updates the rows of
+// layers <= h-s, which only read rows updated by sweep s-1.  Every row is
+// computed with the owner's operand order, so the iterates are bit-identical
+// to the plain solver's; a round costs one cluster barrier instead of h.
+template <int MAXNZ>
+__global__ void __launch_bounds__(reg_threads<MAXNZ>(), 1) solve_halo_kernel(ClusterSolveArgs a) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  extern __shared__ __align__(16) double hsm[];
+  double* xs0 = hsm;                   // [hE] extended-set x, double buffer
+  double* xs1 = hsm + a.hE;
+  double* ex = hsm + 2 * a.hE;         // [2][hT] own rows, exported to peers
+  __shared__ unsigned long long chk[3][2];
+  __shared__ double shred[64];
+  __shared__ double red2[4];
+  __shared__ int s_stop;
+  if (*(volatile int*)&a.flags[0] != 0) return;
+  const int cr = (int)cl.block_rank();
+  const int CL = (int)cl.num_blocks();
+  const int R = a.R, T = a.hT, H = a.halo;
+  const int r0 = cr * R;
+  const int nr = max(0, min(R, a.ns - r0));
+  const int tid = threadIdx.x;
+  const int ncomp = a.h_ncomp[cr], ngat = a.h_ngat[cr];
+  const bool comp = tid < ncomp;
+  const bool own = tid < nr;
+  const size_t base = (size_t)cr * T + tid;
+  const int gi = comp ? a.h_gi[base] : 0;
+  const int layer = comp ? a.h_layer[base] : H;
+  const int beta0 = a.alpha - 1;
+  unsigned long long* tr = a.trace ? a.trace + (size_t)a.alpha * 16 : nullptr;
+  trace_mark(tr, 0);
+  int c[MAXNZ];
+  double v[MAXNZ];
+  int nz = 0;
+  double bi = 0.0, invd = 0.0, di = 1.0;
+  if (comp) {
+    nz = a.h_nz[base];
+#pragma unroll
+    for (int k = 0; k < MAXNZ; ++k) {
+      c[k] = k < nz ? __ldg(a.h_col + base * MAXNZ + k) : 0;
+      v[k] = k < nz ? __ldg(a.h_val + base * MAXNZ + k) : 0.0;
+    }
+    bi = __ldcg(a.b + gi) + near_in(a, gi);
+    di = a.diag[gi];
+    invd = 1.0 / di;
+    const double x0 = a.guess && a.alpha >= 4 ? jacobi_start(a, gi, bi, di) : bi * invd;
+    xs0[tid] = x0;
+    if (own) {
+      ex[tid] = x0;
+      if (a.rhs) a.rhs[(size_t)beta0 * a.ns + a.perm[gi]] = bi;
+    }
+  }
+  if (tid < 6) chk[tid >> 1][tid & 1] = 0ull;
+  trace_mark(tr, 1);
+  cl.sync();
+  trace_mark(tr, 2);
+  int sweeps = 0, ncheck = 0, p = 0;
+  double* cur = xs0;
+  double* nxt = xs1;
+  const int rounds = (a.maxit + H - 1) / H;
+  for (int rd = 0; rd < rounds; ++rd) {
+    // gather layers 1..h from the owners' exported x (parity p)
+    for (int g = tid; g < ngat; g += blockDim.x) {
+      const int src = __ldg(a.h_gsrc + (size_t)cr * a.hG + g);
+      const double* pe = cl.map_shared_rank(ex + p * T, src >> 24);
+      cur[__ldg(a.h_gdst + (size_t)cr * a.hG + g)] = pe[src & 0xffffff];
+    }
+    __syncthreads();
+    double xn = 0.0, xprev = 0.0;
+    for (int s = 1; s <= H; ++s) {
+      if (comp && layer <= H - s) {
+        double xv[MAXNZ];
+#pragma unroll
+        for (int k = 0; k < MAXNZ; ++k) xv[k] = k < nz ? cur[c[k]] : 0.0;
+        double s0 = bi, s1 = 0.0;
+#pragma unroll
+        for (int k = 0; k < MAXNZ; k += 2) {
+          s0 = fma(-v[k], xv[k], s0);
+          if (k + 1 < MAXNZ) s1 = fma(-v[k + 1], xv[k + 1], s1);
+        }
+        xprev = cur[tid];
+        xn = (s0 + s1) * invd;
+        nxt[tid] = xn;
+      }
+      __syncthreads();
+      double* t = cur;
+      cur = nxt;
+      nxt = t;
+    }
+    sweeps += H;
+    const bool last = rd + 1 == rounds;
+    const bool check = !last;
+    if (check && tid < 2) chk[(ncheck + 1) % 3][tid] = 0ull;
+    if (own) ex[(p ^ 1) * T + tid] = xn;
+    if (check) {
+      double dmax = own ? fabs(xn - xprev) : 0.0, xmax = own ? fabs(xn) : 0.0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        dmax = fmax(dmax, __shfl_xor_sync(FULLMASK, dmax, o));
+        xmax = fmax(xmax, __shfl_xor_sync(FULLMASK, xmax, o));
+      }
+      if ((tid & 31) == 0) {
+        atomicMax(&chk[ncheck % 3][0], (unsigned long long)__double_as_longlong(dmax));
+        atomicMax(&chk[ncheck % 3][1], (unsigned long long)__double_as_longlong(xmax));
+      }
+    }
+    cl.sync();
+    p ^= 1;
+    if (check) {
+      if (tid < 32) {
+        unsigned long long D = 0, X = 0;
+        if (tid < CL) {
+          const unsigned long long* rr = cl.map_shared_rank(&chk[ncheck % 3][0], tid);
+          D = rr[0];
+          X = rr[1];
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          D = max(D, __shfl_xor_sync(FULLMASK, D, o));
+          X = max(X, __shfl_xor_sync(FULLMASK, X, o));
+        }
+        if (tid == 0)
+          s_stop = __longlong_as_double((long long)D) <= 1e-15 * __longlong_as_double((long long)X);
+      }
+      __syncthreads();
+      ++ncheck;
+      if (s_stop) break;
+    }
+  }
+  trace_mark(tr, 3);
+  if (tr && tid == 0 && cr == 0) tr[15] = sweeps;
+  // residual with the final x: own rows from ex[p], layer-1 columns gathered fresh
+  for (int g = tid; g < ngat; g += blockDim.x) {
+    const int src = __ldg(a.h_gsrc + (size_t)cr * a.hG + g);
+    const double* pe = cl.map_shared_rank(ex + p * T, src >> 24);
+    cur[__ldg(a.h_gdst + (size_t)cr * a.hG + g)] = pe[src & 0xffffff];
+  }
+  if (own) cur[tid] = ex[p * T + tid];
+  __syncthreads();
+  double r2 = 0.0, b2 = 0.0, xm = 0.0, xi = 0.0;
+  if (own) {
+    xi = cur[tid];
+    double acc = di * xi - bi;
+#pragma unroll
+    for (int k = 0; k < MAXNZ; ++k) acc = fma(v[k], k < nz ? cur[c[k]] : 0.0, acc);
+    r2 = acc * acc;
+    b2 = bi * bi;
+    xm = fabs(xi);
+  }
+  r2 = block_reduce_sum(r2, shred);
+  b2 = block_reduce_sum(b2, shred);
+  xm = block_reduce_max(xm, shred);
+  if (tid == 0) { red2[0] = r2; red2[1] = b2; red2[2] = xm; }
+  trace_mark(tr, 4);
+  cl.sync();
+  trace_mark(tr, 5);
+  double RR = 0.0, BB = 0.0, XM = 0.0;
+  if (tid < 32) {
+    if (tid < CL) {
+      const double* rr = cl.map_shared_rank(red2, tid);
+      RR = rr[0];
+      BB = rr[1];
+      XM = rr[2];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      RR += __shfl_xor_sync(FULLMASK, RR, o);
+      BB += __shfl_xor_sync(FULLMASK, BB, o);
+      XM = fmax(XM, __shfl_xor_sync(FULLMASK, XM, o));
+    }
+    if (tid == 0) { shred[0] = RR; shred[1] = BB; shred[2] = XM; }
+  }
+  trace_mark(tr, 6);
+  cl.sync();  // no CTA leaves while another may still read its shared memory
+  trace_mark(tr, 7);
+  RR = shred[0];
+  BB = shred[1];
+  XM = shred[2];
+  if (sqrt(RR) > 1e-10 * fmax(sqrt(BB), 1e-300)) {
+    if (cr == 0 && tid == 0) {
+      a.flags[2] = a.alpha;
+      atomicExch(&a.flags[0], 2);
+    }
+    return;
+  }
+  const bool unstable = XM > a.threshold;
+  if (own) {
+    const int o = a.perm[gi];
+    const double ph = a.phi[gi];
+    const size_t kb = (size_t)beta0 * a.ns + o;
+    const double qv = ph == 1.0 ? a.qk[kb] : xi;
+    const double uv = ph == 1.0 ? xi : a.uk[kb];
+    a.hist[(size_t)(a.pad + beta0) * a.hcols + gi] = make_double2(qv, uv);
+  }
+  if (cr == 0 && tid == 0) {
+    a.flags[1] = a.alpha;
+    if (unstable) atomicExch(&a.flags[0], 1);
+  }
+  trace_mark(tr, 8);
+}
+
 // Near terms of the density x^(alpha-1) just solved, for the steps alpha-1+g,
 // g = 2..nsl+1: bnear[g-2][(alpha+g-1) % (nsl+1)][i] = sum_k N^g_ik x_col(k).
 // One warp per row over the row-major near structure; x from the history
@@ -1132,6 +1351,19 @@ int make_plan(tdw_problem* pb, LoopPlan& L, double threshold, bool want_rhs) {
   cs.R = pb->sp_R;
   cs.maxit = pb->jac_iters;
   cs.trace = pb->d_trace;
+  cs.halo = pb->sp_halo;
+  cs.hT = pb->sp_hT;
+  cs.hE = pb->sp_hE;
+  cs.hG = pb->sp_hG;
+  cs.h_ncomp = pb->d_h_ncomp;
+  cs.h_gi = pb->d_h_gi;
+  cs.h_layer = pb->d_h_layer;
+  cs.h_nz = pb->d_h_nz;
+  cs.h_col = pb->d_h_col;
+  cs.h_val = pb->d_h_val;
+  cs.h_ngat = pb->d_h_ngat;
+  cs.h_gdst = pb->d_h_gdst;
+  cs.h_gsrc = pb->d_h_gsrc;
 
   return TDW_OK;
 }
@@ -1185,7 +1417,12 @@ int launch_solve(tdw_problem* pb, LoopPlan& L, int alpha, cudaStream_t s) {
     const char* c = getenv("TDW_CHECK_EVERY");
     L.cs.check_mask = (c ? atoi(c) : 4) <= 2 ? 1 : 3;
   }
-  if (pb->sp_reg > 0) {
+  if (pb->sp_reg > 0 && pb->sp_halo > 0) {
+    ccfg.dynamicSmemBytes = pb->sp_hsmem;
+    if (pb->sp_reg == 8) TDW_CUDA(pb->ctx, cudaLaunchKernelEx(&ccfg, solve_halo_kernel<8>, L.cs));
+    else if (pb->sp_reg == 16) TDW_CUDA(pb->ctx, cudaLaunchKernelEx(&ccfg, solve_halo_kernel<16>, L.cs));
+    else TDW_CUDA(pb->ctx, cudaLaunchKernelEx(&ccfg, solve_halo_kernel<24>, L.cs));
+  } else if (pb->sp_reg > 0) {
     ccfg.dynamicSmemBytes = 0;
     if (pb->sp_reg == 8) TDW_CUDA(pb->ctx, cudaLaunchKernelEx(&ccfg, solve_reg_kernel<8>, L.cs));
     else if (pb->sp_reg == 16) TDW_CUDA(pb->ctx, cudaLaunchKernelEx(&ccfg, solve_reg_kernel<16>, L.cs));
@@ -1472,6 +1709,124 @@ int tdw_outputs(tdw_problem* pb, double* u, double* q, double* tau, double* sigm
   return TDW_OK;
 }
 
+// Halo sets of the communication-avoiding register solver (host, once per
+// problem).  For CTA c: layer 0 = its own rows; layer l+1 = the columns of the
+// layer-l rows not in an earlier layer.  The computed rows (layers 0..h-1, one
+// per thread, own rows first) keep the owner's operand order; the extended set
+// (layers 0..h) indexes the CTA's shared-memory x.  The largest h <= 4 that
+// fits the thread count and shared memory is used (env TDW_HALO=0 disables,
+// TDW_HALO=h caps it); h = 1 would equal the plain solver, so h >= 2.
+static int setup_halo(tdw_problem* pb, const std::vector<int>& acol, const std::vector<double>& aval) {
+  tdw_ctx* ctx = pb->ctx;
+  const int ns = pb->ns, CL = pb->sp_cl, R = pb->sp_R, MZ = pb->sp_reg;
+  const int T = MZ == 8 ? 1024 : (MZ == 16 ? 512 : 256);
+  pb->sp_halo = 0;
+  const char* env = getenv("TDW_HALO");
+  const int hmax = env ? std::min(4, atoi(env)) : 4;
+  if (hmax < 2 || CL < 2) return TDW_OK;
+  auto cols_of = [&](int i, std::vector<int>& out) {
+    out.clear();
+    for (int k = 0; k < pb->ell_w; ++k) {
+      const int j = acol[(size_t)k * ns + i];
+      if (j != i) out.push_back(j);
+    }
+  };
+  std::vector<int> layer(ns, -1), cols;
+  for (int h = hmax; h >= 2; --h) {
+    const int E_cap = 8192;
+    std::vector<std::vector<int>> ext(CL), extl(CL);
+    std::vector<int> ncomp(CL), ngat(CL);
+    bool fits = true;
+    size_t maxE = 0, maxG = 0;
+    for (int c = 0; c < CL && fits; ++c) {
+      std::vector<int>& E = ext[c];
+      std::vector<int>& EL = extl[c];
+      const int lo = c * R, hi = std::min(ns, (c + 1) * R);
+      for (int i = lo; i < hi; ++i) { layer[i] = 0; E.push_back(i); EL.push_back(0); }
+      size_t begin = 0;
+      for (int l = 1; l <= h; ++l) {
+        const size_t end = E.size();
+        std::vector<int> add;
+        for (size_t q = begin; q < end; ++q) {
+          cols_of(E[q], cols);
+          for (int j : cols)
+            if (layer[j] < 0) { layer[j] = l; add.push_back(j); }
+        }
+        std::sort(add.begin(), add.end());
+        E.insert(E.end(), add.begin(), add.end());
+        EL.insert(EL.end(), add.size(), l);
+        begin = end;
+        if (l == h - 1) ncomp[c] = (int)E.size();
+      }
+      ngat[c] = (int)E.size() - (hi - lo);
+      for (int j : E) layer[j] = -1;  // reset for the next CTA
+      if (ncomp[c] > T || (int)E.size() > E_cap) fits = false;
+      maxE = std::max(maxE, E.size());
+      maxG = std::max(maxG, (size_t)ngat[c]);
+    }
+    if (!fits) continue;
+    // arrays
+    const int hE = (int)((maxE + 31) / 32 * 32), hG = (int)std::max<size_t>(1, maxG);
+    std::vector<int> h_gi((size_t)CL * T, 0), h_layer((size_t)CL * T, h), h_nz((size_t)CL * T, 0);
+    std::vector<int> h_col((size_t)CL * T * MZ, 0), h_gdst((size_t)CL * hG, 0), h_gsrc((size_t)CL * hG, 0);
+    std::vector<double> h_val((size_t)CL * T * MZ, 0.0);
+    for (int c = 0; c < CL; ++c) {
+      const std::vector<int>& E = ext[c];
+      std::unordered_map<int, int> loc;
+      loc.reserve(E.size() * 2);
+      for (size_t q = 0; q < E.size(); ++q) loc[E[q]] = (int)q;
+      const int lo = c * R, nown = std::min(ns, (c + 1) * R) - lo;
+      const std::vector<int>& lay = extl[c];
+      for (int t = 0; t < ncomp[c]; ++t) {
+        const int i = E[t];
+        const size_t base = (size_t)c * T + t;
+        h_gi[base] = i;
+        h_layer[base] = lay[t];
+        int n = 0;
+        for (int k = 0; k < pb->ell_w; ++k) {
+          const int j = acol[(size_t)k * ns + i];
+          if (j == i) continue;
+          if (n >= MZ) return tdw_fail(ctx, TDW_ERR_LIMIT, "halo solver: row wider than the register budget");
+          h_col[base * MZ + n] = loc.at(j);
+          h_val[base * MZ + n] = aval[(size_t)k * ns + i];
+          ++n;
+        }
+        h_nz[base] = n;
+      }
+      for (int g = 0; g < ngat[c]; ++g) {
+        const int q = nown + g, j = E[q];
+        h_gdst[(size_t)c * hG + g] = q;
+        h_gsrc[(size_t)c * hG + g] = ((j / R) << 24) | (j % R);
+      }
+    }
+    auto up = [&](int** d, const std::vector<int>& h) -> int {
+      TDW_CUDA(ctx, cudaMalloc(d, sizeof(int) * h.size()));
+      TDW_CUDA(ctx, cudaMemcpy(*d, h.data(), sizeof(int) * h.size(), cudaMemcpyHostToDevice));
+      return TDW_OK;
+    };
+    int rc = 0;
+    if ((rc = up(&pb->d_h_ncomp, ncomp)) || (rc = up(&pb->d_h_gi, h_gi)) || (rc = up(&pb->d_h_layer, h_layer)) ||
+        (rc = up(&pb->d_h_nz, h_nz)) || (rc = up(&pb->d_h_col, h_col)) || (rc = up(&pb->d_h_ngat, ngat)) ||
+        (rc = up(&pb->d_h_gdst, h_gdst)) || (rc = up(&pb->d_h_gsrc, h_gsrc)))
+      return rc;
+    TDW_CUDA(ctx, cudaMalloc(&pb->d_h_val, sizeof(double) * h_val.size()));
+    TDW_CUDA(ctx, cudaMemcpy(pb->d_h_val, h_val.data(), sizeof(double) * h_val.size(), cudaMemcpyHostToDevice));
+    pb->sp_halo = h;
+    pb->sp_hT = T;
+    pb->sp_hE = hE;
+    pb->sp_hG = hG;
+    pb->sp_hsmem = sizeof(double) * (2 * (size_t)hE + 2 * (size_t)T);
+    auto attr = [&](const void* f) {
+      return cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pb->sp_hsmem);
+    };
+    TDW_CUDA(ctx, attr((const void*)solve_halo_kernel<8>));
+    TDW_CUDA(ctx, attr((const void*)solve_halo_kernel<16>));
+    TDW_CUDA(ctx, attr((const void*)solve_halo_kernel<24>));
+    return TDW_OK;
+  }
+  return TDW_OK;
+}
+
 // Partition the lag-1 step matrix over a thread-block cluster (host, once per
 // problem): smallest CL in {1,2,4,8,16} whose per-CTA slice fits in shared memory.
 int tdw_setup_cluster_solver(tdw_problem* pb) {
@@ -1624,7 +1979,14 @@ int tdw_setup_cluster_solver(tdw_problem* pb) {
   }
   TDW_CUDA(ctx, cudaFuncSetAttribute(solve_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)pb->sp_smem));
+  if (pb->sp_reg > 0) {
+    int rc = setup_halo(pb, acol, aval);
+    if (rc) return rc;
+  }
   if (CL > 8) {
+    TDW_CUDA(ctx, cudaFuncSetAttribute(solve_halo_kernel<8>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    TDW_CUDA(ctx, cudaFuncSetAttribute(solve_halo_kernel<16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    TDW_CUDA(ctx, cudaFuncSetAttribute(solve_halo_kernel<24>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     TDW_CUDA(ctx, cudaFuncSetAttribute(solve_cluster_kernel,
                                        cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     TDW_CUDA(ctx, cudaFuncSetAttribute(solve_reg_kernel<8>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));

@@ -174,6 +174,12 @@ struct tdw_problem {
   long long* d_sp_nnzoff = nullptr;
   int* d_sp_col = nullptr;
   double* d_sp_val = nullptr;
+  // halo (communication-avoiding) variant of the register solver
+  int sp_halo = 0, sp_hT = 0, sp_hE = 0, sp_hG = 0;
+  size_t sp_hsmem = 0;
+  int *d_h_ncomp = nullptr, *d_h_gi = nullptr, *d_h_layer = nullptr, *d_h_nz = nullptr;
+  int *d_h_col = nullptr, *d_h_ngat = nullptr, *d_h_gdst = nullptr, *d_h_gsrc = nullptr;
+  double* d_h_val = nullptr;
   bool use_graph = true;
   double t_assemble_ms = 0.0, t_fill_ms = 0.0;
 };

@@ -140,11 +140,13 @@ def test_header_widths_agree(monkeypatch):
 
 
 @pytest.mark.parametrize("env", ["TDW_SOLVER=smem+TDW_SOLVE_CL=2", "TDW_SOLVER=smem+TDW_SOLVE_CL=4",
-                                 "TDW_SOLVER=smem+TDW_SOLVE_CL=16", "TDW_SOLVER=reg"])
+                                 "TDW_SOLVER=smem+TDW_SOLVE_CL=16", "TDW_SOLVER=reg+TDW_HALO=0",
+                                 "TDW_SOLVER=reg+TDW_HALO=2", "TDW_SOLVER=reg+TDW_HALO=3"])
 def test_solver_variants_agree(monkeypatch, env):
-    """Every cluster solver the step-time model can pick (register-resident, or
-    shared-memory at 2..16 CTAs; at 2 and 4 CTAs a thread owns several of the
-    2560 / 1280 rows) converges to the same densities on config 2."""
+    """Every cluster solver the step-time model can pick (register-resident with
+    or without halo rounds, or shared-memory at 2..16 CTAs; at 2 and 4 CTAs a
+    thread owns several of the 2560 / 1280 rows) converges to the same densities
+    on config 2."""
     spec = scenarios.build_spec(2)
     ref = marching.march(spec)
     for kv in env.split("+"):
@@ -181,6 +183,26 @@ def test_temporal_block_sizes_match_reference(monkeypatch, kb, overlap):
     for key in ("u", "q"):
         mask = np.linalg.norm(r[key], axis=1) > 0
         assert per_step_rel(getattr(hm, key)[mask], r[key][mask]).max() < TOL[3], key
+
+
+def test_halo_solver_is_bit_identical(monkeypatch):
+    """The communication-avoiding solver (h sweeps per cluster barrier, halo rows
+    recomputed with the owner's operand order) runs the same Jacobi iterates as
+    the plain register solver: with h = 2 and the plain solver testing
+    convergence every 2 sweeps, the densities agree bit for bit."""
+    spec = scenarios.build_spec(2)
+    monkeypatch.setenv("TDW_SOLVER", "reg")
+    monkeypatch.setenv("TDW_CHECK_EVERY", "2")
+    monkeypatch.setenv("TDW_HALO", "0")
+    plain = marching.BandStore(spec).assemble()
+    assert plain.info()["solve_halo"] == 0
+    hp = marching.march(spec, mats=plain)
+    monkeypatch.setenv("TDW_HALO", "2")
+    halo = marching.BandStore(spec).assemble()
+    assert halo.info()["solve_halo"] == 2
+    hh = marching.march(spec, mats=halo)
+    np.testing.assert_array_equal(hh.q, hp.q)
+    np.testing.assert_array_equal(hh.u, hp.u)
 
 
 def test_window_off_is_equivalent():

@@ -36,7 +36,7 @@ for r in range(rounds):
         conv = st.time_conv(20)
         res[v].append((sps, conv * 1e3))
         print(f"cfg{cfg} {v} round {r}: steps/s {sps:.1f}  conv-only {conv*1e3:.2f}us "
-              f"grid {inf['conv_grid']} S {inf['conv_splits']} solve_cluster {inf['solve_cluster']} kb {inf['steps_per_pass']} near_w {inf['near_width']}", flush=True)
+              f"grid {inf['conv_grid']} S {inf['conv_splits']} solve_cluster {inf['solve_cluster']} kb {inf['steps_per_pass']} near_w {inf['near_width']} halo {inf['solve_halo']}", flush=True)
         st.close()
 for v in variants:
     print(f"{v}: best steps/s {max(s for s, _ in res[v]):.1f}  best conv {min(c for _, c in res[v]):.2f}us")
