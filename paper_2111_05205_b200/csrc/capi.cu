@@ -148,7 +148,7 @@ int tdw_problem_create_impl(tdw_ctx* ctx, const tdw_problem_desc* dsc, tdw_probl
     // a pass waits for the solve overlap+1 steps back and runs beside the last
     // `overlap` solves; the split lags reach kb + overlap
     const char* o = getenv("TDW_OVERLAP");
-    pb->overlap = std::max(1, std::min(pb->kb, o ? atoi(o) : 3));
+    pb->overlap = std::max(1, std::min(pb->kb, o ? atoi(o) : pb->kb));
     pb->nsl = pb->kb + pb->overlap - 1;
     pb->bring = pb->kb + pb->overlap;
   }

@@ -1104,7 +1104,7 @@ __device__ __forceinline__ double ldg_keep(const double* p, uint64_t pol) {
   return v;
 }
 
-__global__ void __launch_bounds__(256) near_step_kernel(const int* __restrict__ nptr,
+__global__ void __launch_bounds__(128, 16) near_step_kernel(const int* __restrict__ nptr,
                                                         const int* __restrict__ ncnt,
                                                         const int* __restrict__ ncol_c,
                                                         const double* __restrict__ nval_c, long long nnz,
@@ -1432,7 +1432,7 @@ int launch_solve(tdw_problem* pb, LoopPlan& L, int alpha, cudaStream_t s) {
   }
   if (pb->near_w > 0 && pb->split_lag2) {
     const long long threads = (long long)pb->ns * 32;
-    near_step_kernel<<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(
+    near_step_kernel<<<(unsigned)((threads + 127) / 128), 128, 0, s>>>(
         pb->d_nptr, pb->d_ncnt, pb->d_ncol_rm, pb->d_nval_rm, (long long)pb->n_near, pb->ns, pb->nsl,
         pb->d_hist, pb->hcols, pb->pad, pb->d_bnear, alpha, pb->d_flags);
     TDW_CUDA(pb->ctx, cudaGetLastError());
