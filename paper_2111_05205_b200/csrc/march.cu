@@ -123,6 +123,7 @@ struct ConvArgs {
   const int* __restrict__ flags;
   int hcols, pad, ns, rows_loc, ntiles, S, alpha, nstages, wbox;
   int l2hint;            // L2 eviction-priority hints on the unit stream / history box
+  unsigned long long* stats;  // optional (TDW_CONV_STATS): iterations, lane entries, per-row lmax histogram
   unsigned stage_bytes;  // shared-memory FIFO capacity
 };
 
@@ -301,6 +302,26 @@ __global__ void __launch_bounds__(TDW_CONV_THREADS, 1)
         }
       }
       lmax = __reduce_max_sync(FULLMASK, lmax);
+      if (a.stats) {
+        int tot = 0, mx = 0, mn = 1 << 30;
+#pragma unroll
+        for (int r = 0; r < TDW_ROWS_PER_WARP; ++r) {
+          tot += len[r];
+          const int m1 = __reduce_max_sync(FULLMASK, len[r]), n1 = __reduce_min_sync(FULLMASK, len[r]);
+          mx += m1;
+          mn = min(mn, n1);
+          if (lane == 0) atomicAdd(a.stats + 8 + min(m1, 31), 1ull);
+        }
+        tot = __reduce_add_sync(FULLMASK, tot);
+        if (lane == 0) {
+          constexpr int UKs = KB == 1 ? 4 : (KB == 2 ? 4 : KB);
+          atomicAdd(a.stats + 0, (unsigned long long)((lmax + UKs - 1) / UKs * UKs));
+          atomicAdd(a.stats + 1, (unsigned long long)tot);
+          atomicAdd(a.stats + 2, (unsigned long long)mx);
+          atomicAdd(a.stats + 3, (unsigned long long)mn);
+          atomicAdd(a.stats + 4, 1ull);
+        }
+      }
       // unrolled by a multiple of KB: the window rotation then maps onto
       // register renaming (no moves); the shift and the multiply-adds run
       // unconditionally (a finished lane multiplies zero coefficients with its
@@ -1676,6 +1697,25 @@ int tdw_time_conv_impl(tdw_problem* pb, int n, float* ms_out) {
   TDW_CUDA(ctx, cudaEventCreate(&e0));
   TDW_CUDA(ctx, cudaEventCreate(&e1));
   dim3 grid(pb->conv_grid);
+  if (getenv("TDW_CONV_STATS")) {  // iteration statistics of the consumer k-loop
+    unsigned long long* dstats = nullptr;
+    TDW_CUDA(ctx, cudaMalloc(&dstats, sizeof(unsigned long long) * 40));
+    TDW_CUDA(ctx, cudaMemsetAsync(dstats, 0, sizeof(unsigned long long) * 40, st));
+    c.stats = dstats;
+    conv_launch(pb->kb, grid, smem, st, c, hmap);
+    unsigned long long h[40];
+    TDW_CUDA(ctx, cudaMemcpyAsync(h, dstats, sizeof(h), cudaMemcpyDeviceToHost, st));
+    TDW_CUDA(ctx, cudaStreamSynchronize(st));
+    const double wu = (double)std::max(1ull, h[4]);
+    fprintf(stderr, "conv stats: warp-units %llu, iterations/warp-unit %.2f, lane-entries/warp-unit %.1f, "
+            "lmax/row %.2f, min lmin/warp %.2f, slot use %.3f\nlmax histogram:", h[4], h[0] / wu, h[1] / wu,
+            h[2] / (TDW_ROWS_PER_WARP * wu), h[3] / wu, h[1] / (32.0 * TDW_ROWS_PER_WARP * std::max(1ull, h[0])));
+    for (int k = 0; k < 32; ++k)
+      if (h[8 + k]) fprintf(stderr, " %d:%llu", k, h[8 + k]);
+    fprintf(stderr, "\n");
+    cudaFree(dstats);
+    c.stats = nullptr;
+  }
   conv_launch(pb->kb, grid, smem, st, c, hmap);  // warm-up
   TDW_CUDA(ctx, cudaEventRecord(e0, st));
   for (int k = 0; k < n; ++k) conv_launch(pb->kb, grid, smem, st, c, hmap);
