@@ -11,7 +11,7 @@ from pathlib import Path
 
 import numpy as np
 
-LIB_PATH = Path(__file__).resolve().parent / "libtdw.so"
+LIB_PATH = Path(os.environ.get("TDW_LIB_PATH") or Path(__file__).resolve().parent / "libtdw.so")
 
 TDW_OK = 0
 _ERRORS = {1: ValueError, 2: ValueError, 3: RuntimeError, 4: RuntimeError, 5: RuntimeError,
