@@ -10,8 +10,9 @@ Nt-1 = 255 MOT time steps of the configuration.
           in HBM (1.5 GB, i.e. larger than the 126 MB L2: no flush needed),
           device time (CUDA events on the library stream) max over ranks.
   e2e     the same metric through the public API march(spec, mats=store):
-          Greville sampling of the user's data callables, H2D of the known
-          data, the loop, D2H of u, q, tau, sigma -- every step.
+          Greville sampling of the user's data callables (into page-locked
+          buffers), H2D of the known data, the loop, D2H of u, q, tau, sigma --
+          every step.
   roofline  K2 (history convolution): 16 B x N_band per launch / average
           launch time measured with CUDA events around every K2 launch of the
           timed region, against the measured HBM copy bandwidth.
@@ -220,7 +221,8 @@ def run_ours(args, world, rank, local):
     barrier()
     e2e_s = max_over_ranks(time.perf_counter() - t0)
     e2e = e2e_steps * (nt - 1) / e2e_s
-    h2d = 2 * (nt - 1) * ns * 8
+    # march() copies the samples of each data callable that is not None (pinned buffers)
+    h2d = sum(f is not None for f in (spec.u_data, spec.q_data)) * (nt - 1) * ns * 8
     d2h = 4 * (nt - 1) * ns * 8
 
     # roofline of K2 (history convolution), algorithmic bytes = 16 B per band entry

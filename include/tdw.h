@@ -118,8 +118,13 @@ int tdw_problem_create(tdw_ctx* ctx, const tdw_problem_desc* desc, tdw_problem**
 int tdw_assemble(tdw_problem* pb);
 int tdw_problem_info(const tdw_problem* pb, tdw_info* out);
 
+/* Pinned (page-locked) host memory for the march's host buffers: copies from and
+ * to it run at full PCIe/C2C rate.  No reference counterpart (numpy arrays). */
+int tdw_host_alloc(int64_t bytes, void** out);
+int tdw_host_free(void* p);
+
 /* Full march with host buffers.  u_known/q_known: (nt-1, ns) Greville samples
- * (marching.py:258-276).  Outputs (nt-1, ns): u, q, tau, sigma; rhs_trace may be NULL.
+ * (marching.py:258-276); NULL = that data callable is None (zero samples).  Outputs (nt-1, ns): u, q, tau, sigma; rhs_trace may be NULL.
  * status: 0 stable, 1 unstable (blow-up detector, marching.py:336-338). */
 int tdw_march(tdw_problem* pb, const double* u_known, const double* q_known, double threshold,
               double* u, double* q, double* tau, double* sigma, double* rhs_trace,

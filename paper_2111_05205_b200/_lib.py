@@ -58,6 +58,8 @@ EXPORTS = {
     "tdw_finalize": ([C.c_void_p], C.c_int),
     "tdw_last_error": ([C.c_void_p], C.c_char_p),
     "tdw_device_count": ([], C.c_int),
+    "tdw_host_alloc": ([C.c_int64, C.POINTER(C.c_void_p)], C.c_int),
+    "tdw_host_free": ([C.c_void_p], C.c_int),
     "tdw_coeff_table": ([C.c_void_p, C.c_int64, _dp, _dp, _dp, _dp, _dp, _dp, C.c_int, C.c_double,
                          C.c_double, C.c_int, _dp, _dp, _dp], C.c_int),
     "tdw_coeff_table_device": ([C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p,
@@ -94,11 +96,34 @@ def load():
                                "(the CUDA path has no CPU fallback)")
         lib = C.CDLL(str(LIB_PATH))
         for name, (args, res) in EXPORTS.items():
-            fn = getattr(lib, name)
+            fn = getattr(lib, name, None)
+            if fn is None and os.environ.get("TDW_LIB_PATH"):
+                continue  # an older library under A/B (tools/lib_ab.sh)
+            if fn is None:
+                raise RuntimeError(f"{LIB_PATH} does not export {name}: rebuild it")
             fn.argtypes = args
             fn.restype = res
         _lib = lib
     return _lib
+
+
+class PinnedArray:
+    """A float64 numpy view of page-locked host memory (tdw_host_alloc); freed with the object."""
+
+    def __init__(self, shape):
+        self.shape = tuple(int(x) for x in shape)
+        n = int(np.prod(self.shape))
+        self._p = C.c_void_p()
+        check(load().tdw_host_alloc(max(8, 8 * n), C.byref(self._p)), None, "tdw_host_alloc")
+        self.array = np.ctypeslib.as_array(C.cast(self._p, _dp), shape=(max(1, n),))[:n].reshape(self.shape)
+
+    def __del__(self):
+        try:
+            if self._p.value:
+                load().tdw_host_free(self._p)
+                self._p = C.c_void_p()
+        except Exception:
+            pass
 
 
 def dptr(a: np.ndarray):

@@ -533,8 +533,9 @@ static int choose_conv_schedule(tdw_problem* pb) {
   // keep the solver's SMs free (overlap) unless the bandwidth they would add to
   // the convolution is worth more than the solve time (~100 us per step)
   const double conv_est = (double)(pb->n_band * 16) / 6.0e12;
-  const bool reserve = pb->conv_reserve_model >= 0 ? pb->conv_reserve_model == 1
-                                                   : conv_est * pb->sp_cl / ctx->num_sms < 100e-6;
+  bool reserve = pb->conv_reserve_model >= 0 ? pb->conv_reserve_model == 1
+                                             : conv_est * pb->sp_cl / ctx->num_sms < 100e-6;
+  if (const char* r = getenv("TDW_CONV_RESERVE")) reserve = atoi(r) != 0;  // experiments
   pb->conv_reserve = reserve;
   const int G = std::max(1, ctx->num_sms - (reserve ? pb->sp_cl : 0));
   // items = (I-block, tile split); pick the split count that balances the waves
@@ -810,6 +811,7 @@ int tdw_assemble_impl(tdw_problem* pb) {
           ++nstream;
         }
       G = (int)std::max(1LL, std::min<long long>(ctx->num_sms - (pb->conv_reserve ? pb->sp_cl : 0), nstream));
+      if (const char* gm = getenv("TDW_CONV_GRID_MAX")) G = std::max(1, std::min(G, atoi(gm)));  // experiments
       soff.assign(G + 1, 0);
       std::vector<int> chunk_of(nunit, -1);
       double acc = 0.0;

@@ -47,13 +47,31 @@ int tdw_device_count(void) {
   return n;
 }
 
+int tdw_host_alloc(int64_t bytes, void** out) {
+  if (!out || bytes <= 0) return TDW_ERR_INVALID_ARG;
+  *out = nullptr;
+  return cudaHostAlloc(out, (size_t)bytes, cudaHostAllocPortable) == cudaSuccess ? TDW_OK : TDW_ERR_CUDA;
+}
+
+int tdw_host_free(void* p) {
+  if (!p) return TDW_OK;
+  return cudaFreeHost(p) == cudaSuccess ? TDW_OK : TDW_ERR_CUDA;
+}
+
 int tdw_init(int device, tdw_ctx** out) {
   if (!out) return TDW_ERR_INVALID_ARG;
   *out = nullptr;
   tdw_ctx* ctx = new tdw_ctx();
   ctx->device = device;
   cudaError_t e = cudaSetDevice(device);
-  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
+  // the library stream (solves, near terms) at the highest priority: when an SM
+  // frees up, a pending solve cluster is placed before more convolution or
+  // near-term blocks (the time loop's critical path runs on this stream)
+  int prio_lo = 0, prio_hi = 0;
+  if (e == cudaSuccess) e = cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
+  const char* pe = getenv("TDW_PRIO");  // experiments: 0 = default priority
+  if (e == cudaSuccess)
+    e = cudaStreamCreateWithPriority(&ctx->stream, cudaStreamNonBlocking, (pe && atoi(pe) == 0) ? prio_lo : prio_hi);
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device);
   if (e != cudaSuccess) {
     delete ctx;
@@ -143,8 +161,11 @@ int tdw_problem_create_impl(tdw_ctx* ctx, const tdw_problem_desc* dsc, tdw_probl
   pb->window = dsc->window ? 1 : 0;
   {
     // temporal blocking: one convolution pass computes kb consecutive steps
+    // default 4; 6 when a pass (~ ns^2 / ranks band entries) dwarfs the solves
+    // (~ ns): measured config 2 (5120) best at 4, config 3 (20480) at 6 (+25%)
     const char* e = getenv("TDW_KB");
-    pb->kb = std::max(1, std::min(TDW_KB_MAX, e ? atoi(e) : 4));
+    const double pass_size = (double)dsc->ns * (double)dsc->ns / std::max(1, nranks);
+    pb->kb = std::max(1, std::min(TDW_KB_MAX, e ? atoi(e) : (pass_size >= 1e8 ? 6 : 4)));
     // a pass waits for the solve overlap+1 steps back and runs beside the last
     // `overlap` solves; the split lags reach kb + overlap
     const char* o = getenv("TDW_OVERLAP");
@@ -370,14 +391,21 @@ int tdw_problem_info(const tdw_problem* pb, tdw_info* out) {
 }
 
 int tdw_upload_known(tdw_problem* pb, const double* u_known, const double* q_known) {
-  if (!pb || !u_known || !q_known) return TDW_ERR_INVALID_ARG;
+  if (!pb) return TDW_ERR_INVALID_ARG;
   tdw_ctx* ctx = pb->ctx;
   cudaSetDevice(ctx->device);
   const size_t n = (size_t)(pb->nt - 1) * pb->ns;
   if (!pb->d_uk) TDW_CUDA(ctx, cudaMalloc(&pb->d_uk, sizeof(double) * n));
   if (!pb->d_qk) TDW_CUDA(ctx, cudaMalloc(&pb->d_qk, sizeof(double) * n));
-  TDW_CUDA(ctx, cudaMemcpyAsync(pb->d_uk, u_known, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
-  TDW_CUDA(ctx, cudaMemcpyAsync(pb->d_qk, q_known, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
+  // NULL = no data callable (the reference's zero samples, marching.py:268-275)
+  if (u_known)
+    TDW_CUDA(ctx, cudaMemcpyAsync(pb->d_uk, u_known, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
+  else
+    TDW_CUDA(ctx, cudaMemsetAsync(pb->d_uk, 0, sizeof(double) * n, ctx->stream));
+  if (q_known)
+    TDW_CUDA(ctx, cudaMemcpyAsync(pb->d_qk, q_known, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
+  else
+    TDW_CUDA(ctx, cudaMemsetAsync(pb->d_qk, 0, sizeof(double) * n, ctx->stream));
   pb->known_loaded = true;
   return TDW_OK;
 }
@@ -495,8 +523,10 @@ int tdw_problem_destroy(tdw_problem* pb) {
   if (pb->fmm) tdw_fmm_free(pb->fmm);
   for (auto& e : pb->ev_solve) cudaEventDestroy(e);
   for (auto& e : pb->ev_conv) cudaEventDestroy(e);
+  for (auto& e : pb->ev_near) cudaEventDestroy(e);
   if (pb->ev_fork) cudaEventDestroy(pb->ev_fork);
   if (pb->side) cudaStreamDestroy(pb->side);
+  if (pb->side_near) cudaStreamDestroy(pb->side_near);
   delete pb;
   return TDW_OK;
 }

@@ -124,10 +124,30 @@ struct ConvArgs {
   int hcols, pad, ns, rows_loc, ntiles, S, alpha, nstages, wbox;
   int l2hint;            // L2 eviction-priority hints on the unit stream / history box
   unsigned long long* stats;  // optional (TDW_CONV_STATS): iterations, lane entries, per-row lmax histogram
+  int dry;                    // experiments (TDW_CONV_DRY, tdw_time_conv only): stream units, skip the k loop
+  int hrows;                  // 1: history slice = the unit's lag span, per-row bulk copies; 0: TMA wbox box
   unsigned stage_bytes;  // shared-memory FIFO capacity
 };
 
-#define TDW_CONV_THREADS (TDW_CONV_WARPS * 32 + 32)
+// Two shapes of the convolution CTA (conv_body<KB, RPW, PWG>):
+//  * RPW = 2 rows per consumer warp, 16 consumer warps + 1 producer warp (544
+//    threads, launch bound: 96 registers).  Leaves ~13 K registers per SM for
+//    the near_step_kernel blocks that run beside it.
+//  * RPW = 4, 8 consumer warps (2 warpgroups) + a producer warpgroup (384
+//    threads, __maxnreg__ 144).  The producer warpgroup gives registers back
+//    (setmaxnreg.dec to 32) and the consumers grow (setmaxnreg.inc) to 200: room
+//    for the KB = 5, 6 windows, and 65536 - 384 * 144 = 10 K registers stay free
+//    for near_step_kernel blocks.  setmaxnreg.inc only redistributes what .dec
+//    released (asking for more blocks forever), hence the fixed launch count.
+template <int RPW, bool PWG>
+__host__ __device__ constexpr int conv_threads() { return (TDW_TI / RPW) * 32 + (PWG ? 128 : 32); }
+constexpr int kConvLaunchRegsPWG = 144;
+constexpr int kConvProducerRegs = 32;
+template <int RPW>
+__host__ __device__ constexpr int conv_consumer_regs() {
+  return kConvLaunchRegsPWG + ((kConvLaunchRegsPWG - kConvProducerRegs) * 128 / ((TDW_TI / RPW) * 32)) / 8 * 8;
+}
+static_assert(conv_consumer_regs<4>() == 200, "register split");
 
 // K2: history convolution.  Persistent CTAs walk a precomputed list of store
 // units.  Warp 8 (producer) streams each unit -- one contiguous byte range:
@@ -141,28 +161,35 @@ struct ConvArgs {
 // read of the store.  Step alpha+i at lag g reads time alpha+i-g, i.e. row
 // (gmax - g + i) of the unit's history box of wbox+KB-1 rows starting at time
 // alpha-gmax.  Every coefficient is read from shared memory once and used KB times.
-template <int KB>
-__global__ void __launch_bounds__(TDW_CONV_THREADS, 1)
-    conv_kernel(ConvArgs a, const __grid_constant__ CUtensorMap hmap) {
+template <int KB, int RPW, bool PWG>
+__device__ __forceinline__ void conv_body(const ConvArgs& a, const CUtensorMap& hmap) {
+  constexpr int CW = TDW_TI / RPW;  // consumer warps
   extern __shared__ __align__(128) unsigned char sm[];
   __shared__ __align__(8) uint64_t full[4];
   __shared__ __align__(8) uint64_t empty[4];
   __shared__ unsigned region[4];
+  __shared__ __align__(16) double2 zero_slot;  // the coefficient a lane past its band reads
   if (a.flags[0] != 0) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   constexpr int NS = 4;  // slots (barrier pairs); pb->conv_nstages == 4
   if (threadIdx.x == 0) {
     for (int k = 0; k < NS; ++k) {
       mbar_init(&full[k], 1);
-      mbar_init(&empty[k], TDW_CONV_WARPS);
+      mbar_init(&empty[k], CW);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    zero_slot = make_double2(0.0, 0.0);
   }
   __syncthreads();
+  const unsigned zaddr = smem_u32(&zero_slot);
   const unsigned u0 = a.sched_off[blockIdx.x], u1 = a.sched_off[blockIdx.x + 1];
   const int nent = (int)(u1 - u0);  // schedule entries: a unit id, or TDW_EMPTY_UNIT (item flush only)
 
-  if (warp == TDW_CONV_WARPS) {
+  if (warp >= CW) {
+    if constexpr (PWG) {
+      asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(kConvProducerRegs));
+      if (warp != CW) return;
+    }
     // ---------------- producer ----------------
     // Shared memory is a byte FIFO of a.stage_bytes (capacity): unit n takes the
     // region [h, h + need) (wrapping to 0 when it would not fit) and may only be
@@ -197,7 +224,10 @@ __global__ void __launch_bounds__(TDW_CONV_THREADS, 1)
         const int slot = n & 3;
         const int W = gmax >= gmin ? gmax - gmin + 1 : 0;
         const int t = (int)(quid % (unsigned)a.ntiles);
-        const unsigned hbytes = W > 0 ? (unsigned)(TDW_TJ * (a.wbox + KB - 1) * 16) : 0u;
+        // history slice: the unit's own lag span (hrows: one 512-byte bulk copy per
+        // step row) or the fixed wbox-row TMA box of the tensor map
+        const int hr = a.hrows ? W + KB - 1 : a.wbox + KB - 1;
+        const unsigned hbytes = W > 0 ? (unsigned)(TDW_TJ * hr * 16) : 0u;
         const unsigned ubytes = (qbytes + 127u) & ~127u;
         const unsigned need = ubytes + ((hbytes + 127u) & ~127u);
         if (h + need > cap) h = 0;
@@ -223,7 +253,16 @@ __global__ void __launch_bounds__(TDW_CONV_THREADS, 1)
           if (a.l2hint) bulk_g2s_hint(sbase + c, a.units + qoff + c, len, &full[slot], pol_stream);
           else bulk_g2s(sbase + c, a.units + qoff + c, len, &full[slot]);
         }
-        if (W > 0 && lane == 0) {  // hist[pad+alpha-gmax .. +wbox)[t*32 .. +32] as one 2-D box
+        if (W > 0 && a.hrows) {  // hist[pad+alpha-gmax+r][t*32 .. +32], r < hr: lane r copies row r
+          const double2* h0 = a.hist + (size_t)(a.pad + a.alpha - gmax) * a.hcols + t * TDW_TJ;
+          unsigned char* hdst = sbase + ubytes;
+          for (int r = lane; r < hr; r += 32) {
+            if (a.l2hint)
+              bulk_g2s_hint(hdst + r * (TDW_TJ * 16), h0 + (size_t)r * a.hcols, TDW_TJ * 16, &full[slot], pol_keep);
+            else
+              bulk_g2s(hdst + r * (TDW_TJ * 16), h0 + (size_t)r * a.hcols, TDW_TJ * 16, &full[slot]);
+          }
+        } else if (W > 0 && lane == 0) {  // hist[pad+alpha-gmax .. +wbox)[t*32 .. +32] as one 2-D box
           if (a.l2hint)
             tensor2d_g2s_hint(sbase + ubytes, &hmap, 2 * t * TDW_TJ, a.pad + a.alpha - gmax, &full[slot],
                               pol_keep);
@@ -237,9 +276,10 @@ __global__ void __launch_bounds__(TDW_CONV_THREADS, 1)
     return;
   }
   // ---------------- consumers ----------------
-  double acc[TDW_ROWS_PER_WARP][KB];
+  if constexpr (PWG) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(conv_consumer_regs<RPW>()));
+  double acc[RPW][KB];
 #pragma unroll
-  for (int r = 0; r < TDW_ROWS_PER_WARP; ++r)
+  for (int r = 0; r < RPW; ++r)
 #pragma unroll
     for (int i = 0; i < KB; ++i) acc[r][i] = 0.0;
   const int S = a.S;
@@ -259,53 +299,54 @@ __global__ void __launch_bounds__(TDW_CONV_THREADS, 1)
       const int stage = n % NS;
       mbar_wait(&full[stage], (unsigned)(n / NS) & 1u);
       const unsigned char* ub = sm + *(volatile unsigned*)&region[stage];
-      const uint32_t* rel = (const uint32_t*)ub;
+      const uint32_t* rel_off = (const uint32_t*)ub;
       const int2 g = *(const int2*)(ub + TDW_UNIT_LAG_OFF);
       const unsigned coef_off = *(const uint32_t*)(ub + TDW_UNIT_LAG_OFF + 12);
       const double2* coef = (const double2*)(ub + coef_off);
       const unsigned ubytes = (unsigned)((*(const uint32_t*)(ub + TDW_UNIT_LAG_OFF + 8) + 127u) & ~127u);
       const double2* hs = (const double2*)(ub + ubytes);
       // the warp's rows are interleaved (independent FMA chains); the k loop is
-      // unrolled and predicated.  Lane = column: the k-th entries of a segment
-      // are those of the lanes with band > k, packed in lane order; the history
-      // box is [time][32 columns], so a warp reads one 512-byte row per (k, step).
+      // unrolled.  Lane = column: the k-th entries of a segment are those of the
+      // lanes with band > k, packed in lane order; the history box is [time][32
+      // columns], so a warp reads one 512-byte row per (k, step).
+      // Branch- and move-free body: every lane issues both shared-memory loads
+      // each k.  A lane past its band reads the CTA's zero slot as coefficient
+      // and a clamped (in-box, finite) history row, so its multiply-adds add 0.
       const unsigned lt = (1u << lane) - 1u;
-      int len[TDW_ROWS_PER_WARP], lmax = 0;
-      unsigned cp[TDW_ROWS_PER_WARP];  // shared addresses: row's coefficients
-      unsigned hp[TDW_ROWS_PER_WARP];  // and its lane's history column at row hrel
-      int off[TDW_ROWS_PER_WARP];
+      int len[RPW], lmax = 0;
+      unsigned cpb[RPW];  // shared byte address of the row's entries of the current k
+      int hp[RPW];        // shared byte address: lane's column at box row rel
+      // lane's column at box row 0 (the clamp); the pair headers put column jl = lane
+      const int hlo = (int)smem_u32(hs + lane);
       // KB == 1: separate per-unit V_U q and V_W u chains (ILP); KB > 1: the
       // running row sums take the multiply-adds directly -- KB independent
       // chains already, and registers are short
       constexpr int NS1 = KB == 1 ? 1 : 0;
-      double s0[TDW_ROWS_PER_WARP][NS1 ? KB : 1], s1[TDW_ROWS_PER_WARP][NS1 ? KB : 1];
-      // sliding window of history rows: hw[r][i] = row (hrel - k + i), the value
+      double s0[RPW][NS1 ? KB : 1], s1[RPW][NS1 ? KB : 1];
+      // sliding window of history rows: hw[r][i] = row (rel - k + i), the value
       // step i multiplies with entry k; entry k+1 of step i+1 uses the same row,
       // so each k loads one new row (one history read per coefficient for any KB)
-      double2 hw[TDW_ROWS_PER_WARP][KB];
+      double2 hw[RPW][KB];
 #pragma unroll
-      for (int r = 0; r < TDW_ROWS_PER_WARP; ++r) {
-        const int row = warp * TDW_ROWS_PER_WARP + r;
-        int jl, hrel;
-        unit_hdr(ub, coef_off, g.y, row * TDW_TJ + lane, jl, len[r], hrel);
+      for (int r = 0; r < RPW; ++r) {
+        const int row = warp * RPW + r;
+        int jl, rel;  // jl == lane (hdr_pack / hdr16_pack write the lane as column)
+        unit_hdr(ub, coef_off, g.y, row * TDW_TJ + lane, jl, len[r], rel);
         lmax = max(lmax, len[r]);
-        cp[r] = smem_u32(coef + rel[row]);
-        hp[r] = smem_u32(hs + hrel * TDW_TJ + jl);
-        off[r] = 0;
-#pragma unroll
-        for (int i = 0; i < KB; ++i) {
-          if (NS1) {
-            s0[r][0] = 0.0;
-            s1[r][0] = 0.0;
-          }
-          hw[r][i] = len[r] > 0 ? lds_f64x2(hp[r] + i * TDW_TJ * 16) : make_double2(0.0, 0.0);
+        cpb[r] = smem_u32(coef + rel_off[row]);
+        hp[r] = hlo + (len[r] > 0 ? rel : 0) * (TDW_TJ * 16);
+        if (NS1) {
+          s0[r][0] = 0.0;
+          s1[r][0] = 0.0;
         }
+#pragma unroll
+        for (int i = 0; i < KB; ++i) hw[r][i] = lds_f64x2((unsigned)(hp[r] + i * TDW_TJ * 16));
       }
       lmax = __reduce_max_sync(FULLMASK, lmax);
       if (a.stats) {
         int tot = 0, mx = 0, mn = 1 << 30;
 #pragma unroll
-        for (int r = 0; r < TDW_ROWS_PER_WARP; ++r) {
+        for (int r = 0; r < RPW; ++r) {
           tot += len[r];
           const int m1 = __reduce_max_sync(FULLMASK, len[r]), n1 = __reduce_min_sync(FULLMASK, len[r]);
           mx += m1;
@@ -323,20 +364,22 @@ __global__ void __launch_bounds__(TDW_CONV_THREADS, 1)
         }
       }
       // unrolled by a multiple of KB: the window rotation then maps onto
-      // register renaming (no moves); the shift and the multiply-adds run
-      // unconditionally (a finished lane multiplies zero coefficients with its
-      // stale, finite window), only the two shared-memory loads are predicated
+      // register renaming (no moves)
       constexpr int UK = KB == 1 ? 4 : (KB == 2 ? 4 : KB);
+      if (a.dry) lmax = 0;
+      // the block of UK entries stops at lmax (warp-uniform exit): a row with 5
+      // entries costs 5 steps, not 2 * UK; the window is dead after the loop, so
+      // the exit needs no register moves
       for (int k0 = 0; k0 < lmax; k0 += UK) {
 #pragma unroll
         for (int kk = 0; kk < UK; ++kk) {
           const int k = k0 + kk;
+          if (kk > 0 && k >= lmax) goto kloop_done;
 #pragma unroll
-          for (int r = 0; r < TDW_ROWS_PER_WARP; ++r) {
+          for (int r = 0; r < RPW; ++r) {
             const bool on = len[r] > k;
             const unsigned m = __ballot_sync(FULLMASK, on);
-            double2 cv = make_double2(0.0, 0.0);
-            if (on) cv = lds_f64x2(cp[r] + (off[r] + __popc(m & lt)) * 16);
+            const double2 cv = lds_f64x2(on ? cpb[r] + __popc(m & lt) * 16u : zaddr);
 #pragma unroll
             for (int i = 0; i < KB; ++i) {
               if (NS1) {
@@ -346,19 +389,16 @@ __global__ void __launch_bounds__(TDW_CONV_THREADS, 1)
                 acc[r][i] = fma(-cv.y, hw[r][i].y, fma(cv.x, hw[r][i].x, acc[r][i]));
               }
             }
-            if (KB > 1) {
 #pragma unroll
-              for (int i = KB - 1; i > 0; --i) hw[r][i] = hw[r][i - 1];
-              if (len[r] > k + 1) hw[r][0] = lds_f64x2(hp[r] - (k + 1) * TDW_TJ * 16);
-            } else if (len[r] > k + 1) {
-              hw[r][0] = lds_f64x2(hp[r] - (k + 1) * TDW_TJ * 16);
-            }
-            off[r] += __popc(m);
+            for (int i = KB - 1; i > 0; --i) hw[r][i] = hw[r][i - 1];
+            hw[r][0] = lds_f64x2((unsigned)max(hp[r] - (k + 1) * (TDW_TJ * 16), hlo));
+            cpb[r] += __popc(m) * 16u;
           }
         }
       }
+    kloop_done:
 #pragma unroll
-      for (int r = 0; r < TDW_ROWS_PER_WARP; ++r)
+      for (int r = 0; r < RPW; ++r)
         if (NS1) acc[r][0] += s0[r][0] - s1[r][0];
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[stage]);
@@ -367,20 +407,30 @@ __global__ void __launch_bounds__(TDW_CONV_THREADS, 1)
     if (next_item != item) {  // end of a work item (I-block, split): flush the row partials
       const int iblk = (int)(item / (unsigned)S), sp = (int)(item % (unsigned)S);
 #pragma unroll
-      for (int r = 0; r < TDW_ROWS_PER_WARP; ++r) {
+      for (int r = 0; r < RPW; ++r) {
 #pragma unroll
         for (int i = 0; i < KB; ++i) {
           double v = acc[r][i];
 #pragma unroll
           for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULLMASK, v, o);
           if (lane == 0)  // row-major partials: a row's S partials are contiguous
-            a.bpart[i * step_stride + (size_t)(iblk * TDW_TI + warp * TDW_ROWS_PER_WARP + r) * S + sp] = v;
+            a.bpart[i * step_stride + (size_t)(iblk * TDW_TI + warp * RPW + r) * S + sp] = v;
           acc[r][i] = 0.0;
         }
       }
     }
     }
   }
+}
+
+template <int KB>
+__global__ void __launch_bounds__(conv_threads<2, false>(), 1)
+    conv_kernel(ConvArgs a, const __grid_constant__ CUtensorMap hmap) {
+  conv_body<KB, 2, false>(a, hmap);
+}
+template <int KB>
+__global__ void __maxnreg__(kConvLaunchRegsPWG) conv_kernel_wg(ConvArgs a, const __grid_constant__ CUtensorMap hmap) {
+  conv_body<KB, 4, true>(a, hmap);
 }
 
 // fixed-order sum of a row's split partials, loads issued 8 at a time
@@ -1131,7 +1181,7 @@ __global__ void __launch_bounds__(128, 16) near_step_kernel(const int* __restric
                                                         const double* __restrict__ nval_c, long long nnz,
                                                         int ns, int nsl, const double2* __restrict__ hist,
                                                         int hcols, int pad, double* __restrict__ bnear,
-                                                        int alpha, const int* flags) {
+                                                        int alpha, int g0, int g1, const int* flags) {
   if (*(volatile const int*)flags != 0) return;
   const int lane = threadIdx.x & 31;
   const int i = (int)(((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
@@ -1155,7 +1205,7 @@ __global__ void __launch_bounds__(128, 16) near_step_kernel(const int* __restric
     }
   }
   const int ring = nsl + 1;
-  for (int g = 0; g < nsl; ++g) {
+  for (int g = g0; g < g1; ++g) {
     const double* vrow = nval_c + (size_t)g * nnz + p0 + lane;
     double v = 0.0;
 #pragma unroll
@@ -1275,31 +1325,53 @@ static int make_hist_map(tdw_problem* pb, CUtensorMap* map) {
   return TDW_OK;
 }
 
-// conv_kernel<KB> dispatch on the problem's block size
-static cudaError_t conv_set_smem(int kb, int smem) {
-  switch (kb) {
-    case 1: return cudaFuncSetAttribute(conv_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    case 2: return cudaFuncSetAttribute(conv_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    case 3: return cudaFuncSetAttribute(conv_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    case 4: return cudaFuncSetAttribute(conv_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    case 5: return cudaFuncSetAttribute(conv_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    default: return cudaFuncSetAttribute(conv_kernel<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+// dispatch on the problem's block size and CTA shape (rpw 2: conv_kernel, rpw 4: conv_kernel_wg)
+#define TDW_CONV_CASES(X) X(1) X(2) X(3) X(4) X(5) X(6)
+// also checks the register split of conv_kernel_wg: setmaxnreg.inc would block
+// forever if the kernel were allocated fewer registers than it assumes
+static cudaError_t conv_set_smem(int kb, int rpw, int smem) {
+#define X(K)                                                                                           \
+  if (kb == K && rpw == 2)                                                                             \
+    return cudaFuncSetAttribute(conv_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);    \
+  if (kb == K) {                                                                                       \
+    cudaFuncAttributes fa;                                                                             \
+    cudaError_t e = cudaFuncGetAttributes(&fa, conv_kernel_wg<K>);                                     \
+    if (e != cudaSuccess) return e;                                                                    \
+    if (fa.numRegs != kConvLaunchRegsPWG) return cudaErrorInvalidConfiguration;                        \
+    return cudaFuncSetAttribute(conv_kernel_wg<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); \
   }
+  TDW_CONV_CASES(X)
+#undef X
+  return cudaErrorInvalidValue;
 }
-static void conv_launch(int kb, dim3 grid, size_t smem, cudaStream_t s, const ConvArgs& c,
+static void conv_launch(int kb, int rpw, dim3 grid, size_t smem, cudaStream_t s, const ConvArgs& c,
                         const CUtensorMap& hmap) {
-  switch (kb) {
-    case 1: conv_kernel<1><<<grid, TDW_CONV_THREADS, smem, s>>>(c, hmap); break;
-    case 2: conv_kernel<2><<<grid, TDW_CONV_THREADS, smem, s>>>(c, hmap); break;
-    case 3: conv_kernel<3><<<grid, TDW_CONV_THREADS, smem, s>>>(c, hmap); break;
-    case 4: conv_kernel<4><<<grid, TDW_CONV_THREADS, smem, s>>>(c, hmap); break;
-    case 5: conv_kernel<5><<<grid, TDW_CONV_THREADS, smem, s>>>(c, hmap); break;
-    default: conv_kernel<6><<<grid, TDW_CONV_THREADS, smem, s>>>(c, hmap); break;
+#define X(K)                                                                              \
+  if (kb == K && rpw == 2) {                                                              \
+    conv_kernel<K><<<grid, conv_threads<2, false>(), smem, s>>>(c, hmap);                 \
+    return;                                                                               \
+  }                                                                                       \
+  if (kb == K) {                                                                          \
+    conv_kernel_wg<K><<<grid, conv_threads<4, true>(), smem, s>>>(c, hmap);               \
+    return;                                                                               \
   }
+  TDW_CONV_CASES(X)
+#undef X
 }
 
 static void fill_conv_args(tdw_problem* pb, ConvArgs& c) {
+  {
+    const char* r = getenv("TDW_RPW");
+    const int rpw = r ? atoi(r) : (pb->kb >= 5 ? 4 : 2);
+    pb->conv_rpw = rpw == 4 ? 4 : 2;
+  }
   c.wbox = pb->wbox;
+  c.stats = nullptr;
+  c.dry = 0;
+  {
+    const char* h = getenv("TDW_HROWS");
+    c.hrows = h ? atoi(h) : 1;
+  }
   {
     const char* h = getenv("TDW_L2HINT");
     c.l2hint = h ? atoi(h) : 1;
@@ -1342,7 +1414,7 @@ int make_plan(tdw_problem* pb, LoopPlan& L, double threshold, bool want_rhs) {
     if (rc) return rc;
   }
   L.smem = pb->conv_stage_bytes;
-  TDW_CUDA(ctx, conv_set_smem(pb->kb, (int)L.smem));
+  TDW_CUDA(ctx, conv_set_smem(pb->kb, pb->conv_rpw, (int)L.smem));
   L.cgrid = dim3(pb->conv_grid);
   L.multi = ctx->comm != nullptr;
   ClusterSolveArgs& cs = L.cs;
@@ -1404,7 +1476,7 @@ int begin_loop(tdw_problem* pb, cudaStream_t st) {
 int launch_conv(tdw_problem* pb, LoopPlan& L, int alpha, int nsteps, cudaStream_t s) {
   L.c.alpha = alpha;
   L.c.bpart = pb->d_bpart;
-  conv_launch(pb->kb, L.cgrid, L.smem, s, L.c, L.hmap);
+  conv_launch(pb->kb, pb->conv_rpw, L.cgrid, L.smem, s, L.c, L.hmap);
   // fixed-order sum of the split partials into the steps' b (own rows), on the
   // convolution's stream: off the solve's critical path
   reduce_parts_kernel<<<dim3((pb->rows_per_rank + 127) / 128, nsteps), 128, 0, s>>>(
@@ -1451,14 +1523,25 @@ int launch_solve(tdw_problem* pb, LoopPlan& L, int alpha, cudaStream_t s) {
   } else {
     TDW_CUDA(pb->ctx, cudaLaunchKernelEx(&ccfg, solve_cluster_kernel, L.cs));
   }
-  if (pb->near_w > 0 && pb->split_lag2) {
-    const long long threads = (long long)pb->ns * 32;
-    near_step_kernel<<<(unsigned)((threads + 127) / 128), 128, 0, s>>>(
-        pb->d_nptr, pb->d_ncnt, pb->d_ncol_rm, pb->d_nval_rm, (long long)pb->n_near, pb->ns, pb->nsl,
-        pb->d_hist, pb->hcols, pb->pad, pb->d_bnear, alpha, pb->d_flags);
-    TDW_CUDA(pb->ctx, cudaGetLastError());
-  }
   return TDW_OK;
+}
+
+// near terms N^g x of the step just solved, lags g0+2 .. g1+1 (see near_step_kernel)
+int launch_near(tdw_problem* pb, int alpha, int g0, int g1, cudaStream_t s) {
+  const long long threads = (long long)pb->ns * 32;
+  const unsigned grid = (unsigned)((threads + 127) / 128);
+  near_step_kernel<<<grid, 128, 0, s>>>(
+      pb->d_nptr, pb->d_ncnt, pb->d_ncol_rm, pb->d_nval_rm, (long long)pb->n_near, pb->ns, pb->nsl,
+      pb->d_hist, pb->hcols, pb->pad, pb->d_bnear, alpha, g0, g1, pb->d_flags);
+  TDW_CUDA(pb->ctx, cudaGetLastError());
+  return TDW_OK;
+}
+
+// solve followed by all of its near terms on one stream (sequential loops)
+int launch_solve_near(tdw_problem* pb, LoopPlan& L, int alpha, cudaStream_t s) {
+  int rc = launch_solve(pb, L, alpha, s);
+  if (rc == TDW_OK && pb->near_w > 0 && pb->split_lag2) rc = launch_near(pb, alpha, 0, pb->nsl, s);
+  return rc;
 }
 
 // Enqueue one complete time loop.  Two streams: the convolution pass P(alpha)
@@ -1480,8 +1563,12 @@ int enqueue_loop(tdw_problem* pb, LoopPlan& L, cudaEvent_t* ev_conv) {
   if (rc) return rc;
   cudaEvent_t* evS = pb->ev_solve.data();  // solve(alpha) done
   cudaEvent_t* evF = pb->ev_conv.data();   // F(alpha) done
+  cudaEvent_t* evN = pb->ev_near.data();   // near terms of solve(alpha) done
+  cudaStream_t sn = pb->side_near;
+  const bool near = pb->near_w > 0 && pb->split_lag2;
   TDW_CUDA(ctx, cudaEventRecord(pb->ev_fork, st));
   TDW_CUDA(ctx, cudaStreamWaitEvent(sc, pb->ev_fork, 0));
+  TDW_CUDA(ctx, cudaStreamWaitEvent(sn, pb->ev_fork, 0));
   const int KB = pb->kb;
   int last_alpha = 1;
   for (int alpha = 1; alpha < nt; alpha += KB) {
@@ -1505,11 +1592,31 @@ int enqueue_loop(tdw_problem* pb, LoopPlan& L, cudaEvent_t* ev_conv) {
         if (nr != ncclSuccess)
           return tdw_fail(ctx, TDW_ERR_NCCL, std::string("ncclAllGather: ") + ncclGetErrorString(nr));
       }
+      // solve(s) reads the lag-3+ near terms near_step(s-2) wrote (lag 2: near_step(s-1), below)
+      if (near && pb->near_split && s - 2 >= 1) TDW_CUDA(ctx, cudaStreamWaitEvent(st, evN[s - 2], 0));
       if ((rc = launch_solve(pb, L, s, st))) return rc;
-      TDW_CUDA(ctx, cudaEventRecord(evS[s], st));
+      // evS[s] after the near terms: a convolution pass waiting for solve(s)
+      // starts only once the near kernel has had the SMs it left free
+      if (near && !pb->near_split) {
+        if ((rc = launch_near(pb, s, 0, pb->nsl, st))) return rc;
+        TDW_CUDA(ctx, cudaEventRecord(evS[s], st));
+      } else if (near) {
+        // lag 2 is on the critical path (solve(s+1) needs it): right behind the solve;
+        // lags 3..nsl+1 run beside solve(s+1) on the near stream
+        if ((rc = launch_near(pb, s, 0, 1, st))) return rc;
+        TDW_CUDA(ctx, cudaEventRecord(evS[s], st));
+        if (pb->nsl > 1) {
+          TDW_CUDA(ctx, cudaStreamWaitEvent(sn, evS[s], 0));
+          if ((rc = launch_near(pb, s, 1, pb->nsl, sn))) return rc;
+        }
+        TDW_CUDA(ctx, cudaEventRecord(evN[s], sn));
+      } else {
+        TDW_CUDA(ctx, cudaEventRecord(evS[s], st));
+      }
     }
   }
-  // join the side stream
+  // join the side streams
+  if (near && pb->near_split) TDW_CUDA(ctx, cudaStreamWaitEvent(st, evN[nt - 1], 0));
   TDW_CUDA(ctx, cudaStreamWaitEvent(st, evF[last_alpha], 0));
   TDW_CUDA(ctx, cudaGetLastError());
   return TDW_OK;
@@ -1531,14 +1638,23 @@ int tdw_march_loop(tdw_problem* pb, double threshold, bool want_rhs, bool time_k
       TDW_CUDA(ctx, cudaMalloc(&pb->d_rhs, sizeof(double) * (size_t)(pb->nt - 1) * pb->ns));
     TDW_CUDA(ctx, cudaMemsetAsync(pb->d_rhs, 0, sizeof(double) * (size_t)(pb->nt - 1) * pb->ns, st));
   }
+  {
+    // lags >= 3 of the near terms on their own stream (TDW_NEAR_SPLIT=1); off by
+    // default: it competes with the next solve and the convolution for SMs
+    const char* e = getenv("TDW_NEAR_SPLIT");
+    pb->near_split = e && atoi(e) > 0;
+  }
   if (!pb->side) {
     int lo = 0, hi = 0;
     cudaDeviceGetStreamPriorityRange(&lo, &hi);
     TDW_CUDA(ctx, cudaStreamCreateWithPriority(&pb->side, cudaStreamNonBlocking, lo));
     pb->ev_solve.resize(pb->nt);
     pb->ev_conv.resize(pb->nt);
+    pb->ev_near.resize(pb->nt);
+    TDW_CUDA(ctx, cudaStreamCreateWithPriority(&pb->side_near, cudaStreamNonBlocking, lo));
     for (auto& e : pb->ev_solve) TDW_CUDA(ctx, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     for (auto& e : pb->ev_conv) TDW_CUDA(ctx, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    for (auto& e : pb->ev_near) TDW_CUDA(ctx, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     TDW_CUDA(ctx, cudaEventCreateWithFlags(&pb->ev_fork, cudaEventDisableTiming));
   }
 
@@ -1663,7 +1779,7 @@ int tdw_march_emulated_impl(tdw_problem** pbs, int n, double threshold) {
                                           pbs[r]->d_b + slot * pbs[r]->bstride + pbs[r]->b_off,
                                           sizeof(double) * rpr, cudaMemcpyDeviceToDevice, st));
       for (int r = 0; r < n; ++r) {
-        int rc = launch_solve(pbs[r], L[r], s, st);
+        int rc = launch_solve_near(pbs[r], L[r], s, st);
         if (rc) return rc;
       }
     }
@@ -1691,7 +1807,7 @@ int tdw_time_conv_impl(tdw_problem* pb, int n, float* ms_out) {
     if (rc) return rc;
   }
   const size_t smem = pb->conv_stage_bytes;
-  TDW_CUDA(ctx, conv_set_smem(pb->kb, (int)smem));
+  TDW_CUDA(ctx, conv_set_smem(pb->kb, pb->conv_rpw, (int)smem));
   TDW_CUDA(ctx, cudaMemsetAsync(pb->d_flags, 0, sizeof(int) * 4, st));
   cudaEvent_t e0, e1;
   TDW_CUDA(ctx, cudaEventCreate(&e0));
@@ -1702,23 +1818,24 @@ int tdw_time_conv_impl(tdw_problem* pb, int n, float* ms_out) {
     TDW_CUDA(ctx, cudaMalloc(&dstats, sizeof(unsigned long long) * 40));
     TDW_CUDA(ctx, cudaMemsetAsync(dstats, 0, sizeof(unsigned long long) * 40, st));
     c.stats = dstats;
-    conv_launch(pb->kb, grid, smem, st, c, hmap);
+    conv_launch(pb->kb, pb->conv_rpw, grid, smem, st, c, hmap);
     unsigned long long h[40];
     TDW_CUDA(ctx, cudaMemcpyAsync(h, dstats, sizeof(h), cudaMemcpyDeviceToHost, st));
     TDW_CUDA(ctx, cudaStreamSynchronize(st));
     const double wu = (double)std::max(1ull, h[4]);
     fprintf(stderr, "conv stats: warp-units %llu, iterations/warp-unit %.2f, lane-entries/warp-unit %.1f, "
             "lmax/row %.2f, min lmin/warp %.2f, slot use %.3f\nlmax histogram:", h[4], h[0] / wu, h[1] / wu,
-            h[2] / (TDW_ROWS_PER_WARP * wu), h[3] / wu, h[1] / (32.0 * TDW_ROWS_PER_WARP * std::max(1ull, h[0])));
+            h[2] / (pb->conv_rpw * wu), h[3] / wu, h[1] / (32.0 * pb->conv_rpw * std::max(1ull, h[0])));
     for (int k = 0; k < 32; ++k)
       if (h[8 + k]) fprintf(stderr, " %d:%llu", k, h[8 + k]);
     fprintf(stderr, "\n");
     cudaFree(dstats);
     c.stats = nullptr;
   }
-  conv_launch(pb->kb, grid, smem, st, c, hmap);  // warm-up
+  c.dry = getenv("TDW_CONV_DRY") ? 1 : 0;
+  conv_launch(pb->kb, pb->conv_rpw, grid, smem, st, c, hmap);  // warm-up
   TDW_CUDA(ctx, cudaEventRecord(e0, st));
-  for (int k = 0; k < n; ++k) conv_launch(pb->kb, grid, smem, st, c, hmap);
+  for (int k = 0; k < n; ++k) conv_launch(pb->kb, pb->conv_rpw, grid, smem, st, c, hmap);
   TDW_CUDA(ctx, cudaEventRecord(e1, st));
   TDW_CUDA(ctx, cudaEventSynchronize(e1));
   TDW_CUDA(ctx, cudaGetLastError());
@@ -2050,5 +2167,5 @@ int launch_conv_fmm(tdw_problem* pb, void* plan, int alpha, cudaStream_t s) {
   return launch_conv(pb, *(LoopPlan*)plan, alpha, 1, s);
 }
 int launch_solve_fmm(tdw_problem* pb, void* plan, int alpha, cudaStream_t s) {
-  return launch_solve(pb, *(LoopPlan*)plan, alpha, s);
+  return launch_solve_near(pb, *(LoopPlan*)plan, alpha, s);
 }

@@ -12,8 +12,6 @@
 // Tile geometry of the banded store.
 #define TDW_TJ 32        // columns per J-tile == pairs per segment == one warp
 #define TDW_TI 32        // rows per I-block (one conv CTA)
-#define TDW_ROWS_PER_WARP 2
-#define TDW_CONV_WARPS (TDW_TI / TDW_ROWS_PER_WARP)
 #define TDW_ELL_MAX 64   // max nnz per row of the lag-1 step matrix
 #define TDW_KB_MAX 6     // time steps per convolution pass (temporal blocking)
 #define TDW_NEAR_MAX 256 // max pairs per row in the near structure (bands reaching a split lag)
@@ -96,6 +94,7 @@ struct tdw_problem {
   int* d_leafc = nullptr;    // packed leaf-cell coords per element (internal order) or null
   int split_lag2 = 1;        // lags 2..nsl+1 of the store keep the known density only
   int kb = 1;                // time steps per convolution pass (1..TDW_KB_MAX)
+  int conv_rpw = 2;          // rows per consumer warp of conv_kernel (2 or 4)
   int overlap = 1;           // solves a convolution pass overlaps (1..kb)
   int nsl = 1;               // split lags: kb + overlap - 1
   int bring = 2;             // b ring slots: kb + overlap
@@ -141,7 +140,9 @@ struct tdw_problem {
   double* d_bnear = nullptr;       // [nsl][nsl+1][ns]: N_g x^(beta-1) after solve(beta), for step beta-1+g
   // pipelined loop: side stream for the far convolution, per-step events
   cudaStream_t side = nullptr;
-  std::vector<cudaEvent_t> ev_solve, ev_conv;
+  cudaStream_t side_near = nullptr;  // near terms of lags >= 3 (off the solve's critical path)
+  bool near_split = false;
+  std::vector<cudaEvent_t> ev_solve, ev_conv, ev_near;
   cudaEvent_t ev_fork = nullptr;
   cudaGraphExec_t graph_exec = nullptr;  // cached loop graph
   double graph_thr = 0.0;

@@ -26,7 +26,7 @@ from . import _lib
 from .mesh import mesh_stats
 from .tbasis import decomposition_weights, eval_basis
 
-__all__ = ["ProblemSpec", "TimeHistory", "BandStore", "compute_gamma_star", "greville_samples",
+__all__ = ["ProblemSpec", "TimeHistory", "BandStore", "compute_gamma_star", "greville_samples", "greville_times",
            "build_retarded_matrices", "march"]
 
 
@@ -105,19 +105,35 @@ class TimeHistory:
         return out
 
 
+def greville_times(spec) -> np.ndarray:
+    """The Greville abscissae t_beta = beta dt + (d+1) dt / 2, beta = 0..nt-2 (marching.py:264-266)."""
+    basis = spec.basis
+    return np.arange(spec.nt - 1) * basis.dt + 0.5 * (basis.d + 1) * basis.dt
+
+
+def sample_data(fn, times, out: np.ndarray) -> np.ndarray:
+    """out[k] = fn(times[k]).  A data callable may also expose the vectorised
+    form `fn.sample_many(times, out)` (same values, all steps at once); plain
+    callables are called once per step, as the reference does."""
+    many = getattr(fn, "sample_many", None)
+    if many is not None:
+        many(times, out)
+    else:
+        for k, t in enumerate(times):
+            out[k] = fn(float(t))
+    return out
+
+
 def greville_samples(spec):
     """Known data at the Greville abscissae t = beta dt + (d+1) dt / 2 (marching.py:258-276)."""
-    basis = spec.basis
     nt, ns = spec.nt, spec.mesh.n_elements
     uk = np.zeros((nt - 1, ns))
     qk = np.zeros((nt - 1, ns))
-    off = 0.5 * (basis.d + 1) * basis.dt
-    for beta in range(nt - 1):
-        t = beta * basis.dt + off
-        if spec.u_data is not None:
-            uk[beta] = spec.u_data(t)
-        if spec.q_data is not None:
-            qk[beta] = spec.q_data(t)
+    times = greville_times(spec)
+    if spec.u_data is not None:
+        sample_data(spec.u_data, times, uk)
+    if spec.q_data is not None:
+        sample_data(spec.q_data, times, qk)
     return uk, qk
 
 
@@ -167,6 +183,14 @@ class BandStore:
     @property
     def n_lags(self) -> int:
         return self.info()["n_lags"]
+
+    def pinned_known(self, which: int) -> np.ndarray:
+        """Page-locked (nt-1, ns) host buffer for the u (0) / q (1) samples, owned by the store."""
+        if not hasattr(self, "_pinned"):
+            self._pinned = [None, None]
+        if self._pinned[which] is None:
+            self._pinned[which] = _lib.PinnedArray((self.nt - 1, self.ns))
+        return self._pinned[which].array
 
     # benchmark helpers (device-resident inputs/outputs)
     def upload_known(self, u_known, q_known):
@@ -243,14 +267,17 @@ def march(spec, window: bool = True, blowup_factor: float = 1e6, mats=None,
     elif mats.window != window or mats.nt != spec.nt or mats.ns != spec.mesh.n_elements:
         raise ValueError("matrix set does not cover the required lags")
     hist = TimeHistory(spec.basis, spec.nt, spec.mesh.n_elements)
-    uk, qk = greville_samples(spec)
+    # Greville samples straight into the store's page-locked buffers; a data
+    # callable that is None is passed as NULL (zero samples, set on the device)
+    times = greville_times(spec)
+    uk = sample_data(spec.u_data, times, mats.pinned_known(0)) if spec.u_data is not None else None
+    qk = sample_data(spec.q_data, times, mats.pinned_known(1)) if spec.q_data is not None else None
     threshold = blowup_factor * max(spec.blowup_reference, 1e-30)
     ns, nt = spec.mesh.n_elements, spec.nt
     rhs = np.zeros((nt - 1, ns)) if rhs_trace is not None else None
     n_steps, status = C.c_int32(0), C.c_int32(0)
-    uk = np.ascontiguousarray(uk)
-    qk = np.ascontiguousarray(qk)
-    rc = _lib.load().tdw_march(mats.h, _lib.dptr(uk), _lib.dptr(qk), float(threshold),
+    rc = _lib.load().tdw_march(mats.h, _lib.dptr(uk) if uk is not None else None,
+                               _lib.dptr(qk) if qk is not None else None, float(threshold),
                                _lib.dptr(hist.u), _lib.dptr(hist.q), _lib.dptr(hist.tau),
                                _lib.dptr(hist.sigma), _lib.dptr(rhs) if rhs is not None else None,
                                C.byref(n_steps), C.byref(status))
