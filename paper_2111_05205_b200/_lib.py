@@ -126,6 +126,47 @@ class PinnedArray:
             pass
 
 
+_PINNED_POOL: dict[int, list[int]] = {}
+_PINNED_KEEP = 4  # idle blocks kept per size
+
+
+class _PinnedBlock:
+    """Owner of one page-locked block; it goes back to the pool (still pinned)
+    when the last numpy view of it is gone."""
+
+    def __init__(self, ptr: int, nbytes: int):
+        self.ptr, self.nbytes = ptr, nbytes
+
+    def __del__(self):
+        try:
+            idle = _PINNED_POOL.setdefault(self.nbytes, [])
+            if len(idle) < _PINNED_KEEP:
+                idle.append(self.ptr)
+            else:
+                load().tdw_host_free(C.c_void_p(self.ptr))
+        except Exception:
+            pass
+
+
+def pinned_empty(shape) -> np.ndarray:
+    """Uninitialised float64 array in page-locked host memory, from a pool (the
+    time loop's outputs are copied into such arrays at full link rate).  The
+    array owns its block through `base`; nothing else aliases it."""
+    shape = tuple(int(x) for x in shape)
+    n = int(np.prod(shape))
+    nbytes = max(8, 8 * n)
+    idle = _PINNED_POOL.get(nbytes)
+    if idle:
+        ptr = idle.pop()
+    else:
+        p = C.c_void_p()
+        check(load().tdw_host_alloc(nbytes, C.byref(p)), None, "tdw_host_alloc")
+        ptr = p.value
+    carr = (C.c_double * max(1, n)).from_address(ptr)
+    carr._owner = _PinnedBlock(ptr, nbytes)
+    return np.frombuffer(carr, dtype=np.float64)[:n].reshape(shape)
+
+
 def dptr(a: np.ndarray):
     return a.ctypes.data_as(_dp)
 

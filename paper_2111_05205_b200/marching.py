@@ -267,6 +267,10 @@ def march(spec, window: bool = True, blowup_factor: float = 1e6, mats=None,
     elif mats.window != window or mats.nt != spec.nt or mats.ns != spec.mesh.n_elements:
         raise ValueError("matrix set does not cover the required lags")
     hist = TimeHistory(spec.basis, spec.nt, spec.mesh.n_elements)
+    # outputs in page-locked memory (a pool: blocks come back when the arrays die);
+    # the library writes every entry
+    out = _lib.pinned_empty((4, spec.nt - 1, spec.mesh.n_elements))
+    hist.u, hist.q, hist.tau, hist.sigma = out[0], out[1], out[2], out[3]
     # Greville samples straight into the store's page-locked buffers; a data
     # callable that is None is passed as NULL (zero samples, set on the device)
     times = greville_times(spec)
