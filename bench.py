@@ -35,6 +35,9 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 METRIC = "MOT time-steps/s"
+# SURVEY 8(d) K1 cost model: FP64-pipe instruction-equivalents per (i,j,gamma) evaluation
+K1_COST = {("uw", 1): 3957, ("bm", 1): 6513, ("uw", 2): 4713, ("bm", 2): 10071,
+           ("uw", 3): 4689, ("bm", 3): 9177}
 HBM_FALLBACK = 6650.0  # GB/s, B200_PROFILING.md fallback
 
 
@@ -240,6 +243,17 @@ def run_ours(args, world, rank, local):
         except Exception:
             traffic = None
 
+    # roofline of K1 (coefficient fill, FP64-pipe bound): SURVEY 8(d) cost model in
+    # FP64 instruction-equivalents per (i,j,gamma) evaluation, against the FP64 FMA
+    # peak measured live on this GPU (tdw_fp64_peak; FMA = 2 FLOP)
+    import ctypes as C
+    fp64 = C.c_double(0.0)
+    _lib.check(_lib.load().tdw_fp64_peak(ctx.h, C.byref(fp64)), ctx.h, "tdw_fp64_peak")
+    kind = "bm" if spec.bie == "bmbie" else "uw"
+    cost = K1_COST[(kind, spec.basis.d)]
+    evals_per_s = info["n_evals"] / (info["t_fill_ms"] * 1e-3)
+    k1_achieved = evals_per_s * cost * 2.0 / 1e12
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         try:
@@ -280,8 +294,15 @@ def run_ours(args, world, rank, local):
             # near_step) per step
             "gpu_launches": int(args.steps * (1 + 2 * (-(-(nt - 1) // info["steps_per_pass"])) + 2 * (nt - 1))),
             "assembly": {"ms": info["t_assemble_ms"], "evals": info["n_evals"],
-                         "evals_per_s": info["n_evals"] / (info["t_fill_ms"] * 1e-3),
-                         "metric": "(i,j,gamma) layer-potential evals/s (fill kernel, fp64)"},
+                         "evals_per_s": evals_per_s,
+                         "metric": "(i,j,gamma) layer-potential evals/s (fill kernel, fp64)",
+                         "roofline": {"bound": "fp64", "achieved": k1_achieved, "peak": fp64.value,
+                                      "unit": "TFLOP/s", "frac": k1_achieved / fp64.value,
+                                      "kernel": "fill_kernel (K1)",
+                                      "cost_per_eval": cost, "cost_model": "SURVEY 8(d): FP64 "
+                                      "instruction-equivalents per evaluation (div/sqrt 20, atan 26, "
+                                      "asinh 60); hoisting raises evals/s, the cost stays fixed",
+                                      "peak_source": "measured live (tdw_fp64_peak: DFMA chains)"}},
             "graph": bool(tm.get("solve_ms", 0) > 0),
         }
         print(json.dumps(line), flush=True)

@@ -118,6 +118,10 @@ int tdw_problem_create(tdw_ctx* ctx, const tdw_problem_desc* desc, tdw_problem**
 int tdw_assemble(tdw_problem* pb);
 int tdw_problem_info(const tdw_problem* pb, tdw_info* out);
 
+/* FP64 FMA throughput of the ctx's GPU (TFLOP/s, FMA = 2 FLOP): the denominator
+ * of the coefficient kernel's roofline.  Diagnostics; no reference counterpart. */
+int tdw_fp64_peak(tdw_ctx* ctx, double* tflops);
+
 /* Pinned (page-locked) host memory for the march's host buffers: copies from and
  * to it run at full PCIe/C2C rate.  No reference counterpart (numpy arrays). */
 int tdw_host_alloc(int64_t bytes, void** out);

@@ -59,6 +59,7 @@ EXPORTS = {
     "tdw_last_error": ([C.c_void_p], C.c_char_p),
     "tdw_device_count": ([], C.c_int),
     "tdw_host_alloc": ([C.c_int64, C.POINTER(C.c_void_p)], C.c_int),
+    "tdw_fp64_peak": ([C.c_void_p, C.POINTER(C.c_double)], C.c_int),
     "tdw_host_free": ([C.c_void_p], C.c_int),
     "tdw_coeff_table": ([C.c_void_p, C.c_int64, _dp, _dp, _dp, _dp, _dp, _dp, C.c_int, C.c_double,
                          C.c_double, C.c_int, _dp, _dp, _dp], C.c_int),

@@ -94,6 +94,12 @@ __device__ __forceinline__ void tensor2d_g2s_hint(void* dst, const CUtensorMap* 
       : "memory");
 }
 
+// L2 prefetch of a byte range (no shared memory, no completion): the unit is in
+// L2 when its cp.async.bulk is issued a few units later
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+
 __device__ __forceinline__ void tensor2d_g2s(void* dst, const CUtensorMap* map, int c0, int c1,
                                              uint64_t* bar) {
   asm volatile(
@@ -126,6 +132,7 @@ struct ConvArgs {
   unsigned long long* stats;  // optional (TDW_CONV_STATS): iterations, lane entries, per-row lmax histogram
   int dry;                    // experiments (TDW_CONV_DRY, tdw_time_conv only): stream units, skip the k loop
   int hrows;                  // 1: history slice = the unit's lag span, per-row bulk copies; 0: TMA wbox box
+  int pf;                     // L2 prefetch distance of the unit stream (schedule entries; 0 = off)
   unsigned stage_bytes;  // shared-memory FIFO capacity
 };
 
@@ -220,6 +227,14 @@ __device__ __forceinline__ void conv_body(const ConvArgs& a, const CUtensorMap& 
         const unsigned long long qoff = __shfl_sync(FULLMASK, off, q);
         const unsigned qbytes = (unsigned)__shfl_sync(FULLMASK, nbytes, q);
         const int gmin = __shfl_sync(FULLMASK, g.x, q), gmax = __shfl_sync(FULLMASK, g.y, q);
+        if (a.pf > 0) {  // L2 prefetch of the unit pf entries ahead (and, at a batch start, the first pf)
+          const int pq = q + a.pf;
+          const unsigned long long poff = __shfl_sync(FULLMASK, off, pq & 31);
+          const unsigned pbytes = (unsigned)__shfl_sync(FULLMASK, nbytes, pq & 31);
+          if (lane == 0 && pq < nb && pbytes >= 16) bulk_prefetch_l2(a.units + poff, pbytes & ~15u);
+          if (q == 0 && lane > 0 && lane < a.pf && lane < nb && nbytes >= 16)
+            bulk_prefetch_l2(a.units + off, (unsigned)nbytes & ~15u);
+        }
         if (quid == TDW_EMPTY_UNIT) continue;
         const int slot = n & 3;
         const int W = gmax >= gmin ? gmax - gmin + 1 : 0;
@@ -1368,6 +1383,10 @@ static void fill_conv_args(tdw_problem* pb, ConvArgs& c) {
   c.wbox = pb->wbox;
   c.stats = nullptr;
   c.dry = 0;
+  {
+    const char* f = getenv("TDW_PF");
+    c.pf = f ? std::max(0, std::min(16, atoi(f))) : 0;  // measured: a loss on configs 2, 3
+  }
   {
     const char* h = getenv("TDW_HROWS");
     c.hrows = h ? atoi(h) : 1;
