@@ -87,6 +87,7 @@ typedef struct {
   int32_t near_width;        /* widest row of the near structure                 */
   int32_t pass_overlap;      /* solves a convolution pass runs beside            */
   int32_t solve_halo;        /* halo depth of the communication-avoiding solver (0: none) */
+  int64_t fmm_m2l_pairs;     /* FMM: M2L interaction pairs this rank evaluates (0: direct) */
 } tdw_info;
 
 typedef struct {
@@ -200,7 +201,9 @@ int tdw_fmm_setup(tdw_problem* pb, const tdw_fmm_desc* desc);
 /* Test harness of the row-sharded path on ONE device: create the shard of rank
  * desc->rank of desc->nranks without a communicator, then run all shards in one
  * process with the per-step all-gather emulated by device copies.  Every shard
- * must be assembled and have its known data uploaded; outputs via tdw_download. */
+ * must be assembled and have its known data uploaded; outputs via tdw_download.
+ * FMM shards (tdw_fmm_setup on a shard) own the target leaf cells of their rows
+ * and evaluate M2L only into those cells and their ancestors. */
 int tdw_problem_create_shard(tdw_ctx* ctx, const tdw_problem_desc* desc, tdw_problem** out);
 int tdw_march_emulated(tdw_problem** shards, int n, double threshold);
 

@@ -379,6 +379,7 @@ int tdw_problem_info(const tdw_problem* pb, tdw_info* out) {
   out->max_unit_bytes = (int64_t)pb->max_unit_bytes;
   out->max_lag_span = pb->wmax;
   out->conv_grid = pb->conv_grid;
+  out->fmm_m2l_pairs = tdw_fmm_m2l_pairs(pb);
   out->conv_splits = pb->conv_S;
   out->solve_cluster = pb->sp_cl;
   out->n_units = pb->n_units;

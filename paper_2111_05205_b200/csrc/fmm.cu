@@ -81,6 +81,8 @@ struct FmmState {
   double t_space[2][FPS][FPS], t_time[2][FPT][FPT];
   std::vector<FmmExtra> extra;
   std::vector<long long> ticks_before, k_obs;
+  int r0 = 0, r1 = 0;          // this shard's rows (internal order)
+  long long m2l_pairs = 0;     // M2L interaction pairs this shard evaluates (all levels)
   std::vector<double> wt, dwt, wts;  // [nt][FPT]
 };
 
@@ -140,11 +142,12 @@ __global__ void extra_coeff_kernel(const double* __restrict__ elem, const int* _
 __global__ void extra_apply_kernel(const int* __restrict__ row_ptr, const int* __restrict__ col,
                                    const double* __restrict__ U, const double* __restrict__ W,
                                    int lags, int gmax, const double2* __restrict__ hist, int hcols,
-                                   int pad, int alpha, int d, int ns, double* b, const int* flags) {
+                                   int pad, int alpha, int d, int r0, int r1, double* b,
+                                   const int* flags) {
   if (flags[0] != 0) return;
   double w[5] = {0, 0, 0, 0, 0};
   bw(d, w);
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < ns; i += gridDim.x * blockDim.x) {
+  for (int i = r0 + blockIdx.x * blockDim.x + threadIdx.x; i < r1; i += gridDim.x * blockDim.x) {
     double acc = 0.0;
     for (int p = row_ptr[i]; p < row_ptr[i + 1]; ++p) {
       const int j = col[p];
@@ -165,9 +168,9 @@ struct StepW {
 __global__ void l2p_kernel(const int* __restrict__ elem_cell, const double* __restrict__ own,
                            const double* __restrict__ inherit, int ko_own, int ko_inh, int ncell,
                            const double* __restrict__ lval, const double* __restrict__ lbm, StepW sw,
-                           int ns, double* b, const int* flags) {
+                           int r0, int r1, double* b, const int* flags) {
   if (flags[0] != 0) return;
-  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < ns; j += gridDim.x * blockDim.x) {
+  for (int j = r0 + blockIdx.x * blockDim.x + threadIdx.x; j < r1; j += gridDim.x * blockDim.x) {
     const int cell = elem_cell[j];
     const double* lo = own + ((size_t)ko_own * ncell + cell) * FND;
     const double* li = inherit + ((size_t)ko_inh * ncell + cell) * FND;
@@ -402,7 +405,6 @@ extern "C" int tdw_fmm_setup(tdw_problem* pb, const tdw_fmm_desc* fd) {
   if (pb->assembled) return tdw_fail(ctx, TDW_ERR_STATE, "tdw_fmm_setup must precede tdw_assemble");
   if (fd->ps != FPS || fd->pt != FPT || fd->mu < 1 || fd->mu > FMU_MAX)
     return tdw_fail(ctx, TDW_ERR_LIMIT, "FMM supports ps = pt = 4 and mu <= 8");
-  if (pb->nranks != 1) return tdw_fail(ctx, TDW_ERR_LIMIT, "FMM path is single-GPU in this build");
   const int ns = pb->ns, nt = pb->nt, d = pb->d;
   FmmState* F = new FmmState();
   pb->fmm = F;
@@ -468,6 +470,30 @@ extern "C" int tdw_fmm_setup(tdw_problem* pb, const tdw_fmm_desc* fd) {
         F->t_space[h][i][j] = fd->t_space[(h * FPS + i) * FPS + j];
         F->t_time[h][i][j] = fd->t_time[(h * FPT + i) * FPT + j];
       }
+  // Target-cell sharding: a rank owns the leaf cells of its rows
+  // (internal order [row_lo, row_hi): RCB blocks, compact patches) and their
+  // ancestors.  It runs M2L only into owned observation cells; P2M, M2M, L2L
+  // and the recurrence stay whole-tree (cheap) so every owned cell sees the
+  // same moments and locals as on one GPU.  Cells straddling two ranks' rows are
+  // owned by both (computed twice).
+  std::vector<std::vector<char>> owned(F->leaf + 1);
+  F->r0 = pb->row_lo;
+  F->r1 = pb->row_hi;
+  if (F->leaf >= 2) {
+    owned[F->leaf].assign(fd->lev_ncell[F->leaf - 2], pb->nranks == 1 ? 1 : 0);
+    for (int k = pb->row_lo; k < pb->row_hi; ++k) owned[F->leaf][ecell[k]] = 1;
+    long long oc2 = 0;
+    std::vector<long long> lev_off(F->leaf + 1, 0);
+    for (int li = 0; li < fd->n_levels; ++li) {
+      lev_off[2 + li] = oc2;
+      oc2 += fd->lev_ncell[li];
+    }
+    for (int L = F->leaf; L > 2; --L) {
+      owned[L - 1].assign(fd->lev_ncell[L - 3], pb->nranks == 1 ? 1 : 0);
+      for (int c = 0; c < fd->lev_ncell[L - 2]; ++c)
+        if (owned[L][c]) owned[L - 1][(int)fd->lev_parent[lev_off[L] + c]] = 1;
+    }
+  }
   // levels
   F->lev.resize(F->leaf + 1);
   long long oc = 0, oo = 0, oil = 0, optr = 0, ok0 = 0, okp = 0;
@@ -508,21 +534,29 @@ extern "C" int tdw_fmm_setup(tdw_problem* pb, const tdw_fmm_desc* fd) {
     if ((rc = up(ctx, &V.Kp, fd->lev_Kp + okp, (size_t)d * V.noff * FKR * F->ntaup))) return rc;
     {
       // interaction pairs grouped by offset (stable: by observer within a group)
+      // (a shard keeps the pairs whose observation cell it owns)
       std::vector<long long> grp(V.noff + 1, 0);
-      std::vector<int> gobs(nil), gsrc(nil);
       std::vector<int> obs_of(nil);
       for (int c = 0; c < V.ncell; ++c)
         for (long long q = optr_v[c]; q < optr_v[c + 1]; ++q) obs_of[q] = c;
-      for (long long q = 0; q < nil; ++q) grp[off[q] + 1]++;
+      long long nkeep = 0;
+      for (long long q = 0; q < nil; ++q)
+        if (owned[L][obs_of[q]]) {
+          grp[off[q] + 1]++;
+          ++nkeep;
+        }
+      std::vector<int> gobs(nkeep), gsrc(nkeep);
       for (int o = 0; o < V.noff; ++o) grp[o + 1] += grp[o];
       std::vector<long long> fillp(grp.begin(), grp.end() - 1);
       for (long long q = 0; q < nil; ++q) {
+        if (!owned[L][obs_of[q]]) continue;
         const long long t = fillp[off[q]]++;
         gobs[t] = obs_of[q];
         gsrc[t] = src[q];
       }
       V.grp = grp;
-      V.nil = nil;
+      V.nil = nkeep;
+      F->m2l_pairs += nkeep;
       for (int o = 0; o < V.noff; ++o) V.max_grp = std::max(V.max_grp, grp[o + 1] - grp[o]);
       if ((rc = up(ctx, &V.g_obs, gobs.data(), gobs.size()))) return rc;
       if ((rc = up(ctx, &V.g_src, gsrc.data(), gsrc.size()))) return rc;
@@ -534,7 +568,7 @@ extern "C" int tdw_fmm_setup(tdw_problem* pb, const tdw_fmm_desc* fd) {
         build_kop_kernel<<<4096, 256, 0, ctx->stream>>>(V.K0, V.Kp, V.noff, F->ntau0, F->ntaup, F->mu,
                                                          d, V.Kop);
       TDW_CUDA(ctx, cudaGetLastError());
-      TDW_CUDA(ctx, cudaMalloc(&V.X, sizeof(double) * std::max<long long>(1, nil) * FND));
+      TDW_CUDA(ctx, cudaMalloc(&V.X, sizeof(double) * std::max<long long>(1, V.nil) * FND));
       TDW_CUDA(ctx, cudaMalloc(&V.tmp, sizeof(double) * d * (size_t)V.ncell * FND));
     }
     oc += V.ncell;
@@ -571,9 +605,13 @@ extern "C" int tdw_fmm_setup(tdw_problem* pb, const tdw_fmm_desc* fd) {
     FmmExtra E;
     E.lags = fd->extra_lags[x];
     E.npair = fd->extra_npair[x];
-    std::vector<std::pair<int, int>> pr(E.npair);
-    for (long long p = 0; p < E.npair; ++p)
-      pr[p] = {inv[fd->extra_i[oe + p]], inv[fd->extra_j[oe + p]]};
+    std::vector<std::pair<int, int>> pr;  // this shard's rows only
+    pr.reserve(fd->extra_npair[x]);
+    for (long long p = 0; p < fd->extra_npair[x]; ++p) {
+      const int i = inv[fd->extra_i[oe + p]];
+      if (i >= pb->row_lo && i < pb->row_hi) pr.push_back({i, inv[fd->extra_j[oe + p]]});
+    }
+    E.npair = (long long)pr.size();
     std::stable_sort(pr.begin(), pr.end(), [](auto& u, auto& v) { return u.first < v.first; });
     std::vector<int> rp(ns + 1, 0), col(E.npair), rof(E.npair);
     for (long long p = 0; p < E.npair; ++p) {
@@ -600,7 +638,7 @@ extern "C" int tdw_fmm_setup(tdw_problem* pb, const tdw_fmm_desc* fd) {
       TDW_CUDA(ctx, cudaGetLastError());
     }
     E.gmax.assign(fd->extra_gmax + (size_t)x * nt, fd->extra_gmax + (size_t)(x + 1) * nt);
-    oe += E.npair;
+    oe += fd->extra_npair[x];
     F->extra.push_back(std::move(E));
   }
   {
@@ -727,22 +765,25 @@ int make_plan_fmm(tdw_problem* pb, void** plan, double threshold, bool want_rhs)
 void free_plan_fmm(void* plan);
 int begin_loop_fmm(tdw_problem* pb, cudaStream_t st);
 
-int tdw_fmm_loop(tdw_problem* pb, double threshold, bool want_rhs, tdw_timing* timing) {
+namespace {
+
+// Per-step pieces of the FMM loop, shared by the single-GPU / NCCL loop and the
+// one-GPU emulation of R shards (tdw_fmm_march_emulated).
+struct FmmRun {
+  void* plan = nullptr;
+  long long last_tick = -1;
+};
+
+int fmm_begin(tdw_problem* pb, FmmRun& R, double threshold, bool want_rhs, cudaStream_t st) {
   tdw_ctx* ctx = pb->ctx;
   FmmState* F = pb->fmm;
-  cudaStream_t st = ctx->stream;
   if (want_rhs) {
     if (!pb->d_rhs)
       TDW_CUDA(ctx, cudaMalloc(&pb->d_rhs, sizeof(double) * (size_t)(pb->nt - 1) * pb->ns));
     TDW_CUDA(ctx, cudaMemsetAsync(pb->d_rhs, 0, sizeof(double) * (size_t)(pb->nt - 1) * pb->ns, st));
   }
-  void* plan = nullptr;
-  int rc = make_plan_fmm(pb, &plan, threshold, want_rhs);
+  int rc = make_plan_fmm(pb, &R.plan, threshold, want_rhs);
   if (rc) return rc;
-  cudaEvent_t e0, e1;
-  TDW_CUDA(ctx, cudaEventCreate(&e0));
-  TDW_CUDA(ctx, cudaEventCreate(&e1));
-  TDW_CUDA(ctx, cudaEventRecord(e0, st));
   if ((rc = begin_loop_fmm(pb, st))) return rc;
   for (int L = 2; L <= F->leaf; ++L) {
     FmmLevel& V = F->lev[L];
@@ -753,45 +794,102 @@ int tdw_fmm_loop(tdw_problem* pb, double threshold, bool want_rhs, tdw_timing* t
     TDW_CUDA(ctx, cudaMemsetAsync(V.aux, 0, cs * std::max(1, pb->d * (pb->d - 1) / 2), st));
     TDW_CUDA(ctx, cudaMemsetAsync(V.acc, 0, cs, st));
   }
-  const int ring = F->mu + 3;
-  long long last_tick = -1;
+  R.last_tick = -1;
+  return TDW_OK;
+}
+
+StepW step_weights(const FmmState* F, int alpha) {
+  StepW sw;
+  for (int m = 0; m < FPT; ++m) {
+    sw.wt[m] = F->wt[(size_t)alpha * FPT + m];
+    sw.dwt[m] = F->dwt[(size_t)alpha * FPT + m];
+    sw.wts[m] = F->wts[(size_t)alpha * FPT + m];
+  }
+  return sw;
+}
+
+// far-field ticks due before step alpha, then this shard's rows of b: near field
+// (banded store), extra lists, L2P
+int fmm_step_rhs(tdw_problem* pb, FmmRun& R, int alpha, cudaStream_t st) {
+  tdw_ctx* ctx = pb->ctx;
+  FmmState* F = pb->fmm;
+  int rc;
+  while (R.last_tick < F->ticks_before[alpha]) {
+    if ((rc = tick(pb, (int)(R.last_tick + 1), st))) return rc;
+    ++R.last_tick;
+  }
+  double* b = pb->d_b + (alpha & 1) * pb->bstride;
+  if ((rc = launch_conv_fmm(pb, R.plan, alpha, st))) return rc;  // near field -> b (own rows)
+  const int nrow = F->r1 - F->r0;
+  const int rblocks = std::max(1, (nrow + 127) / 128);
+  for (auto& E : F->extra) {
+    const int g = (int)E.gmax[alpha];
+    if (g <= 0 || E.npair == 0) continue;
+    extra_apply_kernel<<<rblocks, 128, 0, st>>>(E.row_ptr, E.col, E.U, E.W, E.lags, g, pb->d_hist,
+                                                 pb->hcols, pb->pad, alpha, pb->d, F->r0, F->r1, b,
+                                                 pb->d_flags);
+  }
   FmmLevel* LV = F->leaf >= 2 ? &F->lev[F->leaf] : nullptr;
-  for (int alpha = 1; alpha < pb->nt; ++alpha) {
-    while (last_tick < F->ticks_before[alpha]) {
-      if ((rc = tick(pb, (int)(last_tick + 1), st))) return rc;
-      ++last_tick;
+  if (LV) {
+    const int ring = F->mu + 3;
+    const long long ko = F->k_obs[alpha];
+    l2p_kernel<<<rblocks, 128, 0, st>>>(F->elem_cell, LV->own, LV->inherit, (int)(ko % ring), (int)(ko % 4),
+                                         LV->ncell, F->l2p_val,
+                                         pb->bie == TDW_BIE_BMBIE ? F->l2p_bm : nullptr, step_weights(F, alpha),
+                                         F->r0, F->r1, b, pb->d_flags);
+  }
+  TDW_CUDA(ctx, cudaGetLastError());
+  return TDW_OK;
+}
+
+// the (redundant) lag-1 solve on the full b, then the step's sources into the leaf moments
+int fmm_step_solve(tdw_problem* pb, FmmRun& R, int alpha, cudaStream_t st) {
+  tdw_ctx* ctx = pb->ctx;
+  FmmState* F = pb->fmm;
+  int rc = launch_solve_fmm(pb, R.plan, alpha, st);
+  if (rc) return rc;
+  FmmLevel* LV = F->leaf >= 2 ? &F->lev[F->leaf] : nullptr;
+  if (LV)
+    p2m_kernel<<<LV->ncell, FN3, 0, st>>>(F->cell_ptr, F->cell_elems, F->p2m_tau, F->p2m_sig, pb->d_hist,
+                                           pb->hcols, pb->pad, alpha - 1, pb->d, step_weights(F, alpha),
+                                           LV->acc, pb->d_flags);
+  TDW_CUDA(ctx, cudaGetLastError());
+  return TDW_OK;
+}
+
+int fmm_check(tdw_problem* pb) {
+  int hflags[4];
+  TDW_CUDA(pb->ctx, cudaMemcpy(hflags, pb->d_flags, sizeof(hflags), cudaMemcpyDeviceToHost));
+  if (hflags[0] == 2) return tdw_fail(pb->ctx, TDW_ERR_RESIDUAL, "FMM step: solve residual too large");
+  return TDW_OK;
+}
+
+}  // namespace
+
+int tdw_fmm_loop(tdw_problem* pb, double threshold, bool want_rhs, tdw_timing* timing) {
+  tdw_ctx* ctx = pb->ctx;
+  cudaStream_t st = ctx->stream;
+  const bool multi = pb->nranks > 1;
+  if (multi && !ctx->comm)
+    return tdw_fail(ctx, TDW_ERR_STATE, "sharded FMM problem without a communicator (tdw_comm_init)");
+  FmmRun R;
+  cudaEvent_t e0, e1;
+  TDW_CUDA(ctx, cudaEventCreate(&e0));
+  TDW_CUDA(ctx, cudaEventCreate(&e1));
+  TDW_CUDA(ctx, cudaEventRecord(e0, st));
+  int rc = fmm_begin(pb, R, threshold, want_rhs, st);
+  for (int alpha = 1; rc == TDW_OK && alpha < pb->nt; ++alpha) {
+    rc = fmm_step_rhs(pb, R, alpha, st);
+    if (rc == TDW_OK && multi) {  // every rank's block of b, in place (NVLink)
+      double* b = pb->d_b + (alpha & 1) * pb->bstride;
+      ncclResult_t nr = ncclAllGather(b + pb->b_off, b, (size_t)pb->rows_per_rank, ncclDouble, ctx->comm, st);
+      if (nr != ncclSuccess) rc = tdw_fail(ctx, TDW_ERR_NCCL, std::string("ncclAllGather: ") + ncclGetErrorString(nr));
     }
-    double* b = pb->d_b + (alpha & 1) * pb->bstride;
-    if ((rc = launch_conv_fmm(pb, plan, alpha, st))) return rc;  // near field -> b
-    for (auto& E : F->extra) {
-      const int g = (int)E.gmax[alpha];
-      if (g <= 0 || E.npair == 0) continue;
-      extra_apply_kernel<<<(pb->ns + 127) / 128, 128, 0, st>>>(E.row_ptr, E.col, E.U, E.W, E.lags, g,
-                                                              pb->d_hist, pb->hcols, pb->pad,
-                                                              alpha, pb->d, pb->ns, b, pb->d_flags);
-    }
-    StepW sw;
-    for (int m = 0; m < FPT; ++m) {
-      sw.wt[m] = F->wt[(size_t)alpha * FPT + m];
-      sw.dwt[m] = F->dwt[(size_t)alpha * FPT + m];
-      sw.wts[m] = F->wts[(size_t)alpha * FPT + m];
-    }
-    if (LV) {
-      const long long ko = F->k_obs[alpha];
-      l2p_kernel<<<(pb->ns + 127) / 128, 128, 0, st>>>(
-          F->elem_cell, LV->own, LV->inherit, (int)(ko % ring), (int)(ko % 4), LV->ncell,
-          F->l2p_val, pb->bie == TDW_BIE_BMBIE ? F->l2p_bm : nullptr, sw, pb->ns, b, pb->d_flags);
-    }
-    if ((rc = launch_solve_fmm(pb, plan, alpha, st))) return rc;
-    if (LV)
-      p2m_kernel<<<LV->ncell, FN3, 0, st>>>(F->cell_ptr, F->cell_elems, F->p2m_tau, F->p2m_sig,
-                                             pb->d_hist, pb->hcols, pb->pad, alpha - 1, pb->d, sw,
-                                             LV->acc, pb->d_flags);
-    TDW_CUDA(ctx, cudaGetLastError());
+    if (rc == TDW_OK) rc = fmm_step_solve(pb, R, alpha, st);
   }
   TDW_CUDA(ctx, cudaEventRecord(e1, st));
   TDW_CUDA(ctx, cudaEventSynchronize(e1));
-  if (timing) {
+  if (timing && rc == TDW_OK) {
     float ms = 0.f;
     cudaEventElapsedTime(&ms, e0, e1);
     timing->total_ms += ms;
@@ -799,12 +897,47 @@ int tdw_fmm_loop(tdw_problem* pb, double threshold, bool want_rhs, tdw_timing* t
   }
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
-  free_plan_fmm(plan);
-  int hflags[4];
-  TDW_CUDA(ctx, cudaMemcpy(hflags, pb->d_flags, sizeof(hflags), cudaMemcpyDeviceToHost));
-  if (hflags[0] == 2) return tdw_fail(ctx, TDW_ERR_RESIDUAL, "FMM step: solve residual too large");
+  if (R.plan) free_plan_fmm(R.plan);
+  if (rc) return rc;
+  return fmm_check(pb);
+}
+
+// R shards of one FMM problem on ONE device, in lockstep: per step every shard
+// forms its rows of b, the all-gather is replaced by device copies of the row
+// blocks, every shard solves redundantly (the multi-GPU data flow, testable on
+// one GPU).
+int tdw_fmm_march_emulated(tdw_problem** pbs, int n, double threshold) {
+  tdw_ctx* ctx = pbs[0]->ctx;
+  cudaStream_t st = ctx->stream;
+  std::vector<FmmRun> R(n);
+  int rc = TDW_OK;
+  for (int r = 0; r < n && rc == TDW_OK; ++r) {
+    if (!pbs[r]->fmm || !pbs[r]->assembled || !pbs[r]->known_loaded)
+      return tdw_fail(ctx, TDW_ERR_STATE, "emulated FMM march: shard not set up, assembled or without data");
+    rc = fmm_begin(pbs[r], R[r], threshold, false, st);
+  }
+  const size_t rpr = (size_t)pbs[0]->rows_per_rank;
+  for (int alpha = 1; rc == TDW_OK && alpha < pbs[0]->nt; ++alpha) {
+    for (int r = 0; r < n && rc == TDW_OK; ++r) rc = fmm_step_rhs(pbs[r], R[r], alpha, st);
+    const size_t slot = (size_t)(alpha & 1);
+    for (int r = 0; r < n && rc == TDW_OK; ++r)
+      for (int q = 0; q < n; ++q)
+        if (q != r)
+          TDW_CUDA(ctx, cudaMemcpyAsync(pbs[q]->d_b + slot * pbs[q]->bstride + pbs[r]->b_off,
+                                        pbs[r]->d_b + slot * pbs[r]->bstride + pbs[r]->b_off,
+                                        sizeof(double) * rpr, cudaMemcpyDeviceToDevice, st));
+    for (int r = 0; r < n && rc == TDW_OK; ++r) rc = fmm_step_solve(pbs[r], R[r], alpha, st);
+  }
+  TDW_CUDA(ctx, cudaStreamSynchronize(st));
+  for (int r = 0; r < n; ++r)
+    if (R[r].plan) free_plan_fmm(R[r].plan);
+  if (rc) return rc;
+  for (int r = 0; r < n; ++r)
+    if ((rc = fmm_check(pbs[r]))) return rc;
   return TDW_OK;
 }
+
+long long tdw_fmm_m2l_pairs(const tdw_problem* pb) { return pb->fmm ? pb->fmm->m2l_pairs : 0; }
 
 void tdw_fmm_free(FmmState* F) {
   if (!F) return;

@@ -1770,6 +1770,7 @@ int tdw_march_loop(tdw_problem* pb, double threshold, bool want_rhs, bool time_k
 // rank's b (the in-place all-gather).  Test harness for the sharded code path
 // on a single GPU: no kernel waits on another, launches are sequential.
 int tdw_march_emulated_impl(tdw_problem** pbs, int n, double threshold) {
+  if (pbs[0]->fmm) return tdw_fmm_march_emulated(pbs, n, threshold);
   tdw_ctx* ctx = pbs[0]->ctx;
   cudaStream_t st = ctx->stream;
   std::vector<LoopPlan> L(n);

@@ -96,3 +96,27 @@ def march_emulated(spec, nranks: int, window: bool = True, blowup_factor: float 
     for sh in shards:
         sh.close()
     return out, infos
+
+
+def fast_march_emulated(spec, nranks: int, config=None, plan=None, blowup_factor: float = 1e6):
+    """The target-cell-sharded FMM of `nranks` shards on ONE GPU
+    (tdw_march_emulated on FMM shards): each shard assembles its rows' near
+    field and evaluates M2L only into the leaf cells of its rows and their
+    ancestors; b is exchanged by device copies every step.  Returns the shards'
+    TimeHistory and info (fmm_m2l_pairs: the M2L pairs each shard evaluates)."""
+    from . import fmm, fmm_plan, marching
+    plan = plan or fmm_plan.build_plan(spec, config)
+    shards = [fmm.FmmStore(spec, config, plan=plan, nranks=nranks, rank=r, shard_only=True).assemble()
+              for r in range(nranks)]
+    uk, qk = marching.greville_samples(spec)
+    for sh in shards:
+        sh.upload_known(uk, qk)
+    arr = (C.c_void_p * nranks)(*[sh.h.value for sh in shards])
+    thr = blowup_factor * max(spec.blowup_reference, 1e-30)
+    _lib.check(_lib.load().tdw_march_emulated(arr, nranks, float(thr)), shards[0].ctx.h,
+               "tdw_march_emulated (FMM)")
+    out = [sh.download() for sh in shards]
+    infos = [sh.info() for sh in shards]
+    for sh in shards:
+        sh.close()
+    return out, infos

@@ -84,8 +84,12 @@ def _ptr(a, ct):
 class FmmStore(BandStore):
     """Device state of the fast solver: near-field banded store + far-field operators."""
 
-    def __init__(self, spec, config: FmmConfig | None = None, ctx=None, plan=None):
-        super().__init__(spec, window=True, ctx=ctx)
+    def __init__(self, spec, config: FmmConfig | None = None, ctx=None, plan=None,
+                 nranks: int = 1, rank: int = 0, shard_only: bool = False):
+        # nranks > 1: this rank's rows of the near field, M2L into the target
+        # leaf cells of those rows (and their ancestors) only; b is all-gathered
+        # every step (csrc/fmm.cu, tdw_fmm_loop / tdw_fmm_march_emulated)
+        super().__init__(spec, window=True, ctx=ctx, nranks=nranks, rank=rank, shard_only=shard_only)
         self.plan = plan or build_plan(spec, config)
         A = fmm_desc_arrays(self.plan, spec.nt)
         self._arrays = A
@@ -108,10 +112,13 @@ class FmmStore(BandStore):
 
 
 def fast_march(spec, config: FmmConfig | None = None, window: bool = True, blowup_factor: float = 1e6,
-               rhs_trace: list | None = None, return_solver: bool = False):
+               rhs_trace: list | None = None, return_solver: bool = False, ctx=None,
+               nranks: int = 1, rank: int = 0):
     """Run the fast solver on the GPU (fmm.py:534-544).  `window` is accepted for
-    signature compatibility: the near field always uses the gamma_near window."""
-    store = FmmStore(spec, config).assemble()
+    signature compatibility: the near field always uses the gamma_near window.
+    Multi-GPU (one process per GPU): pass the rank's context (with its
+    communicator, distributed.init_comm) and nranks / rank."""
+    store = FmmStore(spec, config, ctx=ctx, nranks=nranks, rank=rank).assemble()
     hist = TimeHistory(spec.basis, spec.nt, spec.mesh.n_elements)
     uk, qk = greville_samples(spec)
     uk, qk = np.ascontiguousarray(uk), np.ascontiguousarray(qk)

@@ -70,3 +70,36 @@ def test_one_rank_nccl_exchange_path(cfg):
         np.testing.assert_array_equal(h.q, ref.q)
     store.close()
     ctx.close()
+
+
+def _fmm_spec(bie, d, nt):
+    import warnings
+    base = scenarios.build_spec(1, nt=nt)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        return marching.ProblemSpec(base.mesh, np.ones(1280), bie, type(base.basis)(d, base.basis.dt),
+                                    1.0, nt, q_data=base.q_data)
+
+
+@pytest.mark.parametrize("bie,d,Z,nt,nranks", [("obie", 1, 100, 64, 2), ("bmbie", 2, 20, 40, 3),
+                                               ("bmbie", 2, 20, 40, 8)])
+def test_fmm_target_cell_shards_equal_single_rank(bie, d, Z, nt, nranks):
+    """Target-cell-sharded FMM, emulated on one GPU: every shard
+    holds the single-rank history (round-off: the near-field row sums are
+    grouped differently), all shards agree bit for bit, and the M2L work is
+    split (each shard evaluates fewer interaction pairs than one GPU does)."""
+    from paper_2111_05205_b200 import fmm, fmm_plan
+    spec = _fmm_spec(bie, d, nt)
+    cfg = fmm_plan.FmmConfig(ps=4, pt=4, leaf_capacity=Z)
+    plan = fmm_plan.build_plan(spec, cfg)
+    single = fmm.FmmStore(spec, cfg, plan=plan).assemble()
+    ref = marching.march(spec, mats=single)
+    pairs1 = single.info()["fmm_m2l_pairs"]
+    single.close()
+    hs, infos = distributed.fast_march_emulated(spec, nranks, cfg, plan=plan)
+    for h in hs:
+        assert h.status == ref.status and h.n_steps == ref.n_steps
+        assert per_step_rel(h.u, ref.u).max() < 1e-11
+        np.testing.assert_array_equal(h.u, hs[0].u)
+    pairs = [i["fmm_m2l_pairs"] for i in infos]
+    assert pairs1 > 0 and max(pairs) < pairs1 and sum(pairs) >= pairs1

@@ -1,1 +1,2 @@
-timeout 400 python bench.py 2>&1 | tail -1
+timeout 900 python tools/fmm_shard_probe.py 4 8 2>&1 | tail -12
+timeout 900 python tools/fmm_shard_probe.py 3 4 --run 2>&1 | tail -8
