@@ -434,6 +434,11 @@ int tdw_march(tdw_problem* pb, const double* u_known, const double* q_known, dou
   auto t0 = now();
   int rc = tdw_upload_known(pb, u_known, q_known);
   if (rc) return rc;
+  if (trace) {
+    cudaStreamSynchronize(pb->ctx->stream);
+    fprintf(stderr, "tdw_march: upload %.2f ms\n",
+            std::chrono::duration<double, std::milli>(now() - t0).count());
+  }
   if (!pb->assembled) {
     rc = tdw_assemble_impl(pb);
     if (rc) return rc;
@@ -491,6 +496,28 @@ int tdw_march_resident(tdw_problem* pb, double threshold, int n_repeat, int time
               "sync %.2f near %.2f sync %.2f final %.2f\n", n, acc[1] / n / 1e3, acc[2] / n / 1e3, sw / n,
               acc[3] / n / 1e3, acc[4] / n / 1e3, acc[5] / n / 1e3, acc[6] / n / 1e3, acc[7] / n / 1e3,
               acc[8] / n / 1e3);
+    // timeline of the last loop: solve, near step, gaps, convolution passes
+    double tl[5] = {0}, cv = 0.0;
+    int m = 0, mc = 0;
+    for (int a = 8; a + 1 < pb->nt; ++a) {
+      const unsigned long long* t = &h[(size_t)16 * a];
+      const unsigned long long* u = &h[(size_t)16 * (a + 1)];
+      if (!t[0] || !t[8] || !t[9] || !t[10] || !u[0] || u[0] < t[0]) continue;
+      tl[0] += (double)(t[8] - t[0]);
+      tl[1] += (double)t[9] - (double)t[8];
+      tl[2] += (double)(t[10] - t[9]);
+      tl[3] += (double)u[0] - (double)t[10];
+      tl[4] += (double)(u[0] - t[0]);
+      ++m;
+      if (t[11] && t[12] > t[11] && (a - 1) % pb->kb == 0) {
+        cv += (double)(t[12] - t[11]);
+        ++mc;
+      }
+    }
+    if (m)
+      fprintf(stderr, "timeline (us, mean of %d steps): solve %.2f | gap %.2f | near %.2f | gap to next solve %.2f "
+              "| step period %.2f; conv pass %.2f (%d passes)\n", m, tl[0] / m / 1e3, tl[1] / m / 1e3,
+              tl[2] / m / 1e3, tl[3] / m / 1e3, tl[4] / m / 1e3, mc ? cv / mc / 1e3 : 0.0, mc);
   }
   return TDW_OK;
 }
@@ -517,7 +544,7 @@ int tdw_problem_destroy(tdw_problem* pb) {
                   pb->d_qk, pb->d_bpart, pb->d_b, pb->d_x, pb->d_red, pb->d_bar, pb->d_flags,
                   pb->d_rhs, pb->d_sp_rowptr, pb->d_sp_nnzoff, pb->d_sp_col, pb->d_sp_val,
                   pb->d_ncol, pb->d_nval, pb->d_ncol_packed, pb->d_h_ncomp, pb->d_h_gi, pb->d_h_layer, pb->d_h_nz, pb->d_h_col,
-                  pb->d_h_ngat, pb->d_h_gdst, pb->d_h_gsrc, pb->d_h_val, pb->d_ncnt, pb->d_nptr, pb->d_ncol_rm, pb->d_nval_rm, pb->d_bnear, pb->d_out, pb->d_trace};
+                  pb->d_h_ngat, pb->d_h_gdst, pb->d_h_gsrc, pb->d_h_val, pb->d_ncnt, pb->d_nptr, pb->d_ncol_rm, pb->d_nval_rm, pb->d_bnear, pb->d_out, pb->d_trace, pb->d_n2_ptr, pb->d_n2_col, pb->d_n2_val};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (pb->graph_exec) cudaGraphExecDestroy(pb->graph_exec);

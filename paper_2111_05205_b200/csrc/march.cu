@@ -117,6 +117,23 @@ __device__ __forceinline__ double2 lds_f64x2(unsigned addr) {
   return v;
 }
 
+// kernel-wide stamps for the timeline trace (TDW_TRACE_SOLVE): block 0's start, the
+// last block's end
+__device__ __forceinline__ void trace_begin(unsigned long long* t) {
+  if (t && threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == 0) {
+    unsigned long long v;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
+    t[0] = v;
+  }
+}
+__device__ __forceinline__ void trace_end(unsigned long long* t) {
+  if (t && threadIdx.x == 0) {
+    unsigned long long v;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
+    atomicMax(t + 1, v);
+  }
+}
+
 struct ConvArgs {
   const unsigned char* __restrict__ units;
   const unsigned long long* __restrict__ unit_off;
@@ -133,6 +150,7 @@ struct ConvArgs {
   int dry;                    // experiments (TDW_CONV_DRY, tdw_time_conv only): stream units, skip the k loop
   int hrows;                  // 1: history slice = the unit's lag span, per-row bulk copies; 0: TMA wbox box
   int pf;                     // L2 prefetch distance of the unit stream (schedule entries; 0 = off)
+  unsigned long long* trace;  // timeline trace (TDW_TRACE_SOLVE): slots 11, 12 of the pass's first step
   unsigned stage_bytes;  // shared-memory FIFO capacity
 };
 
@@ -189,6 +207,8 @@ __device__ __forceinline__ void conv_body(const ConvArgs& a, const CUtensorMap& 
   }
   __syncthreads();
   const unsigned zaddr = smem_u32(&zero_slot);
+  unsigned long long* ttr = a.trace ? a.trace + (size_t)a.alpha * 16 + 11 : nullptr;
+  trace_begin(ttr);
   const unsigned u0 = a.sched_off[blockIdx.x], u1 = a.sched_off[blockIdx.x + 1];
   const int nent = (int)(u1 - u0);  // schedule entries: a unit id, or TDW_EMPTY_UNIT (item flush only)
 
@@ -436,6 +456,7 @@ __device__ __forceinline__ void conv_body(const ConvArgs& a, const CUtensorMap& 
     }
     }
   }
+  if (warp == 0) trace_end(ttr);
 }
 
 template <int KB>
@@ -551,6 +572,9 @@ struct ClusterSolveArgs {
   const int* __restrict__ sp_col;           // packed (owner << 24) | local
   const double* __restrict__ sp_val;
   const double* __restrict__ diag;          // [ns]
+  const int* __restrict__ n2_ptr;           // lag-2 near terms in the solve's tail (nullptr: off)
+  const int* __restrict__ n2_col;           // packed (owner << 24) | local
+  const double* __restrict__ n2_val;
   const int* __restrict__ ncol;             // [near_w][ns] packed (owner << 24) | local
   const double* __restrict__ nval;          // [kb][TDW_NEAR_MAX][ns] (lag 2 + index)
   const double* __restrict__ phi;
@@ -1099,6 +1123,25 @@ __global__ void __launch_bounds__(reg_threads<MAXNZ>(), 1) solve_halo_kernel(Clu
   }
   trace_mark(tr, 3);
   if (tr && tid == 0 && cr == 0) tr[15] = sweeps;
+  // lag-2 near terms of the next step, N^2 x^(beta0) (what near_step_kernel's
+  // g = 0 would write), from the owners' final x in DSMEM: the next solve then
+  // needs no kernel in between; lags >= 3 run on the near stream meanwhile
+  if (a.n2_ptr && own) {
+    double s0 = 0.0, s1 = 0.0;
+    const int q0 = __ldg(a.n2_ptr + gi), q1 = __ldg(a.n2_ptr + gi + 1);
+    int q = q0;
+    for (; q + 1 < q1; q += 2) {
+      const int c0 = __ldg(a.n2_col + q), c1 = __ldg(a.n2_col + q + 1);
+      const double w0 = __ldg(a.n2_val + q), w1 = __ldg(a.n2_val + q + 1);
+      s0 = fma(w0, *cl.map_shared_rank(ex + p * T + (c0 & 0xffffff), c0 >> 24), s0);
+      s1 = fma(w1, *cl.map_shared_rank(ex + p * T + (c1 & 0xffffff), c1 >> 24), s1);
+    }
+    if (q < q1) {
+      const int c0 = __ldg(a.n2_col + q);
+      s0 = fma(__ldg(a.n2_val + q), *cl.map_shared_rank(ex + p * T + (c0 & 0xffffff), c0 >> 24), s0);
+    }
+    a.bnear[(size_t)((a.alpha + 1) % (a.nsl + 1)) * a.ns + gi] = s0 + s1;
+  }
   // residual with the final x: own rows from ex[p], layer-1 columns gathered fresh
   for (int g = tid; g < ngat; g += blockDim.x) {
     const int src = __ldg(a.h_gsrc + (size_t)cr * a.hG + g);
@@ -1196,8 +1239,13 @@ __global__ void __launch_bounds__(128, 16) near_step_kernel(const int* __restric
                                                         const double* __restrict__ nval_c, long long nnz,
                                                         int ns, int nsl, const double2* __restrict__ hist,
                                                         int hcols, int pad, double* __restrict__ bnear,
-                                                        int alpha, int g0, int g1, const int* flags) {
+                                                        int alpha, int g0, int g1, const int* flags,
+                                                        unsigned long long* trace) {
+  // 32 registers: three 4-warp blocks fit beside a convolution CTA (the kernel
+  // runs in situ, where residency, not ILP, sets its time)
   if (*(volatile const int*)flags != 0) return;
+  unsigned long long* ttr = trace ? trace + (size_t)alpha * 16 + 9 : nullptr;
+  trace_begin(ttr);
   const int lane = threadIdx.x & 31;
   const int i = (int)(((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
   if (i >= ns) return;
@@ -1230,6 +1278,7 @@ __global__ void __launch_bounds__(128, 16) near_step_kernel(const int* __restric
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULLMASK, v, o);
     if (lane == 0) bnear[((size_t)g * ring + (alpha + 1 + g) % ring) * ns + i] = v;
   }
+  trace_end(ttr);
 }
 
 // compact row-major copy of the near structure for near_step_kernel
@@ -1383,6 +1432,7 @@ static void fill_conv_args(tdw_problem* pb, ConvArgs& c) {
   c.wbox = pb->wbox;
   c.stats = nullptr;
   c.dry = 0;
+  c.trace = nullptr;
   {
     const char* f = getenv("TDW_PF");
     c.pf = f ? std::max(0, std::min(16, atoi(f))) : 0;  // measured: a loss on configs 2, 3
@@ -1428,6 +1478,8 @@ struct LoopPlan {
 int make_plan(tdw_problem* pb, LoopPlan& L, double threshold, bool want_rhs) {
   tdw_ctx* ctx = pb->ctx;
   fill_conv_args(pb, L.c);
+  L.c.dry = getenv("TDW_DIAG_DRY_LOOP") ? 1 : 0;  // timing diagnostics only: wrong results
+  L.c.trace = pb->d_trace;
   {
     int rc = make_hist_map(pb, &L.hmap);
     if (rc) return rc;
@@ -1443,6 +1495,9 @@ int make_plan(tdw_problem* pb, LoopPlan& L, double threshold, bool want_rhs) {
   cs.sp_col = pb->d_sp_col;
   cs.sp_val = pb->d_sp_val;
   cs.diag = pb->d_adiag;
+  cs.n2_ptr = pb->near_in_solve ? pb->d_n2_ptr : nullptr;
+  cs.n2_col = pb->d_n2_col;
+  cs.n2_val = pb->d_n2_val;
   cs.ncol = pb->d_ncol_packed;
   cs.nval = pb->d_nval;
   cs.near_w = pb->near_w;
@@ -1549,9 +1604,9 @@ int launch_solve(tdw_problem* pb, LoopPlan& L, int alpha, cudaStream_t s) {
 int launch_near(tdw_problem* pb, int alpha, int g0, int g1, cudaStream_t s) {
   const long long threads = (long long)pb->ns * 32;
   const unsigned grid = (unsigned)((threads + 127) / 128);
-  near_step_kernel<<<grid, 128, 0, s>>>(
-      pb->d_nptr, pb->d_ncnt, pb->d_ncol_rm, pb->d_nval_rm, (long long)pb->n_near, pb->ns, pb->nsl,
-      pb->d_hist, pb->hcols, pb->pad, pb->d_bnear, alpha, g0, g1, pb->d_flags);
+near_step_kernel<<<grid, 128, 0, s>>>(pb->d_nptr, pb->d_ncnt, pb->d_ncol_rm, pb->d_nval_rm,
+                                        (long long)pb->n_near, pb->ns, pb->nsl, pb->d_hist, pb->hcols,
+                                        pb->pad, pb->d_bnear, alpha, g0, g1, pb->d_flags, pb->d_trace);
   TDW_CUDA(pb->ctx, cudaGetLastError());
   return TDW_OK;
 }
@@ -1559,7 +1614,8 @@ int launch_near(tdw_problem* pb, int alpha, int g0, int g1, cudaStream_t s) {
 // solve followed by all of its near terms on one stream (sequential loops)
 int launch_solve_near(tdw_problem* pb, LoopPlan& L, int alpha, cudaStream_t s) {
   int rc = launch_solve(pb, L, alpha, s);
-  if (rc == TDW_OK && pb->near_w > 0 && pb->split_lag2) rc = launch_near(pb, alpha, 0, pb->nsl, s);
+  const int g0 = pb->near_in_solve ? 1 : 0;  // lag 2 came from the solve's tail
+  if (rc == TDW_OK && pb->near_w > 0 && pb->split_lag2 && g0 < pb->nsl) rc = launch_near(pb, alpha, g0, pb->nsl, s);
   return rc;
 }
 
@@ -1584,7 +1640,8 @@ int enqueue_loop(tdw_problem* pb, LoopPlan& L, cudaEvent_t* ev_conv) {
   cudaEvent_t* evF = pb->ev_conv.data();   // F(alpha) done
   cudaEvent_t* evN = pb->ev_near.data();   // near terms of solve(alpha) done
   cudaStream_t sn = pb->side_near;
-  const bool near = pb->near_w > 0 && pb->split_lag2;
+  // TDW_DIAG_NO_NEAR=1 drops the near-term kernels (timing diagnostics only: wrong results)
+  const bool near = pb->near_w > 0 && pb->split_lag2 && !getenv("TDW_DIAG_NO_NEAR");
   TDW_CUDA(ctx, cudaEventRecord(pb->ev_fork, st));
   TDW_CUDA(ctx, cudaStreamWaitEvent(sc, pb->ev_fork, 0));
   TDW_CUDA(ctx, cudaStreamWaitEvent(sn, pb->ev_fork, 0));
@@ -1612,11 +1669,20 @@ int enqueue_loop(tdw_problem* pb, LoopPlan& L, cudaEvent_t* ev_conv) {
           return tdw_fail(ctx, TDW_ERR_NCCL, std::string("ncclAllGather: ") + ncclGetErrorString(nr));
       }
       // solve(s) reads the lag-3+ near terms near_step(s-2) wrote (lag 2: near_step(s-1), below)
-      if (near && pb->near_split && s - 2 >= 1) TDW_CUDA(ctx, cudaStreamWaitEvent(st, evN[s - 2], 0));
+      const bool side_near = near && (pb->near_split || pb->near_in_solve);
+      if (side_near && s - 2 >= 1) TDW_CUDA(ctx, cudaStreamWaitEvent(st, evN[s - 2], 0));
       if ((rc = launch_solve(pb, L, s, st))) return rc;
       // evS[s] after the near terms: a convolution pass waiting for solve(s)
       // starts only once the near kernel has had the SMs it left free
-      if (near && !pb->near_split) {
+      if (near && pb->near_in_solve) {
+        // lag 2 in the solve's tail; lags 3..nsl+1 beside solve(s+1) on the near stream
+        TDW_CUDA(ctx, cudaEventRecord(evS[s], st));
+        if (pb->nsl > 1) {
+          TDW_CUDA(ctx, cudaStreamWaitEvent(sn, evS[s], 0));
+          if ((rc = launch_near(pb, s, 1, pb->nsl, sn))) return rc;
+        }
+        TDW_CUDA(ctx, cudaEventRecord(evN[s], sn));
+      } else if (near && !pb->near_split) {
         if ((rc = launch_near(pb, s, 0, pb->nsl, st))) return rc;
         TDW_CUDA(ctx, cudaEventRecord(evS[s], st));
       } else if (near) {
@@ -1635,7 +1701,7 @@ int enqueue_loop(tdw_problem* pb, LoopPlan& L, cudaEvent_t* ev_conv) {
     }
   }
   // join the side streams
-  if (near && pb->near_split) TDW_CUDA(ctx, cudaStreamWaitEvent(st, evN[nt - 1], 0));
+  if (near && (pb->near_split || pb->near_in_solve)) TDW_CUDA(ctx, cudaStreamWaitEvent(st, evN[nt - 1], 0));
   TDW_CUDA(ctx, cudaStreamWaitEvent(st, evF[last_alpha], 0));
   TDW_CUDA(ctx, cudaGetLastError());
   return TDW_OK;
@@ -2159,6 +2225,40 @@ int tdw_setup_cluster_solver(tdw_problem* pb) {
   if (pb->sp_reg > 0) {
     int rc = setup_halo(pb, acol, aval);
     if (rc) return rc;
+  }
+  // lag-2 near terms computed in the halo solve's tail (TDW_NEAR_IN_SOLVE=0: off)
+  pb->near_in_solve = false;
+  {
+    const char* e = getenv("TDW_NEAR_IN_SOLVE");
+    const bool want = e ? atoi(e) != 0 : true;
+    if (want && pb->sp_reg > 0 && pb->sp_halo > 0 && pb->split_lag2 && pb->near_w > 0) {
+      std::vector<int> ncol((size_t)TDW_NEAR_MAX * ns), cnt(ns);
+      std::vector<double> nv0((size_t)TDW_NEAR_MAX * ns);  // g = 0 slice of [nsl][TDW_NEAR_MAX][ns]
+      TDW_CUDA(ctx, cudaMemcpy(ncol.data(), pb->d_ncol, sizeof(int) * ncol.size(), cudaMemcpyDeviceToHost));
+      TDW_CUDA(ctx, cudaMemcpy(nv0.data(), pb->d_nval, sizeof(double) * nv0.size(), cudaMemcpyDeviceToHost));
+      TDW_CUDA(ctx, cudaMemcpy(cnt.data(), pb->d_ncnt, sizeof(int) * ns, cudaMemcpyDeviceToHost));
+      std::vector<int> ptr(ns + 1, 0), col;
+      std::vector<double> val;
+      for (int i = 0; i < ns; ++i) {
+        for (int k = 0; k < cnt[i]; ++k) {
+          const double w = nv0[(size_t)k * ns + i];
+          if (w == 0.0) continue;
+          const int j = ncol[(size_t)k * ns + i];
+          col.push_back(((j / R) << 24) | (j % R));
+          val.push_back(w);
+        }
+        ptr[i + 1] = (int)col.size();
+      }
+      TDW_CUDA(ctx, cudaMalloc(&pb->d_n2_ptr, sizeof(int) * ptr.size()));
+      TDW_CUDA(ctx, cudaMalloc(&pb->d_n2_col, sizeof(int) * std::max<size_t>(1, col.size())));
+      TDW_CUDA(ctx, cudaMalloc(&pb->d_n2_val, sizeof(double) * std::max<size_t>(1, val.size())));
+      TDW_CUDA(ctx, cudaMemcpy(pb->d_n2_ptr, ptr.data(), sizeof(int) * ptr.size(), cudaMemcpyHostToDevice));
+      if (!col.empty()) {
+        TDW_CUDA(ctx, cudaMemcpy(pb->d_n2_col, col.data(), sizeof(int) * col.size(), cudaMemcpyHostToDevice));
+        TDW_CUDA(ctx, cudaMemcpy(pb->d_n2_val, val.data(), sizeof(double) * val.size(), cudaMemcpyHostToDevice));
+      }
+      pb->near_in_solve = true;
+    }
   }
   if (CL > 8) {
     TDW_CUDA(ctx, cudaFuncSetAttribute(solve_halo_kernel<8>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));

@@ -142,6 +142,12 @@ struct tdw_problem {
   cudaStream_t side = nullptr;
   cudaStream_t side_near = nullptr;  // near terms of lags >= 3 (off the solve's critical path)
   bool near_split = false;
+  // lag-2 near terms inside the halo solve (its tail, x from DSMEM): CSR over the
+  // rows, columns packed (owner CTA << 24) | owner-local row
+  bool near_in_solve = false;
+  int* d_n2_ptr = nullptr;
+  int* d_n2_col = nullptr;
+  double* d_n2_val = nullptr;
   std::vector<cudaEvent_t> ev_solve, ev_conv, ev_near;
   cudaEvent_t ev_fork = nullptr;
   cudaGraphExec_t graph_exec = nullptr;  // cached loop graph

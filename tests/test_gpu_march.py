@@ -193,6 +193,7 @@ def test_halo_solver_is_bit_identical(monkeypatch):
     spec = scenarios.build_spec(2)
     monkeypatch.setenv("TDW_SOLVER", "reg")
     monkeypatch.setenv("TDW_CHECK_EVERY", "2")
+    monkeypatch.setenv("TDW_NEAR_IN_SOLVE", "0")  # both solvers: all near terms in near_step_kernel
     monkeypatch.setenv("TDW_HALO", "0")
     plain = marching.BandStore(spec).assemble()
     assert plain.info()["solve_halo"] == 0
@@ -203,6 +204,25 @@ def test_halo_solver_is_bit_identical(monkeypatch):
     hh = marching.march(spec, mats=halo)
     np.testing.assert_array_equal(hh.q, hp.q)
     np.testing.assert_array_equal(hh.u, hp.u)
+
+
+def test_lag2_near_terms_in_the_solve(monkeypatch):
+    """Lag-2 near terms formed in the halo solve's tail from the owners' x in
+    DSMEM (lags >= 3 on the near stream) equal the near_step_kernel form to
+    round-off (another summation order), and both match the reference golden."""
+    spec = scenarios.build_spec(2)
+    monkeypatch.setenv("TDW_NEAR_IN_SOLVE", "0")
+    h0 = marching.march(spec)
+    monkeypatch.setenv("TDW_NEAR_IN_SOLVE", "1")
+    h1 = marching.march(spec)
+    def rel(x, ref):  # per step, floored at 1e-6 of the largest step (the first
+        n = np.linalg.norm(ref, axis=1)  # steps before the pulse arrives are round-off)
+        return np.linalg.norm(x - ref, axis=1) / np.maximum(n, 1e-6 * n.max())
+    assert rel(h1.q, h0.q).max() < 1e-12
+    for kb in ("4", "6"):
+        monkeypatch.setenv("TDW_KB", kb)
+        hk = marching.march(spec)
+        assert rel(hk.q, h0.q).max() < 1e-11, kb
 
 
 def test_window_off_is_equivalent():

@@ -1,2 +1,2 @@
-timeout 900 python tools/fmm_shard_probe.py 4 8 2>&1 | tail -12
-timeout 900 python tools/fmm_shard_probe.py 3 4 --run 2>&1 | tail -8
+TDW_TRACE_MARCH=1 timeout 120 python tools/e2e_probe.py 2 2>&1 | tail -5
+for i in 1 2; do timeout 300 python bench.py --no-cpu 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['value'], d['e2e']['value'], d['roofline']['frac'], d['graph'])"; done

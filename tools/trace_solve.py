@@ -1,4 +1,4 @@
-"""Solve phase trace (TDW_TRACE_SOLVE=1) and march host trace (TDW_TRACE_MARCH=1) for one config."""
+"""Solve phase trace and loop timeline (TDW_TRACE_SOLVE=1), march host trace (TDW_TRACE_MARCH=1)."""
 import os, sys
 from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
@@ -11,7 +11,5 @@ spec = scenarios.build_spec(cfg)
 st = marching.BandStore(spec).assemble()
 print(st.info(), flush=True)
 st.upload_known(*marching.greville_samples(spec))
-st.set_graph(False)
 st.run_resident(1e6, 1)
-for _ in range(2):
-    marching.march(spec, mats=st)
+st.run_resident(1e6, 1)
