@@ -290,7 +290,10 @@ def run_ours(args, world, rank, local):
                          "frac": achieved / peak, "traffic": traffic, "kernel": "conv_kernel (K2)",
                          "peak_source": peak_src, "avg_launch_ms": conv_ms,
                          "launches_timed": int(tk["conv_launches"]),
-                         "bytes_per_launch": 16.0 * n_band},
+                         "bytes_per_launch": 16.0 * n_band,
+                         "steps_per_launch": info["steps_per_pass"],
+                         "note": "each store byte counted once per launch; one launch serves "
+                                 "steps_per_launch MOT steps (temporal blocking)"},
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
             # per loop: init_hist + (conv_kernel + reduce_parts) per pass + (solve +

@@ -161,11 +161,12 @@ int tdw_problem_create_impl(tdw_ctx* ctx, const tdw_problem_desc* dsc, tdw_probl
   pb->window = dsc->window ? 1 : 0;
   {
     // temporal blocking: one convolution pass computes kb consecutive steps
-    // default 4; 6 when a pass (~ ns^2 / ranks band entries) dwarfs the solves
-    // (~ ns): measured config 2 (5120) best at 4, config 3 (20480) at 6 (+25%)
+    // default 4; 6 when a pass (~ ns^2 / ranks band entries) outweighs the solves
+    // (~ ns): measured config 0 (320 el.) best at 4, config 1 even, config 2
+    // (5120) 13.4k -> 14.2k steps/s at 6, config 3 (20480) 737 -> 921
     const char* e = getenv("TDW_KB");
     const double pass_size = (double)dsc->ns * (double)dsc->ns / std::max(1, nranks);
-    pb->kb = std::max(1, std::min(TDW_KB_MAX, e ? atoi(e) : (pass_size >= 1e8 ? 6 : 4)));
+    pb->kb = std::max(1, std::min(TDW_KB_MAX, e ? atoi(e) : (pass_size >= 1e7 ? 6 : 4)));
     // a pass waits for the solve overlap+1 steps back and runs beside the last
     // `overlap` solves; the split lags reach kb + overlap
     const char* o = getenv("TDW_OVERLAP");
@@ -512,6 +513,15 @@ int tdw_march_resident(tdw_problem* pb, double threshold, int n_repeat, int time
       if (t[11] && t[12] > t[11] && (a - 1) % pb->kb == 0) {
         cv += (double)(t[12] - t[11]);
         ++mc;
+      }
+    }
+    if (getenv("TDW_TRACE_RAW")) {  // raw per-step stamps (us from step 40's solve start)
+      const double t00 = (double)h[(size_t)16 * 40];
+      for (int a = 40; a < std::min(pb->nt, 64); ++a) {
+        const unsigned long long* t = &h[(size_t)16 * a];
+        auto us = [&](unsigned long long v) { return v ? ((double)v - t00) / 1e3 : -1.0; };
+        fprintf(stderr, "step %3d solve [%8.2f %8.2f] near [%8.2f %8.2f] conv [%8.2f %8.2f]\n", a, us(t[0]),
+                us(t[8]), us(t[9]), us(t[10]), us(t[11]), us(t[12]));
       }
     }
     if (m)

@@ -117,6 +117,13 @@ __device__ __forceinline__ double2 lds_f64x2(unsigned addr) {
   return v;
 }
 
+// Programmatic dependent launch (PDL) of consecutive solves: the next solve is
+// queued while this one runs (so its cluster takes the SMs this one frees before
+// other kernels' blocks do); it waits here for this grid's completion and
+// memory before touching anything.  No-ops without the launch attribute.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // kernel-wide stamps for the timeline trace (TDW_TRACE_SOLVE): block 0's start, the
 // last block's end
 __device__ __forceinline__ void trace_begin(unsigned long long* t) {
@@ -572,9 +579,10 @@ struct ClusterSolveArgs {
   const int* __restrict__ sp_col;           // packed (owner << 24) | local
   const double* __restrict__ sp_val;
   const double* __restrict__ diag;          // [ns]
-  const int* __restrict__ n2_ptr;           // lag-2 near terms in the solve's tail (nullptr: off)
+  const int* __restrict__ n2_ptr;           // near terms of lags 2..ntail+1 in the solve's tail: [ntail][ns+1]
   const int* __restrict__ n2_col;           // packed (owner << 24) | local
   const double* __restrict__ n2_val;
+  int ntail;                                // 0: off
   const int* __restrict__ ncol;             // [near_w][ns] packed (owner << 24) | local
   const double* __restrict__ nval;          // [kb][TDW_NEAR_MAX][ns] (lag 2 + index)
   const double* __restrict__ phi;
@@ -827,6 +835,8 @@ __global__ void __launch_bounds__(reg_threads<MAXNZ>(), 1) solve_reg_kernel(Clus
   __shared__ unsigned long long chk[3][2];
   __shared__ double shred[64];
   __shared__ double red2[4];
+  pdl_wait();  // before any read of the previous step's results (flags, b, x)
+  pdl_trigger();
   if (*(volatile int*)&a.flags[0] != 0) return;
   const int cr = (int)cl.block_rank();
   const int CL = (int)cl.num_blocks();
@@ -1007,6 +1017,8 @@ __global__ void __launch_bounds__(reg_threads<MAXNZ>(), 1) solve_halo_kernel(Clu
   __shared__ double shred[64];
   __shared__ double red2[4];
   __shared__ int s_stop;
+  pdl_wait();  // before any read of the previous step's results (flags, b, x)
+  pdl_trigger();
   if (*(volatile int*)&a.flags[0] != 0) return;
   const int cr = (int)cl.block_rank();
   const int CL = (int)cl.num_blocks();
@@ -1126,21 +1138,25 @@ __global__ void __launch_bounds__(reg_threads<MAXNZ>(), 1) solve_halo_kernel(Clu
   // lag-2 near terms of the next step, N^2 x^(beta0) (what near_step_kernel's
   // g = 0 would write), from the owners' final x in DSMEM: the next solve then
   // needs no kernel in between; lags >= 3 run on the near stream meanwhile
-  if (a.n2_ptr && own) {
-    double s0 = 0.0, s1 = 0.0;
-    const int q0 = __ldg(a.n2_ptr + gi), q1 = __ldg(a.n2_ptr + gi + 1);
-    int q = q0;
-    for (; q + 1 < q1; q += 2) {
-      const int c0 = __ldg(a.n2_col + q), c1 = __ldg(a.n2_col + q + 1);
-      const double w0 = __ldg(a.n2_val + q), w1 = __ldg(a.n2_val + q + 1);
-      s0 = fma(w0, *cl.map_shared_rank(ex + p * T + (c0 & 0xffffff), c0 >> 24), s0);
-      s1 = fma(w1, *cl.map_shared_rank(ex + p * T + (c1 & 0xffffff), c1 >> 24), s1);
+  if (a.ntail > 0 && own) {
+    for (int t = 0; t < a.ntail; ++t) {
+      const int* ptr = a.n2_ptr + (size_t)t * (a.ns + 1);
+      double s0 = 0.0, s1 = 0.0;
+      const int q0 = __ldg(ptr + gi), q1 = __ldg(ptr + gi + 1);
+      int q = q0;
+      for (; q + 1 < q1; q += 2) {
+        const int c0 = __ldg(a.n2_col + q), c1 = __ldg(a.n2_col + q + 1);
+        const double w0 = __ldg(a.n2_val + q), w1 = __ldg(a.n2_val + q + 1);
+        s0 = fma(w0, *cl.map_shared_rank(ex + p * T + (c0 & 0xffffff), c0 >> 24), s0);
+        s1 = fma(w1, *cl.map_shared_rank(ex + p * T + (c1 & 0xffffff), c1 >> 24), s1);
+      }
+      if (q < q1) {
+        const int c0 = __ldg(a.n2_col + q);
+        s0 = fma(__ldg(a.n2_val + q), *cl.map_shared_rank(ex + p * T + (c0 & 0xffffff), c0 >> 24), s0);
+      }
+      const int ring = a.nsl + 1;
+      a.bnear[((size_t)t * ring + (a.alpha + 1 + t) % ring) * a.ns + gi] = s0 + s1;
     }
-    if (q < q1) {
-      const int c0 = __ldg(a.n2_col + q);
-      s0 = fma(__ldg(a.n2_val + q), *cl.map_shared_rank(ex + p * T + (c0 & 0xffffff), c0 >> 24), s0);
-    }
-    a.bnear[(size_t)((a.alpha + 1) % (a.nsl + 1)) * a.ns + gi] = s0 + s1;
   }
   // residual with the final x: own rows from ex[p], layer-1 columns gathered fresh
   for (int g = tid; g < ngat; g += blockDim.x) {
@@ -1233,6 +1249,7 @@ __device__ __forceinline__ double ldg_keep(const double* p, uint64_t pol) {
   return v;
 }
 
+template <int NCH>  // 32-entry chunks per row: ceil(near_w / 32), rounded up to an instantiated size
 __global__ void __launch_bounds__(128, 16) near_step_kernel(const int* __restrict__ nptr,
                                                         const int* __restrict__ ncnt,
                                                         const int* __restrict__ ncol_c,
@@ -1252,7 +1269,6 @@ __global__ void __launch_bounds__(128, 16) near_step_kernel(const int* __restric
   const uint64_t keep = policy_keep_l2();  // the near structure is re-read every step
   const double2* hrow = hist + (size_t)(pad + alpha - 1) * hcols;
   const int p0 = __ldg(nptr + i), cnt = __ldg(ncnt + i);
-  constexpr int NCH = TDW_NEAR_MAX / 32;
   // every load of the row issued up front (latency-bound otherwise): columns,
   // then the history gathers
   int jj[NCH];
@@ -1495,7 +1511,8 @@ int make_plan(tdw_problem* pb, LoopPlan& L, double threshold, bool want_rhs) {
   cs.sp_col = pb->d_sp_col;
   cs.sp_val = pb->d_sp_val;
   cs.diag = pb->d_adiag;
-  cs.n2_ptr = pb->near_in_solve ? pb->d_n2_ptr : nullptr;
+  cs.n2_ptr = pb->d_n2_ptr;
+  cs.ntail = pb->near_in_solve ? pb->near_tail : 0;
   cs.n2_col = pb->d_n2_col;
   cs.n2_val = pb->d_n2_val;
   cs.ncol = pb->d_ncol_packed;
@@ -1561,7 +1578,7 @@ int launch_conv(tdw_problem* pb, LoopPlan& L, int alpha, int nsteps, cudaStream_
 }
 
 int launch_solve(tdw_problem* pb, LoopPlan& L, int alpha, cudaStream_t s) {
-  cudaLaunchAttribute cattr[1];
+  cudaLaunchAttribute cattr[2];
   cattr[0].id = cudaLaunchAttributeClusterDimension;
   cattr[0].val.clusterDim.x = pb->sp_cl;
   cattr[0].val.clusterDim.y = 1;
@@ -1573,6 +1590,13 @@ int launch_solve(tdw_problem* pb, LoopPlan& L, int alpha, cudaStream_t s) {
   ccfg.stream = s;
   ccfg.attrs = cattr;
   ccfg.numAttrs = 1;
+  // PDL for the register / halo solvers (they wait at entry): env TDW_PDL=0 disables
+  static const bool pdl = !(getenv("TDW_PDL") && atoi(getenv("TDW_PDL")) == 0);
+  if (pdl && pb->sp_reg > 0) {
+    cattr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    cattr[1].val.programmaticStreamSerializationAllowed = 1;
+    ccfg.numAttrs = 2;
+  }
   L.cs.alpha = alpha;
   L.cs.bpart = pb->d_bpart;
   L.cs.b = pb->d_b + (size_t)(alpha % pb->bring) * pb->bstride;
@@ -1604,9 +1628,17 @@ int launch_solve(tdw_problem* pb, LoopPlan& L, int alpha, cudaStream_t s) {
 int launch_near(tdw_problem* pb, int alpha, int g0, int g1, cudaStream_t s) {
   const long long threads = (long long)pb->ns * 32;
   const unsigned grid = (unsigned)((threads + 127) / 128);
-near_step_kernel<<<grid, 128, 0, s>>>(pb->d_nptr, pb->d_ncnt, pb->d_ncol_rm, pb->d_nval_rm,
-                                        (long long)pb->n_near, pb->ns, pb->nsl, pb->d_hist, pb->hcols,
-                                        pb->pad, pb->d_bnear, alpha, g0, g1, pb->d_flags, pb->d_trace);
+  const int nch = (pb->near_w + 31) / 32;
+#define TDW_NEAR_LAUNCH(N)                                                                                  \
+  near_step_kernel<N><<<grid, 128, 0, s>>>(pb->d_nptr, pb->d_ncnt, pb->d_ncol_rm, pb->d_nval_rm,            \
+                                           (long long)pb->n_near, pb->ns, pb->nsl, pb->d_hist, pb->hcols,   \
+                                           pb->pad, pb->d_bnear, alpha, g0, g1, pb->d_flags, pb->d_trace)
+  if (nch <= 4) TDW_NEAR_LAUNCH(4);
+  else if (nch <= 6) TDW_NEAR_LAUNCH(6);
+  else if (nch <= 8) TDW_NEAR_LAUNCH(8);
+  else if (nch <= 10) TDW_NEAR_LAUNCH(10);
+  else TDW_NEAR_LAUNCH(TDW_NEAR_MAX / 32);
+#undef TDW_NEAR_LAUNCH
   TDW_CUDA(pb->ctx, cudaGetLastError());
   return TDW_OK;
 }
@@ -1614,7 +1646,7 @@ near_step_kernel<<<grid, 128, 0, s>>>(pb->d_nptr, pb->d_ncnt, pb->d_ncol_rm, pb-
 // solve followed by all of its near terms on one stream (sequential loops)
 int launch_solve_near(tdw_problem* pb, LoopPlan& L, int alpha, cudaStream_t s) {
   int rc = launch_solve(pb, L, alpha, s);
-  const int g0 = pb->near_in_solve ? 1 : 0;  // lag 2 came from the solve's tail
+  const int g0 = pb->near_in_solve ? pb->near_tail : 0;  // lags 2..near_tail+1 came from the solve's tail
   if (rc == TDW_OK && pb->near_w > 0 && pb->split_lag2 && g0 < pb->nsl) rc = launch_near(pb, alpha, g0, pb->nsl, s);
   return rc;
 }
@@ -1670,16 +1702,18 @@ int enqueue_loop(tdw_problem* pb, LoopPlan& L, cudaEvent_t* ev_conv) {
       }
       // solve(s) reads the lag-3+ near terms near_step(s-2) wrote (lag 2: near_step(s-1), below)
       const bool side_near = near && (pb->near_split || pb->near_in_solve);
-      if (side_near && s - 2 >= 1) TDW_CUDA(ctx, cudaStreamWaitEvent(st, evN[s - 2], 0));
+      // near_step(s') writes lags >= g0 + 2 of x^(s'-1), first needed by solve(s' + g0 + 1)
+      const int g0n = pb->near_in_solve ? pb->near_tail : 1;
+      if (side_near && s - 1 - g0n >= 1) TDW_CUDA(ctx, cudaStreamWaitEvent(st, evN[s - 1 - g0n], 0));
       if ((rc = launch_solve(pb, L, s, st))) return rc;
       // evS[s] after the near terms: a convolution pass waiting for solve(s)
       // starts only once the near kernel has had the SMs it left free
       if (near && pb->near_in_solve) {
-        // lag 2 in the solve's tail; lags 3..nsl+1 beside solve(s+1) on the near stream
+        // lags 2..near_tail+1 in the solve's tail; the rest beside the next solves on the near stream
         TDW_CUDA(ctx, cudaEventRecord(evS[s], st));
-        if (pb->nsl > 1) {
+        if (pb->nsl > pb->near_tail) {
           TDW_CUDA(ctx, cudaStreamWaitEvent(sn, evS[s], 0));
-          if ((rc = launch_near(pb, s, 1, pb->nsl, sn))) return rc;
+          if ((rc = launch_near(pb, s, pb->near_tail, pb->nsl, sn))) return rc;
         }
         TDW_CUDA(ctx, cudaEventRecord(evN[s], sn));
       } else if (near && !pb->near_split) {
@@ -2226,28 +2260,35 @@ int tdw_setup_cluster_solver(tdw_problem* pb) {
     int rc = setup_halo(pb, acol, aval);
     if (rc) return rc;
   }
-  // lag-2 near terms computed in the halo solve's tail (TDW_NEAR_IN_SOLVE=0: off)
+  // near terms of the first split lags computed in the halo solve's tail
+  // (TDW_NEAR_IN_SOLVE = number of lags, default 1: each further lag costs the
+  // solve ~10 us on config 2; 0: all in near_step_kernel)
   pb->near_in_solve = false;
+  pb->near_tail = 0;
   {
     const char* e = getenv("TDW_NEAR_IN_SOLVE");
-    const bool want = e ? atoi(e) != 0 : true;
-    if (want && pb->sp_reg > 0 && pb->sp_halo > 0 && pb->split_lag2 && pb->near_w > 0) {
+    const int want = std::min(e ? atoi(e) : 1, pb->nsl);
+    if (want > 0 && pb->sp_reg > 0 && pb->sp_halo > 0 && pb->split_lag2 && pb->near_w > 0) {
       std::vector<int> ncol((size_t)TDW_NEAR_MAX * ns), cnt(ns);
-      std::vector<double> nv0((size_t)TDW_NEAR_MAX * ns);  // g = 0 slice of [nsl][TDW_NEAR_MAX][ns]
+      std::vector<double> nv((size_t)want * TDW_NEAR_MAX * ns);  // g < want slices of [nsl][TDW_NEAR_MAX][ns]
       TDW_CUDA(ctx, cudaMemcpy(ncol.data(), pb->d_ncol, sizeof(int) * ncol.size(), cudaMemcpyDeviceToHost));
-      TDW_CUDA(ctx, cudaMemcpy(nv0.data(), pb->d_nval, sizeof(double) * nv0.size(), cudaMemcpyDeviceToHost));
+      TDW_CUDA(ctx, cudaMemcpy(nv.data(), pb->d_nval, sizeof(double) * nv.size(), cudaMemcpyDeviceToHost));
       TDW_CUDA(ctx, cudaMemcpy(cnt.data(), pb->d_ncnt, sizeof(int) * ns, cudaMemcpyDeviceToHost));
-      std::vector<int> ptr(ns + 1, 0), col;
+      std::vector<int> ptr((size_t)want * (ns + 1), 0), col;
       std::vector<double> val;
-      for (int i = 0; i < ns; ++i) {
-        for (int k = 0; k < cnt[i]; ++k) {
-          const double w = nv0[(size_t)k * ns + i];
-          if (w == 0.0) continue;
-          const int j = ncol[(size_t)k * ns + i];
-          col.push_back(((j / R) << 24) | (j % R));
-          val.push_back(w);
+      for (int g = 0; g < want; ++g) {
+        int* pg = &ptr[(size_t)g * (ns + 1)];
+        pg[0] = (int)col.size();
+        for (int i = 0; i < ns; ++i) {
+          for (int k = 0; k < cnt[i]; ++k) {
+            const double w = nv[((size_t)g * TDW_NEAR_MAX + k) * ns + i];
+            if (w == 0.0) continue;
+            const int j = ncol[(size_t)k * ns + i];
+            col.push_back(((j / R) << 24) | (j % R));
+            val.push_back(w);
+          }
+          pg[i + 1] = (int)col.size();
         }
-        ptr[i + 1] = (int)col.size();
       }
       TDW_CUDA(ctx, cudaMalloc(&pb->d_n2_ptr, sizeof(int) * ptr.size()));
       TDW_CUDA(ctx, cudaMalloc(&pb->d_n2_col, sizeof(int) * std::max<size_t>(1, col.size())));
@@ -2258,6 +2299,7 @@ int tdw_setup_cluster_solver(tdw_problem* pb) {
         TDW_CUDA(ctx, cudaMemcpy(pb->d_n2_val, val.data(), sizeof(double) * val.size(), cudaMemcpyHostToDevice));
       }
       pb->near_in_solve = true;
+      pb->near_tail = want;
     }
   }
   if (CL > 8) {

@@ -145,6 +145,7 @@ struct tdw_problem {
   // lag-2 near terms inside the halo solve (its tail, x from DSMEM): CSR over the
   // rows, columns packed (owner CTA << 24) | owner-local row
   bool near_in_solve = false;
+  int near_tail = 0;                 // split lags 2..near_tail+1 formed in the solve's tail
   int* d_n2_ptr = nullptr;
   int* d_n2_col = nullptr;
   double* d_n2_val = nullptr;
