@@ -135,6 +135,14 @@ int tdw_march(tdw_problem* pb, const double* u_known, const double* q_known, dou
               double* u, double* q, double* tau, double* sigma, double* rhs_trace,
               int32_t* n_steps, int32_t* status);
 
+/* Pipelined form of tdw_march: the caller uploads the known rows [beta0, beta0 +
+ * nbeta) of u (which = 0) or q (1) as it produces them (src NULL = zeros), on the
+ * library stream, then runs the march on them.  Same outputs and errors as
+ * tdw_march; lets the host's Greville sampling overlap the copies. */
+int tdw_upload_known_rows(tdw_problem* pb, int which, int beta0, int nbeta, const double* src);
+int tdw_march_device_known(tdw_problem* pb, double threshold, double* u, double* q, double* tau,
+                           double* sigma, double* rhs_trace, int32_t* n_steps, int32_t* status);
+
 /* Benchmark form: known data already uploaded (tdw_upload_known), the time loop
  * runs n_repeat times on device-resident data; timings from CUDA events. */
 int tdw_upload_known(tdw_problem* pb, const double* u_known, const double* q_known);

@@ -425,6 +425,30 @@ int tdw_download(tdw_problem* pb, double* u, double* q, double* tau, double* sig
   return TDW_OK;
 }
 
+int tdw_upload_known_rows(tdw_problem* pb, int which, int beta0, int nbeta, const double* src) {
+  if (!pb || which < 0 || which > 1 || beta0 < 0 || nbeta < 0 || beta0 + nbeta > pb->nt - 1)
+    return TDW_ERR_INVALID_ARG;
+  tdw_ctx* ctx = pb->ctx;
+  cudaSetDevice(ctx->device);
+  const size_t n = (size_t)(pb->nt - 1) * pb->ns;
+  double** dst = which == 0 ? &pb->d_uk : &pb->d_qk;
+  if (!*dst) TDW_CUDA(ctx, cudaMalloc(dst, sizeof(double) * n));
+  const size_t off = (size_t)beta0 * pb->ns, cnt = (size_t)nbeta * pb->ns;
+  if (src)
+    TDW_CUDA(ctx, cudaMemcpyAsync(*dst + off, src, sizeof(double) * cnt, cudaMemcpyHostToDevice, ctx->stream));
+  else
+    TDW_CUDA(ctx, cudaMemsetAsync(*dst + off, 0, sizeof(double) * cnt, ctx->stream));
+  return TDW_OK;
+}
+
+int tdw_march_device_known(tdw_problem* pb, double threshold, double* u, double* q, double* tau,
+                           double* sigma, double* rhs_trace, int32_t* n_steps, int32_t* status) {
+  if (!pb || !pb->d_uk || !pb->d_qk) return TDW_ERR_INVALID_ARG;
+  pb->known_loaded = true;
+  pb->known_preloaded_call = true;
+  return tdw_march(pb, nullptr, nullptr, threshold, u, q, tau, sigma, rhs_trace, n_steps, status);
+}
+
 int tdw_march(tdw_problem* pb, const double* u_known, const double* q_known, double threshold,
               double* u, double* q, double* tau, double* sigma, double* rhs_trace,
               int32_t* n_steps, int32_t* status) {
@@ -433,7 +457,12 @@ int tdw_march(tdw_problem* pb, const double* u_known, const double* q_known, dou
   static const bool trace = getenv("TDW_TRACE_MARCH") != nullptr;
   auto now = [] { return std::chrono::steady_clock::now(); };
   auto t0 = now();
-  int rc = tdw_upload_known(pb, u_known, q_known);
+  // tdw_march_device_known: the rows are on the device already (both pointers NULL
+  // with known_loaded set by that entry point)
+  const bool preloaded = !u_known && !q_known && pb->known_loaded && pb->d_uk && pb->d_qk &&
+                         pb->known_preloaded_call;
+  int rc = preloaded ? TDW_OK : tdw_upload_known(pb, u_known, q_known);
+  pb->known_preloaded_call = false;
   if (rc) return rc;
   if (trace) {
     cudaStreamSynchronize(pb->ctx->stream);

@@ -142,6 +142,7 @@ struct tdw_problem {
   cudaStream_t side = nullptr;
   cudaStream_t side_near = nullptr;  // near terms of lags >= 3 (off the solve's critical path)
   bool near_split = false;
+  bool known_preloaded_call = false;  // tdw_march_device_known in progress
   // lag-2 near terms inside the halo solve (its tail, x from DSMEM): CSR over the
   // rows, columns packed (owner CTA << 24) | owner-local row
   bool near_in_solve = false;

@@ -111,16 +111,23 @@ def greville_times(spec) -> np.ndarray:
     return np.arange(spec.nt - 1) * basis.dt + 0.5 * (basis.d + 1) * basis.dt
 
 
-def sample_data(fn, times, out: np.ndarray) -> np.ndarray:
+def sample_data(fn, times, out: np.ndarray, on_chunk=None) -> np.ndarray:
     """out[k] = fn(times[k]).  A data callable may also expose the vectorised
-    form `fn.sample_many(times, out)` (same values, all steps at once); plain
-    callables are called once per step, as the reference does."""
+    form `fn.sample_many(times, out[, on_chunk])` (same values, all steps at
+    once; on_chunk(k0, k1) as rows become ready); plain callables are called
+    once per step, as the reference does.  on_chunk always covers every row."""
     many = getattr(fn, "sample_many", None)
     if many is not None:
-        many(times, out)
+        try:
+            many(times, out, on_chunk=on_chunk)
+            return out
+        except TypeError:
+            many(times, out)
     else:
         for k, t in enumerate(times):
             out[k] = fn(float(t))
+    if on_chunk is not None:
+        on_chunk(0, len(times))
     return out
 
 
@@ -271,20 +278,32 @@ def march(spec, window: bool = True, blowup_factor: float = 1e6, mats=None,
     # the library writes every entry
     out = _lib.pinned_empty((4, spec.nt - 1, spec.mesh.n_elements))
     hist.u, hist.q, hist.tau, hist.sigma = out[0], out[1], out[2], out[3]
-    # Greville samples straight into the store's page-locked buffers; a data
-    # callable that is None is passed as NULL (zero samples, set on the device)
+    # Greville samples straight into the store's page-locked buffers, each chunk
+    # of steps copied to the device as soon as it is written (the copies overlap
+    # the sampling); a data callable that is None gives zero samples on the device
+    lib = _lib.load()
     times = greville_times(spec)
-    uk = sample_data(spec.u_data, times, mats.pinned_known(0)) if spec.u_data is not None else None
-    qk = sample_data(spec.q_data, times, mats.pinned_known(1)) if spec.q_data is not None else None
+    nk = len(times)
+    for which, fn in ((0, spec.u_data), (1, spec.q_data)):
+        _lib.check(lib.tdw_upload_known_rows(mats.h, which, 0, 0 if fn is not None else nk, None),
+                   mats.ctx.h, "tdw_upload_known_rows")
+        if fn is None:
+            continue
+        buf = mats.pinned_known(which)
+
+        def on_chunk(k0, k1, which=which, buf=buf):
+            if k1 > k0:
+                _lib.check(lib.tdw_upload_known_rows(mats.h, which, k0, k1 - k0, _lib.dptr(buf[k0:k1])),
+                           mats.ctx.h, "tdw_upload_known_rows")
+        sample_data(fn, times, buf, on_chunk=on_chunk)
     threshold = blowup_factor * max(spec.blowup_reference, 1e-30)
     ns, nt = spec.mesh.n_elements, spec.nt
     rhs = np.zeros((nt - 1, ns)) if rhs_trace is not None else None
     n_steps, status = C.c_int32(0), C.c_int32(0)
-    rc = _lib.load().tdw_march(mats.h, _lib.dptr(uk) if uk is not None else None,
-                               _lib.dptr(qk) if qk is not None else None, float(threshold),
-                               _lib.dptr(hist.u), _lib.dptr(hist.q), _lib.dptr(hist.tau),
-                               _lib.dptr(hist.sigma), _lib.dptr(rhs) if rhs is not None else None,
-                               C.byref(n_steps), C.byref(status))
+    rc = lib.tdw_march_device_known(mats.h, float(threshold),
+                                    _lib.dptr(hist.u), _lib.dptr(hist.q), _lib.dptr(hist.tau),
+                                    _lib.dptr(hist.sigma), _lib.dptr(rhs) if rhs is not None else None,
+                                    C.byref(n_steps), C.byref(status))
     _lib.check(rc, mats.ctx.h, "march")
     mats.assembled = True
     hist.n_steps = int(n_steps.value)

@@ -43,7 +43,8 @@ def _pool():
     global _POOL
     if _POOL is None:
         from concurrent.futures import ThreadPoolExecutor
-        _POOL = ThreadPoolExecutor(max_workers=max(1, min(16, os.cpu_count() or 1)))
+        n = int(os.environ.get("TDW_SAMPLE_THREADS", "0")) or min(16, os.cpu_count() or 1)
+        _POOL = ThreadPoolExecutor(max_workers=max(1, n))
     return _POOL
 
 
@@ -65,7 +66,9 @@ class PlanePulseData:
             return -np.exp(-a * a)
         return -(self.nz * 2.0 * a / self.sig * np.exp(-a * a))
 
-    def sample_many(self, times, out):
+    def sample_many(self, times, out, on_chunk=None):
+        """out[k] = self(times[k]) for every k; on_chunk(k0, k1), if given, is
+        called (from a pool thread) as soon as rows k0..k1-1 are written."""
         times = np.asarray(times, dtype=np.float64)
         n = len(times)
         step = max(1, -(-n // 16))
@@ -87,6 +90,8 @@ class PlanePulseData:
                 a /= self.sig
                 np.multiply(a, o, out=o)
                 np.negative(o, out=o)
+            if on_chunk is not None:
+                on_chunk(k0, k1)
         list(_pool().map(chunk, range(0, n, step)))
         return out
 
