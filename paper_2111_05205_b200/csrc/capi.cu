@@ -320,7 +320,10 @@ int tdw_problem_create_impl(tdw_ctx* ctx, const tdw_problem_desc* dsc, tdw_probl
   // kappa-combined lags reach gamma = g + kappa <= gamma* with the window (marching.py:216-225)
   pb->cap = pb->window ? std::min(pb->gstar, pb->nt - 1) : pb->nt - 1;
   pb->pad = pb->cap + 1;
-  pb->hstride = pb->pad + pb->nt - 1;
+  // + TDW_KB_MAX zero rows at the end: the last convolution pass of a loop computes
+  // kb steps even when fewer remain, and its history slices reach past step nt-2
+  // (the extra steps are discarded, but their rows must be readable)
+  pb->hstride = pb->pad + pb->nt - 1 + TDW_KB_MAX;
   pb->hcols = pb->ntiles * TDW_TJ;
 
   // step buffers

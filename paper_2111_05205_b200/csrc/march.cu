@@ -382,7 +382,8 @@ __device__ __forceinline__ void conv_body(const ConvArgs& a, const CUtensorMap& 
           s1[r][0] = 0.0;
         }
 #pragma unroll
-        for (int i = 0; i < KB; ++i) hw[r][i] = lds_f64x2((unsigned)(hp[r] + i * TDW_TJ * 16));
+        for (int i = 0; i < KB; ++i)  // a unit without band entries has no history slice
+          hw[r][i] = g.y >= g.x ? lds_f64x2((unsigned)(hp[r] + i * TDW_TJ * 16)) : make_double2(0.0, 0.0);
       }
       lmax = __reduce_max_sync(FULLMASK, lmax);
       if (a.stats) {

@@ -279,3 +279,20 @@ def test_full_size_linearity_and_determinism(cfg):
         spec.u_data = lambda t: 2.0 * f(t)
     h3 = marching.march(spec, mats=store)
     np.testing.assert_array_equal(_unknown(h3, spec), 2.0 * x1)
+
+
+@pytest.mark.parametrize("cfg,nt,kb", [(2, 16, "6"), (2, 17, "4"), (0, 9, "6"), (1, 8, "5")])
+def test_short_loops_last_pass(cfg, nt, kb, monkeypatch):
+    """Loops whose last convolution pass has fewer steps than kb (its history
+    slices reach past the last step) run cleanly and match the oracle."""
+    monkeypatch.setenv("TDW_KB", kb)
+    spec = scenarios.build_spec(cfg, nt=nt)
+    h = marching.march(spec)
+    uk, qk = marching.greville_samples(spec)
+    r = oracle.march(spec.mesh.vertices, spec.mesh.triangles, spec.phi, spec.bie, spec.basis.d, spec.c,
+                     spec.basis.dt, spec.nt, uk, qk)
+    assert h.status == r["status"] and h.n_steps == r["n_steps"]
+    x, xr = (h.u, r["u"]) if spec.phi[0] == 1.0 else (h.q, r["q"])
+    n = np.linalg.norm(xr, axis=1)
+    err = np.linalg.norm(x - xr, axis=1) / np.maximum(n, 1e-6 * n.max())
+    assert err.max() < 1e-9

@@ -1,3 +1,3 @@
-timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -3
-for i in 1 2; do timeout 300 python bench.py --no-cpu 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['value'], d['e2e']['value'], d['roofline']['frac'], d['graph'])"; done
-TDW_TRACE_MARCH=1 timeout 120 python tools/e2e_probe.py 2 2>&1 | tail -4
+for nt in 16 32 64; do echo -n "cfg2 nt$nt: "; timeout 60 python tools/bisect_short.py 2 $nt; done
+echo -n "cfg1 nt16: "; timeout 60 python tools/bisect_short.py 1 16
+timeout 600 python -m pytest tests/test_gpu_march.py -x -q 2>&1 | tail -2

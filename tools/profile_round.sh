@@ -6,7 +6,7 @@ python bench.py --steps 2 --warmup 3 --no-cpu > gpurun_out/bench_plain_$tag.log 
 ncu --metrics gpu__time_duration.sum --clock-control none -c 4000 --csv --log-file gpurun_out/launches_$tag.csv \
     python bench.py --steps 2 --warmup 3 --no-cpu > gpurun_out/ncu_launch_$tag.log 2>&1
 python tools/prof_step.py 2 64 > gpurun_out/prof_plain_$tag.log 2>&1
-for k in conv_kernel solve_reg_kernel solve_halo_kernel near_step_kernel fill_kernel; do
+for k in conv_kernel solve_halo_kernel near_step_kernel; do
   ncu --set full --clock-control none --import-source on -k regex:$k -s 8 -c 1 -o gpurun_out/full_${tag}_$k \
       python tools/prof_step.py 2 64 > gpurun_out/ncu_${tag}_$k.log 2>&1 || true
 done
