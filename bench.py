@@ -255,6 +255,10 @@ def run_ours(args, world, rank, local):
     kind = "bm" if spec.bie == "bmbie" else "uw"
     cost = K1_COST[(kind, spec.basis.d)]
     evals_per_s = info["n_evals"] / (info["t_fill_ms"] * 1e-3)
+    try:  # the fill kernel's own FP64-pipe utilisation from the committed ncu capture
+        k1_ncu = json.loads((ROOT / "profiles" / "k1_fill.json").read_text())
+    except Exception:
+        k1_ncu = None
     k1_achieved = evals_per_s * cost * 2.0 / 1e12
 
     cpu = None
@@ -308,7 +312,8 @@ def run_ours(args, world, rank, local):
                                       "cost_per_eval": cost, "cost_model": "SURVEY 8(d): FP64 "
                                       "instruction-equivalents per evaluation (div/sqrt 20, atan 26, "
                                       "asinh 60); hoisting raises evals/s, the cost stays fixed",
-                                      "peak_source": "measured live (tdw_fp64_peak: DFMA chains)"}},
+                                      "peak_source": "measured live (tdw_fp64_peak: DFMA chains)",
+                                      "ncu": k1_ncu}},
             "graph": bool(tm.get("solve_ms", 0) > 0),
         }
         print(json.dumps(line), flush=True)

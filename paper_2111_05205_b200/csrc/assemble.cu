@@ -211,8 +211,11 @@ __global__ void __launch_bounds__(256) count_kernel(AsmArgs a) {
   }
 }
 
+#ifndef TDW_FILL_MINB
+#define TDW_FILL_MINB 3  // 168 registers, some spills: +6% (config 2), +11% (config 3) over 240 registers
+#endif
 template <int D, bool BM>
-__global__ void __launch_bounds__(128) fill_kernel(AsmArgs a) {
+__global__ void __launch_bounds__(128, TDW_FILL_MINB) fill_kernel(AsmArgs a) {
   const int lane = threadIdx.x & 31;
   const long long seg = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const long long nseg = (long long)a.rows_loc * a.ntiles;
