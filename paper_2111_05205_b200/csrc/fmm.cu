@@ -869,8 +869,10 @@ int fmm_check(tdw_problem* pb) {
 int tdw_fmm_loop(tdw_problem* pb, double threshold, bool want_rhs, tdw_timing* timing) {
   tdw_ctx* ctx = pb->ctx;
   cudaStream_t st = ctx->stream;
-  const bool multi = pb->nranks > 1;
-  if (multi && !ctx->comm)
+  // the exchange runs whenever the context has a communicator (a one-rank
+  // communicator exercises it on one GPU, as the direct loop does)
+  const bool multi = ctx->comm != nullptr;
+  if (pb->nranks > 1 && !ctx->comm)
     return tdw_fail(ctx, TDW_ERR_STATE, "sharded FMM problem without a communicator (tdw_comm_init)");
   FmmRun R;
   cudaEvent_t e0, e1;

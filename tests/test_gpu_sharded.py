@@ -103,3 +103,21 @@ def test_fmm_target_cell_shards_equal_single_rank(bie, d, Z, nt, nranks):
         np.testing.assert_array_equal(h.u, hs[0].u)
     pairs = [i["fmm_m2l_pairs"] for i in infos]
     assert pairs1 > 0 and max(pairs) < pairs1 and sum(pairs) >= pairs1
+
+
+def test_fmm_one_rank_nccl_exchange_path():
+    """The FMM loop's in-place ncclAllGather of b on a one-rank communicator gives
+    the communicator-free fast solver bit for bit."""
+    from paper_2111_05205_b200 import fmm, fmm_plan
+    spec = _fmm_spec("bmbie", 2, 40)
+    cfg = fmm_plan.FmmConfig(ps=4, pt=4, leaf_capacity=20)
+    ref = fmm.fast_march(spec, cfg)
+    lib = _lib.load()
+    ctx = _lib.Context(0)
+    buf = C.create_string_buffer(128)
+    _lib.check(lib.tdw_nccl_unique_id(buf), ctx.h, "tdw_nccl_unique_id")
+    _lib.check(lib.tdw_comm_init(ctx.h, buf.raw, 1, 0), ctx.h, "tdw_comm_init")
+    h = fmm.fast_march(spec, cfg, ctx=ctx, nranks=1, rank=0)
+    assert h.status == ref.status and h.n_steps == ref.n_steps
+    np.testing.assert_array_equal(h.u, ref.u)
+    ctx.close()

@@ -1,2 +1,1 @@
-timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
-python tools/prof_step.py 2 16 > gpurun_out/pp.log 2>&1 && timeout 600 ncu --set full --clock-control none --import-source on -k regex:fill_kernel -c 1 -o gpurun_out/full_r01d_fill3_kernel python tools/prof_step.py 2 16 > gpurun_out/ncu_r01d_fill3.log 2>&1; tail -1 gpurun_out/ncu_r01d_fill3.log
+timeout 900 python -m pytest tests/test_gpu_sharded.py tests/test_gpu_fmm.py -x -q 2>&1 | tail -3
