@@ -139,6 +139,8 @@ __global__ void extra_coeff_kernel(const double* __restrict__ elem, const int* _
   }
 }
 
+// one warp per row, lanes over the row's pairs (each lane runs its pair's lags),
+// fixed-order warp reduction: deterministic
 __global__ void extra_apply_kernel(const int* __restrict__ row_ptr, const int* __restrict__ col,
                                    const double* __restrict__ U, const double* __restrict__ W,
                                    int lags, int gmax, const double2* __restrict__ hist, int hcols,
@@ -147,16 +149,24 @@ __global__ void extra_apply_kernel(const int* __restrict__ row_ptr, const int* _
   if (flags[0] != 0) return;
   double w[5] = {0, 0, 0, 0, 0};
   bw(d, w);
-  for (int i = r0 + blockIdx.x * blockDim.x + threadIdx.x; i < r1; i += gridDim.x * blockDim.x) {
+  const int lane = threadIdx.x & 31;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int i = r0 + (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5); i < r1; i += nw) {
+    const int p0 = __ldg(row_ptr + i), p1 = __ldg(row_ptr + i + 1);
+    if (p0 == p1) continue;  // warp-uniform
     double acc = 0.0;
-    for (int p = row_ptr[i]; p < row_ptr[i + 1]; ++p) {
-      const int j = col[p];
+    for (int p = p0 + lane; p < p1; p += 32) {
+      const int j = __ldg(col + p);
+      const double* up = U + (size_t)p * lags;
+      const double* wp = W + (size_t)p * lags;
       for (int g = 1; g <= gmax; ++g) {
         const double2 ts = stock(hist, hcols, pad, j, alpha - g, d, w);
-        acc += U[(size_t)p * lags + g - 1] * ts.x - W[(size_t)p * lags + g - 1] * ts.y;
+        acc += __ldg(up + g - 1) * ts.x - __ldg(wp + g - 1) * ts.y;
       }
     }
-    b[i] += acc;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(FULLMASK, acc, o);
+    if (lane == 0) b[i] += acc;
   }
 }
 
@@ -825,7 +835,7 @@ int fmm_step_rhs(tdw_problem* pb, FmmRun& R, int alpha, cudaStream_t st) {
   for (auto& E : F->extra) {
     const int g = (int)E.gmax[alpha];
     if (g <= 0 || E.npair == 0) continue;
-    extra_apply_kernel<<<rblocks, 128, 0, st>>>(E.row_ptr, E.col, E.U, E.W, E.lags, g, pb->d_hist,
+    extra_apply_kernel<<<std::max(1, (nrow + 3) / 4), 128, 0, st>>>(E.row_ptr, E.col, E.U, E.W, E.lags, g, pb->d_hist,
                                                  pb->hcols, pb->pad, alpha, pb->d, F->r0, F->r1, b,
                                                  pb->d_flags);
   }
