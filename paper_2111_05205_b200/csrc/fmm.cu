@@ -272,15 +272,14 @@ __global__ void gather_kernel(const int* __restrict__ g_src, long long nil,
 __global__ void scatter_kernel(const int* __restrict__ g_obs, long long p0, long long np,
                                const double* __restrict__ Y, int nops, int mu, int d, int k,
                                int ncell, double* own, double* tmp) {
+  // grid (ceil(M / 256), np): block row = operator op, column = pair; coalesced
+  // column reads of Y (column-major, M = nops * 256) and contiguous 256-vectors out
   const int ring = mu + 3;
   const long long M = (long long)nops * FND;
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < np * M;
-       e += (long long)gridDim.x * blockDim.x) {
-    const long long p = e / M;
-    const int r = (int)(e % M);
-    const int op = r / FND, idx = r % FND;
-    const int cell = g_obs[p0 + p];
-    const double v = Y[e];
+  const int op = blockIdx.x, idx = threadIdx.x;
+  for (long long pp = blockIdx.y; pp < np; pp += gridDim.y) {
+    const int cell = __ldg(g_obs + p0 + pp);
+    const double v = __ldg(Y + pp * M + (long long)op * FND + idx);
     if (op <= mu)
       own[((size_t)((k + op + 1) % ring) * ncell + cell) * FND + idx] += v;
     else
@@ -709,7 +708,7 @@ int launch_m2l(tdw_problem* pb, FmmLevel& V, int k, cudaStream_t st) {
                                       V.Kop + (size_t)o * FND * M, M, V.X + (size_t)p0 * FND, FND,
                                       &zero, F->Y, M);
       if (bs != CUBLAS_STATUS_SUCCESS) return tdw_fail(ctx, TDW_ERR_CUDA, "cublasDgemm failed");
-      scatter_kernel<<<(int)std::min<long long>(2048, (np * M + 255) / 256), 256, 0, st>>>(
+      scatter_kernel<<<dim3(nops, (unsigned)std::min<long long>(np, 65535)), FND, 0, st>>>(
           V.g_obs, p0, np, F->Y, nops, F->mu, d, k, V.ncell, V.own, V.tmp);
     }
     TDW_CUDA(ctx, cudaGetLastError());
