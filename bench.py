@@ -161,6 +161,86 @@ def run_reference(args, world, rank):
     print(json.dumps(line), flush=True)
 
 
+def m2l_flops(plan, nt: int, d: int) -> float:
+    """M2L GEMM FLOPs of the whole FMM loop: per level tick 2 * 256 * (nops * 256) per
+    interaction pair this rank evaluates (nops = mu + 1 + d stacked operators); level
+    leaf - j ticks when the low j bits of the leaf tick are all 1 (csrc/fmm.cu tick())."""
+    from paper_2111_05205_b200 import fmm_plan
+    sch = fmm_plan.step_schedule(plan, nt)
+    n_ticks = int(sch["ticks_before"][nt - 1]) + 1
+    nops = plan.mu + 1 + d
+    total = 0.0
+    for L, lev in plan.levels.items():
+        j = plan.leaf - L
+        ticks = sum(1 for k in range(n_ticks) if (k & ((1 << j) - 1)) == (1 << j) - 1)
+        total += 2.0 * 256 * nops * 256 * len(lev.il_obs) * ticks
+    return total
+
+
+def run_fmm(args, world, rank, local, ctx, spec, barrier, max_over_ranks):
+    """Configs 3-4 on the interpolation FMM (fmm.fast_march's store, target-cell
+    sharded over the ranks): loop steps/s resident, e2e through march(), and the
+    M2L DGEMM FLOP rate of the whole loop against the live FP64 peak."""
+    import ctypes as C
+    import time as _time
+    from paper_2111_05205_b200 import _lib, fmm, fmm_plan, marching, scenarios
+    conf = fmm_plan.FmmConfig(ps=4, pt=4, leaf_capacity=20)
+    t0 = _time.perf_counter()
+    plan = fmm_plan.build_plan(spec, conf)
+    t_plan = _time.perf_counter() - t0
+    store = fmm.FmmStore(spec, conf, plan=plan, nranks=world, rank=rank).assemble()
+    info = store.info()
+    ns, nt = spec.mesh.n_elements, spec.nt
+    thr = 1e6 * max(spec.blowup_reference, 1e-30)
+    store.upload_known(*marching.greville_samples(spec))
+    for _ in range(args.warmup):
+        store.run_resident(thr, 1)
+    barrier()
+    with ClockSampler(local) as clk:
+        tm = store.run_resident(thr, args.steps)
+        barrier()
+    dev_ms = max_over_ranks(tm["total_ms"])
+    value = args.steps * (nt - 1) / (dev_ms * 1e-3)
+    for _ in range(max(2, args.warmup)):
+        h = marching.march(spec, mats=store)
+    barrier()
+    t0 = _time.perf_counter()
+    e2e_steps = max(2, args.steps)
+    for _ in range(e2e_steps):
+        h = marching.march(spec, mats=store)
+    barrier()
+    e2e = e2e_steps * (nt - 1) / max_over_ranks(_time.perf_counter() - t0)
+    fp64 = C.c_double(0.0)
+    _lib.check(_lib.load().tdw_fp64_peak(ctx.h, C.byref(fp64)), ctx.h, "tdw_fp64_peak")
+    # this rank's share of the M2L pairs (target-cell sharding) scales the FLOPs
+    flops = m2l_flops(plan, nt, spec.basis.d) * info["fmm_m2l_pairs"] / max(
+        1, sum(len(l.il_obs) for l in plan.levels.values()))
+    # per-GPU rate (the busiest rank) against the per-GPU peak
+    achieved = max_over_ranks(flops) / (dev_ms / args.steps * 1e-3) / 1e12
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dev_ms / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded BASELINE scenario, generated meshes and incident pulse)",
+            "config": {"workload": scenarios.DESCRIPTION[args.config] + ", interpolation FMM ps = pt = 4, "
+                       "Z = 20, mu = 8 (corrected algorithm)", "ns": ns, "nt": nt,
+                       "mot_steps_per_bench_step": nt - 1, "parallelism": f"target cells x{world}",
+                       "leaf_level": plan.leaf, "m2l_pairs_this_rank": info["fmm_m2l_pairs"],
+                       "near_band_entries": info["n_band"], "plan_host_s": t_plan},
+            "e2e": {"value": e2e, "unit": "steps/s",
+                    "h2d_bytes_per_step": sum(f is not None for f in (spec.u_data, spec.q_data)) * (nt - 1) * ns * 8,
+                    "d2h_bytes_per_step": 4 * (nt - 1) * ns * 8, "api": "marching.march(spec, mats=FmmStore)"},
+            "roofline": {"bound": "fp64", "achieved": achieved, "peak": fp64.value, "unit": "TFLOP/s",
+                         "frac": achieved / fp64.value, "traffic": None,
+                         "kernel": "M2L DGEMMs (cuBLAS, FP64 tensor path): FLOPs of the whole loop / loop time",
+                         "peak_source": "measured live (tdw_fp64_peak: DFMA chains)"},
+            "cpu_baseline": None, "clocks": clk.summary(), "gpu_launches": None,
+        }
+        print(json.dumps(line), flush=True)
+    store.close()
+
+
 def run_ours(args, world, rank, local):
     import numpy as np
     import torch
@@ -193,6 +273,8 @@ def run_ours(args, world, rank, local):
     thr = 1e6 * max(spec.blowup_reference, 1e-30)
 
     # assembly (K1 fused with the kappa combination): timed separately
+    if args.fmm:
+        return run_fmm(args, world, rank, local, ctx, spec, barrier, max_over_ranks)
     store = marching.BandStore(spec, nranks=world, rank=rank).assemble()
     info = store.info()
     uk, qk = marching.greville_samples(spec)
@@ -332,7 +414,10 @@ def main():
     ap.add_argument("--cpu-rows", type=int, default=64)
     ap.add_argument("--ref-rows", type=int, default=64)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--fmm", action="store_true", help="interpolation FMM path (configs 3-4; default for 4)")
     args = ap.parse_args()
+    if args.config == 4:
+        args.fmm = True  # the direct store of config 4 is ~200 GB
     world, rank, local = dist_env()
     if args.impl == "reference":
         run_reference(args, world, rank)
