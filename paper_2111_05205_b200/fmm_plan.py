@@ -24,7 +24,7 @@ from math import comb
 
 import numpy as np
 
-from .fmm_interp import InterpScheme, triangle_gauss_rule
+from .fmm_interp import TRI7_BARY, TRI7_W, InterpScheme, triangle_gauss_rule
 from .fmm_tree import build_tree
 from .tbasis import trunc_pow
 
@@ -158,19 +158,21 @@ def build_plan(spec, config: FmmConfig | None = None) -> FmmPlan:
     ex = cfg.element_extrapolation
     h = leaf.half_width
     n3 = ps ** 3
-    p2m_tau = np.zeros((ns, n3))
-    p2m_sig = np.zeros((ns, n3))
-    for e in range(ns):
-        centre = leaf.centres[plan.elem_cell[e]]
-        pts, wts = triangle_gauss_rule(np.stack([v0[e], v1[e], v2[e]]))
-        xi = (pts - centre) / h
-        w = [sch_s.weights(xi[:, k], ex) for k in range(3)]
-        dw = [sch_s.dweights(xi[:, k], ex) / h for k in range(3)]
-        n = mesh.normals[e]
-        p2m_tau[e] = np.einsum("g,ga,gb,gc->abc", wts, w[0], w[1], w[2]).reshape(-1)
-        p2m_sig[e] = (np.einsum("g,ga,gb,gc->abc", wts, n[0] * dw[0], w[1], w[2])
-                      + np.einsum("g,ga,gb,gc->abc", wts, w[0], n[1] * dw[1], w[2])
-                      + np.einsum("g,ga,gb,gc->abc", wts, w[0], w[1], n[2] * dw[2])).reshape(-1)
+    # all elements at once: 7-point rule points (ns, 7, 3) and weights (ns, 7)
+    E = np.stack([v0, v1, v2], axis=1)
+    pts = np.einsum("gk,ekc->egc", TRI7_BARY, E)
+    area = 0.5 * np.linalg.norm(np.cross(E[:, 1] - E[:, 0], E[:, 2] - E[:, 0]), axis=1)
+    wts = TRI7_W[None, :] * area[:, None]
+    xi = (pts - leaf.centres[plan.elem_cell][:, None, :]) / h
+    ng = xi.shape[1]
+    w = [sch_s.weights(xi[:, :, k].reshape(-1), ex).reshape(ns, ng, ps) for k in range(3)]
+    dw = [(sch_s.dweights(xi[:, :, k].reshape(-1), ex) / h).reshape(ns, ng, ps) for k in range(3)]
+    n = mesh.normals
+    p2m_tau = np.einsum("eg,ega,egb,egc->eabc", wts, w[0], w[1], w[2]).reshape(ns, n3)
+    p2m_sig = (np.einsum("eg,ega,egb,egc->eabc", wts, n[:, 0, None, None] * dw[0], w[1], w[2])
+               + np.einsum("eg,ega,egb,egc->eabc", wts, w[0], n[:, 1, None, None] * dw[1], w[2])
+               + np.einsum("eg,ega,egb,egc->eabc", wts, w[0], w[1], n[:, 2, None, None] * dw[2])
+               ).reshape(ns, n3)
     plan.p2m_tau = prefactor * p2m_tau
     plan.p2m_sig = prefactor * p2m_sig
     xi = (mesh.centroids - leaf.centres[plan.elem_cell]) / h
