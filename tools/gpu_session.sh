@@ -1,2 +1,4 @@
-timeout 900 python bench.py --config 4 --steps 2 --warmup 1 --no-cpu 2>&1 | tail -1
-timeout 600 python bench.py --config 3 --fmm --steps 2 --warmup 1 --no-cpu 2>&1 | tail -1
+timeout 1200 python -m pytest tests -m gpu -q 2>&1 | tail -2
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
+timeout 600 python bench.py 2>&1 | tail -1
+timeout 600 python bench.py --impl reference --steps 1 --warmup 0 2>&1 | tail -1 | cut -c1-400
