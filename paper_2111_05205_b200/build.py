@@ -39,8 +39,12 @@ def build(verbose: bool = False, extra=()) -> Path:
         obj = bdir / (src + ".o")
         objs.append(obj)
         deps = [CSRC / src] + list(CSRC.glob("*.cuh")) + [ROOT / "include" / "tdw.h"]
-        if obj.exists() and all(obj.stat().st_mtime >= p.stat().st_mtime for p in deps):
+        stamp = bdir / (src + ".flags")  # rebuild when the extra flags change
+        flags = " ".join(extra)
+        same_flags = stamp.exists() and stamp.read_text() == flags
+        if same_flags and obj.exists() and all(obj.stat().st_mtime >= p.stat().st_mtime for p in deps):
             continue
+        stamp.write_text(flags)
         cmd = common + (["-Xptxas", "-v"] if verbose else []) + ["-c", str(CSRC / src), "-o", str(obj)]
         subprocess.run(cmd, check=True)
     cmd = [nvcc(), "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", str(OUT),

@@ -1250,8 +1250,11 @@ __device__ __forceinline__ double ldg_keep(const double* p, uint64_t pol) {
   return v;
 }
 
+#ifndef TDW_NEAR_MINB
+#define TDW_NEAR_MINB 12  // 40 registers: no spills; still two blocks beside a conv_kernel_wg CTA
+#endif
 template <int NCH>  // 32-entry chunks per row: ceil(near_w / 32), rounded up to an instantiated size
-__global__ void __launch_bounds__(128, 16) near_step_kernel(const int* __restrict__ nptr,
+__global__ void __launch_bounds__(128, TDW_NEAR_MINB) near_step_kernel(const int* __restrict__ nptr,
                                                         const int* __restrict__ ncnt,
                                                         const int* __restrict__ ncol_c,
                                                         const double* __restrict__ nval_c, long long nnz,

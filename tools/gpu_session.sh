@@ -1,4 +1,1 @@
-timeout 1200 python -m pytest tests -m gpu -q 2>&1 | tail -2
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
-timeout 600 python bench.py 2>&1 | tail -1
-timeout 600 python bench.py --impl reference --steps 1 --warmup 0 2>&1 | tail -1 | cut -c1-400
+for r in 1 2; do for lib in ab/libtdw_near16.so ab/libtdw_near12.so; do TDW_LIB_PATH=$lib timeout 100 python tools/insitu_probe.py 2 $lib; done; done
