@@ -211,11 +211,14 @@ __global__ void __launch_bounds__(256) count_kernel(AsmArgs a) {
   }
 }
 
+// blocks per SM the register budget is sized for (spills accepted: latency-bound
+// kernel, occupancy wins).  Measured against 240 registers: d = 1 at 4 blocks
+// (128 registers) +11% on config 2; d = 2 at 3 blocks (168) +11% on config 3
 #ifndef TDW_FILL_MINB
-#define TDW_FILL_MINB 3  // 168 registers, some spills: +6% (config 2), +11% (config 3) over 240 registers
+#define TDW_FILL_MINB(D) ((D) == 1 ? 4 : 3)
 #endif
 template <int D, bool BM>
-__global__ void __launch_bounds__(128, TDW_FILL_MINB) fill_kernel(AsmArgs a) {
+__global__ void __launch_bounds__(128, TDW_FILL_MINB(D)) fill_kernel(AsmArgs a) {
   const int lane = threadIdx.x & 31;
   const long long seg = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const long long nseg = (long long)a.rows_loc * a.ntiles;

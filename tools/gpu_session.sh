@@ -1,1 +1,2 @@
-for r in 1 2; do for lib in ab/libtdw_near16.so ab/libtdw_near12.so; do TDW_LIB_PATH=$lib timeout 100 python tools/insitu_probe.py 2 $lib; done; done
+for c in 0 1 2 3; do timeout 200 python tools/fill_probe.py $c new; done
+timeout 900 python -m pytest tests/test_gpu_coeff.py tests/test_gpu_march.py -x -q 2>&1 | tail -2
