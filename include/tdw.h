@@ -143,6 +143,15 @@ int tdw_upload_known_rows(tdw_problem* pb, int which, int beta0, int nbeta, cons
 int tdw_march_device_known(tdw_problem* pb, double threshold, double* u, double* q, double* tau,
                            double* sigma, double* rhs_trace, int32_t* n_steps, int32_t* status);
 
+/* Device-side boundary data (no reference counterpart): the
+ * Greville samples of the incident Gaussian plane pulse exp(-((t - z - t0)/sig)^2)
+ * at the centroids (zc, nz: (ns,) centroid z and normal z, caller's element
+ * order) computed on the device into the u (which = 0, -u_in) or q (1,
+ * -du_in/dn) known data.  Follow with tdw_upload_known_rows(.., NULL) for a
+ * None callable and tdw_march_device_known. */
+int tdw_known_plane_pulse(tdw_problem* pb, int which, const double* zc, const double* nz, double t0,
+                          double sig);
+
 /* Benchmark form: known data already uploaded (tdw_upload_known), the time loop
  * runs n_repeat times on device-resident data; timings from CUDA events. */
 int tdw_upload_known(tdw_problem* pb, const double* u_known, const double* q_known);

@@ -57,3 +57,52 @@ extern "C" int tdw_fp64_peak(tdw_ctx* ctx, double* tflops) {
   *tflops = flop / (best * 1e-3) / 1e12;
   return TDW_OK;
 }
+
+// ---------------------------------------------------------------------------
+// Device-side boundary data: the Greville samples of the
+// incident Gaussian plane pulse u_in(x, t) = exp(-((t - z - t0) / sig)^2) at the
+// centroids, written straight into the known-data buffers -- no host sampling,
+// no H2D copy.  which = 0: Dirichlet datum u = -u_in; 1: Neumann datum
+// q = -du_in/dn = -(n_z 2 a / sig) exp(-a^2).  Same expression as
+// scenarios.PlanePulseData (values agree to the last bits of exp).
+namespace tdw {
+__global__ void plane_pulse_kernel(double* out, int nbeta, int ns, const double* __restrict__ zc,
+                                   const double* __restrict__ nz, double dt, double off, double t0,
+                                   double sig, int which) {
+  const long long n = (long long)nbeta * ns;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int beta = (int)(e / ns), j = (int)(e % ns);
+    const double t = (double)beta * dt + off;
+    const double a = (t - zc[j] - t0) / sig;
+    const double ex = exp(-a * a);
+    out[e] = which == 0 ? -ex : -(nz[j] * 2.0 * a / sig * ex);
+  }
+}
+}  // namespace tdw
+
+extern "C" int tdw_known_plane_pulse(tdw_problem* pb, int which, const double* zc, const double* nz,
+                                     double t0, double sig) {
+  if (!pb || which < 0 || which > 1 || !zc || (which == 1 && !nz) || !(sig > 0.0)) return TDW_ERR_INVALID_ARG;
+  tdw_ctx* ctx = pb->ctx;
+  cudaSetDevice(ctx->device);
+  const int ns = pb->ns, nb = pb->nt - 1;
+  const size_t n = (size_t)nb * ns;
+  double** dst = which == 0 ? &pb->d_uk : &pb->d_qk;
+  if (!*dst) TDW_CUDA(ctx, cudaMalloc(dst, sizeof(double) * n));
+  double *dz = nullptr, *dn = nullptr;
+  TDW_CUDA(ctx, cudaMalloc(&dz, sizeof(double) * ns));
+  TDW_CUDA(ctx, cudaMemcpyAsync(dz, zc, sizeof(double) * ns, cudaMemcpyHostToDevice, ctx->stream));
+  if (nz) {
+    TDW_CUDA(ctx, cudaMalloc(&dn, sizeof(double) * ns));
+    TDW_CUDA(ctx, cudaMemcpyAsync(dn, nz, sizeof(double) * ns, cudaMemcpyHostToDevice, ctx->stream));
+  }
+  const double off = 0.5 * (pb->d + 1) * pb->dt;  // Greville abscissae (marching.py:264-266)
+  tdw::plane_pulse_kernel<<<4 * ctx->num_sms, 256, 0, ctx->stream>>>(*dst, nb, ns, dz, dn, pb->dt, off, t0,
+                                                                      sig, which);
+  TDW_CUDA(ctx, cudaGetLastError());
+  TDW_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  cudaFree(dz);
+  if (dn) cudaFree(dn);
+  return TDW_OK;
+}

@@ -261,7 +261,7 @@ def build_retarded_matrices(spec, gamma_max: int | None = None, pairs=None, slab
 
 
 def march(spec, window: bool = True, blowup_factor: float = 1e6, mats=None,
-          rhs_trace: list | None = None) -> TimeHistory:
+          rhs_trace: list | None = None, device_data: bool = False) -> TimeHistory:
     """Run the conventional time marching on the GPU (marching.py:292-338).
 
     gamma* and the lag count are computed by the library from the mesh
@@ -284,7 +284,20 @@ def march(spec, window: bool = True, blowup_factor: float = 1e6, mats=None,
     lib = _lib.load()
     times = greville_times(spec)
     nk = len(times)
+    # device_data: data callables that describe themselves (the incident plane
+    # pulse, scenarios.PlanePulseData.device_form) are sampled on the device
+    dev = {}
+    if device_data:
+        for which, fn in ((0, spec.u_data), (1, spec.q_data)):
+            form = getattr(fn, "device_form", None)
+            if fn is not None and form is not None and getattr(fn, "kind", None) == ("u", "q")[which]:
+                dev[which] = form()
+    for which, (zc, nz, t0, sig) in dev.items():
+        _lib.check(lib.tdw_known_plane_pulse(mats.h, which, _lib.dptr(zc), _lib.dptr(nz), float(t0), float(sig)),
+                   mats.ctx.h, "tdw_known_plane_pulse")
     for which, fn in ((0, spec.u_data), (1, spec.q_data)):
+        if which in dev:
+            continue
         _lib.check(lib.tdw_upload_known_rows(mats.h, which, 0, 0 if fn is not None else nk, None),
                    mats.ctx.h, "tdw_upload_known_rows")
         if fn is None:

@@ -60,6 +60,11 @@ class PlanePulseData:
     def __init__(self, kind: str, zc, nz, t0: float, sig: float):
         self.kind, self.zc, self.nz, self.t0, self.sig = kind, zc, nz, float(t0), float(sig)
 
+    def device_form(self):
+        """(zc, nz, t0, sig) for the device-side sampler (tdw_known_plane_pulse)."""
+        return (np.ascontiguousarray(self.zc, dtype=np.float64), np.ascontiguousarray(self.nz, dtype=np.float64),
+                self.t0, self.sig)
+
     def __call__(self, t):
         a = (t - self.zc - self.t0) / self.sig
         if self.kind == "u":

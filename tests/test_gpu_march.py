@@ -296,3 +296,19 @@ def test_short_loops_last_pass(cfg, nt, kb, monkeypatch):
     n = np.linalg.norm(xr, axis=1)
     err = np.linalg.norm(x - xr, axis=1) / np.maximum(n, 1e-6 * n.max())
     assert err.max() < 1e-9
+
+
+@pytest.mark.parametrize("cfg", [1, 2])
+def test_device_side_boundary_data(cfg):
+    """march(device_data=True) samples the incident plane pulse on the device
+    (tdw_known_plane_pulse): the same densities as the host-sampled march, to
+    the last bits of exp."""
+    spec = scenarios.build_spec(cfg)
+    store = marching.BandStore(spec).assemble()
+    h = marching.march(spec, mats=store)
+    hd = marching.march(spec, mats=store, device_data=True)
+    assert hd.status == h.status and hd.n_steps == h.n_steps
+    for a, b in ((hd.u, h.u), (hd.q, h.q)):
+        n = np.linalg.norm(b, axis=1)
+        assert (np.linalg.norm(a - b, axis=1) / np.maximum(n, 1e-6 * max(n.max(), 1e-300))).max() < 1e-12
+    store.close()
