@@ -1,11 +1,3 @@
-timeout 900 python -m pytest tests/test_gpu_march.py -x -q -k "device_side" 2>&1 | tail -2
-timeout 200 python -c "
-import sys, time; sys.path.insert(0,'.')
-from paper_2111_05205_b200 import marching, scenarios
-spec=scenarios.build_spec(2); st=marching.BandStore(spec).assemble()
-for dd in (False, True, False, True):
-    for _ in range(2): marching.march(spec, mats=st, device_data=dd)
-    t0=time.perf_counter()
-    for _ in range(5): h=marching.march(spec, mats=st, device_data=dd)
-    print('device_data', dd, 255*5/(time.perf_counter()-t0), 'steps/s', flush=True)
-"
+timeout 1200 python -m pytest tests -m gpu -q 2>&1 | tail -2
+python tools/prof_step.py 2 16 > gpurun_out/pp.log 2>&1 && timeout 600 ncu --set full --clock-control none --import-source on -k regex:fill_kernel -c 1 -o gpurun_out/full_r01e_fill_kernel python tools/prof_step.py 2 16 > gpurun_out/ncu_r01e_fill.log 2>&1; tail -1 gpurun_out/ncu_r01e_fill.log
+timeout 600 python bench.py > gpurun_out/bench_final.log 2>&1; tail -1 gpurun_out/bench_final.log | cut -c1-300
