@@ -2265,13 +2265,15 @@ int tdw_setup_cluster_solver(tdw_problem* pb) {
     if (rc) return rc;
   }
   // near terms of the first split lags computed in the halo solve's tail
-  // (TDW_NEAR_IN_SOLVE = number of lags, default 1: each further lag costs the
-  // solve ~10 us on config 2; 0: all in near_step_kernel)
+  // (TDW_NEAR_IN_SOLVE = number of lags; each lag costs the solve ~5-10 us on
+  // config 2; 0: all in near_step_kernel)
   pb->near_in_solve = false;
   pb->near_tail = 0;
   {
     const char* e = getenv("TDW_NEAR_IN_SOLVE");
-    const int want = std::min(e ? atoi(e) : 1, pb->nsl);
+    // default: 2 lags at kb >= 6 (config 2: +3%, the near step then has three solves
+    // of slack), else 1 (config 1: each extra lag costs a solve-bound loop ~35%)
+    const int want = std::min(e ? atoi(e) : (pb->kb >= 6 ? 2 : 1), pb->nsl);
     if (want > 0 && pb->sp_reg > 0 && pb->sp_halo > 0 && pb->split_lag2 && pb->near_w > 0) {
       std::vector<int> ncol((size_t)TDW_NEAR_MAX * ns), cnt(ns);
       std::vector<double> nv((size_t)want * TDW_NEAR_MAX * ns);  // g < want slices of [nsl][TDW_NEAR_MAX][ns]

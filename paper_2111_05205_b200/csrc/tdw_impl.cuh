@@ -14,7 +14,7 @@
 #define TDW_TI 32        // rows per I-block (one conv CTA)
 #define TDW_ELL_MAX 64   // max nnz per row of the lag-1 step matrix
 #define TDW_KB_MAX 6     // time steps per convolution pass (temporal blocking)
-#define TDW_NEAR_MAX 256 // max pairs per row in the near structure (bands reaching a split lag)
+#define TDW_NEAR_MAX 320 // max pairs per row in the near structure (bands reaching a split lag)
 #define TDW_NSL_MAX (2 * TDW_KB_MAX - 1)  // max split lags
 #define TDW_ELEM_STRIDE 16  // doubles per element record: v0 v1 v2 n c rad
 // Unit layout (one (I-block, J-tile) unit = one contiguous byte range of the store):
