@@ -1142,21 +1142,30 @@ __global__ void __launch_bounds__(reg_threads<MAXNZ>(), 1) solve_halo_kernel(Clu
   if (a.ntail > 0 && own) {
     for (int t = 0; t < a.ntail; ++t) {
       const int* ptr = a.n2_ptr + (size_t)t * (a.ns + 1);
-      double s0 = 0.0, s1 = 0.0;
+      // four independent chains, all loads of a group of four in flight
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
       const int q0 = __ldg(ptr + gi), q1 = __ldg(ptr + gi + 1);
       int q = q0;
-      for (; q + 1 < q1; q += 2) {
+      for (; q + 3 < q1; q += 4) {
         const int c0 = __ldg(a.n2_col + q), c1 = __ldg(a.n2_col + q + 1);
+        const int c2 = __ldg(a.n2_col + q + 2), c3 = __ldg(a.n2_col + q + 3);
         const double w0 = __ldg(a.n2_val + q), w1 = __ldg(a.n2_val + q + 1);
-        s0 = fma(w0, *cl.map_shared_rank(ex + p * T + (c0 & 0xffffff), c0 >> 24), s0);
-        s1 = fma(w1, *cl.map_shared_rank(ex + p * T + (c1 & 0xffffff), c1 >> 24), s1);
+        const double w2 = __ldg(a.n2_val + q + 2), w3 = __ldg(a.n2_val + q + 3);
+        const double x0 = *cl.map_shared_rank(ex + p * T + (c0 & 0xffffff), c0 >> 24);
+        const double x1 = *cl.map_shared_rank(ex + p * T + (c1 & 0xffffff), c1 >> 24);
+        const double x2 = *cl.map_shared_rank(ex + p * T + (c2 & 0xffffff), c2 >> 24);
+        const double x3 = *cl.map_shared_rank(ex + p * T + (c3 & 0xffffff), c3 >> 24);
+        s0 = fma(w0, x0, s0);
+        s1 = fma(w1, x1, s1);
+        s2 = fma(w2, x2, s2);
+        s3 = fma(w3, x3, s3);
       }
-      if (q < q1) {
+      for (; q < q1; ++q) {
         const int c0 = __ldg(a.n2_col + q);
         s0 = fma(__ldg(a.n2_val + q), *cl.map_shared_rank(ex + p * T + (c0 & 0xffffff), c0 >> 24), s0);
       }
       const int ring = a.nsl + 1;
-      a.bnear[((size_t)t * ring + (a.alpha + 1 + t) % ring) * a.ns + gi] = s0 + s1;
+      a.bnear[((size_t)t * ring + (a.alpha + 1 + t) % ring) * a.ns + gi] = (s0 + s1) + (s2 + s3);
     }
   }
   // residual with the final x: own rows from ex[p], layer-1 columns gathered fresh
