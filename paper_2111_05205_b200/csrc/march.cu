@@ -175,11 +175,15 @@ template <int RPW, bool PWG>
 __host__ __device__ constexpr int conv_threads() { return (TDW_TI / RPW) * 32 + (PWG ? 128 : 32); }
 constexpr int kConvLaunchRegsPWG = 144;
 constexpr int kConvProducerRegs = 32;
-template <int RPW>
+template <int RPW, int LREGS = kConvLaunchRegsPWG>
 __host__ __device__ constexpr int conv_consumer_regs() {
-  return kConvLaunchRegsPWG + ((kConvLaunchRegsPWG - kConvProducerRegs) * 128 / ((TDW_TI / RPW) * 32)) / 8 * 8;
+  return LREGS + ((LREGS - kConvProducerRegs) * 128 / ((TDW_TI / RPW) * 32)) / 8 * 8;
 }
 static_assert(conv_consumer_regs<4>() == 200, "register split");
+// RPW = 2 with a producer warpgroup (experiments, TDW_RPW=3): 640 threads at 96
+// registers, consumers grow to 112
+constexpr int kConvLaunchRegsPWG2 = 96;
+static_assert(conv_consumer_regs<2, kConvLaunchRegsPWG2>() == 112, "register split");
 
 // K2: history convolution.  Persistent CTAs walk a precomputed list of store
 // units.  Warp 8 (producer) streams each unit -- one contiguous byte range:
@@ -193,7 +197,7 @@ static_assert(conv_consumer_regs<4>() == 200, "register split");
 // read of the store.  Step alpha+i at lag g reads time alpha+i-g, i.e. row
 // (gmax - g + i) of the unit's history box of wbox+KB-1 rows starting at time
 // alpha-gmax.  Every coefficient is read from shared memory once and used KB times.
-template <int KB, int RPW, bool PWG>
+template <int KB, int RPW, bool PWG, int LREGS = kConvLaunchRegsPWG>
 __device__ __forceinline__ void conv_body(const ConvArgs& a, const CUtensorMap& hmap) {
   constexpr int CW = TDW_TI / RPW;  // consumer warps
   extern __shared__ __align__(128) unsigned char sm[];
@@ -318,7 +322,7 @@ __device__ __forceinline__ void conv_body(const ConvArgs& a, const CUtensorMap& 
     return;
   }
   // ---------------- consumers ----------------
-  if constexpr (PWG) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(conv_consumer_regs<RPW>()));
+  if constexpr (PWG) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(conv_consumer_regs<RPW, LREGS>()));
   double acc[RPW][KB];
 #pragma unroll
   for (int r = 0; r < RPW; ++r)
@@ -475,6 +479,10 @@ __global__ void __launch_bounds__(conv_threads<2, false>(), 1)
 template <int KB>
 __global__ void __maxnreg__(kConvLaunchRegsPWG) conv_kernel_wg(ConvArgs a, const __grid_constant__ CUtensorMap hmap) {
   conv_body<KB, 4, true>(a, hmap);
+}
+template <int KB>
+__global__ void __maxnreg__(kConvLaunchRegsPWG2) conv_kernel_wg2(ConvArgs a, const __grid_constant__ CUtensorMap hmap) {
+  conv_body<KB, 2, true, kConvLaunchRegsPWG2>(a, hmap);
 }
 
 // fixed-order sum of a row's split partials, loads issued 8 at a time
@@ -1424,6 +1432,13 @@ static int make_hist_map(tdw_problem* pb, CUtensorMap* map) {
 // forever if the kernel were allocated fewer registers than it assumes
 static cudaError_t conv_set_smem(int kb, int rpw, int smem) {
 #define X(K)                                                                                           \
+  if (kb == K && rpw == 3) {                                                                           \
+    cudaFuncAttributes fa;                                                                             \
+    cudaError_t e = cudaFuncGetAttributes(&fa, conv_kernel_wg2<K>);                                    \
+    if (e != cudaSuccess) return e;                                                                    \
+    if (fa.numRegs != kConvLaunchRegsPWG2) return cudaErrorInvalidConfiguration;                       \
+    return cudaFuncSetAttribute(conv_kernel_wg2<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); \
+  }                                                                                                    \
   if (kb == K && rpw == 2)                                                                             \
     return cudaFuncSetAttribute(conv_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);    \
   if (kb == K) {                                                                                       \
@@ -1440,6 +1455,10 @@ static cudaError_t conv_set_smem(int kb, int rpw, int smem) {
 static void conv_launch(int kb, int rpw, dim3 grid, size_t smem, cudaStream_t s, const ConvArgs& c,
                         const CUtensorMap& hmap) {
 #define X(K)                                                                              \
+  if (kb == K && rpw == 3) {                                                              \
+    conv_kernel_wg2<K><<<grid, conv_threads<2, true>(), smem, s>>>(c, hmap);              \
+    return;                                                                               \
+  }                                                                                       \
   if (kb == K && rpw == 2) {                                                              \
     conv_kernel<K><<<grid, conv_threads<2, false>(), smem, s>>>(c, hmap);                 \
     return;                                                                               \
@@ -1456,7 +1475,7 @@ static void fill_conv_args(tdw_problem* pb, ConvArgs& c) {
   {
     const char* r = getenv("TDW_RPW");
     const int rpw = r ? atoi(r) : (pb->kb >= 5 ? 4 : 2);
-    pb->conv_rpw = rpw == 4 ? 4 : 2;
+    pb->conv_rpw = rpw == 4 ? 4 : (rpw == 3 ? 3 : 2);  // 3: RPW 2 with a producer warpgroup
   }
   c.wbox = pb->wbox;
   c.stats = nullptr;

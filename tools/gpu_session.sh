@@ -1,4 +1,5 @@
-timeout 600 python -m pytest tests/test_gpu_march.py -q -x 2>&1 | tail -1
-for i in 1 2; do timeout 100 python tools/insitu_probe.py 2 "tail4" 2>&1 | tail -1; done
-timeout 100 python tools/trace_solve.py 2 2>&1 | grep "phases\|timeline" | tail -2
-timeout 100 python tools/insitu_probe.py 1 "cfg1" 2>&1 | tail -1
+for i in 1 2; do
+TDW_LIB_PATH=ab/libtdw_near16.so TDW_RPW=3 timeout 100 python tools/insitu_probe.py 2 "near32regs rpw3 kb6" 2>&1 | tail -1
+TDW_LIB_PATH=ab/libtdw_near16.so timeout 100 python tools/insitu_probe.py 2 "near32regs rpw4 kb6" 2>&1 | tail -1
+timeout 100 python tools/insitu_probe.py 2 "current" 2>&1 | tail -1
+done
