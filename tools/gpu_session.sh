@@ -1,5 +1,4 @@
-for i in 1 2; do
-TDW_LIB_PATH=ab/libtdw_near16.so TDW_RPW=3 timeout 100 python tools/insitu_probe.py 2 "near32regs rpw3 kb6" 2>&1 | tail -1
-TDW_LIB_PATH=ab/libtdw_near16.so timeout 100 python tools/insitu_probe.py 2 "near32regs rpw4 kb6" 2>&1 | tail -1
-timeout 100 python tools/insitu_probe.py 2 "current" 2>&1 | tail -1
-done
+timeout 900 python -m pytest tests/test_gpu_march.py tests/test_gpu_sharded.py -q -x 2>&1 | tail -1
+for i in 1 2; do for pk in 1 0; do TDW_NEAR_PACKED=$pk timeout 100 python tools/insitu_probe.py 2 "packed$pk" 2>&1 | tail -1; done; done
+TDW_NEAR_PACKED=1 timeout 100 python tools/trace_solve.py 2 2>&1 | grep "timeline\|near structure" | tail -2
+for c in 0 1; do TDW_NEAR_PACKED=1 timeout 100 python tools/insitu_probe.py $c "packed" 2>&1 | tail -1; done
