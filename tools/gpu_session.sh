@@ -1,4 +1,8 @@
-timeout 900 python -m pytest tests/test_gpu_march.py tests/test_gpu_sharded.py -q -x 2>&1 | tail -1
-for i in 1 2; do for pk in 1 0; do TDW_NEAR_PACKED=$pk timeout 100 python tools/insitu_probe.py 2 "packed$pk" 2>&1 | tail -1; done; done
-TDW_NEAR_PACKED=1 timeout 100 python tools/trace_solve.py 2 2>&1 | grep "timeline\|near structure" | tail -2
-for c in 0 1; do TDW_NEAR_PACKED=1 timeout 100 python tools/insitu_probe.py $c "packed" 2>&1 | tail -1; done
+for t in 2 3 4; do TDW_LIB_PATH=ab/libtdw_nm384.so TDW_NEAR_IN_SOLVE=$t timeout 100 python tools/insitu_probe.py 2 "nm384 tail$t" 2>&1 | tail -1; done
+TDW_LIB_PATH=ab/libtdw_nm384.so TDW_NEAR_IN_SOLVE=3 timeout 100 python tools/trace_solve.py 2 2>&1 | grep "timeline\|pass_overlap" | python -c "
+import sys
+for l in sys.stdin:
+    if l.startswith('{'):
+        d=eval(l); print('m', d['pass_overlap'], 'near_w', d['near_width'])
+    else: print(l.strip())"
+timeout 100 python tools/insitu_probe.py 2 "current" 2>&1 | tail -1
