@@ -12,8 +12,17 @@
  *                          + build_step_matrix                    marching.py:279-289
  *   tdw_march           <- marching.march (+greville inputs,      marching.py:292-338
  *                          TimeHistory outputs)                   marching.py:184-276
+ *   tdw_upload_known_rows + tdw_march_device_known
+ *                       <- marching.march, pipelined form           marching.py:292-338
+ *                          (known rows copied as they are sampled)
+ *   tdw_fmm_setup       <- fmm.fast_march's operator setup          fmm.py:165-531 (corrected,
+ *                          (then tdw_assemble / tdw_march)          SURVEY 8(c)), fmm.py:534-544
  *   tdw_march_resident  <- same time loop, inputs/outputs resident on the device (benchmark form)
  *   tdw_nccl_unique_id / tdw_comm_init  <- (none in the reference; row-sharded multi-GPU)
+ *   tdw_known_plane_pulse <- (none: device-side boundary data)
+ *   tdw_fp64_peak, tdw_host_alloc / tdw_host_free, tdw_time_conv, tdw_set_graph,
+ *   tdw_problem_create_shard / tdw_march_emulated  <- (none: diagnostics, pinned
+ *                          memory, one-GPU emulation of the sharded paths)
  *
  * Host buffers are C-contiguous float64 / int64; the library copies in and out
  * and owns all device memory behind the opaque handles.  A ctx is bound to one
