@@ -1,8 +1,4 @@
-for t in 2 3 4; do TDW_LIB_PATH=ab/libtdw_nm384.so TDW_NEAR_IN_SOLVE=$t timeout 100 python tools/insitu_probe.py 2 "nm384 tail$t" 2>&1 | tail -1; done
-TDW_LIB_PATH=ab/libtdw_nm384.so TDW_NEAR_IN_SOLVE=3 timeout 100 python tools/trace_solve.py 2 2>&1 | grep "timeline\|pass_overlap" | python -c "
-import sys
-for l in sys.stdin:
-    if l.startswith('{'):
-        d=eval(l); print('m', d['pass_overlap'], 'near_w', d['near_width'])
-    else: print(l.strip())"
-timeout 100 python tools/insitu_probe.py 2 "current" 2>&1 | tail -1
+timeout 1200 python -m pytest tests -m gpu -q 2>&1 | tail -2
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
+timeout 600 python bench.py 2>&1 | tail -1 > gpurun_out/bench_r01_final.json; python -c "import json; d=json.load(open('gpurun_out/bench_r01_final.json')); print(d['value'], d['e2e']['value'], d['roofline']['frac'], d['assembly']['evals_per_s'], d['cpu_baseline']['value'], d['clocks'])"
+timeout 600 python bench.py --impl reference --steps 2 --warmup 1 2>&1 | tail -1 | cut -c1-200
