@@ -57,6 +57,12 @@ struct FmmLevel {
   double* X = nullptr;         // [nil][256] gathered source moments
   double* tmp = nullptr;       // [d][ncell][256]
   long long nil = 0, max_grp = 0;
+  // one scatter per level tick: the GEMM outputs of all offset groups side by side,
+  // and per target cell its pairs in group order (the per-group scatters' order)
+  int* t_ptr = nullptr;        // [ncell+1]
+  int* t_pair = nullptr;       // [nil] column of Yall
+  int* t_cells = nullptr;      // [n_tcell] target cells with pairs
+  int n_tcell = 0;
 };
 
 struct FmmExtra {
@@ -260,6 +266,21 @@ __global__ void build_kop_kernel(const double* __restrict__ K0, const double* __
   }
 }
 
+// all offset groups of a level at once: block (target cell with pairs, operator),
+// thread = node; adds the cell's GEMM columns in group order onto own / tmp, the
+// same additions in the same order as one scatter per group
+__global__ void scatter_all_kernel(const int* __restrict__ t_cells, const int* __restrict__ t_ptr,
+                                   const int* __restrict__ t_pair, const double* __restrict__ Y, int nops,
+                                   int mu, int k, int ncell, double* own, double* tmp) {
+  const int ring = mu + 3;
+  const long long M = (long long)nops * FND;
+  const int cell = t_cells[blockIdx.x], op = blockIdx.y, idx = threadIdx.x;
+  double* dst = op <= mu ? own + ((size_t)((k + op + 1) % ring) * ncell + cell) * FND + idx
+                         : tmp + ((size_t)(op - mu - 1) * ncell + cell) * FND + idx;
+  double acc = *dst;
+  for (int q = t_ptr[cell]; q < t_ptr[cell + 1]; ++q) acc += __ldg(Y + (long long)t_pair[q] * M + (long long)op * FND + idx);
+  *dst = acc;
+}
 __global__ void gather_kernel(const int* __restrict__ g_src, long long nil,
                               const double* __restrict__ mom, double* X) {
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < nil * FND;
@@ -267,25 +288,6 @@ __global__ void gather_kernel(const int* __restrict__ g_src, long long nil,
     X[e] = mom[(size_t)g_src[e / FND] * FND + (e % FND)];
 }
 
-// one offset group: targets are distinct cells, so plain adds are race free;
-// groups run one after another on the stream (deterministic order)
-__global__ void scatter_kernel(const int* __restrict__ g_obs, long long p0, long long np,
-                               const double* __restrict__ Y, int nops, int mu, int d, int k,
-                               int ncell, double* own, double* tmp) {
-  // grid (ceil(M / 256), np): block row = operator op, column = pair; coalesced
-  // column reads of Y (column-major, M = nops * 256) and contiguous 256-vectors out
-  const int ring = mu + 3;
-  const long long M = (long long)nops * FND;
-  const int op = blockIdx.x, idx = threadIdx.x;
-  for (long long pp = blockIdx.y; pp < np; pp += gridDim.y) {
-    const int cell = __ldg(g_obs + p0 + pp);
-    const double v = __ldg(Y + pp * M + (long long)op * FND + idx);
-    if (op <= mu)
-      own[((size_t)((k + op + 1) % ring) * ncell + cell) * FND + idx] += v;
-    else
-      tmp[((size_t)(op - mu - 1) * ncell + cell) * FND + idx] += v;
-  }
-}
 
 // distant-future recurrence, elementwise (fmm.py:355-367)
 template <int D>
@@ -566,6 +568,20 @@ extern "C" int tdw_fmm_setup(tdw_problem* pb, const tdw_fmm_desc* fd) {
       V.grp = grp;
       V.nil = nkeep;
       F->m2l_pairs += nkeep;
+      {
+        std::vector<int> tptr(V.ncell + 1, 0), tpair(nkeep), tcells;
+        for (long long q = 0; q < nkeep; ++q) tptr[gobs[q] + 1]++;
+        for (int c = 0; c < V.ncell; ++c) {
+          if (tptr[c + 1] > 0) tcells.push_back(c);
+          tptr[c + 1] += tptr[c];
+        }
+        std::vector<int> fill(tptr.begin(), tptr.end() - 1);
+        for (long long q = 0; q < nkeep; ++q) tpair[fill[gobs[q]]++] = (int)q;  // ascending = group order
+        V.n_tcell = (int)tcells.size();
+        if ((rc = up(ctx, &V.t_ptr, tptr.data(), tptr.size()))) return rc;
+        if ((rc = up(ctx, &V.t_pair, tpair.data(), std::max<size_t>(1, tpair.size())))) return rc;
+        if ((rc = up(ctx, &V.t_cells, tcells.data(), std::max<size_t>(1, tcells.size())))) return rc;
+      }
       for (int o = 0; o < V.noff; ++o) V.max_grp = std::max(V.max_grp, grp[o + 1] - grp[o]);
       if ((rc = up(ctx, &V.g_obs, gobs.data(), gobs.size()))) return rc;
       if ((rc = up(ctx, &V.g_src, gsrc.data(), gsrc.size()))) return rc;
@@ -652,7 +668,7 @@ extern "C" int tdw_fmm_setup(tdw_problem* pb, const tdw_fmm_desc* fd) {
   }
   {
     long long mg = 1;
-    for (int L = 2; L <= F->leaf; ++L) mg = std::max(mg, F->lev[L].max_grp);
+    for (int L = 2; L <= F->leaf; ++L) mg = std::max(mg, F->lev[L].nil);  // all groups of a level
     TDW_CUDA(ctx, cudaMalloc(&F->Y, sizeof(double) * (size_t)mg * std::max(1, F->nops) * FND));
     if (cublasCreate(&F->blas) != CUBLAS_STATUS_SUCCESS)
       return tdw_fail(ctx, TDW_ERR_CUDA, "cublasCreate failed");
@@ -706,11 +722,12 @@ int launch_m2l(tdw_problem* pb, FmmLevel& V, int k, cudaStream_t st) {
       // Y (M x np) = Kop_o (M x 256) * X (256 x np), column-major
       cublasStatus_t bs = cublasDgemm(F->blas, CUBLAS_OP_N, CUBLAS_OP_N, M, (int)np, FND, &one,
                                       V.Kop + (size_t)o * FND * M, M, V.X + (size_t)p0 * FND, FND,
-                                      &zero, F->Y, M);
+                                      &zero, F->Y + (size_t)p0 * M, M);
       if (bs != CUBLAS_STATUS_SUCCESS) return tdw_fail(ctx, TDW_ERR_CUDA, "cublasDgemm failed");
-      scatter_kernel<<<dim3(nops, (unsigned)std::min<long long>(np, 65535)), FND, 0, st>>>(
-          V.g_obs, p0, np, F->Y, nops, F->mu, d, k, V.ncell, V.own, V.tmp);
     }
+    if (V.n_tcell > 0)
+      scatter_all_kernel<<<dim3(V.n_tcell, nops), FND, 0, st>>>(V.t_cells, V.t_ptr, V.t_pair, F->Y, nops, F->mu,
+                                                                 k, V.ncell, V.own, V.tmp);
     TDW_CUDA(ctx, cudaGetLastError());
   }
   const size_t cs = (size_t)V.ncell * FND;
@@ -955,7 +972,7 @@ void tdw_fmm_free(FmmState* F) {
   for (auto& V : F->lev) {
     void* p[] = {V.parent, V.octant, V.child_ptr, V.child_idx, V.obs_ptr, V.il_src, V.il_off, V.dark,
                  V.K0, V.Kp, V.own, V.inherit, V.deriv, V.aux, V.acc, V.mom, V.g_obs, V.g_src,
-                 V.Kop, V.X, V.tmp};
+                 V.Kop, V.X, V.tmp, V.t_ptr, V.t_pair, V.t_cells};
     for (void* q : p)
       if (q) cudaFree(q);
   }
