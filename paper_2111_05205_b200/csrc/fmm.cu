@@ -63,6 +63,13 @@ struct FmmLevel {
   int* t_pair = nullptr;       // [nil] column of Yall
   int* t_cells = nullptr;      // [n_tcell] target cells with pairs
   int n_tcell = 0;
+  // the level's GEMMs as one grouped call (one group per nonempty offset)
+  std::vector<int> gm, gn, gk, glda, gldb, gldc, gsize;
+  std::vector<double> galpha, gbeta;
+  std::vector<cublasOperation_t> gop;
+  const double** gA = nullptr;  // device pointer arrays
+  const double** gB = nullptr;
+  double** gC = nullptr;
 };
 
 struct FmmExtra {
@@ -670,6 +677,38 @@ extern "C" int tdw_fmm_setup(tdw_problem* pb, const tdw_fmm_desc* fd) {
     long long mg = 1;
     for (int L = 2; L <= F->leaf; ++L) mg = std::max(mg, F->lev[L].nil);  // all groups of a level
     TDW_CUDA(ctx, cudaMalloc(&F->Y, sizeof(double) * (size_t)mg * std::max(1, F->nops) * FND));
+    // grouped-GEMM descriptors per level (pointers into Kop, X, Y are fixed)
+    const int M = F->nops * FND;
+    for (int L = 2; L <= F->leaf; ++L) {
+      FmmLevel& V = F->lev[L];
+      std::vector<const double*> A, B;
+      std::vector<double*> Cp;
+      for (int o = 0; o < V.noff; ++o) {
+        const long long p0 = V.grp[o], np = V.grp[o + 1] - V.grp[o];
+        if (np == 0) continue;
+        A.push_back(V.Kop + (size_t)o * FND * M);
+        B.push_back(V.X + (size_t)p0 * FND);
+        Cp.push_back(F->Y + (size_t)p0 * M);
+        V.gm.push_back(M);
+        V.gn.push_back((int)np);
+        V.gk.push_back(FND);
+        V.glda.push_back(M);
+        V.gldb.push_back(FND);
+        V.gldc.push_back(M);
+        V.gsize.push_back(1);
+        V.galpha.push_back(1.0);
+        V.gbeta.push_back(0.0);
+        V.gop.push_back(CUBLAS_OP_N);
+      }
+      if (!A.empty()) {
+        TDW_CUDA(ctx, cudaMalloc(&V.gA, sizeof(double*) * A.size()));
+        TDW_CUDA(ctx, cudaMalloc(&V.gB, sizeof(double*) * B.size()));
+        TDW_CUDA(ctx, cudaMalloc(&V.gC, sizeof(double*) * Cp.size()));
+        TDW_CUDA(ctx, cudaMemcpy(V.gA, A.data(), sizeof(double*) * A.size(), cudaMemcpyHostToDevice));
+        TDW_CUDA(ctx, cudaMemcpy(V.gB, B.data(), sizeof(double*) * B.size(), cudaMemcpyHostToDevice));
+        TDW_CUDA(ctx, cudaMemcpy(V.gC, Cp.data(), sizeof(double*) * Cp.size(), cudaMemcpyHostToDevice));
+      }
+    }
     if (cublasCreate(&F->blas) != CUBLAS_STATUS_SUCCESS)
       return tdw_fail(ctx, TDW_ERR_CUDA, "cublasCreate failed");
     cublasSetMathMode(F->blas, CUBLAS_DEFAULT_MATH);
@@ -716,7 +755,15 @@ int launch_m2l(tdw_problem* pb, FmmLevel& V, int k, cudaStream_t st) {
     if (cublasSetStream(F->blas, st) != CUBLAS_STATUS_SUCCESS)
       return tdw_fail(ctx, TDW_ERR_CUDA, "cublasSetStream failed");
     const double one = 1.0, zero = 0.0;
-    for (int o = 0; o < V.noff; ++o) {
+    static const bool grouped = !(getenv("TDW_GROUPED_GEMM") && atoi(getenv("TDW_GROUPED_GEMM")) == 0);
+    if (grouped && V.gA) {
+      cublasStatus_t bs = cublasDgemmGroupedBatched(
+          F->blas, V.gop.data(), V.gop.data(), V.gm.data(), V.gn.data(), V.gk.data(), V.galpha.data(), V.gA,
+          V.glda.data(), V.gB, V.gldb.data(), V.gbeta.data(), V.gC, V.gldc.data(), (int)V.gm.size(),
+          V.gsize.data());
+      if (bs != CUBLAS_STATUS_SUCCESS) return tdw_fail(ctx, TDW_ERR_CUDA, "cublasDgemmGroupedBatched failed");
+    }
+    for (int o = 0; o < (grouped && V.gA ? 0 : V.noff); ++o) {
       const long long p0 = V.grp[o], np = V.grp[o + 1] - V.grp[o];
       if (np == 0) continue;
       // Y (M x np) = Kop_o (M x 256) * X (256 x np), column-major
@@ -972,7 +1019,7 @@ void tdw_fmm_free(FmmState* F) {
   for (auto& V : F->lev) {
     void* p[] = {V.parent, V.octant, V.child_ptr, V.child_idx, V.obs_ptr, V.il_src, V.il_off, V.dark,
                  V.K0, V.Kp, V.own, V.inherit, V.deriv, V.aux, V.acc, V.mom, V.g_obs, V.g_src,
-                 V.Kop, V.X, V.tmp, V.t_ptr, V.t_pair, V.t_cells};
+                 V.Kop, V.X, V.tmp, V.t_ptr, V.t_pair, V.t_cells, (void*)V.gA, (void*)V.gB, (void*)V.gC};
     for (void* q : p)
       if (q) cudaFree(q);
   }
