@@ -1,2 +1,2 @@
-for v in "" "TDW_L2HINT=0" "TDW_HROWS=0" "TDW_SCHED=rr"; do
-for i in 1 2; do env $v timeout 100 python tools/insitu_probe.py 2 "[$v]" 2>&1 | tail -1; done; done
+timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus 1 --steps 2 --warmup 3 --no-cpu 2>&1 | tail -1 | cut -c1-160
+timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29512 bench.py --impl reference --gpus 1 --steps 1 --warmup 0 2>&1 | tail -1 | cut -c1-160
