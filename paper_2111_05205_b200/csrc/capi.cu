@@ -161,12 +161,14 @@ int tdw_problem_create_impl(tdw_ctx* ctx, const tdw_problem_desc* dsc, tdw_probl
   pb->window = dsc->window ? 1 : 0;
   {
     // temporal blocking: one convolution pass computes kb consecutive steps
-    // default 4; 6 when a pass (~ ns^2 / ranks band entries) outweighs the solves
-    // (~ ns): measured config 0 (320 el.) best at 4, config 1 even, config 2
-    // (5120) 13.4k -> 14.2k steps/s at 6, config 3 (20480) 737 -> 921
+    // default 4; 5 / 6 as a pass (~ ns^2 / ranks band entries) outweighs the solves
+    // (~ ns).  Measured: config 0 (320 el.) best at 4, config 1 even, config 2
+    // (5120) 15.5k steps/s at 5 (14.7k at 6, 13.5k at 4), config 3 (20480) 911 at 6
+    // (811 at 5, 737 at 4)
     const char* e = getenv("TDW_KB");
     const double pass_size = (double)dsc->ns * (double)dsc->ns / std::max(1, nranks);
-    pb->kb = std::max(1, std::min(TDW_KB_MAX, e ? atoi(e) : (pass_size >= 1e7 ? 6 : 4)));
+    const int kb_default = pass_size >= 1e8 ? 6 : (pass_size >= 1e7 ? 5 : 4);
+    pb->kb = std::max(1, std::min(TDW_KB_MAX, e ? atoi(e) : kb_default));
     // a pass waits for the solve overlap+1 steps back and runs beside the last
     // `overlap` solves; the split lags reach kb + overlap
     const char* o = getenv("TDW_OVERLAP");

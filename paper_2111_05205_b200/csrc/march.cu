@@ -2299,9 +2299,10 @@ int tdw_setup_cluster_solver(tdw_problem* pb) {
   pb->near_tail = 0;
   {
     const char* e = getenv("TDW_NEAR_IN_SOLVE");
-    // default: 2 lags at kb >= 6 (config 2: +3%, the near step then has three solves
-    // of slack), else 1 (config 1: each extra lag costs a solve-bound loop ~35%)
-    const int want = std::min(e ? atoi(e) : (pb->kb >= 6 ? 2 : 1), pb->nsl);
+    // default: 3 lags at kb = 5 (config 2: 15.5k steps/s; 2 lags 15.0k, 4 lags 14.1k),
+    // 2 at kb = 6, else 1 (config 1, solve-bound: each extra lag costs ~35%); the
+    // near step of step s is then needed only near_tail + 1 solves later
+    const int want = std::min(e ? atoi(e) : (pb->kb == 5 ? 3 : (pb->kb >= 6 ? 2 : 1)), pb->nsl);
     if (want > 0 && pb->sp_reg > 0 && pb->sp_halo > 0 && pb->split_lag2 && pb->near_w > 0) {
       std::vector<int> ncol((size_t)TDW_NEAR_MAX * ns), cnt(ns);
       std::vector<double> nv((size_t)want * TDW_NEAR_MAX * ns);  // g < want slices of [nsl][TDW_NEAR_MAX][ns]
