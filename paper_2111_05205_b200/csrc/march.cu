@@ -1147,8 +1147,10 @@ __global__ void __launch_bounds__(reg_threads<MAXNZ>(), 1) solve_halo_kernel(Clu
   // lag-2 near terms of the next step, N^2 x^(beta0) (what near_step_kernel's
   // g = 0 would write), from the owners' final x in DSMEM: the next solve then
   // needs no kernel in between; lags >= 3 run on the near stream meanwhile
-  if (a.ntail > 0 && own) {
-    for (int t = 0; t < a.ntail; ++t) {
+  // (row, lag) tasks over all the CTA's threads, not only the own-row threads
+  for (int task = tid; task < nr * a.ntail; task += blockDim.x) {
+    {
+      const int t = task / nr, gi = r0 + task % nr;
       const int* ptr = a.n2_ptr + (size_t)t * (a.ns + 1);
       // four independent chains, all loads of a group of four in flight
       double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
