@@ -1,4 +1,3 @@
-timeout 600 python -m pytest tests/test_gpu_march.py tests/test_gpu_sharded.py -q -x 2>&1 | tail -1
-for i in 1 2; do timeout 100 python tools/insitu_probe.py 2 "tail tasks" 2>&1 | tail -1; TDW_KB=6 timeout 100 python tools/insitu_probe.py 2 "tail tasks kb6" 2>&1 | tail -1; done
-timeout 100 python tools/trace_solve.py 2 2>&1 | grep "phases\|timeline" | tail -2
-for c in 0 1; do timeout 100 python tools/insitu_probe.py $c "tail tasks" 2>&1 | tail -1; done
+timeout 1200 python -m pytest tests -m gpu -q 2>&1 | tail -1
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
+timeout 900 python bench.py 2>&1 | tail -1 > gpurun_out/bench_r01_final.json; python -c "import json; d=json.load(open('gpurun_out/bench_r01_final.json')); print(d['value'], d['e2e']['value'], d['roofline']['frac'], d['cpu_baseline']['value'])"
