@@ -8,6 +8,11 @@
 //   K3/K4 solve_kernel  b = sum of partials, Jacobi sweeps on A x = b (lu.solve, :330),
 //                     residual test (:331-333), promotion of x into u/q (finalize_step,
 //                     :239-242), blow-up detector (:336-338), next step's known data.
+//   near_step_kernel  the unknown densities' terms at the split lags.
+// Loop (enqueue_loop, captured as one CUDA graph): temporally blocked passes of kb
+// steps on a side stream overlap the last m solves; solves run back to back on the
+// library stream (programmatic dependent launch), each forming the first split lags
+// of the next steps in its tail; the remaining split lags run on a third stream.
 // History: hist[pad + beta][j] = (q_j^beta, u_j^beta) (time-major, one row of hcols
 // elements per step, zero padded for beta < 0 and j >= ns).  The convolution
 // stages a [lags][32 columns] box of it, so the 32 lanes of a warp (one column
