@@ -147,3 +147,27 @@ def test_restatement_reproduces_corrected_reference_accuracy(bie, d, expected):
     err = np.linalg.norm(r["u"] - ref["u"]) / np.linalg.norm(ref["u"])
     assert r["status"] == "stable" and r["n_steps"] == spec.nt - 1
     assert abs(err - expected) < 0.002, err
+
+
+def test_p2m_rows_match_per_element_formula():
+    """The vectorised P2M rows (all elements at once) equal the per-element
+    7-point-rule formula (fmm.py:238-275 restated) to round-off."""
+    from paper_2111_05205_b200 import fmm_interp
+    spec = scenarios.build_spec(0)
+    plan = fmm_plan.build_plan(spec, fmm_plan.FmmConfig(ps=4, pt=4, leaf_capacity=20))
+    mesh, leaf = spec.mesh, plan.tree.levels[plan.leaf]
+    v0, v1, v2 = mesh.element_vertices()
+    h = leaf.half_width
+    pref = 1.0 / (4.0 * np.pi * (spec.c * spec.basis.dt) ** spec.basis.d)
+    for e in (0, 7, 101, mesh.n_elements - 1):
+        pts, wts = fmm_interp.triangle_gauss_rule(np.stack([v0[e], v1[e], v2[e]]))
+        xi = (pts - leaf.centres[plan.elem_cell[e]]) / h
+        w = [plan.scheme_s.weights(xi[:, k], 1.0) for k in range(3)]
+        dw = [plan.scheme_s.dweights(xi[:, k], 1.0) / h for k in range(3)]
+        n = mesh.normals[e]
+        tau = np.einsum("g,ga,gb,gc->abc", wts, w[0], w[1], w[2]).reshape(-1)
+        sig = (np.einsum("g,ga,gb,gc->abc", wts, n[0] * dw[0], w[1], w[2])
+               + np.einsum("g,ga,gb,gc->abc", wts, w[0], n[1] * dw[1], w[2])
+               + np.einsum("g,ga,gb,gc->abc", wts, w[0], w[1], n[2] * dw[2])).reshape(-1)
+        np.testing.assert_allclose(plan.p2m_tau[e], pref * tau, rtol=1e-13, atol=1e-16)
+        np.testing.assert_allclose(plan.p2m_sig[e], pref * sig, rtol=1e-13, atol=1e-15)
