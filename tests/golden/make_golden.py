@@ -10,6 +10,8 @@ the reference itself never does.
     NUMBA_CACHE_DIR=/tmp/nb python tests/golden/make_golden.py march 1
     NUMBA_CACHE_DIR=/tmp/nb python tests/golden/make_golden.py march 2   # ~1 h, ~15 GB RAM
     NUMBA_CACHE_DIR=/tmp/nb python tests/golden/make_golden.py tree 3
+    NUMBA_CACHE_DIR=/tmp/nb python tests/golden/make_golden.py tree 4   # two spheres, ~1 min
+    NUMBA_CACHE_DIR=/tmp/nb python tests/golden/make_golden.py fmm_ref  # patched reference fast_march
 
 Scenario recipe: SURVEY.md section 8(c)/(d) (icosphere f=4/8/16, c=1,
 c*dt = 0.5 * mean edge, Gaussian plane pulse along z, sigma=4dt, t0=6 sigma).
@@ -43,11 +45,17 @@ CONFIGS = {
     1: (8, "bmbie", 2, 1.0, 128, None),
     2: (16, "bmbie", 1, 0.0, 256, 12345),
     3: (32, "bmbie", 2, 1.0, 512, None),
+    4: (32, "bmbie", 2, 1.0, 1024, None),   # two spheres, centres (+-1.5, 0, 0); dt of one sphere
 }
 
 
 def build_mesh(cfg):
     f, _, _, _, _, seed = CONFIGS[cfg]
+    if cfg == 4:
+        a = shapes.icosphere(f, radius=1.0, centre=(-1.5, 0.0, 0.0))
+        b = shapes.icosphere(f, radius=1.0, centre=(1.5, 0.0, 0.0))
+        return TriMesh(np.vstack([a.vertices, b.vertices]),
+                       np.vstack([a.triangles, b.triangles + len(a.vertices)]))
     m = shapes.icosphere(f, radius=1.0, centre=(0.0, 0.0, 0.0))
     if seed is None:
         return m
@@ -59,7 +67,7 @@ def build_mesh(cfg):
 def build_spec(cfg):
     f, bie, d, phival, nt, _ = CONFIGS[cfg]
     mesh = build_mesh(cfg)
-    v0, v1, v2 = mesh.element_vertices()
+    v0, v1, v2 = (build_mesh(3) if cfg == 4 else mesh).element_vertices()
     edges = np.concatenate([np.linalg.norm(v1 - v0, axis=1),
                             np.linalg.norm(v2 - v1, axis=1),
                             np.linalg.norm(v0 - v2, axis=1)])
@@ -256,6 +264,82 @@ def make_fmm_setup():
     print("fmm_setup.npz")
 
 
+# the seven line-level corrections of the reference's fast solver,
+# applied to the reference SOURCE text in memory (the tree stays read-only and no
+# reference source is copied into this repo).  Each (file, old, new) must match once.
+FMM_PATCHES = [
+    # 1. P2M contraction: tau[elems] @ p2m_tau[ci] (fmm.py:517-518)
+    ("fmm.py", "spat = (self.p2m_tau[ci] @ hist.tau[beta0][elems]\n"
+               "                        - self.p2m_sig[ci] @ hist.sigma[beta0][elems])",
+               "spat = (hist.tau[beta0][elems] @ self.p2m_tau[ci]\n"
+               "                        - hist.sigma[beta0][elems] @ self.p2m_sig[ci])"),
+    # 2. node-offset sign of the kernel samples (fmm.py:87)
+    ("fmm.py", "g = h_s * self._node_diff", "g = -h_s * self._node_diff"),
+    # 3. source interval: the one containing t_{beta+1} (fmm.py:512)
+    ("fmm.py", "k_src = int(np.floor(t_src / interval + 1e-12))",
+               "k_src = int(np.floor((t_src + self.dt) / interval + 1e-12))"),
+    # 4. its temporal weights may extrapolate by 2 dt / I (fmm.py:514)
+    ("fmm.py", "wts = self.scheme_t.weights([eta_s])[0]",
+               "wts = self.scheme_t.weights([eta_s], 2.0 * self.dt / interval)[0]"),
+    # 5. extra-list break test on the corrected source interval (fmm.py:464)
+    ("fmm.py", "if int(np.floor(t_src / int_L + 1e-12)) != k_now:",
+               "if int(np.floor((t_src + self.dt) / int_L + 1e-12)) != k_now:"),
+    # 6. extra-list lag count (fmm.py:226)
+    ("fmm.py", "lags = int(np.floor(tree.interval(L) / self.dt)) + 1",
+               "lags = int(np.floor(tree.interval(L) / self.dt)) + 2"),
+    # 7. marginal margin c I_L and reach c (I_L + dt) + 2 rho (fmm_tree.py:202, 206)
+    ("fmm_tree.py", "margin = c * (interval - dt)", "margin = c * interval"),
+    ("fmm_tree.py", "reach = c * interval + 2 * rho", "reach = c * (interval + dt) + 2 * rho"),
+    # not a correction: numba cannot cache functions of an in-memory module
+    ("fmm.py", "@numba.njit(cache=True, fastmath=True)", "@numba.njit(cache=False, fastmath=True)"),
+]
+
+
+def patched_fmm():
+    """The reference's fmm / fmm_tree modules with FMM_PATCHES applied (in memory)."""
+    import types
+    mods = {}
+    for name in ("fmm_tree", "fmm"):
+        src = (REF / "tdwavebem" / f"{name}.py").read_text()
+        for f, old, new in FMM_PATCHES:
+            if f == f"{name}.py":
+                assert src.count(old) == 1, (f, old)
+                src = src.replace(old, new)
+        mod = types.ModuleType(f"tdwavebem.{name}")
+        mod.__package__ = "tdwavebem"
+        mod.__file__ = f"<patched {name}.py>"
+        sys.modules[f"tdwavebem.{name}"] = mod
+        exec(compile(src, mod.__file__, "exec"), mod.__dict__)
+        mods[name] = mod
+    return mods["fmm"]
+
+
+def make_fmm_ref():
+    """fast_march of the runtime-corrected reference on the 1280-element sphere
+    (OBIE d=1 and BMBIE d=2, Neumann, ps = pt = 4, Nt = 128, leaf capacity 100
+    and 20): per-step rhs and unknown density, the pin of oracle/fmm_oracle.py."""
+    fmm = patched_fmm()
+    base = build_spec(1)
+    out = dict(versions=VERSIONS, patches=np.array([f"{f}: {o!r} -> {n!r}" for f, o, n in FMM_PATCHES]))
+    import warnings
+    for bie, d in (("obie", 1), ("bmbie", 2)):
+        for Z in (100, 20):
+            with warnings.catch_warnings():
+                warnings.simplefilter("ignore")
+                spec = marching.ProblemSpec(base.mesh, np.ones(base.mesh.n_elements), bie,
+                                            BSplineBasis(d, base.basis.dt), 1.0, 128, q_data=base.q_data)
+            trace = []
+            t0 = time.perf_counter()
+            hist = fmm.fast_march(spec, fmm.FmmConfig(ps=4, pt=4, leaf_capacity=Z, mu=8), rhs_trace=trace)
+            key = f"{bie}{d}_Z{Z}"
+            out[f"{key}_u"] = hist.u
+            out[f"{key}_rhs"] = np.array(trace)
+            out[f"{key}_status"] = hist.status
+            out[f"{key}_n_steps"] = hist.n_steps
+            print(f"{key}: {hist.status} {hist.n_steps} steps, {time.perf_counter() - t0:.1f} s")
+    np.savez_compressed(OUT / "fmm_ref.npz", **out)
+
+
 if __name__ == "__main__":
     what = sys.argv[1]
     if what == "coeff":
@@ -264,6 +348,8 @@ if __name__ == "__main__":
         make_march(int(sys.argv[2]))
     elif what == "tree":
         make_tree(int(sys.argv[2]))
+    elif what == "fmm_ref":
+        make_fmm_ref()
     elif what == "fmm_setup":
         make_fmm_setup()
     else:

@@ -3,7 +3,8 @@ restatement of the fast solver (oracle/fmm_oracle.py).
 
 Pins:
 * the octree and interaction lists are bit-exact against the reference's own
-  build_tree (tests/golden/tree_cfg{1,2,3}.npz, uncorrected extra-pair rule);
+  build_tree (tests/golden/tree_cfg{1,2,3,4}.npz, uncorrected extra-pair rule; config 4
+  is the two-sphere, 40960-element tree: leaf level 6, 4.35e6 near pairs);
 * interpolation rows, transfer matrices, the triangle rule, cmp_coeff, the
   Toeplitz kernel tensors (node-offset sign corrected) and the materialised M2L
   matrix against values computed by the reference (tests/golden/fmm_setup.npz);
@@ -22,7 +23,7 @@ from paper_2111_05205_b200 import fmm_plan, fmm_tree, marching, scenarios
 from paper_2111_05205_b200.fmm_interp import InterpScheme, triangle_gauss_rule
 
 
-@pytest.mark.parametrize("cfg", [1, 2, 3])
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4])
 def test_tree_bit_exact(cfg):
     g = golden(f"tree_cfg{cfg}.npz")
     spec = scenarios.build_spec(cfg)
