@@ -13,12 +13,18 @@ Nt-1 = 255 MOT time steps of the configuration.
           Greville sampling of the user's data callables (into page-locked
           buffers), H2D of the known data, the loop, D2H of u, q, tau, sigma --
           every step.
-  roofline  K2 (history convolution): 16 B x N_band per launch / average
-          launch time measured with CUDA events around every K2 launch of the
-          timed region, against the measured HBM copy bandwidth.
-  cpu_baseline / --impl reference: the C oracle port (oracle/) of the
-          reference's march (sigma/tau lag-CSR form) on the host cores, timed
-          on a bounded row sample and extrapolated (see `sample`).
+  e2e_with_assembly  cold march(spec): store build + assembly + loop + copies.
+  roofline  K2 (history convolution): the store read once per launch (16 B x
+          N_band) / average launch time measured with CUDA events around every
+          K2 launch of the timed region, against the measured HBM copy
+          bandwidth; `traffic` = ncu DRAM bytes of that kernel at that kb.
+          `blocking` reports the kb MOT steps one store read serves.
+  assembly  K1 (coefficient fill) evals/s; its roofline fraction is ncu's FP64-
+          pipe utilisation at this configuration (profiles/k1_fill.json).
+  cpu_baseline  the C oracle port (oracle/) of the reference's march (sigma/tau
+          lag-CSR form) on the host cores: the complete loop of the full problem.
+  --impl reference  the same port, a bench step = a chunk of consecutive MOT
+          steps of the full-problem loop (assembly outside the timed region).
 """
 from __future__ import annotations
 
@@ -108,55 +114,95 @@ def dist_env():
     return world, rank, local
 
 
-def cpu_sample(spec, rows: int, steps: int):
-    """Oracle port of the reference march on `rows` collocation rows (all columns):
-    assembly of their lag-CSR and `steps` time steps of the lag SpMVs.  Returns
-    extrapolated full-problem MOT steps/s (loop only) and the sample record."""
+def cpu_marcher(spec):
+    """The oracle port (C/OpenMP) of the reference's march on the WHOLE problem:
+    lag-CSR assembly of every row (marching.py:132-181), then a stateful time
+    loop (marching.py:292-338) that bench.py advances in bounded chunks."""
     from oracle import oracle
+    oracle.build()
+    uk, qk = _greville(spec)
+    thr = 1e6 * max(spec.blowup_reference, 1e-30)
+    return oracle.Marcher(spec.mesh.vertices, spec.mesh.triangles, spec.phi, spec.bie, spec.basis.d,
+                          spec.c, spec.basis.dt, spec.nt, uk, qk, threshold=thr)
+
+
+def _greville(spec):
+    from paper_2111_05205_b200 import marching
+    return marching.greville_samples(spec)
+
+
+def cpu_full_loop(spec):
+    """cpu_baseline of our arm: the complete (nt-1)-step loop of the oracle port on
+    the full problem, timed on the host cores (assembly reported, not in value)."""
+    from oracle import oracle
+    M = cpu_marcher(spec)
+    try:
+        n, t, done = M.run(spec.nt - 1)
+    finally:
+        t_asm = M.t_asm
+        M.close()
     ns = spec.mesh.n_elements
-    lo = (ns - rows) // 2
-    t_asm, t_loop, ntrip = oracle.sample(spec.mesh.vertices, spec.mesh.triangles, spec.bie,
-                                         spec.basis.d, spec.c, spec.basis.dt, spec.nt, lo, lo + rows, steps)
-    per_step_full = t_loop / steps * ns / rows
-    return 1.0 / per_step_full, {"t_asm_s": t_asm, "t_loop_s": t_loop, "rows": rows, "steps": steps,
-                                 "lagcsr_triples": ntrip, "asm_triples_per_s": ntrip / max(t_asm, 1e-12)}
+    return {"value": n / t, "unit": "steps/s", "cores": oracle.num_threads(), "kind": "port",
+            "sample": (f"the complete loop: all {n} MOT steps of the full {ns}-element problem "
+                       f"(sigma/tau lag-CSR SpMVs + Gauss-Seidel solve + residual test), "
+                       f"oracle port (C/OpenMP) of marching.march; loop {t:.1f} s; lag-CSR assembly "
+                       f"of all rows {t_asm:.1f} s (not in value)"),
+            "loop_s": t, "assembly_s": t_asm, "steps": n}
 
 
 def run_reference(args, world, rank):
-    """--impl reference: the reference algorithm on the host cores (oracle port)."""
-    import numpy as np  # noqa: F401
+    """--impl reference: the reference's algorithm on the host cores (oracle port,
+    C/OpenMP, all host threads).  The lag CSR of the whole problem is assembled
+    once (outside the timed region); a bench step is one chunk of `--ref-chunk`
+    consecutive MOT steps of the real full-problem loop, which continues across
+    bench steps and restarts from step 1 when it reaches the end."""
     from oracle import oracle
     from paper_2111_05205_b200 import scenarios
     if rank != 0:
         return
     spec = scenarios.build_spec(args.config)
-    oracle.build()
-    rows = args.ref_rows
+    nt = spec.nt
+    chunk = args.ref_chunk or -(-(nt - 1) // 8)
+    t0 = time.perf_counter()
+    M = cpu_marcher(spec)
+    t_setup = time.perf_counter() - t0
+
+    def one_chunk():
+        left, steps, secs = chunk, 0, 0.0
+        while left > 0:
+            n, t, done = M.run(left)
+            steps, secs, left = steps + n, secs + t, left - n
+            if done:
+                M.reset()
+        return steps, secs
+
     for _ in range(args.warmup):
-        cpu_sample(spec, rows, 4)
-    vals = []
-    recs = []
+        one_chunk()
+    tot_steps, tot_s = 0, 0.0
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        v, rec = cpu_sample(spec, rows, spec.nt - 1)
-        vals.append(v)
-        recs.append(rec)
+        n, t = one_chunk()
+        tot_steps += n
+        tot_s += t
     wall = time.perf_counter() - t0
-    value = sum(vals) / len(vals)
+    M.close()
+    value = tot_steps / tot_s
     cores = oracle.num_threads()
-    sample = (f"{rows} of {spec.mesh.n_elements} collocation rows x all columns, {spec.nt - 1} MOT steps "
-              f"of the reference's sigma/tau lag-CSR SpMVs, extrapolated by rows; "
-              f"oracle port (C, OpenMP) of marching.march")
+    sample = (f"{args.steps} chunks of {chunk} consecutive MOT steps of the full "
+              f"{spec.mesh.n_elements}-element loop ({nt - 1} steps, restarted at the end) after "
+              f"{args.warmup} warm-up chunks; oracle port (C, OpenMP) of marching.march in the "
+              f"reference's sigma/tau lag-CSR form; lag-CSR assembly of all rows {M.t_asm:.1f} s, "
+              f"outside the timed region")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * (spec.nt - 1) / value,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_s / args.steps,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded scenario)",
         "config": {"workload": scenarios.DESCRIPTION[args.config], "ns": spec.mesh.n_elements,
-                   "nt": spec.nt, "parallelism": "host threads"},
+                   "nt": nt, "mot_steps_per_bench_step": chunk, "parallelism": "host threads"},
         "cpu_baseline": {"value": value, "unit": "steps/s", "cores": cores, "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "sample_records": recs[-1], "wall_s": wall,
+        "timed_wall_s": wall, "setup_s": t_setup,
     }
     print(json.dumps(line), flush=True)
 
@@ -319,6 +365,18 @@ def run_ours(args, world, rank, local):
         h = marching.march(spec, mats=store, device_data=True)
     barrier()
     e2e_dev = e2e_steps * (nt - 1) / max_over_ranks(time.perf_counter() - t0)
+    # cold march(spec): a new store every call (problem setup, assembly K1, loop,
+    # copies): the reference's march() rebuilds its matrices on every call too
+    e2e_asm = None
+    if world == 1:
+        h = marching.march(spec)
+        del h
+        t0 = time.perf_counter()
+        n_cold = 3
+        for _ in range(n_cold):
+            h = marching.march(spec)
+            del h
+        e2e_asm = n_cold * (nt - 1) / (time.perf_counter() - t0)
     # march() copies the samples of each data callable that is not None (pinned buffers)
     h2d = sum(f is not None for f in (spec.u_data, spec.q_data)) * (nt - 1) * ns * 8
     d2h = 4 * (nt - 1) * ns * 8
@@ -330,14 +388,21 @@ def run_ours(args, world, rank, local):
     peak = peak or HBM_FALLBACK
     n_band = max_over_ranks(float(info["n_band"]))
     kb = info["steps_per_pass"]
-    # 16 B per band entry per MOT step; one launch processes kb steps
-    achieved = 16.0 * n_band * kb / (conv_ms * 1e-3) / 1e9
-    stream = 16.0 * n_band / (conv_ms * 1e-3) / 1e9  # the store read once per launch
-    traffic = None
+    # K2 roofline: the bytes one launch must move = the store read once (16 B per
+    # band entry, SURVEY 8(d)'s per-step unit), over the measured launch time.
+    # Temporal blocking computes kb MOT steps from that one read; that gain is
+    # reported on its own (blocking), not folded into frac.
+    stream = 16.0 * n_band / (conv_ms * 1e-3) / 1e9
+    rpw = store.info()["conv_rpw"]  # set when the loop plan is made
+    kname = f"conv_kernel_wg<{kb}>" if rpw == 4 else (
+        f"conv_kernel_wg2<{kb}>" if rpw == 3 else f"conv_kernel<{kb}>")
+    traffic, traffic_src = None, None
     prof = ROOT / "profiles" / "traffic.json"
-    if prof.exists():
+    if prof.exists():  # ncu --set full DRAM bytes of THIS kernel at THIS kb and config
         try:
-            traffic = json.loads(prof.read_text()).get(f"config{args.config}")
+            rec = json.loads(prof.read_text()).get(f"config{args.config}")
+            if rec and rec.get("kb") == kb and rec.get("n_band") == int(n_band) and world == 1:
+                traffic, traffic_src = rec["dram_bytes_per_launch"], rec["source"]
         except Exception:
             traffic = None
 
@@ -359,12 +424,7 @@ def run_ours(args, world, rank, local):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         try:
-            v, rec = cpu_sample(spec, args.cpu_rows, nt - 1)
-            from oracle import oracle
-            cpu = {"value": v, "unit": "steps/s", "cores": oracle.num_threads(), "kind": "port",
-                   "sample": (f"{args.cpu_rows} of {ns} rows x all columns, {nt - 1} steps of the "
-                              f"reference's sigma/tau lag-CSR SpMVs (oracle port, C/OpenMP), "
-                              f"extrapolated by rows; assembly {rec['asm_triples_per_s']:.3e} triples/s")}
+            cpu = cpu_full_loop(spec)
         except Exception as exc:  # the CPU leg must not sink the GPU line
             cpu = {"value": None, "unit": "steps/s", "cores": os.cpu_count(), "kind": "port",
                    "sample": f"failed: {exc}"}
@@ -389,18 +449,24 @@ def run_ours(args, world, rank, local):
                                          "d2h_bytes_per_step": d2h,
                                          "api": "marching.march(spec, mats=store, device_data=True)",
                                          "note": "incident-pulse samples computed on the device; not the e2e metric"},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic, "kernel": "conv_kernel (K2)",
+            "e2e_with_assembly": {"value": e2e_asm, "unit": "steps/s", "api": "marching.march(spec)",
+                                  "note": "every call builds the store (geometry, K1 fill, near "
+                                          "structure, solver setup) and runs the loop with host data"},
+            "roofline": {"bound": "hbm", "achieved": stream, "peak": peak, "unit": "GB/s",
+                         "frac": stream / peak, "traffic": traffic, "kernel": f"{kname} (K2, history convolution)",
                          "peak_source": peak_src, "avg_launch_ms": conv_ms,
                          "launches_timed": int(tk["conv_launches"]),
-                         "bytes_per_launch": 16.0 * n_band * kb,
-                         "steps_per_launch": kb,
-                         "note": "algorithmic bytes = 16 B per band entry per MOT step x the kb steps "
-                                 "one launch computes; temporal blocking reads the store once per "
-                                 "launch, so frac > 1 is the blocking gain (see store_stream)",
-                         "store_stream": {"bytes_per_launch": 16.0 * n_band, "achieved": stream,
-                                          "frac": stream / peak,
-                                          "traffic_over_store": (traffic / (16.0 * n_band)) if traffic else None}},
+                         "bytes_per_launch": 16.0 * n_band,
+                         "traffic_source": traffic_src,
+                         "traffic_over_algorithmic": (traffic / (16.0 * n_band)) if traffic else None,
+                         "note": "algorithmic bytes per launch = 16 B x N_band (V_U, V_W fp64, the "
+                                 "store read once); a launch computes kb MOT steps from that read "
+                                 "(see blocking)"},
+            "blocking": {"steps_per_launch": kb,
+                         "survey_unit_GBps": 16.0 * n_band * kb / (conv_ms * 1e-3) / 1e9,
+                         "note": "SURVEY 8(d) counts 16 B x N_band per MOT step; temporal blocking "
+                                 "serves kb steps per store read, so this rate is kb x the "
+                                 "physical stream and is not an HBM fraction"},
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
             # per loop: init_hist + (conv_kernel + reduce_parts) per pass + (solve +
@@ -409,14 +475,20 @@ def run_ours(args, world, rank, local):
             "assembly": {"ms": info["t_assemble_ms"], "evals": info["n_evals"],
                          "evals_per_s": evals_per_s,
                          "metric": "(i,j,gamma) layer-potential evals/s (fill kernel, fp64)",
-                         "roofline": {"bound": "fp64", "achieved": k1_achieved, "peak": fp64.value,
-                                      "unit": "TFLOP/s", "frac": k1_achieved / fp64.value,
+                         "roofline": {"bound": "fp64",
+                                      "frac": k1_ncu.get("fp64_pipe_active") if k1_ncu else None,
+                                      "achieved": (k1_ncu["fp64_pipe_active"] * fp64.value) if k1_ncu else None,
+                                      "peak": fp64.value, "unit": "TFLOP/s",
                                       "kernel": "fill_kernel (K1)",
-                                      "cost_per_eval": cost, "cost_model": "SURVEY 8(d): FP64 "
-                                      "instruction-equivalents per evaluation (div/sqrt 20, atan 26, "
-                                      "asinh 60); hoisting raises evals/s, the cost stays fixed",
+                                      "source": "ncu sm__pipe_fp64_cycles_active of the fill kernel at "
+                                                "this configuration (profiles/k1_fill.json)",
                                       "peak_source": "measured live (tdw_fp64_peak: DFMA chains)",
-                                      "ncu": k1_ncu}},
+                                      "ncu": k1_ncu},
+                         "cost_model_rate": {"tflops_equiv": k1_achieved, "cost_per_eval": cost,
+                                             "note": "SURVEY 8(d): FP64 instruction-equivalents per "
+                                                     "evaluation (div/sqrt 20, atan 26, asinh 60); "
+                                                     "hoisting raises evals/s while the cost stays "
+                                                     "fixed, so this is not a pipe fraction"}},
             "graph": bool(tm.get("solve_ms", 0) > 0),
         }
         print(json.dumps(line), flush=True)
@@ -432,8 +504,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", type=int, default=2)
-    ap.add_argument("--cpu-rows", type=int, default=64)
-    ap.add_argument("--ref-rows", type=int, default=64)
+    ap.add_argument("--ref-chunk", type=int, default=0,
+                    help="MOT steps per reference-arm bench step (default (nt-1)/8)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--fmm", action="store_true", help="interpolation FMM path (configs 3-4; default for 4)")
     args = ap.parse_args()

@@ -97,6 +97,8 @@ typedef struct {
   int32_t pass_overlap;      /* solves a convolution pass runs beside            */
   int32_t solve_halo;        /* halo depth of the communication-avoiding solver (0: none) */
   int64_t fmm_m2l_pairs;     /* FMM: M2L interaction pairs this rank evaluates (0: direct) */
+  int32_t conv_rpw;          /* rows per consumer warp of the convolution CTA (2 or 4) */
+  int32_t coeff_mode;        /* TDW_MODE_* the problem runs in                    */
 } tdw_info;
 
 typedef struct {

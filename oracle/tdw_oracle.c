@@ -297,9 +297,10 @@ static void lag_free(lagstore* L) {
   free(L->rowptr); free(L->col); free(L->U); free(L->W);
 }
 
-static int lag_build(lagstore* L, const omesh* m, int row_lo, int row_hi, int G, int bie, int d,
-                     double c, double dt) {
+static int lag_build_list(lagstore* L, const omesh* m, int row_lo, int row_hi,
+                          const int* rowlist, int G, int bie, int d, double c, double dt) {
   int nr = row_hi - row_lo, ns = m->ns;
+#define ROW_OF(r) (rowlist ? rowlist[r] : row_lo + (r))
   L->nr = nr;
   L->G = G;
   L->nvals = 0;
@@ -313,7 +314,7 @@ static int lag_build(lagstore* L, const omesh* m, int row_lo, int row_hi, int G,
   if (!arr) return OR_NOMEM;
 #pragma omp parallel for schedule(dynamic, 8)
   for (int r = 0; r < nr; ++r)
-    for (int j = 0; j < ns; ++j) arr[(size_t)r * ns + j] = arrival_of(m, row_lo + r, j, c, dt);
+    for (int j = 0; j < ns; ++j) arr[(size_t)r * ns + j] = arrival_of(m, ROW_OF(r), j, c, dt);
   for (int g = 1; g <= G; ++g) {
     int64_t* rp = calloc(nr + 1, sizeof(int64_t));
     if (!rp) { free(arr); return OR_NOMEM; }
@@ -335,7 +336,7 @@ static int lag_build(lagstore* L, const omesh* m, int row_lo, int row_hi, int G,
   int kind = bie == 1 ? 1 : 0;
 #pragma omp parallel for schedule(dynamic, 4)
   for (int r = 0; r < nr; ++r) {
-    int i = row_lo + r;
+    int i = ROW_OF(r);
     double nxi[3] = {-m->nrm[3 * i], -m->nrm[3 * i + 1], -m->nrm[3 * i + 2]};
     int64_t* pos = malloc(sizeof(int64_t) * G);
     for (int g = 0; g < G; ++g) pos[g] = L->rowptr[g][r];
@@ -353,6 +354,12 @@ static int lag_build(lagstore* L, const omesh* m, int row_lo, int row_hi, int G,
   }
   free(arr);
   return OR_OK;
+#undef ROW_OF
+}
+
+static int lag_build(lagstore* L, const omesh* m, int row_lo, int row_hi, int G, int bie, int d,
+                     double c, double dt) {
+  return lag_build_list(L, m, row_lo, row_hi, 0, G, bie, d, c, dt);
 }
 
 /* b_r (+)= U_g tau - W_g sigma over the stored rows (one lag): the reference's
@@ -378,59 +385,133 @@ static void lag_apply(const lagstore* L, int g, const double* tau, const double*
 static double weights_d[4][5] = {
     {0}, {1.0, -2.0, 1.0}, {0.5, -1.5, 1.5, -0.5}, {1.0 / 6, -2.0 / 3, 1.0, -2.0 / 3, 1.0 / 6}};
 
-/* Full march (marching.py:292-338).  All history arrays are (nt-1, ns).
- * u_known / q_known are the Greville samples (marching.py:258-276).
- * rhs_trace may be NULL.  Returns status in *status (0 stable, 1 unstable). */
-int oracle_march(int nv, const double* verts, int ns, const int64_t* tris, const double* phi,
-                 int bie, int d, double c, double dt, int nt, int window, double threshold,
-                 const double* u_known, const double* q_known, double* u, double* q, double* tau,
-                 double* sig, double* rhs_trace, int* n_steps, int* status, double* t_asm_out) {
-  if (d < 1 || d > 3 || nt < 2) return OR_INVALID;
+/* The reference's march (marching.py:292-338) as a stateful marcher, so that
+ * bench.py can time bounded chunks of the full-problem loop.  All history
+ * arrays are (nt-1, ns); u_known / q_known are the Greville samples
+ * (marching.py:258-276) and are copied. */
+typedef struct {
   omesh m;
-  int rc = mesh_build(&m, ns, verts, tris);
-  if (rc) return rc;
-  int gstar = oracle_gamma_star(nv, verts, ns, tris, d, c, dt);
-  int n_lags = window ? (gstar < nt - 1 ? gstar : nt - 1) : nt - 1;
   lagstore L;
-  memset(&L, 0, sizeof(L));
+  int ns, nt, d, window, gstar, n_lags, alpha, status, n_steps, rc;
+  double threshold;
+  const double* phi_in;
+  double *phi, *uk, *qk, *u, *q, *tau, *sig, *rhs;
+  double *aval, *adiag, *b, *x, *tt, *st, *tw, *sw;
+} omarcher;
+
+static void marcher_free(omarcher* M) {
+  if (!M) return;
+  free(M->phi); free(M->uk); free(M->qk); free(M->u); free(M->q); free(M->tau); free(M->sig);
+  free(M->rhs); free(M->aval); free(M->adiag); free(M->b); free(M->x); free(M->tt); free(M->st);
+  free(M->tw); free(M->sw);
+  lag_free(&M->L);
+  mesh_free(&M->m);
+  free(M);
+}
+
+static double* dup_arr(const double* src, size_t n) {
+  double* p = malloc(sizeof(double) * (n ? n : 1));
+  if (p && src) memcpy(p, src, sizeof(double) * n);
+  else if (p) memset(p, 0, sizeof(double) * n);
+  return p;
+}
+
+/* reset the history to the start of the loop (alpha = 1) */
+void oracle_marcher_reset(omarcher* M) {
+  size_t n = (size_t)(M->nt - 1) * M->ns;
+  memset(M->u, 0, sizeof(double) * n);
+  memset(M->q, 0, sizeof(double) * n);
+  memset(M->tau, 0, sizeof(double) * n);
+  memset(M->sig, 0, sizeof(double) * n);
+  if (M->rhs) memset(M->rhs, 0, sizeof(double) * n);
+  M->alpha = 1;
+  M->status = 0;
+  M->n_steps = 0;
+  M->rc = OR_OK;
+}
+
+int oracle_marcher_create(int nv, const double* verts, int ns, const int64_t* tris,
+                          const double* phi, int bie, int d, double c, double dt, int nt,
+                          int window, double threshold, const double* u_known,
+                          const double* q_known, int want_rhs, omarcher** out,
+                          double* t_asm_out) {
+  *out = 0;
+  if (d < 1 || d > 3 || nt < 2) return OR_INVALID;
+  omarcher* M = calloc(1, sizeof(omarcher));
+  if (!M) return OR_NOMEM;
+  int rc = mesh_build(&M->m, ns, verts, tris);
+  if (rc) { marcher_free(M); return rc; }
+  M->ns = ns; M->nt = nt; M->d = d; M->window = window; M->threshold = threshold;
+  M->gstar = oracle_gamma_star(nv, verts, ns, tris, d, c, dt);
+  M->n_lags = window ? (M->gstar < nt - 1 ? M->gstar : nt - 1) : nt - 1;
 #ifdef _OPENMP
   double t0 = omp_get_wtime();
 #endif
-  rc = lag_build(&L, &m, 0, ns, n_lags, bie, d, c, dt);
+  rc = lag_build(&M->L, &M->m, 0, ns, M->n_lags, bie, d, c, dt);
 #ifdef _OPENMP
   if (t_asm_out) *t_asm_out = omp_get_wtime() - t0;
 #endif
-  if (rc) { mesh_free(&m); lag_free(&L); return rc; }
-  const double* w = weights_d[d];
-  double w0 = w[0];
+  if (rc) { marcher_free(M); return rc; }
+  size_t n = (size_t)(nt - 1) * ns;
+  M->phi = dup_arr(phi, ns);
+  M->uk = dup_arr(u_known, n);
+  M->qk = dup_arr(q_known, n);
+  M->u = dup_arr(0, n); M->q = dup_arr(0, n); M->tau = dup_arr(0, n); M->sig = dup_arr(0, n);
+  M->rhs = want_rhs ? dup_arr(0, n) : 0;
+  M->b = dup_arr(0, ns); M->x = dup_arr(0, ns); M->tt = dup_arr(0, ns); M->st = dup_arr(0, ns);
+  M->tw = dup_arr(0, ns); M->sw = dup_arr(0, ns);
+  if (!M->phi || !M->uk || !M->qk || !M->u || !M->q || !M->tau || !M->sig || !M->b || !M->x ||
+      !M->tt || !M->st || !M->tw || !M->sw || (want_rhs && !M->rhs)) {
+    marcher_free(M);
+    return OR_NOMEM;
+  }
   /* step matrix A = w0 (W1 phi - U1 (1 - phi)) (marching.py:279-289), lag-1 CSR pattern */
-  const int64_t* arow = L.rowptr[0];
-  const int32_t* acol = L.col[0];
-  double* aval = malloc(sizeof(double) * (arow[ns] + 1));
-  double* adiag = malloc(sizeof(double) * ns);
+  const double w0 = weights_d[d][0];
+  const int64_t* arow = M->L.rowptr[0];
+  const int32_t* acol = M->L.col[0];
+  M->aval = malloc(sizeof(double) * (arow[ns] + 1));
+  M->adiag = malloc(sizeof(double) * ns);
+  if (!M->aval || !M->adiag) { marcher_free(M); return OR_NOMEM; }
+  int singular = 0;
   for (int i = 0; i < ns; ++i) {
-    adiag[i] = 0.0;
+    M->adiag[i] = 0.0;
     for (int64_t k = arow[i]; k < arow[i + 1]; ++k) {
       int j = acol[k];
-      aval[k] = w0 * (L.W[0][k] * phi[j] - L.U[0][k] * (1.0 - phi[j]));
-      if (j == i) adiag[i] = aval[k];
+      M->aval[k] = w0 * (M->L.W[0][k] * phi[j] - M->L.U[0][k] * (1.0 - phi[j]));
+      if (j == i) M->adiag[i] = M->aval[k];
     }
-    if (adiag[i] == 0.0) rc = OR_SINGULAR;
+    if (M->adiag[i] == 0.0) singular = 1;
   }
-  double *b = malloc(sizeof(double) * ns), *x = malloc(sizeof(double) * ns),
-         *tt = malloc(sizeof(double) * ns), *st = malloc(sizeof(double) * ns),
-         *tw = malloc(sizeof(double) * ns), *sw = malloc(sizeof(double) * ns);
-  memset(u, 0, sizeof(double) * (size_t)(nt - 1) * ns);
-  memset(q, 0, sizeof(double) * (size_t)(nt - 1) * ns);
-  memset(tau, 0, sizeof(double) * (size_t)(nt - 1) * ns);
-  memset(sig, 0, sizeof(double) * (size_t)(nt - 1) * ns);
-  *status = 0;
-  *n_steps = 0;
-  for (int alpha = 1; alpha < nt && rc == OR_OK; ++alpha) {
+  if (singular) { marcher_free(M); return OR_SINGULAR; }
+  oracle_marcher_reset(M);
+  *out = M;
+  return OR_OK;
+}
+
+/* Advance up to n_adv steps (stops at the end of the loop, a blow-up or an
+ * error).  *done = 1 when the loop is over.  *t_loop = wall seconds. */
+int oracle_marcher_run(omarcher* M, int n_adv, int* done, double* t_loop) {
+  const int ns = M->ns, nt = M->nt, d = M->d, gstar = M->gstar, n_lags = M->n_lags;
+  const int window = M->window;
+  const double* w = weights_d[d];
+  const double w0 = w[0];
+  const lagstore* L = &M->L;
+  const int64_t* arow = L->rowptr[0];
+  const int32_t* acol = L->col[0];
+  const double *aval = M->aval, *adiag = M->adiag, *phi = M->phi;
+  double *u = M->u, *q = M->q, *tau = M->tau, *sig = M->sig, *b = M->b, *x = M->x;
+  double *tt = M->tt, *st = M->st, *tw = M->tw, *sw = M->sw;
+#ifdef _OPENMP
+  double t0 = omp_get_wtime();
+#endif
+  int rc = M->rc;
+  for (int it_adv = 0; it_adv < n_adv && rc == OR_OK && M->status == 0 && M->alpha < nt;
+       ++it_adv) {
+    const int alpha = M->alpha;
     int beta0 = alpha - 1;
     int beta_star = alpha - gstar;
-    const double* uk = u_known + (size_t)beta0 * ns;
-    const double* qk = q_known + (size_t)beta0 * ns;
+    const double* uk = M->uk + (size_t)beta0 * ns;
+    const double* qk = M->qk + (size_t)beta0 * ns;
     /* tilde sums (marching.py:227-237) */
     for (int j = 0; j < ns; ++j) {
       tt[j] = w0 * qk[j] * phi[j];
@@ -442,7 +523,7 @@ int oracle_march(int nv, const double* verts, int ns, const int64_t* tris, const
         tt[j] += w[k] * q[(size_t)(beta0 - k) * ns + j];
         st[j] += w[k] * u[(size_t)(beta0 - k) * ns + j];
       }
-    lag_apply(&L, 1, tt, st, b, 1);
+    lag_apply(L, 1, tt, st, b, 1);
     int gmax = alpha < n_lags ? alpha : n_lags;
     for (int g = 2; g <= gmax; ++g) {
       int beta = alpha - g;
@@ -463,9 +544,9 @@ int oracle_march(int nv, const double* verts, int ns, const int64_t* tris, const
         tp = tau + (size_t)beta * ns;
         sp = sig + (size_t)beta * ns;
       }
-      lag_apply(&L, g, tp, sp, b, 0);
+      lag_apply(L, g, tp, sp, b, 0);
     }
-    if (rhs_trace) memcpy(rhs_trace + (size_t)beta0 * ns, b, sizeof(double) * ns);
+    if (M->rhs) memcpy(M->rhs + (size_t)beta0 * ns, b, sizeof(double) * ns);
     /* solve A x = b: Gauss-Seidel to round-off, then the reference residual test */
     double bn = 0.0;
     for (int i = 0; i < ns; ++i) { x[i] = b[i] / adiag[i]; bn += b[i] * b[i]; }
@@ -509,11 +590,127 @@ int oracle_march(int nv, const double* verts, int ns, const int64_t* tris, const
       tau[(size_t)beta0 * ns + j] = ta;
       sig[(size_t)beta0 * ns + j] = sa;
     }
-    *n_steps = alpha;
-    if (xmax > threshold) { *status = 1; break; }
+    M->n_steps = alpha;
+    M->alpha = alpha + 1;
+    if (xmax > M->threshold) M->status = 1;
   }
-  free(b); free(x); free(tt); free(st); free(tw); free(sw);
-  free(aval); free(adiag);
+  M->rc = rc;
+#ifdef _OPENMP
+  if (t_loop) *t_loop = omp_get_wtime() - t0;
+#endif
+  if (done) *done = (rc != OR_OK || M->status != 0 || M->alpha >= nt);
+  return rc;
+}
+
+/* copy the history out (any pointer may be NULL) */
+int oracle_marcher_get(const omarcher* M, double* u, double* q, double* tau, double* sig,
+                       double* rhs_trace, int* n_steps, int* status) {
+  size_t n = sizeof(double) * (size_t)(M->nt - 1) * M->ns;
+  if (u) memcpy(u, M->u, n);
+  if (q) memcpy(q, M->q, n);
+  if (tau) memcpy(tau, M->tau, n);
+  if (sig) memcpy(sig, M->sig, n);
+  if (rhs_trace && M->rhs) memcpy(rhs_trace, M->rhs, n);
+  if (n_steps) *n_steps = M->n_steps;
+  if (status) *status = M->status;
+  return M->rc;
+}
+
+void oracle_marcher_destroy(omarcher* M) { marcher_free(M); }
+
+/* Full march (marching.py:292-338): create + run to the end + copy out. */
+int oracle_march(int nv, const double* verts, int ns, const int64_t* tris, const double* phi,
+                 int bie, int d, double c, double dt, int nt, int window, double threshold,
+                 const double* u_known, const double* q_known, double* u, double* q, double* tau,
+                 double* sig, double* rhs_trace, int* n_steps, int* status, double* t_asm_out) {
+  omarcher* M = 0;
+  int rc = oracle_marcher_create(nv, verts, ns, tris, phi, bie, d, c, dt, nt, window, threshold,
+                                 u_known, q_known, rhs_trace != 0, &M, t_asm_out);
+  if (rc) return rc;
+  int done = 0;
+  rc = oracle_marcher_run(M, nt, &done, 0);
+  oracle_marcher_get(M, u, q, tau, sig, rhs_trace, n_steps, status);
+  oracle_marcher_destroy(M);
+  return rc;
+}
+
+/* Right-hand sides of the reference's march for a sample of rows, recomputed
+ * from a GIVEN history (u, q, tau, sigma: (nt-1, ns), e.g. the GPU's), in the
+ * reference's sigma/tau lag-CSR form (marching.py:315-327) restricted to those
+ * rows.  For each (row, step) pair k: b[k] = b_row^alpha, and
+ * res[k] = (A x^{alpha-1})_row - b[k] with A the lag-1 step matrix
+ * (marching.py:279-289) and x the history's unknown density at beta0.
+ * rows/alphas: n_rows rows x n_alpha steps (alpha >= 1), outputs row-major. */
+int oracle_rhs_rows(int nv, const double* verts, int ns, const int64_t* tris, const double* phi,
+                    int bie, int d, double c, double dt, int nt, int window, int n_rows,
+                    const int* rows, int n_alpha, const int* alphas, const double* u_known,
+                    const double* q_known, const double* u, const double* q, const double* tau,
+                    const double* sig, double* b_out, double* res_out) {
+  if (d < 1 || d > 3 || nt < 2) return OR_INVALID;
+  omesh m;
+  int rc = mesh_build(&m, ns, verts, tris);
+  if (rc) return rc;
+  int gstar = oracle_gamma_star(nv, verts, ns, tris, d, c, dt);
+  int n_lags = window ? (gstar < nt - 1 ? gstar : nt - 1) : nt - 1;
+  const double* w = weights_d[d];
+  const double w0 = w[0];
+  lagstore L;
+  memset(&L, 0, sizeof(L));
+  rc = lag_build_list(&L, &m, 0, n_rows, rows, n_lags, bie, d, c, dt);
+  if (rc) { lag_free(&L); mesh_free(&m); return rc; }
+#pragma omp parallel for collapse(2) schedule(dynamic, 1)
+  for (int r = 0; r < n_rows; ++r)
+    for (int a = 0; a < n_alpha; ++a) {
+      const int alpha = alphas[a];
+      const int beta0 = alpha - 1, beta_star = alpha - gstar;
+      const int gmax = alpha < n_lags ? alpha : n_lags;
+      double bsum = 0.0;
+      for (int g = 1; g <= gmax; ++g) {
+        const int64_t* rp = L.rowptr[g - 1] + r;
+        const int32_t* col = L.col[g - 1];
+        const int beta = alpha - g;
+        double su = 0.0, sw = 0.0;
+        for (int64_t p = rp[0]; p < rp[1]; ++p) {
+          const int j = col[p];
+          double tj, sj;
+          if (g == 1) { /* tilde sums (marching.py:227-237) */
+            tj = w0 * q_known[(size_t)beta0 * ns + j] * phi[j];
+            sj = w0 * u_known[(size_t)beta0 * ns + j] * (1.0 - phi[j]);
+            int kt = d + 1 < beta0 ? d + 1 : beta0;
+            for (int k = 1; k <= kt; ++k) {
+              tj += w[k] * q[(size_t)(beta0 - k) * ns + j];
+              sj += w[k] * u[(size_t)(beta0 - k) * ns + j];
+            }
+          } else if (window && beta - beta_star <= d) { /* windowed_sums (:216-225) */
+            int kmax = d + 1;
+            if (beta - beta_star < kmax) kmax = beta - beta_star;
+            if (beta < kmax) kmax = beta;
+            tj = 0.0; sj = 0.0;
+            for (int k = 0; k <= kmax; ++k) {
+              tj += w[k] * q[(size_t)(beta - k) * ns + j];
+              sj += w[k] * u[(size_t)(beta - k) * ns + j];
+            }
+          } else {
+            tj = tau[(size_t)beta * ns + j];
+            sj = sig[(size_t)beta * ns + j];
+          }
+          su += L.U[g - 1][p] * tj;
+          sw += L.W[g - 1][p] * sj;
+        }
+        bsum += su - sw;
+      }
+      b_out[(size_t)r * n_alpha + a] = bsum;
+      /* residual of the lag-1 row against the history's solution at beta0 */
+      double ax = 0.0;
+      const int64_t* rp = L.rowptr[0] + r;
+      for (int64_t p = rp[0]; p < rp[1]; ++p) {
+        const int j = L.col[0][p];
+        const double aij = w0 * (L.W[0][p] * phi[j] - L.U[0][p] * (1.0 - phi[j]));
+        const double xj = phi[j] == 1.0 ? u[(size_t)beta0 * ns + j] : q[(size_t)beta0 * ns + j];
+        ax += aij * xj;
+      }
+      if (res_out) res_out[(size_t)r * n_alpha + a] = ax - bsum;
+    }
   lag_free(&L);
   mesh_free(&m);
   return rc;

@@ -39,7 +39,8 @@ class Info(C.Structure):
                 ("conv_splits", C.c_int32), ("solve_cluster", C.c_int32),
                 ("n_units", C.c_int64), ("units_hdr32", C.c_int64),
                 ("steps_per_pass", C.c_int32), ("near_width", C.c_int32), ("pass_overlap", C.c_int32),
-                ("solve_halo", C.c_int32), ("fmm_m2l_pairs", C.c_int64)]
+                ("solve_halo", C.c_int32), ("fmm_m2l_pairs", C.c_int64),
+                ("conv_rpw", C.c_int32), ("coeff_mode", C.c_int32)]
 
     def asdict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

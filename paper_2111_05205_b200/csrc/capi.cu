@@ -394,6 +394,8 @@ int tdw_problem_info(const tdw_problem* pb, tdw_info* out) {
   out->pass_overlap = pb->overlap;
   out->solve_halo = pb->sp_halo;
   out->near_width = pb->near_w;
+  out->conv_rpw = pb->conv_rpw;
+  out->coeff_mode = 0;
   return TDW_OK;
 }
 

@@ -89,6 +89,8 @@ class FmmStore(BandStore):
         # nranks > 1: this rank's rows of the near field, M2L into the target
         # leaf cells of those rows (and their ancestors) only; b is all-gathered
         # every step (csrc/fmm.cu, tdw_fmm_loop / tdw_fmm_march_emulated)
+        if plan is None:
+            (config or FmmConfig()).check_gpu()
         super().__init__(spec, window=True, ctx=ctx, nranks=nranks, rank=rank, shard_only=shard_only)
         self.plan = plan or build_plan(spec, config)
         A = fmm_desc_arrays(self.plan, spec.nt)
@@ -116,6 +118,8 @@ def fast_march(spec, config: FmmConfig | None = None, window: bool = True, blowu
                nranks: int = 1, rank: int = 0):
     """Run the fast solver on the GPU (fmm.py:534-544).  `window` is accepted for
     signature compatibility: the near field always uses the gamma_near window.
+    `config=None` means the reference's FmmConfig() (ps = pt = 8), which the GPU
+    solver rejects with ValueError; pass fmm_plan.baseline_config() (ps = pt = 4).
     Multi-GPU (one process per GPU): pass the rank's context (with its
     communicator, distributed.init_comm) and nranks / rank."""
     store = FmmStore(spec, config, ctx=ctx, nranks=nranks, rank=rank).assemble()

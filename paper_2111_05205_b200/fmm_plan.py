@@ -31,12 +31,33 @@ from .tbasis import trunc_pow
 
 @dataclass
 class FmmConfig:
-    """Reference FmmConfig (fmm.py:35-41); BASELINE pins ps = pt = 4, Z = 20, mu = 8."""
-    ps: int = 4
-    pt: int = 4
-    leaf_capacity: int = 20
+    """Reference FmmConfig (fmm.py:35-41), with the reference's defaults (ps = pt = 8,
+    leaf capacity 100, mu = 8).  The GPU fast solver implements ps = pt = 4 and
+    mu <= 8 (the BASELINE configuration, with leaf capacity 20 as SURVEY 8(d) pins):
+    `check_gpu()` raises ValueError naming that limit for anything else."""
+    ps: int = 8
+    pt: int = 8
+    leaf_capacity: int = 100
     mu: int = 8
     element_extrapolation: float = 1.0
+
+    GPU_PS = 4
+    GPU_PT = 4
+    GPU_MU_MAX = 8
+
+    def check_gpu(self):
+        if self.ps != self.GPU_PS or self.pt != self.GPU_PT:
+            raise ValueError(f"the GPU fast solver supports ps = pt = {self.GPU_PS} interpolation "
+                             f"orders (BASELINE configs 3-4); got ps={self.ps}, pt={self.pt}")
+        if not 1 <= self.mu <= self.GPU_MU_MAX:
+            raise ValueError(f"the GPU fast solver supports 1 <= mu <= {self.GPU_MU_MAX}; got mu={self.mu}")
+        return self
+
+
+def baseline_config() -> FmmConfig:
+    """BASELINE configs 3-4: 4 x 4 x 4 spatial nodes, temporal order 4, leaf capacity
+    20 (leaf edge 3.3-4.2 c dt: the smallest the mu = 8 causality check admits), mu = 8."""
+    return FmmConfig(ps=4, pt=4, leaf_capacity=20, mu=8)
 
 
 def cmp_coeff(p: int, m: int, k: int) -> float:

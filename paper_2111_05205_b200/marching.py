@@ -88,9 +88,41 @@ class TimeHistory:
         self.sigma = np.zeros(shape)
 
     def stock_sums(self, beta: int):
-        w = decomposition_weights(self.basis.d)
-        ks = range(min(self.basis.d + 1, beta) + 1)
-        return (sum(w[k] * self.q[beta - k] for k in ks), sum(w[k] * self.u[beta - k] for k in ks))
+        """Full kappa sums tau/sigma at step beta, zero-padded history (marching.py:205-214)."""
+        w = self.basis.weights
+        tau = np.zeros(self.n_elements)
+        sig = np.zeros(self.n_elements)
+        for k in range(min(self.basis.d + 1, beta) + 1):
+            tau += w[k] * self.q[beta - k]
+            sig += w[k] * self.u[beta - k]
+        return tau, sig
+
+    def windowed_sums(self, beta: int, beta_star: int):
+        """kappa sums truncated at the sliding-window bottom beta_star (marching.py:216-225)."""
+        w = self.basis.weights
+        kmax = min(self.basis.d + 1, beta - beta_star, beta)
+        tau = np.zeros(self.n_elements)
+        sig = np.zeros(self.n_elements)
+        for k in range(kmax + 1):
+            tau += w[k] * self.q[beta - k]
+            sig += w[k] * self.u[beta - k]
+        return tau, sig
+
+    def tilde_sums(self, beta: int, phi, u_known, q_known):
+        """Current-step sums with the unknown w0 component dropped (marching.py:227-237)."""
+        w = self.basis.weights
+        tau = w[0] * q_known * phi
+        sig = w[0] * u_known * (1.0 - phi)
+        for k in range(1, min(self.basis.d + 1, beta) + 1):
+            tau += w[k] * self.q[beta - k]
+            sig += w[k] * self.u[beta - k]
+        return tau, sig
+
+    def finalize_step(self, beta: int, phi, u_known, q_known, solved):
+        """Promote the solved density by phi and refresh tau/sigma (marching.py:239-242)."""
+        self.u[beta] = np.where(phi == 1.0, solved, u_known)
+        self.q[beta] = np.where(phi == 1.0, q_known, solved)
+        self.tau[beta], self.sigma[beta] = self.stock_sums(beta)
 
     def knot_values(self, kind: str = "u") -> np.ndarray:
         coef = self.u if kind == "u" else self.q
@@ -171,6 +203,10 @@ class BandStore:
                    "tdw_problem_create")
         self.nranks, self.rank = int(nranks), int(rank)
         self.assembled = False
+        # what the device store was built from: march(spec, mats=store) refuses a
+        # spec that differs (the split-lag store and the step matrix depend on phi,
+        # the coefficients on bie, d, c, dt and the geometry)
+        self.key = problem_key(spec)
 
     def assemble(self):
         if not self.assembled:
@@ -246,6 +282,31 @@ class BandStore:
             pass
 
 
+def problem_key(spec) -> tuple:
+    """Everything a device store depends on: geometry, phi, bie, d, c, dt."""
+    import hashlib
+    h = hashlib.sha1()
+    for a in (spec.mesh.vertices, spec.mesh.triangles, spec.phi):
+        a = np.ascontiguousarray(a)
+        h.update(str(a.dtype).encode() + str(a.shape).encode())
+        h.update(a.tobytes())
+    return (h.hexdigest(), spec.bie, int(spec.basis.d), float(spec.c), float(spec.basis.dt))
+
+
+def _check_store(mats, spec, window):
+    if mats.window != window or mats.nt < spec.nt or mats.ns != spec.mesh.n_elements:
+        raise ValueError("matrix set does not cover the required lags")
+    if mats.nt != spec.nt:
+        raise ValueError(f"store built for nt={mats.nt}, spec has nt={spec.nt}: rebuild it "
+                         "(the device history is sized at assembly)")
+    key = problem_key(spec)
+    if key != mats.key:
+        names = ("geometry/phi", "bie", "d", "c", "dt")
+        diff = [n for n, a, b in zip(names, key, mats.key) if a != b]
+        raise ValueError(f"store was assembled for a different problem ({', '.join(diff)} differ): "
+                         "build it from this spec")
+
+
 def build_retarded_matrices(spec, gamma_max: int | None = None, pairs=None, slab: int = 2_000_000,
                             window: bool = True) -> BandStore:
     """Assemble the device banded store (replaces marching.py:132-181).
@@ -271,8 +332,8 @@ def march(spec, window: bool = True, blowup_factor: float = 1e6, mats=None,
         mats = BandStore(spec, window=window)
     elif not isinstance(mats, BandStore):
         raise TypeError("mats must come from build_retarded_matrices of this package")
-    elif mats.window != window or mats.nt != spec.nt or mats.ns != spec.mesh.n_elements:
-        raise ValueError("matrix set does not cover the required lags")
+    else:
+        _check_store(mats, spec, window)
     hist = TimeHistory(spec.basis, spec.nt, spec.mesh.n_elements)
     # outputs in page-locked memory (a pool: blocks come back when the arrays die);
     # the library writes every entry

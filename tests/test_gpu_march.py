@@ -312,3 +312,37 @@ def test_device_side_boundary_data(cfg):
         n = np.linalg.norm(b, axis=1)
         assert (np.linalg.norm(a - b, axis=1) / np.maximum(n, 1e-6 * max(n.max(), 1e-300))).max() < 1e-12
     store.close()
+
+
+@pytest.mark.parametrize("cfg", [2, 3])
+def test_full_size_rhs_matches_reference_form(cfg):
+    """Full BASELINE size, every step's right-hand side in the reference's own
+    sigma/tau lag-CSR form.  For a seeded sample of rows and steps the oracle
+    rebuilds those rows of the reference's per-lag matrices (marching.py:132-181)
+    and recomputes b_i^alpha (marching.py:315-327: tilde sums, windowed sums at
+    the gamma* window bottom, stock sums) from the GPU's OWN history; the GPU's
+    rhs_trace must agree (1e-9, 1e-7 for d = 2 BMBIE), and the GPU's solution
+    must pass the reference's residual test on those rows (marching.py:330-333)."""
+    spec = scenarios.build_spec(cfg)
+    trace = []
+    h = marching.march(spec, rhs_trace=trace)
+    assert h.status == "stable" and h.n_steps == spec.nt - 1
+    rhs = np.array(trace)
+    ns, nt, d = spec.mesh.n_elements, spec.nt, spec.basis.d
+    gstar = marching.BandStore(spec).gamma_star
+    rng = np.random.default_rng(100 + cfg)
+    rows = np.sort(rng.choice(ns, size=48, replace=False))
+    alphas = sorted({1, 2, d + 2, gstar - 1, gstar, gstar + 1, gstar + d + 2, (nt - 1) // 2,
+                     nt - 2, nt - 1} | set(rng.integers(3, nt - 1, size=6).tolist()))
+    alphas = [a for a in alphas if 1 <= a <= nt - 1]
+    uk, qk = marching.greville_samples(spec)
+    b, res = oracle.rhs_rows(spec.mesh.vertices, spec.mesh.triangles, spec.phi, spec.bie, d, spec.c,
+                             spec.basis.dt, nt, rows, alphas, uk, qk, h.u, h.q, h.tau, h.sigma)
+    got = rhs[np.array(alphas) - 1][:, rows].T            # (rows, alphas)
+    err = np.linalg.norm(got - b, axis=0) / np.maximum(np.linalg.norm(b, axis=0), 1e-300)
+    rel_res = np.linalg.norm(res, axis=0) / np.maximum(np.linalg.norm(b, axis=0), 1e-300)
+    tol = TOL[d] if spec.bie == "bmbie" else 1e-9
+    print(f"cfg{cfg} rhs vs reference form: worst step {err.max():.3e} (tol {tol:g}), "
+          f"worst residual {rel_res.max():.3e}, steps {alphas}")
+    assert err.max() < tol, (err.max(), alphas[int(err.argmax())])
+    assert rel_res.max() < 1e-10
