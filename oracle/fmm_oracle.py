@@ -95,9 +95,12 @@ class FmmOracle:
                                  aux={(p, m): np.zeros((n, self.nd)) for p in range(2, self.d + 1)
                                       for m in range(p - 1)},
                                  acc=np.zeros((n, self.nd)))
-        # dense operators per (level, offset, op): op 0..mu = lags 1..mu+1, mu+1.. = p=1..d
+        # dense operators per (level, offset): op 0..mu = lags 1..mu+1, mu+1.. = p=1..d,
+        # stacked (nops, nd, nd); the interaction pairs of a level grouped by offset
+        # (an observer appears at most once per offset, so a group's updates never collide)
         from paper_2111_05205_b200.fmm_plan import dense_operator
         self.ops = {}
+        self.groups = {}
         for L, ops in plan.levels.items():
             mats = []
             for o in range(len(ops.offsets)):
@@ -106,46 +109,59 @@ class FmmOracle:
                 for p in range(1, self.d + 1):
                     Kp = ops.Kp[p - 1][o].reshape(2 * ps - 1, 2 * ps - 1, 2 * ps - 1, -1)
                     row.append(dense_operator(Kp, ps, pt, pt - 1))
-                mats.append(row)
+                mats.append(np.stack(row))
             self.ops[L] = mats
+            obs = np.repeat(np.arange(ops.n_cells), np.diff(ops.obs_ptr))
+            src, off = np.asarray(ops.il_src), np.asarray(ops.il_off)
+            order = np.argsort(off, kind="stable")
+            bounds = np.searchsorted(off[order], np.arange(len(ops.offsets) + 1))
+            self.groups[L] = [(obs[order[bounds[o]:bounds[o + 1]]], src[order[bounds[o]:bounds[o + 1]]])
+                              for o in range(len(ops.offsets))]
 
-    # -- translation operators (fmm.py:314-326): index order (a1, a2, a3, m)
+    # -- translation operators (fmm.py:314-326): index order (a1, a2, a3, m), applied
+    #    to all cells of one octant at once
     def _transfer_moment(self, M, octant, half):
         P = self.plan
-        X = M.reshape(P.ps, P.ps, P.ps, P.pt)
-        X = np.einsum("pa,abcm->pbcm", P.t_space[octant[0]], X)
-        X = np.einsum("qb,pbcm->pqcm", P.t_space[octant[1]], X)
-        X = np.einsum("rc,pqcm->pqrm", P.t_space[octant[2]], X)
-        X = np.einsum("sm,pqrm->pqrs", P.t_time[half], X)
-        return X.reshape(-1)
+        X = M.reshape(-1, P.ps, P.ps, P.ps, P.pt)
+        X = np.einsum("pa,nabcm->npbcm", P.t_space[octant[0]], X)
+        X = np.einsum("qb,npbcm->npqcm", P.t_space[octant[1]], X)
+        X = np.einsum("rc,npqcm->npqrm", P.t_space[octant[2]], X)
+        X = np.einsum("sm,npqrm->npqrs", P.t_time[half], X)
+        return X.reshape(len(X), -1)
 
     def _transfer_local(self, Lp, octant, half):
         P = self.plan
-        X = Lp.reshape(P.ps, P.ps, P.ps, P.pt)
-        X = np.einsum("pa,pbcm->abcm", P.t_space[octant[0]], X)
-        X = np.einsum("qb,aqcm->abcm", P.t_space[octant[1]], X)
-        X = np.einsum("rc,abrm->abcm", P.t_space[octant[2]], X)
-        X = np.einsum("sm,abcs->abcm", P.t_time[half], X)
-        return X.reshape(-1)
+        X = Lp.reshape(-1, P.ps, P.ps, P.ps, P.pt)
+        X = np.einsum("pa,npbcm->nabcm", P.t_space[octant[0]], X)
+        X = np.einsum("qb,naqcm->nabcm", P.t_space[octant[1]], X)
+        X = np.einsum("rc,nabrm->nabcm", P.t_space[octant[2]], X)
+        X = np.einsum("sm,nabcs->nabcm", P.t_time[half], X)
+        return X.reshape(len(X), -1)
+
+    def _octant_groups(self, ops):
+        oc = np.asarray(ops.octant)
+        key = oc[:, 0] + 2 * oc[:, 1] + 4 * oc[:, 2]
+        return [(np.nonzero(key == g)[0], oc[np.nonzero(key == g)[0][0]]) for g in range(8) if (key == g).any()]
 
     def _do_m2l(self, L, k, moments):
+        """Near-future lags, derivative operators and the Algorithm-1 recurrence
+        (fmm.py:329-368), one dense contraction per offset group."""
         P, st, ops = self.plan, self.state[L], self.plan.levels[L]
-        mu, d = P.mu, self.d
+        mu, d, nd = P.mu, self.d, self.nd
         T = P.c * ops.interval
         ring = mu + 3
-        tmp = np.zeros((d, ops.n_cells, self.nd))
-        for o_cell in range(ops.n_cells):
-            for q in range(ops.obs_ptr[o_cell], ops.obs_ptr[o_cell + 1]):
-                s, oi = ops.il_src[q], ops.il_off[q]
-                Ms = moments[s]
-                if not Ms.any():
+        tmp = np.zeros((d, ops.n_cells, nd))
+        for oi, (obs, src) in enumerate(self.groups[L]):
+            if len(obs) == 0:
+                continue
+            Ms = moments[src]                                    # (n, nd)
+            Y = np.einsum("onm,pm->opn", self.ops[L][oi], Ms)     # (nops, n, nd)
+            for l in range(1, mu + 2):
+                if ops.dark[oi, l - 1]:
                     continue
-                for l in range(1, mu + 2):
-                    if ops.dark[oi, l - 1]:
-                        continue
-                    st["own"][(k + l) % ring, o_cell] += self.ops[L][oi][l - 1] @ Ms
-                for p in range(1, d + 1):
-                    tmp[p - 1, o_cell] += self.ops[L][oi][mu + p] @ Ms
+                st["own"][(k + l) % ring][obs] += Y[l - 1]
+            for p in range(1, d + 1):
+                tmp[p - 1][obs] += Y[mu + p]
         from paper_2111_05205_b200.fmm_plan import cmp_coeff
         for p in range(1, d + 1):
             upd = tmp[p - 1].copy()
@@ -161,6 +177,9 @@ class FmmOracle:
                 st["aux"][(p, m)] += tmp[p - 1] * float(k) ** m
 
     def _tick(self, k_leaf):
+        """Close leaf interval k_leaf (fmm.py:371-419): M2L at the leaf, M2M up while
+        the time-half bit is 1 (M2L at each closed level), L2L down into the
+        children's inherit slots."""
         P = self.plan
         leaf = P.leaf
         completed = [leaf]
@@ -172,10 +191,9 @@ class FmmOracle:
             ops = P.levels[L]
             pst = self.state[L - 1]
             half = cur_k & 1
-            for ci in range(ops.n_cells):
-                if not moments[ci].any():
-                    continue
-                pst["acc"][ops.parent[ci]] += self._transfer_moment(moments[ci], ops.octant[ci], half)
+            for cells, oc in self._octant_groups(ops):
+                np.add.at(pst["acc"], np.asarray(ops.parent)[cells],
+                          self._transfer_moment(moments[cells], oc, half))
             if half == 0:
                 break
             cur_k >>= 1
@@ -193,12 +211,11 @@ class FmmOracle:
             total = st["own"][(k_level + 1) % ring] + st["inherit"][(k_level + 1) % 4]
             child = P.levels[L + 1]
             cst = self.state[L + 1]
-            for ci in range(child.n_cells):
-                p = child.parent[ci]
+            par = np.asarray(child.parent)
+            for cells, oc in self._octant_groups(child):
                 for half in (0, 1):
                     kc = 2 * (k_level + 1) + half
-                    cst["inherit"][kc % 4, ci] = (self._transfer_local(total[p], child.octant[ci], half)
-                                                  if total[p].any() else 0.0)
+                    cst["inherit"][kc % 4, cells] = self._transfer_local(total[par[cells]], oc, half)
 
     def run(self, u_known, q_known, threshold=1e6):
         spec, P = self.spec, self.plan

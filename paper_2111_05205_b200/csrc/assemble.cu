@@ -801,54 +801,56 @@ int tdw_assemble_impl(tdw_problem* pb) {
     auto streamed = [&](long long u) { return hu[u].y >= hu[u].x || !pb->skip_empty_units; };
     const char* sm = getenv("TDW_SCHED");
     if (!(sm && strcmp(sm, "rr") == 0)) {
-      // byte-balanced contiguous chunks: the units in (I-block, tile) order are cut
-      // into G runs of equal streamed bytes (+ a fixed per-unit cost), so every
-      // persistent CTA ends together.  An I-block cut by chunk boundaries gets one
-      // partial per chunk touching it; S = the most chunks touching one I-block.
+      // Fixed summation groups: the J-tiles of an I-block are cut into groups of
+      // TDW_GROUP_TILES (default 4) consecutive tiles.  A group is always summed by
+      // ONE CTA (units in tile order, then the warp's lane reduction) into its own
+      // partial, and the partials of a row are added in group order
+      // (reduce_parts / sum_parts).  The grouping depends on the problem only, not
+      // on the grid size or on how rows are sharded over ranks, so b -- and every
+      // density -- is bit-identical for any rank count and any SM reservation.
+      // The persistent CTAs get byte-balanced contiguous runs of whole groups.
       // weight: coefficient bytes + a fixed per-unit cost (header, history box);
       // independent of the header width, so both widths give the same schedule
       const double per_unit = 4096.0;
       auto weight = [&](long long u) { return (double)(uoff[u + 1] - uoff[u] - ucoef[u]) + per_unit; };
+      int gt = 4;
+      if (const char* e = getenv("TDW_GROUP_TILES")) gt = std::max(1, atoi(e));
+      const int SG = (pb->ntiles + gt - 1) / gt;
+      const long long ngroup = (long long)pb->n_iblk * SG;
+      std::vector<double> gw(ngroup, 0.0);
+      std::vector<char> gstream(ngroup, 0);
       double total = 0.0;
-      long long nstream = 0;
       for (long long u = 0; u < nunit; ++u)
         if (streamed(u)) {
+          const long long ib = u / pb->ntiles, t = u % pb->ntiles, gidx = ib * SG + t / gt;
+          gw[gidx] += weight(u);
+          gstream[gidx] = 1;
           total += weight(u);
-          ++nstream;
         }
-      G = (int)std::max(1LL, std::min<long long>(ctx->num_sms - (pb->conv_reserve ? pb->sp_cl : 0), nstream));
+      long long nlive = 0;
+      for (long long gidx = 0; gidx < ngroup; ++gidx) nlive += gstream[gidx];
+      G = (int)std::max(1LL, std::min<long long>(ctx->num_sms - (pb->conv_reserve ? pb->sp_cl : 0), nlive));
       if (const char* gm = getenv("TDW_CONV_GRID_MAX")) G = std::max(1, std::min(G, atoi(gm)));  // experiments
       soff.assign(G + 1, 0);
-      std::vector<int> chunk_of(nunit, -1);
+      std::vector<int> chunk_of_group(ngroup, -1);
       double acc = 0.0;
-      for (long long u = 0; u < nunit; ++u) {
-        if (!streamed(u)) continue;
-        const double w = weight(u);
-        chunk_of[u] = std::min(G - 1, (int)((acc + 0.5 * w) / total * G));
-        acc += w;
-      }
-      std::vector<int> clo(pb->n_iblk, INT_MAX);
-      S = 1;
-      for (int ib = 0; ib < pb->n_iblk; ++ib) {
-        int lo = INT_MAX, hi = -1;
-        for (int t = 0; t < pb->ntiles; ++t) {
-          const int c = chunk_of[(long long)ib * pb->ntiles + t];
-          if (c >= 0) { lo = std::min(lo, c); hi = std::max(hi, c); }
-        }
-        clo[ib] = lo;
-        if (hi >= 0) S = std::max(S, hi - lo + 1);
+      for (long long gidx = 0; gidx < ngroup; ++gidx) {
+        if (!gstream[gidx]) continue;
+        chunk_of_group[gidx] = std::min(G - 1, (int)((acc + 0.5 * gw[gidx]) / total * G));
+        acc += gw[gidx];
       }
       int k = 0;
       for (long long u = 0; u < nunit; ++u) {
-        if (chunk_of[u] < 0) continue;
-        while (k <= chunk_of[u]) soff[k++] = (unsigned)sched.size();
-        const long long ib = u / pb->ntiles;
+        if (!streamed(u)) continue;
+        const long long ib = u / pb->ntiles, t = u % pb->ntiles, gidx = ib * SG + t / gt;
+        const int c = chunk_of_group[gidx];
+        while (k <= c) soff[k++] = (unsigned)sched.size();
         sched.push_back((unsigned)u);
-        sitem.push_back((unsigned)(ib * S + (chunk_of[u] - clo[ib])));
+        sitem.push_back((unsigned)gidx);
       }
       while (k < G) soff[k++] = (unsigned)sched.size();
       pb->conv_grid = G;
-      pb->conv_S = S;
+      pb->conv_S = S = SG;
     } else {
     const long long items = (long long)pb->n_iblk * S;
     for (int b = 0; b < G; ++b) {

@@ -63,6 +63,11 @@ struct FmmLevel {
   int* t_pair = nullptr;       // [nil] column of Yall
   int* t_cells = nullptr;      // [n_tcell] target cells with pairs
   int n_tcell = 0;
+  // own M2L kernel (m2l_dmma_kernel): work items (offset, first pair, pairs) and
+  // the dark-lag bits of each grouped pair's offset (the scatter skips those rows)
+  int4* items = nullptr;
+  int n_items = 0;
+  unsigned* g_dark = nullptr;  // [nil]
   // the level's GEMMs as one grouped call (one group per nonempty offset)
   std::vector<int> gm, gn, gk, glda, gldb, gldc, gsize;
   std::vector<double> galpha, gbeta;
@@ -276,16 +281,23 @@ __global__ void build_kop_kernel(const double* __restrict__ K0, const double* __
 // all offset groups of a level at once: block (target cell with pairs, operator),
 // thread = node; adds the cell's GEMM columns in group order onto own / tmp, the
 // same additions in the same order as one scatter per group
+// (g_dark != null: rows of a pair's dark lags were not computed -- skipped, as the
+// reference skips dark lags, fmm.py:343-346)
 __global__ void scatter_all_kernel(const int* __restrict__ t_cells, const int* __restrict__ t_ptr,
-                                   const int* __restrict__ t_pair, const double* __restrict__ Y, int nops,
-                                   int mu, int k, int ncell, double* own, double* tmp) {
+                                   const int* __restrict__ t_pair, const unsigned* __restrict__ g_dark,
+                                   const double* __restrict__ Y, int nops, int mu, int k, int ncell,
+                                   double* own, double* tmp) {
   const int ring = mu + 3;
   const long long M = (long long)nops * FND;
   const int cell = t_cells[blockIdx.x], op = blockIdx.y, idx = threadIdx.x;
   double* dst = op <= mu ? own + ((size_t)((k + op + 1) % ring) * ncell + cell) * FND + idx
                          : tmp + ((size_t)(op - mu - 1) * ncell + cell) * FND + idx;
   double acc = *dst;
-  for (int q = t_ptr[cell]; q < t_ptr[cell + 1]; ++q) acc += __ldg(Y + (long long)t_pair[q] * M + (long long)op * FND + idx);
+  for (int q = t_ptr[cell]; q < t_ptr[cell + 1]; ++q) {
+    const int pq = t_pair[q];
+    if (g_dark && op <= mu && ((__ldg(g_dark + pq) >> op) & 1u)) continue;
+    acc += __ldg(Y + (long long)pq * M + (long long)op * FND + idx);
+  }
   *dst = acc;
 }
 __global__ void gather_kernel(const int* __restrict__ g_src, long long nil,
@@ -295,6 +307,119 @@ __global__ void gather_kernel(const int* __restrict__ g_src, long long nil,
     X[e] = mom[(size_t)g_src[e / FND] * FND + (e % FND)];
 }
 
+
+// ------------------------------------------------------------- M2L contraction
+// The level tick's M2L (fmm.py:52-69 _toeplitz_apply, :329-368 _do_m2l) in the
+// GEMM form, on the FP64 tensor cores (DMMA, mma.sync m8n8k4 f64).  One CTA =
+// one work item (offset o, up to M2L_NC interaction pairs of that offset):
+//   Y[pair][op*256 + a*4 + m] = sum_{b,n} Kx_op[a-b][m-n+toff_op] * mom[src][b*4 + n]
+// for every non-dark operator op (lags 1..mu+1 from K0, derivative orders p =
+// 1..d from Kp).  The operator is never materialised: the offset's Toeplitz
+// tensors (343 spatial differences x 31 / 7 time differences, ~123 KB for
+// d = 2) are staged in shared memory once per item and every A fragment is read
+// from them directly (address = row part - column part, both precomputed); the
+// pairs' source moments are gathered into shared memory (column stride 260
+// doubles: conflict-free B fragments).  Each warp owns 32-row blocks (4 m8 x 4 n8
+// DMMA tiles, 16 accumulators) of the stacked operator rows; the epilogue writes
+// the pair-major output Y that scatter_all_kernel sums per target cell in
+// group order (deterministic, as with the library GEMM it replaces).
+constexpr int M2L_NC = 32;            // pairs (columns) per work item
+constexpr int M2L_BLD = FND + 4;      // shared-memory column stride of the gathered moments
+constexpr int M2L_WARPS = 8;
+
+__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+__host__ __device__ constexpr size_t m2l_smem_bytes(int d, int ntau0, int ntaup) {
+  return sizeof(double) * ((size_t)FKR * ntau0 + (size_t)d * FKR * ntaup + (size_t)M2L_NC * M2L_BLD);
+}
+
+// S(x) = 49 x1 + 7 x2 + x3 of spatial node x = (x1 << 4) | (x2 << 2) | x3: the
+// Toeplitz row of (a, b) is S(a) - S(b) + 171
+__device__ __forceinline__ int m2l_S(int x) { return 49 * (x >> 4) + 7 * ((x >> 2) & 3) + (x & 3); }
+
+template <int D>
+__global__ void __launch_bounds__(M2L_WARPS * 32, 1)
+m2l_dmma_kernel(const int4* __restrict__ items, const double* __restrict__ K0, const double* __restrict__ Kp,
+                const int* __restrict__ g_src, const unsigned* __restrict__ dark, const double* __restrict__ mom,
+                int noff, int ntau0, int ntaup, int mu, double* __restrict__ Y) {
+  extern __shared__ __align__(16) double m2l_sm[];
+  const int4 it = items[blockIdx.x];  // (offset, first grouped pair, pairs)
+  const int o = it.x, p0 = it.y, np = it.z;
+  double* T0 = m2l_sm;                                   // [343][ntau0]
+  double* Tp = T0 + (size_t)FKR * ntau0;                 // [D][343][ntaup]
+  double* Bs = Tp + (size_t)D * FKR * ntaup;             // [M2L_NC][M2L_BLD]
+  const int tid = threadIdx.x, nthr = M2L_WARPS * 32;
+  {
+    const double* src0 = K0 + (size_t)o * FKR * ntau0;
+    for (int e = tid; e < FKR * ntau0; e += nthr) T0[e] = __ldg(src0 + e);
+    for (int p = 0; p < D; ++p) {
+      const double* srcp = Kp + ((size_t)p * noff + o) * FKR * ntaup;
+      for (int e = tid; e < FKR * ntaup; e += nthr) Tp[p * FKR * ntaup + e] = __ldg(srcp + e);
+    }
+    // gathered source moments, two doubles per thread and step (zero columns past np)
+    for (int e = tid; e < M2L_NC * (FND / 2); e += nthr) {
+      const int j = e / (FND / 2), k2 = e % (FND / 2);
+      double2 v = make_double2(0.0, 0.0);
+      if (j < np) v = __ldg(reinterpret_cast<const double2*>(mom + (size_t)g_src[p0 + j] * FND) + k2);
+      *reinterpret_cast<double2*>(Bs + j * M2L_BLD + 2 * k2) = v;
+    }
+  }
+  __syncthreads();
+  const int nops = mu + 1 + D, lane = tid & 31, warp = tid >> 5;
+  const unsigned dk = dark[o];
+  const int lr = lane >> 2, lc = lane & 3;  // fragment row / column of this lane
+  const int nblk = nops * (FND / 32);        // 32-row blocks of the stacked operator
+  for (int blk = warp; blk < nblk; blk += M2L_WARPS) {
+    const int op = blk >> 3, r0 = (blk & 7) * 32;  // rows r0..r0+31 of operator op
+    if (op <= mu && ((dk >> op) & 1u)) continue;   // dark lag: the reference skips it too
+    const double* Tb;
+    int ld, toff;
+    if (op <= mu) { Tb = T0; ld = ntau0; toff = (op + 1) * (FPT - 1); }
+    else { Tb = Tp + (size_t)(op - mu - 1) * FKR * ntaup; ld = ntaup; toff = FPT - 1; }
+    // row part of the A address per m8 tile: (S(a) + 171) * ld + m + toff
+    int rowp[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const int row = r0 + 8 * t + lr;
+      rowp[t] = (m2l_S(row >> 2) + 171) * ld + (row & 3) + toff;
+    }
+    double acc[4][4][2];
+#pragma unroll
+    for (int t = 0; t < 4; ++t)
+#pragma unroll
+      for (int u = 0; u < 4; ++u) acc[t][u][0] = acc[t][u][1] = 0.0;
+    const double* Bl = Bs + lr * M2L_BLD + lc;  // B[k = lc][col = lr] of n8 tile 0
+#pragma unroll 4
+    for (int b = 0; b < FN3; ++b) {               // k-step: spatial source node b, n = 0..3
+      const int colp = m2l_S(b) * ld + lc;
+      double af[4], bf[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) af[t] = Tb[rowp[t] - colp];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) bf[u] = Bl[u * 8 * M2L_BLD + b * FPT];
+#pragma unroll
+      for (int t = 0; t < 4; ++t)
+#pragma unroll
+        for (int u = 0; u < 4; ++u) dmma884(acc[t][u][0], acc[t][u][1], af[t], bf[u]);
+    }
+    // epilogue: C[row lr][col 2 lc + i] of tile (t, u) -> Y[pair][op * 256 + row]
+    const long long M = (long long)nops * FND;
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const int col = u * 8 + 2 * lc + i;
+        if (col >= np) continue;
+        double* yc = Y + (long long)(p0 + col) * M + (long long)op * FND + r0 + lr;
+#pragma unroll
+        for (int t = 0; t < 4; ++t) yc[8 * t] = acc[t][u][i];
+      }
+  }
+}
 
 // distant-future recurrence, elementwise (fmm.py:355-367)
 template <int D>
@@ -590,10 +715,29 @@ extern "C" int tdw_fmm_setup(tdw_problem* pb, const tdw_fmm_desc* fd) {
         if ((rc = up(ctx, &V.t_cells, tcells.data(), std::max<size_t>(1, tcells.size())))) return rc;
       }
       for (int o = 0; o < V.noff; ++o) V.max_grp = std::max(V.max_grp, grp[o + 1] - grp[o]);
+      {
+        std::vector<int4> items;
+        std::vector<unsigned> gd(std::max<long long>(1, nkeep), 0u);
+        for (int o = 0; o < V.noff; ++o) {
+          for (long long q = grp[o]; q < grp[o + 1]; ++q) gd[q] = dark[o];
+          for (long long q = grp[o]; q < grp[o + 1]; q += M2L_NC)
+            items.push_back(make_int4(o, (int)q, (int)std::min<long long>(M2L_NC, grp[o + 1] - q), 0));
+        }
+        V.n_items = (int)items.size();
+        if ((rc = up(ctx, &V.items, items.data(), std::max<size_t>(1, items.size())))) return rc;
+        if ((rc = up(ctx, &V.g_dark, gd.data(), gd.size()))) return rc;
+      }
       if ((rc = up(ctx, &V.g_obs, gobs.data(), gobs.size()))) return rc;
       if ((rc = up(ctx, &V.g_src, gsrc.data(), gsrc.size()))) return rc;
       const int nops = F->mu + 1 + d;
       F->nops = nops;
+      {
+        const int smem = (int)m2l_smem_bytes(d, F->ntau0, F->ntaup);
+        cudaError_t ea = d == 1 ? cudaFuncSetAttribute(m2l_dmma_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)
+                       : d == 2 ? cudaFuncSetAttribute(m2l_dmma_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)
+                                : cudaFuncSetAttribute(m2l_dmma_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        TDW_CUDA(ctx, ea);
+      }
       const size_t kop = (size_t)V.noff * FND * nops * FND;
       TDW_CUDA(ctx, cudaMalloc(&V.Kop, sizeof(double) * std::max<size_t>(1, kop)));
       if (V.noff)
@@ -743,12 +887,32 @@ int snapshot(tdw_ctx* ctx, FmmLevel& V, cudaStream_t st) {
   return TDW_OK;
 }
 
+void m2l_launch(int d, const FmmLevel& V, const FmmState* F, size_t smem, cudaStream_t st) {
+  auto go = [&](auto kern) {
+    kern<<<V.n_items, M2L_WARPS * 32, smem, st>>>(V.items, V.K0, V.Kp, V.g_src, V.dark, V.mom, V.noff,
+                                                  F->ntau0, F->ntaup, F->mu, F->Y);
+  };
+  if (d == 1) go(m2l_dmma_kernel<1>);
+  if (d == 2) go(m2l_dmma_kernel<2>);
+  if (d == 3) go(m2l_dmma_kernel<3>);
+}
+
 int launch_m2l(tdw_problem* pb, FmmLevel& V, int k, cudaStream_t st) {
   FmmState* F = pb->fmm;
   tdw_ctx* ctx = pb->ctx;
   const int d = pb->d, nops = F->nops, M = nops * FND;
   TDW_CUDA(ctx, cudaMemsetAsync(V.tmp, 0, sizeof(double) * d * (size_t)V.ncell * FND, st));
-  if (V.nil > 0) {
+  static const bool use_blas = getenv("TDW_M2L") && strcmp(getenv("TDW_M2L"), "cublas") == 0;
+  if (V.nil > 0 && !use_blas) {
+    // own DMMA contraction straight from the Toeplitz tensors and the moments
+    const size_t smem = m2l_smem_bytes(d, F->ntau0, F->ntaup);
+    m2l_launch(d, V, F, smem, st);
+    TDW_CUDA(ctx, cudaGetLastError());
+    if (V.n_tcell > 0)
+      scatter_all_kernel<<<dim3(V.n_tcell, nops), FND, 0, st>>>(V.t_cells, V.t_ptr, V.t_pair, V.g_dark, F->Y,
+                                                                 nops, F->mu, k, V.ncell, V.own, V.tmp);
+    TDW_CUDA(ctx, cudaGetLastError());
+  } else if (V.nil > 0) {
     gather_kernel<<<(int)std::min<long long>(4096, (V.nil * FND + 255) / 256), 256, 0, st>>>(
         V.g_src, V.nil, V.mom, V.X);
     TDW_CUDA(ctx, cudaGetLastError());
@@ -773,8 +937,8 @@ int launch_m2l(tdw_problem* pb, FmmLevel& V, int k, cudaStream_t st) {
       if (bs != CUBLAS_STATUS_SUCCESS) return tdw_fail(ctx, TDW_ERR_CUDA, "cublasDgemm failed");
     }
     if (V.n_tcell > 0)
-      scatter_all_kernel<<<dim3(V.n_tcell, nops), FND, 0, st>>>(V.t_cells, V.t_ptr, V.t_pair, F->Y, nops, F->mu,
-                                                                 k, V.ncell, V.own, V.tmp);
+      scatter_all_kernel<<<dim3(V.n_tcell, nops), FND, 0, st>>>(V.t_cells, V.t_ptr, V.t_pair, nullptr, F->Y,
+                                                                 nops, F->mu, k, V.ncell, V.own, V.tmp);
     TDW_CUDA(ctx, cudaGetLastError());
   }
   const size_t cs = (size_t)V.ncell * FND;
@@ -1017,7 +1181,7 @@ long long tdw_fmm_m2l_pairs(const tdw_problem* pb) { return pb->fmm ? pb->fmm->m
 void tdw_fmm_free(FmmState* F) {
   if (!F) return;
   for (auto& V : F->lev) {
-    void* p[] = {V.parent, V.octant, V.child_ptr, V.child_idx, V.obs_ptr, V.il_src, V.il_off, V.dark,
+    void* p[] = {V.items, V.g_dark, V.parent, V.octant, V.child_ptr, V.child_idx, V.obs_ptr, V.il_src, V.il_off, V.dark,
                  V.K0, V.Kp, V.own, V.inherit, V.deriv, V.aux, V.acc, V.mom, V.g_obs, V.g_src,
                  V.Kop, V.X, V.tmp, V.t_ptr, V.t_pair, V.t_cells, (void*)V.gA, (void*)V.gB, (void*)V.gC};
     for (void* q : p)

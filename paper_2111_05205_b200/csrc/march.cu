@@ -1727,18 +1727,25 @@ int enqueue_loop(tdw_problem* pb, LoopPlan& L, cudaEvent_t* ev_conv) {
     if (ev_conv) TDW_CUDA(ctx, cudaEventRecordWithFlags(ev_conv[2 * pass], sc, cudaEventRecordExternal));
     if ((rc = launch_conv(pb, L, alpha, nb, sc))) return rc;
     if (ev_conv) TDW_CUDA(ctx, cudaEventRecordWithFlags(ev_conv[2 * pass + 1], sc, cudaEventRecordExternal));
+    if (L.multi) {
+      // the pass's nb slots of b are complete together: one grouped in-place
+      // all-gather of the ranks' row blocks, on the convolution's stream (off the
+      // solve chain; the solves of the pass wait for it through evF)
+      ncclResult_t nr = ncclGroupStart();
+      for (int s = alpha; s < alpha + nb && nr == ncclSuccess; ++s) {
+        double* bb = pb->d_b + (size_t)(s % pb->bring) * pb->bstride;
+        nr = ncclAllGather(bb + pb->b_off, bb, (size_t)pb->rows_per_rank, ncclDouble, ctx->comm, sc);
+      }
+      const ncclResult_t ne = ncclGroupEnd();
+      if (nr == ncclSuccess) nr = ne;
+      if (nr != ncclSuccess)
+        return tdw_fail(ctx, TDW_ERR_NCCL, std::string("ncclAllGather: ") + ncclGetErrorString(nr));
+    }
     TDW_CUDA(ctx, cudaEventRecord(evF[alpha], sc));
     last_alpha = alpha;
     // solves of the pass's steps on the main stream
     TDW_CUDA(ctx, cudaStreamWaitEvent(st, evF[alpha], 0));
     for (int s = alpha; s < alpha + nb; ++s) {
-      if (L.multi) {
-        double* bb = pb->d_b + (size_t)(s % pb->bring) * pb->bstride;
-        ncclResult_t nr = ncclAllGather(bb + pb->b_off, bb, (size_t)pb->rows_per_rank, ncclDouble,
-                                        ctx->comm, st);
-        if (nr != ncclSuccess)
-          return tdw_fail(ctx, TDW_ERR_NCCL, std::string("ncclAllGather: ") + ncclGetErrorString(nr));
-      }
       // solve(s) reads the lag-3+ near terms near_step(s-2) wrote (lag 2: near_step(s-1), below)
       const bool side_near = near && (pb->near_split || pb->near_in_solve);
       // near_step(s') writes lags >= g0 + 2 of x^(s'-1), first needed by solve(s' + g0 + 1)

@@ -314,13 +314,17 @@ def patched_fmm():
     return mods["fmm"]
 
 
+FMM_REF_SUB = np.sort(np.random.default_rng(5).choice(1280, size=256, replace=False))
+
+
 def make_fmm_ref():
     """fast_march of the runtime-corrected reference on the 1280-element sphere
     (OBIE d=1 and BMBIE d=2, Neumann, ps = pt = 4, Nt = 128, leaf capacity 100
     and 20): per-step rhs and unknown density, the pin of oracle/fmm_oracle.py."""
     fmm = patched_fmm()
     base = build_spec(1)
-    out = dict(versions=VERSIONS, patches=np.array([f"{f}: {o!r} -> {n!r}" for f, o, n in FMM_PATCHES]))
+    out = dict(versions=VERSIONS, patches=np.array([f"{f}: {o!r} -> {n!r}" for f, o, n in FMM_PATCHES]),
+               sub=FMM_REF_SUB)
     import warnings
     for bie, d in (("obie", 1), ("bmbie", 2)):
         for Z in (100, 20):
@@ -332,8 +336,11 @@ def make_fmm_ref():
             t0 = time.perf_counter()
             hist = fmm.fast_march(spec, fmm.FmmConfig(ps=4, pt=4, leaf_capacity=Z, mu=8), rhs_trace=trace)
             key = f"{bie}{d}_Z{Z}"
-            out[f"{key}_u"] = hist.u
-            out[f"{key}_rhs"] = np.array(trace)
+            rhs = np.array(trace)
+            out[f"{key}_u_sub"] = hist.u[:, FMM_REF_SUB]
+            out[f"{key}_rhs_sub"] = rhs[:, FMM_REF_SUB]
+            out[f"{key}_u_norm"] = np.linalg.norm(hist.u, axis=1)
+            out[f"{key}_rhs_norm"] = np.linalg.norm(rhs, axis=1)
             out[f"{key}_status"] = hist.status
             out[f"{key}_n_steps"] = hist.n_steps
             print(f"{key}: {hist.status} {hist.n_steps} steps, {time.perf_counter() - t0:.1f} s")
