@@ -165,8 +165,11 @@ int tdw_problem_create_impl(tdw_ctx* ctx, const tdw_problem_desc* dsc, tdw_probl
     // (~ ns).  Measured: config 0 (320 el.) best at 4, config 1 even, config 2
     // (5120) 15.5k steps/s at 5 (14.7k at 6, 13.5k at 4), config 3 (20480) 911 at 6
     // (811 at 5, 737 at 4)
+    // (a function of the whole problem, not of the rank count: kb and the split
+    // lags decide how each b_i is grouped into sums, so any rank count gives the
+    // single-GPU densities bit for bit)
     const char* e = getenv("TDW_KB");
-    const double pass_size = (double)dsc->ns * (double)dsc->ns / std::max(1, nranks);
+    const double pass_size = (double)dsc->ns * (double)dsc->ns;
     const int kb_default = pass_size >= 1e8 ? 6 : (pass_size >= 1e7 ? 5 : 4);
     pb->kb = std::max(1, std::min(TDW_KB_MAX, e ? atoi(e) : kb_default));
     // a pass waits for the solve overlap+1 steps back and runs beside the last

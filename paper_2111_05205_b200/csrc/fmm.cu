@@ -333,8 +333,11 @@ __device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double
                : "d"(a), "d"(b));
 }
 
+// shared-memory tables, each padded to an even number of doubles (16-byte aligned)
+__host__ __device__ constexpr int m2l_even(int n) { return (n + 1) & ~1; }
 __host__ __device__ constexpr size_t m2l_smem_bytes(int d, int ntau0, int ntaup) {
-  return sizeof(double) * ((size_t)FKR * ntau0 + (size_t)d * FKR * ntaup + (size_t)M2L_NC * M2L_BLD);
+  return sizeof(double) * ((size_t)m2l_even(FKR * ntau0) + (size_t)d * m2l_even(FKR * ntaup) +
+                           (size_t)M2L_NC * M2L_BLD);
 }
 
 // S(x) = 49 x1 + 7 x2 + x3 of spatial node x = (x1 << 4) | (x2 << 2) | x3: the
@@ -349,16 +352,17 @@ m2l_dmma_kernel(const int4* __restrict__ items, const double* __restrict__ K0, c
   extern __shared__ __align__(16) double m2l_sm[];
   const int4 it = items[blockIdx.x];  // (offset, first grouped pair, pairs)
   const int o = it.x, p0 = it.y, np = it.z;
+  const int tp_stride = m2l_even(FKR * ntaup);
   double* T0 = m2l_sm;                                   // [343][ntau0]
-  double* Tp = T0 + (size_t)FKR * ntau0;                 // [D][343][ntaup]
-  double* Bs = Tp + (size_t)D * FKR * ntaup;             // [M2L_NC][M2L_BLD]
+  double* Tp = T0 + m2l_even(FKR * ntau0);               // [D][343][ntaup] (stride tp_stride)
+  double* Bs = Tp + (size_t)D * tp_stride;               // [M2L_NC][M2L_BLD], 16-byte aligned
   const int tid = threadIdx.x, nthr = M2L_WARPS * 32;
   {
     const double* src0 = K0 + (size_t)o * FKR * ntau0;
     for (int e = tid; e < FKR * ntau0; e += nthr) T0[e] = __ldg(src0 + e);
     for (int p = 0; p < D; ++p) {
       const double* srcp = Kp + ((size_t)p * noff + o) * FKR * ntaup;
-      for (int e = tid; e < FKR * ntaup; e += nthr) Tp[p * FKR * ntaup + e] = __ldg(srcp + e);
+      for (int e = tid; e < FKR * ntaup; e += nthr) Tp[p * tp_stride + e] = __ldg(srcp + e);
     }
     // gathered source moments, two doubles per thread and step (zero columns past np)
     for (int e = tid; e < M2L_NC * (FND / 2); e += nthr) {
@@ -379,7 +383,7 @@ m2l_dmma_kernel(const int4* __restrict__ items, const double* __restrict__ K0, c
     const double* Tb;
     int ld, toff;
     if (op <= mu) { Tb = T0; ld = ntau0; toff = (op + 1) * (FPT - 1); }
-    else { Tb = Tp + (size_t)(op - mu - 1) * FKR * ntaup; ld = ntaup; toff = FPT - 1; }
+    else { Tb = Tp + (size_t)(op - mu - 1) * tp_stride; ld = ntaup; toff = FPT - 1; }
     // row part of the A address per m8 tile: (S(a) + 171) * ld + m + toff
     int rowp[4];
 #pragma unroll
