@@ -258,11 +258,19 @@ def run_fmm(args, world, rank, local, ctx, spec, barrier, max_over_ranks):
     e2e = e2e_steps * (nt - 1) / max_over_ranks(_time.perf_counter() - t0)
     fp64 = C.c_double(0.0)
     _lib.check(_lib.load().tdw_fp64_peak(ctx.h, C.byref(fp64)), ctx.h, "tdw_fp64_peak")
-    # this rank's share of the M2L pairs (target-cell sharding) scales the FLOPs
-    flops = m2l_flops(plan, nt, spec.basis.d) * info["fmm_m2l_pairs"] / max(
-        1, sum(len(l.il_obs) for l in plan.levels.values()))
-    # per-GPU rate (the busiest rank) against the per-GPU peak
-    achieved = max_over_ranks(flops) / (dev_ms / args.steps * 1e-3) / 1e12
+    # roofline of the dominant kernel: the leaf level's M2L contraction (own DMMA
+    # kernel), FLOPs per launch (non-dark operators) / its average launch time
+    mf, m2l_ms = C.c_double(0.0), C.c_float(0.0)
+    _lib.check(_lib.load().tdw_fmm_time_m2l(store.h, 10, C.byref(mf), C.byref(m2l_ms)), ctx.h,
+               "tdw_fmm_time_m2l")
+    achieved = max_over_ranks(mf.value / max(m2l_ms.value * 1e-3, 1e-12) / 1e12 if m2l_ms.value else 0.0)
+    # whole-loop M2L rate: this rank's share of the M2L FLOPs of the loop / loop time
+    loop_rate = m2l_flops(plan, nt, spec.basis.d) * info["fmm_m2l_pairs"] / max(
+        1, sum(len(l.il_obs) for l in plan.levels.values())) / (dev_ms / args.steps * 1e-3) / 1e12
+    try:
+        ncu_m2l = json.loads((ROOT / "profiles" / "m2l_ncu.json").read_text())
+    except Exception:
+        ncu_m2l = None
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "steps/s", "n_gpus": world,
@@ -279,8 +287,12 @@ def run_fmm(args, world, rank, local, ctx, spec, barrier, max_over_ranks):
                     "d2h_bytes_per_step": 4 * (nt - 1) * ns * 8, "api": "marching.march(spec, mats=FmmStore)"},
             "roofline": {"bound": "fp64", "achieved": achieved, "peak": fp64.value, "unit": "TFLOP/s",
                          "frac": achieved / fp64.value, "traffic": None,
-                         "kernel": "M2L DGEMMs (cuBLAS, FP64 tensor path): FLOPs of the whole loop / loop time",
-                         "peak_source": "measured live (tdw_fp64_peak: DFMA chains)"},
+                         "kernel": "m2l_dmma_kernel (own, FP64 tensor cores: mma.sync m8n8k4 f64), "
+                                   "leaf level, one launch = one level tick",
+                         "flops_per_launch": mf.value, "avg_launch_ms": m2l_ms.value,
+                         "peak_source": "measured live (tdw_fp64_peak: DFMA chains)",
+                         "ncu": ncu_m2l,
+                         "whole_loop_m2l_tflops": loop_rate},
             "cpu_baseline": None, "clocks": clk.summary(), "gpu_launches": None,
         }
         print(json.dumps(line), flush=True)

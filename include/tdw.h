@@ -20,7 +20,7 @@
  *   tdw_march_resident  <- same time loop, inputs/outputs resident on the device (benchmark form)
  *   tdw_nccl_unique_id / tdw_comm_init  <- (none in the reference; row-sharded multi-GPU)
  *   tdw_known_plane_pulse <- (none: device-side boundary data)
- *   tdw_fp64_peak, tdw_host_alloc / tdw_host_free, tdw_time_conv, tdw_set_graph,
+ *   tdw_fp64_peak, tdw_host_alloc / tdw_host_free, tdw_time_conv, tdw_fmm_time_m2l, tdw_set_graph,
  *   tdw_problem_create_shard / tdw_march_emulated  <- (none: diagnostics, pinned
  *                          memory, one-GPU emulation of the sharded paths)
  *
@@ -174,6 +174,11 @@ int tdw_download(tdw_problem* pb, double* u, double* q, double* tau, double* sig
 /* Average device time of one history-convolution launch (kernel K2) over n
  * back-to-back launches at a fixed step; inputs resident.  For the roofline. */
 int tdw_time_conv(tdw_problem* pb, int n, float* ms);
+
+/* FMM: average device time of the leaf level's M2L contraction (the fast
+ * solver's dominant kernel) over n launches, and its FLOPs per launch (2 x 256 x
+ * 256 per interaction pair and non-dark operator).  For the roofline. */
+int tdw_fmm_time_m2l(tdw_problem* pb, int n, double* flops, float* ms);
 
 /* 0 = launch the time loop kernel by kernel, 1 = capture it in a CUDA graph (default). */
 int tdw_set_graph(tdw_problem* pb, int enable);

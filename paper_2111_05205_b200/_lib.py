@@ -80,6 +80,7 @@ EXPORTS = {
     "tdw_march_resident": ([C.c_void_p, C.c_double, C.c_int, C.c_int, C.POINTER(Timing)], C.c_int),
     "tdw_download": ([C.c_void_p, _dp, _dp, _dp, _dp, _i32p, _i32p], C.c_int),
     "tdw_time_conv": ([C.c_void_p, C.c_int, C.POINTER(C.c_float)], C.c_int),
+    "tdw_fmm_time_m2l": ([C.c_void_p, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_float)], C.c_int),
     "tdw_set_graph": ([C.c_void_p, C.c_int], C.c_int),
     "tdw_problem_destroy": ([C.c_void_p], C.c_int),
     "tdw_fmm_setup": ([C.c_void_p, C.c_void_p], C.c_int),

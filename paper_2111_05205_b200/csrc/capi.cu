@@ -571,6 +571,12 @@ int tdw_march_resident(tdw_problem* pb, double threshold, int n_repeat, int time
   return TDW_OK;
 }
 
+int tdw_fmm_time_m2l(tdw_problem* pb, int n, double* flops, float* ms) {
+  if (!pb) return TDW_ERR_INVALID_ARG;
+  cudaSetDevice(pb->ctx->device);
+  return tdw_fmm_time_m2l_impl(pb, n, flops, ms);
+}
+
 int tdw_time_conv(tdw_problem* pb, int n, float* ms) {
   if (!pb || n < 1 || !ms) return TDW_ERR_INVALID_ARG;
   if (!pb->assembled) return tdw_fail(pb->ctx, TDW_ERR_STATE, "tdw_time_conv before tdw_assemble");

@@ -67,6 +67,7 @@ struct FmmLevel {
   // the dark-lag bits of each grouped pair's offset (the scatter skips those rows)
   int4* items = nullptr;
   int n_items = 0;
+  double m2l_flops = 0.0;      // FLOPs of one M2L launch (non-dark operators only)
   unsigned* g_dark = nullptr;  // [nil]
   // the level's GEMMs as one grouped call (one group per nonempty offset)
   std::vector<int> gm, gn, gk, glda, gldb, gldc, gsize;
@@ -728,6 +729,9 @@ extern "C" int tdw_fmm_setup(tdw_problem* pb, const tdw_fmm_desc* fd) {
             items.push_back(make_int4(o, (int)q, (int)std::min<long long>(M2L_NC, grp[o + 1] - q), 0));
         }
         V.n_items = (int)items.size();
+        for (int o = 0; o < V.noff; ++o)
+          V.m2l_flops += 2.0 * FND * FND * (double)(grp[o + 1] - grp[o]) *
+                         (double)(F->mu + 1 + d - __builtin_popcount(dark[o]));
         if ((rc = up(ctx, &V.items, items.data(), std::max<size_t>(1, items.size())))) return rc;
         if ((rc = up(ctx, &V.g_dark, gd.data(), gd.size()))) return rc;
       }
@@ -1181,6 +1185,35 @@ int tdw_fmm_march_emulated(tdw_problem** pbs, int n, double threshold) {
 }
 
 long long tdw_fmm_m2l_pairs(const tdw_problem* pb) { return pb->fmm ? pb->fmm->m2l_pairs : 0; }
+
+// Average device time of the leaf level's M2L contraction (m2l_dmma_kernel, the
+// FMM's dominant kernel) over n back-to-back launches on the current moments,
+// and its FLOPs per launch (2 x 256 x 256 per pair and non-dark operator).
+int tdw_fmm_time_m2l_impl(tdw_problem* pb, int n, double* flops, float* ms) {
+  FmmState* F = pb->fmm;
+  tdw_ctx* ctx = pb->ctx;
+  if (!F) return tdw_fail(ctx, TDW_ERR_STATE, "tdw_fmm_time_m2l: not an FMM problem");
+  FmmLevel& V = F->lev[F->leaf];
+  if (flops) *flops = V.m2l_flops;
+  if (ms) *ms = 0.0f;
+  if (V.n_items == 0 || n < 1) return TDW_OK;
+  const size_t smem = m2l_smem_bytes(pb->d, F->ntau0, F->ntaup);
+  cudaStream_t st = ctx->stream;
+  m2l_launch(pb->d, V, F, smem, st);  // warm-up
+  cudaEvent_t e0, e1;
+  TDW_CUDA(ctx, cudaEventCreate(&e0));
+  TDW_CUDA(ctx, cudaEventCreate(&e1));
+  TDW_CUDA(ctx, cudaEventRecord(e0, st));
+  for (int k = 0; k < n; ++k) m2l_launch(pb->d, V, F, smem, st);
+  TDW_CUDA(ctx, cudaEventRecord(e1, st));
+  TDW_CUDA(ctx, cudaEventSynchronize(e1));
+  float t = 0.0f;
+  TDW_CUDA(ctx, cudaEventElapsedTime(&t, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  if (ms) *ms = t / n;
+  return TDW_OK;
+}
 
 void tdw_fmm_free(FmmState* F) {
   if (!F) return;

@@ -213,6 +213,7 @@ int tdw_setup_cluster_solver(tdw_problem* pb);
 int tdw_fmm_loop(tdw_problem* pb, double threshold, bool want_rhs, tdw_timing* timing);
 int tdw_fmm_march_emulated(tdw_problem** pbs, int n, double threshold);
 long long tdw_fmm_m2l_pairs(const tdw_problem* pb);
+int tdw_fmm_time_m2l_impl(tdw_problem* pb, int n, double* flops, float* ms);
 void tdw_fmm_free(struct FmmState* F);
 int tdw_march_emulated_impl(tdw_problem** pbs, int n, double threshold);
 int tdw_problem_create_impl(tdw_ctx* ctx, const tdw_problem_desc* dsc, tdw_problem** out, bool shard_only);
