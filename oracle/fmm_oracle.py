@@ -109,7 +109,8 @@ class FmmOracle:
                 for p in range(1, self.d + 1):
                     Kp = ops.Kp[p - 1][o].reshape(2 * ps - 1, 2 * ps - 1, 2 * ps - 1, -1)
                     row.append(dense_operator(Kp, ps, pt, pt - 1))
-                mats.append(np.stack(row))
+                # (nd, nops * nd): Y = Ms @ stack gives every operator's result side by side
+                mats.append(np.ascontiguousarray(np.concatenate(row, axis=0).T))
             self.ops[L] = mats
             obs = np.repeat(np.arange(ops.n_cells), np.diff(ops.obs_ptr))
             src, off = np.asarray(ops.il_src), np.asarray(ops.il_off)
@@ -154,14 +155,13 @@ class FmmOracle:
         for oi, (obs, src) in enumerate(self.groups[L]):
             if len(obs) == 0:
                 continue
-            Ms = moments[src]                                    # (n, nd)
-            Y = np.einsum("onm,pm->opn", self.ops[L][oi], Ms)     # (nops, n, nd)
+            Y = moments[src] @ self.ops[L][oi]                   # (n, nops * nd), BLAS
             for l in range(1, mu + 2):
                 if ops.dark[oi, l - 1]:
                     continue
-                st["own"][(k + l) % ring][obs] += Y[l - 1]
+                st["own"][(k + l) % ring][obs] += Y[:, (l - 1) * nd:l * nd]
             for p in range(1, d + 1):
-                tmp[p - 1][obs] += Y[mu + p]
+                tmp[p - 1][obs] += Y[:, (mu + p) * nd:(mu + p + 1) * nd]
         from paper_2111_05205_b200.fmm_plan import cmp_coeff
         for p in range(1, d + 1):
             upd = tmp[p - 1].copy()
