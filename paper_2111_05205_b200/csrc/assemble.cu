@@ -802,7 +802,7 @@ int tdw_assemble_impl(tdw_problem* pb) {
     const char* sm = getenv("TDW_SCHED");
     if (!(sm && strcmp(sm, "rr") == 0)) {
       // Fixed summation groups: the J-tiles of an I-block are cut into groups of
-      // TDW_GROUP_TILES (default 4) consecutive tiles.  A group is always summed by
+      // gt consecutive tiles.  A group is always summed by
       // ONE CTA (units in tile order, then the warp's lane reduction) into its own
       // partial, and the partials of a row are added in group order
       // (reduce_parts / sum_parts).  The grouping depends on the problem only, not
@@ -813,7 +813,13 @@ int tdw_assemble_impl(tdw_problem* pb) {
       // independent of the header width, so both widths give the same schedule
       const double per_unit = 4096.0;
       auto weight = [&](long long u) { return (double)(uoff[u + 1] - uoff[u] - ucoef[u]) + per_unit; };
-      int gt = 4;
+      // groups per I-block: 4, more when the whole problem has few I-blocks (at
+      // least 2 groups per SM); from the WHOLE problem's I-block count, so every
+      // rank count cuts the same groups.  A bandwidth-bound pass tolerates the
+      // coarse balance (config 2: 2% slower than cuts at unit granularity)
+      const int nblk_total = (pb->ns + TDW_TI - 1) / TDW_TI;
+      const int gpi = std::min(pb->ntiles, std::max(4, (2 * ctx->num_sms + nblk_total - 1) / nblk_total));
+      int gt = (pb->ntiles + gpi - 1) / gpi;
       if (const char* e = getenv("TDW_GROUP_TILES")) gt = std::max(1, atoi(e));
       const int SG = (pb->ntiles + gt - 1) / gt;
       const long long ngroup = (long long)pb->n_iblk * SG;

@@ -456,20 +456,36 @@ __device__ __forceinline__ void conv_body(const ConvArgs& a, const CUtensorMap& 
       if (lane == 0) mbar_arrive(&empty[stage]);
       ++n;
     }
-    if (next_item != item) {  // end of a work item (I-block, split): flush the row partials
+    if (next_item != item) {  // end of a work item (I-block, tile group): flush the row partials
       const int iblk = (int)(item / (unsigned)S), sp = (int)(item % (unsigned)S);
+      // the warp's RPW * KB row sums at once: a butterfly reduce-scatter over the
+      // lanes (value j ends in lane j; 16 + 8 + 4 + 2 + 1 shuffles for up to 32
+      // values instead of 5 per value); the same pairwise tree for every value
+      constexpr int NV = RPW * KB;
+      constexpr int P = NV <= 8 ? 8 : (NV <= 16 ? 16 : 32);
+      double v[P];
 #pragma unroll
-      for (int r = 0; r < RPW; ++r) {
+      for (int j = 0; j < P; ++j) v[j] = j < NV ? acc[j / KB][j % KB] : 0.0;
 #pragma unroll
-        for (int i = 0; i < KB; ++i) {
-          double v = acc[r][i];
+      for (int h = P / 2; h >= 1; h >>= 1) {
+        const bool up = (lane & h) != 0;
 #pragma unroll
-          for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULLMASK, v, o);
-          if (lane == 0)  // row-major partials: a row's S partials are contiguous
-            a.bpart[i * step_stride + (size_t)(iblk * TDW_TI + warp * RPW + r) * S + sp] = v;
-          acc[r][i] = 0.0;
+        for (int j = 0; j < h; ++j) {
+          const double send = up ? v[j] : v[j + h];
+          const double keep = up ? v[j + h] : v[j];
+          v[j] = keep + __shfl_xor_sync(FULLMASK, send, h);
         }
       }
+      // P < 32: lanes l and l + P hold the same value sums of two lane halves
+#pragma unroll
+      for (int h = 16; h >= P; h >>= 1) v[0] += __shfl_xor_sync(FULLMASK, v[0], h);
+      const int j = lane & (P - 1);
+      if (lane < P && j < NV)  // row-major partials: a row's S partials are contiguous
+        a.bpart[(j % KB) * step_stride + (size_t)(iblk * TDW_TI + warp * RPW + j / KB) * S + sp] = v[0];
+#pragma unroll
+      for (int r = 0; r < RPW; ++r)
+#pragma unroll
+        for (int i = 0; i < KB; ++i) acc[r][i] = 0.0;
     }
     }
   }
@@ -575,6 +591,7 @@ struct ClusterSolveArgs {
   int nsl;                                  // split lags 2..nsl+1
   int guess;                                // 1: start Jacobi from 2 x^(beta-1) - x^(beta-2)
   int check_mask;                           // register solver: convergence test when (it & mask) == 0
+  double stop_tol;                          // sweeps stop at max|dx| <= stop_tol max|x| (1e-15)
   // halo solver (communication-avoiding sweeps): per CTA, the computed rows (own
   // rows first, then halo layers 1..h-1) and the gathered rows (layers 1..h)
   int halo;                                 // h (0: plain register solver)
@@ -760,7 +777,7 @@ __global__ void __launch_bounds__(1024, 1) solve_cluster_kernel(ClusterSolveArgs
           D = fmax(D, __shfl_xor_sync(FULLMASK, D, o));
           X = fmax(X, __shfl_xor_sync(FULLMASK, X, o));
         }
-        if (tid == 0) s_stop = D <= 1e-15 * X;
+        if (tid == 0) s_stop = D <= a.stop_tol * X;
       }
       __syncthreads();
       if (s_stop) break;
@@ -937,7 +954,7 @@ __global__ void __launch_bounds__(reg_threads<MAXNZ>(), 1) solve_reg_kernel(Clus
           X = max(X, __shfl_xor_sync(FULLMASK, X, o));
         }
         if (tid == 0)
-          s_stop = __longlong_as_double((long long)D) <= 1e-15 * __longlong_as_double((long long)X);
+          s_stop = __longlong_as_double((long long)D) <= a.stop_tol * __longlong_as_double((long long)X);
       }
       __syncthreads();
       ++ncheck;
@@ -1140,7 +1157,7 @@ __global__ void __launch_bounds__(reg_threads<MAXNZ>(), 1) solve_halo_kernel(Clu
           X = max(X, __shfl_xor_sync(FULLMASK, X, o));
         }
         if (tid == 0)
-          s_stop = __longlong_as_double((long long)D) <= 1e-15 * __longlong_as_double((long long)X);
+          s_stop = __longlong_as_double((long long)D) <= a.stop_tol * __longlong_as_double((long long)X);
       }
       __syncthreads();
       ++ncheck;
@@ -1646,6 +1663,8 @@ int launch_solve(tdw_problem* pb, LoopPlan& L, int alpha, cudaStream_t s) {
     L.cs.guess = g ? atoi(g) : 1;
     const char* c = getenv("TDW_CHECK_EVERY");
     L.cs.check_mask = (c ? atoi(c) : 4) <= 2 ? 1 : 3;
+    const char* tl = getenv("TDW_SOLVE_TOL");  // experiments: stop tolerance of the sweeps
+    L.cs.stop_tol = tl ? atof(tl) : 1e-15;
   }
   if (pb->sp_reg > 0 && pb->sp_halo > 0) {
     ccfg.dynamicSmemBytes = pb->sp_hsmem;
