@@ -9,6 +9,8 @@
  *   tdw_problem_create  <- marching.ProblemSpec (+mesh_stats,     marching.py:33-69,
  *                          compute_gamma_star)                    mesh.py:85-107
  *   tdw_assemble        <- marching.build_retarded_matrices       marching.py:132-181
+ *   tdw_restrict_pairs  <- its pairs= argument (near-field subsets) marching.py:132-133, 149
+ *   tdw_step_matrix, tdw_step_solve <- build_step_matrix (A, lu)    marching.py:279-289, 330
  *                          + build_step_matrix                    marching.py:279-289
  *   tdw_march           <- marching.march (+greville inputs,      marching.py:292-338
  *                          TimeHistory outputs)                   marching.py:184-276
@@ -128,6 +130,20 @@ int tdw_coeff_table_device(tdw_ctx* ctx, int64_t n, const double* P, const doubl
 
 int tdw_problem_create(tdw_ctx* ctx, const tdw_problem_desc* desc, tdw_problem** out);
 int tdw_assemble(tdw_problem* pb);
+
+/* build_retarded_matrices(spec, gamma_max, pairs=(ii, jj)) (marching.py:132-181):
+ * restrict the store (and the lag-1 step matrix built from it) to the listed
+ * (row, column) element pairs, caller's element order.  Call between
+ * tdw_problem_create and tdw_assemble; repeated pairs count once. */
+int tdw_restrict_pairs(tdw_problem* pb, int64_t n, const int64_t* ii, const int64_t* jj);
+
+/* build_step_matrix(spec, mats) (marching.py:279-289): the assembled lag-1 step
+ * matrix A = w0 (W1 phi - U1 (1 - phi)) as COO in the caller's element order
+ * (rows == NULL: only *nnz), and its solve lu.solve(b) (marching.py:330) on the
+ * device (BiCGSTAB with a diagonal preconditioner); stats (nullable) =
+ * (||A x - b||, ||b||, iterations). */
+int tdw_step_matrix(tdw_problem* pb, int64_t* nnz, int64_t* rows, int64_t* cols, double* vals);
+int tdw_step_solve(tdw_problem* pb, const double* b, double* x, double* stats);
 int tdw_problem_info(const tdw_problem* pb, tdw_info* out);
 
 /* FP64 FMA throughput of the ctx's GPU (TFLOP/s, FMA = 2 FLOP): the denominator

@@ -70,6 +70,9 @@ EXPORTS = {
                                 C.POINTER(C.c_float)], C.c_int),
     "tdw_problem_create": ([C.c_void_p, C.POINTER(ProblemDesc), C.POINTER(C.c_void_p)], C.c_int),
     "tdw_assemble": ([C.c_void_p], C.c_int),
+    "tdw_restrict_pairs": ([C.c_void_p, C.c_int64, _i64p, _i64p], C.c_int),
+    "tdw_step_matrix": ([C.c_void_p, _i64p, _i64p, _i64p, _dp], C.c_int),
+    "tdw_step_solve": ([C.c_void_p, _dp, _dp, _dp], C.c_int),
     "tdw_problem_info": ([C.c_void_p, C.POINTER(Info)], C.c_int),
     "tdw_march": ([C.c_void_p, _dp, _dp, C.c_double, _dp, _dp, _dp, _dp, _dp, _i32p, _i32p],
                   C.c_int),

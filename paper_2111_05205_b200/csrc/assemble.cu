@@ -139,8 +139,21 @@ __device__ __forceinline__ void bspline_weights(int d, double* w) {
   if (d == 3) { w[0] = 1.0 / 6.0; w[1] = -(2.0 / 3.0); w[2] = 1.0; w[3] = -(2.0 / 3.0); w[4] = 1.0 / 6.0; }
 }
 
-// FMM near field: only pairs whose leaf cells are adjacent (fmm_tree.py:163-177)
-__device__ __forceinline__ bool pair_allowed(const int* leafc, int i, int j) {
+// Pair restrictions of the store:
+//  * FMM near field: only pairs whose leaf cells are adjacent (fmm_tree.py:163-177);
+//  * build_retarded_matrices(pairs=(ii, jj)) (marching.py:132-181): only the listed
+//    pairs -- per row a sorted column list (internal order), binary search.
+__device__ __forceinline__ bool pair_allowed(const int* leafc, const int* pptr, const int* pcol, int i, int j) {
+  if (pptr) {
+    int lo = pptr[i], hi = pptr[i + 1];
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      const int c = pcol[mid];
+      if (c == j) return true;
+      if (c < j) lo = mid + 1; else hi = mid;
+    }
+    return false;
+  }
   if (!leafc) return true;
   const int a = leafc[i], b = leafc[j];
   const int dx = (a & 1023) - (b & 1023), dy = ((a >> 10) & 1023) - ((b >> 10) & 1023),
@@ -151,6 +164,8 @@ __device__ __forceinline__ bool pair_allowed(const int* leafc, int i, int j) {
 struct AsmArgs {
   const double* elem;
   const int* leafc;                    // packed leaf-cell coords (FMM near field) or null
+  const int* pptr;                     // pairs= restriction: [ns+1] row pointers or null
+  const int* pcol;                     // sorted columns per row
   int split_lag2;                      // 1: lag 2..nsl+1 entries keep the known density only
   int nsl;                             // split lags
   int ns, row_lo, rows_loc, ntiles, d, cap;
@@ -176,7 +191,7 @@ __global__ void __launch_bounds__(256) count_kernel(AsmArgs a) {
   const double cdt = a.c * a.dt;
   int len = 0, glo = 0;
   bool any = false;
-  if (i < a.ns && j < a.ns && pair_allowed(a.leafc, i, j)) {
+  if (i < a.ns && j < a.ns && pair_allowed(a.leafc, a.pptr, a.pcol, i, j)) {
     Elem ej;
     load_elem(a.elem, j, ej);
     const double* ci = a.elem + (size_t)i * TDW_ELEM_STRIDE + 12;
@@ -371,6 +386,8 @@ __global__ void unit_layout_kernel(const unsigned long long* segcount, const uin
 struct NearArgs {
   const double* elem;
   const int* leafc;
+  const int* pptr;
+  const int* pcol;
   int split_lag2, nsl;
   const double* phi;
   int ns, ntiles, d, cap;
@@ -420,7 +437,7 @@ __global__ void __launch_bounds__(128) near_kernel(NearArgs a) {
       load_elem(a.elem, j, ej);
       double dx = ci[0] - ej.c[0], dy = ci[1] - ej.c[1], dz = ci[2] - ej.c[2];
       double dcc = sqrt(dx * dx + dy * dy + dz * dz);
-      if (dcc - ej.rad <= (gtop + 1) * cdt * (1.0 + 1e-9) && pair_allowed(a.leafc, i, j)) {
+      if (dcc - ej.rad <= (gtop + 1) * cdt * (1.0 + 1e-9) && pair_allowed(a.leafc, a.pptr, a.pcol, i, j)) {
         b = pair_band(ci, ej, cdt, a.d, a.cap);
         cand = true;
       }
@@ -604,6 +621,8 @@ int tdw_assemble_impl(tdw_problem* pb) {
   NearArgs s{};
   s.elem = pb->d_elem;
   s.leafc = pb->d_leafc;
+  s.pptr = pb->d_pair_ptr;
+  s.pcol = pb->d_pair_col;
   s.split_lag2 = pb->split_lag2;
   s.nsl = pb->nsl;
   s.phi = pb->d_phi;
@@ -647,6 +666,8 @@ int tdw_assemble_impl(tdw_problem* pb) {
   AsmArgs a{};
   a.elem = pb->d_elem;
   a.leafc = pb->d_leafc;
+  a.pptr = pb->d_pair_ptr;
+  a.pcol = pb->d_pair_col;
   a.split_lag2 = pb->split_lag2;
   a.nsl = pb->nsl;
   a.ns = pb->ns;
@@ -764,13 +785,19 @@ int tdw_assemble_impl(tdw_problem* pb) {
   pb->ell_w = hellw;
   if (hflags[3] == 1)
     return tdw_fail(ctx, TDW_ERR_LIMIT, "near structure: more than the supported pairs near a row");
-  if (!(bound < 0.9))
-    return tdw_fail(ctx, TDW_ERR_SINGULAR,
-                    "step matrix is not diagonally dominant (Jacobi bound " +
-                        std::to_string(bound) + "); the on-device solver needs bound < 0.9");
+  // a zero diagonal: the reference's splu raises "step matrix is singular"
+  // (marching.py:284-288); the loop's solver divides by the diagonal
+  {
+    std::vector<double> dg(pb->ns);
+    TDW_CUDA(ctx, cudaMemcpy(dg.data(), pb->d_adiag, sizeof(double) * pb->ns, cudaMemcpyDeviceToHost));
+    for (int i = 0; i < pb->ns; ++i)
+      if (!(dg[i] != 0.0) || !std::isfinite(dg[i]))
+        return tdw_fail(ctx, TDW_ERR_SINGULAR, "step matrix is singular (zero diagonal)");
+  }
   // sweeps for a contraction of 1e-17 under the infinity-norm bound (cap; the
-  // solver stops earlier once the update is at round-off)
-  int it = bound > 0.0 ? (int)ceil(log(1e-17) / log(bound)) : 1;
+  // solver stops earlier once the update is at round-off); bound >= 0.9 selects
+  // the BiCGSTAB solver (tdw_setup_cluster_solver)
+  int it = (bound > 0.0 && bound < 0.9) ? (int)ceil(log(1e-17) / log(bound)) : 400;
   pb->jac_iters = std::max(2, std::min(it, 400));
   float ms = 0.f, fms = 0.f;
   cudaEventElapsedTime(&ms, e0, e1);

@@ -571,6 +571,52 @@ int tdw_march_resident(tdw_problem* pb, double threshold, int n_repeat, int time
   return TDW_OK;
 }
 
+int tdw_step_matrix(tdw_problem* pb, int64_t* nnz, int64_t* rows, int64_t* cols, double* vals) {
+  if (!pb || !nnz || (rows && (!cols || !vals))) return TDW_ERR_INVALID_ARG;
+  cudaSetDevice(pb->ctx->device);
+  return tdw_step_matrix_impl(pb, nnz, rows, cols, vals);
+}
+
+int tdw_step_solve(tdw_problem* pb, const double* b, double* x, double* stats) {
+  if (!pb || !b || !x) return TDW_ERR_INVALID_ARG;
+  cudaSetDevice(pb->ctx->device);
+  return tdw_step_solve_impl(pb, b, x, stats);
+}
+
+int tdw_restrict_pairs(tdw_problem* pb, int64_t n, const int64_t* ii, const int64_t* jj) {
+  if (!pb || n < 0 || (n > 0 && (!ii || !jj))) return TDW_ERR_INVALID_ARG;
+  tdw_ctx* ctx = pb->ctx;
+  if (pb->assembled) return tdw_fail(ctx, TDW_ERR_STATE, "tdw_restrict_pairs after tdw_assemble");
+  if (pb->fmm) return tdw_fail(ctx, TDW_ERR_STATE, "tdw_restrict_pairs on an FMM problem");
+  cudaSetDevice(ctx->device);
+  const int ns = pb->ns;
+  std::vector<int> inv(ns);
+  for (int k = 0; k < ns; ++k) inv[pb->perm[k]] = k;
+  std::vector<std::vector<int>> rows(ns);
+  for (int64_t p = 0; p < n; ++p) {
+    if (ii[p] < 0 || ii[p] >= ns || jj[p] < 0 || jj[p] >= ns)
+      return tdw_fail(ctx, TDW_ERR_INVALID_ARG, "pairs: element index out of range");
+    rows[inv[ii[p]]].push_back(inv[jj[p]]);
+  }
+  std::vector<int> ptr(ns + 1, 0), col;
+  col.reserve((size_t)n);
+  for (int i = 0; i < ns; ++i) {
+    std::sort(rows[i].begin(), rows[i].end());
+    rows[i].erase(std::unique(rows[i].begin(), rows[i].end()), rows[i].end());
+    col.insert(col.end(), rows[i].begin(), rows[i].end());
+    ptr[i + 1] = (int)col.size();
+  }
+  cudaFree(pb->d_pair_ptr);
+  cudaFree(pb->d_pair_col);
+  pb->d_pair_ptr = pb->d_pair_col = nullptr;
+  TDW_CUDA(ctx, cudaMalloc(&pb->d_pair_ptr, sizeof(int) * (ns + 1)));
+  TDW_CUDA(ctx, cudaMalloc(&pb->d_pair_col, sizeof(int) * std::max<size_t>(1, col.size())));
+  TDW_CUDA(ctx, cudaMemcpy(pb->d_pair_ptr, ptr.data(), sizeof(int) * (ns + 1), cudaMemcpyHostToDevice));
+  if (!col.empty())
+    TDW_CUDA(ctx, cudaMemcpy(pb->d_pair_col, col.data(), sizeof(int) * col.size(), cudaMemcpyHostToDevice));
+  return TDW_OK;
+}
+
 int tdw_fmm_time_m2l(tdw_problem* pb, int n, double* flops, float* ms) {
   if (!pb) return TDW_ERR_INVALID_ARG;
   cudaSetDevice(pb->ctx->device);
@@ -594,7 +640,7 @@ int tdw_problem_destroy(tdw_problem* pb) {
   if (!pb) return TDW_OK;
   cudaSetDevice(pb->ctx->device);
   void* ptrs[] = {pb->d_perm, pb->d_elem, pb->d_phi, pb->d_units, pb->d_unit_off, pb->d_sched, pb->d_sched_off,
-                  pb->d_sched_item, pb->d_leafc,
+                  pb->d_sched_item, pb->d_leafc, pb->d_pair_ptr, pb->d_pair_col, pb->d_kw,
                   pb->d_unit, pb->d_acol, pb->d_aval, pb->d_adiag, pb->d_hist, pb->d_uk,
                   pb->d_qk, pb->d_bpart, pb->d_b, pb->d_x, pb->d_red, pb->d_bar, pb->d_flags,
                   pb->d_rhs, pb->d_sp_rowptr, pb->d_sp_nnzoff, pb->d_sp_col, pb->d_sp_val,

@@ -92,6 +92,9 @@ struct tdw_problem {
   double* d_phi = nullptr;   // internal order
   // FMM near-field mode: pair filter (adjacent leaf cells), no lag-2 split
   int* d_leafc = nullptr;    // packed leaf-cell coords per element (internal order) or null
+  int* d_pair_ptr = nullptr; // pairs= restriction (internal order): [ns+1] row pointers or null
+  int* d_pair_col = nullptr; //   sorted columns of each row
+  int gamma_max = 0;         // lags the store was asked to cover (0: all it needs)
   int split_lag2 = 1;        // lags 2..nsl+1 of the store keep the known density only
   int kb = 1;                // time steps per convolution pass (1..TDW_KB_MAX)
   int conv_rpw = 2;          // rows per consumer warp of conv_kernel (2 or 4)
@@ -124,6 +127,8 @@ struct tdw_problem {
   double* d_aval = nullptr;
   double* d_adiag = nullptr;
   int jac_iters = 0;
+  bool solver_krylov = false;      // BiCGSTAB solve (Jacobi bound >= 0.9 or TDW_SOLVER=krylov)
+  double* d_kw = nullptr;          // [9][ns] Krylov / standalone-solve workspace
   // near structure: pairs whose band reaches a split lag g in 2..nsl+1, all rows,
   // ELL columns [TDW_NEAR_MAX][ns], values [nsl][TDW_NEAR_MAX][ns] (lag g = 2 + index)
   int near_w = 0;
@@ -214,6 +219,8 @@ int tdw_fmm_loop(tdw_problem* pb, double threshold, bool want_rhs, tdw_timing* t
 int tdw_fmm_march_emulated(tdw_problem** pbs, int n, double threshold);
 long long tdw_fmm_m2l_pairs(const tdw_problem* pb);
 int tdw_fmm_time_m2l_impl(tdw_problem* pb, int n, double* flops, float* ms);
+int tdw_step_solve_impl(tdw_problem* pb, const double* b, double* x, double* stats);
+int tdw_step_matrix_impl(tdw_problem* pb, int64_t* nnz, int64_t* rows, int64_t* cols, double* vals);
 void tdw_fmm_free(struct FmmState* F);
 int tdw_march_emulated_impl(tdw_problem** pbs, int n, double threshold);
 int tdw_problem_create_impl(tdw_ctx* ctx, const tdw_problem_desc* dsc, tdw_problem** out, bool shard_only);

@@ -26,8 +26,8 @@ from . import _lib
 from .mesh import mesh_stats
 from .tbasis import decomposition_weights, eval_basis
 
-__all__ = ["ProblemSpec", "TimeHistory", "BandStore", "compute_gamma_star", "greville_samples", "greville_times",
-           "build_retarded_matrices", "march"]
+__all__ = ["ProblemSpec", "TimeHistory", "BandStore", "StepSolver", "compute_gamma_star", "greville_samples",
+           "greville_times", "build_retarded_matrices", "build_step_matrix", "march"]
 
 
 @dataclass
@@ -180,7 +180,8 @@ class BandStore:
     """Device-resident banded coefficient store + lag-1 step matrix (tdw_problem)."""
 
     def __init__(self, spec, window: bool = True, ctx: _lib.Context | None = None,
-                 nranks: int = 1, rank: int = 0, shard_only: bool = False):
+                 nranks: int = 1, rank: int = 0, shard_only: bool = False, pairs=None,
+                 gamma_max: int | None = None):
         self.ctx = ctx or _lib.default_context()
         lib = _lib.load()
         mesh = spec.mesh
@@ -207,6 +208,17 @@ class BandStore:
         # spec that differs (the split-lag store and the step matrix depend on phi,
         # the coefficients on bie, d, c, dt and the geometry)
         self.key = problem_key(spec)
+        self.gamma_max = None if gamma_max is None else int(gamma_max)
+        self.pairs = None
+        if pairs is not None:
+            ii = np.ascontiguousarray(np.asarray(pairs[0]).reshape(-1), dtype=np.int64)
+            jj = np.ascontiguousarray(np.asarray(pairs[1]).reshape(-1), dtype=np.int64)
+            if ii.shape != jj.shape:
+                raise ValueError("pairs: row and column index arrays differ in length")
+            _lib.check(lib.tdw_restrict_pairs(self.h, len(ii), ii.ctypes.data_as(C.POINTER(C.c_int64)),
+                                              jj.ctypes.data_as(C.POINTER(C.c_int64))),
+                       self.ctx.h, "tdw_restrict_pairs")
+            self.pairs = len(ii)
 
     def assemble(self):
         if not self.assembled:
@@ -296,6 +308,8 @@ def problem_key(spec) -> tuple:
 def _check_store(mats, spec, window):
     if mats.window != window or mats.nt < spec.nt or mats.ns != spec.mesh.n_elements:
         raise ValueError("matrix set does not cover the required lags")
+    if mats.gamma_max is not None and mats.gamma_max < mats.n_lags:
+        raise ValueError("matrix set does not cover the required lags")
     if mats.nt != spec.nt:
         raise ValueError(f"store built for nt={mats.nt}, spec has nt={spec.nt}: rebuild it "
                          "(the device history is sized at assembly)")
@@ -311,14 +325,59 @@ def build_retarded_matrices(spec, gamma_max: int | None = None, pairs=None, slab
                             window: bool = True) -> BandStore:
     """Assemble the device banded store (replaces marching.py:132-181).
 
-    `gamma_max` is accepted for signature compatibility; the store always
-    covers the lags `march` needs (min(gamma*, nt-1), or nt-1 without window).
-    `pairs` restriction (the fast solver's near field) is not part of the
-    direct path.
-    """
-    if pairs is not None:
-        raise NotImplementedError("pair-restricted assembly belongs to the FMM near field")
-    return BandStore(spec, window=window).assemble()
+    `pairs=(ii, jj)` restricts the store -- and the lag-1 step matrix built from
+    it -- to those element pairs (marching.py:132-133, 149; tdw_restrict_pairs).
+    `gamma_max` is recorded: like the reference's matrix set, a store asked for
+    fewer lags than march needs makes march raise ValueError.  The store itself
+    always holds the lags of its window (min(gamma*, nt-1), or nt-1 without
+    window).  `slab` (the reference's memory chunking) has no meaning here."""
+    return BandStore(spec, window=window, pairs=pairs, gamma_max=gamma_max).assemble()
+
+
+class StepSolver:
+    """The factorisation object of build_step_matrix: `solve(b)` = A^{-1} b on the
+    device (tdw_step_solve, BiCGSTAB to round-off), with the reference's
+    residual test (marching.py:330-333)."""
+
+    def __init__(self, store: BandStore):
+        self.store = store
+        self.last_stats = None
+
+    def solve(self, b):
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        if b.shape != (self.store.ns,):
+            raise ValueError(f"b must have shape ({self.store.ns},)")
+        x = np.empty_like(b)
+        st = np.zeros(3)
+        _lib.check(_lib.load().tdw_step_solve(self.store.h, _lib.dptr(b), _lib.dptr(x), _lib.dptr(st)),
+                   self.store.ctx.h, "tdw_step_solve")
+        self.last_stats = st
+        if st[0] > 1e-10 * max(st[1], 1e-300):
+            raise RuntimeError(f"step solve residual {st[0]:.3e} too large")
+        return x
+
+
+def build_step_matrix(spec, mats):
+    """A = w0 (W1 phi - U1 (1 - phi)) and its solver (marching.py:279-289): A as a
+    scipy CSC matrix in the caller's element order, downloaded from the device
+    store, and a StepSolver whose solve(b) runs on the GPU."""
+    import scipy.sparse as sp
+    if not isinstance(mats, BandStore):
+        raise TypeError("mats must come from build_retarded_matrices of this package")
+    _check_store(mats, spec, mats.window)
+    mats.assemble()
+    lib = _lib.load()
+    nnz = C.c_int64(0)
+    _lib.check(lib.tdw_step_matrix(mats.h, C.byref(nnz), None, None, None), mats.ctx.h, "tdw_step_matrix")
+    rows = np.empty(nnz.value, np.int64)
+    cols = np.empty(nnz.value, np.int64)
+    vals = np.empty(nnz.value)
+    p64 = C.POINTER(C.c_int64)
+    _lib.check(lib.tdw_step_matrix(mats.h, C.byref(nnz), rows.ctypes.data_as(p64), cols.ctypes.data_as(p64),
+                                   _lib.dptr(vals)), mats.ctx.h, "tdw_step_matrix")
+    ns = spec.mesh.n_elements
+    A = sp.csc_matrix((vals, (rows, cols)), shape=(ns, ns))
+    return A, StepSolver(mats)
 
 
 def march(spec, window: bool = True, blowup_factor: float = 1e6, mats=None,

@@ -12,6 +12,7 @@ the reference itself never does.
     NUMBA_CACHE_DIR=/tmp/nb python tests/golden/make_golden.py tree 3
     NUMBA_CACHE_DIR=/tmp/nb python tests/golden/make_golden.py tree 4   # two spheres, ~1 min
     NUMBA_CACHE_DIR=/tmp/nb python tests/golden/make_golden.py fmm_ref  # patched reference fast_march
+    NUMBA_CACHE_DIR=/tmp/nb python tests/golden/make_golden.py march_pairs  # pairs= restriction
 
 Scenario recipe: SURVEY.md section 8(c)/(d) (icosphere f=4/8/16, c=1,
 c*dt = 0.5 * mean edge, Gaussian plane pulse along z, sigma=4dt, t0=6 sigma).
@@ -189,6 +190,29 @@ def make_march(cfg):
           f"status={hist.status} n_steps={hist.n_steps} max|x|={np.abs(unknown).max():.4g}")
 
 
+def pair_subset(mesh, radius=1.2):
+    """The pair restriction of the pairs= fixture: centroid distance < radius."""
+    c = mesh.centroids
+    dist = np.linalg.norm(c[:, None, :] - c[None, :, :], axis=2)
+    ii, jj = np.nonzero(dist < radius)
+    return ii.astype(np.int64), jj.astype(np.int64)
+
+
+def make_march_pairs():
+    """build_retarded_matrices(spec, n_lags, pairs=...) + march(mats=...) of the
+    reference on config 0 with the pairs restricted to centroid distance < 1.2."""
+    spec = build_spec(0)
+    stats = marching.mesh_stats(spec.mesh)
+    n_lags = min(marching.compute_gamma_star(stats, spec.basis, spec.c), spec.nt - 1)
+    ii, jj = pair_subset(spec.mesh)
+    mats = marching.build_retarded_matrices(spec, n_lags, pairs=(ii, jj))
+    trace = []
+    hist = marching.march(spec, mats=mats, rhs_trace=trace)
+    np.savez_compressed(OUT / "march_pairs_cfg0.npz", radius=1.2, n_pairs=len(ii), u=hist.u, rhs=np.array(trace),
+                        status=hist.status, n_steps=hist.n_steps, versions=VERSIONS)
+    print("march_pairs_cfg0:", len(ii), "pairs", hist.status, hist.n_steps, np.abs(hist.u).max())
+
+
 def make_tree(cfg, leaf_capacity=20):
     """Octree + interaction lists from the reference build_tree (bit-exact target)."""
     from tdwavebem.fmm_tree import build_tree
@@ -355,6 +379,8 @@ if __name__ == "__main__":
         make_march(int(sys.argv[2]))
     elif what == "tree":
         make_tree(int(sys.argv[2]))
+    elif what == "march_pairs":
+        make_march_pairs()
     elif what == "fmm_ref":
         make_fmm_ref()
     elif what == "fmm_setup":

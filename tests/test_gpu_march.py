@@ -348,3 +348,85 @@ def test_full_size_rhs_matches_reference_form(cfg):
           f"worst residual {rel_res.max():.3e}, steps {alphas}")
     assert err.max() < tol, (err.max(), alphas[int(err.argmax())])
     assert rel_res.max() < 1e-10
+
+
+def test_pair_restricted_store_matches_reference():
+    """build_retarded_matrices(spec, pairs=(ii, jj)) (marching.py:132-181 with the
+    pairs argument): the reference's own restricted march (config 0, pairs at
+    centroid distance < 1.2; tests/golden/march_pairs_cfg0.npz) is reproduced."""
+    g = golden("march_pairs_cfg0.npz")
+    spec = scenarios.build_spec(0)
+    c = spec.mesh.centroids
+    ii, jj = np.nonzero(np.linalg.norm(c[:, None, :] - c[None, :, :], axis=2) < float(g["radius"]))
+    assert len(ii) == int(g["n_pairs"])
+    store = marching.build_retarded_matrices(spec, pairs=(ii, jj))
+    trace = []
+    h = marching.march(spec, mats=store, rhs_trace=trace)
+    assert h.status == str(g["status"]) and h.n_steps == int(g["n_steps"])
+    assert per_step_rel(h.u, g["u"]).max() < 1e-9
+    assert per_step_rel(np.array(trace), g["rhs"]).max() < 1e-9
+    full = marching.march(spec)
+    assert per_step_rel(h.u, full.u).max() > 1e-3   # the restriction really changes the problem
+
+
+def test_build_step_matrix_and_solve():
+    """build_step_matrix (marching.py:279-289): A from the device store equals the
+    oracle's w0 (W1 phi - U1 (1 - phi)) entry for entry, and lu.solve(b) on the
+    device equals scipy's sparse LU solution."""
+    import scipy.sparse.linalg as spla
+    for cfg in (0, 2):
+        spec = scenarios.build_spec(cfg)
+        store = marching.build_retarded_matrices(spec)
+        A, lu = marching.build_step_matrix(spec, store)
+        mesh, d = spec.mesh, spec.basis.d
+        v0, v1, v2 = mesh.element_vertices()
+        rows, cols = A.nonzero()
+        kw = dict(which="bm", nx=-mesh.normals[rows]) if spec.bie == "bmbie" else {}
+        U1, W1 = oracle.coeff_table(mesh.centroids[rows], v0[cols], v1[cols], v2[cols], mesh.normals[cols],
+                                    np.full(len(rows), spec.c * spec.basis.dt), d, spec.c, spec.basis.dt, **kw)
+        w0 = spec.basis.weights[0]
+        ref = w0 * (W1 * spec.phi[cols] - U1 * (1.0 - spec.phi[cols]))
+        got = np.asarray(A[rows, cols]).ravel()
+        assert np.abs(got - ref).max() <= 1e-12 * np.abs(ref).max()
+        # every arrived lag-1 pair is present: arrival = max(ceil(max(|ci-cj| - rho_j, 0)/(c dt)) - 1, 1) == 1
+        cen, rad = mesh.centroids, mesh.element_radii()
+        dist = np.maximum(np.linalg.norm(cen[:, None, :] - cen[None, :, :], axis=2) - rad[None, :], 0.0)
+        arr = np.maximum(np.ceil(dist / (spec.c * spec.basis.dt)).astype(int) - 1, 1)
+        assert A.nnz <= int((arr == 1).sum()) and A.nnz >= 0.9 * int((arr == 1).sum())
+        b = np.random.default_rng(cfg).standard_normal(mesh.n_elements)
+        x = lu.solve(b)
+        xr = spla.spsolve(A.tocsc(), b)
+        assert np.linalg.norm(x - xr) <= 1e-12 * np.linalg.norm(xr)
+        store.close()
+
+
+@pytest.mark.parametrize("cfg", [0, 1, 2])
+def test_krylov_solver_matches(cfg, monkeypatch):
+    """The BiCGSTAB solve the loop switches to for step matrices with a Jacobi
+    bound >= 0.9 (forced here with TDW_SOLVER=krylov) reproduces the reference
+    (goldens) like the Jacobi cluster solvers do."""
+    monkeypatch.setenv("TDW_SOLVER", "krylov")
+    spec = scenarios.build_spec(cfg)
+    h = marching.march(spec)
+    g = golden(f"march_cfg{cfg}.npz")
+    assert h.status == str(g["status"]) and h.n_steps == int(g["n_steps"])
+    x = _unknown(h, spec)
+    tol = TOL[spec.basis.d] if spec.bie == "bmbie" else 1e-9
+    assert per_step_rel(x[:, g["sub"]], g["unknown_sub"]).max() < tol
+
+
+def test_store_validation():
+    """A store is tied to the problem it was assembled for (phi, bie, d, c, dt,
+    geometry): march refuses another spec; a gamma_max below the lags march
+    needs raises like the reference (marching.py:306-308)."""
+    spec = scenarios.build_spec(0)
+    store = marching.build_retarded_matrices(spec)
+    other = scenarios.build_spec(0)
+    other.phi = np.zeros_like(other.phi)
+    other.u_data, other.q_data = other.q_data, None
+    with pytest.raises(ValueError, match="phi"):
+        marching.march(other, mats=store)
+    short = marching.build_retarded_matrices(spec, gamma_max=3)
+    with pytest.raises(ValueError, match="cover the required lags"):
+        marching.march(spec, mats=short)
+    marching.march(spec, mats=store)  # the matching spec still runs

@@ -132,3 +132,55 @@ def test_vectorised_boundary_data_equals_per_step_calls():
         marching.sample_data(plain, times, out2, on_chunk=lambda a, b: seen.append((a, b)))
         np.testing.assert_array_equal(out2, ref)
         assert seen == [(0, len(times))]
+
+
+def test_time_history_sums_follow_the_reference():
+    """TimeHistory.stock_sums / windowed_sums / tilde_sums / finalize_step
+    (marching.py:205-242) on the reference's own config-0 history
+    (tests/golden/march_cfg0.npz): stock sums reproduce its tau/sigma, the
+    windowed sums truncate at the window bottom, the tilde sums drop the
+    unknown w0 term, finalize_step promotes the solved density by phi."""
+    g = golden("march_cfg0.npz")
+    spec = scenarios.build_spec(0)
+    h = marching.TimeHistory(spec.basis, spec.nt, spec.mesh.n_elements)
+    h.u[:], h.q[:] = g["u"], g["q"]
+    w, d = spec.basis.weights, spec.basis.d
+    for beta in (0, 1, 2, 5, 40, spec.nt - 2):
+        tau, sig = h.stock_sums(beta)
+        np.testing.assert_allclose(tau, g["tau"][beta], rtol=0, atol=1e-13 * np.abs(g["tau"]).max())
+        np.testing.assert_allclose(sig, g["sigma"][beta], rtol=0, atol=1e-13 * np.abs(g["sigma"]).max())
+        for bstar in (beta - 1, beta - 2, beta - d - 1, beta - 10):
+            tw, sw = h.windowed_sums(beta, bstar)
+            kmax = min(d + 1, beta - bstar, beta)
+            ref = sum(w[k] * h.q[beta - k] for k in range(kmax + 1))
+            np.testing.assert_array_equal(tw, ref)
+    uk, qk = marching.greville_samples(spec)
+    beta = 7
+    tt, st = h.tilde_sums(beta, spec.phi, uk[beta], qk[beta])
+    tau, sig = h.stock_sums(beta)
+    np.testing.assert_allclose(tt, tau - w[0] * h.q[beta] + w[0] * qk[beta] * spec.phi, atol=1e-12)
+    np.testing.assert_allclose(st, sig - w[0] * h.u[beta] + w[0] * uk[beta] * (1 - spec.phi), atol=1e-12)
+    x = g["u"][beta]
+    h2 = marching.TimeHistory(spec.basis, spec.nt, spec.mesh.n_elements)
+    h2.u[:beta], h2.q[:beta] = g["u"][:beta], g["q"][:beta]
+    h2.finalize_step(beta, spec.phi, uk[beta], qk[beta], x)
+    np.testing.assert_array_equal(h2.u[beta], x)            # phi = 1: u solved
+    np.testing.assert_array_equal(h2.q[beta], qk[beta])     # q known
+    np.testing.assert_allclose(h2.tau[beta], g["tau"][beta], atol=1e-13 * np.abs(g["tau"]).max())
+
+
+def test_fmm_config_defaults_and_gpu_limits():
+    """FmmConfig keeps the reference's defaults (ps = pt = 8, leaf capacity 100,
+    fmm.py:35-41); the GPU fast solver implements ps = pt = 4 and raises
+    ValueError naming that limit before any device work."""
+    from paper_2111_05205_b200 import fmm, fmm_plan
+    c = fmm_plan.FmmConfig()
+    assert (c.ps, c.pt, c.leaf_capacity, c.mu) == (8, 8, 100, 8)
+    spec = scenarios.build_spec(0)
+    with pytest.raises(ValueError, match="ps = pt = 4"):
+        fmm.fast_march(spec)
+    with pytest.raises(ValueError, match="mu"):
+        fmm_plan.FmmConfig(ps=4, pt=4, mu=9).check_gpu()
+    b = fmm_plan.baseline_config()
+    assert (b.ps, b.pt, b.leaf_capacity, b.mu) == (4, 4, 20, 8)
+    b.check_gpu()
