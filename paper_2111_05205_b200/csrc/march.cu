@@ -2386,6 +2386,40 @@ static int setup_halo(tdw_problem* pb, const std::vector<int>& acol, const std::
   return TDW_OK;
 }
 
+// The near structure in the forms the loop reads: columns in the cluster's
+// (owner CTA, local row) packing for R rows per CTA, and the compact row-major
+// copy near_step_kernel streams.
+static int build_near_compact(tdw_problem* pb, int R) {
+  tdw_ctx* ctx = pb->ctx;
+  const int ns = pb->ns;
+  {
+    // near columns in the cluster's (owner, local) packing
+    std::vector<int> ncol((size_t)TDW_NEAR_MAX * ns);
+    TDW_CUDA(ctx, cudaMemcpy(ncol.data(), pb->d_ncol, sizeof(int) * ncol.size(), cudaMemcpyDeviceToHost));
+    for (int& j : ncol) j = ((j / R) << 24) | (j % R);
+    TDW_CUDA(ctx, cudaMalloc(&pb->d_ncol_packed, sizeof(int) * ncol.size()));
+    TDW_CUDA(ctx, cudaMemcpy(pb->d_ncol_packed, ncol.data(), sizeof(int) * ncol.size(), cudaMemcpyHostToDevice));
+    // compact row-major near structure for near_step_kernel
+    std::vector<int> cnt(ns), ptr(ns);
+    TDW_CUDA(ctx, cudaMemcpy(cnt.data(), pb->d_ncnt, sizeof(int) * ns, cudaMemcpyDeviceToHost));
+    long long nnz = 0;
+    for (int i = 0; i < ns; ++i) {
+      ptr[i] = (int)nnz;
+      nnz += cnt[i];
+    }
+    pb->n_near = nnz;
+    TDW_CUDA(ctx, cudaMalloc(&pb->d_nptr, sizeof(int) * ns));
+    TDW_CUDA(ctx, cudaMemcpy(pb->d_nptr, ptr.data(), sizeof(int) * ns, cudaMemcpyHostToDevice));
+    TDW_CUDA(ctx, cudaMalloc(&pb->d_ncol_rm, sizeof(int) * std::max(1LL, nnz)));
+    TDW_CUDA(ctx, cudaMalloc(&pb->d_nval_rm, sizeof(double) * std::max(1LL, nnz * pb->nsl)));
+    near_compact_kernel<<<2 * ctx->num_sms, 256, 0, ctx->stream>>>(pb->d_ncol, pb->d_nval, pb->d_phi, ns,
+                                                                  pb->nsl, pb->d_nptr, pb->d_ncnt, nnz,
+                                                                  pb->d_ncol_rm, pb->d_nval_rm);
+    TDW_CUDA(ctx, cudaGetLastError());
+  }
+  return TDW_OK;
+}
+
 // Partition the lag-1 step matrix over a thread-block cluster (host, once per
 // problem): smallest CL in {1,2,4,8,16} whose per-CTA slice fits in shared memory.
 int tdw_setup_cluster_solver(tdw_problem* pb) {
@@ -2406,7 +2440,7 @@ int tdw_setup_cluster_solver(tdw_problem* pb) {
       pb->near_in_solve = false;
       pb->near_tail = 0;
       pb->jac_iters = 400;  // BiCGSTAB iteration cap
-      return TDW_OK;
+      return build_near_compact(pb, ns);
     }
   }
   std::vector<int> acol((size_t)TDW_ELL_MAX * ns);
@@ -2530,29 +2564,8 @@ int tdw_setup_cluster_solver(tdw_problem* pb) {
     TDW_CUDA(ctx, cudaMemcpy(pb->d_sp_val, val.data(), sizeof(double) * val.size(), cudaMemcpyHostToDevice));
   }
   {
-    // near columns in the cluster's (owner, local) packing
-    std::vector<int> ncol((size_t)TDW_NEAR_MAX * ns);
-    TDW_CUDA(ctx, cudaMemcpy(ncol.data(), pb->d_ncol, sizeof(int) * ncol.size(), cudaMemcpyDeviceToHost));
-    for (int& j : ncol) j = ((j / R) << 24) | (j % R);
-    TDW_CUDA(ctx, cudaMalloc(&pb->d_ncol_packed, sizeof(int) * ncol.size()));
-    TDW_CUDA(ctx, cudaMemcpy(pb->d_ncol_packed, ncol.data(), sizeof(int) * ncol.size(), cudaMemcpyHostToDevice));
-    // compact row-major near structure for near_step_kernel
-    std::vector<int> cnt(ns), ptr(ns);
-    TDW_CUDA(ctx, cudaMemcpy(cnt.data(), pb->d_ncnt, sizeof(int) * ns, cudaMemcpyDeviceToHost));
-    long long nnz = 0;
-    for (int i = 0; i < ns; ++i) {
-      ptr[i] = (int)nnz;
-      nnz += cnt[i];
-    }
-    pb->n_near = nnz;
-    TDW_CUDA(ctx, cudaMalloc(&pb->d_nptr, sizeof(int) * ns));
-    TDW_CUDA(ctx, cudaMemcpy(pb->d_nptr, ptr.data(), sizeof(int) * ns, cudaMemcpyHostToDevice));
-    TDW_CUDA(ctx, cudaMalloc(&pb->d_ncol_rm, sizeof(int) * std::max(1LL, nnz)));
-    TDW_CUDA(ctx, cudaMalloc(&pb->d_nval_rm, sizeof(double) * std::max(1LL, nnz * pb->nsl)));
-    near_compact_kernel<<<2 * ctx->num_sms, 256, 0, ctx->stream>>>(pb->d_ncol, pb->d_nval, pb->d_phi, ns,
-                                                                  pb->nsl, pb->d_nptr, pb->d_ncnt, nnz,
-                                                                  pb->d_ncol_rm, pb->d_nval_rm);
-    TDW_CUDA(ctx, cudaGetLastError());
+    int rc = build_near_compact(pb, R);
+    if (rc) return rc;
   }
   TDW_CUDA(ctx, cudaFuncSetAttribute(solve_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)pb->sp_smem));
