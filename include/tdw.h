@@ -56,6 +56,12 @@ typedef struct tdw_problem tdw_problem;
 /* kind: 0 = "uw" (U, W), 1 = "bm" (Burton-Miller Ubar, Wbar) */
 #define TDW_KIND_UW 0
 #define TDW_KIND_BM 1
+/* coefficient mode: AUTO = the banded store when it fits in device
+ * memory, else on the fly; STORED_BAND = always the store (HBM-bound pass);
+ * ON_THE_FLY = every convolution pass re-evaluates the closed forms (FP64-bound) */
+#define TDW_MODE_AUTO 0
+#define TDW_MODE_STORED_BAND 1
+#define TDW_MODE_ON_THE_FLY 2
 /* bie: 0 = "obie", 1 = "bmbie" */
 #define TDW_BIE_OBIE 0
 #define TDW_BIE_BMBIE 1
@@ -72,6 +78,7 @@ typedef struct {
   int32_t nt;                /* time steps; the loop solves nt-1 of them         */
   int32_t window;            /* 1 = sliding window at gamma* (reference default) */
   int32_t nranks, rank;      /* row sharding; 1, 0 for a single GPU              */
+  int32_t mode;              /* TDW_MODE_*: coefficients stored or recomputed     */
 } tdw_problem_desc;
 
 typedef struct {

@@ -14,6 +14,7 @@ import numpy as np
 LIB_PATH = Path(os.environ.get("TDW_LIB_PATH") or Path(__file__).resolve().parent / "libtdw.so")
 
 TDW_OK = 0
+MODES = {"auto": 0, "stored": 1, "on_the_fly": 2}
 _ERRORS = {1: ValueError, 2: ValueError, 3: RuntimeError, 4: RuntimeError, 5: RuntimeError,
            6: RuntimeError, 7: RuntimeError, 8: RuntimeError}
 
@@ -26,7 +27,7 @@ class ProblemDesc(C.Structure):
     _fields_ = [("ns", C.c_int32), ("nv", C.c_int32), ("vertices", _dp), ("triangles", _i64p),
                 ("phi", _dp), ("bie", C.c_int32), ("d", C.c_int32), ("c", C.c_double),
                 ("dt", C.c_double), ("nt", C.c_int32), ("window", C.c_int32),
-                ("nranks", C.c_int32), ("rank", C.c_int32)]
+                ("nranks", C.c_int32), ("rank", C.c_int32), ("mode", C.c_int32)]
 
 
 class Info(C.Structure):

@@ -532,6 +532,108 @@ __global__ void fill_unit_init(int2* u, long long n) {
     u[k] = make_int2(INT_MAX, -1);
 }
 
+// ---------------------------------------------------------------- K2, on the fly
+// On-the-fly history convolution (coefficient mode TDW_MODE_ON_THE_FLY; SURVEY
+// 8(b) `mode`, north_star (1) "recomputed on the fly (FP64-pipe bound)"): no
+// banded store.  Every pass re-evaluates, per pair, the closed forms
+// U^(g), W^(g) for g in [glo - d - 1, ghi] (elemint.py:89-186 through the same
+// coeff_eval as the fill kernel), kappa-combines them into V^(gamma) exactly as
+// the fill kernel does -- including the known-density-only split lags -- and
+// multiplies them straight into the pass's kb step sums, reading the history
+// from global memory.  One warp per (row, group of OTF_TG J-tiles), lane =
+// column; the group's row partial goes to bpart[step][row][group], summed by
+// reduce_parts in group order.  Same sums as the stored path up to the order
+// of the additions; the cost is FP64-bound (~100x the stored pass), so the
+// loop uses it only when the store does not fit (or when asked).
+struct OtfArgs {
+  const double* elem;
+  const int* leafc;
+  const int* pptr;
+  const int* pcol;
+  const double* phi;
+  const double2* hist;
+  double* bpart;
+  const int* flags;
+  unsigned long long* n_evals;
+  int hcols, pad, ns, row_lo, rows_loc, ntiles, tg, S, cap, split_lag2, nsl, alpha, nb;
+  double c, dt, K;
+};
+
+template <int D, bool BM>
+__global__ void __launch_bounds__(128) otf_conv_kernel(OtfArgs a) {
+  if (a.flags[0] != 0) return;
+  const int lane = threadIdx.x & 31;
+  const long long task = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (task >= (long long)a.rows_loc * a.S) return;
+  const int rloc = (int)(task / a.S), grp = (int)(task % a.S);
+  const int i = a.row_lo + rloc;
+  double acc[TDW_KB_MAX];
+#pragma unroll
+  for (int s = 0; s < TDW_KB_MAX; ++s) acc[s] = 0.0;
+  long long nev = 0;
+  if (i < a.ns) {
+    const double cdt = a.c * a.dt;
+    double w[D + 2];
+    bspline_weights(D, w);
+    const double* pi = a.elem + (size_t)i * TDW_ELEM_STRIDE;
+    const double ci[3] = {pi[12], pi[13], pi[14]};
+    const double nx[3] = {-pi[9], -pi[10], -pi[11]};  // BM operator normal (marching.py:168-173)
+    const int t1 = min(a.ntiles, (grp + 1) * a.tg);
+    for (int t = grp * a.tg; t < t1; ++t) {
+      const int j = t * TDW_TJ + lane;
+      if (j >= a.ns || !pair_allowed(a.leafc, a.pptr, a.pcol, i, j)) continue;
+      Elem ej;
+      load_elem(a.elem, j, ej);
+      const Band b = pair_band(ci, ej, cdt, D, a.cap);
+      if (b.ghi < b.glo) continue;
+      PairGeom g;
+      pair_geom<BM>(ci, ej.v0, ej.v1, ej.v2, ej.n, nx, g);
+      const double pj = a.phi[j];
+      double ru[D + 2], rw[D + 2];
+#pragma unroll
+      for (int k = 0; k < D + 2; ++k) { ru[k] = 0.0; rw[k] = 0.0; }
+      for (int gg = max(b.arr, b.glo - (D + 1)); gg <= b.ghi; ++gg) {
+        double u, v;
+        coeff_eval<D, BM>(g, (double)gg * a.c * a.dt, a.K, u, v);
+        ++nev;
+#pragma unroll
+        for (int q = D + 1; q > 0; --q) { ru[q] = ru[q - 1]; rw[q] = rw[q - 1]; }
+        ru[0] = u;
+        rw[0] = v;
+        if (gg < b.glo) continue;
+        double vu = 0.0, vw = 0.0;
+#pragma unroll
+        for (int q = 0; q < D + 2; ++q) {
+          vu += w[q] * ru[q];
+          vw += w[q] * rw[q];
+        }
+        if (a.split_lag2 && gg >= 2 && gg <= a.nsl + 1) {  // known density only (as the fill kernel)
+          vu = pj == 1.0 ? vu : 0.0;
+          vw = pj == 1.0 ? 0.0 : vw;
+        }
+        // step alpha + s at lag gg reads time alpha + s - gg (zero rows before t = 0)
+        const double2* h = a.hist + (size_t)(a.pad + a.alpha - gg) * a.hcols + j;
+#pragma unroll
+        for (int s = 0; s < TDW_KB_MAX; ++s)
+          if (s < a.nb) {
+            const double2 x = __ldg(h + (size_t)s * a.hcols);
+            acc[s] = fma(-vw, x.y, fma(vu, x.x, acc[s]));
+          }
+      }
+    }
+  }
+#pragma unroll
+  for (int s = 0; s < TDW_KB_MAX; ++s) {
+    double v = acc[s];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULLMASK, v, o);
+    if (lane == 0 && s < a.nb) a.bpart[(size_t)s * a.rows_loc * a.S + (size_t)rloc * a.S + grp] = v;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) nev += __shfl_xor_sync(FULLMASK, nev, o);
+  if (lane == 0 && a.n_evals) atomicAdd(a.n_evals, (unsigned long long)nev);
+}
+
 }  // namespace tdw
 
 using namespace tdw;
@@ -741,6 +843,16 @@ int tdw_assemble_impl(tdw_problem* pb) {
       }
     pb->wmax = wm;
   }
+  // coefficient mode (SURVEY 8(b) `mode`): the banded store when it fits in device
+  // memory (TDW_MODE_AUTO) or when asked; otherwise the coefficients are
+  // recomputed by every convolution pass (otf_conv_kernel)
+  {
+    size_t fr = 0, tot = 0;
+    TDW_CUDA(ctx, cudaMemGetInfo(&fr, &tot));
+    pb->otf = pb->mode == TDW_MODE_ON_THE_FLY ||
+              (pb->mode == TDW_MODE_AUTO && total_bytes + (2ull << 30) > (unsigned long long)fr);
+  }
+  if (!pb->otf) {
   TDW_CUDA(ctx, cudaMalloc(&pb->d_units, total_bytes));
   {
     const int threads = 256;
@@ -759,6 +871,10 @@ int tdw_assemble_impl(tdw_problem* pb) {
   if (pb->d == 3) { if (bm) launch_fill<3, true>(a, nseg, st); else launch_fill<3, false>(a, nseg, st); }
   TDW_CUDA(ctx, cudaGetLastError());
   TDW_CUDA(ctx, cudaEventRecord(f1, st));
+  } else {
+    TDW_CUDA(ctx, cudaEventRecord(f0, st));
+    TDW_CUDA(ctx, cudaEventRecord(f1, st));
+  }
 
   TDW_CUDA(ctx, cudaEventRecord(e1, st));
   TDW_CUDA(ctx, cudaStreamSynchronize(st));
@@ -814,6 +930,22 @@ int tdw_assemble_impl(tdw_problem* pb) {
   {
     int src = tdw_setup_cluster_solver(pb);
     if (src) return src;
+  }
+  if (pb->otf) {
+    // on the fly: one warp per (row, group of 8 J-tiles), partials per group
+    pb->otf_tg = 8;
+    const int S = (pb->ntiles + pb->otf_tg - 1) / pb->otf_tg;
+    pb->nsplit = pb->conv_S = S;
+    pb->conv_grid = 0;
+    cudaFree(pb->d_bpart);
+    TDW_CUDA(ctx, cudaMalloc(&pb->d_bpart, pb->kb * sizeof(double) * (size_t)S * pb->rows_per_rank));
+    TDW_CUDA(ctx, cudaMemset(pb->d_bpart, 0, pb->kb * sizeof(double) * (size_t)S * pb->rows_per_rank));
+    TDW_CUDA(ctx, cudaMalloc(&pb->d_bnear, sizeof(double) * (size_t)pb->nsl * (pb->nsl + 1) * pb->ns));
+    if (!pb->d_otf_evals) TDW_CUDA(ctx, cudaMalloc(&pb->d_otf_evals, sizeof(unsigned long long)));
+    TDW_CUDA(ctx, cudaMemset(pb->d_otf_evals, 0, sizeof(unsigned long long)));
+    pb->store_bytes = 0;
+    pb->assembled = true;
+    return TDW_OK;
   }
   // convolution schedule (persistent CTAs, unit list per CTA)
   {
@@ -923,5 +1055,43 @@ int tdw_assemble_impl(tdw_problem* pb) {
   }
   pb->store_bytes = (int64_t)(total_bytes + sizeof(unsigned long long) * (nunit + 1) + sizeof(int2) * nunit);
   pb->assembled = true;
+  return TDW_OK;
+}
+
+// one on-the-fly convolution pass of steps alpha .. alpha + nb - 1 into bpart
+int launch_otf_conv(tdw_problem* pb, int alpha, int nb, cudaStream_t st) {
+  OtfArgs o{};
+  o.elem = pb->d_elem;
+  o.leafc = pb->d_leafc;
+  o.pptr = pb->d_pair_ptr;
+  o.pcol = pb->d_pair_col;
+  o.phi = pb->d_phi;
+  o.hist = pb->d_hist;
+  o.bpart = pb->d_bpart;
+  o.flags = pb->d_flags;
+  o.n_evals = pb->d_otf_evals;
+  o.hcols = pb->hcols;
+  o.pad = pb->pad;
+  o.ns = pb->ns;
+  o.row_lo = pb->row_lo;
+  o.rows_loc = pb->rows_per_rank;
+  o.ntiles = pb->ntiles;
+  o.tg = pb->otf_tg;
+  o.S = pb->nsplit;
+  o.cap = pb->cap;
+  o.split_lag2 = pb->split_lag2;
+  o.nsl = pb->nsl;
+  o.alpha = alpha;
+  o.nb = nb;
+  o.c = pb->c;
+  o.dt = pb->dt;
+  o.K = pb->K;
+  const bool bm = pb->bie == TDW_BIE_BMBIE;
+  const long long threads = (long long)pb->rows_per_rank * pb->nsplit * 32;
+  const unsigned blocks = (unsigned)((threads + 127) / 128);
+  if (pb->d == 1) { if (bm) otf_conv_kernel<1, true><<<blocks, 128, 0, st>>>(o); else otf_conv_kernel<1, false><<<blocks, 128, 0, st>>>(o); }
+  if (pb->d == 2) { if (bm) otf_conv_kernel<2, true><<<blocks, 128, 0, st>>>(o); else otf_conv_kernel<2, false><<<blocks, 128, 0, st>>>(o); }
+  if (pb->d == 3) { if (bm) otf_conv_kernel<3, true><<<blocks, 128, 0, st>>>(o); else otf_conv_kernel<3, false><<<blocks, 128, 0, st>>>(o); }
+  TDW_CUDA(pb->ctx, cudaGetLastError());
   return TDW_OK;
 }

@@ -159,6 +159,11 @@ int tdw_problem_create_impl(tdw_ctx* ctx, const tdw_problem_desc* dsc, tdw_probl
   pb->d = dsc->d;
   pb->nt = dsc->nt;
   pb->window = dsc->window ? 1 : 0;
+  if (dsc->mode < TDW_MODE_AUTO || dsc->mode > TDW_MODE_ON_THE_FLY) {
+    delete pb;
+    return tdw_fail(ctx, TDW_ERR_INVALID_ARG, "unknown coefficient mode");
+  }
+  pb->mode = dsc->mode;
   {
     // temporal blocking: one convolution pass computes kb consecutive steps
     // default 4; 5 / 6 as a pass (~ ns^2 / ranks band entries) outweighs the solves
@@ -398,7 +403,7 @@ int tdw_problem_info(const tdw_problem* pb, tdw_info* out) {
   out->solve_halo = pb->sp_halo;
   out->near_width = pb->near_w;
   out->conv_rpw = pb->conv_rpw;
-  out->coeff_mode = 0;
+  out->coeff_mode = pb->assembled ? (pb->otf ? TDW_MODE_ON_THE_FLY : TDW_MODE_STORED_BAND) : pb->mode;
   return TDW_OK;
 }
 
@@ -640,7 +645,7 @@ int tdw_problem_destroy(tdw_problem* pb) {
   if (!pb) return TDW_OK;
   cudaSetDevice(pb->ctx->device);
   void* ptrs[] = {pb->d_perm, pb->d_elem, pb->d_phi, pb->d_units, pb->d_unit_off, pb->d_sched, pb->d_sched_off,
-                  pb->d_sched_item, pb->d_leafc, pb->d_pair_ptr, pb->d_pair_col, pb->d_kw,
+                  pb->d_sched_item, pb->d_leafc, pb->d_pair_ptr, pb->d_pair_col, pb->d_kw, pb->d_otf_evals,
                   pb->d_unit, pb->d_acol, pb->d_aval, pb->d_adiag, pb->d_hist, pb->d_uk,
                   pb->d_qk, pb->d_bpart, pb->d_b, pb->d_x, pb->d_red, pb->d_bar, pb->d_flags,
                   pb->d_rhs, pb->d_sp_rowptr, pb->d_sp_nnzoff, pb->d_sp_col, pb->d_sp_val,

@@ -574,6 +574,7 @@ extern "C" int tdw_fmm_setup(tdw_problem* pb, const tdw_fmm_desc* fd) {
   int rc = up(ctx, &pb->d_leafc, leafc.data(), ns);
   if (rc) return rc;
   pb->split_lag2 = 0;
+  pb->mode = TDW_MODE_STORED_BAND;  // the near field is always a store
   pb->kb = 1;  // the FMM loop is sequential: one step per convolution pass
   pb->overlap = 1;
   pb->nsl = 1;

@@ -1762,12 +1762,12 @@ int make_plan(tdw_problem* pb, LoopPlan& L, double threshold, bool want_rhs) {
   fill_conv_args(pb, L.c);
   L.c.dry = getenv("TDW_DIAG_DRY_LOOP") ? 1 : 0;  // timing diagnostics only: wrong results
   L.c.trace = pb->d_trace;
-  {
+  if (!pb->otf) {  // the stored pass streams units and history boxes (TMA)
     int rc = make_hist_map(pb, &L.hmap);
     if (rc) return rc;
+    L.smem = pb->conv_stage_bytes;
+    TDW_CUDA(ctx, conv_set_smem(pb->kb, pb->conv_rpw, (int)L.smem));
   }
-  L.smem = pb->conv_stage_bytes;
-  TDW_CUDA(ctx, conv_set_smem(pb->kb, pb->conv_rpw, (int)L.smem));
   L.cgrid = dim3(pb->conv_grid);
   L.multi = ctx->comm != nullptr;
   ClusterSolveArgs& cs = L.cs;
@@ -1837,7 +1837,12 @@ int begin_loop(tdw_problem* pb, cudaStream_t st) {
 int launch_conv(tdw_problem* pb, LoopPlan& L, int alpha, int nsteps, cudaStream_t s) {
   L.c.alpha = alpha;
   L.c.bpart = pb->d_bpart;
-  conv_launch(pb->kb, pb->conv_rpw, L.cgrid, L.smem, s, L.c, L.hmap);
+  if (pb->otf) {
+    int rc = launch_otf_conv(pb, alpha, nsteps, s);
+    if (rc) return rc;
+  } else {
+    conv_launch(pb->kb, pb->conv_rpw, L.cgrid, L.smem, s, L.c, L.hmap);
+  }
   // fixed-order sum of the split partials into the steps' b (own rows), on the
   // convolution's stream: off the solve's critical path
   reduce_parts_kernel<<<dim3((pb->rows_per_rank + 127) / 128, nsteps), 128, 0, s>>>(
@@ -2200,6 +2205,25 @@ int tdw_march_emulated_impl(tdw_problem** pbs, int n, double threshold) {
 int tdw_time_conv_impl(tdw_problem* pb, int n, float* ms_out) {
   tdw_ctx* ctx = pb->ctx;
   cudaStream_t st = ctx->stream;
+  if (pb->otf) {  // on-the-fly pass
+    const int alpha = std::max(1, pb->nt - pb->kb);
+    TDW_CUDA(ctx, cudaMemsetAsync(pb->d_flags, 0, sizeof(int) * 4, st));
+    int rc = launch_otf_conv(pb, alpha, pb->kb, st);  // warm-up
+    if (rc) return rc;
+    cudaEvent_t e0, e1;
+    TDW_CUDA(ctx, cudaEventCreate(&e0));
+    TDW_CUDA(ctx, cudaEventCreate(&e1));
+    TDW_CUDA(ctx, cudaEventRecord(e0, st));
+    for (int k = 0; k < n && !rc; ++k) rc = launch_otf_conv(pb, alpha, pb->kb, st);
+    TDW_CUDA(ctx, cudaEventRecord(e1, st));
+    TDW_CUDA(ctx, cudaEventSynchronize(e1));
+    float t = 0.f;
+    cudaEventElapsedTime(&t, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    *ms_out = t / std::max(1, n);
+    return rc;
+  }
   ConvArgs c{};
   fill_conv_args(pb, c);
   c.alpha = std::max(1, pb->nt - pb->kb);

@@ -95,6 +95,10 @@ struct tdw_problem {
   int* d_pair_ptr = nullptr; // pairs= restriction (internal order): [ns+1] row pointers or null
   int* d_pair_col = nullptr; //   sorted columns of each row
   int gamma_max = 0;         // lags the store was asked to cover (0: all it needs)
+  int mode = 0;              // TDW_MODE_* requested
+  bool otf = false;          // coefficients recomputed by every pass (no banded store)
+  int otf_tg = 8;            // J-tiles per on-the-fly partial
+  unsigned long long* d_otf_evals = nullptr;  // closed-form evaluations of the on-the-fly passes
   int split_lag2 = 1;        // lags 2..nsl+1 of the store keep the known density only
   int kb = 1;                // time steps per convolution pass (1..TDW_KB_MAX)
   int conv_rpw = 2;          // rows per consumer warp of conv_kernel (2 or 4)
@@ -220,6 +224,7 @@ int tdw_fmm_march_emulated(tdw_problem** pbs, int n, double threshold);
 long long tdw_fmm_m2l_pairs(const tdw_problem* pb);
 int tdw_fmm_time_m2l_impl(tdw_problem* pb, int n, double* flops, float* ms);
 int tdw_step_solve_impl(tdw_problem* pb, const double* b, double* x, double* stats);
+int launch_otf_conv(tdw_problem* pb, int alpha, int nb, cudaStream_t st);
 int tdw_step_matrix_impl(tdw_problem* pb, int64_t* nnz, int64_t* rows, int64_t* cols, double* vals);
 void tdw_fmm_free(struct FmmState* F);
 int tdw_march_emulated_impl(tdw_problem** pbs, int n, double threshold);

@@ -181,7 +181,7 @@ class BandStore:
 
     def __init__(self, spec, window: bool = True, ctx: _lib.Context | None = None,
                  nranks: int = 1, rank: int = 0, shard_only: bool = False, pairs=None,
-                 gamma_max: int | None = None):
+                 gamma_max: int | None = None, mode: str = "auto"):
         self.ctx = ctx or _lib.default_context()
         lib = _lib.load()
         mesh = spec.mesh
@@ -197,7 +197,7 @@ class BandStore:
             triangles=self._t.ctypes.data_as(C.POINTER(C.c_int64)), phi=_lib.dptr(self._phi),
             bie=1 if spec.bie == "bmbie" else 0, d=int(spec.basis.d), c=float(spec.c),
             dt=float(spec.basis.dt), nt=self.nt, window=int(self.window), nranks=int(nranks),
-            rank=int(rank))
+            rank=int(rank), mode=_mode(mode))
         self.h = C.c_void_p()
         create = lib.tdw_problem_create_shard if shard_only else lib.tdw_problem_create
         _lib.check(create(self.ctx.h, C.byref(desc), C.byref(self.h)), self.ctx.h,
@@ -294,6 +294,14 @@ class BandStore:
             pass
 
 
+def _mode(mode: str) -> int:
+    """Coefficient mode: "auto" (the banded store when it fits in
+    device memory, else on the fly), "stored", "on_the_fly"."""
+    if mode not in _lib.MODES:
+        raise ValueError(f"unknown coefficient mode {mode!r} (expected one of {sorted(_lib.MODES)})")
+    return _lib.MODES[mode]
+
+
 def problem_key(spec) -> tuple:
     """Everything a device store depends on: geometry, phi, bie, d, c, dt."""
     import hashlib
@@ -322,7 +330,7 @@ def _check_store(mats, spec, window):
 
 
 def build_retarded_matrices(spec, gamma_max: int | None = None, pairs=None, slab: int = 2_000_000,
-                            window: bool = True) -> BandStore:
+                            window: bool = True, mode: str = "auto") -> BandStore:
     """Assemble the device banded store (replaces marching.py:132-181).
 
     `pairs=(ii, jj)` restricts the store -- and the lag-1 step matrix built from
@@ -330,8 +338,11 @@ def build_retarded_matrices(spec, gamma_max: int | None = None, pairs=None, slab
     `gamma_max` is recorded: like the reference's matrix set, a store asked for
     fewer lags than march needs makes march raise ValueError.  The store itself
     always holds the lags of its window (min(gamma*, nt-1), or nt-1 without
-    window).  `slab` (the reference's memory chunking) has no meaning here."""
-    return BandStore(spec, window=window, pairs=pairs, gamma_max=gamma_max).assemble()
+    window).  `slab` (the reference's memory chunking) has no meaning here.
+    `mode`: "auto" keeps the coefficients in the banded store when it fits in
+    device memory and otherwise recomputes them in every convolution pass;
+    "stored" / "on_the_fly" force one of the two."""
+    return BandStore(spec, window=window, pairs=pairs, gamma_max=gamma_max, mode=mode).assemble()
 
 
 class StepSolver:
@@ -381,14 +392,14 @@ def build_step_matrix(spec, mats):
 
 
 def march(spec, window: bool = True, blowup_factor: float = 1e6, mats=None,
-          rhs_trace: list | None = None, device_data: bool = False) -> TimeHistory:
+          rhs_trace: list | None = None, device_data: bool = False, mode: str = "auto") -> TimeHistory:
     """Run the conventional time marching on the GPU (marching.py:292-338).
 
     gamma* and the lag count are computed by the library from the mesh
     (tdw_problem_create), so a supplied store is validated against its own
     record of them."""
     if mats is None:
-        mats = BandStore(spec, window=window)
+        mats = BandStore(spec, window=window, mode=mode)
     elif not isinstance(mats, BandStore):
         raise TypeError("mats must come from build_retarded_matrices of this package")
     else:

@@ -39,6 +39,7 @@ def test_cfg0_matches_reference_everywhere():
     trace = []
     h = marching.march(spec, rhs_trace=trace)
     assert h.status == str(g["status"]) and h.n_steps == int(g["n_steps"])
+    print(f"cfg0 vs reference: worst step {per_step_rel(h.u, g['u']).max():.3e}")
     assert per_step_rel(h.u, g["u"]).max() < 1e-9
     np.testing.assert_array_equal(h.q, g["q"])
     assert per_step_rel(h.tau, g["tau"]).max() < 1e-9
@@ -53,6 +54,7 @@ def test_cfg1_d2_bmbie_matches_reference():
     h = marching.march(spec)
     assert h.status == str(g["status"]) and h.n_steps == int(g["n_steps"])
     err = per_step_rel(h.u[:, g["sub"]], g["unknown_sub"])
+    print(f"cfg1 vs reference: worst step {err.max():.3e} (256-element sample)")
     assert err.max() < TOL[2], err.max()
     for k, b in enumerate(g["full_steps"]):
         ref = g["unknown_full"][k]
@@ -76,6 +78,7 @@ def test_cfg2_full_size_matches_reference():
     h = marching.march(spec)
     assert h.status == str(g["status"]) and h.n_steps == int(g["n_steps"])
     err = per_step_rel(h.q[:, g["sub"]], g["unknown_sub"])
+    print(f"cfg2 vs reference: worst step {err.max():.3e} (256-element sample)")
     assert err.max() < TOL[1], err.max()
     for k, b in enumerate(g["full_steps"]):
         ref = g["unknown_full"][k]
@@ -429,3 +432,26 @@ def test_store_validation():
     with pytest.raises(ValueError, match="cover the required lags"):
         marching.march(spec, mats=short)
     marching.march(spec, mats=store)  # the matching spec still runs
+
+
+@pytest.mark.parametrize("cfg", [0, 1, 2])
+def test_on_the_fly_mode_matches_reference(cfg):
+    """Coefficient mode ON_THE_FLY (SURVEY 8(b) `mode`; north_star (1)): no banded
+    store, every convolution pass re-evaluates the closed forms.  Same reference
+    goldens and tolerances as the stored mode, and agreement with the stored
+    mode to round-off."""
+    spec = scenarios.build_spec(cfg)
+    store = marching.build_retarded_matrices(spec, mode="on_the_fly")
+    inf = store.info()
+    assert inf["coeff_mode"] == 2 and inf["store_bytes"] == 0 and inf["n_band"] > 0
+    h = marching.march(spec, mats=store)
+    g = golden(f"march_cfg{cfg}.npz")
+    assert h.status == str(g["status"]) and h.n_steps == int(g["n_steps"])
+    x = _unknown(h, spec)
+    tol = TOL[spec.basis.d] if spec.bie == "bmbie" else 1e-9
+    assert per_step_rel(x[:, g["sub"]], g["unknown_sub"]).max() < tol
+    hs = marching.march(spec, mode="stored")
+    assert per_step_rel(x, _unknown(hs, spec)).max() < 1e-11   # the same sums, grouped differently
+    ms = store.time_conv(3)
+    print(f"cfg{cfg} on-the-fly pass {ms:.3f} ms (kb = {inf['steps_per_pass']})")
+    store.close()
