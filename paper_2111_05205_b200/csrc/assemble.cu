@@ -560,7 +560,7 @@ struct OtfArgs {
 };
 
 template <int D, bool BM>
-__global__ void __launch_bounds__(128) otf_conv_kernel(OtfArgs a) {
+__global__ void __launch_bounds__(128, TDW_FILL_MINB(D)) otf_conv_kernel(OtfArgs a) {
   if (a.flags[0] != 0) return;
   const int lane = threadIdx.x & 31;
   const long long task = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
