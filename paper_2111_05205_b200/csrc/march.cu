@@ -593,6 +593,7 @@ struct ClusterSolveArgs {
   int guess;                                // 1: start Jacobi from 2 x^(beta-1) - x^(beta-2)
   int check_mask;                           // register solver: convergence test when (it & mask) == 0
   double stop_tol;                          // sweeps stop at max|dx| <= stop_tol max|x| (1e-15)
+  double cheb_rho2;                         // halo solver: Chebyshev acceleration with rho^2 (0: Jacobi)
   // halo solver (communication-avoiding sweeps): per CTA, the computed rows (own
   // rows first, then halo layers 1..h-1) and the gathered rows (layers 1..h)
   int halo;                                 // h (0: plain register solver)
@@ -1049,6 +1050,8 @@ __global__ void __launch_bounds__(reg_threads<MAXNZ>(), 1) solve_halo_kernel(Clu
   double* xs0 = hsm;                   // [hE] extended-set x, double buffer
   double* xs1 = hsm + a.hE;
   double* ex = hsm + 2 * a.hE;         // [2][hT] own rows, exported to peers
+  double* exo = ex + 2 * a.hT;         // [2][hT] own rows' previous iterate (Chebyshev)
+  double* xo = exo + 2 * a.hT;         // [hT] computed halo rows' previous iterate, gathered
   __shared__ unsigned long long chk[3][2];
   __shared__ double shred[64];
   __shared__ double red2[4];
@@ -1100,14 +1103,25 @@ __global__ void __launch_bounds__(reg_threads<MAXNZ>(), 1) solve_halo_kernel(Clu
   double* cur = xs0;
   double* nxt = xs1;
   const int rounds = (a.maxit + H - 1) / H;
+  // Chebyshev semi-iteration on the Jacobi map x -> Gx + c (spectrum of G within
+  // [-rho, rho], rho from the assembly's estimate): x_{k+1} = om_{k+1} (G x_k + c
+  // - x_{k-1}) + x_{k-1}, om_1 = 1, om_2 = 1 / (1 - rho^2 / 2), om_{k+1} = 1 / (1 -
+  // rho^2 om_k / 4).  A polynomial in G like the Jacobi sweeps: the same halo
+  // validity per sweep; the previous iterate of a computed halo row comes from its
+  // owner with the current one.  cheb_rho2 = 0 gives plain Jacobi (om = 1).
+  const bool cheb = a.cheb_rho2 > 0.0;
+  double om = 1.0, xold = own ? xs0[tid] : 0.0;
   for (int rd = 0; rd < rounds; ++rd) {
     // gather layers 1..h from the owners' exported x (parity p)
     for (int g = tid; g < ngat; g += blockDim.x) {
       const int src = __ldg(a.h_gsrc + (size_t)cr * a.hG + g);
+      const int dst = __ldg(a.h_gdst + (size_t)cr * a.hG + g);
       const double* pe = cl.map_shared_rank(ex + p * T, src >> 24);
-      cur[__ldg(a.h_gdst + (size_t)cr * a.hG + g)] = pe[src & 0xffffff];
+      cur[dst] = pe[src & 0xffffff];
+      if (cheb && rd > 0 && dst < ncomp) xo[dst] = cl.map_shared_rank(exo + p * T, src >> 24)[src & 0xffffff];
     }
     __syncthreads();
+    if (cheb && rd > 0 && comp && !own) xold = xo[tid];
     double xn = 0.0, xprev = 0.0;
     for (int s = 1; s <= H; ++s) {
       if (comp && layer <= H - s) {
@@ -1122,8 +1136,13 @@ __global__ void __launch_bounds__(reg_threads<MAXNZ>(), 1) solve_halo_kernel(Clu
         }
         xprev = cur[tid];
         xn = (s0 + s1) * invd;
+        if (cheb) {
+          xn = fma(om, xn - xold, xold);
+          xold = xprev;
+        }
         nxt[tid] = xn;
       }
+      if (cheb) om = sweeps + s == 1 ? 1.0 / (1.0 - 0.5 * a.cheb_rho2) : 1.0 / (1.0 - 0.25 * a.cheb_rho2 * om);
       __syncthreads();
       double* t = cur;
       cur = nxt;
@@ -1133,7 +1152,10 @@ __global__ void __launch_bounds__(reg_threads<MAXNZ>(), 1) solve_halo_kernel(Clu
     const bool last = rd + 1 == rounds;
     const bool check = !last;
     if (check && tid < 2) chk[(ncheck + 1) % 3][tid] = 0ull;
-    if (own) ex[(p ^ 1) * T + tid] = xn;
+    if (own) {
+      ex[(p ^ 1) * T + tid] = xn;
+      if (cheb) exo[(p ^ 1) * T + tid] = xold;
+    }
     if (check) {
       double dmax = own ? fabs(xn - xprev) : 0.0, xmax = own ? fabs(xn) : 0.0;
 #pragma unroll
@@ -1804,6 +1826,11 @@ int make_plan(tdw_problem* pb, LoopPlan& L, double threshold, bool want_rhs) {
   cs.nt = pb->nt;
   cs.R = pb->sp_R;
   cs.maxit = pb->jac_iters;
+  {
+    const char* ce = getenv("TDW_CHEB");  // 0: plain Jacobi sweeps
+    const bool on = !(ce && atoi(ce) == 0) && pb->cheb_rho > 0.0 && pb->cheb_rho < 0.9;
+    cs.cheb_rho2 = on ? pb->cheb_rho * pb->cheb_rho : 0.0;
+  }
   cs.trace = pb->d_trace;
   cs.halo = pb->sp_halo;
   cs.hT = pb->sp_hT;
@@ -2299,6 +2326,46 @@ int tdw_outputs(tdw_problem* pb, double* u, double* q, double* tau, double* sigm
 // (layers 0..h) indexes the CTA's shared-memory x.  The largest h <= 4 that
 // fits the thread count and shared memory is used (env TDW_HALO=0 disables,
 // TDW_HALO=h caps it); h = 1 would equal the plain solver, so h >= 2.
+// Spectral radius of the Jacobi map G = I - D^-1 A, for the Chebyshev sweeps:
+// power iteration (two-step norm ratio: G's extreme eigenvalues come in near +-
+// pairs), raised by 5% and capped by the infinity-norm bound.  A modest
+// underestimate only slows Chebyshev down (eigenvalues just outside the interval
+// still decay), and the loop's residual test guards every step.
+static double jacobi_rho_estimate(const tdw_problem* pb, const std::vector<int>& acol,
+                                  const std::vector<double>& aval) {
+  const int ns = pb->ns, w = pb->ell_w;
+  std::vector<double> dg(ns, 0.0), x(ns), y(ns);
+  for (int i = 0; i < ns; ++i)
+    for (int k = 0; k < w; ++k)
+      if (acol[(size_t)k * ns + i] == i) dg[i] += aval[(size_t)k * ns + i];
+  for (int i = 0; i < ns; ++i) x[i] = 1.0 + 0.5 * std::sin(0.7 * i + 0.3);
+  auto apply = [&](const std::vector<double>& u, std::vector<double>& v) {
+    double n2 = 0.0;
+    for (int i = 0; i < ns; ++i) {
+      double sacc = 0.0;
+      for (int k = 0; k < w; ++k) {
+        const int j = acol[(size_t)k * ns + i];
+        if (j != i) sacc += aval[(size_t)k * ns + i] * u[j];
+      }
+      v[i] = -sacc / dg[i];
+      n2 += v[i] * v[i];
+    }
+    return std::sqrt(n2);
+  };
+  double est = 0.0;
+  for (int it = 0; it < 24; ++it) {
+    double n0 = 0.0;
+    for (double v : x) n0 += v * v;
+    n0 = std::sqrt(n0);
+    if (!(n0 > 0.0)) return 0.0;
+    for (double& v : x) v /= n0;
+    apply(x, y);
+    const double n2 = apply(y, x);  // ||G^2 x|| for ||x|| = 1
+    est = std::sqrt(n2);
+  }
+  return std::min(pb->jac_bound, 1.05 * est);
+}
+
 static int setup_halo(tdw_problem* pb, const std::vector<int>& acol, const std::vector<double>& aval) {
   tdw_ctx* ctx = pb->ctx;
   const int ns = pb->ns, CL = pb->sp_cl, R = pb->sp_R, MZ = pb->sp_reg;
@@ -2394,11 +2461,12 @@ static int setup_halo(tdw_problem* pb, const std::vector<int>& acol, const std::
       return rc;
     TDW_CUDA(ctx, cudaMalloc(&pb->d_h_val, sizeof(double) * h_val.size()));
     TDW_CUDA(ctx, cudaMemcpy(pb->d_h_val, h_val.data(), sizeof(double) * h_val.size(), cudaMemcpyHostToDevice));
+    pb->cheb_rho = jacobi_rho_estimate(pb, acol, aval);
     pb->sp_halo = h;
     pb->sp_hT = T;
     pb->sp_hE = hE;
     pb->sp_hG = hG;
-    pb->sp_hsmem = sizeof(double) * (2 * (size_t)hE + 2 * (size_t)T);
+    pb->sp_hsmem = sizeof(double) * (2 * (size_t)hE + 5 * (size_t)T);
     auto attr = [&](const void* f) {
       return cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pb->sp_hsmem);
     };

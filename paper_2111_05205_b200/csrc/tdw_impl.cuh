@@ -131,6 +131,7 @@ struct tdw_problem {
   double* d_aval = nullptr;
   double* d_adiag = nullptr;
   int jac_iters = 0;
+  double cheb_rho = 0.0;           // Chebyshev bound of the halo solver's sweeps (0: Jacobi)
   bool solver_krylov = false;      // BiCGSTAB solve (Jacobi bound >= 0.9 or TDW_SOLVER=krylov)
   double* d_kw = nullptr;          // [9][ns] Krylov / standalone-solve workspace
   // near structure: pairs whose band reaches a split lag g in 2..nsl+1, all rows,

@@ -194,6 +194,7 @@ def test_halo_solver_is_bit_identical(monkeypatch):
     the plain register solver: with h = 2 and the plain solver testing
     convergence every 2 sweeps, the densities agree bit for bit."""
     spec = scenarios.build_spec(2)
+    monkeypatch.setenv("TDW_CHEB", "0")  # plain Jacobi sweeps in the halo solver
     monkeypatch.setenv("TDW_SOLVER", "reg")
     monkeypatch.setenv("TDW_CHECK_EVERY", "2")
     monkeypatch.setenv("TDW_NEAR_IN_SOLVE", "0")  # both solvers: all near terms in near_step_kernel
@@ -207,6 +208,22 @@ def test_halo_solver_is_bit_identical(monkeypatch):
     hh = marching.march(spec, mats=halo)
     np.testing.assert_array_equal(hh.q, hp.q)
     np.testing.assert_array_equal(hh.u, hp.u)
+
+
+@pytest.mark.parametrize("cfg", [1, 2])
+def test_chebyshev_sweeps_match_jacobi(cfg, monkeypatch):
+    """The halo solver's Chebyshev-accelerated sweeps (default; rho from the
+    assembly's power iteration) converge to the same densities as plain Jacobi
+    sweeps and the reference goldens."""
+    spec = scenarios.build_spec(cfg)
+    h = marching.march(spec)
+    monkeypatch.setenv("TDW_CHEB", "0")
+    hj = marching.march(spec)
+    x, xj = _unknown(h, spec), _unknown(hj, spec)
+    assert per_step_rel(x, xj).max() < 1e-12
+    g = golden(f"march_cfg{cfg}.npz")
+    tol = TOL[spec.basis.d] if spec.bie == "bmbie" else 1e-9
+    assert per_step_rel(x[:, g["sub"]], g["unknown_sub"]).max() < tol
 
 
 def test_lag2_near_terms_in_the_solve(monkeypatch):
