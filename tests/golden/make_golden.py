@@ -13,6 +13,7 @@ the reference itself never does.
     NUMBA_CACHE_DIR=/tmp/nb python tests/golden/make_golden.py tree 4   # two spheres, ~1 min
     NUMBA_CACHE_DIR=/tmp/nb python tests/golden/make_golden.py fmm_ref  # patched reference fast_march
     NUMBA_CACHE_DIR=/tmp/nb python tests/golden/make_golden.py march_pairs  # pairs= restriction
+    NUMBA_CACHE_DIR=/tmp/nb python tests/golden/make_golden.py physics      # sphere series validation
 
 Scenario recipe: SURVEY.md section 8(c)/(d) (icosphere f=4/8/16, c=1,
 c*dt = 0.5 * mean edge, Gaussian plane pulse along z, sigma=4dt, t0=6 sigma).
@@ -213,6 +214,58 @@ def make_march_pairs():
     print("march_pairs_cfg0:", len(ii), "pairs", hist.status, hist.n_steps, np.abs(hist.u).max())
 
 
+def physics_spec(bc, bie, d, frequency=4, nt=64):
+    """The reference's own sphere scenario (reference.py:23-93): icosphere of
+    radius 0.5 at (0.5, 0, 0), plane cosine pulse of length 0.5 along +x1, the
+    scattered field solved with the incident field's data (Neumann: q = -du_in/dn;
+    Dirichlet: u = -u_in), c dt = 0.5 mean edge."""
+    from tdwavebem.reference import IncidentPulse
+    mesh = shapes.icosphere(frequency, radius=0.5, centre=(0.5, 0.0, 0.0))
+    v0, v1, v2 = mesh.element_vertices()
+    dt = 0.5 * float(np.concatenate([np.linalg.norm(v1 - v0, axis=1), np.linalg.norm(v2 - v1, axis=1),
+                                     np.linalg.norm(v0 - v2, axis=1)]).mean())
+    pulse = IncidentPulse(0.5, 1.0)
+    cen, nrm = mesh.centroids, mesh.normals
+    phi = np.full(mesh.n_elements, 1.0 if bc == "neumann" else 0.0)
+    import warnings
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        return marching.ProblemSpec(mesh, phi, bie, BSplineBasis(d, dt), 1.0, nt,
+                                    u_data=(lambda t: -pulse.value(cen, t)) if bc == "dirichlet" else None,
+                                    q_data=(lambda t: -pulse.normal_derivative(cen, nrm, t)) if bc == "neumann" else None)
+
+
+def make_physics():
+    """Physics validation fixture: the reference's march on its
+    sphere scenario, the total field on the arc x2 = 0, x3 >= 0 at the knots, the
+    reference's semi-analytic series there (reference_solution) and the relative
+    L2 error between the two, for Neumann (OBIE d=1, BMBIE d=2) and Dirichlet
+    (BMBIE d=1)."""
+    from tdwavebem import reference as R
+    out = dict(versions=VERSIONS)
+    for bc, bie, d in (("neumann", "obie", 1), ("neumann", "bmbie", 2), ("dirichlet", "bmbie", 1)):
+        spec = physics_spec(bc, bie, d)
+        scen = R.SphereScenario(0.5, (0.5, 0.0, 0.0), bc, 0.5, 1.0)
+        idx = R.arc_evaluation_indices(spec.mesh, scen)
+        hist = marching.march(spec)
+        pulse = R.IncidentPulse(0.5, 1.0)
+        cen, nrm = spec.mesh.centroids[idx], spec.mesh.normals[idx]
+        times = np.arange(spec.nt) * spec.basis.dt
+        if bc == "neumann":
+            num = hist.knot_values("u")[:, idx] + np.array([pulse.value(cen, t) for t in times])
+        else:
+            num = hist.knot_values("q")[:, idx] + np.array([pulse.normal_derivative(cen, nrm, t) for t in times])
+        ref = R.reference_solution(scen, cen, spec.nt, spec.basis.dt)
+        key = f"{bc}_{bie}{d}"
+        out[f"{key}_idx"] = idx
+        out[f"{key}_numerical"] = num
+        out[f"{key}_reference"] = ref
+        out[f"{key}_error"] = R.rel_l2_error(num, ref)
+        out[f"{key}_status"] = hist.status
+        print(key, hist.status, "rel L2 error vs the sphere series", out[f"{key}_error"])
+    np.savez_compressed(OUT / "physics_sphere.npz", **out)
+
+
 def make_tree(cfg, leaf_capacity=20):
     """Octree + interaction lists from the reference build_tree (bit-exact target)."""
     from tdwavebem.fmm_tree import build_tree
@@ -379,6 +432,8 @@ if __name__ == "__main__":
         make_march(int(sys.argv[2]))
     elif what == "tree":
         make_tree(int(sys.argv[2]))
+    elif what == "physics":
+        make_physics()
     elif what == "march_pairs":
         make_march_pairs()
     elif what == "fmm_ref":

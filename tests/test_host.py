@@ -184,3 +184,73 @@ def test_fmm_config_defaults_and_gpu_limits():
     b = fmm_plan.baseline_config()
     assert (b.ps, b.pt, b.leaf_capacity, b.mu) == (4, 4, 20, 8)
     b.check_gpu()
+
+
+def _physics_spec(bc, bie, d, nt=64):
+    """The reference's sphere scenario (tests/golden/make_golden.py physics_spec)."""
+    import warnings
+    from paper_2111_05205_b200.reference import IncidentPulse
+    from paper_2111_05205_b200.tbasis import BSplineBasis
+    mesh = icosphere(4, radius=0.5, centre=(0.5, 0.0, 0.0))
+    v0, v1, v2 = mesh.element_vertices()
+    dt = 0.5 * float(np.concatenate([np.linalg.norm(v1 - v0, axis=1), np.linalg.norm(v2 - v1, axis=1),
+                                     np.linalg.norm(v0 - v2, axis=1)]).mean())
+    pulse = IncidentPulse(0.5, 1.0)
+    cen, nrm = mesh.centroids, mesh.normals
+    phi = np.full(mesh.n_elements, 1.0 if bc == "neumann" else 0.0)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        return marching.ProblemSpec(mesh, phi, bie, BSplineBasis(d, dt), 1.0, nt,
+                                    u_data=(lambda t: -pulse.value(cen, t)) if bc == "dirichlet" else None,
+                                    q_data=(lambda t: -pulse.normal_derivative(cen, nrm, t))
+                                    if bc == "neumann" else None)
+
+
+@pytest.mark.parametrize("bc,bie,d", [("neumann", "obie", 1), ("neumann", "bmbie", 2), ("dirichlet", "bmbie", 1)])
+def test_sphere_reference_matches_the_reference(bc, bie, d):
+    """reference_solution / arc_evaluation_indices / rel_l2_error (reference.py:124-254)
+    reproduce the reference's own values on its sphere scenario
+    (tests/golden/physics_sphere.npz)."""
+    from paper_2111_05205_b200 import reference as R
+    g = golden("physics_sphere.npz")
+    key = f"{bc}_{bie}{d}"
+    spec = _physics_spec(bc, bie, d)
+    scen = R.SphereScenario(0.5, (0.5, 0.0, 0.0), bc, 0.5, 1.0)
+    idx = R.arc_evaluation_indices(spec.mesh, scen)
+    np.testing.assert_array_equal(idx, g[f"{key}_idx"])
+    ref = R.reference_solution(scen, spec.mesh.centroids[idx], spec.nt, spec.basis.dt)
+    gref = g[f"{key}_reference"]
+    assert np.abs(ref - gref).max() <= 1e-10 * np.abs(gref).max()
+    assert abs(R.rel_l2_error(g[f"{key}_numerical"], ref) - float(g[f"{key}_error"])) < 1e-9
+
+
+def test_mesh_loaders_and_orientation(tmp_path):
+    """load_mesh (Gmsh MSH 2 ASCII, Wavefront OBJ) and check_orientation
+    (mesh.py:110-223): round trips, rejected element types, a flipped sphere."""
+    from paper_2111_05205_b200.mesh import check_orientation, load_mesh
+    obj = tmp_path / "tri.obj"
+    obj.write_text("# one triangle\nv 0 0 0\nv 1 0 0\nv 0 1 0\nf 1/1 2/2 -1\n")
+    m = load_mesh(obj)
+    assert m.n_elements == 1
+    np.testing.assert_allclose(m.normals[0], [0, 0, 1])
+    quad = tmp_path / "quad.obj"
+    quad.write_text("v 0 0 0\nv 1 0 0\nv 1 1 0\nv 0 1 0\nf 1 2 3 4\n")
+    with pytest.raises(MeshError, match="non-triangle"):
+        load_mesh(quad)
+    msh = tmp_path / "tri.msh"
+    msh.write_text("$MeshFormat\n2.2 0 8\n$EndMeshFormat\n$Nodes\n3\n7 0 0 0\n9 1 0 0\n8 0 1 0\n$EndNodes\n"
+                   "$Elements\n2\n1 15 2 0 1 7\n2 2 2 0 1 7 9 8\n$EndElements\n")
+    m = load_mesh(msh)
+    assert m.n_elements == 1 and m.areas[0] == pytest.approx(0.5)
+    np.testing.assert_array_equal(m.triangles[0], [0, 2, 1])   # nodes renumbered in id order
+    bad = tmp_path / "quad.msh"
+    bad.write_text("$MeshFormat\n2.2 0 8\n$EndMeshFormat\n$Nodes\n4\n1 0 0 0\n2 1 0 0\n3 1 1 0\n4 0 1 0\n"
+                   "$EndNodes\n$Elements\n1\n1 3 2 0 1 1 2 3 4\n$EndElements\n")
+    with pytest.raises(MeshError, match="non-triangle"):
+        load_mesh(bad)
+    with pytest.raises(MeshError, match="unsupported"):
+        load_mesh(tmp_path / "x.stl")
+    s = icosphere(4)
+    check_orientation(s)
+    with pytest.raises(MeshError):
+        check_orientation(TriMesh(s.vertices, s.triangles[:, ::-1]))
