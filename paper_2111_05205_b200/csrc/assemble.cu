@@ -27,6 +27,8 @@
 
 #include <algorithm>
 #include <climits>
+#include <chrono>
+#include <cstdio>
 #include <cstring>
 #include <cmath>
 
@@ -678,7 +680,14 @@ static int choose_conv_schedule(tdw_problem* pb) {
   return TDW_OK;
 }
 
+// host wall-clock split of tdw_assemble (TDW_TRACE_ASM=1, stderr)
+static double asm_now_ms() {
+  return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
 int tdw_assemble_impl(tdw_problem* pb) {
+  static const bool trace_asm = getenv("TDW_TRACE_ASM") != nullptr;
+  const double tw0 = asm_now_ms();
   tdw_ctx* ctx = pb->ctx;
   cudaStream_t st = ctx->stream;
   cudaEvent_t e0, e1, f0, f1;
@@ -928,7 +937,11 @@ int tdw_assemble_impl(tdw_problem* pb) {
   // cluster solver first: its CTAs' SMs are kept free of convolution CTAs so
   // the far convolution of the next step overlaps the solve
   {
+    const double tw1 = asm_now_ms();
     int src = tdw_setup_cluster_solver(pb);
+    if (trace_asm)
+      fprintf(stderr, "assemble: device part + host readback %.2f ms, solver setup %.2f ms\n", tw1 - tw0,
+              asm_now_ms() - tw1);
     if (src) return src;
   }
   if (pb->otf) {
@@ -1055,6 +1068,7 @@ int tdw_assemble_impl(tdw_problem* pb) {
   }
   pb->store_bytes = (int64_t)(total_bytes + sizeof(unsigned long long) * (nunit + 1) + sizeof(int2) * nunit);
   pb->assembled = true;
+  if (trace_asm) fprintf(stderr, "assemble: total %.2f ms\n", asm_now_ms() - tw0);
   return TDW_OK;
 }
 

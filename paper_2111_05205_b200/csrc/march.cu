@@ -19,7 +19,9 @@
 // each) read one 512-byte row: shared-memory reads without bank conflicts.
 #include <cooperative_groups.h>
 #include <cuda.h>
+#include <cub/cub.cuh>
 #include <cuda_runtime.h>
+#include <chrono>
 #include <cstring>
 #include <nccl.h>
 
@@ -2112,7 +2114,11 @@ int tdw_march_loop(tdw_problem* pb, double threshold, bool want_rhs, bool time_k
   // direct launches if capture is not possible
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
-  bool use_graph = pb->use_graph;
+  // the first loop of a problem runs launch by launch (23 ms on config 2 against
+  // ~30 ms of capture + instantiation): a cold march(spec) does not pay for a
+  // graph it uses once; later loops capture it and reuse it
+  bool use_graph = pb->use_graph && (pb->loop_calls > 0 || pb->graph_exec);
+  ++pb->loop_calls;
   const bool cacheable = !time_kernels;
   if (use_graph && cacheable && pb->graph_exec && pb->graph_thr == threshold &&
       pb->graph_rhs == want_rhs) {
@@ -2326,6 +2332,40 @@ int tdw_outputs(tdw_problem* pb, double* u, double* q, double* tau, double* sigm
 // (layers 0..h) indexes the CTA's shared-memory x.  The largest h <= 4 that
 // fits the thread count and shared memory is used (env TDW_HALO=0 disables,
 // TDW_HALO=h caps it); h = 1 would equal the plain solver, so h >= 2.
+// The solve tail's CSR (lags 2..want+1 of the near structure, nonzero entries,
+// columns packed (owner CTA << 24) | owner-local row for R rows per CTA)
+__global__ void tail_csr_count_kernel(const double* __restrict__ nval, const int* __restrict__ ncnt, int ns,
+                                      int want, int* cnt) {
+  const size_t n = (size_t)want * (ns + 1);
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < n; e += (size_t)gridDim.x * blockDim.x) {
+    const int g = (int)(e / (ns + 1)), s1 = (int)(e % (ns + 1));
+    int c = 0;
+    if (s1 > 0) {
+      const int i = s1 - 1;
+      for (int k = 0; k < ncnt[i]; ++k) c += nval[((size_t)g * TDW_NEAR_MAX + k) * ns + i] != 0.0;
+    }
+    cnt[e] = c;
+  }
+}
+
+__global__ void tail_csr_fill_kernel(const int* __restrict__ ncol, const double* __restrict__ nval,
+                                     const int* __restrict__ ncnt, int ns, int want, int R,
+                                     const int* __restrict__ ptr, int* col, double* val) {
+  const size_t n = (size_t)want * ns;
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < n; e += (size_t)gridDim.x * blockDim.x) {
+    const int g = (int)(e / ns), i = (int)(e % ns);
+    int pos = ptr[(size_t)g * (ns + 1) + i];
+    for (int k = 0; k < ncnt[i]; ++k) {
+      const double w = nval[((size_t)g * TDW_NEAR_MAX + k) * ns + i];
+      if (w == 0.0) continue;
+      const int j = ncol[(size_t)k * ns + i];
+      col[pos] = ((j / R) << 24) | (j % R);
+      val[pos] = w;
+      ++pos;
+    }
+  }
+}
+
 // Spectral radius of the Jacobi map G = I - D^-1 A, for the Chebyshev sweeps:
 // power iteration (two-step norm ratio: G's extreme eigenvalues come in near +-
 // pairs), raised by 5% and capped by the infinity-norm bound.  A modest
@@ -2517,6 +2557,11 @@ static int build_near_compact(tdw_problem* pb, int R) {
 int tdw_setup_cluster_solver(tdw_problem* pb) {
   tdw_ctx* ctx = pb->ctx;
   const int ns = pb->ns;
+  static const bool trace_asm = getenv("TDW_TRACE_ASM") != nullptr;
+  auto now_ms = [] {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+  };
+  const double t0 = now_ms();
   {
     // the Jacobi sweeps contract only for a Jacobi bound < 1 (measured 0.05-0.31 on
     // configs 0-4); from 0.9 on -- or on request (TDW_SOLVER=krylov) -- the loop
@@ -2661,10 +2706,12 @@ int tdw_setup_cluster_solver(tdw_problem* pb) {
   }
   TDW_CUDA(ctx, cudaFuncSetAttribute(solve_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)pb->sp_smem));
+  const double t1 = now_ms();
   if (pb->sp_reg > 0) {
     int rc = setup_halo(pb, acol, aval);
     if (rc) return rc;
   }
+  const double t2 = now_ms();
   // near terms of the first split lags computed in the halo solve's tail
   // (TDW_NEAR_IN_SOLVE = number of lags; each lag costs the solve ~5-10 us on
   // config 2; 0: all in near_step_kernel)
@@ -2677,39 +2724,39 @@ int tdw_setup_cluster_solver(tdw_problem* pb) {
     // near step of step s is then needed only near_tail + 1 solves later
     const int want = std::min(e ? atoi(e) : (pb->kb == 5 ? 3 : (pb->kb >= 6 ? 2 : 1)), pb->nsl);
     if (want > 0 && pb->sp_reg > 0 && pb->sp_halo > 0 && pb->split_lag2 && pb->near_w > 0) {
-      std::vector<int> ncol((size_t)TDW_NEAR_MAX * ns), cnt(ns);
-      std::vector<double> nv((size_t)want * TDW_NEAR_MAX * ns);  // g < want slices of [nsl][TDW_NEAR_MAX][ns]
-      TDW_CUDA(ctx, cudaMemcpy(ncol.data(), pb->d_ncol, sizeof(int) * ncol.size(), cudaMemcpyDeviceToHost));
-      TDW_CUDA(ctx, cudaMemcpy(nv.data(), pb->d_nval, sizeof(double) * nv.size(), cudaMemcpyDeviceToHost));
-      TDW_CUDA(ctx, cudaMemcpy(cnt.data(), pb->d_ncnt, sizeof(int) * ns, cudaMemcpyDeviceToHost));
-      std::vector<int> ptr((size_t)want * (ns + 1), 0), col;
-      std::vector<double> val;
-      for (int g = 0; g < want; ++g) {
-        int* pg = &ptr[(size_t)g * (ns + 1)];
-        pg[0] = (int)col.size();
-        for (int i = 0; i < ns; ++i) {
-          for (int k = 0; k < cnt[i]; ++k) {
-            const double w = nv[((size_t)g * TDW_NEAR_MAX + k) * ns + i];
-            if (w == 0.0) continue;
-            const int j = ncol[(size_t)k * ns + i];
-            col.push_back(((j / R) << 24) | (j % R));
-            val.push_back(w);
-          }
-          pg[i + 1] = (int)col.size();
-        }
-      }
-      TDW_CUDA(ctx, cudaMalloc(&pb->d_n2_ptr, sizeof(int) * ptr.size()));
-      TDW_CUDA(ctx, cudaMalloc(&pb->d_n2_col, sizeof(int) * std::max<size_t>(1, col.size())));
-      TDW_CUDA(ctx, cudaMalloc(&pb->d_n2_val, sizeof(double) * std::max<size_t>(1, val.size())));
-      TDW_CUDA(ctx, cudaMemcpy(pb->d_n2_ptr, ptr.data(), sizeof(int) * ptr.size(), cudaMemcpyHostToDevice));
-      if (!col.empty()) {
-        TDW_CUDA(ctx, cudaMemcpy(pb->d_n2_col, col.data(), sizeof(int) * col.size(), cudaMemcpyHostToDevice));
-        TDW_CUDA(ctx, cudaMemcpy(pb->d_n2_val, val.data(), sizeof(double) * val.size(), cudaMemcpyHostToDevice));
-      }
+      // on the device: per (lag, row) the nonzero count, one inclusive scan over
+      // [want][ns + 1] (a zero at each lag's slot 0) gives the row pointers with
+      // global offsets, then the fill in the near structure's column order
+      int* d_cnt = nullptr;
+      const size_t nptr = (size_t)want * (ns + 1);
+      TDW_CUDA(ctx, cudaMalloc(&pb->d_n2_ptr, sizeof(int) * nptr));
+      TDW_CUDA(ctx, cudaMalloc(&d_cnt, sizeof(int) * nptr));
+      const int blocks = (int)std::min<size_t>(4096, (nptr + 255) / 256);
+      tail_csr_count_kernel<<<blocks, 256, 0, ctx->stream>>>(pb->d_nval, pb->d_ncnt, ns, want, d_cnt);
+      TDW_CUDA(ctx, cudaGetLastError());
+      size_t tmp_bytes = 0;
+      cub::DeviceScan::InclusiveSum(nullptr, tmp_bytes, d_cnt, pb->d_n2_ptr, (int)nptr, ctx->stream);
+      void* tmp = nullptr;
+      TDW_CUDA(ctx, cudaMalloc(&tmp, std::max<size_t>(1, tmp_bytes)));
+      cub::DeviceScan::InclusiveSum(tmp, tmp_bytes, d_cnt, pb->d_n2_ptr, (int)nptr, ctx->stream);
+      TDW_CUDA(ctx, cudaGetLastError());
+      int total = 0;
+      TDW_CUDA(ctx, cudaMemcpyAsync(&total, pb->d_n2_ptr + nptr - 1, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+      TDW_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+      cudaFree(tmp);
+      cudaFree(d_cnt);
+      TDW_CUDA(ctx, cudaMalloc(&pb->d_n2_col, sizeof(int) * std::max(1, total)));
+      TDW_CUDA(ctx, cudaMalloc(&pb->d_n2_val, sizeof(double) * std::max(1, total)));
+      tail_csr_fill_kernel<<<blocks, 256, 0, ctx->stream>>>(pb->d_ncol, pb->d_nval, pb->d_ncnt, ns, want, R,
+                                                            pb->d_n2_ptr, pb->d_n2_col, pb->d_n2_val);
+      TDW_CUDA(ctx, cudaGetLastError());
       pb->near_in_solve = true;
       pb->near_tail = want;
     }
   }
+  if (trace_asm)
+    fprintf(stderr, "solver setup: partition + near compact %.2f ms, halo %.2f ms, solve-tail CSR %.2f ms\n",
+            t1 - t0, t2 - t1, now_ms() - t2);
   if (CL > 8) {
     TDW_CUDA(ctx, cudaFuncSetAttribute(solve_halo_kernel<8>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     TDW_CUDA(ctx, cudaFuncSetAttribute(solve_halo_kernel<16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));

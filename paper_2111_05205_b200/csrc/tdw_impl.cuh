@@ -200,6 +200,7 @@ struct tdw_problem {
   int *d_h_col = nullptr, *d_h_ngat = nullptr, *d_h_gdst = nullptr, *d_h_gsrc = nullptr;
   double* d_h_val = nullptr;
   bool use_graph = true;
+  int loop_calls = 0;               // time loops run on this problem (the first one is not captured)
   double t_assemble_ms = 0.0, t_fill_ms = 0.0;
 };
 

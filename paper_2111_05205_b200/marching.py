@@ -243,9 +243,9 @@ class BandStore:
         """Page-locked (nt-1, ns) host buffer for the u (0) / q (1) samples, owned by the store."""
         if not hasattr(self, "_pinned"):
             self._pinned = [None, None]
-        if self._pinned[which] is None:
-            self._pinned[which] = _lib.PinnedArray((self.nt - 1, self.ns))
-        return self._pinned[which].array
+        if self._pinned[which] is None:  # from the page-locked pool (cold stores skip cudaHostAlloc)
+            self._pinned[which] = _lib.pinned_empty((self.nt - 1, self.ns))
+        return self._pinned[which]
 
     # benchmark helpers (device-resident inputs/outputs)
     def upload_known(self, u_known, q_known):
