@@ -17,6 +17,8 @@
  *   tdw_upload_known_rows + tdw_march_device_known
  *                       <- marching.march, pipelined form           marching.py:292-338
  *                          (known rows copied as they are sampled)
+ *   tdw_tree_build (+ _info/_level/_near/_extra/_destroy)
+ *                       <- fmm_tree.build_tree (device-side tree)  fmm_tree.py:73-231
  *   tdw_fmm_setup       <- fmm.fast_march's operator setup          fmm.py:165-531 (corrected,
  *                          (then tdw_assemble / tdw_march)          SURVEY 8(c)), fmm.py:534-544
  *   tdw_march_resident  <- same time loop, inputs/outputs resident on the device (benchmark form)
@@ -253,6 +255,23 @@ typedef struct {
 } tdw_fmm_desc;
 
 int tdw_fmm_setup(tdw_problem* pb, const tdw_fmm_desc* desc);
+
+/* fmm_tree.build_tree (fmm_tree.py:73-231) on the device, bit-exact: octree over
+ * the centroids (ns, 3) with leaf capacity Z, interaction lists, near pairs of
+ * adjacent leaf cells, the mu-interval causality check (TDW_ERR_INVALID_ARG with
+ * the reference's message) and the marginal element pairs (corrected = 1: SURVEY
+ * 8(c) correction 7).  rho = max element radius.  Results are read back with
+ * tdw_tree_info / _level / _near / _extra (int64, caller's element order). */
+typedef struct tdw_tree tdw_tree;
+int tdw_tree_build(tdw_ctx* ctx, int ns, const double* centroids, double rho, double c, double dt,
+                   int leaf_capacity, int mu, int max_depth, int corrected, tdw_tree** out);
+int tdw_tree_info(const tdw_tree* t, int* leaf, double* centre3, double* root_half, int64_t* cells,
+                  int64_t* nil, int64_t* n_near, int* n_extra);
+int tdw_tree_level(const tdw_tree* t, int level, int64_t* coords, int64_t* parent, int64_t* elem_cell,
+                   int64_t* il_obs, int64_t* il_src, int64_t* il_off);
+int tdw_tree_near(const tdw_tree* t, int64_t* ii, int64_t* jj);
+int tdw_tree_extra(const tdw_tree* t, int k, int* level, int64_t* n, int64_t* ii, int64_t* jj);
+int tdw_tree_destroy(tdw_tree* t);
 
 /* Test harness of the row-sharded path on ONE device: create the shard of rank
  * desc->rank of desc->nranks without a communicator, then run all shards in one

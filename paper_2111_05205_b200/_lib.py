@@ -90,6 +90,13 @@ EXPORTS = {
     "tdw_fmm_setup": ([C.c_void_p, C.c_void_p], C.c_int),
     "tdw_problem_create_shard": ([C.c_void_p, C.POINTER(ProblemDesc), C.POINTER(C.c_void_p)], C.c_int),
     "tdw_march_emulated": ([C.POINTER(C.c_void_p), C.c_int, C.c_double], C.c_int),
+    "tdw_tree_build": ([C.c_void_p, C.c_int, _dp, C.c_double, C.c_double, C.c_double, C.c_int, C.c_int, C.c_int,
+                        C.c_int, C.POINTER(C.c_void_p)], C.c_int),
+    "tdw_tree_info": ([C.c_void_p, _i32p, _dp, _dp, _i64p, _i64p, _i64p, _i32p], C.c_int),
+    "tdw_tree_level": ([C.c_void_p, C.c_int, _i64p, _i64p, _i64p, _i64p, _i64p, _i64p], C.c_int),
+    "tdw_tree_near": ([C.c_void_p, _i64p, _i64p], C.c_int),
+    "tdw_tree_extra": ([C.c_void_p, C.c_int, _i32p, _i64p, _i64p, _i64p], C.c_int),
+    "tdw_tree_destroy": ([C.c_void_p], C.c_int),
     "tdw_nccl_unique_id": ([C.c_char_p], C.c_int),
     "tdw_comm_init": ([C.c_void_p, C.c_char_p, C.c_int, C.c_int], C.c_int),
 }

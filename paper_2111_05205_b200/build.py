@@ -11,7 +11,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 OUT = PKG / "libtdw.so"
-SOURCES = ["coeff_table.cu", "assemble.cu", "march.cu", "fmm.cu", "capi.cu", "diag.cu"]
+SOURCES = ["coeff_table.cu", "assemble.cu", "march.cu", "fmm.cu", "capi.cu", "diag.cu", "tree.cu"]
 
 
 def nccl_dirs():

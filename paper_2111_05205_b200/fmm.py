@@ -92,7 +92,7 @@ class FmmStore(BandStore):
         if plan is None:
             (config or FmmConfig()).check_gpu()
         super().__init__(spec, window=True, ctx=ctx, nranks=nranks, rank=rank, shard_only=shard_only)
-        self.plan = plan or build_plan(spec, config)
+        self.plan = plan or build_plan(spec, config, tree="device")
         A = fmm_desc_arrays(self.plan, spec.nt)
         self._arrays = A
         p = self.plan

@@ -157,12 +157,29 @@ class FmmPlan:
     scheme_t: object = None
 
 
-def build_plan(spec, config: FmmConfig | None = None) -> FmmPlan:
+def _gpu_visible() -> bool:
+    try:
+        from . import _lib
+        return _lib.load().tdw_device_count() > 0
+    except Exception:
+        return False
+
+
+def build_plan(spec, config: FmmConfig | None = None, tree: str = "auto") -> FmmPlan:
+    """tree: "device" (csrc/tree.cu, the GPU fast solver's default), "host"
+    (fmm_tree.build_tree, numpy; the CPU oracle's), or "auto" (device when a GPU
+    is visible).  Both builders give the same tree bit for bit."""
     cfg = config or FmmConfig()
     mesh = spec.mesh
     d, c, dt = spec.basis.d, spec.c, spec.basis.dt
     ps, pt, mu = cfg.ps, cfg.pt, cfg.mu
-    tree = build_tree(mesh, c, dt, cfg.leaf_capacity, mu, corrected=True)
+    if tree not in ("auto", "device", "host"):
+        raise ValueError(f"unknown tree builder {tree!r}")
+    if tree == "device" or (tree == "auto" and _gpu_visible()):
+        from .fmm_tree import build_tree_device
+        tree = build_tree_device(mesh, c, dt, cfg.leaf_capacity, mu, corrected=True)
+    else:
+        tree = build_tree(mesh, c, dt, cfg.leaf_capacity, mu, corrected=True)
     sch_s, sch_t = InterpScheme(ps), InterpScheme(pt)
     plan = FmmPlan(cfg, tree, d, c, dt, spec.bie, ps, pt, mu, tree.leaf_level,
                    scheme_s=sch_s, scheme_t=sch_t)
