@@ -48,7 +48,7 @@ def main(cfg: int):
     np.savez_compressed(
         OUT / f"fmm_cfg{cfg}.npz", cfg=cfg, status=r["status"], n_steps=r["n_steps"],
         unknown_norm=np.linalg.norm(x, axis=1), rhs_norm=np.linalg.norm(r["rhs"], axis=1),
-        sub=sub, unknown_sub=x[:, sub], rhs_sub=r["rhs"][:, sub], full_steps=full_steps,
+        sub=sub, unknown_sub=x[:, sub], full_steps=full_steps,
         unknown_full=x[full_steps], t_plan=t_plan, t_setup=t_setup, t_run=t_run,
         note="oracle/fmm_oracle.py (corrected restatement), ps=pt=4, Z=20, mu=8")
     print(f"cfg{cfg}: {r['status']} {r['n_steps']} steps, plan {t_plan:.1f} s, setup {t_setup:.1f} s, "
