@@ -222,18 +222,20 @@ def run_reference(args, world, rank):
 
 
 def m2l_flops(plan, nt: int, d: int) -> float:
-    """M2L GEMM FLOPs of the whole FMM loop: per level tick 2 * 256 * (nops * 256) per
-    interaction pair this rank evaluates (nops = mu + 1 + d stacked operators); level
-    leaf - j ticks when the low j bits of the leaf tick are all 1 (csrc/fmm.cu tick())."""
+    """Executed M2L FLOPs of the whole FMM loop: per interaction pair and level tick
+    2 * 256 * (64 NT + 256 d) -- the NT = (mu+1)(pt-1)+1 distinct near-future time
+    offsets (shared rows of consecutive lags) plus the d derivative operators
+    (csrc/fmm.cu m2l_dmma_kernel); level leaf - j ticks when the low j bits of the
+    leaf tick are all 1 (csrc/fmm.cu tick())."""
     from paper_2111_05205_b200 import fmm_plan
     sch = fmm_plan.step_schedule(plan, nt)
     n_ticks = int(sch["ticks_before"][nt - 1]) + 1
-    nops = plan.mu + 1 + d
+    rows = 64 * ((plan.mu + 1) * (plan.pt - 1) + 1) + 256 * d
     total = 0.0
     for L, lev in plan.levels.items():
         j = plan.leaf - L
         ticks = sum(1 for k in range(n_ticks) if (k & ((1 << j) - 1)) == (1 << j) - 1)
-        total += 2.0 * 256 * nops * 256 * len(lev.il_obs) * ticks
+        total += 2.0 * 256 * rows * len(lev.il_obs) * ticks
     return total
 
 

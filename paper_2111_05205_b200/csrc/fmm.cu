@@ -284,23 +284,73 @@ __global__ void build_kop_kernel(const double* __restrict__ K0, const double* __
 // same additions in the same order as one scatter per group
 // (g_dark != null: rows of a pair's dark lags were not computed -- skipped, as the
 // reference skips dark lags, fmm.py:343-346)
+// tau_rows: Y in m2l_dmma_kernel's layout (64 NT shared near-future rows (a, tau),
+// then the derivative operators); 0: one 256-row block per operator (cuBLAS path)
 __global__ void scatter_all_kernel(const int* __restrict__ t_cells, const int* __restrict__ t_ptr,
                                    const int* __restrict__ t_pair, const unsigned* __restrict__ g_dark,
                                    const double* __restrict__ Y, int nops, int mu, int k, int ncell,
-                                   double* own, double* tmp) {
+                                   double* own, double* tmp, int tau_rows) {
   const int ring = mu + 3;
-  const long long M = (long long)nops * FND;
+  const int d = nops - mu - 1, NT = (mu + 1) * (FPT - 1) + 1;
+  const long long M = tau_rows ? 64LL * NT + (long long)d * FND : (long long)nops * FND;
   const int cell = t_cells[blockIdx.x], op = blockIdx.y, idx = threadIdx.x;
   double* dst = op <= mu ? own + ((size_t)((k + op + 1) % ring) * ncell + cell) * FND + idx
                          : tmp + ((size_t)(op - mu - 1) * ncell + cell) * FND + idx;
+  // this thread's row of operator op: lag op+1's (a, m) is the shared row (a, tau =
+  // m + 3 (op + 1)), stored at a NT + tau - 3
+  const long long yr = !tau_rows ? (long long)op * FND + idx
+                                 : (op <= mu ? (long long)(idx >> 2) * NT + (FPT - 1) * op + (idx & 3)
+                                             : 64LL * NT + (long long)(op - mu - 1) * FND + idx);
   double acc = *dst;
   for (int q = t_ptr[cell]; q < t_ptr[cell + 1]; ++q) {
     const int pq = t_pair[q];
     if (g_dark && op <= mu && ((__ldg(g_dark + pq) >> op) & 1u)) continue;
-    acc += __ldg(Y + (long long)pq * M + (long long)op * FND + idx);
+    acc += __ldg(Y + (long long)pq * M + yr);
   }
   *dst = acc;
 }
+// The level's M2L outputs (m2l_dmma_kernel layout) summed into the target cells,
+// coalesced: thread = one row j of Y (consecutive threads read consecutive rows),
+// looping over the cell's pairs in group order.  A shared near-future row (a, tau)
+// feeds lag tau/3's row m = tau%3 and, when tau%3 == 0, lag tau/3 - 1's row m = 3:
+// each destination has exactly one owner thread, and every destination receives
+// its additions in the same order as one scatter per operator would (bit-identical).
+__global__ void scatter_tau_kernel(const int* __restrict__ t_cells, const int* __restrict__ t_ptr,
+                                   const int* __restrict__ t_pair, const unsigned* __restrict__ g_dark,
+                                   const double* __restrict__ Y, int d, int mu, int k, int ncell, double* own,
+                                   double* tmp) {
+  const int ring = mu + 3, NT = (mu + 1) * (FPT - 1) + 1;
+  const long long M = 64LL * NT + (long long)d * FND;
+  const int cell = t_cells[blockIdx.x];
+  const int j = blockIdx.y * blockDim.x + threadIdx.x;
+  if (j >= M) return;
+  const int q0 = t_ptr[cell], q1 = t_ptr[cell + 1];
+  if (j >= 64 * NT) {  // derivative operators
+    const int p = (j - 64 * NT) / FND, idx = (j - 64 * NT) % FND;
+    double* dst = tmp + ((size_t)p * ncell + cell) * FND + idx;
+    double acc = *dst;
+    for (int q = q0; q < q1; ++q) acc += __ldg(Y + (long long)t_pair[q] * M + j);
+    *dst = acc;
+    return;
+  }
+  const int a = j / NT, tau = (FPT - 1) + j % NT;
+  const int l1 = min(mu + 1, tau / (FPT - 1));       // lag with row m1 = tau - 3 l1 in 0..2 (or 3 at the top)
+  const int m1 = tau - (FPT - 1) * l1;
+  const bool two = m1 == 0 && l1 >= 2;               // also lag l1 - 1, row m = 3
+  double* d1 = own + ((size_t)((k + l1) % ring) * ncell + cell) * FND + a * FPT + m1;
+  double* d2 = two ? own + ((size_t)((k + l1 - 1) % ring) * ncell + cell) * FND + a * FPT + (FPT - 1) : nullptr;
+  double acc1 = *d1, acc2 = two ? *d2 : 0.0;
+  for (int q = q0; q < q1; ++q) {
+    const int pq = t_pair[q];
+    const unsigned dk = __ldg(g_dark + pq);
+    const double y = __ldg(Y + (long long)pq * M + j);
+    if (!((dk >> (l1 - 1)) & 1u)) acc1 += y;
+    if (two && !((dk >> (l1 - 2)) & 1u)) acc2 += y;
+  }
+  *d1 = acc1;
+  if (two) *d2 = acc2;
+}
+
 __global__ void gather_kernel(const int* __restrict__ g_src, long long nil,
                               const double* __restrict__ mom, double* X) {
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < nil * FND;
@@ -374,23 +424,31 @@ m2l_dmma_kernel(const int4* __restrict__ items, const double* __restrict__ K0, c
     }
   }
   __syncthreads();
-  const int nops = mu + 1 + D, lane = tid & 31, warp = tid >> 5;
-  const unsigned dk = dark[o];
+  const int lane = tid & 31, warp = tid >> 5;
+  // Rows of the contraction: the near-future lags l = 1..mu+1 read the time
+  // differences m - n + l (pt - 1) of K0, and lag l's row m = pt-1 is lag l+1's
+  // row m = 0: the (mu+1) pt rows per spatial node have only NT = (mu+1)(pt-1)+1
+  // distinct time offsets tau = m + l (pt-1).  Each is computed once: rows
+  // (a, tau) for a in 0..63, tau in pt-1 .. (mu+2)(pt-1) (64 NT rows; the
+  // scatter reads both lags from the shared row -- the same products, 18% fewer
+  // FLOPs at mu = 8), then the d derivative operators (a, m) (256 rows each).
+  const int NT = (mu + 1) * (FPT - 1) + 1;
+  const int nnear = 2 * NT;                  // 32-row blocks of the near-future rows (64 NT / 32)
   const int lr = lane >> 2, lc = lane & 3;  // fragment row / column of this lane
-  const int nblk = nops * (FND / 32);        // 32-row blocks of the stacked operator
+  const int nblk = nnear + D * (FND / 32);
+  const long long M = 64LL * NT + (long long)D * FND;
   for (int blk = warp; blk < nblk; blk += M2L_WARPS) {
-    const int op = blk >> 3, r0 = (blk & 7) * 32;  // rows r0..r0+31 of operator op
-    if (op <= mu && ((dk >> op) & 1u)) continue;   // dark lag: the reference skips it too
-    const double* Tb;
-    int ld, toff;
-    if (op <= mu) { Tb = T0; ld = ntau0; toff = (op + 1) * (FPT - 1); }
-    else { Tb = Tp + (size_t)(op - mu - 1) * tp_stride; ld = ntaup; toff = FPT - 1; }
-    // row part of the A address per m8 tile: (S(a) + 171) * ld + m + toff
+    const bool nearf = blk < nnear;
+    const int r0 = nearf ? blk * 32 : (blk - nnear) % 8 * 32;
+    const double* Tb = nearf ? T0 : Tp + (size_t)((blk - nnear) / 8) * tp_stride;
+    const int ld = nearf ? ntau0 : ntaup;
+    // row part of the A address per m8 tile: (S(a) + 171) * ld + time offset
     int rowp[4];
 #pragma unroll
     for (int t = 0; t < 4; ++t) {
       const int row = r0 + 8 * t + lr;
-      rowp[t] = (m2l_S(row >> 2) + 171) * ld + (row & 3) + toff;
+      rowp[t] = nearf ? (m2l_S(row / NT) + 171) * ld + (FPT - 1) + row % NT
+                      : (m2l_S(row >> 2) + 171) * ld + (row & 3) + (FPT - 1);
     }
     double acc[4][4][2];
 #pragma unroll
@@ -411,15 +469,15 @@ m2l_dmma_kernel(const int4* __restrict__ items, const double* __restrict__ K0, c
 #pragma unroll
         for (int u = 0; u < 4; ++u) dmma884(acc[t][u][0], acc[t][u][1], af[t], bf[u]);
     }
-    // epilogue: C[row lr][col 2 lc + i] of tile (t, u) -> Y[pair][op * 256 + row]
-    const long long M = (long long)nops * FND;
+    // epilogue: C[row lr][col 2 lc + i] of tile (t, u) -> Y[pair][block row]
+    const long long yrow = nearf ? (long long)r0 : 64LL * NT + (long long)(blk - nnear) * 32;
 #pragma unroll
     for (int u = 0; u < 4; ++u)
 #pragma unroll
       for (int i = 0; i < 2; ++i) {
         const int col = u * 8 + 2 * lc + i;
         if (col >= np) continue;
-        double* yc = Y + (long long)(p0 + col) * M + (long long)op * FND + r0 + lr;
+        double* yc = Y + (long long)(p0 + col) * M + yrow + lr;
 #pragma unroll
         for (int t = 0; t < 4; ++t) yc[8 * t] = acc[t][u][i];
       }
@@ -730,9 +788,9 @@ extern "C" int tdw_fmm_setup(tdw_problem* pb, const tdw_fmm_desc* fd) {
             items.push_back(make_int4(o, (int)q, (int)std::min<long long>(M2L_NC, grp[o + 1] - q), 0));
         }
         V.n_items = (int)items.size();
-        for (int o = 0; o < V.noff; ++o)
-          V.m2l_flops += 2.0 * FND * FND * (double)(grp[o + 1] - grp[o]) *
-                         (double)(F->mu + 1 + d - __builtin_popcount(dark[o]));
+        // executed FLOPs: 64 NT shared near-future rows + d * 256 derivative rows per pair
+        const double rows = 64.0 * ((F->mu + 1) * (FPT - 1) + 1) + (double)d * FND;
+        V.m2l_flops = 2.0 * FND * rows * (double)nkeep;
         if ((rc = up(ctx, &V.items, items.data(), std::max<size_t>(1, items.size())))) return rc;
         if ((rc = up(ctx, &V.g_dark, gd.data(), gd.size()))) return rc;
       }
@@ -918,8 +976,12 @@ int launch_m2l(tdw_problem* pb, FmmLevel& V, int k, cudaStream_t st) {
     m2l_launch(d, V, F, smem, st);
     TDW_CUDA(ctx, cudaGetLastError());
     if (V.n_tcell > 0)
-      scatter_all_kernel<<<dim3(V.n_tcell, nops), FND, 0, st>>>(V.t_cells, V.t_ptr, V.t_pair, V.g_dark, F->Y,
-                                                                 nops, F->mu, k, V.ncell, V.own, V.tmp);
+    {
+      const int NT = (F->mu + 1) * (FPT - 1) + 1;
+      const int rows = 64 * NT + d * FND;
+      scatter_tau_kernel<<<dim3(V.n_tcell, (rows + 255) / 256), 256, 0, st>>>(V.t_cells, V.t_ptr, V.t_pair, V.g_dark,
+                                                                            F->Y, d, F->mu, k, V.ncell, V.own, V.tmp);
+    }
     TDW_CUDA(ctx, cudaGetLastError());
   } else if (V.nil > 0) {
     gather_kernel<<<(int)std::min<long long>(4096, (V.nil * FND + 255) / 256), 256, 0, st>>>(
@@ -947,7 +1009,7 @@ int launch_m2l(tdw_problem* pb, FmmLevel& V, int k, cudaStream_t st) {
     }
     if (V.n_tcell > 0)
       scatter_all_kernel<<<dim3(V.n_tcell, nops), FND, 0, st>>>(V.t_cells, V.t_ptr, V.t_pair, nullptr, F->Y,
-                                                                 nops, F->mu, k, V.ncell, V.own, V.tmp);
+                                                                 nops, F->mu, k, V.ncell, V.own, V.tmp, 0);
     TDW_CUDA(ctx, cudaGetLastError());
   }
   const size_t cs = (size_t)V.ncell * FND;
