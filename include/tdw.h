@@ -14,6 +14,9 @@
  *                          + build_step_matrix                    marching.py:279-289
  *   tdw_march           <- marching.march (+greville inputs,      marching.py:292-338
  *                          TimeHistory outputs)                   marching.py:184-276
+ *   tdw_march_stream_begin / _finish
+ *                       <- marching.march with the Greville sampling  marching.py:258-338
+ *                          overlapped with the loop (chunked, mapped buffers)
  *   tdw_upload_known_rows + tdw_march_device_known
  *                       <- marching.march, pipelined form           marching.py:292-338
  *                          (known rows copied as they are sampled)
@@ -178,6 +181,19 @@ int tdw_march(tdw_problem* pb, const double* u_known, const double* q_known, dou
 int tdw_upload_known_rows(tdw_problem* pb, int which, int beta0, int nbeta, const double* src);
 int tdw_march_device_known(tdw_problem* pb, double threshold, double* u, double* q, double* tau,
                            double* sigma, double* rhs_trace, int32_t* n_steps, int32_t* status);
+
+/* Streamed form of tdw_march (marching.py:292-338 with the Greville sampling of
+ * :258-276 overlapped): the loop is launched at once; the caller samples the known
+ * data into page-locked buffers from tdw_host_alloc (u_host / q_host; NULL = that
+ * callable is None, zeros), step by step, and after every `chunk` steps stores the
+ * number of complete chunks in *flag (a page-locked int32; -1 aborts the loop, e.g.
+ * when a data callable raised).  The device copies each chunk in as soon as its
+ * flag is seen; tdw_march_stream_finish waits and returns the outputs and errors of
+ * tdw_march.  Direct path only (not FMM problems). */
+int tdw_march_stream_begin(tdw_problem* pb, double threshold, int want_rhs, const double* u_host,
+                           const double* q_host, int chunk, int32_t* flag);
+int tdw_march_stream_finish(tdw_problem* pb, double* u, double* q, double* tau, double* sigma,
+                            double* rhs_trace, int32_t* n_steps, int32_t* status);
 
 /* Device-side boundary data (no reference counterpart): the
  * Greville samples of the incident Gaussian plane pulse exp(-((t - z - t0)/sig)^2)

@@ -80,6 +80,9 @@ EXPORTS = {
     "tdw_upload_known": ([C.c_void_p, _dp, _dp], C.c_int),
     "tdw_upload_known_rows": ([C.c_void_p, C.c_int, C.c_int, C.c_int, _dp], C.c_int),
     "tdw_known_plane_pulse": ([C.c_void_p, C.c_int, _dp, _dp, C.c_double, C.c_double], C.c_int),
+    "tdw_march_stream_begin": ([C.c_void_p, C.c_double, C.c_int, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p],
+                               C.c_int),
+    "tdw_march_stream_finish": ([C.c_void_p, _dp, _dp, _dp, _dp, _dp, _i32p, _i32p], C.c_int),
     "tdw_march_device_known": ([C.c_void_p, C.c_double, _dp, _dp, _dp, _dp, _dp, _i32p, _i32p], C.c_int),
     "tdw_march_resident": ([C.c_void_p, C.c_double, C.c_int, C.c_int, C.POINTER(Timing)], C.c_int),
     "tdw_download": ([C.c_void_p, _dp, _dp, _dp, _dp, _i32p, _i32p], C.c_int),

@@ -50,7 +50,9 @@ int tdw_device_count(void) {
 int tdw_host_alloc(int64_t bytes, void** out) {
   if (!out || bytes <= 0) return TDW_ERR_INVALID_ARG;
   *out = nullptr;
-  return cudaHostAlloc(out, (size_t)bytes, cudaHostAllocPortable) == cudaSuccess ? TDW_OK : TDW_ERR_CUDA;
+  // mapped: the streamed march reads the known-data samples in place
+  return cudaHostAlloc(out, (size_t)bytes, cudaHostAllocPortable | cudaHostAllocMapped) == cudaSuccess
+             ? TDW_OK : TDW_ERR_CUDA;
 }
 
 int tdw_host_free(void* p) {
@@ -464,6 +466,47 @@ int tdw_march_device_known(tdw_problem* pb, double threshold, double* u, double*
   return tdw_march(pb, nullptr, nullptr, threshold, u, q, tau, sigma, rhs_trace, n_steps, status);
 }
 
+// Streamed march: launch the loop now, the host fills the page-locked sample
+// buffers (u_host / q_host from tdw_host_alloc, NULL = that datum is zero) chunk by
+// chunk and publishes the number of complete chunks of `chunk` steps in *flag
+// (page-locked int, -1 aborts); then tdw_march_stream_finish.
+int tdw_march_stream_begin(tdw_problem* pb, double threshold, int want_rhs, const double* u_host,
+                           const double* q_host, int chunk, int32_t* flag) {
+  if (!pb || !flag || chunk < 1) return TDW_ERR_INVALID_ARG;
+  tdw_ctx* ctx = pb->ctx;
+  cudaSetDevice(ctx->device);
+  if (pb->stream_in_flight) return tdw_fail(ctx, TDW_ERR_STATE, "a streamed march is already in flight");
+  if (pb->fmm) return tdw_fail(ctx, TDW_ERR_STATE, "streamed march: direct path only");
+  const size_t n = (size_t)(pb->nt - 1) * pb->ns;
+  if (!pb->d_uk) TDW_CUDA(ctx, cudaMalloc(&pb->d_uk, sizeof(double) * n));
+  if (!pb->d_qk) TDW_CUDA(ctx, cudaMalloc(&pb->d_qk, sizeof(double) * n));
+  void* dp = nullptr;
+  pb->h_uk_dev = pb->h_qk_dev = nullptr;
+  if (u_host) { TDW_CUDA(ctx, cudaHostGetDevicePointer(&dp, (void*)u_host, 0)); pb->h_uk_dev = (const double*)dp; }
+  if (q_host) { TDW_CUDA(ctx, cudaHostGetDevicePointer(&dp, (void*)q_host, 0)); pb->h_qk_dev = (const double*)dp; }
+  TDW_CUDA(ctx, cudaHostGetDevicePointer(&dp, (void*)flag, 0));
+  pb->h_flag_dev = (const volatile int*)dp;
+  pb->stream_chunk = chunk;
+  if (!pb->assembled) {
+    int rc = tdw_assemble_impl(pb);
+    if (rc) return rc;
+  }
+  pb->known_loaded = true;
+  return tdw_march_stream_launch(pb, threshold, want_rhs != 0);
+}
+
+int tdw_march_stream_finish(tdw_problem* pb, double* u, double* q, double* tau, double* sigma,
+                            double* rhs_trace, int32_t* n_steps, int32_t* status) {
+  if (!pb) return TDW_ERR_INVALID_ARG;
+  cudaSetDevice(pb->ctx->device);
+  int rc = tdw_march_stream_wait(pb);
+  if (rc) return rc;
+  if (rhs_trace)
+    TDW_CUDA(pb->ctx, cudaMemcpy(rhs_trace, pb->d_rhs, sizeof(double) * (size_t)(pb->nt - 1) * pb->ns,
+                                 cudaMemcpyDeviceToHost));
+  return tdw_download(pb, u, q, tau, sigma, n_steps, status);
+}
+
 int tdw_march(tdw_problem* pb, const double* u_known, const double* q_known, double threshold,
               double* u, double* q, double* tau, double* sigma, double* rhs_trace,
               int32_t* n_steps, int32_t* status) {
@@ -661,6 +704,11 @@ int tdw_problem_destroy(tdw_problem* pb) {
   if (pb->ev_fork) cudaEventDestroy(pb->ev_fork);
   if (pb->side) cudaStreamDestroy(pb->side);
   if (pb->side_near) cudaStreamDestroy(pb->side_near);
+  if (pb->stream_in_flight && pb->ev_stream_end) cudaEventSynchronize(pb->ev_stream_end);
+  if (pb->graph_exec_s) cudaGraphExecDestroy(pb->graph_exec_s);
+  for (auto e : pb->ev_chunk) cudaEventDestroy(e);
+  if (pb->ev_stream_end) cudaEventDestroy(pb->ev_stream_end);
+  if (pb->side_data) cudaStreamDestroy(pb->side_data);
   delete pb;
   return TDW_OK;
 }

@@ -1596,19 +1596,70 @@ __global__ void near_compact_kernel(const int* ncol, const double* nval, const d
 // for beta < 0 and for the columns j >= ns.
 __global__ void init_hist_kernel(double2* hist, int hstride, int hcols, int pad, int ns, int nt,
                                  const double* phi, const int* perm, const double* uk,
-                                 const double* qk) {
+                                 const double* qk, int known) {
   const long long n = (long long)hcols * hstride;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n;
        e += (long long)gridDim.x * blockDim.x) {
     const int sl = (int)(e / hcols), j = (int)(e % hcols);
     const int beta = sl - pad;
     double2 v = make_double2(0.0, 0.0);
-    if (beta >= 0 && beta < nt - 1 && j < ns) {
+    if (known && beta >= 0 && beta < nt - 1 && j < ns) {
       const double ph = phi[j];
       const size_t o = (size_t)beta * ns + perm[j];
       v = make_double2(ph * qk[o], (1.0 - ph) * uk[o]);
     }
     hist[e] = v;
+  }
+}
+
+// ---- streamed march: the known data arrive chunk by chunk from the host
+// Wait until the host has published `need` complete chunks (page-locked flag,
+// read through its device mapping); a negative flag (the host aborted: a data
+// callable raised), a stopped loop or 120 s without progress set flags[0] = 3
+// and every later kernel of the loop returns at entry.
+__global__ void stream_wait_kernel(const volatile int* flag, int need, int* flags) {
+  if (threadIdx.x != 0) return;
+  unsigned long long t0, t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (;;) {
+    const int f = *flag;
+    if (f >= need) break;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (f < 0 || *(volatile int*)flags != 0 || t - t0 > 120000000000ull) {
+      atomicCAS(flags, 0, 3);
+      break;
+    }
+    __nanosleep(2000);
+  }
+  __threadfence_system();
+}
+
+// rows [r0, r1) of the host samples (caller's order) into d_uk / d_qk, coalesced
+__global__ void stream_copy_kernel(const double* hu, const double* hq, double* du, double* dq, size_t r0,
+                                   size_t r1, int ns, const int* flags) {
+  if (*(volatile const int*)flags == 3) return;
+  const size_t a = r0 * ns, b = r1 * ns;
+  for (size_t e = a + blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < b; e += (size_t)gridDim.x * blockDim.x) {
+    du[e] = hu ? hu[e] : 0.0;
+    dq[e] = hq ? hq[e] : 0.0;
+  }
+}
+
+// history rows of the known data for steps [r0, r1) (internal order), as init_hist
+__global__ void stream_hist_kernel(double2* hist, int hcols, int pad, int ns, int r0, int r1,
+                                   const double* phi, const int* perm, const double* uk, const double* qk,
+                                   const int* flags) {
+  if (*(volatile const int*)flags == 3) return;
+  const long long n = (long long)(r1 - r0) * hcols;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
+    const int beta = r0 + (int)(e / hcols), j = (int)(e % hcols);
+    double2 v = make_double2(0.0, 0.0);
+    if (j < ns) {
+      const double ph = phi[j];
+      const size_t o = (size_t)beta * ns + perm[j];
+      v = make_double2(ph * qk[o], (1.0 - ph) * uk[o]);
+    }
+    hist[(size_t)(pad + beta) * hcols + j] = v;
   }
 }
 
@@ -1856,8 +1907,10 @@ int begin_loop(tdw_problem* pb, cudaStream_t st) {
   tdw_ctx* ctx = pb->ctx;
   TDW_CUDA(ctx, cudaMemsetAsync(pb->d_flags, 0, sizeof(int) * 4, st));
   TDW_CUDA(ctx, cudaMemsetAsync(pb->d_bnear, 0, sizeof(double) * pb->nsl * (pb->nsl + 1) * (size_t)pb->ns, st));
+  // streamed march: zeros now, each chunk's known rows once the host has sampled it
   init_hist_kernel<<<2 * ctx->num_sms, 256, 0, st>>>(pb->d_hist, pb->hstride, pb->hcols, pb->pad, pb->ns,
-                                                    pb->nt, pb->d_phi, pb->d_perm, pb->d_uk, pb->d_qk);
+                                                    pb->nt, pb->d_phi, pb->d_perm, pb->d_uk, pb->d_qk,
+                                                    pb->streaming ? 0 : 1);
   TDW_CUDA(ctx, cudaGetLastError());
   return TDW_OK;
 }
@@ -1986,10 +2039,35 @@ int enqueue_loop(tdw_problem* pb, LoopPlan& L, cudaEvent_t* ev_conv) {
   TDW_CUDA(ctx, cudaEventRecord(pb->ev_fork, st));
   TDW_CUDA(ctx, cudaStreamWaitEvent(sc, pb->ev_fork, 0));
   TDW_CUDA(ctx, cudaStreamWaitEvent(sn, pb->ev_fork, 0));
+  // streamed march: the data stream takes each chunk in as soon as the host has
+  // published it; a pass waits for the chunk of the last step it can touch
+  const int C = pb->stream_chunk, nchunks = pb->streaming ? (nt - 1 + C - 1) / C : 0;
+  int chunk_waited = -1;
+  if (pb->streaming) {
+    cudaStream_t sd = pb->side_data;
+    TDW_CUDA(ctx, cudaStreamWaitEvent(sd, pb->ev_fork, 0));
+    for (int c = 0; c < nchunks; ++c) {
+      const int r0 = c * C, r1 = std::min(nt - 1, (c + 1) * C);
+      stream_wait_kernel<<<1, 32, 0, sd>>>(pb->h_flag_dev, c + 1, pb->d_flags);
+      stream_copy_kernel<<<64, 256, 0, sd>>>(pb->h_uk_dev, pb->h_qk_dev, pb->d_uk, pb->d_qk, (size_t)r0, (size_t)r1,
+                                             pb->ns, pb->d_flags);
+      stream_hist_kernel<<<64, 256, 0, sd>>>(pb->d_hist, pb->hcols, pb->pad, pb->ns, r0, r1, pb->d_phi, pb->d_perm,
+                                             pb->d_uk, pb->d_qk, pb->d_flags);
+      TDW_CUDA(ctx, cudaGetLastError());
+      TDW_CUDA(ctx, cudaEventRecord(pb->ev_chunk[c], sd));
+    }
+  }
   const int KB = pb->kb;
   int last_alpha = 1;
   for (int alpha = 1; alpha < nt; alpha += KB) {
     const int nb = std::min(KB, nt - alpha);
+    if (pb->streaming) {  // known data up to step alpha + kb - 1 (conservative)
+      const int c = std::min(nchunks - 1, std::min(nt - 2, alpha + KB - 1) / C);
+      if (c > chunk_waited) {
+        TDW_CUDA(ctx, cudaStreamWaitEvent(sc, pb->ev_chunk[c], 0));
+        chunk_waited = c;
+      }
+    }
     // convolution pass of steps alpha..alpha+nb-1 on the side stream
     const int dep = alpha - 1 - pb->overlap;  // the last solve this pass reads
     if (dep >= 1) TDW_CUDA(ctx, cudaStreamWaitEvent(sc, evS[dep], 0));
@@ -2051,6 +2129,7 @@ int enqueue_loop(tdw_problem* pb, LoopPlan& L, cudaEvent_t* ev_conv) {
     }
   }
   // join the side streams
+  if (pb->streaming && nchunks > 0) TDW_CUDA(ctx, cudaStreamWaitEvent(st, pb->ev_chunk[nchunks - 1], 0));
   if (near && (pb->near_split || pb->near_in_solve)) TDW_CUDA(ctx, cudaStreamWaitEvent(st, evN[nt - 1], 0));
   TDW_CUDA(ctx, cudaStreamWaitEvent(st, evF[last_alpha], 0));
   TDW_CUDA(ctx, cudaGetLastError());
@@ -2059,20 +2138,9 @@ int enqueue_loop(tdw_problem* pb, LoopPlan& L, cudaEvent_t* ev_conv) {
 
 }  // namespace
 
-int tdw_march_loop(tdw_problem* pb, double threshold, bool want_rhs, bool time_kernels,
-                   tdw_timing* timing) {
+// streams and events of the pipelined loop (created once per problem)
+static int loop_streams(tdw_problem* pb) {
   tdw_ctx* ctx = pb->ctx;
-  cudaStream_t st = ctx->stream;
-  if (!pb->assembled) return tdw_fail(ctx, TDW_ERR_STATE, "tdw_march before tdw_assemble");
-  if (!pb->known_loaded) return tdw_fail(ctx, TDW_ERR_STATE, "known boundary data not uploaded");
-  if (pb->nranks > 1 && !ctx->comm)
-    return tdw_fail(ctx, TDW_ERR_STATE, "row-sharded problem without a communicator (tdw_comm_init)");
-  if (pb->fmm) return tdw_fmm_loop(pb, threshold, want_rhs, timing);
-  if (want_rhs) {
-    if (!pb->d_rhs)
-      TDW_CUDA(ctx, cudaMalloc(&pb->d_rhs, sizeof(double) * (size_t)(pb->nt - 1) * pb->ns));
-    TDW_CUDA(ctx, cudaMemsetAsync(pb->d_rhs, 0, sizeof(double) * (size_t)(pb->nt - 1) * pb->ns, st));
-  }
   {
     // lags >= 3 of the near terms on their own stream (TDW_NEAR_SPLIT=1); off by
     // default: it competes with the next solve and the convolution for SMs
@@ -2091,6 +2159,27 @@ int tdw_march_loop(tdw_problem* pb, double threshold, bool want_rhs, bool time_k
     for (auto& e : pb->ev_conv) TDW_CUDA(ctx, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     for (auto& e : pb->ev_near) TDW_CUDA(ctx, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     TDW_CUDA(ctx, cudaEventCreateWithFlags(&pb->ev_fork, cudaEventDisableTiming));
+  }
+  return TDW_OK;
+}
+
+int tdw_march_loop(tdw_problem* pb, double threshold, bool want_rhs, bool time_kernels,
+                   tdw_timing* timing) {
+  tdw_ctx* ctx = pb->ctx;
+  cudaStream_t st = ctx->stream;
+  if (!pb->assembled) return tdw_fail(ctx, TDW_ERR_STATE, "tdw_march before tdw_assemble");
+  if (!pb->known_loaded) return tdw_fail(ctx, TDW_ERR_STATE, "known boundary data not uploaded");
+  if (pb->nranks > 1 && !ctx->comm)
+    return tdw_fail(ctx, TDW_ERR_STATE, "row-sharded problem without a communicator (tdw_comm_init)");
+  if (pb->fmm) return tdw_fmm_loop(pb, threshold, want_rhs, timing);
+  if (want_rhs) {
+    if (!pb->d_rhs)
+      TDW_CUDA(ctx, cudaMalloc(&pb->d_rhs, sizeof(double) * (size_t)(pb->nt - 1) * pb->ns));
+    TDW_CUDA(ctx, cudaMemsetAsync(pb->d_rhs, 0, sizeof(double) * (size_t)(pb->nt - 1) * pb->ns, st));
+  }
+  {
+    int rc = loop_streams(pb);
+    if (rc) return rc;
   }
 
   LoopPlan L{};
@@ -2189,6 +2278,100 @@ int tdw_march_loop(tdw_problem* pb, double threshold, bool want_rhs, bool time_k
 // exchange emulated by device copies of each rank's own rows of b into every
 // rank's b (the in-place all-gather).  Test harness for the sharded code path
 // on a single GPU: no kernel waits on another, launches are sequential.
+// Streamed march: launch the loop (direct launches on a problem's first streamed
+// loop, a cached graph afterwards) and return; tdw_march_stream_wait finishes it.
+int tdw_march_stream_launch(tdw_problem* pb, double threshold, bool want_rhs) {
+  tdw_ctx* ctx = pb->ctx;
+  cudaStream_t st = ctx->stream;
+  if (pb->nranks > 1 && !ctx->comm)
+    return tdw_fail(ctx, TDW_ERR_STATE, "row-sharded problem without a communicator (tdw_comm_init)");
+  if (want_rhs) {
+    if (!pb->d_rhs)
+      TDW_CUDA(ctx, cudaMalloc(&pb->d_rhs, sizeof(double) * (size_t)(pb->nt - 1) * pb->ns));
+    TDW_CUDA(ctx, cudaMemsetAsync(pb->d_rhs, 0, sizeof(double) * (size_t)(pb->nt - 1) * pb->ns, st));
+  }
+  {
+    int rc = loop_streams(pb);
+    if (rc) return rc;
+  }
+  const int nchunks = (pb->nt - 1 + pb->stream_chunk - 1) / pb->stream_chunk;
+  if (!pb->side_data) {
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    TDW_CUDA(ctx, cudaStreamCreateWithPriority(&pb->side_data, cudaStreamNonBlocking, lo));
+    TDW_CUDA(ctx, cudaEventCreateWithFlags(&pb->ev_stream_end, cudaEventDisableTiming));
+  }
+  while ((int)pb->ev_chunk.size() < nchunks) {
+    cudaEvent_t e;
+    TDW_CUDA(ctx, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    pb->ev_chunk.push_back(e);
+  }
+  LoopPlan L{};
+  {
+    int rc = make_plan(pb, L, threshold, want_rhs);
+    if (rc) return rc;
+  }
+  pb->streaming = true;
+  // the graph bakes the mapped buffers, the chunk size, the threshold and the rhs switch in
+  const bool same = pb->graph_exec_s && pb->graph_thr_s == threshold && pb->graph_rhs_s == want_rhs &&
+                    pb->stream_key_u == pb->h_uk_dev && pb->stream_key_q == pb->h_qk_dev &&
+                    pb->stream_key_f == pb->h_flag_dev && pb->stream_key_c == pb->stream_chunk;
+  int rc = TDW_OK;
+  if (!same && pb->use_graph && pb->loop_calls_s > 0) {
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    if (cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
+      rc = enqueue_loop(pb, L, nullptr);
+      const cudaError_t ce = cudaStreamEndCapture(st, &graph);
+      if (rc == TDW_OK && ce == cudaSuccess && cudaGraphInstantiate(&exec, graph, 0) == cudaSuccess) {
+        if (pb->graph_exec_s) cudaGraphExecDestroy(pb->graph_exec_s);
+        pb->graph_exec_s = exec;
+        pb->graph_thr_s = threshold;
+        pb->graph_rhs_s = want_rhs;
+        pb->stream_key_u = pb->h_uk_dev;
+        pb->stream_key_q = pb->h_qk_dev;
+        pb->stream_key_f = pb->h_flag_dev;
+        pb->stream_key_c = pb->stream_chunk;
+      } else {
+        cudaGetLastError();
+        rc = TDW_OK;
+      }
+      if (graph) cudaGraphDestroy(graph);
+    }
+  }
+  const bool graphed = pb->graph_exec_s && pb->graph_thr_s == threshold && pb->graph_rhs_s == want_rhs &&
+                       pb->stream_key_u == pb->h_uk_dev && pb->stream_key_q == pb->h_qk_dev &&
+                       pb->stream_key_f == pb->h_flag_dev && pb->stream_key_c == pb->stream_chunk;
+  ++pb->loop_calls_s;
+  if (graphed) {
+    if (cudaGraphLaunch(pb->graph_exec_s, st) != cudaSuccess) rc = tdw_fail(ctx, TDW_ERR_CUDA, "cudaGraphLaunch");
+  } else {
+    rc = enqueue_loop(pb, L, nullptr);
+  }
+  pb->streaming = false;
+  if (rc) return rc;
+  TDW_CUDA(ctx, cudaEventRecord(pb->ev_stream_end, st));
+  pb->stream_in_flight = true;
+  return TDW_OK;
+}
+
+int tdw_march_stream_wait(tdw_problem* pb) {
+  tdw_ctx* ctx = pb->ctx;
+  if (!pb->stream_in_flight) return tdw_fail(ctx, TDW_ERR_STATE, "no streamed march in flight");
+  pb->stream_in_flight = false;
+  TDW_CUDA(ctx, cudaEventSynchronize(pb->ev_stream_end));
+  int hflags[4];
+  TDW_CUDA(ctx, cudaMemcpy(hflags, pb->d_flags, sizeof(hflags), cudaMemcpyDeviceToHost));
+  if (hflags[0] == 2) {
+    char msg[128];
+    snprintf(msg, sizeof(msg), "step %d: solve residual too large", hflags[2]);
+    return tdw_fail(ctx, TDW_ERR_RESIDUAL, msg);
+  }
+  if (hflags[0] == 3)
+    return tdw_fail(ctx, TDW_ERR_STATE, "streamed march: the known data never arrived (aborted or timed out)");
+  return TDW_OK;
+}
+
 int tdw_march_emulated_impl(tdw_problem** pbs, int n, double threshold) {
   if (pbs[0]->fmm) return tdw_fmm_march_emulated(pbs, n, threshold);
   tdw_ctx* ctx = pbs[0]->ctx;

@@ -200,6 +200,26 @@ struct tdw_problem {
   int *d_h_col = nullptr, *d_h_ngat = nullptr, *d_h_gdst = nullptr, *d_h_gsrc = nullptr;
   double* d_h_val = nullptr;
   bool use_graph = true;
+  // streamed march (tdw_march_stream_begin/finish): the host samples the known
+  // data chunk by chunk into mapped page-locked buffers while the loop runs; a
+  // data stream waits for each chunk's flag before copying it in
+  bool streaming = false;
+  const double* h_uk_dev = nullptr;  // device view of the host u samples (or null: zeros)
+  const double* h_qk_dev = nullptr;
+  const volatile int* h_flag_dev = nullptr;  // device view of the host's "chunks ready" counter
+  int stream_chunk = 16;            // steps per chunk
+  cudaStream_t side_data = nullptr;
+  std::vector<cudaEvent_t> ev_chunk;
+  cudaGraphExec_t graph_exec_s = nullptr;  // cached streamed-loop graph
+  double graph_thr_s = 0.0;
+  bool graph_rhs_s = false;
+  int loop_calls_s = 0;
+  const void* stream_key_u = nullptr;  // what the cached streamed graph baked in
+  const void* stream_key_q = nullptr;
+  const volatile void* stream_key_f = nullptr;
+  int stream_key_c = 0;
+  bool stream_in_flight = false;
+  cudaEvent_t ev_stream_end = nullptr;
   int loop_calls = 0;               // time loops run on this problem (the first one is not captured)
   double t_assemble_ms = 0.0, t_fill_ms = 0.0;
 };
@@ -218,6 +238,8 @@ int tdw_fail(tdw_ctx* ctx, int code, const std::string& msg);
 int tdw_assemble_impl(tdw_problem* pb);
 int tdw_march_loop(tdw_problem* pb, double threshold, bool want_rhs, bool time_kernels,
                    tdw_timing* timing);
+int tdw_march_stream_launch(tdw_problem* pb, double threshold, bool want_rhs);
+int tdw_march_stream_wait(tdw_problem* pb);
 int tdw_outputs(tdw_problem* pb, double* u, double* q, double* tau, double* sigma);
 int tdw_time_conv_impl(tdw_problem* pb, int n, float* ms_out);
 int tdw_setup_cluster_solver(tdw_problem* pb);

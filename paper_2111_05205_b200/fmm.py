@@ -84,6 +84,8 @@ def _ptr(a, ct):
 class FmmStore(BandStore):
     """Device state of the fast solver: near-field banded store + far-field operators."""
 
+    _streamable = False  # the fast solver's loop takes its known data up front
+
     def __init__(self, spec, config: FmmConfig | None = None, ctx=None, plan=None,
                  nranks: int = 1, rank: int = 0, shard_only: bool = False):
         # nranks > 1: this rank's rows of the near field, M2L into the target

@@ -239,6 +239,15 @@ class BandStore:
     def n_lags(self) -> int:
         return self.info()["n_lags"]
 
+    _streamable = True  # the direct path runs the streamed march (FmmStore: False)
+
+    def pinned_flag(self) -> np.ndarray:
+        """Page-locked int32 counter of the streamed march (chunks ready), from the
+        process-wide page-locked pool (a cold store allocates nothing)."""
+        if not hasattr(self, "_flag"):
+            self._flag = _lib.pinned_empty((1,)).view(np.int32)
+        return self._flag
+
     def pinned_known(self, which: int) -> np.ndarray:
         """Page-locked (nt-1, ns) host buffer for the u (0) / q (1) samples, owned by the store."""
         if not hasattr(self, "_pinned"):
@@ -390,6 +399,55 @@ def build_step_matrix(spec, mats):
     A = sp.csc_matrix((vals, (rows, cols)), shape=(ns, ns))
     return A, StepSolver(mats)
 
+STREAM_CHUNK = 16  # steps per chunk of the streamed march
+
+
+def _march_streamed(mats, spec, times, threshold, rhs, hist, n_steps, status) -> int:
+    """march()'s streamed form: launch, sample chunk by chunk, publish, finish."""
+    lib = _lib.load()
+    nk = len(times)
+    bufs = {w: (mats.pinned_known(w) if fn is not None else None)
+            for w, fn in ((0, spec.u_data), (1, spec.q_data))}
+    flag = mats.pinned_flag()
+    flag[0] = 0
+    _lib.check(lib.tdw_march_stream_begin(
+        mats.h, threshold, int(rhs is not None),
+        bufs[0].ctypes.data if bufs[0] is not None else None,
+        bufs[1].ctypes.data if bufs[1] is not None else None,
+        STREAM_CHUNK, flag.ctypes.data), mats.ctx.h, "tdw_march_stream_begin")
+    try:
+        fns = [(bufs[w], fn) for w, fn in ((0, spec.u_data), (1, spec.q_data)) if fn is not None]
+        if all(getattr(fn, "sample_many", None) is None for _, fn in fns):
+            # plain callables: the reference's order (u then q per step, marching.py:268-275)
+            for k, t in enumerate(times):
+                for buf, fn in fns:
+                    buf[k] = fn(float(t))
+                if (k + 1) % STREAM_CHUNK == 0 or k + 1 == nk:
+                    flag[0] = -(-(k + 1) // STREAM_CHUNK)
+        else:
+            # vectorised sources fill rows out of order (thread pool): publish the
+            # longest prefix every source has completed
+            import threading
+            done = np.zeros((len(fns), nk), dtype=bool)
+            lock = threading.Lock()
+
+            def progress(i, k0, k1):
+                with lock:
+                    done[i, k0:k1] = True
+                    full = done.all(axis=0)
+                    pre = nk if full.all() else int(np.argmin(full))
+                    c = nk if pre == nk else pre // STREAM_CHUNK * STREAM_CHUNK
+                    flag[0] = max(int(flag[0]), -(-c // STREAM_CHUNK))
+            for i, (buf, fn) in enumerate(fns):
+                sample_data(fn, times, buf, on_chunk=lambda k0, k1, i=i: progress(i, k0, k1))
+    except BaseException:
+        flag[0] = -1  # the device loop stops at the next chunk boundary
+        lib.tdw_march_stream_finish(mats.h, None, None, None, None, None, None, None)
+        raise
+    return lib.tdw_march_stream_finish(mats.h, _lib.dptr(hist.u), _lib.dptr(hist.q), _lib.dptr(hist.tau),
+                                       _lib.dptr(hist.sigma), _lib.dptr(rhs) if rhs is not None else None,
+                                       C.byref(n_steps), C.byref(status))
+
 
 def march(spec, window: bool = True, blowup_factor: float = 1e6, mats=None,
           rhs_trace: list | None = None, device_data: bool = False, mode: str = "auto") -> TimeHistory:
@@ -426,28 +484,35 @@ def march(spec, window: bool = True, blowup_factor: float = 1e6, mats=None,
     for which, (zc, nz, t0, sig) in dev.items():
         _lib.check(lib.tdw_known_plane_pulse(mats.h, which, _lib.dptr(zc), _lib.dptr(nz), float(t0), float(sig)),
                    mats.ctx.h, "tdw_known_plane_pulse")
-    for which, fn in ((0, spec.u_data), (1, spec.q_data)):
-        if which in dev:
-            continue
-        _lib.check(lib.tdw_upload_known_rows(mats.h, which, 0, 0 if fn is not None else nk, None),
-                   mats.ctx.h, "tdw_upload_known_rows")
-        if fn is None:
-            continue
-        buf = mats.pinned_known(which)
-
-        def on_chunk(k0, k1, which=which, buf=buf):
-            if k1 > k0:
-                _lib.check(lib.tdw_upload_known_rows(mats.h, which, k0, k1 - k0, _lib.dptr(buf[k0:k1])),
-                           mats.ctx.h, "tdw_upload_known_rows")
-        sample_data(fn, times, buf, on_chunk=on_chunk)
     threshold = blowup_factor * max(spec.blowup_reference, 1e-30)
     ns, nt = spec.mesh.n_elements, spec.nt
     rhs = np.zeros((nt - 1, ns)) if rhs_trace is not None else None
     n_steps, status = C.c_int32(0), C.c_int32(0)
-    rc = lib.tdw_march_device_known(mats.h, float(threshold),
-                                    _lib.dptr(hist.u), _lib.dptr(hist.q), _lib.dptr(hist.tau),
-                                    _lib.dptr(hist.sigma), _lib.dptr(rhs) if rhs is not None else None,
-                                    C.byref(n_steps), C.byref(status))
+    host = [(w, fn) for w, fn in ((0, spec.u_data), (1, spec.q_data)) if fn is not None and w not in dev]
+    if host and not dev and mats._streamable:
+        # streamed: the loop starts at once and takes each chunk of steps as soon as
+        # the host has sampled it (tdw_march_stream_begin): the Greville sampling of
+        # the data callables (marching.py:258-276) overlaps the device loop
+        rc = _march_streamed(mats, spec, times, float(threshold), rhs, hist, n_steps, status)
+    else:
+        for which, fn in ((0, spec.u_data), (1, spec.q_data)):
+            if which in dev:
+                continue
+            _lib.check(lib.tdw_upload_known_rows(mats.h, which, 0, 0 if fn is not None else nk, None),
+                       mats.ctx.h, "tdw_upload_known_rows")
+            if fn is None:
+                continue
+            buf = mats.pinned_known(which)
+
+            def on_chunk(k0, k1, which=which, buf=buf):
+                if k1 > k0:
+                    _lib.check(lib.tdw_upload_known_rows(mats.h, which, k0, k1 - k0, _lib.dptr(buf[k0:k1])),
+                               mats.ctx.h, "tdw_upload_known_rows")
+            sample_data(fn, times, buf, on_chunk=on_chunk)
+        rc = lib.tdw_march_device_known(mats.h, float(threshold),
+                                        _lib.dptr(hist.u), _lib.dptr(hist.q), _lib.dptr(hist.tau),
+                                        _lib.dptr(hist.sigma), _lib.dptr(rhs) if rhs is not None else None,
+                                        C.byref(n_steps), C.byref(status))
     _lib.check(rc, mats.ctx.h, "march")
     mats.assembled = True
     hist.n_steps = int(n_steps.value)

@@ -472,3 +472,47 @@ def test_on_the_fly_mode_matches_reference(cfg):
     ms = store.time_conv(3)
     print(f"cfg{cfg} on-the-fly pass {ms:.3f} ms (kb = {inf['steps_per_pass']})")
     store.close()
+
+
+@pytest.mark.parametrize("cfg", [0, 2])
+def test_streamed_march_matches_preloaded(cfg):
+    """march() with host data callables runs the streamed loop (the device takes
+    each chunk of Greville samples as soon as the host has written it,
+    tdw_march_stream_begin/finish): the same densities as the loop on data
+    uploaded up front (tdw_march_device_known), for plain per-step callables and
+    vectorised sources, first call (direct launches) and later calls (graph)."""
+    spec = scenarios.build_spec(cfg)
+    store = marching.BandStore(spec).assemble()
+    uk, qk = marching.greville_samples(spec)
+    store.upload_known(uk, qk)
+    store.run_resident(1e6 * max(spec.blowup_reference, 1e-30), 1)
+    ref = store.download()
+    f_u, f_q = spec.u_data, spec.q_data
+    plain = type(spec)(spec.mesh, spec.phi, spec.bie, spec.basis, spec.c, spec.nt,
+                       u_data=(lambda t: f_u(t)) if f_u else None, q_data=(lambda t: f_q(t)) if f_q else None)
+    for s in (plain, plain, spec, spec):
+        h = marching.march(s, mats=store)
+        assert h.status == ref.status and h.n_steps == ref.n_steps
+        np.testing.assert_array_equal(h.u, ref.u)
+        np.testing.assert_array_equal(h.q, ref.q)
+
+
+def test_streamed_march_aborts_when_the_data_raises():
+    """A data callable that raises mid-way stops the device loop (flag -1) and the
+    exception reaches the caller; the store stays usable."""
+    spec = scenarios.build_spec(0)
+    store = marching.BandStore(spec).assemble()
+    f = spec.q_data
+    calls = [0]
+
+    def bad(t):
+        calls[0] += 1
+        if calls[0] > 40:
+            raise ArithmeticError("boom")
+        return f(t)
+    broken = type(spec)(spec.mesh, spec.phi, spec.bie, spec.basis, spec.c, spec.nt, q_data=bad)
+    with pytest.raises(ArithmeticError, match="boom"):
+        marching.march(broken, mats=store)
+    good = type(spec)(spec.mesh, spec.phi, spec.bie, spec.basis, spec.c, spec.nt, q_data=lambda t: f(t))
+    h = marching.march(good, mats=store)
+    assert h.status == "stable" and h.n_steps == spec.nt - 1
