@@ -704,6 +704,7 @@ int tdw_problem_destroy(tdw_problem* pb) {
   if (pb->ev_fork) cudaEventDestroy(pb->ev_fork);
   if (pb->side) cudaStreamDestroy(pb->side);
   if (pb->side_near) cudaStreamDestroy(pb->side_near);
+  if (pb->stream_thread.joinable()) pb->stream_thread.join();
   if (pb->stream_in_flight && pb->ev_stream_end) cudaEventSynchronize(pb->ev_stream_end);
   if (pb->graph_exec_s) cudaGraphExecDestroy(pb->graph_exec_s);
   for (auto e : pb->ev_chunk) cudaEventDestroy(e);

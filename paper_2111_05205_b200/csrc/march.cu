@@ -2280,7 +2280,24 @@ int tdw_march_loop(tdw_problem* pb, double threshold, bool want_rhs, bool time_k
 // on a single GPU: no kernel waits on another, launches are sequential.
 // Streamed march: launch the loop (direct launches on a problem's first streamed
 // loop, a cached graph afterwards) and return; tdw_march_stream_wait finishes it.
+// The enqueueing runs on its own host thread: thousands of direct launches fill
+// the launch queue, and a full queue blocks the launching thread until the device
+// drains it -- which it cannot do before the caller publishes the first chunks.
+static int stream_enqueue(tdw_problem* pb, double threshold, bool want_rhs);
+
 int tdw_march_stream_launch(tdw_problem* pb, double threshold, bool want_rhs) {
+  if (pb->stream_thread.joinable()) pb->stream_thread.join();
+  pb->stream_rc = TDW_OK;
+  pb->stream_in_flight = true;
+  const int dev = pb->ctx->device;
+  pb->stream_thread = std::thread([pb, threshold, want_rhs, dev] {
+    cudaSetDevice(dev);
+    pb->stream_rc = stream_enqueue(pb, threshold, want_rhs);
+  });
+  return TDW_OK;
+}
+
+static int stream_enqueue(tdw_problem* pb, double threshold, bool want_rhs) {
   tdw_ctx* ctx = pb->ctx;
   cudaStream_t st = ctx->stream;
   if (pb->nranks > 1 && !ctx->comm)
@@ -2351,14 +2368,18 @@ int tdw_march_stream_launch(tdw_problem* pb, double threshold, bool want_rhs) {
   pb->streaming = false;
   if (rc) return rc;
   TDW_CUDA(ctx, cudaEventRecord(pb->ev_stream_end, st));
-  pb->stream_in_flight = true;
   return TDW_OK;
 }
 
 int tdw_march_stream_wait(tdw_problem* pb) {
   tdw_ctx* ctx = pb->ctx;
   if (!pb->stream_in_flight) return tdw_fail(ctx, TDW_ERR_STATE, "no streamed march in flight");
+  if (pb->stream_thread.joinable()) pb->stream_thread.join();
   pb->stream_in_flight = false;
+  if (pb->stream_rc) {  // the enqueue failed: drain whatever it launched
+    cudaDeviceSynchronize();
+    return pb->stream_rc;
+  }
   TDW_CUDA(ctx, cudaEventSynchronize(pb->ev_stream_end));
   int hflags[4];
   TDW_CUDA(ctx, cudaMemcpy(hflags, pb->d_flags, sizeof(hflags), cudaMemcpyDeviceToHost));

@@ -5,6 +5,7 @@
 #include <stdint.h>
 
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/tdw.h"
@@ -219,6 +220,8 @@ struct tdw_problem {
   const volatile void* stream_key_f = nullptr;
   int stream_key_c = 0;
   bool stream_in_flight = false;
+  std::thread stream_thread;        // enqueues the streamed loop while the caller samples
+  int stream_rc = 0;                // its result
   cudaEvent_t ev_stream_end = nullptr;
   int loop_calls = 0;               // time loops run on this problem (the first one is not captured)
   double t_assemble_ms = 0.0, t_fill_ms = 0.0;
