@@ -462,11 +462,13 @@ def march(spec, window: bool = True, blowup_factor: float = 1e6, mats=None,
         raise TypeError("mats must come from build_retarded_matrices of this package")
     else:
         _check_store(mats, spec, window)
-    hist = TimeHistory(spec.basis, spec.nt, spec.mesh.n_elements)
     # outputs in page-locked memory (a pool: blocks come back when the arrays die);
-    # the library writes every entry
+    # the library writes every entry, so the history gets no zero-filled arrays first
     out = _lib.pinned_empty((4, spec.nt - 1, spec.mesh.n_elements))
+    hist = TimeHistory.__new__(TimeHistory)
+    hist.basis, hist.nt, hist.n_elements = spec.basis, spec.nt, spec.mesh.n_elements
     hist.u, hist.q, hist.tau, hist.sigma = out[0], out[1], out[2], out[3]
+    hist.n_steps, hist.status = 0, "stable"
     # Greville samples straight into the store's page-locked buffers, each chunk
     # of steps copied to the device as soon as it is written (the copies overlap
     # the sampling); a data callable that is None gives zero samples on the device
