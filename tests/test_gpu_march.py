@@ -164,12 +164,12 @@ def test_solver_variants_agree(monkeypatch, env):
     assert per_step_rel(h.q, ref.q).max() < 1e-11
 
 
-@pytest.mark.parametrize("kb,overlap", [(1, 1), (2, 1), (2, 2), (3, 2), (4, 1), (6, 3)])
+@pytest.mark.parametrize("kb,overlap", [(1, 1), (2, 1), (2, 2), (3, 2), (4, 1), (4, 4), (5, 5), (6, 3)])
 def test_temporal_block_sizes_match_reference(monkeypatch, kb, overlap):
     """One convolution pass per kb steps, running beside `overlap` solves
     (split lags 2..kb+overlap, their unknown part added by the near terms after
     each solve), reproduces the reference golden march of config 2 for every
-    block size and overlap; the default (4, 4) is covered by the tests above."""
+    block size and overlap; the config-2 default is (5, 5)."""
     g = golden("march_cfg2.npz")
     spec = scenarios.build_spec(2)
     monkeypatch.setenv("TDW_KB", str(kb))
@@ -226,23 +226,24 @@ def test_chebyshev_sweeps_match_jacobi(cfg, monkeypatch):
     assert per_step_rel(x[:, g["sub"]], g["unknown_sub"]).max() < tol
 
 
-def test_lag2_near_terms_in_the_solve(monkeypatch):
-    """Lag-2 near terms formed in the halo solve's tail from the owners' x in
-    DSMEM (lags >= 3 on the near stream) equal the near_step_kernel form to
-    round-off (another summation order), and both match the reference golden."""
+@pytest.mark.parametrize("kb,tail", [("5", "1"), ("5", "2"), ("5", "3"), ("6", "1"), ("6", "2"), ("6", "3")])
+def test_near_terms_in_the_solve_tail(monkeypatch, kb, tail):
+    """The first split lags' near terms formed in the halo solve's tail from the
+    owners' x in DSMEM (TDW_NEAR_IN_SOLVE lags; the rest on the near stream) equal
+    the all-near_step_kernel form (TDW_NEAR_IN_SOLVE=0) to round-off (another
+    summation order), at kb 5 (the config-2 default: a three-lag tail) and kb 6."""
     spec = scenarios.build_spec(2)
+    monkeypatch.setenv("TDW_KB", kb)
     monkeypatch.setenv("TDW_NEAR_IN_SOLVE", "0")
     h0 = marching.march(spec)
-    monkeypatch.setenv("TDW_NEAR_IN_SOLVE", "1")
-    h1 = marching.march(spec)
+    monkeypatch.setenv("TDW_NEAR_IN_SOLVE", tail)
+    st = marching.BandStore(spec).assemble()
+    h1 = marching.march(spec, mats=st)
+
     def rel(x, ref):  # per step, floored at 1e-6 of the largest step (the first
         n = np.linalg.norm(ref, axis=1)  # steps before the pulse arrives are round-off)
         return np.linalg.norm(x - ref, axis=1) / np.maximum(n, 1e-6 * n.max())
-    assert rel(h1.q, h0.q).max() < 1e-12
-    for kb in ("4", "6"):
-        monkeypatch.setenv("TDW_KB", kb)
-        hk = marching.march(spec)
-        assert rel(hk.q, h0.q).max() < 1e-11, kb
+    assert rel(h1.q, h0.q).max() < 1e-11
 
 
 def test_window_off_is_equivalent():
