@@ -93,7 +93,11 @@ template <int D, bool BM>
 __device__ __forceinline__ void coeff_eval(const PairGeom& g, double s, double K, double& o0,
                                            double& o1) {
   double acc0 = 0.0, acc1 = 0.0;
-#pragma unroll
+  // Not unrolled: the closed-form bundles are large (bm d1: ~200 operations), and
+  // 3 edges x 2 limits of inlined copies overflow the instruction cache (the fill
+  // kernel stalled on instruction fetch more than on anything else); one copy of
+  // the bundle evaluated for both limits in a 2-trip loop keeps the code small.
+#pragma unroll 1
   for (int e = 0; e < 3; ++e) {
     const bool alive = g.yok[e] && (s > g.za);
     if (!alive) continue;  // every term of a dead sub-triangle is exactly zero
@@ -107,8 +111,16 @@ __device__ __forceinline__ void coeff_eval(const PairGeom& g, double s, double K
     if (!BM) {
       double lo[2] = {0.0, 0.0}, hi[2] = {0.0, 0.0};
       if (fmask) {
-        uw_bundle<D>(xlo, y, g.za, s, lo);
-        uw_bundle<D>(xhi, y, g.za, s, hi);
+#pragma unroll 1
+        for (int side = 0; side < 2; ++side) {
+          double r[2];
+          uw_bundle<D>(side ? xhi : xlo, y, g.za, s, r);
+#pragma unroll
+          for (int k = 0; k < 2; ++k) {
+            if (side) hi[k] = r[k];
+            else lo[k] = r[k];
+          }
+        }
       }
       const double a0 = -ipow<D + 1>(pw) / (D + 1) * datan;
       const double az = g.sgn * ipow<D>(pw) * datan;
@@ -119,8 +131,16 @@ __device__ __forceinline__ void coeff_eval(const PairGeom& g, double s, double K
 #pragma unroll
       for (int k = 0; k < 8; ++k) { lo[k] = 0.0; hi[k] = 0.0; }
       if (fmask) {
-        bm_bundle<D>(xlo, y, g.za, s, lo);
-        bm_bundle<D>(xhi, y, g.za, s, hi);
+#pragma unroll 1
+        for (int side = 0; side < 2; ++side) {
+          double r[8];
+          bm_bundle<D>(side ? xhi : xlo, y, g.za, s, r);
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            if (side) hi[k] = r[k];
+            else lo[k] = r[k];
+          }
+        }
       }
       const bool m1 = fmask && (x1 > -xc) && (x1 < xc);
       const bool m2 = fmask && (x2 > -xc) && (x2 < xc);
