@@ -229,10 +229,11 @@ __global__ void __launch_bounds__(256) count_kernel(AsmArgs a) {
 }
 
 // blocks per SM the register budget is sized for (spills accepted: latency-bound
-// kernel, occupancy wins).  Measured against 240 registers: d = 1 at 4 blocks
-// (128 registers) +11% on config 2; d = 2 at 3 blocks (168) +11% on config 3
+// kernel, occupancy wins).  With the compact (not unrolled) closed forms, 4 blocks
+// (128 registers) is best for every order: config 2 (d = 1) 37.1 ms (5 blocks:
+// 38.2), config 3 (d = 2) 804 ms (3 blocks: 835, 5 blocks: 905)
 #ifndef TDW_FILL_MINB
-#define TDW_FILL_MINB(D) ((D) == 1 ? 4 : 3)
+#define TDW_FILL_MINB(D) 4
 #endif
 template <int D, bool BM>
 __global__ void __launch_bounds__(128, TDW_FILL_MINB(D)) fill_kernel(AsmArgs a) {
