@@ -646,7 +646,9 @@ static int choose_conv_schedule(tdw_problem* pb) {
   int maxsm = 0;
   cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device);
   // FIFO capacity: all opt-in shared memory but the kernel's static part
-  const size_t cap = std::min<size_t>((size_t)maxsm - 1024, 224 * 1024) / 128 * 128;
+  size_t cap = std::min<size_t>((size_t)maxsm - 1024, 224 * 1024) / 128 * 128;
+  if (const char* e = getenv("TDW_CONV_CAP"))  // experiments: a smaller FIFO (KB)
+    cap = std::min(cap, (size_t)atoi(e) * 1024 / 128 * 128);
   pb->wbox = pb->wmax;
   if (pb->wbox + pb->kb - 1 > 256)
     return tdw_fail(ctx, TDW_ERR_LIMIT, "history slice of a unit exceeds 256 lags (TMA box limit)");
