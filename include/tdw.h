@@ -14,7 +14,7 @@
  *                          + build_step_matrix                    marching.py:279-289
  *   tdw_march           <- marching.march (+greville inputs,      marching.py:292-338
  *                          TimeHistory outputs)                   marching.py:184-276
- *   tdw_march_stream_begin / _finish
+ *   tdw_march_stream_begin / _finish (/ _outputs)
  *                       <- marching.march with the Greville sampling  marching.py:258-338
  *                          overlapped with the loop (chunked, mapped buffers)
  *   tdw_upload_known_rows + tdw_march_device_known
@@ -194,6 +194,13 @@ int tdw_march_stream_begin(tdw_problem* pb, double threshold, int want_rhs, cons
                            const double* q_host, int chunk, int32_t* flag);
 int tdw_march_stream_finish(tdw_problem* pb, double* u, double* q, double* tau, double* sigma,
                             double* rhs_trace, int32_t* n_steps, int32_t* status);
+/* Optional, before tdw_march_stream_begin: the (nt-1, ns) TimeHistory arrays
+ * (marching.py:184-203) the NEXT streamed march will return, in page-locked memory
+ * from tdw_host_alloc (NULL = not wanted).  The loop then writes each chunk's rows
+ * of u, q, tau, sigma into them as soon as the chunk's last step is solved, so the
+ * device-to-host traffic overlaps the loop; tdw_march_stream_finish, given the same
+ * pointers, copies nothing.  Arrays that are not page-locked: TDW_ERR_INVALID_ARG. */
+int tdw_march_stream_outputs(tdw_problem* pb, double* u, double* q, double* tau, double* sigma);
 
 /* Device-side boundary data (no reference counterpart): the
  * Greville samples of the incident Gaussian plane pulse exp(-((t - z - t0)/sig)^2)

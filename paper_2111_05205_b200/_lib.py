@@ -83,6 +83,7 @@ EXPORTS = {
     "tdw_march_stream_begin": ([C.c_void_p, C.c_double, C.c_int, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p],
                                C.c_int),
     "tdw_march_stream_finish": ([C.c_void_p, _dp, _dp, _dp, _dp, _dp, _i32p, _i32p], C.c_int),
+    "tdw_march_stream_outputs": ([C.c_void_p, _dp, _dp, _dp, _dp], C.c_int),
     "tdw_march_device_known": ([C.c_void_p, C.c_double, _dp, _dp, _dp, _dp, _dp, _i32p, _i32p], C.c_int),
     "tdw_march_resident": ([C.c_void_p, C.c_double, C.c_int, C.c_int, C.POINTER(Timing)], C.c_int),
     "tdw_download": ([C.c_void_p, _dp, _dp, _dp, _dp, _i32p, _i32p], C.c_int),

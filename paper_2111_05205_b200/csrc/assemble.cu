@@ -558,13 +558,26 @@ struct OtfArgs {
   double* bpart;
   const int* flags;
   unsigned long long* n_evals;
+  const int* ready;  // streamed march: chunks of known data on the device
+  int need_ready;    //   chunks this pass needs (0: not streamed)
   int hcols, pad, ns, row_lo, rows_loc, ntiles, tg, S, cap, split_lag2, nsl, alpha, nb;
   double c, dt, K;
 };
 
 template <int D, bool BM>
 __global__ void __launch_bounds__(128, TDW_FILL_MINB(D)) otf_conv_kernel(OtfArgs a) {
-  if (a.flags[0] != 0) return;
+  if (a.need_ready > 0) {  // streamed march: wait for the known rows this pass reads
+    if (threadIdx.x == 0) {
+      for (;;) {
+        int v;
+        asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(a.ready) : "memory");
+        if (v >= a.need_ready || *(volatile const int*)a.flags != 0) break;
+        __nanosleep(500);
+      }
+    }
+    __syncthreads();
+  }
+  if (*(volatile const int*)a.flags != 0) return;
   const int lane = threadIdx.x & 31;
   const long long task = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (task >= (long long)a.rows_loc * a.S) return;
@@ -619,7 +632,7 @@ __global__ void __launch_bounds__(128, TDW_FILL_MINB(D)) otf_conv_kernel(OtfArgs
 #pragma unroll
         for (int s = 0; s < TDW_KB_MAX; ++s)
           if (s < a.nb) {
-            const double2 x = __ldg(h + (size_t)s * a.hcols);
+            const double2 x = __ldcg(h + (size_t)s * a.hcols);  // L2: rows may have arrived during this launch
             acc[s] = fma(-vw, x.y, fma(vu, x.x, acc[s]));
           }
       }
@@ -1087,6 +1100,8 @@ int launch_otf_conv(tdw_problem* pb, int alpha, int nb, cudaStream_t st) {
   o.bpart = pb->d_bpart;
   o.flags = pb->d_flags;
   o.n_evals = pb->d_otf_evals;
+  o.ready = pb->d_ready;
+  o.need_ready = pb->need_ready;
   o.hcols = pb->hcols;
   o.pad = pb->pad;
   o.ns = pb->ns;

@@ -480,12 +480,9 @@ int tdw_march_stream_begin(tdw_problem* pb, double threshold, int want_rhs, cons
   const size_t n = (size_t)(pb->nt - 1) * pb->ns;
   if (!pb->d_uk) TDW_CUDA(ctx, cudaMalloc(&pb->d_uk, sizeof(double) * n));
   if (!pb->d_qk) TDW_CUDA(ctx, cudaMalloc(&pb->d_qk, sizeof(double) * n));
-  void* dp = nullptr;
-  pb->h_uk_dev = pb->h_qk_dev = nullptr;
-  if (u_host) { TDW_CUDA(ctx, cudaHostGetDevicePointer(&dp, (void*)u_host, 0)); pb->h_uk_dev = (const double*)dp; }
-  if (q_host) { TDW_CUDA(ctx, cudaHostGetDevicePointer(&dp, (void*)q_host, 0)); pb->h_qk_dev = (const double*)dp; }
-  TDW_CUDA(ctx, cudaHostGetDevicePointer(&dp, (void*)flag, 0));
-  pb->h_flag_dev = (const volatile int*)dp;
+  pb->h_uk_host = u_host;
+  pb->h_qk_host = q_host;
+  pb->h_flag_host = (const volatile int*)flag;
   pb->stream_chunk = chunk;
   if (!pb->assembled) {
     int rc = tdw_assemble_impl(pb);
@@ -495,16 +492,46 @@ int tdw_march_stream_begin(tdw_problem* pb, double threshold, int want_rhs, cons
   return tdw_march_stream_launch(pb, threshold, want_rhs != 0);
 }
 
+// Destinations of the NEXT streamed march's outputs: page-locked (nt-1, ns) arrays
+// (tdw_host_alloc; NULL = not wanted).  The loop then writes each chunk's rows as
+// soon as its last step is solved, and tdw_march_stream_finish -- called with the
+// same pointers -- has nothing left to copy.
+int tdw_march_stream_outputs(tdw_problem* pb, double* u, double* q, double* tau, double* sigma) {
+  if (!pb) return TDW_ERR_INVALID_ARG;
+  tdw_ctx* ctx = pb->ctx;
+  cudaSetDevice(ctx->device);
+  if (pb->stream_in_flight) return tdw_fail(ctx, TDW_ERR_STATE, "a streamed march is already in flight");
+  double* outs[4] = {u, q, tau, sigma};
+  for (int k = 0; k < 4; ++k) {
+    if (!outs[k]) continue;
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, outs[k]) != cudaSuccess || at.type != cudaMemoryTypeHost) {
+      cudaGetLastError();
+      return tdw_fail(ctx, TDW_ERR_INVALID_ARG, "tdw_march_stream_outputs: the arrays must be page-locked (tdw_host_alloc)");
+    }
+  }
+  for (int k = 0; k < 4; ++k) pb->out_host[k] = outs[k];
+  pb->out_registered = true;
+  return TDW_OK;
+}
+
 int tdw_march_stream_finish(tdw_problem* pb, double* u, double* q, double* tau, double* sigma,
                             double* rhs_trace, int32_t* n_steps, int32_t* status) {
   if (!pb) return TDW_ERR_INVALID_ARG;
   cudaSetDevice(pb->ctx->device);
   int rc = tdw_march_stream_wait(pb);
+  const bool streamed = pb->out_streamed;
+  pb->out_streamed = false;
   if (rc) return rc;
   if (rhs_trace)
     TDW_CUDA(pb->ctx, cudaMemcpy(rhs_trace, pb->d_rhs, sizeof(double) * (size_t)(pb->nt - 1) * pb->ns,
                                  cudaMemcpyDeviceToHost));
-  return tdw_download(pb, u, q, tau, sigma, n_steps, status);
+  // arrays the loop has written already (same pointers as registered) need no copy
+  double* outs[4] = {u, q, tau, sigma};
+  if (streamed)
+    for (int k = 0; k < 4; ++k)
+      if (outs[k] && outs[k] == pb->out_host[k]) outs[k] = nullptr;
+  return tdw_download(pb, outs[0], outs[1], outs[2], outs[3], n_steps, status);
 }
 
 int tdw_march(tdw_problem* pb, const double* u_known, const double* q_known, double threshold,
@@ -707,9 +734,15 @@ int tdw_problem_destroy(tdw_problem* pb) {
   if (pb->stream_thread.joinable()) pb->stream_thread.join();
   if (pb->stream_in_flight && pb->ev_stream_end) cudaEventSynchronize(pb->ev_stream_end);
   if (pb->graph_exec_s) cudaGraphExecDestroy(pb->graph_exec_s);
-  for (auto e : pb->ev_chunk) cudaEventDestroy(e);
+  if (pb->chunk_thread.joinable()) pb->chunk_thread.join();
+  if (pb->ev_begin) cudaEventDestroy(pb->ev_begin);
+  if (pb->d_ready) cudaFree(pb->d_ready);
   if (pb->ev_stream_end) cudaEventDestroy(pb->ev_stream_end);
   if (pb->side_data) cudaStreamDestroy(pb->side_data);
+  if (pb->side_out) cudaStreamDestroy(pb->side_out);
+  if (pb->ev_out) cudaEventDestroy(pb->ev_out);
+  if (pb->d_outdesc) cudaFree(pb->d_outdesc);
+  if (pb->d_iperm) cudaFree(pb->d_iperm);
   delete pb;
   return TDW_OK;
 }

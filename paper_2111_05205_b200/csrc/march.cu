@@ -21,7 +21,9 @@
 #include <cuda.h>
 #include <cub/cub.cuh>
 #include <cuda_runtime.h>
+#include <atomic>
 #include <chrono>
+#include <thread>
 #include <cstring>
 #include <nccl.h>
 
@@ -38,6 +40,9 @@
 namespace tdw {
 
 #define FULLMASK 0xffffffffu
+#ifndef TDW_STREAM_TIMEOUT_NS
+#define TDW_STREAM_TIMEOUT_NS 150000000000ull  // a streamed pass gives up on its data after 150 s
+#endif
 
 // --- mbarrier / bulk-copy primitives (sm_90+ PTX, used on sm_100a) ---------
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
@@ -168,6 +173,8 @@ struct ConvArgs {
   unsigned long long* trace;  // timeline trace (TDW_TRACE_SOLVE): slots 11, 12 of the pass's first step
   unsigned stage_bytes;  // shared-memory FIFO capacity
   unsigned chunk;             // bytes per bulk copy of the unit stream
+  const int* ready;           // streamed march: chunks of known data on the device
+  int need_ready;             //   chunks this pass needs (0: not streamed)
   unsigned long long* tstat;  // optional (TDW_CONV_TSTAT, tdw_time_conv only): wait / busy cycle sums
 };
 
@@ -215,7 +222,28 @@ __device__ __forceinline__ void conv_body(const ConvArgs& a, const CUtensorMap& 
   __shared__ __align__(8) uint64_t empty[4];
   __shared__ unsigned region[4];
   __shared__ __align__(16) double2 zero_slot;  // the coefficient a lane past its band reads
-  if (a.flags[0] != 0) return;
+  if (a.need_ready > 0) {
+    // streamed march: the chunk server raises *ready as the host's samples reach
+    // the device; this pass reads known rows up to chunk need_ready
+    if (threadIdx.x == 0) {
+      unsigned long long t0, t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+      for (;;) {
+        int v;
+        asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(a.ready) : "memory");
+        if (v >= a.need_ready || *(volatile const int*)a.flags != 0) break;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        if (t - t0 > TDW_STREAM_TIMEOUT_NS) {  // the chunk server died: do not hang the device
+          atomicCAS((int*)a.flags, 0, 3);
+          break;
+        }
+        __nanosleep(500);
+      }
+    }
+    __syncthreads();
+    asm volatile("fence.proxy.async;" ::: "memory");  // the rows are read by bulk copies
+  }
+  if (*(volatile const int*)a.flags != 0) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   constexpr int NS = 4;  // slots (barrier pairs); pb->conv_nstages == 4
   if (threadIdx.x == 0) {
@@ -1639,37 +1667,13 @@ __global__ void init_hist_kernel(double2* hist, int hstride, int hcols, int pad,
 }
 
 // ---- streamed march: the known data arrive chunk by chunk from the host
-// Wait until the host has published `need` complete chunks (page-locked flag,
-// read through its device mapping); a negative flag (the host aborted: a data
-// callable raised), a stopped loop or 120 s without progress set flags[0] = 3
-// and every later kernel of the loop returns at entry.
-__global__ void stream_wait_kernel(const volatile int* flag, int need, int* flags) {
-  if (threadIdx.x != 0) return;
-  unsigned long long t0, t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-  for (;;) {
-    const int f = *flag;
-    if (f >= need) break;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    if (f < 0 || *(volatile int*)flags != 0 || t - t0 > 120000000000ull) {
-      atomicCAS(flags, 0, 3);
-      break;
-    }
-    __nanosleep(2000);
-  }
-  __threadfence_system();
+// (chunk_server): copies, the history rows below, then the chunk counter
+__global__ void stream_ready_kernel(int* ready, int value) {
+  asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(ready), "r"(value) : "memory");
 }
-
-// rows [r0, r1) of the host samples (caller's order) into d_uk / d_qk, coalesced
-__global__ void stream_copy_kernel(const double* hu, const double* hq, double* du, double* dq, size_t r0,
-                                   size_t r1, int ns, const int* flags) {
-  if (*(volatile const int*)flags == 3) return;
-  const size_t a = r0 * ns, b = r1 * ns;
-  for (size_t e = a + blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < b; e += (size_t)gridDim.x * blockDim.x) {
-    du[e] = hu ? hu[e] : 0.0;
-    dq[e] = hq ? hq[e] : 0.0;
-  }
-}
+// the host aborted (a data callable raised) or stalled: every later kernel of the
+// loop returns at entry, a pass waiting for data stops waiting
+__global__ void stream_abort_kernel(int* flags) { atomicCAS(flags, 0, 3); }
 
 // history rows of the known data for steps [r0, r1) (internal order), as init_hist
 __global__ void stream_hist_kernel(double2* hist, int hcols, int pad, int ns, int r0, int r1,
@@ -1726,6 +1730,47 @@ __global__ void outputs_kernel(const double2* hist, int hcols, int pad, int ns, 
       if (tau) tau[o] = ta;
       if (sig) sig[o] = sa;
     }
+  }
+}
+
+// Streamed outputs: rows [r0, r1) of u, q, tau, sigma (as outputs_kernel) written
+// straight into the caller's mapped page-locked arrays dst[0..3] (null = not
+// wanted).  Threads run over the ORIGINAL element index, so the writes that cross
+// the bus are contiguous; the history gather stays on the device.
+__global__ void outputs_rows_kernel(const double2* __restrict__ hist, int hcols, int pad, int ns, int d,
+                                    const int* __restrict__ iperm, const int* flags,
+                                    double* const* __restrict__ dst, int r0, int r1) {
+  const int nsteps = *(volatile const int*)(flags + 1);
+  double* u = dst[0];
+  double* q = dst[1];
+  double* tau = dst[2];
+  double* sig = dst[3];
+  double w[5] = {0, 0, 0, 0, 0};
+  if (d == 1) { w[0] = 1.0; w[1] = -2.0; w[2] = 1.0; }
+  if (d == 2) { w[0] = 0.5; w[1] = -1.5; w[2] = 1.5; w[3] = -0.5; }
+  if (d == 3) { w[0] = 1.0 / 6.0; w[1] = -(2.0 / 3.0); w[2] = 1.0; w[3] = -(2.0 / 3.0); w[4] = 1.0 / 6.0; }
+  const long long n = (long long)(r1 - r0) * ns;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int beta = r0 + (int)(e / ns), o = (int)(e % ns);
+    const size_t at = (size_t)beta * ns + o;
+    double uv = 0.0, qv = 0.0, ta = 0.0, sa = 0.0;
+    if (beta < nsteps) {
+      const double2* h = hist + (size_t)pad * hcols + iperm[o];
+      const double2 hb = h[(size_t)beta * hcols];
+      qv = hb.x;
+      uv = hb.y;
+      const int kmax = min(d + 1, beta);
+      for (int k = 0; k <= kmax; ++k) {  // kappa sums in the order of outputs_kernel
+        const double2 v = h[(size_t)(beta - k) * hcols];
+        ta += w[k] * v.x;
+        sa += w[k] * v.y;
+      }
+    }
+    if (u) u[at] = uv;
+    if (q) q[at] = qv;
+    if (tau) tau[at] = ta;
+    if (sig) sig[at] = sa;
   }
 }
 
@@ -1815,6 +1860,8 @@ static void fill_conv_args(tdw_problem* pb, ConvArgs& c) {
   c.wbox = pb->wbox;
   c.stats = nullptr;
   c.tstat = nullptr;
+  c.ready = pb->d_ready;
+  c.need_ready = 0;
   c.chunk = 32768u;
   if (const char* e = getenv("TDW_CONV_CHUNK")) c.chunk = (unsigned)std::max(512, atoi(e)) / 128u * 128u;  // experiments
   c.dry = 0;
@@ -1948,6 +1995,8 @@ int begin_loop(tdw_problem* pb, cudaStream_t st) {
 int launch_conv(tdw_problem* pb, LoopPlan& L, int alpha, int nsteps, cudaStream_t s) {
   L.c.alpha = alpha;
   L.c.bpart = pb->d_bpart;
+  L.c.ready = pb->d_ready;
+  L.c.need_ready = pb->need_ready;
   if (pb->otf) {
     int rc = launch_otf_conv(pb, alpha, nsteps, s);
     if (rc) return rc;
@@ -2053,11 +2102,16 @@ int launch_solve_near(tdw_problem* pb, LoopPlan& L, int alpha, cudaStream_t s) {
 //   P(alpha)      waits solve(alpha-1-m)            writes b[(alpha+i) % (kb+m)]
 //   solve(s)      waits P(pass of s), solve(s-1)    reads b[s % (kb+m)], bnear[.][s % (nsl+1)]
 // Also used under stream capture (one CUDA graph per loop configuration).
-int enqueue_loop(tdw_problem* pb, LoopPlan& L, cudaEvent_t* ev_conv) {
+}  // namespace
+static bool stream_wait_chunk(tdw_problem* pb, int c);
+static int stream_deliver_chunk(tdw_problem* pb, int c);
+namespace {
+
+int enqueue_loop(tdw_problem* pb, LoopPlan& L, cudaEvent_t* ev_conv, bool begin = true) {
   tdw_ctx* ctx = pb->ctx;
   cudaStream_t st = ctx->stream, sc = pb->side;
   const int nt = pb->nt;
-  int rc = begin_loop(pb, st);
+  int rc = begin ? begin_loop(pb, st) : TDW_OK;  // the streamed march initialises before the launch
   if (rc) return rc;
   cudaEvent_t* evS = pb->ev_solve.data();  // solve(alpha) done
   cudaEvent_t* evF = pb->ev_conv.data();   // F(alpha) done
@@ -2068,34 +2122,35 @@ int enqueue_loop(tdw_problem* pb, LoopPlan& L, cudaEvent_t* ev_conv) {
   TDW_CUDA(ctx, cudaEventRecord(pb->ev_fork, st));
   TDW_CUDA(ctx, cudaStreamWaitEvent(sc, pb->ev_fork, 0));
   TDW_CUDA(ctx, cudaStreamWaitEvent(sn, pb->ev_fork, 0));
-  // streamed march: the data stream takes each chunk in as soon as the host has
-  // published it; a pass waits for the chunk of the last step it can touch
+  // streamed march: a pass needs the chunk of the last step it can touch
   const int C = pb->stream_chunk, nchunks = pb->streaming ? (nt - 1 + C - 1) / C : 0;
-  int chunk_waited = -1;
-  if (pb->streaming) {
-    cudaStream_t sd = pb->side_data;
-    TDW_CUDA(ctx, cudaStreamWaitEvent(sd, pb->ev_fork, 0));
-    for (int c = 0; c < nchunks; ++c) {
-      const int r0 = c * C, r1 = std::min(nt - 1, (c + 1) * C);
-      stream_wait_kernel<<<1, 32, 0, sd>>>(pb->h_flag_dev, c + 1, pb->d_flags);
-      stream_copy_kernel<<<64, 256, 0, sd>>>(pb->h_uk_dev, pb->h_qk_dev, pb->d_uk, pb->d_qk, (size_t)r0, (size_t)r1,
-                                             pb->ns, pb->d_flags);
-      stream_hist_kernel<<<64, 256, 0, sd>>>(pb->d_hist, pb->hcols, pb->pad, pb->ns, r0, r1, pb->d_phi, pb->d_perm,
-                                             pb->d_uk, pb->d_qk, pb->d_flags);
-      TDW_CUDA(ctx, cudaGetLastError());
-      TDW_CUDA(ctx, cudaEventRecord(pb->ev_chunk[c], sd));
-    }
-  }
+  int chunks_sent = 0;
+  // streamed outputs: after the last solve of a chunk its rows go to the host
+  const bool outs = pb->streaming && pb->out_streamed;
+  if (outs) TDW_CUDA(ctx, cudaStreamWaitEvent(pb->side_out, pb->ev_fork, 0));
   const int KB = pb->kb;
   int last_alpha = 1;
   for (int alpha = 1; alpha < nt; alpha += KB) {
     const int nb = std::min(KB, nt - alpha);
-    if (pb->streaming) {  // known data up to step alpha + kb - 1 (conservative)
-      const int c = std::min(nchunks - 1, std::min(nt - 2, alpha + KB - 1) / C);
-      if (c > chunk_waited) {
-        TDW_CUDA(ctx, cudaStreamWaitEvent(sc, pb->ev_chunk[c], 0));
-        chunk_waited = c;
+    // known data up to step alpha + kb - 1 (conservative)
+    pb->need_ready = pb->streaming ? std::min(nchunks - 1, std::min(nt - 2, alpha + KB - 1) / C) + 1 : 0;
+    if (pb->streaming && pb->stream_direct) {
+      // direct launches (a problem's first streamed march, or graphs off): this
+      // thread delivers the chunks itself, in launch order, and the pass waits for
+      // the copy through an event -- nothing spins on the device while kernels are
+      // launched (and their code loaded) for the first time
+      for (; chunks_sent < pb->need_ready; ++chunks_sent) {
+        if (!stream_wait_chunk(pb, chunks_sent)) {
+          stream_abort_kernel<<<1, 1, 0, st>>>(pb->d_flags);
+          TDW_CUDA(ctx, cudaGetLastError());
+          pb->need_ready = 0;
+          return TDW_OK;  // tdw_march_stream_wait reports flags[0] == 3
+        }
+        if ((rc = stream_deliver_chunk(pb, chunks_sent))) return rc;
+        TDW_CUDA(ctx, cudaEventRecord(pb->ev_begin, pb->side_data));
+        TDW_CUDA(ctx, cudaStreamWaitEvent(sc, pb->ev_begin, 0));
       }
+      pb->need_ready = 0;
     }
     // convolution pass of steps alpha..alpha+nb-1 on the side stream
     const int dep = alpha - 1 - pb->overlap;  // the last solve this pass reads
@@ -2155,10 +2210,21 @@ int enqueue_loop(tdw_problem* pb, LoopPlan& L, cudaEvent_t* ev_conv) {
       } else {
         TDW_CUDA(ctx, cudaEventRecord(evS[s], st));
       }
+      if (outs && (s % C == 0 || s == nt - 1)) {  // rows [r0, s) are final (solve(s) wrote row s - 1)
+        const int r0 = (s - 1) / C * C;
+        TDW_CUDA(ctx, cudaStreamWaitEvent(pb->side_out, evS[s], 0));
+        outputs_rows_kernel<<<32, 256, 0, pb->side_out>>>(pb->d_hist, pb->hcols, pb->pad, pb->ns, pb->d, pb->d_iperm,
+                                                          pb->d_flags, pb->d_outdesc, r0, s);
+        TDW_CUDA(ctx, cudaGetLastError());
+      }
     }
   }
+  if (outs) {
+    TDW_CUDA(ctx, cudaEventRecord(pb->ev_out, pb->side_out));
+    TDW_CUDA(ctx, cudaStreamWaitEvent(st, pb->ev_out, 0));
+  }
   // join the side streams
-  if (pb->streaming && nchunks > 0) TDW_CUDA(ctx, cudaStreamWaitEvent(st, pb->ev_chunk[nchunks - 1], 0));
+  pb->need_ready = 0;
   if (near && (pb->near_split || pb->near_in_solve)) TDW_CUDA(ctx, cudaStreamWaitEvent(st, evN[nt - 1], 0));
   TDW_CUDA(ctx, cudaStreamWaitEvent(st, evF[last_alpha], 0));
   TDW_CUDA(ctx, cudaGetLastError());
@@ -2316,13 +2382,70 @@ static int stream_enqueue(tdw_problem* pb, double threshold, bool want_rhs);
 
 int tdw_march_stream_launch(tdw_problem* pb, double threshold, bool want_rhs) {
   if (pb->stream_thread.joinable()) pb->stream_thread.join();
-  pb->stream_rc = TDW_OK;
+  if (pb->chunk_thread.joinable()) pb->chunk_thread.join();
+  pb->stream_rc = pb->chunk_rc = TDW_OK;
   pb->stream_in_flight = true;
   const int dev = pb->ctx->device;
   pb->stream_thread = std::thread([pb, threshold, want_rhs, dev] {
     cudaSetDevice(dev);
     pb->stream_rc = stream_enqueue(pb, threshold, want_rhs);
   });
+  return TDW_OK;
+}
+
+// Streamed march, host side.  stream_wait_chunk blocks until the caller has
+// published chunk c (false: aborted -- a data callable raised -- or 120 s without
+// progress); stream_deliver_chunk copies the chunk's Greville samples to the
+// device on the data stream, writes its history rows and raises *d_ready.
+static bool stream_wait_chunk(tdw_problem* pb, int c) {
+  const auto t0 = std::chrono::steady_clock::now();
+  for (unsigned spins = 0;; ++spins) {
+    const int f = *pb->h_flag_host;
+    if (f >= c + 1) break;
+    if (f < 0 || std::chrono::steady_clock::now() - t0 > std::chrono::seconds(120)) return false;
+    if (spins > 4000) std::this_thread::sleep_for(std::chrono::microseconds(20));
+  }
+  std::atomic_thread_fence(std::memory_order_acquire);  // the rows were written before the counter
+  return true;
+}
+
+static int stream_deliver_chunk(tdw_problem* pb, int c) {
+  tdw_ctx* ctx = pb->ctx;
+  cudaStream_t sd = pb->side_data;
+  const int C = pb->stream_chunk, nt = pb->nt, ns = pb->ns;
+  const int r0 = c * C, r1 = std::min(nt - 1, (c + 1) * C);
+  const size_t off = (size_t)r0 * ns, bytes = sizeof(double) * (size_t)(r1 - r0) * ns;
+  if (pb->h_uk_host)
+    TDW_CUDA(ctx, cudaMemcpyAsync(pb->d_uk + off, pb->h_uk_host + off, bytes, cudaMemcpyHostToDevice, sd));
+  else
+    TDW_CUDA(ctx, cudaMemsetAsync(pb->d_uk + off, 0, bytes, sd));
+  if (pb->h_qk_host)
+    TDW_CUDA(ctx, cudaMemcpyAsync(pb->d_qk + off, pb->h_qk_host + off, bytes, cudaMemcpyHostToDevice, sd));
+  else
+    TDW_CUDA(ctx, cudaMemsetAsync(pb->d_qk + off, 0, bytes, sd));
+  stream_hist_kernel<<<64, 256, 0, sd>>>(pb->d_hist, pb->hcols, pb->pad, ns, r0, r1, pb->d_phi, pb->d_perm,
+                                         pb->d_uk, pb->d_qk, pb->d_flags);
+  stream_ready_kernel<<<1, 1, 0, sd>>>(pb->d_ready, c + 1);
+  TDW_CUDA(ctx, cudaGetLastError());
+  return TDW_OK;
+}
+
+// The chunk server (graph launches): a host thread that delivers every chunk as
+// soon as it is published, while the loop -- launched in one call -- runs; a pass
+// waits on the device for the chunk it needs (need_ready).  Every kernel involved
+// has run before (the problem's first streamed march uses direct launches, below),
+// so no launch of the server has to load code while a pass is waiting.
+static int chunk_server(tdw_problem* pb) {
+  const int C = pb->stream_chunk, nchunks = (pb->nt - 1 + C - 1) / C;
+  for (int c = 0; c < nchunks; ++c) {
+    if (!stream_wait_chunk(pb, c)) {
+      stream_abort_kernel<<<1, 1, 0, pb->side_data>>>(pb->d_flags);
+      TDW_CUDA(pb->ctx, cudaGetLastError());
+      return TDW_OK;  // tdw_march_stream_wait reports flags[0] == 3
+    }
+    int rc = stream_deliver_chunk(pb, c);
+    if (rc) return rc;
+  }
   return TDW_OK;
 }
 
@@ -2340,17 +2463,38 @@ static int stream_enqueue(tdw_problem* pb, double threshold, bool want_rhs) {
     int rc = loop_streams(pb);
     if (rc) return rc;
   }
-  const int nchunks = (pb->nt - 1 + pb->stream_chunk - 1) / pb->stream_chunk;
   if (!pb->side_data) {
     int lo = 0, hi = 0;
     cudaDeviceGetStreamPriorityRange(&lo, &hi);
-    TDW_CUDA(ctx, cudaStreamCreateWithPriority(&pb->side_data, cudaStreamNonBlocking, lo));
+    TDW_CUDA(ctx, cudaStreamCreateWithPriority(&pb->side_data, cudaStreamNonBlocking, hi));
     TDW_CUDA(ctx, cudaEventCreateWithFlags(&pb->ev_stream_end, cudaEventDisableTiming));
+    TDW_CUDA(ctx, cudaEventCreateWithFlags(&pb->ev_begin, cudaEventDisableTiming));
+    TDW_CUDA(ctx, cudaMalloc(&pb->d_ready, sizeof(int)));
   }
-  while ((int)pb->ev_chunk.size() < nchunks) {
-    cudaEvent_t e;
-    TDW_CUDA(ctx, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    pb->ev_chunk.push_back(e);
+  pb->out_streamed = false;
+  if (pb->out_registered) {  // destinations of the streamed outputs for THIS march
+    pb->out_registered = false;
+    if (!pb->side_out) {
+      int lo = 0, hi = 0;
+      cudaDeviceGetStreamPriorityRange(&lo, &hi);
+      TDW_CUDA(ctx, cudaStreamCreateWithPriority(&pb->side_out, cudaStreamNonBlocking, lo));
+      TDW_CUDA(ctx, cudaEventCreateWithFlags(&pb->ev_out, cudaEventDisableTiming));
+      TDW_CUDA(ctx, cudaMalloc(&pb->d_outdesc, sizeof(double*) * 4));
+      std::vector<int> ip(pb->ns);
+      for (int k = 0; k < pb->ns; ++k) ip[pb->perm[k]] = k;
+      TDW_CUDA(ctx, cudaMalloc(&pb->d_iperm, sizeof(int) * pb->ns));
+      TDW_CUDA(ctx, cudaMemcpy(pb->d_iperm, ip.data(), sizeof(int) * pb->ns, cudaMemcpyHostToDevice));
+    }
+    double* dev[4] = {nullptr, nullptr, nullptr, nullptr};
+    for (int k = 0; k < 4; ++k)
+      if (pb->out_host[k]) {
+        void* dp = nullptr;
+        TDW_CUDA(ctx, cudaHostGetDevicePointer(&dp, pb->out_host[k], 0));
+        dev[k] = (double*)dp;
+      }
+    TDW_CUDA(ctx, cudaMemcpyAsync(pb->d_outdesc, dev, sizeof(dev), cudaMemcpyHostToDevice, st));
+    TDW_CUDA(ctx, cudaStreamSynchronize(st));  // dev[] is on this thread's stack
+    pb->out_streamed = true;
   }
   LoopPlan L{};
   {
@@ -2358,26 +2502,53 @@ static int stream_enqueue(tdw_problem* pb, double threshold, bool want_rhs) {
     if (rc) return rc;
   }
   pb->streaming = true;
-  // the graph bakes the mapped buffers, the chunk size, the threshold and the rhs switch in
-  const bool same = pb->graph_exec_s && pb->graph_thr_s == threshold && pb->graph_rhs_s == want_rhs &&
-                    pb->stream_key_u == pb->h_uk_dev && pb->stream_key_q == pb->h_qk_dev &&
-                    pb->stream_key_f == pb->h_flag_dev && pb->stream_key_c == pb->stream_chunk;
-  int rc = TDW_OK;
-  if (!same && pb->use_graph && pb->loop_calls_s > 0) {
+  // History, flags and the chunk counter are initialised here, outside the graph;
+  // the chunk server may then write known rows while the loop is still being
+  // launched (its first pass waits for chunk 1 on the device).
+  TDW_CUDA(ctx, cudaMemsetAsync(pb->d_ready, 0, sizeof(int), st));
+  int rc = begin_loop(pb, st);
+  if (rc) { pb->streaming = false; return rc; }
+  TDW_CUDA(ctx, cudaEventRecord(pb->ev_begin, st));
+  TDW_CUDA(ctx, cudaStreamWaitEvent(pb->side_data, pb->ev_begin, 0));
+  {
+    // Everything the chunk server will launch runs once now, while no pass is
+    // waiting: with lazy module loading the FIRST launch of a kernel loads its code,
+    // which synchronises with the running kernels -- a pass spinning for the very
+    // chunk that launch delivers would never be released.
+    static std::atomic<bool> warm{false};
+    if (!warm.exchange(true)) {
+      cudaStream_t sd = pb->side_data;
+      TDW_CUDA(ctx, cudaMemsetAsync(pb->d_uk, 0, sizeof(double), sd));
+      TDW_CUDA(ctx, cudaMemcpyAsync(pb->d_qk, pb->d_uk, sizeof(double), cudaMemcpyDeviceToDevice, sd));
+      stream_hist_kernel<<<1, 32, 0, sd>>>(pb->d_hist, pb->hcols, pb->pad, pb->ns, 0, 0, pb->d_phi, pb->d_perm,
+                                           pb->d_uk, pb->d_qk, pb->d_flags);
+      stream_ready_kernel<<<1, 1, 0, sd>>>(pb->d_ready, 0);
+      cudaFuncAttributes fa;
+      TDW_CUDA(ctx, cudaFuncGetAttributes(&fa, stream_abort_kernel));
+      TDW_CUDA(ctx, cudaFuncGetAttributes(&fa, outputs_rows_kernel));
+      TDW_CUDA(ctx, cudaStreamSynchronize(sd));
+    }
+  }
+  // the graph bakes the chunk size (which pass waits for which chunk, where the
+  // output kernels sit), the threshold and the rhs / output switches in
+  auto cached = [&] {
+    return pb->graph_exec_s && pb->graph_thr_s == threshold && pb->graph_rhs_s == want_rhs &&
+           pb->stream_key_c == pb->stream_chunk && pb->stream_key_out == pb->out_streamed;
+  };
+  pb->stream_direct = false;
+  if (!cached() && pb->use_graph && pb->loop_calls_s > 0) {
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
     if (cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
-      rc = enqueue_loop(pb, L, nullptr);
+      rc = enqueue_loop(pb, L, nullptr, false);
       const cudaError_t ce = cudaStreamEndCapture(st, &graph);
       if (rc == TDW_OK && ce == cudaSuccess && cudaGraphInstantiate(&exec, graph, 0) == cudaSuccess) {
         if (pb->graph_exec_s) cudaGraphExecDestroy(pb->graph_exec_s);
         pb->graph_exec_s = exec;
         pb->graph_thr_s = threshold;
         pb->graph_rhs_s = want_rhs;
-        pb->stream_key_u = pb->h_uk_dev;
-        pb->stream_key_q = pb->h_qk_dev;
-        pb->stream_key_f = pb->h_flag_dev;
         pb->stream_key_c = pb->stream_chunk;
+        pb->stream_key_out = pb->out_streamed;
       } else {
         cudaGetLastError();
         rc = TDW_OK;
@@ -2385,18 +2556,49 @@ static int stream_enqueue(tdw_problem* pb, double threshold, bool want_rhs) {
       if (graph) cudaGraphDestroy(graph);
     }
   }
-  const bool graphed = pb->graph_exec_s && pb->graph_thr_s == threshold && pb->graph_rhs_s == want_rhs &&
-                       pb->stream_key_u == pb->h_uk_dev && pb->stream_key_q == pb->h_qk_dev &&
-                       pb->stream_key_f == pb->h_flag_dev && pb->stream_key_c == pb->stream_chunk;
+  const bool graphed = cached();
   ++pb->loop_calls_s;
+  if (graphed) {  // one launch; the chunk server feeds it
+    const int dev = ctx->device;
+    pb->chunk_thread = std::thread([pb, dev] {
+      cudaSetDevice(dev);
+      pb->chunk_rc = chunk_server(pb);
+      if (pb->chunk_rc) {  // a copy failed: stop the loop rather than let its passes wait for the data
+        cudaGetLastError();
+        stream_abort_kernel<<<1, 1, 0, pb->side_data>>>(pb->d_flags);
+      }
+    });
+  } else {
+    pb->stream_direct = true;
+  }
+  static const bool trace = getenv("TDW_TRACE_MARCH") != nullptr;
+  cudaEvent_t t0 = nullptr, t1 = nullptr;
+  const auto h0 = std::chrono::steady_clock::now();
+  if (trace) {
+    cudaEventCreate(&t0);
+    cudaEventCreate(&t1);
+    cudaEventRecord(t0, st);
+  }
   if (graphed) {
     if (cudaGraphLaunch(pb->graph_exec_s, st) != cudaSuccess) rc = tdw_fail(ctx, TDW_ERR_CUDA, "cudaGraphLaunch");
   } else {
-    rc = enqueue_loop(pb, L, nullptr);
+    rc = enqueue_loop(pb, L, nullptr, false);
   }
   pb->streaming = false;
+  pb->stream_direct = false;
   if (rc) return rc;
   TDW_CUDA(ctx, cudaEventRecord(pb->ev_stream_end, st));
+  if (trace) {  // host time of the enqueue, device time of the streamed loop
+    const double hms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count();
+    cudaEventRecord(t1, st);
+    cudaEventSynchronize(t1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, t0, t1);
+    fprintf(stderr, "streamed loop: %s, enqueue %.2f ms on the host, %.2f ms on the device\n",
+            graphed ? "graph" : "direct launches", hms, ms);
+    cudaEventDestroy(t0);
+    cudaEventDestroy(t1);
+  }
   return TDW_OK;
 }
 
@@ -2404,12 +2606,14 @@ int tdw_march_stream_wait(tdw_problem* pb) {
   tdw_ctx* ctx = pb->ctx;
   if (!pb->stream_in_flight) return tdw_fail(ctx, TDW_ERR_STATE, "no streamed march in flight");
   if (pb->stream_thread.joinable()) pb->stream_thread.join();
+  if (pb->chunk_thread.joinable()) pb->chunk_thread.join();
   pb->stream_in_flight = false;
-  if (pb->stream_rc) {  // the enqueue failed: drain whatever it launched
+  if (pb->stream_rc || pb->chunk_rc) {  // the enqueue or a copy failed: drain whatever was launched
     cudaDeviceSynchronize();
-    return pb->stream_rc;
+    return pb->stream_rc ? pb->stream_rc : pb->chunk_rc;
   }
   TDW_CUDA(ctx, cudaEventSynchronize(pb->ev_stream_end));
+  TDW_CUDA(ctx, cudaStreamSynchronize(pb->side_data));
   int hflags[4];
   TDW_CUDA(ctx, cudaMemcpy(hflags, pb->d_flags, sizeof(hflags), cudaMemcpyDeviceToHost));
   if (hflags[0] == 2) {
@@ -2559,6 +2763,7 @@ int tdw_outputs(tdw_problem* pb, double* u, double* q, double* tau, double* sigm
   tdw_ctx* ctx = pb->ctx;
   cudaStream_t st = ctx->stream;
   const size_t n = (size_t)(pb->nt - 1) * pb->ns;
+  if (!u && !q && !tau && !sigma) return TDW_OK;  // nothing wanted (or streamed out already)
   if (!pb->d_out) TDW_CUDA(ctx, cudaMalloc(&pb->d_out, sizeof(double) * 4 * n));
   double* buf = pb->d_out;
   outputs_kernel<<<1024, 256, 0, st>>>(pb->d_hist, pb->hcols, pb->pad, pb->ns, pb->nt, pb->d,

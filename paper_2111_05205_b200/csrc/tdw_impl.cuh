@@ -202,27 +202,46 @@ struct tdw_problem {
   double* d_h_val = nullptr;
   bool use_graph = true;
   // streamed march (tdw_march_stream_begin/finish): the host samples the known
-  // data chunk by chunk into mapped page-locked buffers while the loop runs; a
-  // data stream waits for each chunk's flag before copying it in
+  // data chunk by chunk into page-locked buffers while the loop runs.  A host
+  // thread (the chunk server) watches the caller's chunk counter, copies every
+  // published chunk to the device on the data stream and raises *d_ready; a
+  // convolution pass waits (at kernel entry, on its own SMs) until the chunk of
+  // the last step it reads has arrived.  No kernel of the loop itself waits on the
+  // host, and no waiting kernel sits on an SM the solve cluster needs.
   bool streaming = false;
-  const double* h_uk_dev = nullptr;  // device view of the host u samples (or null: zeros)
-  const double* h_qk_dev = nullptr;
-  const volatile int* h_flag_dev = nullptr;  // device view of the host's "chunks ready" counter
+  bool stream_direct = false;       // this streamed march is launched kernel by kernel (no graph)
+  const double* h_uk_host = nullptr;  // the caller's page-locked u samples (or null: zeros)
+  const double* h_qk_host = nullptr;
+  const volatile int* h_flag_host = nullptr;  // the caller's "chunks complete" counter (-1: abort)
   int stream_chunk = 16;            // steps per chunk
+  int* d_ready = nullptr;           // chunks of known data on the device (this march)
+  int need_ready = 0;               // chunks the pass being launched needs (0: not streamed)
   cudaStream_t side_data = nullptr;
-  std::vector<cudaEvent_t> ev_chunk;
+  cudaEvent_t ev_begin = nullptr;   // history initialised: the chunk copies may start
   cudaGraphExec_t graph_exec_s = nullptr;  // cached streamed-loop graph
   double graph_thr_s = 0.0;
   bool graph_rhs_s = false;
   int loop_calls_s = 0;
-  const void* stream_key_u = nullptr;  // what the cached streamed graph baked in
-  const void* stream_key_q = nullptr;
-  const volatile void* stream_key_f = nullptr;
-  int stream_key_c = 0;
+  int stream_key_c = 0;             // what the cached streamed graph baked in: the chunk size
   bool stream_in_flight = false;
   std::thread stream_thread;        // enqueues the streamed loop while the caller samples
-  int stream_rc = 0;                // its result
+  std::thread chunk_thread;         // the chunk server
+  int stream_rc = 0;                // their results
+  int chunk_rc = 0;
   cudaEvent_t ev_stream_end = nullptr;
+  // streamed outputs (tdw_march_stream_outputs): after the last solve of each chunk
+  // a side stream writes the chunk's rows of u, q, tau, sigma straight into the
+  // caller's page-locked arrays (mapped), so the device-to-host traffic overlaps
+  // the loop.  The destinations reach the kernels through d_outdesc (rewritten
+  // before every launch), so the cached graph does not depend on them.
+  double* out_host[4] = {nullptr, nullptr, nullptr, nullptr};  // registered for the next streamed march
+  bool out_registered = false;
+  bool out_streamed = false;       // the march in flight (or just finished) wrote them
+  bool stream_key_out = false;     // the cached streamed graph contains the output kernels
+  double** d_outdesc = nullptr;    // device: the four mapped destinations
+  int* d_iperm = nullptr;          // original element index -> internal index
+  cudaStream_t side_out = nullptr;
+  cudaEvent_t ev_out = nullptr;
   int loop_calls = 0;               // time loops run on this problem (the first one is not captured)
   double t_assemble_ms = 0.0, t_fill_ms = 0.0;
 };

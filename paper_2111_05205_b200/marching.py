@@ -15,6 +15,8 @@ Keeps the reference's public surface (pkg/src/tdwavebem/marching.py):
 """
 from __future__ import annotations
 
+import os
+
 import ctypes as C
 import warnings
 from dataclasses import dataclass, field
@@ -410,6 +412,11 @@ def _march_streamed(mats, spec, times, threshold, rhs, hist, n_steps, status) ->
             for w, fn in ((0, spec.u_data), (1, spec.q_data))}
     flag = mats.pinned_flag()
     flag[0] = 0
+    # the history arrays are page-locked: the loop writes each chunk's rows into
+    # them while it runs (tdw_march_stream_outputs), nothing is copied at the end
+    if os.environ.get("TDW_STREAM_OUT", "1") != "0":   # 0: A/B, everything copied at the end
+        _lib.check(lib.tdw_march_stream_outputs(mats.h, _lib.dptr(hist.u), _lib.dptr(hist.q), _lib.dptr(hist.tau),
+                                                _lib.dptr(hist.sigma)), mats.ctx.h, "tdw_march_stream_outputs")
     _lib.check(lib.tdw_march_stream_begin(
         mats.h, threshold, int(rhs is not None),
         bufs[0].ctypes.data if bufs[0] is not None else None,

@@ -496,6 +496,36 @@ def test_streamed_march_matches_preloaded(cfg):
         assert h.status == ref.status and h.n_steps == ref.n_steps
         np.testing.assert_array_equal(h.u, ref.u)
         np.testing.assert_array_equal(h.q, ref.q)
+        # the history arrays are written chunk by chunk while the loop runs
+        # (tdw_march_stream_outputs): the same values as the download at the end
+        np.testing.assert_array_equal(h.tau, ref.tau)
+        np.testing.assert_array_equal(h.sigma, ref.sigma)
+
+
+def test_streamed_outputs_of_an_unstable_march():
+    """Blow-up inside a streamed march: the rows written while the loop ran equal
+    those of the march on preloaded data, zero from n_steps on (marching.py:336-338)."""
+    import ctypes as C
+    from paper_2111_05205_b200 import _lib
+    spec = scenarios.build_spec(0)
+    store = marching.BandStore(spec).assemble()
+    uk, qk = marching.greville_samples(spec)
+    store.upload_known(uk, qk)
+    thr = 1e-3 * float(np.abs(qk).max() + np.abs(uk).max())   # tripped after a few steps
+    store.run_resident(thr, 1)
+    ref = store.download()
+    assert ref.status == "unstable" and 0 < ref.n_steps < spec.nt - 1
+    h = marching.march(spec, mats=store, blowup_factor=thr / max(spec.blowup_reference, 1e-30))
+    assert h.status == "unstable" and h.n_steps == ref.n_steps
+    for name in ("u", "q", "tau", "sigma"):
+        np.testing.assert_array_equal(getattr(h, name), getattr(ref, name))
+    assert not h.u[h.n_steps:].any()
+    # arrays that are not page-locked are refused
+    lib = _lib.load()
+    bad = np.zeros((spec.nt - 1, spec.mesh.n_elements))
+    rc = lib.tdw_march_stream_outputs(store.h, _lib.dptr(bad), None, None, None)
+    assert rc != 0
+    store.close()
 
 
 def test_streamed_march_aborts_when_the_data_raises():
