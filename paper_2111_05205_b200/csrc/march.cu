@@ -2213,7 +2213,10 @@ int enqueue_loop(tdw_problem* pb, LoopPlan& L, cudaEvent_t* ev_conv, bool begin 
       if (outs && (s % C == 0 || s == nt - 1)) {  // rows [r0, s) are final (solve(s) wrote row s - 1)
         const int r0 = (s - 1) / C * C;
         TDW_CUDA(ctx, cudaStreamWaitEvent(pb->side_out, evS[s], 0));
-        outputs_rows_kernel<<<32, 256, 0, pb->side_out>>>(pb->d_hist, pb->hcols, pb->pad, pb->ns, pb->d, pb->d_iperm,
+        // 128-thread blocks: with 56 registers they fit beside a convolution CTA (10 K
+        // registers free per SM) instead of waiting for -- and then holding -- an SM of
+        // the solve cluster, whose CTAs need a whole register file each
+        outputs_rows_kernel<<<64, 128, 0, pb->side_out>>>(pb->d_hist, pb->hcols, pb->pad, pb->ns, pb->d, pb->d_iperm,
                                                           pb->d_flags, pb->d_outdesc, r0, s);
         TDW_CUDA(ctx, cudaGetLastError());
       }
@@ -3077,7 +3080,8 @@ int tdw_setup_cluster_solver(tdw_problem* pb) {
     const int T = mz == 8 ? 1024 : (mz == 16 ? 512 : 256);
     int CL = 1;
     while (CL < 16 && (ns + CL - 1) / CL > T) CL *= 2;
-    if (cl_force) CL = std::max(CL, cl_force);
+    // TDW_SOLVE_CL: any cluster size that gives every row a thread (experiments)
+    if (cl_force) CL = std::min(16, std::max((ns + T - 1) / T, cl_force));
     const int R = (ns + CL - 1) / CL;
     if (R <= T) cands.push_back({mz, CL, R, 0, 30.0 + 0.1 * R});
   }
