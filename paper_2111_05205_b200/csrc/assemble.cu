@@ -789,6 +789,37 @@ int tdw_assemble_impl(tdw_problem* pb) {
   }
   break;
   }
+  // the near kernel's results (complete: synchronised above); the solver setup
+  // below needs them while the fill kernel is still running
+  {
+    unsigned long long hc[8];
+    int hfl[4], hellw = 0;
+    TDW_CUDA(ctx, cudaMemcpy(hc, d_cnt, sizeof(hc), cudaMemcpyDeviceToHost));
+    TDW_CUDA(ctx, cudaMemcpy(hfl, pb->d_flags, sizeof(hfl), cudaMemcpyDeviceToHost));
+    TDW_CUDA(ctx, cudaMemcpy(&hellw, d_ellw, sizeof(int), cudaMemcpyDeviceToHost));
+    pb->n_near = (int64_t)hc[5];
+    pb->n_near_evals = (int64_t)hc[6];
+    pb->near_w = hfl[2];
+    pb->step_nnz = (int)hc[2];
+    double bound;
+    memcpy(&bound, &hc[3], sizeof(bound));
+    pb->jac_bound = bound;
+    pb->ell_w = hellw;
+    if (hfl[3] == 1)
+      return tdw_fail(ctx, TDW_ERR_LIMIT, "near structure: more than the supported pairs near a row");
+    // a zero diagonal: the reference's splu raises "step matrix is singular"
+    // (marching.py:284-288); the loop's solver divides by the diagonal
+    std::vector<double> dg(pb->ns);
+    TDW_CUDA(ctx, cudaMemcpy(dg.data(), pb->d_adiag, sizeof(double) * pb->ns, cudaMemcpyDeviceToHost));
+    for (int i = 0; i < pb->ns; ++i)
+      if (!(dg[i] != 0.0) || !std::isfinite(dg[i]))
+        return tdw_fail(ctx, TDW_ERR_SINGULAR, "step matrix is singular (zero diagonal)");
+    // sweeps for a contraction of 1e-17 under the infinity-norm bound (cap; the
+    // solver stops earlier once the update is at round-off); bound >= 0.9 selects
+    // the BiCGSTAB solver (tdw_setup_cluster_solver)
+    const int it = (bound > 0.0 && bound < 0.9) ? (int)ceil(log(1e-17) / log(bound)) : 400;
+    pb->jac_iters = std::max(2, std::min(it, 400));
+  }
 
   AsmArgs a{};
   a.elem = pb->d_elem;
@@ -902,6 +933,21 @@ int tdw_assemble_impl(tdw_problem* pb) {
   }
 
   TDW_CUDA(ctx, cudaEventRecord(e1, st));
+  // Cluster solver first: its CTAs' SMs are kept free of convolution CTAs so the
+  // far convolution of the next step overlaps the solve.  Its setup is host work
+  // (partition, halo sets) on the near kernel's results: it runs here, while the
+  // fill kernel -- most of the assembly's device time -- is still running.
+  {
+    const double tw1 = asm_now_ms();
+    int src = tdw_setup_cluster_solver(pb);
+    if (trace_asm)
+      fprintf(stderr, "assemble: launches + host readback %.2f ms, solver setup (beside the fill kernel) %.2f ms\n",
+              tw1 - tw0, asm_now_ms() - tw1);
+    if (src) {
+      cudaStreamSynchronize(st);
+      return src;
+    }
+  }
   TDW_CUDA(ctx, cudaStreamSynchronize(st));
   cudaFree(d_hdr_tmp);
   cudaFree(d_segcnt);
@@ -910,36 +956,10 @@ int tdw_assemble_impl(tdw_problem* pb) {
   unsigned long long hc[8];
   TDW_CUDA(ctx, cudaMemcpy(hc, d_cnt, sizeof(hc), cudaMemcpyDeviceToHost));
   TDW_CUDA(ctx, cudaMemcpy(hflags, pb->d_flags, sizeof(hflags), cudaMemcpyDeviceToHost));
-  int hellw = 0;
-  TDW_CUDA(ctx, cudaMemcpy(&hellw, d_ellw, sizeof(int), cudaMemcpyDeviceToHost));
   cudaFree(d_cnt);
   cudaFree(d_ellw);
   pb->n_evals = (int64_t)hc[0];
-  pb->n_near = (int64_t)hc[5];
-  pb->n_near_evals = (int64_t)hc[6];
-  pb->near_w = hflags[2];
   pb->n_pairs = (int64_t)hc[1];
-  pb->step_nnz = (int)hc[2];
-  double bound;
-  memcpy(&bound, &hc[3], sizeof(bound));
-  pb->jac_bound = bound;
-  pb->ell_w = hellw;
-  if (hflags[3] == 1)
-    return tdw_fail(ctx, TDW_ERR_LIMIT, "near structure: more than the supported pairs near a row");
-  // a zero diagonal: the reference's splu raises "step matrix is singular"
-  // (marching.py:284-288); the loop's solver divides by the diagonal
-  {
-    std::vector<double> dg(pb->ns);
-    TDW_CUDA(ctx, cudaMemcpy(dg.data(), pb->d_adiag, sizeof(double) * pb->ns, cudaMemcpyDeviceToHost));
-    for (int i = 0; i < pb->ns; ++i)
-      if (!(dg[i] != 0.0) || !std::isfinite(dg[i]))
-        return tdw_fail(ctx, TDW_ERR_SINGULAR, "step matrix is singular (zero diagonal)");
-  }
-  // sweeps for a contraction of 1e-17 under the infinity-norm bound (cap; the
-  // solver stops earlier once the update is at round-off); bound >= 0.9 selects
-  // the BiCGSTAB solver (tdw_setup_cluster_solver)
-  int it = (bound > 0.0 && bound < 0.9) ? (int)ceil(log(1e-17) / log(bound)) : 400;
-  pb->jac_iters = std::max(2, std::min(it, 400));
   float ms = 0.f, fms = 0.f;
   cudaEventElapsedTime(&ms, e0, e1);
   cudaEventElapsedTime(&fms, f0, f1);
@@ -949,17 +969,7 @@ int tdw_assemble_impl(tdw_problem* pb) {
   cudaEventDestroy(e1);
   cudaEventDestroy(f0);
   cudaEventDestroy(f1);
-
-  // cluster solver first: its CTAs' SMs are kept free of convolution CTAs so
-  // the far convolution of the next step overlaps the solve
-  {
-    const double tw1 = asm_now_ms();
-    int src = tdw_setup_cluster_solver(pb);
-    if (trace_asm)
-      fprintf(stderr, "assemble: device part + host readback %.2f ms, solver setup %.2f ms\n", tw1 - tw0,
-              asm_now_ms() - tw1);
-    if (src) return src;
-  }
+  if (trace_asm) fprintf(stderr, "assemble: fill kernel done at %.2f ms\n", asm_now_ms() - tw0);
   if (pb->otf) {
     // on the fly: one warp per (row, group of 8 J-tiles), partials per group
     pb->otf_tg = 8;
