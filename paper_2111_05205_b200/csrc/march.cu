@@ -40,6 +40,12 @@
 namespace tdw {
 
 #define FULLMASK 0xffffffffu
+#ifndef TDW_CONV_CHUNK_BYTES
+#define TDW_CONV_CHUNK_BYTES 32768u  // bytes per bulk copy of the unit stream (smaller measured slower, DESIGN 4.2)
+#endif
+#ifndef TDW_TSTAT
+#define TDW_TSTAT 0  // 1: build the convolution with its cycle counters (TDW_CONV_TSTAT=1 at run time)
+#endif
 #ifndef TDW_STREAM_TIMEOUT_NS
 #define TDW_STREAM_TIMEOUT_NS 150000000000ull  // a streamed pass gives up on its data after 150 s
 #endif
@@ -172,7 +178,6 @@ struct ConvArgs {
   int pf;                     // L2 prefetch distance of the unit stream (schedule entries; 0 = off)
   unsigned long long* trace;  // timeline trace (TDW_TRACE_SOLVE): slots 11, 12 of the pass's first step
   unsigned stage_bytes;  // shared-memory FIFO capacity
-  unsigned chunk;             // bytes per bulk copy of the unit stream
   const int* ready;           // streamed march: chunks of known data on the device
   int need_ready;             //   chunks this pass needs (0: not streamed)
   unsigned long long* tstat;  // optional (TDW_CONV_TSTAT, tdw_time_conv only): wait / busy cycle sums
@@ -279,7 +284,7 @@ __device__ __forceinline__ void conv_body(const ConvArgs& a, const CUtensorMap& 
     const uint64_t pol_stream = policy_evict_first(), pol_keep = policy_evict_last();
     int n = 0;  // real units issued
     long long pwait = 0;
-    const long long pstart = a.tstat ? clock64() : 0;
+    const long long pstart = (TDW_TSTAT && a.tstat) ? clock64() : 0;
     for (int base = 0; base < nent; base += 32) {
       unsigned uid = TDW_EMPTY_UNIT;
       unsigned long long off = 0, nbytes = 0;
@@ -324,9 +329,9 @@ __device__ __forceinline__ void conv_body(const ConvArgs& a, const CUtensorMap& 
         if (n >= 2 && rs2 < e && h < re2) wait_for = n - 2;
         if (n >= 1 && rs1 < e && h < re1) wait_for = n - 1;
         if (wait_for >= 0) {
-          const long long tw = a.tstat ? clock64() : 0;
+          const long long tw = (TDW_TSTAT && a.tstat) ? clock64() : 0;
           mbar_wait(&empty[wait_for & 3], (unsigned)(wait_for >> 2) & 1u);
-          if (a.tstat) pwait += clock64() - tw;
+          if (TDW_TSTAT && a.tstat) pwait += clock64() - tw;
         }
         rs3 = rs2; re3 = re2;
         rs2 = rs1; re2 = re1;
@@ -337,7 +342,7 @@ __device__ __forceinline__ void conv_body(const ConvArgs& a, const CUtensorMap& 
           mbar_expect_tx(&full[slot], qbytes + hbytes);
         }
         __syncwarp();
-        const unsigned chunk = a.chunk;
+        const unsigned chunk = TDW_CONV_CHUNK_BYTES;
         for (unsigned c = lane * chunk; c < qbytes; c += 32u * chunk) {
           const unsigned len = min(chunk, qbytes - c);
           if (a.l2hint) bulk_g2s_hint(sbase + c, a.units + qoff + c, len, &full[slot], pol_stream);
@@ -363,7 +368,7 @@ __device__ __forceinline__ void conv_body(const ConvArgs& a, const CUtensorMap& 
         ++n;
       }
     }
-    if (a.tstat && lane == 0) {
+    if (TDW_TSTAT && a.tstat && lane == 0) {
       atomicAdd(a.tstat + 0, (unsigned long long)pwait);
       atomicAdd(a.tstat + 1, (unsigned long long)(clock64() - pstart));
     }
@@ -380,7 +385,7 @@ __device__ __forceinline__ void conv_body(const ConvArgs& a, const CUtensorMap& 
   const size_t step_stride = (size_t)a.rows_loc * S;
   int n = 0;
   long long cwait = 0, cpro = 0, ckl = 0;  // TDW_CONV_TSTAT: cycles waiting for data, in the unit prologue, in the k loop
-  const long long cstart = a.tstat ? clock64() : 0;
+  const long long cstart = (TDW_TSTAT && a.tstat) ? clock64() : 0;
   for (int base = 0; base < nent; base += 32) {
     const unsigned my_uid = base + lane < nent ? a.sched[u0 + base + lane] : TDW_EMPTY_UNIT;
     const unsigned my_item = base + lane < nent ? a.sched_item[u0 + base + lane] : 0xffffffffu;
@@ -393,10 +398,10 @@ __device__ __forceinline__ void conv_body(const ConvArgs& a, const CUtensorMap& 
     const unsigned next_item = q + 1 < nb ? nxt : after;
     if (uid != TDW_EMPTY_UNIT) {
       const int stage = n % NS;
-      const long long tw = a.tstat ? clock64() : 0;
+      const long long tw = (TDW_TSTAT && a.tstat) ? clock64() : 0;
       mbar_wait(&full[stage], (unsigned)(n / NS) & 1u);
-      const long long tp0 = a.tstat ? clock64() : 0;
-      if (a.tstat) cwait += tp0 - tw;
+      const long long tp0 = (TDW_TSTAT && a.tstat) ? clock64() : 0;
+      if (TDW_TSTAT && a.tstat) cwait += tp0 - tw;
       const unsigned char* ub = sm + *(volatile unsigned*)&region[stage];
       const uint32_t* rel_off = (const uint32_t*)ub;
       const int2 g = *(const int2*)(ub + TDW_UNIT_LAG_OFF);
@@ -467,8 +472,8 @@ __device__ __forceinline__ void conv_body(const ConvArgs& a, const CUtensorMap& 
       // register renaming (no moves)
       constexpr int UK = KB == 1 ? 4 : (KB == 2 ? 4 : KB);
       if (a.dry) lmax = 0;
-      const long long tp1 = a.tstat ? clock64() : 0;
-      if (a.tstat) cpro += tp1 - tp0;
+      const long long tp1 = (TDW_TSTAT && a.tstat) ? clock64() : 0;
+      if (TDW_TSTAT && a.tstat) cpro += tp1 - tp0;
       // the block of UK entries stops at lmax (warp-uniform exit): a row with 5
       // entries costs 5 steps, not 2 * UK; the window is dead after the loop, so
       // the exit needs no register moves
@@ -499,7 +504,7 @@ __device__ __forceinline__ void conv_body(const ConvArgs& a, const CUtensorMap& 
         }
       }
     kloop_done:
-      if (a.tstat) ckl += clock64() - tp1;
+      if (TDW_TSTAT && a.tstat) ckl += clock64() - tp1;
 #pragma unroll
       for (int r = 0; r < RPW; ++r)
         if (NS1) acc[r][0] += s0[r][0] - s1[r][0];
@@ -540,7 +545,7 @@ __device__ __forceinline__ void conv_body(const ConvArgs& a, const CUtensorMap& 
     }
     }
   }
-  if (a.tstat && lane == 0) {
+  if (TDW_TSTAT && a.tstat && lane == 0) {
     atomicAdd(a.tstat + 2, (unsigned long long)cwait);
     atomicAdd(a.tstat + 3, (unsigned long long)(clock64() - cstart));
     atomicAdd(a.tstat + 4, (unsigned long long)cpro);
@@ -1862,8 +1867,6 @@ static void fill_conv_args(tdw_problem* pb, ConvArgs& c) {
   c.tstat = nullptr;
   c.ready = pb->d_ready;
   c.need_ready = 0;
-  c.chunk = 32768u;
-  if (const char* e = getenv("TDW_CONV_CHUNK")) c.chunk = (unsigned)std::max(512, atoi(e)) / 128u * 128u;  // experiments
   c.dry = 0;
   c.trace = nullptr;
   {
@@ -2732,7 +2735,9 @@ int tdw_time_conv_impl(tdw_problem* pb, int n, float* ms_out) {
     c.stats = nullptr;
   }
   c.dry = getenv("TDW_CONV_DRY") ? 1 : 0;
-  if (getenv("TDW_CONV_TSTAT")) {  // where the producer and the consumers spend their cycles (mean per warp)
+  if (getenv("TDW_CONV_TSTAT") && !TDW_TSTAT)
+    fprintf(stderr, "TDW_CONV_TSTAT needs a library built with -DTDW_TSTAT=1 (build.build(extra=('-DTDW_TSTAT=1',)))\n");
+  if (getenv("TDW_CONV_TSTAT") && TDW_TSTAT) {  // where the producer and the consumers spend their cycles (mean per warp)
     unsigned long long* dt = nullptr;
     TDW_CUDA(ctx, cudaMalloc(&dt, sizeof(unsigned long long) * 8));
     TDW_CUDA(ctx, cudaMemsetAsync(dt, 0, sizeof(unsigned long long) * 8, st));
