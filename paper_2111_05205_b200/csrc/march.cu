@@ -1585,19 +1585,22 @@ __device__ __forceinline__ double ldg_keep(const double* p, uint64_t pol) {
 }
 
 #ifndef TDW_NEAR_MINB
-#define TDW_NEAR_MINB 12  // 40 registers: no spills; still two blocks beside a conv_kernel_wg CTA
+#define TDW_NEAR_MINB 12  // <= 40 registers: still two blocks beside a conv_kernel_wg CTA
 #endif
-template <int NCH>  // 32-entry chunks per row: ceil(near_w / 32), rounded up to an instantiated size
-__global__ void __launch_bounds__(128, TDW_NEAR_MINB) near_step_kernel(const int* __restrict__ nptr,
-                                                        const int* __restrict__ ncnt,
-                                                        const int* __restrict__ ncol_c,
-                                                        const double* __restrict__ nval_c, long long nnz,
+// near_step_kernel: N^gamma x^{alpha-1} for the split lags gamma = g0+2 .. g1+1 that are
+// not formed in the solve's tail.  The near structure is stored per (lag, row) as a
+// CSR of its NONZERO entries only (a pair's band covers ~3 of the ~10 split lags, so
+// the dense [lag][pair] form streamed 3x the bytes): ptr[g][ns + 1], columns with the
+// sign bit set where the unknown is u (phi_j = 1).  One warp per row, entries strided
+// over the lanes in fixed order, four gathers in flight per lane.
+__global__ void __launch_bounds__(128, TDW_NEAR_MINB) near_step_kernel(const int* __restrict__ ptr,
+                                                        const int* __restrict__ col,
+                                                        const double* __restrict__ val,
                                                         int ns, int nsl, const double2* __restrict__ hist,
                                                         int hcols, int pad, double* __restrict__ bnear,
                                                         int alpha, int g0, int g1, const int* flags,
                                                         unsigned long long* trace) {
-  // 32 registers: three 4-warp blocks fit beside a convolution CTA (the kernel
-  // runs in situ, where residency, not ILP, sets its time)
+  // the kernel runs in situ beside the convolution, where residency, not ILP, sets its time
   if (*(volatile const int*)flags != 0) return;
   unsigned long long* ttr = trace ? trace + (size_t)alpha * 16 + 9 : nullptr;
   trace_begin(ttr);
@@ -1606,28 +1609,28 @@ __global__ void __launch_bounds__(128, TDW_NEAR_MINB) near_step_kernel(const int
   if (i >= ns) return;
   const uint64_t keep = policy_keep_l2();  // the near structure is re-read every step
   const double2* hrow = hist + (size_t)(pad + alpha - 1) * hcols;
-  const int p0 = __ldg(nptr + i), cnt = __ldg(ncnt + i);
-  // every load of the row issued up front (latency-bound otherwise): columns,
-  // then the history gathers
-  int jj[NCH];
-  double xv[NCH];
-#pragma unroll
-  for (int m = 0; m < NCH; ++m) jj[m] = 32 * m + lane < cnt ? ldg_keep(ncol_c + p0 + 32 * m + lane, keep) : 0;
-#pragma unroll
-  for (int m = 0; m < NCH; ++m) {
-    xv[m] = 0.0;
-    if (32 * m + lane < cnt) {
-      const double2 h = __ldcg(hrow + (jj[m] & 0x7fffffff));
-      xv[m] = jj[m] < 0 ? h.y : h.x;  // sign bit: phi_j = 1, the unknown is u
-    }
-  }
   const int ring = nsl + 1;
   for (int g = g0; g < g1; ++g) {
-    const double* vrow = nval_c + (size_t)g * nnz + p0 + lane;
+    const int* pp = ptr + (size_t)g * (ns + 1) + i;
+    const int p0 = __ldg(pp), p1 = __ldg(pp + 1);
     double v = 0.0;
+    for (int e0 = p0 + lane; e0 < p1; e0 += 128) {
+      int jj[4];
+      double w[4];
 #pragma unroll
-    for (int m = 0; m < NCH; ++m)
-      if (32 * m + lane < cnt) v = fma(ldg_keep(vrow + 32 * m, keep), xv[m], v);
+      for (int m = 0; m < 4; ++m) {
+        const int e = e0 + 32 * m;
+        jj[m] = e < p1 ? ldg_keep(col + e, keep) : 0;
+        w[m] = e < p1 ? ldg_keep(val + e, keep) : 0.0;
+      }
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        if (e0 + 32 * m < p1) {
+          const double2 h = __ldcg(hrow + (jj[m] & 0x7fffffff));
+          v = fma(w[m], jj[m] < 0 ? h.y : h.x, v);  // sign bit: phi_j = 1, the unknown is u
+        }
+      }
+    }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULLMASK, v, o);
     if (lane == 0) bnear[((size_t)g * ring + (alpha + 1 + g) % ring) * ns + i] = v;
@@ -1635,18 +1638,11 @@ __global__ void __launch_bounds__(128, TDW_NEAR_MINB) near_step_kernel(const int
   trace_end(ttr);
 }
 
-// compact row-major copy of the near structure for near_step_kernel
-__global__ void near_compact_kernel(const int* ncol, const double* nval, const double* phi, int ns, int nsl,
-                                    const int* nptr, const int* ncnt, long long nnz, int* ncol_c,
-                                    double* nval_c) {
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < (long long)ns * TDW_NEAR_MAX;
-       e += (long long)gridDim.x * blockDim.x) {
-    const int i = (int)(e / TDW_NEAR_MAX), k = (int)(e % TDW_NEAR_MAX);
-    if (k >= ncnt[i]) continue;
-    const int j = ncol[(size_t)k * ns + i];
-    ncol_c[nptr[i] + k] = j | (phi[j] == 1.0 ? (int)0x80000000 : 0);
-    for (int g = 0; g < nsl; ++g)
-      nval_c[(size_t)g * nnz + nptr[i] + k] = nval[(size_t)g * TDW_NEAR_MAX * ns + (size_t)k * ns + i];
+// near columns in the cluster solver's (owner CTA << 24 | owner-local row) packing
+__global__ void near_pack_kernel(const int* __restrict__ ncol, int* __restrict__ packed, size_t n, int R) {
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < n; e += (size_t)gridDim.x * blockDim.x) {
+    const int j = ncol[e];
+    packed[e] = ((j / R) << 24) | (j % R);
   }
 }
 
@@ -2071,17 +2067,8 @@ int launch_solve(tdw_problem* pb, LoopPlan& L, int alpha, cudaStream_t s) {
 int launch_near(tdw_problem* pb, int alpha, int g0, int g1, cudaStream_t s) {
   const long long threads = (long long)pb->ns * 32;
   const unsigned grid = (unsigned)((threads + 127) / 128);
-  const int nch = (pb->near_w + 31) / 32;
-#define TDW_NEAR_LAUNCH(N)                                                                                  \
-  near_step_kernel<N><<<grid, 128, 0, s>>>(pb->d_nptr, pb->d_ncnt, pb->d_ncol_rm, pb->d_nval_rm,            \
-                                           (long long)pb->n_near, pb->ns, pb->nsl, pb->d_hist, pb->hcols,   \
-                                           pb->pad, pb->d_bnear, alpha, g0, g1, pb->d_flags, pb->d_trace)
-  if (nch <= 4) TDW_NEAR_LAUNCH(4);
-  else if (nch <= 6) TDW_NEAR_LAUNCH(6);
-  else if (nch <= 8) TDW_NEAR_LAUNCH(8);
-  else if (nch <= 10) TDW_NEAR_LAUNCH(10);
-  else TDW_NEAR_LAUNCH(TDW_NEAR_MAX / 32);
-#undef TDW_NEAR_LAUNCH
+  near_step_kernel<<<grid, 128, 0, s>>>(pb->d_n3_ptr, pb->d_n3_col, pb->d_n3_val, pb->ns, pb->nsl, pb->d_hist,
+                                        pb->hcols, pb->pad, pb->d_bnear, alpha, g0, g1, pb->d_flags, pb->d_trace);
   TDW_CUDA(pb->ctx, cudaGetLastError());
   return TDW_OK;
 }
@@ -2735,9 +2722,10 @@ int tdw_time_conv_impl(tdw_problem* pb, int n, float* ms_out) {
     c.stats = nullptr;
   }
   c.dry = getenv("TDW_CONV_DRY") ? 1 : 0;
-  if (getenv("TDW_CONV_TSTAT") && !TDW_TSTAT)
+  const bool want_tstat = getenv("TDW_CONV_TSTAT") != nullptr;
+  if (want_tstat && !TDW_TSTAT)
     fprintf(stderr, "TDW_CONV_TSTAT needs a library built with -DTDW_TSTAT=1 (build.build(extra=('-DTDW_TSTAT=1',)))\n");
-  if (getenv("TDW_CONV_TSTAT") && TDW_TSTAT) {  // where the producer and the consumers spend their cycles (mean per warp)
+  if (want_tstat && TDW_TSTAT) {  // where the producer and the consumers spend their cycles (mean per warp)
     unsigned long long* dt = nullptr;
     TDW_CUDA(ctx, cudaMalloc(&dt, sizeof(unsigned long long) * 8));
     TDW_CUDA(ctx, cudaMemsetAsync(dt, 0, sizeof(unsigned long long) * 8, st));
@@ -2796,8 +2784,8 @@ int tdw_outputs(tdw_problem* pb, double* u, double* q, double* tau, double* sigm
 // TDW_HALO=h caps it); h = 1 would equal the plain solver, so h >= 2.
 // The solve tail's CSR (lags 2..want+1 of the near structure, nonzero entries,
 // columns packed (owner CTA << 24) | owner-local row for R rows per CTA)
-__global__ void tail_csr_count_kernel(const double* __restrict__ nval, const int* __restrict__ ncnt, int ns,
-                                      int want, int* cnt) {
+__global__ void lag_csr_count_kernel(const double* __restrict__ nval, const int* __restrict__ ncnt, int ns,
+                                     int want, int* cnt) {
   const size_t n = (size_t)want * (ns + 1);
   for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < n; e += (size_t)gridDim.x * blockDim.x) {
     const int g = (int)(e / (ns + 1)), s1 = (int)(e % (ns + 1));
@@ -2810,9 +2798,12 @@ __global__ void tail_csr_count_kernel(const double* __restrict__ nval, const int
   }
 }
 
-__global__ void tail_csr_fill_kernel(const int* __restrict__ ncol, const double* __restrict__ nval,
-                                     const int* __restrict__ ncnt, int ns, int want, int R,
-                                     const int* __restrict__ ptr, int* col, double* val) {
+// R > 0: columns packed for the cluster (owner CTA << 24 | local row); R == 0: the
+// global column, sign bit set where phi_j = 1 (near_step_kernel)
+__global__ void lag_csr_fill_kernel(const int* __restrict__ ncol, const double* __restrict__ nval,
+                                    const int* __restrict__ ncnt, int ns, int want, int R,
+                                    const double* __restrict__ phi, const int* __restrict__ ptr, int* col,
+                                    double* val) {
   const size_t n = (size_t)want * ns;
   for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < n; e += (size_t)gridDim.x * blockDim.x) {
     const int g = (int)(e / ns), i = (int)(e % ns);
@@ -2821,7 +2812,7 @@ __global__ void tail_csr_fill_kernel(const int* __restrict__ ncol, const double*
       const double w = nval[((size_t)g * TDW_NEAR_MAX + k) * ns + i];
       if (w == 0.0) continue;
       const int j = ncol[(size_t)k * ns + i];
-      col[pos] = ((j / R) << 24) | (j % R);
+      col[pos] = R > 0 ? (((j / R) << 24) | (j % R)) : (j | (phi[j] == 1.0 ? (int)0x80000000 : 0));
       val[pos] = w;
       ++pos;
     }
@@ -2980,36 +2971,52 @@ static int setup_halo(tdw_problem* pb, const std::vector<int>& acol, const std::
   return TDW_OK;
 }
 
-// The near structure in the forms the loop reads: columns in the cluster's
-// (owner CTA, local row) packing for R rows per CTA, and the compact row-major
-// copy near_step_kernel streams.
-static int build_near_compact(tdw_problem* pb, int R) {
+// CSR of the nonzero near values of lags 2 .. want+1, per (lag, row), on the
+// device: the count per (lag, row), one inclusive scan over [want][ns + 1] (a zero
+// at each lag's slot 0) gives the row pointers with global offsets, then the fill
+// in the near structure's column order.
+static int build_lag_csr(tdw_problem* pb, int want, int R, int** ptr, int** col, double** val) {
   tdw_ctx* ctx = pb->ctx;
   const int ns = pb->ns;
-  {
-    // near columns in the cluster's (owner, local) packing
-    std::vector<int> ncol((size_t)TDW_NEAR_MAX * ns);
-    TDW_CUDA(ctx, cudaMemcpy(ncol.data(), pb->d_ncol, sizeof(int) * ncol.size(), cudaMemcpyDeviceToHost));
-    for (int& j : ncol) j = ((j / R) << 24) | (j % R);
-    TDW_CUDA(ctx, cudaMalloc(&pb->d_ncol_packed, sizeof(int) * ncol.size()));
-    TDW_CUDA(ctx, cudaMemcpy(pb->d_ncol_packed, ncol.data(), sizeof(int) * ncol.size(), cudaMemcpyHostToDevice));
-    // compact row-major near structure for near_step_kernel
-    std::vector<int> cnt(ns), ptr(ns);
-    TDW_CUDA(ctx, cudaMemcpy(cnt.data(), pb->d_ncnt, sizeof(int) * ns, cudaMemcpyDeviceToHost));
-    long long nnz = 0;
-    for (int i = 0; i < ns; ++i) {
-      ptr[i] = (int)nnz;
-      nnz += cnt[i];
-    }
-    pb->n_near = nnz;
-    TDW_CUDA(ctx, cudaMalloc(&pb->d_nptr, sizeof(int) * ns));
-    TDW_CUDA(ctx, cudaMemcpy(pb->d_nptr, ptr.data(), sizeof(int) * ns, cudaMemcpyHostToDevice));
-    TDW_CUDA(ctx, cudaMalloc(&pb->d_ncol_rm, sizeof(int) * std::max(1LL, nnz)));
-    TDW_CUDA(ctx, cudaMalloc(&pb->d_nval_rm, sizeof(double) * std::max(1LL, nnz * pb->nsl)));
-    near_compact_kernel<<<2 * ctx->num_sms, 256, 0, ctx->stream>>>(pb->d_ncol, pb->d_nval, pb->d_phi, ns,
-                                                                  pb->nsl, pb->d_nptr, pb->d_ncnt, nnz,
-                                                                  pb->d_ncol_rm, pb->d_nval_rm);
-    TDW_CUDA(ctx, cudaGetLastError());
+  int* d_cnt = nullptr;
+  const size_t nptr = (size_t)want * (ns + 1);
+  TDW_CUDA(ctx, cudaMalloc(ptr, sizeof(int) * nptr));
+  TDW_CUDA(ctx, cudaMalloc(&d_cnt, sizeof(int) * nptr));
+  const int blocks = (int)std::min<size_t>(4096, (nptr + 255) / 256);
+  lag_csr_count_kernel<<<blocks, 256, 0, ctx->stream>>>(pb->d_nval, pb->d_ncnt, ns, want, d_cnt);
+  TDW_CUDA(ctx, cudaGetLastError());
+  size_t tmp_bytes = 0;
+  cub::DeviceScan::InclusiveSum(nullptr, tmp_bytes, d_cnt, *ptr, (int)nptr, ctx->stream);
+  void* tmp = nullptr;
+  TDW_CUDA(ctx, cudaMalloc(&tmp, std::max<size_t>(1, tmp_bytes)));
+  cub::DeviceScan::InclusiveSum(tmp, tmp_bytes, d_cnt, *ptr, (int)nptr, ctx->stream);
+  TDW_CUDA(ctx, cudaGetLastError());
+  int total = 0;
+  TDW_CUDA(ctx, cudaMemcpyAsync(&total, *ptr + nptr - 1, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  TDW_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  cudaFree(tmp);
+  cudaFree(d_cnt);
+  TDW_CUDA(ctx, cudaMalloc(col, sizeof(int) * std::max(1, total)));
+  TDW_CUDA(ctx, cudaMalloc(val, sizeof(double) * std::max(1, total)));
+  lag_csr_fill_kernel<<<blocks, 256, 0, ctx->stream>>>(pb->d_ncol, pb->d_nval, pb->d_ncnt, ns, want, R, pb->d_phi,
+                                                       *ptr, *col, *val);
+  TDW_CUDA(ctx, cudaGetLastError());
+  return TDW_OK;
+}
+
+// The near structure in the forms the loop reads: columns in the cluster's
+// (owner CTA, local row) packing for R rows per CTA, and the per-(lag, row) CSR
+// of its nonzero values that near_step_kernel streams (every split lag: the loop
+// chooses which of them the solve's tail takes).
+static int build_near_compact(tdw_problem* pb, int R) {
+  tdw_ctx* ctx = pb->ctx;
+  const size_t n = (size_t)TDW_NEAR_MAX * pb->ns;
+  TDW_CUDA(ctx, cudaMalloc(&pb->d_ncol_packed, sizeof(int) * n));
+  near_pack_kernel<<<2 * ctx->num_sms, 256, 0, ctx->stream>>>(pb->d_ncol, pb->d_ncol_packed, n, R);
+  TDW_CUDA(ctx, cudaGetLastError());
+  if (pb->nsl > 0 && pb->near_w > 0) {
+    int rc = build_lag_csr(pb, pb->nsl, 0, &pb->d_n3_ptr, &pb->d_n3_col, &pb->d_n3_val);
+    if (rc) return rc;
   }
   return TDW_OK;
 }
@@ -3187,32 +3194,8 @@ int tdw_setup_cluster_solver(tdw_problem* pb) {
     // near step of step s is then needed only near_tail + 1 solves later
     const int want = std::min(e ? atoi(e) : (pb->kb == 5 ? 3 : (pb->kb >= 6 ? 2 : 1)), pb->nsl);
     if (want > 0 && pb->sp_reg > 0 && pb->sp_halo > 0 && pb->split_lag2 && pb->near_w > 0) {
-      // on the device: per (lag, row) the nonzero count, one inclusive scan over
-      // [want][ns + 1] (a zero at each lag's slot 0) gives the row pointers with
-      // global offsets, then the fill in the near structure's column order
-      int* d_cnt = nullptr;
-      const size_t nptr = (size_t)want * (ns + 1);
-      TDW_CUDA(ctx, cudaMalloc(&pb->d_n2_ptr, sizeof(int) * nptr));
-      TDW_CUDA(ctx, cudaMalloc(&d_cnt, sizeof(int) * nptr));
-      const int blocks = (int)std::min<size_t>(4096, (nptr + 255) / 256);
-      tail_csr_count_kernel<<<blocks, 256, 0, ctx->stream>>>(pb->d_nval, pb->d_ncnt, ns, want, d_cnt);
-      TDW_CUDA(ctx, cudaGetLastError());
-      size_t tmp_bytes = 0;
-      cub::DeviceScan::InclusiveSum(nullptr, tmp_bytes, d_cnt, pb->d_n2_ptr, (int)nptr, ctx->stream);
-      void* tmp = nullptr;
-      TDW_CUDA(ctx, cudaMalloc(&tmp, std::max<size_t>(1, tmp_bytes)));
-      cub::DeviceScan::InclusiveSum(tmp, tmp_bytes, d_cnt, pb->d_n2_ptr, (int)nptr, ctx->stream);
-      TDW_CUDA(ctx, cudaGetLastError());
-      int total = 0;
-      TDW_CUDA(ctx, cudaMemcpyAsync(&total, pb->d_n2_ptr + nptr - 1, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
-      TDW_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
-      cudaFree(tmp);
-      cudaFree(d_cnt);
-      TDW_CUDA(ctx, cudaMalloc(&pb->d_n2_col, sizeof(int) * std::max(1, total)));
-      TDW_CUDA(ctx, cudaMalloc(&pb->d_n2_val, sizeof(double) * std::max(1, total)));
-      tail_csr_fill_kernel<<<blocks, 256, 0, ctx->stream>>>(pb->d_ncol, pb->d_nval, pb->d_ncnt, ns, want, R,
-                                                            pb->d_n2_ptr, pb->d_n2_col, pb->d_n2_val);
-      TDW_CUDA(ctx, cudaGetLastError());
+      int rc = build_lag_csr(pb, want, R, &pb->d_n2_ptr, &pb->d_n2_col, &pb->d_n2_val);
+      if (rc) return rc;
       pb->near_in_solve = true;
       pb->near_tail = want;
     }

@@ -142,12 +142,11 @@ struct tdw_problem {
   int* d_ncol = nullptr;
   double* d_nval = nullptr;
   int* d_ncol_packed = nullptr;    // ncol in the cluster solver's (owner << 24 | local) form
-  // compact row-major copy for near_step_kernel: row i holds ncnt[i] entries at
-  // nptr[i]: columns (sign bit = phi_j) and values [nsl][n_near]
-  int* d_ncnt = nullptr;
-  int* d_nptr = nullptr;
-  int* d_ncol_rm = nullptr;
-  double* d_nval_rm = nullptr;
+  int* d_ncnt = nullptr;           // near pairs per row
+  // near_step_kernel's form: CSR of the nonzero near values per (split lag, row)
+  int* d_n3_ptr = nullptr;         // [nsl][ns + 1]
+  int* d_n3_col = nullptr;         // column | sign bit (phi_j = 1)
+  double* d_n3_val = nullptr;
   double* d_bnear = nullptr;       // [nsl][nsl+1][ns]: N_g x^(beta-1) after solve(beta), for step beta-1+g
   // pipelined loop: side stream for the far convolution, per-step events
   cudaStream_t side = nullptr;
