@@ -720,7 +720,7 @@ int tdw_problem_destroy(tdw_problem* pb) {
                   pb->d_qk, pb->d_bpart, pb->d_b, pb->d_x, pb->d_red, pb->d_bar, pb->d_flags,
                   pb->d_rhs, pb->d_sp_rowptr, pb->d_sp_nnzoff, pb->d_sp_col, pb->d_sp_val,
                   pb->d_ncol, pb->d_nval, pb->d_ncol_packed, pb->d_h_ncomp, pb->d_h_gi, pb->d_h_layer, pb->d_h_nz, pb->d_h_col,
-                  pb->d_h_ngat, pb->d_h_gdst, pb->d_h_gsrc, pb->d_h_val, pb->d_ncnt, pb->d_n3_ptr, pb->d_n3_col, pb->d_n3_val, pb->d_bnear, pb->d_out, pb->d_trace, pb->d_n2_ptr, pb->d_n2_col, pb->d_n2_val};
+                  pb->d_h_ngat, pb->d_h_gdst, pb->d_h_gsrc, pb->d_h_val, pb->d_ncnt, pb->d_n3_ptr, pb->d_n3_ent, pb->d_bnear, pb->d_out, pb->d_trace, pb->d_n2_ptr, pb->d_n2_col, pb->d_n2_val};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (pb->graph_exec) cudaGraphExecDestroy(pb->graph_exec);

@@ -1590,17 +1590,23 @@ __device__ __forceinline__ double ldg_keep(const double* p, uint64_t pol) {
 // near_step_kernel: N^gamma x^{alpha-1} for the split lags gamma = g0+2 .. g1+1 that are
 // not formed in the solve's tail.  The near structure is stored per (lag, row) as a
 // CSR of its NONZERO entries only (a pair's band covers ~3 of the ~10 split lags, so
-// the dense [lag][pair] form streamed 3x the bytes): ptr[g][ns + 1], columns with the
-// sign bit set where the unknown is u (phi_j = 1).  One warp per row, entries strided
-// over the lanes in fixed order, four gathers in flight per lane.
+// the dense [lag][pair] form streamed 3x the bytes): ptr[g][ns + 1] and 16-byte
+// entries (value, column) with the column's sign bit set where the unknown is u
+// (phi_j = 1).  One warp per row, entries strided over the lanes in fixed order.
+// The kernel runs beside the convolution, two blocks per SM at most, so its time
+// is (loads per row) x (memory latency under load): one load per entry plus one
+// 8-byte gather, six entries in flight per lane.
+__device__ __forceinline__ double2 ldg_keep2(const double2* p, uint64_t pol) {
+  double2 v;
+  asm("ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(v.x), "=d"(v.y) : "l"(p), "l"(pol));
+  return v;
+}
 __global__ void __launch_bounds__(128, TDW_NEAR_MINB) near_step_kernel(const int* __restrict__ ptr,
-                                                        const int* __restrict__ col,
-                                                        const double* __restrict__ val,
+                                                        const double2* __restrict__ ent,
                                                         int ns, int nsl, const double2* __restrict__ hist,
                                                         int hcols, int pad, double* __restrict__ bnear,
                                                         int alpha, int g0, int g1, const int* flags,
                                                         unsigned long long* trace) {
-  // the kernel runs in situ beside the convolution, where residency, not ILP, sets its time
   if (*(volatile const int*)flags != 0) return;
   unsigned long long* ttr = trace ? trace + (size_t)alpha * 16 + 9 : nullptr;
   trace_begin(ttr);
@@ -1608,28 +1614,26 @@ __global__ void __launch_bounds__(128, TDW_NEAR_MINB) near_step_kernel(const int
   const int i = (int)(((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
   if (i >= ns) return;
   const uint64_t keep = policy_keep_l2();  // the near structure is re-read every step
-  const double2* hrow = hist + (size_t)(pad + alpha - 1) * hcols;
+  const double* hrow = (const double*)(hist + (size_t)(pad + alpha - 1) * hcols);  // (q, u) pairs
   const int ring = nsl + 1;
+  constexpr int U = 6;
   for (int g = g0; g < g1; ++g) {
     const int* pp = ptr + (size_t)g * (ns + 1) + i;
     const int p0 = __ldg(pp), p1 = __ldg(pp + 1);
     double v = 0.0;
-    for (int e0 = p0 + lane; e0 < p1; e0 += 128) {
-      int jj[4];
-      double w[4];
+    for (int e0 = p0 + lane; e0 < p1; e0 += 32 * U) {
+      double2 en[U];
 #pragma unroll
-      for (int m = 0; m < 4; ++m) {
-        const int e = e0 + 32 * m;
-        jj[m] = e < p1 ? ldg_keep(col + e, keep) : 0;
-        w[m] = e < p1 ? ldg_keep(val + e, keep) : 0.0;
+      for (int m = 0; m < U; ++m)
+        en[m] = e0 + 32 * m < p1 ? ldg_keep2(ent + e0 + 32 * m, keep) : make_double2(0.0, 0.0);
+      double x[U];
+#pragma unroll
+      for (int m = 0; m < U; ++m) {
+        const int j = (int)__double_as_longlong(en[m].y);  // sign bit: phi_j = 1, the unknown is u
+        x[m] = e0 + 32 * m < p1 ? __ldcg(hrow + 2 * (j & 0x7fffffff) + (j < 0 ? 1 : 0)) : 0.0;
       }
 #pragma unroll
-      for (int m = 0; m < 4; ++m) {
-        if (e0 + 32 * m < p1) {
-          const double2 h = __ldcg(hrow + (jj[m] & 0x7fffffff));
-          v = fma(w[m], jj[m] < 0 ? h.y : h.x, v);  // sign bit: phi_j = 1, the unknown is u
-        }
-      }
+      for (int m = 0; m < U; ++m) v = fma(en[m].x, x[m], v);
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULLMASK, v, o);
@@ -2067,7 +2071,7 @@ int launch_solve(tdw_problem* pb, LoopPlan& L, int alpha, cudaStream_t s) {
 int launch_near(tdw_problem* pb, int alpha, int g0, int g1, cudaStream_t s) {
   const long long threads = (long long)pb->ns * 32;
   const unsigned grid = (unsigned)((threads + 127) / 128);
-  near_step_kernel<<<grid, 128, 0, s>>>(pb->d_n3_ptr, pb->d_n3_col, pb->d_n3_val, pb->ns, pb->nsl, pb->d_hist,
+  near_step_kernel<<<grid, 128, 0, s>>>(pb->d_n3_ptr, pb->d_n3_ent, pb->ns, pb->nsl, pb->d_hist,
                                         pb->hcols, pb->pad, pb->d_bnear, alpha, g0, g1, pb->d_flags, pb->d_trace);
   TDW_CUDA(pb->ctx, cudaGetLastError());
   return TDW_OK;
@@ -2803,7 +2807,7 @@ __global__ void lag_csr_count_kernel(const double* __restrict__ nval, const int*
 __global__ void lag_csr_fill_kernel(const int* __restrict__ ncol, const double* __restrict__ nval,
                                     const int* __restrict__ ncnt, int ns, int want, int R,
                                     const double* __restrict__ phi, const int* __restrict__ ptr, int* col,
-                                    double* val) {
+                                    double* val, double2* ent) {
   const size_t n = (size_t)want * ns;
   for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < n; e += (size_t)gridDim.x * blockDim.x) {
     const int g = (int)(e / ns), i = (int)(e % ns);
@@ -2812,8 +2816,13 @@ __global__ void lag_csr_fill_kernel(const int* __restrict__ ncol, const double* 
       const double w = nval[((size_t)g * TDW_NEAR_MAX + k) * ns + i];
       if (w == 0.0) continue;
       const int j = ncol[(size_t)k * ns + i];
-      col[pos] = R > 0 ? (((j / R) << 24) | (j % R)) : (j | (phi[j] == 1.0 ? (int)0x80000000 : 0));
-      val[pos] = w;
+      if (R > 0) {
+        col[pos] = ((j / R) << 24) | (j % R);
+        val[pos] = w;
+      } else {  // near_step_kernel's 16-byte entries
+        const int c = j | (phi[j] == 1.0 ? (int)0x80000000 : 0);
+        ent[pos] = make_double2(w, __longlong_as_double((long long)c));
+      }
       ++pos;
     }
   }
@@ -2975,7 +2984,8 @@ static int setup_halo(tdw_problem* pb, const std::vector<int>& acol, const std::
 // device: the count per (lag, row), one inclusive scan over [want][ns + 1] (a zero
 // at each lag's slot 0) gives the row pointers with global offsets, then the fill
 // in the near structure's column order.
-static int build_lag_csr(tdw_problem* pb, int want, int R, int** ptr, int** col, double** val) {
+static int build_lag_csr(tdw_problem* pb, int want, int R, int** ptr, int** col, double** val,
+                         double2** ent = nullptr) {
   tdw_ctx* ctx = pb->ctx;
   const int ns = pb->ns;
   int* d_cnt = nullptr;
@@ -2996,10 +3006,15 @@ static int build_lag_csr(tdw_problem* pb, int want, int R, int** ptr, int** col,
   TDW_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
   cudaFree(tmp);
   cudaFree(d_cnt);
-  TDW_CUDA(ctx, cudaMalloc(col, sizeof(int) * std::max(1, total)));
-  TDW_CUDA(ctx, cudaMalloc(val, sizeof(double) * std::max(1, total)));
+  if (ent) {
+    TDW_CUDA(ctx, cudaMalloc(ent, sizeof(double2) * std::max(1, total)));
+  } else {
+    TDW_CUDA(ctx, cudaMalloc(col, sizeof(int) * std::max(1, total)));
+    TDW_CUDA(ctx, cudaMalloc(val, sizeof(double) * std::max(1, total)));
+  }
   lag_csr_fill_kernel<<<blocks, 256, 0, ctx->stream>>>(pb->d_ncol, pb->d_nval, pb->d_ncnt, ns, want, R, pb->d_phi,
-                                                       *ptr, *col, *val);
+                                                       *ptr, ent ? nullptr : *col, ent ? nullptr : *val,
+                                                       ent ? *ent : nullptr);
   TDW_CUDA(ctx, cudaGetLastError());
   return TDW_OK;
 }
@@ -3015,7 +3030,7 @@ static int build_near_compact(tdw_problem* pb, int R) {
   near_pack_kernel<<<2 * ctx->num_sms, 256, 0, ctx->stream>>>(pb->d_ncol, pb->d_ncol_packed, n, R);
   TDW_CUDA(ctx, cudaGetLastError());
   if (pb->nsl > 0 && pb->near_w > 0) {
-    int rc = build_lag_csr(pb, pb->nsl, 0, &pb->d_n3_ptr, &pb->d_n3_col, &pb->d_n3_val);
+    int rc = build_lag_csr(pb, pb->nsl, 0, &pb->d_n3_ptr, nullptr, nullptr, &pb->d_n3_ent);
     if (rc) return rc;
   }
   return TDW_OK;

@@ -15,7 +15,7 @@
 #define TDW_TI 32        // rows per I-block (one conv CTA)
 #define TDW_ELL_MAX 64   // max nnz per row of the lag-1 step matrix
 #define TDW_KB_MAX 6     // time steps per convolution pass (temporal blocking)
-#define TDW_NEAR_MAX 320 // max pairs per row in the near structure (bands reaching a split lag)
+#define TDW_NEAR_MAX 384 // max pairs per row in the near structure (bands reaching a split lag)
 #define TDW_NSL_MAX (2 * TDW_KB_MAX - 1)  // max split lags
 #define TDW_ELEM_STRIDE 16  // doubles per element record: v0 v1 v2 n c rad
 // Unit layout (one (I-block, J-tile) unit = one contiguous byte range of the store):
@@ -145,8 +145,7 @@ struct tdw_problem {
   int* d_ncnt = nullptr;           // near pairs per row
   // near_step_kernel's form: CSR of the nonzero near values per (split lag, row)
   int* d_n3_ptr = nullptr;         // [nsl][ns + 1]
-  int* d_n3_col = nullptr;         // column | sign bit (phi_j = 1)
-  double* d_n3_val = nullptr;
+  double2* d_n3_ent = nullptr;     // (value, column | sign bit where phi_j = 1)
   double* d_bnear = nullptr;       // [nsl][nsl+1][ns]: N_g x^(beta-1) after solve(beta), for step beta-1+g
   // pipelined loop: side stream for the far convolution, per-step events
   cudaStream_t side = nullptr;
