@@ -476,7 +476,7 @@ def test_on_the_fly_mode_matches_reference(cfg):
 
 
 @pytest.mark.parametrize("cfg", [0, 2])
-def test_streamed_march_matches_preloaded(cfg):
+def test_streamed_march_matches_preloaded(cfg, monkeypatch):
     """march() with host data callables runs the streamed loop (the device takes
     each chunk of Greville samples as soon as the host has written it,
     tdw_march_stream_begin/finish): the same densities as the loop on data
@@ -500,6 +500,11 @@ def test_streamed_march_matches_preloaded(cfg):
         # (tdw_march_stream_outputs): the same values as the download at the end
         np.testing.assert_array_equal(h.tau, ref.tau)
         np.testing.assert_array_equal(h.sigma, ref.sigma)
+    # without registered outputs tdw_march_stream_finish copies everything at the end
+    monkeypatch.setenv("TDW_STREAM_OUT", "0")
+    h = marching.march(plain, mats=store)
+    for name in ("u", "q", "tau", "sigma"):
+        np.testing.assert_array_equal(getattr(h, name), getattr(ref, name))
 
 
 def test_streamed_outputs_of_an_unstable_march():
