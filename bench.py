@@ -369,6 +369,11 @@ def run_ours(args, world, rank, local):
     tk = store.run_resident(thr, args.steps, time_kernels=True)
     barrier()
     conv_ms = max_over_ranks(tk["conv_ms"] / max(tk["conv_launches"], 1))
+    # the same kernel launched back to back with nothing beside it (outside the timed region)
+    try:
+        conv_alone_ms = max_over_ranks(store.time_conv(20))
+    except Exception:
+        conv_alone_ms = None
 
     # e2e: public API with host buffers, every step, with the REFERENCE's data
     # contract: plain per-step callables u_data(t) / q_data(t), called once per
@@ -506,6 +511,13 @@ def run_ours(args, world, rank, local):
                          "bytes_per_launch": 16.0 * n_band,
                          "traffic_source": traffic_src,
                          "traffic_over_algorithmic": (traffic / (16.0 * n_band)) if traffic else None,
+                         "kernel_alone": ({"avg_launch_ms": conv_alone_ms,
+                                           "achieved": 16.0 * n_band / (conv_alone_ms * 1e-3) / 1e9,
+                                           "frac": 16.0 * n_band / (conv_alone_ms * 1e-3) / 1e9 / peak,
+                                           "note": "20 launches back to back with nothing beside them; "
+                                                   "achieved / frac above are the launches INSIDE the timed "
+                                                   "loops, where the solve cluster and the near steps run "
+                                                   "beside the pass"} if conv_alone_ms else None),
                          "note": "algorithmic bytes per launch = 16 B x N_band (V_U, V_W fp64, the "
                                  "store read once); a launch computes kb MOT steps from that read "
                                  "(see blocking)"},

@@ -1584,6 +1584,9 @@ __device__ __forceinline__ double ldg_keep(const double* p, uint64_t pol) {
   return v;
 }
 
+#ifndef TDW_NEAR_U
+#define TDW_NEAR_U 3  // near entries in flight per lane (config 2, steps/s in the loop: 3 >= 4 > 6 by 0.5-1%: fewer predicated-off slots beside the pass)
+#endif
 #ifndef TDW_NEAR_MINB
 #define TDW_NEAR_MINB 12  // <= 40 registers: still two blocks beside a conv_kernel_wg CTA
 #endif
@@ -1595,7 +1598,7 @@ __device__ __forceinline__ double ldg_keep(const double* p, uint64_t pol) {
 // (phi_j = 1).  One warp per row, entries strided over the lanes in fixed order.
 // The kernel runs beside the convolution, two blocks per SM at most, so its time
 // is (loads per row) x (memory latency under load): one load per entry plus one
-// 8-byte gather, six entries in flight per lane.
+// 8-byte gather, TDW_NEAR_U entries in flight per lane.
 __device__ __forceinline__ double2 ldg_keep2(const double2* p, uint64_t pol) {
   double2 v;
   asm("ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(v.x), "=d"(v.y) : "l"(p), "l"(pol));
@@ -1616,7 +1619,7 @@ __global__ void __launch_bounds__(128, TDW_NEAR_MINB) near_step_kernel(const int
   const uint64_t keep = policy_keep_l2();  // the near structure is re-read every step
   const double* hrow = (const double*)(hist + (size_t)(pad + alpha - 1) * hcols);  // (q, u) pairs
   const int ring = nsl + 1;
-  constexpr int U = 6;
+  constexpr int U = TDW_NEAR_U;
   for (int g = g0; g < g1; ++g) {
     const int* pp = ptr + (size_t)g * (ns + 1) + i;
     const int p0 = __ldg(pp), p1 = __ldg(pp + 1);
