@@ -16,7 +16,7 @@
  *                          TimeHistory outputs)                   marching.py:184-276
  *   tdw_march_stream_begin / _finish (/ _outputs)
  *                       <- marching.march with the Greville sampling  marching.py:258-338
- *                          overlapped with the loop (chunked, mapped buffers)
+ *                          and the history copies overlapped with the loop (chunks)
  *   tdw_upload_known_rows + tdw_march_device_known
  *                       <- marching.march, pipelined form           marching.py:292-338
  *                          (known rows copied as they are sampled)
@@ -187,8 +187,9 @@ int tdw_march_device_known(tdw_problem* pb, double threshold, double* u, double*
  * data into page-locked buffers from tdw_host_alloc (u_host / q_host; NULL = that
  * callable is None, zeros), step by step, and after every `chunk` steps stores the
  * number of complete chunks in *flag (a page-locked int32; -1 aborts the loop, e.g.
- * when a data callable raised).  The device copies each chunk in as soon as its
- * flag is seen; tdw_march_stream_finish waits and returns the outputs and errors of
+ * when a data callable raised).  A host thread of the library copies each chunk
+ * to the device as soon as it is published (the pass that needs it waits for it on
+ * the device); tdw_march_stream_finish waits and returns the outputs and errors of
  * tdw_march.  Direct path only (not FMM problems). */
 int tdw_march_stream_begin(tdw_problem* pb, double threshold, int want_rhs, const double* u_host,
                            const double* q_host, int chunk, int32_t* flag);
