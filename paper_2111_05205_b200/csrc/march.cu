@@ -2608,6 +2608,9 @@ int tdw_march_stream_wait(tdw_problem* pb) {
   if (pb->stream_thread.joinable()) pb->stream_thread.join();
   if (pb->chunk_thread.joinable()) pb->chunk_thread.join();
   pb->stream_in_flight = false;
+  pb->streaming = false;  // (an enqueue that failed half-way returns without resetting these)
+  pb->stream_direct = false;
+  pb->need_ready = 0;
   if (pb->stream_rc || pb->chunk_rc) {  // the enqueue or a copy failed: drain whatever was launched
     cudaDeviceSynchronize();
     return pb->stream_rc ? pb->stream_rc : pb->chunk_rc;
@@ -2621,8 +2624,10 @@ int tdw_march_stream_wait(tdw_problem* pb) {
     snprintf(msg, sizeof(msg), "step %d: solve residual too large", hflags[2]);
     return tdw_fail(ctx, TDW_ERR_RESIDUAL, msg);
   }
-  if (hflags[0] == 3)
+  if (hflags[0] == 3) {
+    cudaDeviceSynchronize();  // an aborted direct-launch loop leaves its side streams unjoined
     return tdw_fail(ctx, TDW_ERR_STATE, "streamed march: the known data never arrived (aborted or timed out)");
+  }
   return TDW_OK;
 }
 

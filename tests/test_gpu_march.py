@@ -552,3 +552,12 @@ def test_streamed_march_aborts_when_the_data_raises():
     good = type(spec)(spec.mesh, spec.phi, spec.bie, spec.basis, spec.c, spec.nt, q_data=lambda t: f(t))
     h = marching.march(good, mats=store)
     assert h.status == "stable" and h.n_steps == spec.nt - 1
+    # the same once the loop is a cached graph fed by the chunk server (the first
+    # streamed marches of a store are launched kernel by kernel)
+    ref = marching.march(good, mats=store)
+    calls[0] = 0
+    with pytest.raises(ArithmeticError, match="boom"):
+        marching.march(broken, mats=store)
+    h = marching.march(good, mats=store)
+    np.testing.assert_array_equal(h.q, ref.q)
+    np.testing.assert_array_equal(h.u, ref.u)
