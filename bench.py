@@ -460,7 +460,14 @@ def run_ours(args, world, rank, local):
     _lib.check(_lib.load().tdw_fp64_peak(ctx.h, C.byref(fp64)), ctx.h, "tdw_fp64_peak")
     kind = "bm" if spec.bie == "bmbie" else "uw"
     cost = K1_COST[(kind, spec.basis.d)]
-    evals_per_s = info["n_evals"] / (info["t_fill_ms"] * 1e-3)
+    # whole-job rate: the evaluations of all ranks (each assembles only its rows) over
+    # the slowest rank's fill time
+    n_evals_all = info["n_evals"]
+    if world > 1:
+        t = torch.tensor([float(info["n_evals"])], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        n_evals_all = int(t.item())
+    evals_per_s = n_evals_all / (max_over_ranks(info["t_fill_ms"]) * 1e-3)
     try:  # the fill kernel's own FP64-pipe utilisation from the committed ncu capture
         k1_ncu = json.loads((ROOT / "profiles" / "k1_fill.json").read_text())
     except Exception:
@@ -531,7 +538,7 @@ def run_ours(args, world, rank, local):
             # per loop: init_hist + (conv_kernel + reduce_parts) per pass + (solve +
             # near_step) per step
             "gpu_launches": int(args.steps * (1 + 2 * (-(-(nt - 1) // info["steps_per_pass"])) + 2 * (nt - 1))),
-            "assembly": {"ms": info["t_assemble_ms"], "evals": info["n_evals"],
+            "assembly": {"ms": max_over_ranks(info["t_assemble_ms"]), "evals": n_evals_all,
                          "evals_per_s": evals_per_s,
                          "metric": "(i,j,gamma) layer-potential evals/s (fill kernel, fp64)",
                          "roofline": {"bound": "fp64",
