@@ -898,6 +898,20 @@ int tdw_assemble_impl(tdw_problem* pb) {
         pb->units_hdr32 += ucoef[u] == TDW_UNIT_COEF_OFF;
       }
     pb->wmax = wm;
+    // TMA box heights for the units' history slices (rows = lag span + kb - 1): the
+    // 50 / 80 / 95 % quantiles of the spans and the largest
+    std::vector<int> spans;
+    spans.reserve(nunit);
+    for (long long u = 0; u < nunit; ++u)
+      if (hu[u].y >= hu[u].x) spans.push_back(hu[u].y - hu[u].x + 1);
+    std::sort(spans.begin(), spans.end());
+    pb->hbox_n = 0;
+    const double qs[4] = {0.5, 0.8, 0.95, 1.0};
+    for (int k = 0; k < 4; ++k) {
+      const int w = spans.empty() ? wm : spans[std::min(spans.size() - 1, (size_t)(qs[k] * (spans.size() - 1) + 0.5))];
+      const int rows = (k == 3 ? wm : w) + pb->kb - 1;
+      if (pb->hbox_n == 0 || rows > pb->hbox_rows[pb->hbox_n - 1]) pb->hbox_rows[pb->hbox_n++] = rows;
+    }
   }
   // coefficient mode (SURVEY 8(b) `mode`): the banded store when it fits in device
   // memory (TDW_MODE_AUTO) or when asked; otherwise the coefficients are

@@ -160,6 +160,14 @@ __device__ __forceinline__ void trace_end(unsigned long long* t) {
   }
 }
 
+// History boxes of a few heights (rows = steps): a unit's history slice is fetched
+// with ONE 2-D TMA copy of the smallest box that covers its lag span + kb - 1 rows
+// (a bulk copy per 512-byte row costs the SM's copy engine ~30 ns each: 14 per unit
+// were a quarter of its time; the single widest box instead wastes the FIFO)
+struct HistMaps {
+  CUtensorMap m[4];
+};
+
 struct ConvArgs {
   const unsigned char* __restrict__ units;
   const unsigned long long* __restrict__ unit_off;
@@ -174,7 +182,9 @@ struct ConvArgs {
   int l2hint;            // L2 eviction-priority hints on the unit stream / history box
   unsigned long long* stats;  // optional (TDW_CONV_STATS): iterations, lane entries, per-row lmax histogram
   int dry;                    // experiments (TDW_CONV_DRY, tdw_time_conv only): stream units, skip the k loop
-  int hrows;                  // 1: history slice = the unit's lag span, per-row bulk copies; 0: TMA wbox box
+  int hrows;                  // 2: smallest TMA box covering the unit's lag span (default); 1: the span, one bulk
+                              // copy per row; 0: the widest TMA box
+  int hbox_n, hbox_rows[4];   // the box heights of HistMaps, ascending (the last one covers every unit)
   int pf;                     // L2 prefetch distance of the unit stream (schedule entries; 0 = off)
   unsigned long long* trace;  // timeline trace (TDW_TRACE_SOLVE): slots 11, 12 of the pass's first step
   unsigned stage_bytes;  // shared-memory FIFO capacity
@@ -220,7 +230,7 @@ static_assert(conv_consumer_regs<2, kConvLaunchRegsPWG2>() == 112, "register spl
 // (gmax - g + i) of the unit's history box of wbox+KB-1 rows starting at time
 // alpha-gmax.  Every coefficient is read from shared memory once and used KB times.
 template <int KB, int RPW, bool PWG, int LREGS = kConvLaunchRegsPWG>
-__device__ __forceinline__ void conv_body(const ConvArgs& a, const CUtensorMap& hmap) {
+__device__ __forceinline__ void conv_body(const ConvArgs& a, const HistMaps& hmaps) {
   constexpr int CW = TDW_TI / RPW;  // consumer warps
   extern __shared__ __align__(128) unsigned char sm[];
   __shared__ __align__(8) uint64_t full[4];
@@ -317,7 +327,10 @@ __device__ __forceinline__ void conv_body(const ConvArgs& a, const CUtensorMap& 
         const int t = (int)(quid % (unsigned)a.ntiles);
         // history slice: the unit's own lag span (hrows: one 512-byte bulk copy per
         // step row) or the fixed wbox-row TMA box of the tensor map
-        const int hr = a.hrows ? W + KB - 1 : a.wbox + KB - 1;
+        int hr = a.hrows == 1 ? W + KB - 1 : a.hbox_rows[a.hbox_n - 1], bi = a.hbox_n - 1;
+        if (a.hrows == 2)
+          for (bi = 0; bi < a.hbox_n - 1 && a.hbox_rows[bi] < W + KB - 1; ++bi) {}
+        if (a.hrows == 2) hr = a.hbox_rows[bi];
         const unsigned hbytes = W > 0 ? (unsigned)(TDW_TJ * hr * 16) : 0u;
         const unsigned ubytes = (qbytes + 127u) & ~127u;
         const unsigned need = ubytes + ((hbytes + 127u) & ~127u);
@@ -348,7 +361,7 @@ __device__ __forceinline__ void conv_body(const ConvArgs& a, const CUtensorMap& 
           if (a.l2hint) bulk_g2s_hint(sbase + c, a.units + qoff + c, len, &full[slot], pol_stream);
           else bulk_g2s(sbase + c, a.units + qoff + c, len, &full[slot]);
         }
-        if (W > 0 && a.hrows) {  // hist[pad+alpha-gmax+r][t*32 .. +32], r < hr: lane r copies row r
+        if (W > 0 && a.hrows == 1) {  // hist[pad+alpha-gmax+r][t*32 .. +32], r < hr: lane r copies row r
           const double2* h0 = a.hist + (size_t)(a.pad + a.alpha - gmax) * a.hcols + t * TDW_TJ;
           unsigned char* hdst = sbase + ubytes;
           for (int r = lane; r < hr; r += 32) {
@@ -359,10 +372,10 @@ __device__ __forceinline__ void conv_body(const ConvArgs& a, const CUtensorMap& 
           }
         } else if (W > 0 && lane == 0) {  // hist[pad+alpha-gmax .. +wbox)[t*32 .. +32] as one 2-D box
           if (a.l2hint)
-            tensor2d_g2s_hint(sbase + ubytes, &hmap, 2 * t * TDW_TJ, a.pad + a.alpha - gmax, &full[slot],
+            tensor2d_g2s_hint(sbase + ubytes, &hmaps.m[bi], 2 * t * TDW_TJ, a.pad + a.alpha - gmax, &full[slot],
                               pol_keep);
           else
-            tensor2d_g2s(sbase + ubytes, &hmap, 2 * t * TDW_TJ, a.pad + a.alpha - gmax, &full[slot]);
+            tensor2d_g2s(sbase + ubytes, &hmaps.m[bi], 2 * t * TDW_TJ, a.pad + a.alpha - gmax, &full[slot]);
         }
         h += need;
         ++n;
@@ -556,15 +569,15 @@ __device__ __forceinline__ void conv_body(const ConvArgs& a, const CUtensorMap& 
 
 template <int KB>
 __global__ void __launch_bounds__(conv_threads<2, false>(), 1)
-    conv_kernel(ConvArgs a, const __grid_constant__ CUtensorMap hmap) {
+    conv_kernel(ConvArgs a, const __grid_constant__ HistMaps hmap) {
   conv_body<KB, 2, false>(a, hmap);
 }
 template <int KB>
-__global__ void __maxnreg__(kConvLaunchRegsPWG) conv_kernel_wg(ConvArgs a, const __grid_constant__ CUtensorMap hmap) {
+__global__ void __maxnreg__(kConvLaunchRegsPWG) conv_kernel_wg(ConvArgs a, const __grid_constant__ HistMaps hmap) {
   conv_body<KB, 4, true>(a, hmap);
 }
 template <int KB>
-__global__ void __maxnreg__(kConvLaunchRegsPWG2) conv_kernel_wg2(ConvArgs a, const __grid_constant__ CUtensorMap hmap) {
+__global__ void __maxnreg__(kConvLaunchRegsPWG2) conv_kernel_wg2(ConvArgs a, const __grid_constant__ HistMaps hmap) {
   conv_body<KB, 2, true, kConvLaunchRegsPWG2>(a, hmap);
 }
 
@@ -1793,7 +1806,7 @@ typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_
 
 // 2-D view of the history: rows = steps, inner = 2*hcols doubles; box =
 // [wbox + kb - 1 steps][64 doubles = 32 elements x (q, u)].
-static int make_hist_map(tdw_problem* pb, CUtensorMap* map) {
+static int make_hist_map(tdw_problem* pb, HistMaps* maps) {
   static PFN_encodeTiled enc = nullptr;
   if (!enc) {
     cudaDriverEntryPointQueryResult q;
@@ -1805,12 +1818,15 @@ static int make_hist_map(tdw_problem* pb, CUtensorMap* map) {
   }
   cuuint64_t dims[2] = {(cuuint64_t)2 * pb->hcols, (cuuint64_t)pb->hstride};
   cuuint64_t strides[1] = {(cuuint64_t)pb->hcols * 16};
-  cuuint32_t box[2] = {(cuuint32_t)(2 * TDW_TJ), (cuuint32_t)(pb->wbox + pb->kb - 1)};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, pb->d_hist, dims, strides, box, estr,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                   CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) return tdw_fail(pb->ctx, TDW_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+  for (int k = 0; k < 4; ++k) {  // unused slots repeat the last (widest) box
+    const int rows = pb->hbox_rows[std::min(k, pb->hbox_n - 1)];
+    cuuint32_t box[2] = {(cuuint32_t)(2 * TDW_TJ), (cuuint32_t)rows};
+    CUresult r = enc(&maps->m[k], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, pb->d_hist, dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return tdw_fail(pb->ctx, TDW_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+  }
   return TDW_OK;
 }
 
@@ -1841,7 +1857,7 @@ static cudaError_t conv_set_smem(int kb, int rpw, int smem) {
   return cudaErrorInvalidValue;
 }
 static void conv_launch(int kb, int rpw, dim3 grid, size_t smem, cudaStream_t s, const ConvArgs& c,
-                        const CUtensorMap& hmap) {
+                        const HistMaps& hmap) {
 #define X(K)                                                                              \
   if (kb == K && rpw == 3) {                                                              \
     conv_kernel_wg2<K><<<grid, conv_threads<2, true>(), smem, s>>>(c, hmap);              \
@@ -1878,7 +1894,9 @@ static void fill_conv_args(tdw_problem* pb, ConvArgs& c) {
   }
   {
     const char* h = getenv("TDW_HROWS");
-    c.hrows = h ? atoi(h) : 1;
+    c.hrows = h ? atoi(h) : 2;
+    c.hbox_n = pb->hbox_n;
+    for (int k = 0; k < 4; ++k) c.hbox_rows[k] = pb->hbox_rows[std::min(k, pb->hbox_n - 1)];
   }
   {
     const char* h = getenv("TDW_L2HINT");
@@ -1906,7 +1924,7 @@ static void fill_conv_args(tdw_problem* pb, ConvArgs& c) {
 namespace {
 
 struct LoopPlan {
-  CUtensorMap hmap;
+  HistMaps hmap;
   ConvArgs c;
   ClusterSolveArgs cs;
   dim3 cgrid;
@@ -2702,7 +2720,7 @@ int tdw_time_conv_impl(tdw_problem* pb, int n, float* ms_out) {
   ConvArgs c{};
   fill_conv_args(pb, c);
   c.alpha = std::max(1, pb->nt - pb->kb);
-  CUtensorMap hmap;
+  HistMaps hmap;
   {
     int rc = make_hist_map(pb, &hmap);
     if (rc) return rc;

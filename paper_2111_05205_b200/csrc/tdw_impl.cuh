@@ -114,7 +114,8 @@ struct tdw_problem {
   unsigned long long* d_unit_off = nullptr; // [n_iblk * ntiles + 1] byte offsets
   int2* d_unit = nullptr;          // [n_iblk * ntiles] lag range (gmin, gmax)
   int wmax = 0;                    // max unit lag span
-  int wbox = 0;                    // history box width (lags) of the TMA copy, even, >= wmax
+  int wbox = 0;                    // history box width (lags) of the widest TMA copy, >= wmax
+  int hbox_n = 1, hbox_rows[4] = {1, 1, 1, 1};  // TMA box heights (rows = lag span + kb - 1), ascending
   size_t max_unit_bytes = 0;
   // conv schedule: persistent CTAs over items (I-block, tile split)
   int conv_grid = 0, conv_S = 1, conv_nstages = 2;
