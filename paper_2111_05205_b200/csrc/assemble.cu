@@ -377,7 +377,7 @@ __global__ void unit_layout_kernel(const unsigned long long* segcount, const uin
     for (int r = 0; r < TDW_TI; ++r) {
       const uint32_t w = src[(size_t)r * ntiles * TDW_TJ];
       const int len = hdr_len(w);
-      h[r * TDW_TJ + lane] = hdr16_pack(hdr_jl(w), len, len ? g.y - hdr_glo(w) : 0);
+      h[hdr16_index(r, lane)] = hdr16_pack(hdr_jl(w), len, len ? g.y - hdr_glo(w) : 0);
     }
   } else {
     uint32_t* h = (uint32_t*)(ub + TDW_UNIT_HDR_OFF);

@@ -136,6 +136,22 @@ __device__ __forceinline__ double2 lds_f64x2(unsigned addr) {
   return v;
 }
 
+__device__ __forceinline__ uint4 lds_u32x4(unsigned addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ uint2 lds_u32x2(unsigned addr) {
+  uint2 v;
+  asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ unsigned lds_u32(unsigned addr) {
+  unsigned v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
+}
+
 // Programmatic dependent launch (PDL) of consecutive solves: the next solve is
 // queued while this one runs (so its cluster takes the SMs this one frees before
 // other kernels' blocks do); it waits here for this grid's completion and
@@ -397,6 +413,7 @@ __device__ __forceinline__ void conv_body(const ConvArgs& a, const HistMaps& hma
   const int S = a.S;
   const size_t step_stride = (size_t)a.rows_loc * S;
   int n = 0;
+  const unsigned sm0 = smem_u32(sm), l16 = (unsigned)lane * 16u, lt = (1u << lane) - 1u;
   long long cwait = 0, cpro = 0, ckl = 0;  // TDW_CONV_TSTAT: cycles waiting for data, in the unit prologue, in the k loop
   const long long cstart = (TDW_TSTAT && a.tstat) ? clock64() : 0;
   for (int base = 0; base < nent; base += 32) {
@@ -415,13 +432,29 @@ __device__ __forceinline__ void conv_body(const ConvArgs& a, const HistMaps& hma
       mbar_wait(&full[stage], (unsigned)(n / NS) & 1u);
       const long long tp0 = (TDW_TSTAT && a.tstat) ? clock64() : 0;
       if (TDW_TSTAT && a.tstat) cwait += tp0 - tw;
-      const unsigned char* ub = sm + *(volatile unsigned*)&region[stage];
-      const uint32_t* rel_off = (const uint32_t*)ub;
-      const int2 g = *(const int2*)(ub + TDW_UNIT_LAG_OFF);
-      const unsigned coef_off = *(const uint32_t*)(ub + TDW_UNIT_LAG_OFF + 12);
-      const double2* coef = (const double2*)(ub + coef_off);
-      const unsigned ubytes = (unsigned)((*(const uint32_t*)(ub + TDW_UNIT_LAG_OFF + 8) + 127u) & ~127u);
-      const double2* hs = (const double2*)(ub + ubytes);
+      // Unit prologue.  Everything that depends only on the unit's base is read
+      // in one round of shared-memory loads: the lag word (gmin, gmax, bytes,
+      // coefficient offset), the segment offsets of the warp's RPW rows and --
+      // speculatively, they are the rule -- the rows' 16-bit pair headers, which
+      // sit side by side per lane (hdr16_index); a unit with 32-bit headers
+      // reloads them.
+      const unsigned ubs = sm0 + *(volatile unsigned*)&region[stage];
+      const uint4 lw = lds_u32x4(ubs + TDW_UNIT_LAG_OFF);
+      unsigned ro[RPW], h16[RPW];
+      if constexpr (RPW == 4) {
+        const uint4 o = lds_u32x4(ubs + warp * 16);
+        const uint2 hh = lds_u32x2(ubs + TDW_UNIT_HDR_OFF + warp * 256 + lane * 8);
+        ro[0] = o.x; ro[1] = o.y; ro[2] = o.z; ro[3] = o.w;
+        h16[0] = hh.x & 0xffffu; h16[1] = hh.x >> 16; h16[2] = hh.y & 0xffffu; h16[3] = hh.y >> 16;
+      } else {
+        static_assert(RPW == 2, "rows per consumer warp");
+        const uint2 o = lds_u32x2(ubs + warp * 8);
+        const unsigned hh = lds_u32(ubs + TDW_UNIT_HDR_OFF + (warp >> 1) * 256 + lane * 8 + (warp & 1) * 4);
+        ro[0] = o.x; ro[1] = o.y;
+        h16[0] = hh & 0xffffu; h16[1] = hh >> 16;
+      }
+      const int2 g = make_int2((int)lw.x, (int)lw.y);
+      const unsigned coef_off = lw.w;
       // the warp's rows are interleaved (independent FMA chains); the k loop is
       // unrolled.  Lane = column: the k-th entries of a segment are those of the
       // lanes with band > k, packed in lane order; the history box is [time][32
@@ -429,12 +462,25 @@ __device__ __forceinline__ void conv_body(const ConvArgs& a, const HistMaps& hma
       // Branch- and move-free body: every lane issues both shared-memory loads
       // each k.  A lane past its band reads the CTA's zero slot as coefficient
       // and a clamped (in-box, finite) history row, so its multiply-adds add 0.
-      const unsigned lt = (1u << lane) - 1u;
-      int len[RPW], lmax = 0;
+      int len[RPW], rel[RPW], lmax = 0;
       unsigned cpb[RPW];  // shared byte address of the row's entries of the current k
       int hp[RPW];        // shared byte address: lane's column at box row rel
       // lane's column at box row 0 (the clamp); the pair headers put column jl = lane
-      const int hlo = (int)smem_u32(hs + lane);
+      const int hlo = (int)(ubs + ((lw.z + 127u) & ~127u) + l16);
+      if (coef_off == TDW_UNIT_COEF_OFF16) {
+#pragma unroll
+        for (int r = 0; r < RPW; ++r) {
+          len[r] = (int)((h16[r] >> 5) & 31u);
+          rel[r] = (int)(h16[r] >> 10);
+        }
+      } else {
+#pragma unroll
+        for (int r = 0; r < RPW; ++r) {
+          const uint32_t h = lds_u32(ubs + TDW_UNIT_HDR_OFF + ((warp * RPW + r) * TDW_TJ + lane) * 4);
+          len[r] = hdr_len(h);
+          rel[r] = g.y - hdr_glo(h);
+        }
+      }
       // KB == 1: separate per-unit V_U q and V_W u chains (ILP); KB > 1: the
       // running row sums take the multiply-adds directly -- KB independent
       // chains already, and registers are short
@@ -446,12 +492,9 @@ __device__ __forceinline__ void conv_body(const ConvArgs& a, const HistMaps& hma
       double2 hw[RPW][KB];
 #pragma unroll
       for (int r = 0; r < RPW; ++r) {
-        const int row = warp * RPW + r;
-        int jl, rel;  // jl == lane (hdr_pack / hdr16_pack write the lane as column)
-        unit_hdr(ub, coef_off, g.y, row * TDW_TJ + lane, jl, len[r], rel);
         lmax = max(lmax, len[r]);
-        cpb[r] = smem_u32(coef + rel_off[row]);
-        hp[r] = hlo + (len[r] > 0 ? rel : 0) * (TDW_TJ * 16);
+        cpb[r] = ubs + coef_off + ro[r] * 16u;
+        hp[r] = hlo + (len[r] > 0 ? rel[r] : 0) * (TDW_TJ * 16);
         if (NS1) {
           s0[r][0] = 0.0;
           s1[r][0] = 0.0;

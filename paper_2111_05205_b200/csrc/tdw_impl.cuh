@@ -23,7 +23,9 @@
 //   [128, 136)      int2 (gmin, gmax)   lag range of the unit (history slice)
 //   [136, 140)      uint32              unit bytes
 //   [140, 144)      uint32              coef offset: 2304 (16-bit headers) or 4352 (32-bit)
-//   [256, coef)     hdr[32][32]         pair headers, row-major, lane = column
+//   [256, coef)     hdr[32][32]         pair headers, lane = column: 32-bit ones row-major;
+//                                       16-bit ones with the four rows of a consumer
+//                                       warp side by side per lane (hdr16_index)
 //   [coef, ...)     double2 coef[]      (V_U, V_W) entries, jagged k-major per segment:
 //                                       the k-th entries of the lanes with band > k,
 //                                       in lane order
@@ -60,11 +62,13 @@ __host__ __device__ inline int hdr_glo(uint32_t h) { return (int)(h >> 16); }
 __host__ __device__ inline uint16_t hdr16_pack(int jl, int len, int rel) {
   return (uint16_t)(jl | (len << 5) | (rel << 10));
 }
-// (column, length, rel) of pair (row, lane) of a unit, either header width
+// position of the 16-bit header of (row, lane): rows 4w..4w+3 of a lane are one 8-byte word
+__host__ __device__ inline int hdr16_index(int row, int lane) { return (row >> 2) * 128 + lane * 4 + (row & 3); }
+// (column, length, rel) of pair idx = row * 32 + lane of a unit, either header width
 __device__ __forceinline__ void unit_hdr(const unsigned char* ub, unsigned coef_off, int gmax,
                                          int idx, int& jl, int& len, int& rel) {
   if (coef_off == TDW_UNIT_COEF_OFF16) {
-    const unsigned h = ((const uint16_t*)(ub + TDW_UNIT_HDR_OFF))[idx];
+    const unsigned h = ((const uint16_t*)(ub + TDW_UNIT_HDR_OFF))[hdr16_index(idx >> 5, idx & 31)];
     jl = (int)(h & 31u);
     len = (int)((h >> 5) & 31u);
     rel = (int)(h >> 10);
