@@ -3273,10 +3273,11 @@ int tdw_setup_cluster_solver(tdw_problem* pb) {
   pb->near_tail = 0;
   {
     const char* e = getenv("TDW_NEAR_IN_SOLVE");
-    // default: 3 lags at kb = 5 (config 2: 15.5k steps/s; 2 lags 15.0k, 4 lags 14.1k),
-    // 2 at kb = 6, else 1 (config 1, solve-bound: each extra lag costs ~35%); the
-    // near step of step s is then needed only near_tail + 1 solves later
-    const int want = std::min(e ? atoi(e) : (pb->kb == 5 ? 3 : (pb->kb >= 6 ? 2 : 1)), pb->nsl);
+    // default: 2 lags at kb >= 5 (config 2 with the CSR near step: 2 lags 15.98k
+    // steps/s, 3 lags 15.84k, 4 lags 14.7k), else 1 (config 1, solve-bound: each
+    // extra lag costs ~35%); the near step of step s is then needed only
+    // near_tail + 1 solves later
+    const int want = std::min(e ? atoi(e) : (pb->kb >= 5 ? 2 : 1), pb->nsl);
     if (want > 0 && pb->sp_reg > 0 && pb->sp_halo > 0 && pb->split_lag2 && pb->near_w > 0) {
       int rc = build_lag_csr(pb, want, R, &pb->d_n2_ptr, &pb->d_n2_col, &pb->d_n2_val);
       if (rc) return rc;
