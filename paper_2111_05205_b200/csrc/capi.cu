@@ -714,6 +714,12 @@ int tdw_set_graph(tdw_problem* pb, int enable) {
 int tdw_problem_destroy(tdw_problem* pb) {
   if (!pb) return TDW_OK;
   cudaSetDevice(pb->ctx->device);
+  // a streamed march nobody finished: stop waiting for its data, let the loop
+  // drain, and only then free what its kernels use
+  pb->stream_cancel = true;
+  if (pb->stream_thread.joinable()) pb->stream_thread.join();
+  if (pb->chunk_thread.joinable()) pb->chunk_thread.join();
+  if (pb->stream_in_flight) cudaDeviceSynchronize();
   void* ptrs[] = {pb->d_perm, pb->d_elem, pb->d_phi, pb->d_units, pb->d_unit_off, pb->d_sched, pb->d_sched_off,
                   pb->d_sched_item, pb->d_leafc, pb->d_pair_ptr, pb->d_pair_col, pb->d_kw, pb->d_otf_evals,
                   pb->d_unit, pb->d_acol, pb->d_aval, pb->d_adiag, pb->d_hist, pb->d_uk,
@@ -731,10 +737,7 @@ int tdw_problem_destroy(tdw_problem* pb) {
   if (pb->ev_fork) cudaEventDestroy(pb->ev_fork);
   if (pb->side) cudaStreamDestroy(pb->side);
   if (pb->side_near) cudaStreamDestroy(pb->side_near);
-  if (pb->stream_thread.joinable()) pb->stream_thread.join();
-  if (pb->stream_in_flight && pb->ev_stream_end) cudaEventSynchronize(pb->ev_stream_end);
   if (pb->graph_exec_s) cudaGraphExecDestroy(pb->graph_exec_s);
-  if (pb->chunk_thread.joinable()) pb->chunk_thread.join();
   if (pb->ev_begin) cudaEventDestroy(pb->ev_begin);
   if (pb->d_ready) cudaFree(pb->d_ready);
   if (pb->ev_stream_end) cudaEventDestroy(pb->ev_stream_end);

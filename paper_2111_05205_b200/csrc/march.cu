@@ -2463,7 +2463,7 @@ static bool stream_wait_chunk(tdw_problem* pb, int c) {
   for (unsigned spins = 0;; ++spins) {
     const int f = *pb->h_flag_host;
     if (f >= c + 1) break;
-    if (f < 0 || std::chrono::steady_clock::now() - t0 > std::chrono::seconds(120)) return false;
+    if (f < 0 || pb->stream_cancel || std::chrono::steady_clock::now() - t0 > std::chrono::seconds(120)) return false;
     if (spins > 4000) std::this_thread::sleep_for(std::chrono::microseconds(20));
   }
   std::atomic_thread_fence(std::memory_order_acquire);  // the rows were written before the counter

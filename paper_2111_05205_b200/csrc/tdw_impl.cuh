@@ -231,6 +231,7 @@ struct tdw_problem {
   std::thread chunk_thread;         // the chunk server
   int stream_rc = 0;                // their results
   int chunk_rc = 0;
+  volatile bool stream_cancel = false;  // tdw_problem_destroy with a streamed march still waiting for its data
   cudaEvent_t ev_stream_end = nullptr;
   // streamed outputs (tdw_march_stream_outputs): after the last solve of each chunk
   // a side stream writes the chunk's rows of u, q, tau, sigma straight into the

@@ -561,3 +561,28 @@ def test_streamed_march_aborts_when_the_data_raises():
     h = marching.march(good, mats=store)
     np.testing.assert_array_equal(h.q, ref.q)
     np.testing.assert_array_equal(h.u, ref.u)
+
+
+def test_store_closed_with_a_streamed_march_in_flight():
+    """tdw_problem_destroy while a streamed march still waits for its data (begin
+    without finish): the loop is cancelled and drained before anything is freed."""
+    import ctypes as C
+    import time
+    from paper_2111_05205_b200 import _lib
+    spec = scenarios.build_spec(0)
+    store = marching.BandStore(spec).assemble()
+    marching.march(spec, mats=store)                      # first streamed march: direct launches
+    marching.march(spec, mats=store)                      # the cached graph and the chunk server
+    lib = _lib.load()
+    bu, bq = store.pinned_known(0), store.pinned_known(1)
+    flag = store.pinned_flag()
+    flag[0] = 0                                           # nothing published, ever
+    rc = lib.tdw_march_stream_begin(store.h, 1e30, 0, bu.ctypes.data if spec.u_data else None,
+                                    bq.ctypes.data if spec.q_data else None, marching.STREAM_CHUNK,
+                                    flag.ctypes.data)
+    assert rc == 0
+    t0 = time.perf_counter()
+    store.close()
+    assert time.perf_counter() - t0 < 30.0
+    h = marching.march(spec)                              # the device is fine afterwards
+    assert h.status == "stable"
